@@ -1,0 +1,219 @@
+/* ember_b200.h — C-ABI of the B200 fire-spread engine (libember_b200.so).
+ *
+ * The reference (emberline, /root/reference/proj) has no FFI: its interface is
+ * the C++ header API in proj/include/emberline/.  Every entry point below is the
+ * flat-pointer form of one reference function or type on the north-star path,
+ * cited as file:line; include/emberline_b200.hpp wraps them back into the
+ * reference's C++ signatures (the drop-in), and paper_2512_06102_b200/_lib.py binds
+ * them with ctypes (INTEGRATION.md shows both bindings).
+ *
+ * Conventions (identical to the reference):
+ *  - a grid is H x W row-major, index row*W + col, row 0 = south (grid.hpp:5-7,42);
+ *  - cell state is uint8 {0 Unburned, 1 Burning, 2 Burned} (grid.hpp:98);
+ *  - a batch is B envs stored batch-major [env][row][col] ("members", engine.hpp:250-258);
+ *  - config doubles in the order of BasicSimConfig (grid.hpp:171-180);
+ *  - the RNG key of env e at lockstep step t is {seed, t, stream[e]} (rng.hpp:15-19,
+ *    engine.cpp:145), draw domain kDrawFireEvent, cell index = row*W + col.
+ *
+ * Errors: every function returning int returns 0 on success and a negative
+ * EBL_E* code on failure; ebl_last_error() gives the message (thread-local).
+ * The C++ wrapper rethrows the reference's exception types (std::invalid_argument
+ * for EBL_EINVAL, std::logic_error for EBL_ELOGIC, std::out_of_range for
+ * EBL_ERANGE), matching grid.cpp:18-24, engine.cpp:124, rl_env.cpp:60-93,173.
+ * There is no CPU fallback: without a usable CUDA device ebl_batch_create fails
+ * with EBL_ECUDA. */
+#ifndef EMBER_B200_H
+#define EMBER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EBL_OK 0
+#define EBL_EINVAL -1 /* std::invalid_argument */
+#define EBL_ELOGIC -2 /* std::logic_error */
+#define EBL_ERANGE -3 /* std::out_of_range */
+#define EBL_ECUDA -4  /* device / driver failure */
+#define EBL_ESTATE -5 /* call order (e.g. stepping before a grid is set) */
+
+#define EBL_ABI_VERSION 1
+
+typedef struct ebl_batch ebl_batch; /* opaque: one device, one stream, B envs of H x W */
+
+/* BasicSimConfig<double> (grid.hpp:171-180). */
+typedef struct {
+  double p_base, alpha_w1, alpha_w2, alpha_s, alpha_gamma, p_continue;
+  int max_steps;
+} ebl_sim_config;
+
+int ebl_abi_version(void);
+const char* ebl_last_error(void);
+/* validate_config (grid.cpp:107-124). */
+int ebl_validate_config(const ebl_sim_config* cfg);
+void ebl_default_config(ebl_sim_config* cfg);
+
+/* ---- batch lifetime: the device-resident StochasticBatch (engine.hpp:250-261) ---- */
+/* `cuda_stream` may be NULL (library-owned stream) or a cudaStream_t to launch on. */
+int ebl_batch_create(ebl_batch** out, int device, int n_envs, int height, int width,
+                     void* cuda_stream);
+void ebl_batch_destroy(ebl_batch* b);
+int ebl_batch_set_config(ebl_batch* b, const ebl_sim_config* cfg);
+
+/* Static layers, form 1 — a general GridState (grid.hpp:192-211): per-cell wind
+ * speed/direction, veg/den, 8 slopes per cell ([cell*8+k], kNeighborOffsets order).
+ * n_grids = 1 (all members share one grid, as StochasticBatch does) or n_envs.
+ * Built into SpreadTables<double> (engine.hpp:76-125) in fp64 on the host and
+ * kept resident; rebuilt when the config changes. Validation as in
+ * WindField/FuelField/SlopeField/GridState construction (grid.cpp:49-142). */
+int ebl_batch_set_grid(ebl_batch* b, int n_grids, const double* wind_speed,
+                       const double* wind_direction, const double* veg, const double* den,
+                       const double* slope8);
+
+/* Static layers, form 2 — terrain (the north-star layout): per-cell uint8 fuel
+ * class into a palette of (veg, den) pairs (FuelTable, geodata.hpp:63-86), fp32
+ * elevation in metres from which the 8 slopes are derived on the fly exactly as
+ * slope_from_dem does (geodata.cpp:209-229) at `cellsize`.  n_grids = 1 or n_envs. */
+int ebl_batch_set_terrain(ebl_batch* b, int n_grids, const uint8_t* fuel_class,
+                          const float* elevation, int n_classes, const double* class_veg,
+                          const double* class_den, double cellsize);
+/* Spatially uniform wind per env (WindField::uniform, grid.cpp:64-66) for the
+ * terrain form; n_winds = 1 or n_envs. */
+int ebl_batch_set_wind(ebl_batch* b, int n_winds, const double* speed, const double* direction);
+
+/* Member fire layers, host <-> device, [n_envs][H*W] uint8 (values must be 0..2). */
+int ebl_batch_set_state(ebl_batch* b, const uint8_t* states);
+int ebl_batch_get_state(ebl_batch* b, uint8_t* states);
+/* Same, device pointers (no host round trip). */
+int ebl_batch_set_state_device(ebl_batch* b, const void* d_states);
+int ebl_batch_get_state_device(ebl_batch* b, void* d_states);
+/* Device pointer of the current state buffer (valid until the next step). */
+void* ebl_batch_state_device_ptr(ebl_batch* b);
+
+/* RNG identity: StochasticBatch::seed/step and Member::stream (engine.hpp:250-258).
+ * streams == NULL means stream[e] = first_stream + e (make_stochastic_batch,
+ * engine.cpp:122-132). */
+int ebl_batch_set_key(ebl_batch* b, uint64_t seed, uint64_t step, const uint64_t* streams,
+                      uint64_t first_stream);
+uint64_t ebl_batch_step_index(const ebl_batch* b);
+
+/* step_batch (engine.cpp:134-159) applied n_steps times: step t uses key
+ * {seed, step+t, stream[e]}; the batch step counter advances by n_steps. */
+int ebl_step_batch(ebl_batch* b, int n_steps);
+
+/* Kernel selection for ebl_step_batch (results are identical by construction):
+ * EBL_KERNEL_AUTO picks the fused env-resident multi-step kernel when one env's
+ * layers fit in shared memory, else the tiled one-step-per-launch kernel. */
+#define EBL_KERNEL_AUTO 0
+#define EBL_KERNEL_TILED 1
+#define EBL_KERNEL_RESIDENT 2
+int ebl_batch_set_kernel(ebl_batch* b, int which);
+
+/* fire_fraction_stats (engine.cpp:185-198) as integer counts of the current
+ * state, out[e*4 + {0,1,2,3}] = {unburned, burning, burned, newly ignited in the
+ * last step}. */
+int ebl_batch_counts(ebl_batch* b, int32_t* out);
+
+/* Per-cell arrival intensity and ignition probability of the current state
+ * (kernel.hpp:53-78, the fp32 fast path): lambda/p [n_envs][H*W] float. */
+int ebl_batch_intensity(ebl_batch* b, float* lambda, float* p);
+
+/* Diagnostics since the last reset: [0] draws decided in the fp64 guard band,
+ * [1] draws within 1e-12 of their fp64 threshold ("ambiguous": a flip vs the
+ * CPU reference is only possible here), [2] steps, [3] kernel
+ * launches issued. */
+int ebl_batch_diag(ebl_batch* b, uint64_t* out4, int reset);
+/* rng_word (rng.hpp:38-46) evaluated ON THE DEVICE for n keys
+ * keys5[i*5 + {0..4}] = {seed, step, stream, cell, draw}; the parity probe of the
+ * device generator (device 0). */
+int ebl_device_rng_words(int n, const uint64_t* keys5, uint64_t* out);
+int ebl_batch_sync(ebl_batch* b);
+
+/* ---- one-shot entry points (exact reference signatures, host buffers) ---- */
+/* step_stochastic(fire, grid, cfg, key) (engine.hpp:204-207) on general layers. */
+int ebl_step_stochastic(int height, int width, const uint8_t* fire, const double* wind_speed,
+                        const double* wind_direction, const double* veg, const double* den,
+                        const double* slope8, const ebl_sim_config* cfg, uint64_t seed,
+                        uint64_t step, uint64_t stream, uint8_t* out);
+/* run_stochastic(initial, grid, cfg, key, steps) (engine.hpp:215-217), final state only. */
+int ebl_run_stochastic(int height, int width, const uint8_t* initial, const double* wind_speed,
+                       const double* wind_direction, const double* veg, const double* den,
+                       const double* slope8, const ebl_sim_config* cfg, uint64_t seed,
+                       uint64_t step, uint64_t stream, int steps, uint8_t* out);
+
+/* ---- RL (rl_env.hpp) ---------------------------------------------------------- */
+/* EnvConfig (rl_env.hpp:24-40). */
+typedef struct {
+  int height, width, window_radius, water_capacity;
+  double burn_penalty;
+  int max_episode_steps, ignition_count, waste_water;
+  double wind_speed, wind_direction, fuel_veg, fuel_den;
+  ebl_sim_config spread;
+} ebl_env_config;
+
+/* EnvState minus the fire layer (rl_env.hpp:67-75). */
+typedef struct {
+  int32_t agent_row, agent_col, water, step;
+  uint64_t seed, stream;
+  int32_t done;
+  uint32_t episode; /* tanker episode counter (RNG stream = episode << 32 | env id) */
+} ebl_env_state;
+
+#define EBL_RL_REFERENCE 0 /* FireSuppressionEnv semantics: Move x Valve, single-cell douse */
+#define EBL_RL_TANKER 1    /* BASELINE C2: (x,y) action, 3x3 extinguish+wet, auto-reset */
+
+void ebl_env_default_preset(ebl_env_config* c); /* default_preset, rl_env.cpp:10-27 */
+void ebl_env_smoke10_preset(ebl_env_config* c); /* smoke10_preset, rl_env.cpp:29-57 */
+int ebl_env_observation_size(const ebl_env_config* c); /* rl_env.cpp:73-76 */
+
+/* Puts the batch in RL mode.  EBL_RL_REFERENCE: the batch's statics become the
+ * config's flat terrain (rl_env.cpp:99-105).  EBL_RL_TANKER: statics must be
+ * set (terrain form), `ignitions` per reset at burnable cells, `max_steps` cap,
+ * auto-reset on.  Env e has id env_id0 + e. */
+int ebl_rl_configure(ebl_batch* b, int variant, const ebl_env_config* c, int tanker_ignitions,
+                     int tanker_max_steps, uint32_t env_id0);
+/* FireSuppressionEnv::reset (rl_env.cpp:125-145) of every env (mask[e] != 0, or all
+ * when mask == NULL).  REFERENCE: streams[e] (NULL: env id). TANKER: episode 0. */
+int ebl_rl_reset(ebl_batch* b, uint64_t seed, const uint64_t* streams, const uint8_t* mask);
+/* One step of every env: FireSuppressionEnv::step (rl_env.cpp:172-210) or the tanker
+ * step.  actions[e]: REFERENCE action_index (rl_env.hpp:62-64) in [0,10);
+ * TANKER row*W+col.  actions == NULL: the device-side random policy
+ * (random_policy, rl_env.cpp:237-239 / uniform (x,y) for TANKER).  reward/done
+ * may be NULL; host pointers unless `device_io` is 1.  Returns EBL_ELOGIC if a
+ * REFERENCE env is already done (rl_env.cpp:173). */
+int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* done, int device_io);
+/* Tanker fused rollout: n_steps random-policy steps on device, rewards summed
+ * into reward_sum[e] (host), episodes finished counted into episodes[e]. */
+int ebl_rl_rollout(ebl_batch* b, int n_steps, double* reward_sum, int32_t* episodes);
+/* Observation (rl_env.cpp:147-170): [n_envs][observation_size] doubles (REFERENCE). */
+int ebl_rl_observe(ebl_batch* b, double* obs);
+int ebl_rl_get_env_states(ebl_batch* b, ebl_env_state* out);
+int ebl_rl_set_env_states(ebl_batch* b, const ebl_env_state* in);
+int ebl_rl_get_wet(ebl_batch* b, uint8_t* wet);
+
+/* ---- input preparation (BASELINE configs; not part of the reference API) ---- */
+/* Synthetic per-env terrain for C1-C4: landcover class from
+ * 4-octave value noise thresholded at 11 equal quantiles into the WorldCover codes,
+ * fractal elevation in [0, elev_max] m, per-env uniform wind V~U(0,vmax),
+ * dir~U(0,2pi), all keyed by the reference RNG in domain kDrawSynthesis.
+ * fuel_class [n_envs][H*W] holds palette indices 0..10 (codes 10..100); wind may be
+ * NULL. Env e uses stream env_id0 + e. */
+int ebl_synth_terrain(uint64_t seed, uint32_t env_id0, int n_envs, int height, int width,
+                      double elev_max, double wind_max, uint8_t* fuel_class, float* elevation,
+                      double* wind_speed, double* wind_direction);
+/* The WorldCover palette of default_worldcover_table (geodata.cpp:305-319):
+ * codes[11], veg[11], den[11]. */
+void ebl_worldcover_palette(int32_t* codes, double* veg, double* den);
+/* `count` ignitions at uniform burnable cells (veg>-1, den>-1 after lookup) per
+ * env via rng_below(key{seed,0,env_id0+e}, counter++, kDrawEnvSetup, H*W),
+ * redrawing duplicates; states [n_envs][H*W] are zeroed first. */
+int ebl_synth_ignitions(uint64_t seed, uint32_t env_id0, int n_envs, int height, int width,
+                        const uint8_t* fuel_class, const double* class_veg,
+                        const double* class_den, int count, uint8_t* states);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMBER_B200_H */

@@ -1,0 +1,448 @@
+/* TEST INFRASTRUCTURE ONLY — CPU restatement of the reference's hot path.
+ * See ember_oracle.h for the contract and what pins it.  Compiled with
+ * -ffp-contract=off like the reference (proj/CMakeLists.txt:16) so every
+ * double expression rounds exactly as the reference's does; the association
+ * of each product below is the reference's (kernel.hpp:9-10 "fixed on
+ * purpose"). */
+#include "ember_oracle.h"
+
+#include <math.h>
+#include <omp.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+#define TWO_PI (2.0 * 3.14159265358979323846)
+#define SQRT2 1.41421356237309504880
+
+/* grid.hpp:74-83 — (dx east, dy north) */
+static const int kDx[8] = {1, 1, 0, -1, -1, -1, 0, 1};
+static const int kDy[8] = {0, 1, 1, 1, 0, -1, -1, -1};
+
+enum { DRAW_FIRE = 0, DRAW_SETUP = 1, DRAW_POLICY = 2 }; /* rng.hpp:22-25 */
+
+/* ---------------------------------------------------------------- rng.hpp:28-58 */
+static uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+uint64_t ebo_rng_word(uint64_t seed, uint64_t step, uint64_t stream, uint64_t cell, uint64_t draw) {
+  /* hash order seed -> stream -> step -> cell -> draw (rng.hpp:40-44) */
+  uint64_t h = mix64(0x243F6A8885A308D3ull ^ seed);
+  h = mix64(h ^ stream);
+  h = mix64(h ^ step);
+  h = mix64(h ^ cell);
+  return mix64(h ^ draw);
+}
+
+double ebo_rng_uniform(uint64_t seed, uint64_t step, uint64_t stream, uint64_t cell, uint64_t draw) {
+  return (double)(ebo_rng_word(seed, step, stream, cell, draw) >> 11) * 0x1.0p-53;
+}
+
+uint64_t ebo_rng_below(uint64_t seed, uint64_t step, uint64_t stream, uint64_t cell, uint64_t draw,
+                       uint64_t n) {
+  const uint64_t v = (uint64_t)(ebo_rng_uniform(seed, step, stream, cell, draw) * (double)n);
+  return v < n ? v : n - 1;
+}
+
+/* ---------------------------------------------------------------- grid.cpp:35-47 */
+double ebo_wrap_angle(double a) {
+  double w = fmod(a, TWO_PI);
+  if (w < 0.0) w += TWO_PI;
+  return w;
+}
+
+double ebo_offset_angle(int k) { return ebo_wrap_angle(atan2((double)kDy[k], (double)kDx[k])); }
+
+static double clamp1(double v) { return v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v); }
+
+static ebo_grid* grid_alloc(int h, int w) {
+  ebo_grid* g = (ebo_grid*)calloc(1, sizeof(ebo_grid));
+  const size_t n = (size_t)h * w;
+  g->h = h;
+  g->w = w;
+  g->speed = (double*)malloc(n * sizeof(double));
+  g->dir = (double*)malloc(n * sizeof(double));
+  g->veg = (double*)malloc(n * sizeof(double));
+  g->den = (double*)malloc(n * sizeof(double));
+  g->slope8 = (double*)calloc(n * 8, sizeof(double));
+  return g;
+}
+
+ebo_grid* ebo_grid_layers(int h, int w, const double* speed, const double* dir, const double* veg,
+                          const double* den, const double* slope8) {
+  ebo_grid* g = grid_alloc(h, w);
+  const size_t n = (size_t)h * w;
+  for (size_t i = 0; i < n; ++i) {
+    g->speed[i] = speed[i];
+    g->dir[i] = ebo_wrap_angle(dir[i]); /* WindField ctor, grid.cpp:57-60 */
+    g->veg[i] = clamp1(veg[i]);         /* FuelField ctor, grid.cpp:75-76 */
+    g->den[i] = clamp1(den[i]);
+  }
+  memcpy(g->slope8, slope8, n * 8 * sizeof(double));
+  return g;
+}
+
+/* slope_from_dem (geodata.cpp:209-229) on model-order fp32 elevation widened
+ * exactly to double; no nodata cells. */
+ebo_grid* ebo_grid_terrain(int h, int w, const double* veg, const double* den, const float* elev,
+                           double cellsize, double speed, double dir) {
+  ebo_grid* g = grid_alloc(h, w);
+  const double wd = ebo_wrap_angle(dir);
+  for (int r = 0; r < h; ++r)
+    for (int c = 0; c < w; ++c) {
+      const size_t i = (size_t)r * w + c;
+      g->speed[i] = speed;
+      g->dir[i] = wd;
+      g->veg[i] = clamp1(veg[i]);
+      g->den[i] = clamp1(den[i]);
+      for (int k = 0; k < 8; ++k) {
+        const int nr = r + kDy[k], nc = c + kDx[k];
+        if (nr < 0 || nr >= h || nc < 0 || nc >= w) continue;
+        const double dist = cellsize * ((kDx[k] != 0 && kDy[k] != 0) ? SQRT2 : 1.0);
+        g->slope8[i * 8 + k] = atan(((double)elev[(size_t)nr * w + nc] - (double)elev[i]) / dist);
+      }
+    }
+  return g;
+}
+
+void ebo_grid_free(ebo_grid* g) {
+  if (!g) return;
+  free(g->speed);
+  free(g->dir);
+  free(g->veg);
+  free(g->den);
+  free(g->slope8);
+  free(g);
+}
+
+/* ---------------------------------------------------------------- kernel.hpp:21-78 */
+static double kappa_wind(double speed, double direction, int k, const double* cfg) {
+  const double align = cos(ebo_offset_angle(k) - direction) - 1.0;
+  return exp(cfg[1] * speed) * exp((cfg[2] * speed) * align);
+}
+
+static double kappa_slope(double s, const double* cfg) { return exp(cfg[3] * s); }
+
+static double source_of(const ebo_grid* g, size_t i, const double* cfg) {
+  return (cfg[0] * (1.0 + g->veg[i])) * (1.0 + g->den[i]);
+}
+
+static double gamma_of(const ebo_grid* g, size_t i, const double* cfg) {
+  return (cfg[4] * (1.0 + g->veg[i])) * (1.0 + g->den[i]);
+}
+
+/* potential(u, d) (kernel.hpp:37-45) */
+static double potential(const ebo_grid* g, size_t u, int k, const double* cfg) {
+  const double src = source_of(g, u, cfg);
+  const double wind = kappa_wind(g->speed[u], g->dir[u], k, cfg);
+  const double slope = kappa_slope(g->slope8[u * 8 + k], cfg);
+  return (src * wind) * slope;
+}
+
+/* SpreadTables (engine.hpp:79-110): same products, so bitwise equal to potential(). */
+void ebo_tables(const ebo_grid* g, const double* cfg, double* pot, double* gamma) {
+  const size_t n = (size_t)g->h * g->w;
+#pragma omp parallel for schedule(static) if (n > 65536)
+  for (long long ii = 0; ii < (long long)n; ++ii) {
+    const size_t i = (size_t)ii;
+    const double src = source_of(g, i, cfg);
+    gamma[i] = gamma_of(g, i, cfg);
+    for (int k = 0; k < 8; ++k) {
+      const double sf = kappa_slope(g->slope8[i * 8 + k], cfg);
+      const double kw = kappa_wind(g->speed[i], g->dir[i], k, cfg);
+      pot[i * 8 + k] = (src * kw) * sf;
+    }
+  }
+}
+
+/* arrival_intensity: fixed k order, skip OOB, skip zero weight (kernel.hpp:53-67) */
+void ebo_intensity(const ebo_grid* g, const double* cfg, const uint8_t* fire, double* lambda,
+                   double* p) {
+  const int h = g->h, w = g->w;
+  for (int r = 0; r < h; ++r)
+    for (int c = 0; c < w; ++c) {
+      double l = 0.0;
+      for (int k = 0; k < 8; ++k) {
+        const int ur = r - kDy[k], uc = c - kDx[k];
+        if (ur < 0 || ur >= h || uc < 0 || uc >= w) continue;
+        const size_t u = (size_t)ur * w + uc;
+        if (fire[u] != 1) continue;
+        l += 1.0 * potential(g, u, k, cfg);
+      }
+      const size_t v = (size_t)r * w + c;
+      lambda[v] = l;
+      p[v] = 1.0 - exp(-(gamma_of(g, v, cfg) * l)); /* kernel.hpp:71-78 */
+    }
+}
+
+/* ---------------------------------------------------------------- engine.cpp:12-38 */
+static uint8_t next_cell(int h, int w, const double* pot, const double* gamma, double pc,
+                         uint64_t seed, uint64_t step, uint64_t stream, const uint8_t* in, int r,
+                         int c) {
+  const size_t i = (size_t)r * w + c;
+  const uint8_t s = in[i];
+  if (s == 2) return 2;
+  const double u = ebo_rng_uniform(seed, step, stream, (uint64_t)i, DRAW_FIRE);
+  if (s == 1) return u < pc ? 1 : 2;
+  double l = 0.0;
+  for (int k = 0; k < 8; ++k) {
+    const int ur = r - kDy[k], uc = c - kDx[k];
+    if (ur < 0 || ur >= h || uc < 0 || uc >= w) continue;
+    const size_t uu = (size_t)ur * w + uc;
+    if (in[uu] != 1) continue;
+    l += 1.0 * pot[uu * 8 + k];
+  }
+  const double p = 1.0 - exp(-(gamma[i] * l));
+  return u < p ? 1 : 0;
+}
+
+void ebo_step_tables(int h, int w, const double* pot, const double* gamma, double p_continue,
+                     uint64_t seed, uint64_t step, uint64_t stream, const uint8_t* in, uint8_t* out) {
+  for (int r = 0; r < h; ++r)
+    for (int c = 0; c < w; ++c)
+      out[(size_t)r * w + c] = next_cell(h, w, pot, gamma, p_continue, seed, step, stream, in, r, c);
+}
+
+void ebo_run(const ebo_grid* g, const double* cfg, uint64_t seed, uint64_t step0, uint64_t stream,
+             int steps, uint8_t* state) {
+  const size_t n = (size_t)g->h * g->w;
+  double* pot = (double*)malloc(n * 8 * sizeof(double));
+  double* gam = (double*)malloc(n * sizeof(double));
+  uint8_t* tmp = (uint8_t*)malloc(n);
+  ebo_tables(g, cfg, pot, gam);
+  for (int t = 0; t < steps; ++t) {
+    ebo_step_tables(g->h, g->w, pot, gam, cfg[5], seed, step0 + (uint64_t)t, stream, state, tmp);
+    memcpy(state, tmp, n);
+  }
+  free(pot);
+  free(gam);
+  free(tmp);
+}
+
+double ebo_run_envs(ebo_grid* const* grids, int n_envs, const double* cfg, uint64_t seed,
+                    const uint64_t* streams, int steps, uint8_t* states, int threads) {
+  const size_t n = (size_t)grids[0]->h * grids[0]->w;
+  if (threads > 0) omp_set_num_threads(threads);
+  struct timespec t0, t1;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int e = 0; e < n_envs; ++e) ebo_run(grids[e], cfg, seed, 0, streams[e], steps, states + e * n);
+  clock_gettime(CLOCK_MONOTONIC, &t1);
+  return (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+}
+
+void ebo_counts(const uint8_t* fire, int n, int32_t* counts) {
+  counts[0] = counts[1] = counts[2] = 0;
+  for (int i = 0; i < n; ++i) counts[fire[i] > 2 ? 2 : fire[i]]++;
+}
+
+/* ---------------------------------------------------------------- rl_env.cpp */
+int ebo_env_obs_size(const ebo_env_cfg* c) {
+  const int side = 2 * c->window_radius + 1;
+  return 3 * side * side + 3;
+}
+
+static int count_state(const uint8_t* f, int n, uint8_t v) {
+  int k = 0;
+  for (int i = 0; i < n; ++i) k += f[i] == v;
+  return k;
+}
+
+/* reset (rl_env.cpp:125-145) */
+void ebo_env_reset(const ebo_env_cfg* c, uint64_t seed, uint64_t stream, ebo_env_state* s,
+                   uint8_t* fire) {
+  const uint64_t n = (uint64_t)c->height * c->width;
+  memset(fire, 0, n);
+  uint64_t counter = 0;
+  for (int placed = 0; placed < c->ignition_count;) {
+    const uint64_t cell = ebo_rng_below(seed, 0, stream, counter++, DRAW_SETUP, n);
+    if (fire[cell] == 1) continue;
+    fire[cell] = 1;
+    ++placed;
+  }
+  const uint64_t a = ebo_rng_below(seed, 0, stream, counter++, DRAW_SETUP, n);
+  s->agent_row = (int)(a / (uint64_t)c->width);
+  s->agent_col = (int)(a % (uint64_t)c->width);
+  s->water = c->water_capacity;
+  s->step = 0;
+  s->seed = seed;
+  s->stream = stream;
+  s->done = count_state(fire, (int)n, 1) == 0;
+}
+
+/* observe (rl_env.cpp:147-170) */
+void ebo_env_observe(const ebo_env_cfg* c, const ebo_env_state* s, const uint8_t* fire,
+                     double* obs) {
+  const int r = c->window_radius;
+  memset(obs, 0, sizeof(double) * (size_t)ebo_env_obs_size(c));
+  size_t at = 0;
+  for (int dy = r; dy >= -r; --dy)
+    for (int dx = -r; dx <= r; ++dx) {
+      const int row = s->agent_row + dy, col = s->agent_col + dx;
+      if (row >= 0 && row < c->height && col >= 0 && col < c->width)
+        obs[at + fire[row * c->width + col]] = 1.0;
+      at += 3;
+    }
+  obs[at++] = (double)s->water / c->water_capacity;
+  obs[at++] = c->height > 1 ? (double)s->agent_row / (c->height - 1) : 0.0;
+  obs[at++] = c->width > 1 ? (double)s->agent_col / (c->width - 1) : 0.0;
+}
+
+/* step (rl_env.cpp:172-210) on the flat terrain of the config (rl_env.cpp:99-105) */
+int ebo_env_step(const ebo_env_cfg* c, const ebo_env_state* s, const uint8_t* fire, int action,
+                 ebo_env_state* so, uint8_t* fo, double* reward, double* obs) {
+  if (s->done) return -1;
+  if (action < 0 || action >= 10) return -2;
+  const int h = c->height, w = c->width, n = h * w;
+  *so = *s;
+  uint8_t* cur = (uint8_t*)malloc((size_t)n);
+  memcpy(cur, fire, (size_t)n);
+  const int move = action / 2, open = action % 2;
+  switch (move) {
+    case 0: so->agent_row = so->agent_row + 1 < h - 1 ? so->agent_row + 1 : h - 1; break;
+    case 1: so->agent_row = so->agent_row - 1 > 0 ? so->agent_row - 1 : 0; break;
+    case 2: so->agent_col = so->agent_col + 1 < w - 1 ? so->agent_col + 1 : w - 1; break;
+    case 3: so->agent_col = so->agent_col - 1 > 0 ? so->agent_col - 1 : 0; break;
+    default: break;
+  }
+  if (open && so->water > 0) {
+    const int a = so->agent_row * w + so->agent_col;
+    const int on_fire = cur[a] == 1;
+    if (on_fire) cur[a] = 2;
+    if (on_fire || c->waste_water) so->water -= 1;
+  }
+  /* flat terrain tables */
+  double* pot = (double*)malloc(sizeof(double) * 8 * (size_t)n);
+  double* gam = (double*)malloc(sizeof(double) * (size_t)n);
+  double* zero8 = (double*)calloc((size_t)n * 8, sizeof(double));
+  double *sp = (double*)malloc(sizeof(double) * n), *dr = (double*)malloc(sizeof(double) * n);
+  double *vg = (double*)malloc(sizeof(double) * n), *dn = (double*)malloc(sizeof(double) * n);
+  for (int i = 0; i < n; ++i) {
+    sp[i] = c->wind_speed;
+    dr[i] = c->wind_direction;
+    vg[i] = c->fuel_veg;
+    dn[i] = c->fuel_den;
+  }
+  ebo_grid* g = ebo_grid_layers(h, w, sp, dr, vg, dn, zero8);
+  ebo_tables(g, c->spread, pot, gam);
+  ebo_step_tables(h, w, pot, gam, c->spread[5], s->seed, (uint64_t)s->step, s->stream, cur, fo);
+  so->step = s->step + 1;
+  const int burning = count_state(fo, n, 1);
+  double rw = -c->burn_penalty * burning;
+  if (burning == 0 && count_state(fo, n, 0) != n) rw += 10.0; /* kTerminalBonus */
+  so->done = burning == 0 || so->step >= c->max_episode_steps;
+  *reward = rw;
+  if (obs) ebo_env_observe(c, so, fo, obs);
+  ebo_grid_free(g);
+  free(pot), free(gam), free(zero8), free(sp), free(dr), free(vg), free(dn), free(cur);
+  return 0;
+}
+
+/* random_policy (rl_env.cpp:237-239) */
+int ebo_random_policy(uint64_t seed, uint64_t step, uint64_t stream) {
+  return (int)ebo_rng_below(seed, step, stream, 0, DRAW_POLICY, 10);
+}
+
+/* ---------------------------------------------------------------- tanker (C2) */
+static uint64_t tanker_stream(uint32_t env_id, uint32_t episode) {
+  return ((uint64_t)episode << 32) | env_id;
+}
+
+static int burnable(const ebo_grid* g, size_t i) {
+  return (1.0 + g->veg[i]) * (1.0 + g->den[i]) > 0.0;
+}
+
+void ebo_tanker_reset(const ebo_grid* g, const ebo_tanker_cfg* tc, uint64_t seed, uint32_t env_id,
+                      uint32_t episode, ebo_tanker_state* s, uint8_t* fire, uint8_t* wet) {
+  const uint64_t n = (uint64_t)g->h * g->w;
+  const uint64_t stream = tanker_stream(env_id, episode);
+  memset(fire, 0, n);
+  memset(wet, 0, n);
+  uint64_t counter = 0;
+  const uint64_t max_draws = 64 * n;
+  for (int placed = 0; placed < tc->ignitions && counter < max_draws;) {
+    const uint64_t cell = ebo_rng_below(seed, 0, stream, counter++, DRAW_SETUP, n);
+    if (fire[cell] == 1 || !burnable(g, cell)) continue;
+    fire[cell] = 1;
+    ++placed;
+  }
+  s->step = 0;
+  s->episode = episode;
+  s->done = count_state(fire, (int)n, 1) == 0;
+}
+
+int ebo_tanker_policy(uint64_t seed, uint32_t env_id, const ebo_tanker_state* s, int n_cells) {
+  return (int)ebo_rng_below(seed, (uint64_t)s->step, tanker_stream(env_id, s->episode), 0,
+                            DRAW_POLICY, (uint64_t)n_cells);
+}
+
+void ebo_tanker_step(const ebo_grid* g, const double* pot, const double* gamma, double p_continue,
+                     const ebo_tanker_cfg* tc, uint64_t seed, uint32_t env_id, int action,
+                     ebo_tanker_state* s, uint8_t* fire, uint8_t* wet, float* reward,
+                     uint8_t* done) {
+  const int h = g->h, w = g->w, n = h * w;
+  const int ar = action / w, ac = action % w;
+  /* 1) drop: extinguish (Burning -> Burned) and wet (Unburned stays, never ignites) a 3x3 patch */
+  for (int dr = -1; dr <= 1; ++dr)
+    for (int dc = -1; dc <= 1; ++dc) {
+      const int r = ar + dr, c = ac + dc;
+      if (r < 0 || r >= h || c < 0 || c >= w) continue;
+      const int i = r * w + c;
+      if (fire[i] == 1) fire[i] = 2;
+      else if (fire[i] == 0) wet[i] = 1;
+    }
+  /* 2) fire step with key {seed, step, stream}; wet cells are not ignitable */
+  const uint64_t stream = tanker_stream(env_id, s->episode);
+  uint8_t* nx = (uint8_t*)malloc((size_t)n);
+  int newly = 0;
+  for (int r = 0; r < h; ++r)
+    for (int c = 0; c < w; ++c) {
+      const int i = r * w + c;
+      if (fire[i] == 0 && wet[i]) {
+        nx[i] = 0;
+        continue;
+      }
+      nx[i] = next_cell(h, w, pot, gamma, p_continue, seed, (uint64_t)s->step, stream, fire, r, c);
+      newly += fire[i] == 0 && nx[i] == 1;
+    }
+  memcpy(fire, nx, (size_t)n);
+  free(nx);
+  s->step += 1;
+  const int burning = count_state(fire, n, 1);
+  *reward = -(float)newly;
+  s->done = burning == 0 || s->step >= tc->max_steps;
+  *done = (uint8_t)s->done;
+  if (s->done && tc->autoreset) ebo_tanker_reset(g, tc, seed, env_id, s->episode + 1, s, fire, wet);
+}
+
+/* ---------------------------------------------------------------- engine.hpp:147-175 */
+void ebo_det_step_tables(int h, int w, const double* pot, const double* gamma, double pc,
+                         const double* un, const double* burn, const double* bd, double* un_o,
+                         double* burn_o, double* bd_o) {
+  for (int r = 0; r < h; ++r)
+    for (int c = 0; c < w; ++c) {
+      const size_t i = (size_t)r * w + c;
+      double l = 0.0;
+      for (int k = 0; k < 8; ++k) {
+        const int ur = r - kDy[k], uc = c - kDx[k];
+        if (ur < 0 || ur >= h || uc < 0 || uc >= w) continue;
+        const size_t u = (size_t)ur * w + uc;
+        const double wgt = burn[u];
+        if (wgt == 0.0) continue;
+        l += wgt * pot[u * 8 + k];
+      }
+      const double p_ig = 1.0 - exp(-(gamma[i] * l));
+      const double newly = un[i] * p_ig;
+      const double continuing = burn[i] * pc;
+      const double burned_now = burn[i] * (1.0 - pc);
+      burn_o[i] = newly + continuing;
+      un_o[i] = un[i] - newly;
+      bd_o[i] = bd[i] + burned_now;
+    }
+}

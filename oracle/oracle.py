@@ -1,0 +1,225 @@
+"""TEST INFRASTRUCTURE ONLY: ctypes bindings of the CPU oracles.
+
+* ``port()``  -> oracle/libember_oracle.so, the C restatement (ember_oracle.c), built from
+  source anywhere (make -C oracle).
+* ``ref()``   -> oracle/_ref/libebl_ref.so, the UNMODIFIED reference sources compiled in
+  place (make -C oracle ref; only where /root/reference exists — the built .so travels).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+import this module, and only as the checker or the CPU baseline.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PORT_SO = os.path.join(HERE, "libember_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libebl_ref.so")
+
+_P, _I, _U64, _U32, _D = C.c_void_p, C.c_int, C.c_uint64, C.c_uint32, C.c_double
+
+
+class EnvCfg(C.Structure):
+    _fields_ = [("height", _I), ("width", _I), ("window_radius", _I), ("water_capacity", _I),
+                ("burn_penalty", _D), ("max_episode_steps", _I), ("ignition_count", _I),
+                ("waste_water", _I), ("wind_speed", _D), ("wind_direction", _D),
+                ("fuel_veg", _D), ("fuel_den", _D), ("spread", _D * 6)]
+
+
+class EnvSt(C.Structure):
+    _fields_ = [("agent_row", _I), ("agent_col", _I), ("water", _I), ("step", _I),
+                ("seed", _U64), ("stream", _U64), ("done", _I)]
+
+
+class TankerCfg(C.Structure):
+    _fields_ = [("ignitions", _I), ("max_steps", _I), ("autoreset", _I)]
+
+
+class TankerSt(C.Structure):
+    _fields_ = [("step", _I), ("episode", _U32), ("done", _I)]
+
+
+def ptr(a):
+    return None if a is None else a.ctypes.data_as(_P)
+
+
+def _bind(L, table):
+    for name, (res, args) in table.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    return L
+
+
+_PORT_SIG = {
+    "ebo_rng_word": (_U64, [_U64] * 5),
+    "ebo_rng_uniform": (_D, [_U64] * 5),
+    "ebo_rng_below": (_U64, [_U64] * 6),
+    "ebo_wrap_angle": (_D, [_D]),
+    "ebo_offset_angle": (_D, [_I]),
+    "ebo_grid_layers": (_P, [_I, _I, _P, _P, _P, _P, _P]),
+    "ebo_grid_terrain": (_P, [_I, _I, _P, _P, _P, _D, _D, _D]),
+    "ebo_grid_free": (None, [_P]),
+    "ebo_tables": (None, [_P, _P, _P, _P]),
+    "ebo_intensity": (None, [_P, _P, _P, _P, _P]),
+    "ebo_step_tables": (None, [_I, _I, _P, _P, _D, _U64, _U64, _U64, _P, _P]),
+    "ebo_run": (None, [_P, _P, _U64, _U64, _U64, _I, _P]),
+    "ebo_run_envs": (_D, [_P, _I, _P, _U64, _P, _I, _P, _I]),
+    "ebo_counts": (None, [_P, _I, _P]),
+    "ebo_env_obs_size": (_I, [C.POINTER(EnvCfg)]),
+    "ebo_env_reset": (None, [C.POINTER(EnvCfg), _U64, _U64, C.POINTER(EnvSt), _P]),
+    "ebo_env_step": (_I, [C.POINTER(EnvCfg), C.POINTER(EnvSt), _P, _I, C.POINTER(EnvSt), _P,
+                          C.POINTER(_D), _P]),
+    "ebo_env_observe": (None, [C.POINTER(EnvCfg), C.POINTER(EnvSt), _P, _P]),
+    "ebo_random_policy": (_I, [_U64, _U64, _U64]),
+    "ebo_tanker_reset": (None, [_P, C.POINTER(TankerCfg), _U64, _U32, _U32, C.POINTER(TankerSt),
+                                _P, _P]),
+    "ebo_tanker_step": (None, [_P, _P, _P, _D, C.POINTER(TankerCfg), _U64, _U32, _I,
+                               C.POINTER(TankerSt), _P, _P, _P, _P]),
+    "ebo_tanker_policy": (_I, [_U64, _U32, C.POINTER(TankerSt), _I]),
+    "ebo_det_step_tables": (None, [_I, _I, _P, _P, _D, _P, _P, _P, _P, _P, _P]),
+}
+
+_REF_SIG = {
+    "ref_last_error": (C.c_char_p, []),
+    "ref_rng_word": (_U64, [_U64] * 5),
+    "ref_rng_uniform": (_D, [_U64] * 5),
+    "ref_rng_below": (_U64, [_U64] * 6),
+    "ref_grid_layers": (_P, [_I, _I, _P, _P, _P, _P, _P]),
+    "ref_grid_terrain": (_P, [_I, _I, _P, _P, _P, _D, _D, _D]),
+    "ref_grid_free": (None, [_P]),
+    "ref_grid_slope": (_I, [_P, _P]),
+    "ref_tables": (_I, [_P, _P, _P, _P]),
+    "ref_intensity": (_I, [_P, _P, _P, _P, _P]),
+    "ref_run_stochastic": (_I, [_P, _P, _U64, _U64, _U64, _I, _I, _P, _P]),
+    "ref_reference_step": (_I, [_P, _P, _U64, _U64, _U64, _P, _P]),
+    "ref_step_batch": (_I, [_P, _P, _U64, _U64, _I, _I, _P, _P]),
+    "ref_run_envs": (_D, [_P, _I, _P, _U64, _P, _I, _P, _I]),
+    "ref_max_threads": (_I, []),
+    "ref_worldcover": (_I, [_I, C.POINTER(_D), C.POINTER(_D)]),
+    "ref_env_preset": (_I, [_I, C.POINTER(EnvCfg)]),
+    "ref_env_reset": (_I, [C.POINTER(EnvCfg), _U64, _U64, C.POINTER(EnvSt), _P]),
+    "ref_env_step": (_I, [C.POINTER(EnvCfg), C.POINTER(EnvSt), _P, _I, C.POINTER(EnvSt), _P,
+                          C.POINTER(_D), _P]),
+    "ref_env_observe": (_I, [C.POINTER(EnvCfg), C.POINTER(EnvSt), _P, _P]),
+    "ref_random_policy": (_I, [_U64, _U64, _U64]),
+    "ref_run_deterministic": (_I, [_P, _P, _I, _P, _P, _P]),
+    "ref_loss_grad": (_I, [_P, _P, _I, _P, _P, _D, _D, _I, C.POINTER(_D), _P]),
+}
+
+_port = None
+_ref = None
+
+
+def build_port() -> None:
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def port():
+    """The C restatement; built on demand (gcc is in the image everywhere)."""
+    global _port
+    if _port is None:
+        if not os.path.exists(PORT_SO) or (os.path.getmtime(PORT_SO) <
+                                           os.path.getmtime(os.path.join(HERE, "ember_oracle.c"))):
+            build_port()
+        _port = _bind(C.CDLL(PORT_SO), _PORT_SIG)
+    return _port
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    """The reference compiled in place; None when neither built nor buildable here."""
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_SO):
+            if not os.path.isdir("/root/reference/proj"):
+                return None
+            subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+        _ref = _bind(C.CDLL(REF_SO), _REF_SIG)
+    return _ref
+
+
+def cfg_array(cfg) -> np.ndarray:
+    """(p_base, alpha_w1, alpha_w2, alpha_s, alpha_gamma, p_continue) as float64[6]."""
+    if hasattr(cfg, "as_list"):
+        cfg = cfg.as_list()
+    return np.ascontiguousarray(np.asarray(cfg, dtype=np.float64)[:6])
+
+
+DEFAULT_CFG = np.array([0.12, 0.2, 0.4, 1.0, 1.0, 0.6])
+
+
+class Grid:
+    """Owns an oracle grid handle (port or ref) built from layers or terrain."""
+
+    def __init__(self, L, kind: str, handle):
+        self.L, self.kind, self.h = L, kind, handle
+
+    def __del__(self):
+        try:
+            (self.L.ebo_grid_free if self.kind == "port" else self.L.ref_grid_free)(self.h)
+        except Exception:
+            pass
+
+
+def grid_layers(L, kind, speed, direction, veg, den, slope8) -> Grid:
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (speed, direction, veg, den, slope8)]
+    h, w = arrs[0].shape
+    fn = L.ebo_grid_layers if kind == "port" else L.ref_grid_layers
+    g = fn(h, w, *[ptr(a) for a in arrs])
+    assert g, "oracle rejected the grid"
+    return Grid(L, kind, g)
+
+
+def grid_terrain(L, kind, veg, den, elev, cellsize, speed, direction) -> Grid:
+    v = np.ascontiguousarray(veg, dtype=np.float64)
+    d = np.ascontiguousarray(den, dtype=np.float64)
+    e = np.ascontiguousarray(elev, dtype=np.float32)
+    h, w = v.shape
+    fn = L.ebo_grid_terrain if kind == "port" else L.ref_grid_terrain
+    g = fn(h, w, ptr(v), ptr(d), ptr(e), float(cellsize), float(speed), float(direction))
+    assert g, "oracle rejected the grid"
+    return Grid(L, kind, g)
+
+
+def run(L, kind, grid: Grid, cfg, seed, step0, stream, steps, state) -> np.ndarray:
+    st = np.ascontiguousarray(state, dtype=np.uint8).copy()
+    c = cfg_array(cfg)
+    if kind == "port":
+        L.ebo_run(grid.h, ptr(c), seed, step0, stream, steps, ptr(st))
+        return st
+    out = np.empty_like(st)
+    rc = L.ref_run_stochastic(grid.h, ptr(c), seed, step0, stream, steps, 0, ptr(st), ptr(out))
+    assert rc == 0, L.ref_last_error()
+    return out
+
+
+def intensity(L, kind, grid: Grid, cfg, fire):
+    f = np.ascontiguousarray(fire, dtype=np.uint8)
+    lam = np.empty(f.shape, dtype=np.float64)
+    p = np.empty(f.shape, dtype=np.float64)
+    c = cfg_array(cfg)
+    (L.ebo_intensity if kind == "port" else L.ref_intensity)(grid.h, ptr(c), ptr(f), ptr(lam), ptr(p))
+    return lam, p
+
+
+def tables(L, kind, grid: Grid, cfg, n):
+    pot = np.empty(n * 8, dtype=np.float64)
+    gam = np.empty(n, dtype=np.float64)
+    c = cfg_array(cfg)
+    (L.ebo_tables if kind == "port" else L.ref_tables)(grid.h, ptr(c), ptr(pot), ptr(gam))
+    return pot, gam
+
+
+def fnv1a64(data: bytes) -> int:
+    h = 0xCBF29CE484222325
+    for b in data:
+        h ^= b
+        h = (h * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
+    return h

@@ -1,0 +1,13 @@
+"""B200-native batched CA fire-spread step (drop-in for emberline's stochastic engine path).
+
+The compute path is libember_b200.so (hand-written sm_100a kernels behind the C-ABI in
+include/ember_b200.h); this package is its Python face.  See DESIGN.md.
+"""
+from ._lib import (EmberError, EnvConfig, EnvState, InvalidArgument, LogicError, OutOfRange,
+                   RL_REFERENCE, RL_TANKER, SimConfig, lib)
+from .engine import (BURNED, BURNING, KERNEL_AUTO, KERNEL_RESIDENT, KERNEL_TILED, UNBURNED, Batch,
+                     Terrain, VecFireEnv, as_config, default_config, default_preset,
+                     observation_size, run_stochastic, smoke10_preset, step_stochastic,
+                     synth_ignitions, synth_terrain, validate_config, worldcover_palette)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,855 @@
+// C-ABI implementation (include/ember_b200.h): the device-resident batch object,
+// static-layer management, launch sequencing and error convention.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/ember_b200.h"
+#include "ember_host.h"
+#include "ember_kernels.h"
+#include "ember_params.h"
+
+using ebl::Cfg6;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define EBL_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return set_err(EBL_ECUDA, std::string(#call ": ") + cudaGetErrorString(e_));       \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  cudaError_t alloc(size_t count) {
+    if (count == n && p) return cudaSuccess;
+    reset();
+    n = count;
+    return cudaMalloc(&p, count * sizeof(T) + 16);
+  }
+};
+
+bool finite_all(const double* v, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) return false;
+  return true;
+}
+
+}  // namespace
+
+struct ebl_batch {
+  int device = 0;
+  int n_envs = 0, h = 0, w = 0;
+  size_t ncell = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ebl_sim_config cfg{};
+
+  DevBuf<uint8_t> state[2];
+  int cur = 0;
+  int kernel = EBL_KERNEL_AUTO;
+  bool counts_valid = false;
+  DevBuf<int32_t> counts;
+  DevBuf<unsigned long long> diag;
+  uint64_t launches = 0, steps_done = 0;
+
+  uint64_t seed = 0, step = 0;
+  std::vector<uint64_t> h_streams;
+  DevBuf<uint64_t> streams;
+
+  int mode = ebl::kStaticNone;
+  int n_grids = 0;
+  // general form
+  std::vector<double> g_speed, g_dir, g_veg, g_den, g_slope;
+  bool tables_dirty = false;
+  DevBuf<double> pot, gamma;
+  // terrain form
+  DevBuf<uint8_t> fuel;
+  DevBuf<float> elev;
+  std::vector<double> pal_veg, pal_den;
+  double cellsize = 30.0;
+  int n_winds = 0;
+  std::vector<double> wind_speed, wind_dir;
+  bool derived_dirty = false;
+  DevBuf<float> pal32, kw32;
+  DevBuf<double> pal64, kw64;
+
+  // RL
+  int rl_variant = -1;
+  ebl_env_config env_cfg{};
+  int tanker_ignitions = 5, tanker_max_steps = 256;
+  uint32_t env_id0 = 0;
+  uint64_t rl_seed = 0;
+  DevBuf<ebl::RlEnv> rl_env;
+  DevBuf<uint8_t> wet, done, mask;
+  DevBuf<double> reward, reward_sum;
+  DevBuf<int32_t> actions, error, episodes;
+  DevBuf<double> obs;
+};
+
+namespace {
+
+Cfg6 cfg6(const ebl_sim_config& c) {
+  return Cfg6{c.p_base, c.alpha_w1, c.alpha_w2, c.alpha_s, c.alpha_gamma, c.p_continue};
+}
+
+int check_batch(const ebl_batch* b) {
+  if (!b) return set_err(EBL_EINVAL, "null batch");
+  return EBL_OK;
+}
+
+// Brings the derived device-side statics in line with (config, layers).
+int prepare(ebl_batch* b) {
+  if (b->mode == ebl::kStaticNone) return set_err(EBL_ESTATE, "no grid or terrain set on the batch");
+  EBL_CUDA(cudaSetDevice(b->device));
+  const Cfg6 c = cfg6(b->cfg);
+  if (b->mode == ebl::kStaticTables && b->tables_dirty) {
+    const size_t n = b->ncell * b->n_grids;
+    std::vector<double> pot(n * 8), gam(n);
+    ebl::build_tables(n, b->g_speed.data(), b->g_dir.data(), b->g_veg.data(), b->g_den.data(),
+                      b->g_slope.data(), c, pot.data(), gam.data());
+    EBL_CUDA(b->pot.alloc(n * 8));
+    EBL_CUDA(b->gamma.alloc(n));
+    EBL_CUDA(cudaMemcpyAsync(b->pot.p, pot.data(), n * 8 * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaMemcpyAsync(b->gamma.p, gam.data(), n * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaStreamSynchronize(b->stream));
+    b->tables_dirty = false;
+  }
+  if (b->mode == ebl::kStaticTerrain && b->derived_dirty) {
+    if (b->n_winds == 0) return set_err(EBL_ESTATE, "terrain form needs ebl_batch_set_wind");
+    std::vector<float> p32(512, 0.f);
+    std::vector<double> p64(768, 0.0);
+    for (size_t k = 0; k < b->pal_veg.size(); ++k) {
+      const double v = ebl::clamp_fuel(b->pal_veg[k]), d = ebl::clamp_fuel(b->pal_den[k]);
+      p64[k] = (c.p_base * (1.0 + v)) * (1.0 + d);            // kernel.hpp:39-40
+      p64[256 + k] = (c.alpha_gamma * (1.0 + v)) * (1.0 + d);  // kernel.hpp:75-76
+      p64[512 + k] = (1.0 + v) * (1.0 + d) > 0.0 ? 1.0 : 0.0;
+      p32[k] = static_cast<float>(p64[k]);
+      p32[256 + k] = static_cast<float>(p64[256 + k]);
+    }
+    std::vector<double> k64(static_cast<size_t>(b->n_winds) * 8);
+    std::vector<float> k32(k64.size());
+    for (int e = 0; e < b->n_winds; ++e) ebl::kappa_wind8(b->wind_speed[e], b->wind_dir[e], c, &k64[e * 8]);
+    for (size_t i = 0; i < k64.size(); ++i) k32[i] = static_cast<float>(k64[i]);
+    EBL_CUDA(b->pal32.alloc(512));
+    EBL_CUDA(b->pal64.alloc(768));
+    EBL_CUDA(b->kw32.alloc(k32.size()));
+    EBL_CUDA(b->kw64.alloc(k64.size()));
+    EBL_CUDA(cudaMemcpyAsync(b->pal32.p, p32.data(), 512 * sizeof(float), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaMemcpyAsync(b->pal64.p, p64.data(), 768 * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaMemcpyAsync(b->kw32.p, k32.data(), k32.size() * sizeof(float), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaMemcpyAsync(b->kw64.p, k64.data(), k64.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaStreamSynchronize(b->stream));
+    b->derived_dirty = false;
+  }
+  return EBL_OK;
+}
+
+ebl::StepArgs step_args(const ebl_batch* b) {
+  ebl::StepArgs a{};
+  a.h = b->h;
+  a.w = b->w;
+  a.n_envs = b->n_envs;
+  a.seed = b->seed;
+  a.step = b->step;
+  a.streams = b->streams.p;
+  a.pc_thr = ebl::continue_threshold(b->cfg.p_continue);
+  a.in = b->state[b->cur].p;
+  a.out = b->state[b->cur ^ 1].p;
+  a.diag = b->diag.p;
+  a.pot = b->pot.p;
+  a.gamma = b->gamma.p;
+  a.tab_stride = b->n_grids > 1 ? b->ncell : 0;
+  a.fuel = b->fuel.p;
+  a.elev = b->elev.p;
+  a.ter_stride = b->n_grids > 1 ? b->ncell : 0;
+  a.pal32 = b->pal32.p;
+  a.pal64 = b->pal64.p;
+  a.kw32 = b->kw32.p;
+  a.kw64 = b->kw64.p;
+  a.kw_stride = b->n_winds > 1 ? 8 : 0;
+  a.alpha_s = b->cfg.alpha_s;
+  a.alpha_s32 = static_cast<float>(b->cfg.alpha_s);
+  const double d0 = b->cellsize * 1.0, d1 = b->cellsize * 1.41421356237309504880;  // geodata.cpp:222-223
+  a.dist64[0] = d0;
+  a.dist64[1] = d1;
+  a.inv_dist32[0] = static_cast<float>(1.0 / d0);
+  a.inv_dist32[1] = static_cast<float>(1.0 / d1);
+  // the fp32 guard band (1e-4 relative) holds while |alpha_s * slope| stays O(10)
+  a.force64 = !(std::fabs(b->cfg.alpha_s) <= 50.0);
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ebl_abi_version(void) { return EBL_ABI_VERSION; }
+const char* ebl_last_error(void) { return g_err.c_str(); }
+
+void ebl_default_config(ebl_sim_config* c) {
+  *c = ebl_sim_config{0.12, 0.2, 0.4, 1.0, 1.0, 0.6, 200};  // grid.hpp:173-179
+}
+
+int ebl_validate_config(const ebl_sim_config* c) {  // grid.cpp:107-124
+  auto finite = [](double v) { return std::isfinite(v); };
+  if (!finite(c->p_base) || c->p_base <= 0.0) return set_err(EBL_EINVAL, "SimConfig: p_base must be > 0");
+  if (!finite(c->alpha_gamma) || c->alpha_gamma <= 0.0)
+    return set_err(EBL_EINVAL, "SimConfig: alpha_gamma must be > 0");
+  if (!finite(c->p_continue) || c->p_continue < 0.0 || c->p_continue > 1.0)
+    return set_err(EBL_EINVAL, "SimConfig: p_continue must be in [0, 1]");
+  if (!finite(c->alpha_w1) || !finite(c->alpha_w2) || !finite(c->alpha_s))
+    return set_err(EBL_EINVAL, "SimConfig: wind/slope parameters must be finite");
+  if (c->max_steps < 1) return set_err(EBL_EINVAL, "SimConfig: max_steps must be positive");
+  return EBL_OK;
+}
+
+int ebl_batch_create(ebl_batch** out, int device, int n_envs, int height, int width, void* stream) {
+  if (!out) return set_err(EBL_EINVAL, "null out");
+  *out = nullptr;
+  if (height < 1 || width < 1) return set_err(EBL_EINVAL, "Grid: dimensions must be at least 1x1");
+  if (n_envs < 1) return set_err(EBL_EINVAL, "make_stochastic_batch: count must be >= 1");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(EBL_ECUDA, "no CUDA device available (the engine has no CPU path)");
+  if (device < 0 || device >= ndev) return set_err(EBL_EINVAL, "device ordinal out of range");
+  EBL_CUDA(cudaSetDevice(device));
+  auto b = std::make_unique<ebl_batch>();
+  b->device = device;
+  b->n_envs = n_envs;
+  b->h = height;
+  b->w = width;
+  b->ncell = static_cast<size_t>(height) * width;
+  if (stream) {
+    b->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    EBL_CUDA(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+    b->own_stream = true;
+  }
+  ebl_default_config(&b->cfg);
+  const size_t total = b->ncell * n_envs;
+  EBL_CUDA(b->state[0].alloc(total));
+  EBL_CUDA(b->state[1].alloc(total));
+  EBL_CUDA(cudaMemsetAsync(b->state[0].p, 0, total, b->stream));
+  EBL_CUDA(b->counts.alloc(static_cast<size_t>(n_envs) * 4));
+  EBL_CUDA(b->diag.alloc(2));
+  EBL_CUDA(cudaMemsetAsync(b->diag.p, 0, 2 * sizeof(unsigned long long), b->stream));
+  EBL_CUDA(b->streams.alloc(n_envs));
+  b->h_streams.resize(n_envs);
+  for (int e = 0; e < n_envs; ++e) b->h_streams[e] = static_cast<uint64_t>(e);
+  EBL_CUDA(cudaMemcpyAsync(b->streams.p, b->h_streams.data(), n_envs * sizeof(uint64_t),
+                           cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  *out = b.release();
+  return EBL_OK;
+}
+
+void ebl_batch_destroy(ebl_batch* b) {
+  if (!b) return;
+  cudaSetDevice(b->device);
+  cudaStreamSynchronize(b->stream);
+  if (b->own_stream) cudaStreamDestroy(b->stream);
+  delete b;
+}
+
+int ebl_batch_set_config(ebl_batch* b, const ebl_sim_config* c) {
+  if (int e = check_batch(b)) return e;
+  if (!c) return set_err(EBL_EINVAL, "null config");
+  b->cfg = *c;
+  b->tables_dirty = b->mode == ebl::kStaticTables;
+  b->derived_dirty = b->mode == ebl::kStaticTerrain;
+  return EBL_OK;
+}
+
+int ebl_batch_set_grid(ebl_batch* b, int n_grids, const double* speed, const double* dir,
+                       const double* veg, const double* den, const double* slope8) {
+  if (int e = check_batch(b)) return e;
+  if (n_grids != 1 && n_grids != b->n_envs) return set_err(EBL_EINVAL, "n_grids must be 1 or n_envs");
+  if (!speed || !dir || !veg || !den || !slope8) return set_err(EBL_EINVAL, "null layer");
+  const size_t n = b->ncell * n_grids;
+  for (size_t i = 0; i < n; ++i) {  // grid.cpp:49-62, 68-77, 86-90
+    if (!std::isfinite(speed[i])) return set_err(EBL_EINVAL, "WindField: non-finite speed");
+    if (speed[i] < 0.0) return set_err(EBL_EINVAL, "WindField: negative speed");
+    if (!std::isfinite(dir[i])) return set_err(EBL_EINVAL, "WindField: non-finite direction");
+    if (std::isnan(veg[i])) return set_err(EBL_EINVAL, "FuelField veg: NaN value in layer");
+    if (std::isnan(den[i])) return set_err(EBL_EINVAL, "FuelField den: NaN value in layer");
+  }
+  for (size_t i = 0; i < n * 8; ++i)
+    if (std::isnan(slope8[i])) return set_err(EBL_EINVAL, "SlopeField: NaN slope");
+  b->g_speed.assign(speed, speed + n);
+  b->g_dir.assign(dir, dir + n);
+  b->g_veg.assign(veg, veg + n);
+  b->g_den.assign(den, den + n);
+  b->g_slope.assign(slope8, slope8 + n * 8);
+  b->mode = ebl::kStaticTables;
+  b->n_grids = n_grids;
+  b->tables_dirty = true;
+  b->fuel.reset();
+  b->elev.reset();
+  return EBL_OK;
+}
+
+int ebl_batch_set_terrain(ebl_batch* b, int n_grids, const uint8_t* fuel_class, const float* elevation,
+                          int n_classes, const double* class_veg, const double* class_den,
+                          double cellsize) {
+  if (int e = check_batch(b)) return e;
+  if (n_grids != 1 && n_grids != b->n_envs) return set_err(EBL_EINVAL, "n_grids must be 1 or n_envs");
+  if (n_classes < 1 || n_classes > 256) return set_err(EBL_EINVAL, "n_classes must be in [1, 256]");
+  if (!(cellsize > 0.0) || !std::isfinite(cellsize))
+    return set_err(EBL_EINVAL, "raster_from_model: cellsize must be positive");
+  for (int k = 0; k < n_classes; ++k)
+    if (std::isnan(class_veg[k]) || std::isnan(class_den[k]))
+      return set_err(EBL_EINVAL, "FuelField: NaN value in layer");
+  const size_t n = b->ncell * n_grids;
+  for (size_t i = 0; i < n; ++i) {
+    if (fuel_class[i] >= n_classes) return set_err(EBL_EINVAL, "fuel class outside the palette");
+    if (!std::isfinite(elevation[i])) return set_err(EBL_EINVAL, "elevation must be finite");
+  }
+  EBL_CUDA(cudaSetDevice(b->device));
+  EBL_CUDA(b->fuel.alloc(n));
+  EBL_CUDA(b->elev.alloc(n));
+  EBL_CUDA(cudaMemcpyAsync(b->fuel.p, fuel_class, n, cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(b->elev.p, elevation, n * sizeof(float), cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  b->pal_veg.assign(class_veg, class_veg + n_classes);
+  b->pal_den.assign(class_den, class_den + n_classes);
+  b->cellsize = cellsize;
+  b->mode = ebl::kStaticTerrain;
+  b->n_grids = n_grids;
+  b->derived_dirty = true;
+  b->pot.reset();
+  b->gamma.reset();
+  if (b->n_winds == 0) {  // calm air until set
+    b->n_winds = 1;
+    b->wind_speed.assign(1, 0.0);
+    b->wind_dir.assign(1, 0.0);
+  }
+  return EBL_OK;
+}
+
+int ebl_batch_set_wind(ebl_batch* b, int n_winds, const double* speed, const double* dir) {
+  if (int e = check_batch(b)) return e;
+  if (n_winds != 1 && n_winds != b->n_envs) return set_err(EBL_EINVAL, "n_winds must be 1 or n_envs");
+  for (int i = 0; i < n_winds; ++i) {
+    if (!std::isfinite(speed[i])) return set_err(EBL_EINVAL, "WindField: non-finite speed");
+    if (speed[i] < 0.0) return set_err(EBL_EINVAL, "WindField: negative speed");
+    if (!std::isfinite(dir[i])) return set_err(EBL_EINVAL, "WindField: non-finite direction");
+  }
+  b->n_winds = n_winds;
+  b->wind_speed.assign(speed, speed + n_winds);
+  b->wind_dir.assign(dir, dir + n_winds);
+  b->derived_dirty = true;
+  return EBL_OK;
+}
+
+int ebl_batch_set_state(ebl_batch* b, const uint8_t* states) {
+  if (int e = check_batch(b)) return e;
+  const size_t total = b->ncell * b->n_envs;
+  {  // every byte in {0,1,2} (grid.cpp:133-136), 8 bytes per test
+    size_t i = 0;
+    uint64_t bad = 0;
+    for (; i + 8 <= total; i += 8) {
+      uint64_t v;
+      std::memcpy(&v, states + i, 8);
+      bad |= (v & 0xFCFCFCFCFCFCFCFCull) | (v & (v >> 1) & 0x0101010101010101ull);
+    }
+    for (; i < total; ++i) bad |= states[i] > 2;
+    if (bad) return set_err(EBL_EINVAL, "GridState: invalid fire state value");
+  }
+  EBL_CUDA(cudaSetDevice(b->device));
+  EBL_CUDA(cudaMemcpyAsync(b->state[b->cur].p, states, total, cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  b->counts_valid = false;
+  return EBL_OK;
+}
+
+int ebl_batch_get_state(ebl_batch* b, uint8_t* states) {
+  if (int e = check_batch(b)) return e;
+  EBL_CUDA(cudaSetDevice(b->device));
+  EBL_CUDA(cudaMemcpyAsync(states, b->state[b->cur].p, b->ncell * b->n_envs, cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_batch_set_state_device(ebl_batch* b, const void* d) {
+  if (int e = check_batch(b)) return e;
+  EBL_CUDA(cudaMemcpyAsync(b->state[b->cur].p, d, b->ncell * b->n_envs, cudaMemcpyDeviceToDevice, b->stream));
+  b->counts_valid = false;
+  return EBL_OK;
+}
+
+int ebl_batch_get_state_device(ebl_batch* b, void* d) {
+  if (int e = check_batch(b)) return e;
+  EBL_CUDA(cudaMemcpyAsync(d, b->state[b->cur].p, b->ncell * b->n_envs, cudaMemcpyDeviceToDevice, b->stream));
+  return EBL_OK;
+}
+
+void* ebl_batch_state_device_ptr(ebl_batch* b) { return b ? b->state[b->cur].p : nullptr; }
+
+int ebl_batch_set_key(ebl_batch* b, uint64_t seed, uint64_t step, const uint64_t* streams,
+                      uint64_t first_stream) {
+  if (int e = check_batch(b)) return e;
+  b->seed = seed;
+  b->step = step;
+  for (int e = 0; e < b->n_envs; ++e) b->h_streams[e] = streams ? streams[e] : first_stream + e;
+  EBL_CUDA(cudaSetDevice(b->device));
+  EBL_CUDA(cudaMemcpyAsync(b->streams.p, b->h_streams.data(), b->n_envs * sizeof(uint64_t),
+                           cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+uint64_t ebl_batch_step_index(const ebl_batch* b) { return b ? b->step : 0; }
+
+int ebl_batch_set_kernel(ebl_batch* b, int which) {
+  if (int e = check_batch(b)) return e;
+  if (which < EBL_KERNEL_AUTO || which > EBL_KERNEL_RESIDENT) return set_err(EBL_EINVAL, "unknown kernel");
+  if (which == EBL_KERNEL_RESIDENT && !ebl::resident_fits(b->h, b->w))
+    return set_err(EBL_EINVAL, "env too large for the resident kernel");
+  b->kernel = which;
+  return EBL_OK;
+}
+
+int ebl_step_batch(ebl_batch* b, int n_steps) {
+  if (int e = check_batch(b)) return e;
+  if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
+  if (n_steps == 0) return EBL_OK;
+  if (int e = prepare(b)) return e;
+  const bool resident = b->kernel == EBL_KERNEL_RESIDENT ||
+                        (b->kernel == EBL_KERNEL_AUTO && ebl::resident_fits(b->h, b->w));
+  if (resident) {
+    if (!ebl::resident_fits(b->h, b->w))
+      return set_err(EBL_EINVAL, "env too large for the resident kernel");
+    ebl::StepArgs a = step_args(b);
+    a.counts = b->counts.p;
+    EBL_CUDA(ebl::launch_step_resident(a, b->mode, n_steps, b->stream));
+    b->cur ^= 1;
+    b->step += n_steps;
+    b->launches += 1;
+    b->steps_done += n_steps;
+    b->counts_valid = true;
+    return EBL_OK;
+  }
+  for (int t = 0; t < n_steps; ++t) {
+    ebl::StepArgs a = step_args(b);
+    const bool last = t == n_steps - 1;
+    if (last) {
+      EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
+      a.counts = b->counts.p;
+    }
+    EBL_CUDA(ebl::launch_step_tile(a, b->mode, b->stream));
+    b->cur ^= 1;
+    b->step += 1;
+    b->launches += 1;
+  }
+  b->steps_done += n_steps;
+  b->counts_valid = true;
+  return EBL_OK;
+}
+
+int ebl_batch_counts(ebl_batch* b, int32_t* out) {
+  if (int e = check_batch(b)) return e;
+  EBL_CUDA(cudaSetDevice(b->device));
+  if (!b->counts_valid) {
+    EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
+    EBL_CUDA(ebl::launch_counts(b->state[b->cur].p, b->n_envs, static_cast<int>(b->ncell), b->counts.p, b->stream));
+    b->counts_valid = true;
+  }
+  EBL_CUDA(cudaMemcpyAsync(out, b->counts.p, b->n_envs * 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_batch_intensity(ebl_batch* b, float* lambda, float* p) {
+  if (int e = check_batch(b)) return e;
+  if (int e = prepare(b)) return e;
+  const size_t total = b->ncell * b->n_envs;
+  DevBuf<float> dl, dp;
+  EBL_CUDA(dl.alloc(total));
+  EBL_CUDA(dp.alloc(total));
+  ebl::StepArgs a = step_args(b);
+  EBL_CUDA(ebl::launch_intensity(a, b->mode, dl.p, dp.p, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(lambda, dl.p, total * sizeof(float), cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(p, dp.p, total * sizeof(float), cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_batch_diag(ebl_batch* b, uint64_t* out4, int reset) {
+  if (int e = check_batch(b)) return e;
+  unsigned long long d[2];
+  EBL_CUDA(cudaMemcpyAsync(d, b->diag.p, sizeof d, cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  out4[0] = d[0];
+  out4[1] = d[1];
+  out4[2] = b->steps_done;
+  out4[3] = b->launches;
+  if (reset) {
+    EBL_CUDA(cudaMemsetAsync(b->diag.p, 0, sizeof d, b->stream));
+    b->steps_done = 0;
+    b->launches = 0;
+  }
+  return EBL_OK;
+}
+
+int ebl_device_rng_words(int n, const uint64_t* keys5, uint64_t* out) {
+  if (n < 0 || (n > 0 && (!keys5 || !out))) return set_err(EBL_EINVAL, "bad arguments");
+  if (n == 0) return EBL_OK;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(EBL_ECUDA, "no CUDA device available (the engine has no CPU path)");
+  EBL_CUDA(cudaSetDevice(0));
+  DevBuf<uint64_t> dk, dout;
+  EBL_CUDA(dk.alloc(5 * static_cast<size_t>(n)));
+  EBL_CUDA(dout.alloc(n));
+  EBL_CUDA(cudaMemcpy(dk.p, keys5, 5 * sizeof(uint64_t) * n, cudaMemcpyHostToDevice));
+  EBL_CUDA(ebl::launch_rng_probe(n, dk.p, dout.p, nullptr));
+  EBL_CUDA(cudaMemcpy(out, dout.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  return EBL_OK;
+}
+
+int ebl_batch_sync(ebl_batch* b) {
+  if (int e = check_batch(b)) return e;
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+// ---- one-shot reference signatures --------------------------------------------------
+int ebl_run_stochastic(int h, int w, const uint8_t* initial, const double* speed, const double* dir,
+                       const double* veg, const double* den, const double* slope8,
+                       const ebl_sim_config* cfg, uint64_t seed, uint64_t step, uint64_t stream,
+                       int steps, uint8_t* out) {
+  if (steps < 0) return set_err(EBL_EINVAL, "steps must be >= 0");
+  ebl_batch* b = nullptr;
+  int rc = ebl_batch_create(&b, 0, 1, h, w, nullptr);
+  if (rc) return rc;
+  std::unique_ptr<ebl_batch, void (*)(ebl_batch*)> guard(b, ebl_batch_destroy);
+  if ((rc = ebl_batch_set_config(b, cfg))) return rc;
+  if ((rc = ebl_batch_set_grid(b, 1, speed, dir, veg, den, slope8))) return rc;
+  if ((rc = ebl_batch_set_state(b, initial))) return rc;
+  if ((rc = ebl_batch_set_key(b, seed, step, &stream, 0))) return rc;
+  if ((rc = ebl_step_batch(b, steps))) return rc;
+  return ebl_batch_get_state(b, out);
+}
+
+int ebl_step_stochastic(int h, int w, const uint8_t* fire, const double* speed, const double* dir,
+                        const double* veg, const double* den, const double* slope8,
+                        const ebl_sim_config* cfg, uint64_t seed, uint64_t step, uint64_t stream,
+                        uint8_t* out) {
+  return ebl_run_stochastic(h, w, fire, speed, dir, veg, den, slope8, cfg, seed, step, stream, 1, out);
+}
+
+// ---- RL ------------------------------------------------------------------------------
+void ebl_env_default_preset(ebl_env_config* c) {  // rl_env.cpp:10-27
+  *c = ebl_env_config{20, 20, 2, 30, 0.05, 120, 1, 1, 1.0, 0.0, 0.0, 0.0,
+                      ebl_sim_config{0.06, 0.1, 0.2, 0.5, 1.0, 0.9, 200}};
+}
+
+void ebl_env_smoke10_preset(ebl_env_config* c) {  // rl_env.cpp:29-57
+  *c = ebl_env_config{10, 10, 2, 60, 0.05, 100, 3, 0, 0.5, 0.0, 0.0, 0.0,
+                      ebl_sim_config{0.03, 0.1, 0.2, 0.5, 1.0, 0.985, 200}};
+}
+
+int ebl_env_observation_size(const ebl_env_config* c) {
+  const int side = 2 * c->window_radius + 1;
+  return 3 * side * side + 3;
+}
+
+namespace {
+int validate_env(const ebl_env_config* c) {  // rl_env.cpp:80-93
+  if (c->height < 1 || c->width < 1) return set_err(EBL_EINVAL, "EnvConfig: dimensions must be at least 1x1");
+  if (c->window_radius < 0) return set_err(EBL_EINVAL, "EnvConfig: negative window radius");
+  if (c->water_capacity < 1) return set_err(EBL_EINVAL, "EnvConfig: water capacity must be >= 1");
+  if (!(c->burn_penalty > 0.0)) return set_err(EBL_EINVAL, "EnvConfig: burn penalty must be > 0");
+  if (c->max_episode_steps < 1) return set_err(EBL_EINVAL, "EnvConfig: max episode steps must be >= 1");
+  if (c->ignition_count < 0 || c->ignition_count > c->height * c->width)
+    return set_err(EBL_EINVAL, "EnvConfig: ignition count outside [0, cells]");
+  return EBL_OK;
+}
+
+ebl::RlArgs rl_args(ebl_batch* b) {
+  ebl::RlArgs g{};
+  g.s = step_args(b);
+  g.env = b->rl_env.p;
+  g.state = b->state[b->cur].p;
+  g.wet = b->wet.p;
+  g.error = b->error.p;
+  g.water_capacity = b->env_cfg.water_capacity;
+  g.max_episode_steps = b->env_cfg.max_episode_steps;
+  g.waste_water = b->env_cfg.waste_water;
+  g.burn_penalty = b->env_cfg.burn_penalty;
+  g.ignitions = b->tanker_ignitions;
+  g.max_steps = b->tanker_max_steps;
+  g.env_id0 = b->env_id0;
+  g.seed = b->rl_seed;
+  g.n_steps = 1;
+  return g;
+}
+}  // namespace
+
+int ebl_rl_configure(ebl_batch* b, int variant, const ebl_env_config* c, int tanker_ignitions,
+                     int tanker_max_steps, uint32_t env_id0) {
+  if (int e = check_batch(b)) return e;
+  if (variant != EBL_RL_REFERENCE && variant != EBL_RL_TANKER) return set_err(EBL_EINVAL, "unknown RL variant");
+  if (b->ncell > static_cast<size_t>(ebl::kRlMaxCells))
+    return set_err(EBL_EINVAL, "RL envs must have at most 16384 cells (layer resident in shared memory)");
+  EBL_CUDA(cudaSetDevice(b->device));
+  if (variant == EBL_RL_REFERENCE) {
+    if (!c) return set_err(EBL_EINVAL, "null env config");
+    if (int e = validate_env(c)) return e;
+    if (c->height != b->h || c->width != b->w) return set_err(EBL_EINVAL, "EnvConfig dims differ from the batch");
+    b->env_cfg = *c;
+    // flat terrain of the config (rl_env.cpp:99-105): one fuel class, zero elevation
+    const uint8_t zero = 0;
+    std::vector<uint8_t> cls(b->ncell, zero);
+    std::vector<float> el(b->ncell, 0.f);
+    const double veg = c->fuel_veg, den = c->fuel_den;
+    if (int e = ebl_batch_set_terrain(b, 1, cls.data(), el.data(), 1, &veg, &den, 30.0)) return e;
+    if (int e = ebl_batch_set_wind(b, 1, &c->wind_speed, &c->wind_direction)) return e;
+    if (int e = ebl_batch_set_config(b, &c->spread)) return e;
+  } else {
+    if (b->mode == ebl::kStaticNone) return set_err(EBL_ESTATE, "tanker RL needs terrain set first");
+    if (tanker_max_steps < 1 || tanker_ignitions < 0) return set_err(EBL_EINVAL, "bad tanker config");
+    b->tanker_ignitions = tanker_ignitions;
+    b->tanker_max_steps = tanker_max_steps;
+    b->env_id0 = env_id0;
+  }
+  b->rl_variant = variant;
+  const size_t n = b->n_envs;
+  EBL_CUDA(b->rl_env.alloc(n));
+  EBL_CUDA(b->wet.alloc(n * b->ncell));
+  EBL_CUDA(cudaMemsetAsync(b->wet.p, 0, n * b->ncell, b->stream));
+  EBL_CUDA(b->done.alloc(n));
+  EBL_CUDA(b->reward.alloc(n));
+  EBL_CUDA(b->reward_sum.alloc(n));
+  EBL_CUDA(b->episodes.alloc(n));
+  EBL_CUDA(b->actions.alloc(n));
+  EBL_CUDA(b->mask.alloc(n));
+  EBL_CUDA(b->error.alloc(1));
+  EBL_CUDA(cudaMemsetAsync(b->error.p, 0, sizeof(int32_t), b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_rl_reset(ebl_batch* b, uint64_t seed, const uint64_t* streams, const uint8_t* mask) {
+  if (int e = check_batch(b)) return e;
+  if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
+  if (int e = prepare(b)) return e;
+  EBL_CUDA(cudaSetDevice(b->device));
+  if (b->rl_variant == EBL_RL_REFERENCE) {
+    // FireSuppressionEnv::reset is a short serial draw loop per env (rl_env.cpp:125-145);
+    // it runs on the host and uploads the layers (once per episode, off the step path).
+    const ebl_env_config& c = b->env_cfg;
+    const uint64_t n = b->ncell;
+    std::vector<uint8_t> st(n * b->n_envs);
+    std::vector<ebl::RlEnv> ev(b->n_envs);
+    EBL_CUDA(cudaMemcpyAsync(st.data(), b->state[b->cur].p, st.size(), cudaMemcpyDeviceToHost, b->stream));
+    EBL_CUDA(cudaMemcpyAsync(ev.data(), b->rl_env.p, ev.size() * sizeof(ebl::RlEnv), cudaMemcpyDeviceToHost, b->stream));
+    EBL_CUDA(cudaStreamSynchronize(b->stream));
+    for (int e = 0; e < b->n_envs; ++e) {
+      if (mask && !mask[e]) continue;
+      const uint64_t stream = streams ? streams[e] : b->env_id0 + static_cast<uint64_t>(e);
+      uint8_t* f = st.data() + e * n;
+      std::memset(f, 0, n);
+      uint64_t counter = 0;
+      int burning = 0;
+      for (int placed = 0; placed < c.ignition_count;) {
+        const uint64_t cell = ebl::rng_below(seed, 0, stream, counter++, 1, n);
+        if (f[cell] == 1) continue;
+        f[cell] = 1;
+        ++placed;
+        ++burning;
+      }
+      const uint64_t a = ebl::rng_below(seed, 0, stream, counter++, 1, n);
+      ebl::RlEnv& r = ev[e];
+      r.row = static_cast<int32_t>(a / static_cast<uint64_t>(c.width));
+      r.col = static_cast<int32_t>(a % static_cast<uint64_t>(c.width));
+      r.water = c.water_capacity;
+      r.step = 0;
+      r.seed = seed;
+      r.stream = stream;
+      r.done = burning == 0;
+      r.episode = 0;
+    }
+    EBL_CUDA(cudaMemcpyAsync(b->state[b->cur].p, st.data(), st.size(), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaMemcpyAsync(b->rl_env.p, ev.data(), ev.size() * sizeof(ebl::RlEnv), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaStreamSynchronize(b->stream));
+  } else {
+    b->rl_seed = seed;
+    const uint8_t* dmask = nullptr;
+    if (mask) {
+      EBL_CUDA(cudaMemcpyAsync(b->mask.p, mask, b->n_envs, cudaMemcpyHostToDevice, b->stream));
+      dmask = b->mask.p;
+    }
+    ebl::RlArgs g = rl_args(b);
+    EBL_CUDA(ebl::launch_rl_tanker_reset(g, b->mode, dmask, b->stream));
+    b->launches += 1;
+  }
+  b->counts_valid = false;
+  return EBL_OK;
+}
+
+int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* done, int device_io) {
+  if (int e = check_batch(b)) return e;
+  if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
+  if (int e = prepare(b)) return e;
+  EBL_CUDA(cudaSetDevice(b->device));
+  ebl::RlArgs g = rl_args(b);
+  if (actions) {
+    if (device_io) {
+      g.actions = actions;
+    } else {
+      if (b->rl_variant == EBL_RL_REFERENCE)
+        for (int e = 0; e < b->n_envs; ++e)
+          if (actions[e] < 0 || actions[e] >= 10)
+            return set_err(EBL_ERANGE, "action_from_index: index " + std::to_string(actions[e]) + " outside [0, 10)");
+      EBL_CUDA(cudaMemcpyAsync(b->actions.p, actions, b->n_envs * sizeof(int32_t), cudaMemcpyHostToDevice, b->stream));
+      g.actions = b->actions.p;
+    }
+  }
+  g.reward = device_io && reward ? reward : b->reward.p;
+  g.done = device_io && done ? done : b->done.p;
+  if (b->rl_variant == EBL_RL_REFERENCE) {
+    EBL_CUDA(ebl::launch_rl_ref_step(g, b->mode, b->stream));
+  } else {
+    EBL_CUDA(ebl::launch_rl_tanker(g, b->mode, b->stream));
+  }
+  b->launches += 1;
+  b->steps_done += 1;
+  b->counts_valid = false;
+  if (!device_io) {
+    if (reward) EBL_CUDA(cudaMemcpyAsync(reward, b->reward.p, b->n_envs * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+    if (done) EBL_CUDA(cudaMemcpyAsync(done, b->done.p, b->n_envs, cudaMemcpyDeviceToHost, b->stream));
+  }
+  if (b->rl_variant == EBL_RL_REFERENCE) {
+    int32_t err = 0;
+    EBL_CUDA(cudaMemcpyAsync(&err, b->error.p, sizeof err, cudaMemcpyDeviceToHost, b->stream));
+    EBL_CUDA(cudaStreamSynchronize(b->stream));
+    if (err) {
+      EBL_CUDA(cudaMemsetAsync(b->error.p, 0, sizeof(int32_t), b->stream));
+      return set_err(EBL_ELOGIC, "FireSuppressionEnv::step: episode already finished");
+    }
+  } else if (!device_io && (reward || done)) {
+    EBL_CUDA(cudaStreamSynchronize(b->stream));
+  }
+  return EBL_OK;
+}
+
+int ebl_rl_rollout(ebl_batch* b, int n_steps, double* reward_sum, int32_t* episodes) {
+  if (int e = check_batch(b)) return e;
+  if (b->rl_variant != EBL_RL_TANKER) return set_err(EBL_ESTATE, "rollout needs the tanker variant");
+  if (n_steps < 1) return set_err(EBL_EINVAL, "n_steps must be >= 1");
+  if (int e = prepare(b)) return e;
+  EBL_CUDA(cudaSetDevice(b->device));
+  EBL_CUDA(cudaMemsetAsync(b->reward_sum.p, 0, b->n_envs * sizeof(double), b->stream));
+  EBL_CUDA(cudaMemsetAsync(b->episodes.p, 0, b->n_envs * sizeof(int32_t), b->stream));
+  ebl::RlArgs g = rl_args(b);
+  g.n_steps = n_steps;
+  g.reward_sum = b->reward_sum.p;
+  g.episodes = b->episodes.p;
+  EBL_CUDA(ebl::launch_rl_tanker(g, b->mode, b->stream));
+  b->launches += 1;
+  b->steps_done += n_steps;
+  b->counts_valid = false;
+  if (reward_sum) EBL_CUDA(cudaMemcpyAsync(reward_sum, b->reward_sum.p, b->n_envs * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+  if (episodes) EBL_CUDA(cudaMemcpyAsync(episodes, b->episodes.p, b->n_envs * sizeof(int32_t), cudaMemcpyDeviceToHost, b->stream));
+  if (reward_sum || episodes) EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_rl_observe(ebl_batch* b, double* obs) {
+  if (int e = check_batch(b)) return e;
+  if (b->rl_variant != EBL_RL_REFERENCE) return set_err(EBL_ESTATE, "observe needs the reference variant");
+  const int osz = ebl_env_observation_size(&b->env_cfg);
+  const size_t total = static_cast<size_t>(b->n_envs) * osz;
+  EBL_CUDA(b->obs.alloc(total));
+  EBL_CUDA(ebl::launch_rl_observe(b->state[b->cur].p, b->rl_env.p, b->n_envs, b->h, b->w,
+                                  b->env_cfg.window_radius, b->env_cfg.water_capacity, b->obs.p, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(obs, b->obs.p, total * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_rl_get_env_states(ebl_batch* b, ebl_env_state* out) {
+  if (int e = check_batch(b)) return e;
+  if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
+  std::vector<ebl::RlEnv> ev(b->n_envs);
+  EBL_CUDA(cudaMemcpyAsync(ev.data(), b->rl_env.p, ev.size() * sizeof(ebl::RlEnv), cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  for (int e = 0; e < b->n_envs; ++e) {
+    const ebl::RlEnv& r = ev[e];
+    out[e] = ebl_env_state{r.row, r.col, r.water, r.step, r.seed, r.stream, r.done,
+                           r.episode};
+  }
+  return EBL_OK;
+}
+
+int ebl_rl_set_env_states(ebl_batch* b, const ebl_env_state* in) {
+  if (int e = check_batch(b)) return e;
+  if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
+  std::vector<ebl::RlEnv> ev(b->n_envs);
+  for (int e = 0; e < b->n_envs; ++e) {
+    const ebl_env_state& s = in[e];
+    ev[e] = ebl::RlEnv{s.agent_row, s.agent_col, s.water, s.step, s.seed, s.stream, s.done,
+                       s.episode};
+  }
+  EBL_CUDA(cudaMemcpyAsync(b->rl_env.p, ev.data(), ev.size() * sizeof(ebl::RlEnv), cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_rl_get_wet(ebl_batch* b, uint8_t* wet) {
+  if (int e = check_batch(b)) return e;
+  if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
+  EBL_CUDA(cudaMemcpyAsync(wet, b->wet.p, b->ncell * b->n_envs, cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+// ---- inputs ----------------------------------------------------------------------------
+int ebl_synth_terrain(uint64_t seed, uint32_t env_id0, int n_envs, int h, int w, double elev_max,
+                      double wind_max, uint8_t* fuel_class, float* elevation, double* wind_speed,
+                      double* wind_direction) {
+  if (n_envs < 1 || h < 2 || w < 2) return set_err(EBL_EINVAL, "synth_terrain: need n_envs >= 1, dims >= 2");
+  if (!fuel_class || !elevation) return set_err(EBL_EINVAL, "null output");
+  ebl::synth_terrain(seed, env_id0, n_envs, h, w, elev_max, wind_max, fuel_class, elevation,
+                     wind_speed, wind_direction);
+  return EBL_OK;
+}
+
+void ebl_worldcover_palette(int32_t* codes, double* veg, double* den) {
+  ebl::worldcover_palette(codes, veg, den);
+}
+
+int ebl_synth_ignitions(uint64_t seed, uint32_t env_id0, int n_envs, int h, int w,
+                        const uint8_t* fuel_class, const double* class_veg, const double* class_den,
+                        int count, uint8_t* states) {
+  if (n_envs < 1 || h < 1 || w < 1 || count < 0) return set_err(EBL_EINVAL, "synth_ignitions: bad sizes");
+  return ebl::synth_ignitions(seed, env_id0, n_envs, h, w, fuel_class, class_veg, class_den, count,
+                              states) >= 0
+             ? EBL_OK
+             : EBL_EINVAL;
+}
+
+}  // extern "C"

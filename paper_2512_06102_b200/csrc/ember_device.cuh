@@ -1,0 +1,188 @@
+// Device-side core of the stochastic CA step: the reference's counter RNG
+// (rng.hpp:28-58) reproduced bit-exactly, and the per-cell transition
+// (engine.cpp:12-26 next_fire_cell) evaluated as
+//   * an exact integer test for Burning cells (u < p_continue  <=>  (w>>11) < ceil(p_continue*2^53)),
+//   * a skip for Unburned cells with no burning neighbour (lambda = 0 => p = 0 => u < p is false,
+//     so the draw the reference takes there cannot change the outcome; the RNG is counter-based,
+//     so not drawing is invisible to every other cell),
+//   * an fp32 fast path with a relative guard band for Unburned front cells, falling back to
+//     an fp64 evaluation in the reference's exact association (kernel.hpp:21-78,
+//     engine.hpp:79-143) only when the draw lies inside the band.
+#pragma once
+#include <cstdint>
+
+#include "ember_params.h"
+
+namespace ebl {
+
+// grid.hpp:74-83, (dx east, dy north), k = 0..7 : E NE N NW W SW S SE
+__device__ __constant__ const int8_t kDx[8] = {1, 1, 0, -1, -1, -1, 0, 1};
+__device__ __constant__ const int8_t kDy[8] = {0, 1, 1, 1, 0, -1, -1, -1};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+// First three rounds of rng_word (seed -> stream -> step), constant per (env, step).
+__device__ __forceinline__ uint64_t key_prefix(uint64_t seed, uint64_t stream, uint64_t step) {
+  return mix64(mix64(mix64(0x243F6A8885A308D3ull ^ seed) ^ stream) ^ step);
+}
+
+// Remaining two rounds (cell, draw); >> 11 gives the 53-bit mantissa m, u = m * 2^-53.
+__device__ __forceinline__ uint64_t cell_bits53(uint64_t prefix, uint64_t cell, uint64_t draw) {
+  return mix64(mix64(prefix ^ cell) ^ draw) >> 11;
+}
+
+__device__ __forceinline__ double bits_to_uniform(uint64_t m) {
+  return static_cast<double>(m) * 0x1.0p-53;  // exact
+}
+
+// rng_below (rng.hpp:54-58): truncating conversion of u*n, clamped.
+__device__ __forceinline__ uint64_t below(uint64_t m, uint64_t n) {
+  const double x = __dmul_rn(bits_to_uniform(m), static_cast<double>(n));
+  const uint64_t v = __double2ull_rz(x);
+  return v < n ? v : n - 1;
+}
+
+struct DiagCounters {
+  unsigned long long* g;  // [0] fp64 fallbacks, [1] ambiguous draws
+  __device__ __forceinline__ void fallback() const { atomicAdd(g + 0, 1ull); }
+  __device__ __forceinline__ void ambiguous() const { atomicAdd(g + 1, 1ull); }
+};
+
+// |u - p| below this (absolute) is reported as "ambiguous": the device libm
+// (exp/atan) may differ from glibc by an ulp there, so a flip vs the CPU is
+// possible only for these draws.
+constexpr double kAmbiguousBand = 1e-12;
+
+// ---- general form: SpreadTables<double> resident in HBM --------------------------
+// lambda fold in k order, skipping zero weights, then p = 1 - exp(-(gamma*lambda))
+// (engine.hpp:130-143, engine.cpp:21-25), all fp64 with explicit round-to-nearest ops.
+__device__ __forceinline__ bool ignite_tables(const double* __restrict__ pot,
+                                              const double* __restrict__ gamma, int w, int r,
+                                              int c, uint32_t nb, uint64_t m,
+                                              const DiagCounters& dg) {
+  double lam = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (nb & (1u << k)) {
+      const int u = (r - kDy[k]) * w + (c - kDx[k]);
+      lam = __dadd_rn(lam, __ldg(pot + static_cast<size_t>(u) * 8 + k));
+    }
+  }
+  const double p = __dsub_rn(1.0, exp(-__dmul_rn(__ldg(gamma + r * w + c), lam)));
+  const double u = bits_to_uniform(m);
+  if (fabs(u - p) < kAmbiguousBand) dg.ambiguous();
+  return u < p;
+}
+
+// ---- terrain form: uint8 fuel class + fp32 elevation -------------------------------
+struct TerrainView {
+  const uint8_t* __restrict__ fuel;  // env base applied
+  const float* __restrict__ elev;
+  const float* pal_src32;   // [256] (p_base*(1+veg))*(1+den)   (kernel.hpp:39-40)
+  const float* pal_gam32;   // [256] (alpha_gamma*(1+veg))*(1+den) (kernel.hpp:75-76)
+  const double* pal_src64;
+  const double* pal_gam64;
+  const float* kw32;        // [8] kappa_wind of this env (kernel.hpp:21-26)
+  const double* kw64;
+  float alpha_s32;
+  double alpha_s;
+  float inv_dist32[2];      // 1/cellsize, 1/(cellsize*sqrt2)
+  double dist64[2];         // cellsize*1.0, cellsize*sqrt2 (geodata.cpp:222-223)
+  int force64;              // parameters outside the fp32 guard's validity range
+};
+
+// fp64 re-evaluation in the reference's exact association:
+//   S   = atan((z(v) - z(u)) / dist)                 geodata.cpp:222-224
+//   pot = (source(u) * kappa_wind(k)) * exp(alpha_s*S)  engine.hpp:91,106-107
+//   p   = 1 - exp(-(gamma(v) * lambda))               engine.cpp:24
+static __device__ __noinline__ double terrain_p64(const TerrainView& t, int w, int r, int c, uint32_t nb) {
+  const int v = r * w + c;
+  const double zv = static_cast<double>(t.elev[v]);
+  double lam = 0.0;
+  for (int k = 0; k < 8; ++k) {
+    if (nb & (1u << k)) {
+      const int u = (r - kDy[k]) * w + (c - kDx[k]);
+      const double s = atan(__ddiv_rn(__dsub_rn(zv, static_cast<double>(t.elev[u])),
+                                      t.dist64[k & 1]));
+      const double ks = exp(__dmul_rn(t.alpha_s, s));
+      const double pot = __dmul_rn(__dmul_rn(t.pal_src64[t.fuel[u]], t.kw64[k]), ks);
+      lam = __dadd_rn(lam, pot);
+    }
+  }
+  return __dsub_rn(1.0, exp(-__dmul_rn(t.pal_gam64[t.fuel[v]], lam)));
+}
+
+// fp32 fast path: lambda and p within ~1e-6 relative of fp64 for |alpha_s| <= 50.
+__device__ __forceinline__ float terrain_lambda32(const TerrainView& t, int w, int r, int c,
+                                                  uint32_t nb) {
+  const float zv = t.elev[r * w + c];
+  float lam = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (nb & (1u << k)) {
+      const int u = (r - kDy[k]) * w + (c - kDx[k]);
+      const float s = atanf((zv - t.elev[u]) * t.inv_dist32[k & 1]);
+      lam += t.pal_src32[t.fuel[u]] * t.kw32[k] * expf(t.alpha_s32 * s);
+    }
+  }
+  return lam;
+}
+
+constexpr double kGuardRel = 1e-4;
+
+__device__ __forceinline__ bool ignite_terrain(const TerrainView& t, int w, int r, int c,
+                                               uint32_t nb, uint64_t m, const DiagCounters& dg) {
+  const double u = bits_to_uniform(m);
+  if (!t.force64) {
+    const float lam = terrain_lambda32(t, w, r, c, nb);
+    const double p32 = static_cast<double>(-expm1f(-t.pal_gam32[t.fuel[r * w + c]] * lam));
+    if (u < p32 * (1.0 - kGuardRel)) return true;
+    if (u >= p32 * (1.0 + kGuardRel) + 1e-37) return false;
+  }
+  dg.fallback();
+  const double p = terrain_p64(t, w, r, c, nb);
+  if (fabs(u - p) < kAmbiguousBand) dg.ambiguous();
+  return u < p;
+}
+
+__device__ __forceinline__ TerrainView terrain_view(const StepArgs& a, int env) {
+  TerrainView t;
+  const size_t base = static_cast<size_t>(env) * a.ter_stride;
+  t.fuel = a.fuel + base;
+  t.elev = a.elev + base;
+  t.pal_src32 = a.pal32;
+  t.pal_gam32 = a.pal32 + 256;
+  t.pal_src64 = a.pal64;
+  t.pal_gam64 = a.pal64 + 256;
+  t.kw32 = a.kw32 + env * a.kw_stride;
+  t.kw64 = a.kw64 + env * a.kw_stride;
+  t.alpha_s32 = a.alpha_s32;
+  t.alpha_s = a.alpha_s;
+  t.inv_dist32[0] = a.inv_dist32[0];
+  t.inv_dist32[1] = a.inv_dist32[1];
+  t.dist64[0] = a.dist64[0];
+  t.dist64[1] = a.dist64[1];
+  t.force64 = a.force64;
+  return t;
+}
+
+// Decision for an Unburned cell with burning-neighbour mask nb != 0.
+template <int MODE>
+__device__ __forceinline__ bool ignite(const StepArgs& a, int env, int r, int c, uint32_t nb,
+                                       uint64_t m, const DiagCounters& dg) {
+  if constexpr (MODE == kStaticTables) {
+    const size_t base = static_cast<size_t>(env) * a.tab_stride;
+    return ignite_tables(a.pot + base * 8, a.gamma + base, a.w, r, c, nb, m, dg);
+  } else {
+    return ignite_terrain(terrain_view(a, env), a.w, r, c, nb, m, dg);
+  }
+}
+
+}  // namespace ebl

@@ -1,0 +1,74 @@
+// Launch parameter blocks shared by the host launcher (ember_capi.cu) and the
+// kernels (ember_kernels.cu).  Plain structs, passed by value as kernel params.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace ebl {
+
+enum StaticMode : int { kStaticNone = 0, kStaticTables = 1, kStaticTerrain = 2 };
+
+// Everything one stochastic step of the whole batch needs.  Per-env statics are
+// addressed as base + env * stride (stride 0 = one grid shared by all members,
+// the StochasticBatch layout of engine.hpp:250-258).
+struct StepArgs {
+  int h, w, n_envs;
+  uint64_t seed;
+  uint64_t step;                  // lockstep step index t (RngKey::step)
+  const uint64_t* streams;        // [n_envs] Member::stream
+  uint64_t pc_thr;                // Burning survives iff (word>>11) < pc_thr (= ceil(p_continue*2^53))
+  const uint8_t* in;              // [n_envs][h*w]
+  uint8_t* out;
+  int32_t* counts;                // [n_envs][4] U,B,X,newly (nullable)
+  unsigned long long* diag;       // [2]
+  // general form (SpreadTables)
+  const double* pot;              // [grid][h*w*8]
+  const double* gamma;            // [grid][h*w]
+  size_t tab_stride;              // cells per grid, or 0
+  // terrain form
+  const uint8_t* fuel;            // [grid][h*w]
+  const float* elev;              // [grid][h*w]
+  size_t ter_stride;
+  const float* pal32;             // [2][256] src32, gam32
+  const double* pal64;            // [2][256] src64, gam64
+  const float* kw32;              // [wind][8]
+  const double* kw64;
+  int kw_stride;                  // 8 or 0
+  float alpha_s32;
+  double alpha_s;
+  float inv_dist32[2];
+  double dist64[2];
+  int force64;
+};
+
+// Per-env RL record (rl_env.hpp:67-75 EnvState minus the layer, plus the tanker
+// episode counter).
+struct RlEnv {
+  int32_t row, col, water, step;
+  uint64_t seed, stream;
+  int32_t done;
+  uint32_t episode;
+};
+
+struct RlArgs {
+  StepArgs s;                     // statics, streams unused (per-env stream in RlEnv)
+  RlEnv* env;                     // [n_envs]
+  uint8_t* state;                 // [n_envs][h*w], updated in place
+  uint8_t* wet;                   // [n_envs][h*w] (tanker)
+  const int32_t* actions;         // [n_envs] or null (device random policy)
+  double* reward;                 // [n_envs] (nullable)
+  uint8_t* done;                  // [n_envs] (nullable)
+  int32_t* error;                 // set to 1 when a finished REFERENCE env is stepped
+  // reference variant
+  int water_capacity, max_episode_steps, waste_water;
+  double burn_penalty;
+  // tanker variant
+  int ignitions, max_steps;
+  uint32_t env_id0;
+  uint64_t seed;
+  int n_steps;                    // fused rollout length (tanker)
+  double* reward_sum;             // [n_envs] (rollout)
+  int32_t* episodes;              // [n_envs] (rollout)
+};
+
+}  // namespace ebl

@@ -1,0 +1,338 @@
+"""Python mirror of the reference's engine / RL interface on top of the C-ABI.
+
+Names and argument meaning follow proj/include/emberline/engine.hpp and
+rl_env.hpp (cited per method) so the parity tests read like the reference's own
+tests.  Arrays are numpy; state layers are uint8 [..., H, W] with row 0 = south.
+Everything runs on the GPU through libember_b200.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import EnvConfig, EnvState, SimConfig, check, lib
+
+UNBURNED, BURNING, BURNED = 0, 1, 2
+KERNEL_AUTO, KERNEL_TILED, KERNEL_RESIDENT = 0, 1, 2
+
+
+def _ptr(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"], "arrays must be C-contiguous"
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def default_config(**overrides) -> SimConfig:
+    """SimConfig{} (grid.hpp:173-179) with keyword overrides."""
+    c = SimConfig()
+    lib().ebl_default_config(C.byref(c))
+    for k, v in overrides.items():
+        setattr(c, k, v)
+    return c
+
+
+def as_config(cfg) -> SimConfig:
+    if cfg is None:
+        return default_config()
+    if isinstance(cfg, SimConfig):
+        return cfg
+    if isinstance(cfg, dict):
+        return default_config(**cfg)
+    vals = list(cfg)
+    return default_config(p_base=vals[0], alpha_w1=vals[1], alpha_w2=vals[2], alpha_s=vals[3],
+                          alpha_gamma=vals[4], p_continue=vals[5])
+
+
+def validate_config(cfg) -> None:
+    """validate_config (grid.cpp:107-124): raises InvalidArgument."""
+    check(lib().ebl_validate_config(C.byref(as_config(cfg))))
+
+
+class Batch:
+    """Device-resident lockstep batch: StochasticBatch (engine.hpp:250-266) whose members
+    may each carry their own grid (n_grids == n_envs) or share one (n_grids == 1)."""
+
+    def __init__(self, n_envs: int, height: int, width: int, device: int = 0, stream=None):
+        self._h = C.c_void_p()
+        check(lib().ebl_batch_create(C.byref(self._h), device, n_envs, height, width,
+                                     C.c_void_p(stream) if stream else None))
+        self.n_envs, self.height, self.width = n_envs, height, width
+
+    # -- lifetime -----------------------------------------------------------------------
+    def close(self):
+        if self._h:
+            lib().ebl_batch_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- configuration --------------------------------------------------------------------
+    def set_config(self, cfg) -> None:
+        check(lib().ebl_batch_set_config(self._h, C.byref(as_config(cfg))))
+
+    def set_grid(self, wind_speed, wind_direction, veg, den, slope8) -> None:
+        """General GridState layers (grid.hpp:192-211): [G, H, W] (+ [.., 8] for slope)."""
+        arrs = [np.ascontiguousarray(x, dtype=np.float64)
+                for x in (wind_speed, wind_direction, veg, den, slope8)]
+        n_grids = arrs[0].size // (self.height * self.width)
+        check(lib().ebl_batch_set_grid(self._h, n_grids, *[_ptr(a) for a in arrs]))
+
+    def set_terrain(self, fuel_class, elevation, class_veg, class_den, cellsize=30.0) -> None:
+        """North-star layout: uint8 class [G,H,W] into a (veg, den) palette, fp32 elevation."""
+        fc = np.ascontiguousarray(fuel_class, dtype=np.uint8)
+        el = np.ascontiguousarray(elevation, dtype=np.float32)
+        cv = np.ascontiguousarray(class_veg, dtype=np.float64)
+        cd = np.ascontiguousarray(class_den, dtype=np.float64)
+        n_grids = fc.size // (self.height * self.width)
+        check(lib().ebl_batch_set_terrain(self._h, n_grids, _ptr(fc), _ptr(el), cv.size, _ptr(cv),
+                                          _ptr(cd), float(cellsize)))
+
+    def set_wind(self, speed, direction) -> None:
+        sp = np.ascontiguousarray(np.atleast_1d(speed), dtype=np.float64)
+        dr = np.ascontiguousarray(np.atleast_1d(direction), dtype=np.float64)
+        check(lib().ebl_batch_set_wind(self._h, sp.size, _ptr(sp), _ptr(dr)))
+
+    def set_kernel(self, which: int) -> None:
+        check(lib().ebl_batch_set_kernel(self._h, which))
+
+    # -- state / key ----------------------------------------------------------------------
+    def set_state(self, states) -> None:
+        st = np.ascontiguousarray(np.broadcast_to(np.asarray(states, dtype=np.uint8),
+                                                  (self.n_envs, self.height, self.width)))
+        check(lib().ebl_batch_set_state(self._h, _ptr(st)))
+
+    def get_state(self) -> np.ndarray:
+        out = np.empty((self.n_envs, self.height, self.width), dtype=np.uint8)
+        check(lib().ebl_batch_get_state(self._h, _ptr(out)))
+        return out
+
+    def state_device_ptr(self) -> int:
+        return lib().ebl_batch_state_device_ptr(self._h)
+
+    def set_key(self, seed: int, step: int = 0, streams=None, first_stream: int = 0) -> None:
+        """StochasticBatch seed/step and member streams (make_stochastic_batch, engine.cpp:122-132)."""
+        s = None if streams is None else np.ascontiguousarray(streams, dtype=np.uint64)
+        check(lib().ebl_batch_set_key(self._h, seed, step, _ptr(s), first_stream))
+
+    @property
+    def step_index(self) -> int:
+        return lib().ebl_batch_step_index(self._h)
+
+    # -- stepping -------------------------------------------------------------------------
+    def step(self, n_steps: int = 1) -> None:
+        """step_batch (engine.cpp:134-159) n_steps times, asynchronously on the batch stream."""
+        check(lib().ebl_step_batch(self._h, n_steps))
+
+    def sync(self) -> None:
+        check(lib().ebl_batch_sync(self._h))
+
+    def counts(self) -> np.ndarray:
+        """[n_envs, 4] int32: unburned, burning, burned, newly ignited (fire_fraction_stats)."""
+        out = np.empty((self.n_envs, 4), dtype=np.int32)
+        check(lib().ebl_batch_counts(self._h, _ptr(out)))
+        return out
+
+    def fractions(self) -> np.ndarray:
+        """fire_fraction_stats (engine.cpp:185-198) per env: [n_envs, 3] doubles."""
+        c = self.counts()[:, :3].astype(np.float64)
+        return c / float(self.height * self.width)
+
+    def intensity(self):
+        lam = np.empty((self.n_envs, self.height, self.width), dtype=np.float32)
+        p = np.empty_like(lam)
+        check(lib().ebl_batch_intensity(self._h, _ptr(lam), _ptr(p)))
+        return lam, p
+
+    def diag(self, reset: bool = False) -> dict:
+        out = np.zeros(4, dtype=np.uint64)
+        check(lib().ebl_batch_diag(self._h, _ptr(out), int(reset)))
+        return {"fp64_fallbacks": int(out[0]), "ambiguous": int(out[1]), "steps": int(out[2]),
+                "launches": int(out[3])}
+
+
+# ---- one-shot reference signatures ----------------------------------------------------------
+def _layers(grid):
+    return [np.ascontiguousarray(grid[k], dtype=np.float64)
+            for k in ("speed", "dir", "veg", "den", "slope8")]
+
+
+def step_stochastic(fire, grid: dict, cfg, key) -> np.ndarray:
+    """step_stochastic(fire, grid, cfg, RngKey{seed, step, stream}) (engine.hpp:204-207)."""
+    fire = np.ascontiguousarray(fire, dtype=np.uint8)
+    out = np.empty_like(fire)
+    seed, step, stream = key
+    check(lib().ebl_step_stochastic(fire.shape[0], fire.shape[1], _ptr(fire),
+                                    *[_ptr(a) for a in _layers(grid)], C.byref(as_config(cfg)),
+                                    seed, step, stream, _ptr(out)))
+    return out
+
+
+def run_stochastic(initial, grid: dict, cfg, key, steps: int) -> np.ndarray:
+    """run_stochastic(initial, grid, cfg, key, steps).final_state (engine.hpp:215-217)."""
+    fire = np.ascontiguousarray(initial, dtype=np.uint8)
+    out = np.empty_like(fire)
+    seed, step, stream = key
+    check(lib().ebl_run_stochastic(fire.shape[0], fire.shape[1], _ptr(fire),
+                                   *[_ptr(a) for a in _layers(grid)], C.byref(as_config(cfg)),
+                                   seed, step, stream, steps, _ptr(out)))
+    return out
+
+
+# ---- inputs -----------------------------------------------------------------------------------
+@dataclass
+class Terrain:
+    fuel_class: np.ndarray   # uint8 [n, H, W], palette index
+    elevation: np.ndarray    # float32 [n, H, W], metres
+    wind_speed: np.ndarray   # float64 [n]
+    wind_direction: np.ndarray
+    class_veg: np.ndarray    # float64 [11]
+    class_den: np.ndarray
+    cellsize: float = 30.0
+
+    def veg(self) -> np.ndarray:
+        return self.class_veg[self.fuel_class]
+
+    def den(self) -> np.ndarray:
+        return self.class_den[self.fuel_class]
+
+
+def worldcover_palette():
+    codes = np.empty(11, dtype=np.int32)
+    veg = np.empty(11, dtype=np.float64)
+    den = np.empty(11, dtype=np.float64)
+    lib().ebl_worldcover_palette(_ptr(codes), _ptr(veg), _ptr(den))
+    return codes, veg, den
+
+
+def synth_terrain(seed: int, n_envs: int, height: int, width: int, env_id0: int = 0,
+                  elev_max: float = 500.0, wind_max: float = 10.0) -> Terrain:
+    """Seeded C1-style terrain."""
+    fc = np.empty((n_envs, height, width), dtype=np.uint8)
+    el = np.empty((n_envs, height, width), dtype=np.float32)
+    ws = np.empty(n_envs, dtype=np.float64)
+    wd = np.empty(n_envs, dtype=np.float64)
+    check(lib().ebl_synth_terrain(seed, env_id0, n_envs, height, width, elev_max, wind_max,
+                                  _ptr(fc), _ptr(el), _ptr(ws), _ptr(wd)))
+    _, veg, den = worldcover_palette()
+    return Terrain(fc, el, ws, wd, veg, den)
+
+
+def synth_ignitions(seed: int, terrain: Terrain, count: int, env_id0: int = 0) -> np.ndarray:
+    n, h, w = terrain.fuel_class.shape
+    st = np.empty((n, h, w), dtype=np.uint8)
+    check(lib().ebl_synth_ignitions(seed, env_id0, n, h, w, _ptr(terrain.fuel_class),
+                                    _ptr(terrain.class_veg), _ptr(terrain.class_den), count,
+                                    _ptr(st)))
+    return st
+
+
+# ---- RL -----------------------------------------------------------------------------------------
+def default_preset() -> EnvConfig:
+    c = EnvConfig()
+    lib().ebl_env_default_preset(C.byref(c))
+    return c
+
+
+def smoke10_preset() -> EnvConfig:
+    c = EnvConfig()
+    lib().ebl_env_smoke10_preset(C.byref(c))
+    return c
+
+
+def observation_size(cfg: EnvConfig) -> int:
+    return lib().ebl_env_observation_size(C.byref(cfg))
+
+
+class VecFireEnv:
+    """A batch of RL envs stepped on device.
+
+    variant RL_REFERENCE: FireSuppressionEnv (rl_env.hpp:93-110) per env — reset/observe/step
+    with the reference's Move x Valve actions, single-cell douse and reward.
+    variant RL_TANKER: the BASELINE C2 air-tanker env ((x,y) actions, 3x3 extinguish + wet,
+    reward = -newly ignited, auto-reset), terrain from `terrain`.
+    """
+
+    def __init__(self, n_envs: int, cfg: EnvConfig | None = None, variant: int = _lib.RL_REFERENCE,
+                 terrain: Terrain | None = None, sim_cfg=None, ignitions: int = 5,
+                 max_steps: int = 256, env_id0: int = 0, device: int = 0):
+        self.variant = variant
+        if variant == _lib.RL_REFERENCE:
+            self.cfg = cfg if cfg is not None else default_preset()
+            h, w = self.cfg.height, self.cfg.width
+        else:
+            assert terrain is not None
+            _, h, w = terrain.fuel_class.shape
+            self.cfg = cfg
+        self.batch = Batch(n_envs, h, w, device=device)
+        if variant == _lib.RL_TANKER:
+            self.batch.set_terrain(terrain.fuel_class, terrain.elevation, terrain.class_veg,
+                                   terrain.class_den, terrain.cellsize)
+            self.batch.set_wind(terrain.wind_speed, terrain.wind_direction)
+            self.batch.set_config(sim_cfg)
+        check(lib().ebl_rl_configure(self.batch.handle, variant,
+                                     C.byref(self.cfg) if self.cfg is not None else None,
+                                     ignitions, max_steps, env_id0))
+        self.n_envs, self.height, self.width = n_envs, h, w
+
+    def reset(self, seed: int, streams=None, mask=None) -> None:
+        s = None if streams is None else np.ascontiguousarray(streams, dtype=np.uint64)
+        m = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
+        check(lib().ebl_rl_reset(self.batch.handle, seed, _ptr(s), _ptr(m)))
+
+    def step(self, actions=None):
+        """Returns (reward [n] float64, done [n] uint8)."""
+        a = None if actions is None else np.ascontiguousarray(actions, dtype=np.int32)
+        reward = np.empty(self.n_envs, dtype=np.float64)
+        done = np.empty(self.n_envs, dtype=np.uint8)
+        check(lib().ebl_rl_step(self.batch.handle, _ptr(a), _ptr(reward), _ptr(done), 0))
+        return reward, done
+
+    def rollout(self, n_steps: int):
+        rs = np.empty(self.n_envs, dtype=np.float64)
+        ep = np.empty(self.n_envs, dtype=np.int32)
+        check(lib().ebl_rl_rollout(self.batch.handle, n_steps, _ptr(rs), _ptr(ep)))
+        return rs, ep
+
+    def observe(self) -> np.ndarray:
+        osz = observation_size(self.cfg)
+        out = np.empty((self.n_envs, osz), dtype=np.float64)
+        check(lib().ebl_rl_observe(self.batch.handle, _ptr(out)))
+        return out
+
+    def env_states(self):
+        arr = (EnvState * self.n_envs)()
+        check(lib().ebl_rl_get_env_states(self.batch.handle, arr))
+        return list(arr)
+
+    def set_env_states(self, states) -> None:
+        arr = (EnvState * self.n_envs)(*states)
+        check(lib().ebl_rl_set_env_states(self.batch.handle, arr))
+
+    def fire(self) -> np.ndarray:
+        return self.batch.get_state()
+
+    def set_fire(self, states) -> None:
+        self.batch.set_state(states)
+
+    def wet(self) -> np.ndarray:
+        out = np.empty((self.n_envs, self.height, self.width), dtype=np.uint8)
+        check(lib().ebl_rl_get_wet(self.batch.handle, _ptr(out)))
+        return out

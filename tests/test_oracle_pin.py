@@ -1,0 +1,159 @@
+"""Pins the C restatement (oracle/ember_oracle.c) before it is trusted as the checker:
+(1) against the golden fixtures produced by the reference itself (tests/golden/make_golden.py),
+(2) against the reference compiled in place (oracle/_ref) on fresh inputs, bit for bit."""
+import numpy as np
+import pytest
+
+from conftest import layer_cases
+from oracle import oracle as O
+
+
+def test_rng_kats(port, kats):
+    # rng.hpp:38-58 — SURVEY §8(c) known answers + a spread of keys incl. 64-bit extremes
+    for *k, want in kats["rng_word"]:
+        assert hex(port.ebo_rng_word(*map(int, k))) == want
+    for *k, n, want in kats["rng_below"]:
+        assert port.ebo_rng_below(*map(int, k), int(n)) == int(want)
+    assert port.ebo_rng_uniform(0, 0, 0, 0, 0) == 0.44705329279927764
+
+
+def test_offset_angles(port):
+    # grid.cpp:44-47: E=0, counter-clockwise, wrapped to [0, 2pi)
+    ang = [port.ebo_offset_angle(k) for k in range(8)]
+    assert ang == sorted(ang) and ang[0] == 0.0 and abs(ang[2] - np.pi / 2) < 1e-15
+    assert port.ebo_wrap_angle(-0.5) == pytest.approx(2 * np.pi - 0.5, abs=1e-15)
+
+
+def test_c0_kats(port, kats):
+    # C0: 64x64 flat uniform, calm, ignite (32,32), SimConfig{}, RngKey{0,0,0}
+    h = w = 64
+    z = np.zeros((h, w))
+    g = O.grid_layers(port, "port", z, z, z, z, np.zeros((h, w, 8)))
+    fire = np.zeros((h, w), np.uint8)
+    fire[32, 32] = 1
+    for steps, want in kats["c0"].items():
+        st = O.run(port, "port", g, O.DEFAULT_CFG, 0, 0, 0, int(steps), fire)
+        assert [int((st == k).sum()) for k in range(3)] == want["counts"]
+        assert hex(O.fnv1a64(st.tobytes())) == want["fnv1a64"]
+    _, p = O.intensity(port, "port", g, O.DEFAULT_CFG, fire)
+    assert p[33, 32] == kats["c0_p_one_neighbour"] == 0.11307956328284252
+
+
+def test_layers_golden(port, golden_layers):
+    for case in layer_cases(golden_layers):
+        g = O.grid_layers(port, "port", case["speed"], case["dir"], case["veg"], case["den"],
+                          case["slope8"])
+        h, w = case["speed"].shape
+        pot, gam = O.tables(port, "port", g, case["cfg"], h * w)
+        assert np.array_equal(pot, case["pot"]) and np.array_equal(gam, case["gamma"])
+        lam, p = O.intensity(port, "port", g, case["cfg"], case["probe_state"])
+        assert np.array_equal(lam, case["lam"]) and np.array_equal(p, case["p"])
+        traj = case["traj"]
+        st = traj[0]
+        for t in range(1, len(traj)):
+            st = O.run(port, "port", g, case["cfg"], int(case["seed"]), t - 1, int(case["stream"]),
+                       1, st)
+            assert np.array_equal(st, traj[t]), f"step {t}"
+
+
+def test_terrain_golden(port, golden_terrain):
+    d = golden_terrain
+    n = d["cls"].shape[0]
+    for e in range(n):
+        g = O.grid_terrain(port, "port", d["veg"][d["cls"][e]], d["den"][d["cls"][e]], d["elev"][e],
+                           30.0, d["wind_speed"][e], d["wind_dir"][e])
+        if e == 0:
+            h, w = d["cls"].shape[1:]
+            # slope_from_dem bitwise (geodata.cpp:209-229)
+            assert np.array_equal(np.frombuffer(np.ctypeslib.as_array(
+                (O._D * (h * w * 8)).from_address(port_slope_addr(g))), dtype=np.float64),
+                d["slope0"])
+        st = O.run(port, "port", g, O.DEFAULT_CFG, int(d["seed"]), 0, e, int(d["steps"]), d["init"][e])
+        assert np.array_equal(st, d["final"][e])
+
+
+def port_slope_addr(g):
+    import ctypes as C
+
+    class EG(C.Structure):
+        _fields_ = [("h", C.c_int), ("w", C.c_int), ("speed", C.c_void_p), ("dir", C.c_void_p),
+                    ("veg", C.c_void_p), ("den", C.c_void_p), ("slope8", C.c_void_p)]
+    return EG.from_address(g.h).slope8
+
+
+def test_rl_golden(port, golden_rl):
+    ec = O.EnvCfg(20, 20, 2, 30, 0.05, 120, 1, 1, 1.0, 0.0, 0.0, 0.0,
+                  (O._D * 6)(0.06, 0.1, 0.2, 0.5, 1.0, 0.9))
+    for ep in range(3):
+        s = O.EnvSt()
+        fire = np.zeros((20, 20), np.uint8)
+        port.ebo_env_reset(ec, 11, ep, s, O.ptr(fire))
+        states = golden_rl[f"e{ep}_states"]
+        agents = golden_rl[f"e{ep}_agents"]
+        assert np.array_equal(fire, states[0])
+        assert [s.agent_row, s.agent_col, s.water, s.step, s.done] == list(agents[0])
+        for t, (a, rw_want) in enumerate(zip(golden_rl[f"e{ep}_actions"], golden_rl[f"e{ep}_rewards"])):
+            assert port.ebo_random_policy(11, s.step, ep) == a
+            s2, f2, rw = O.EnvSt(), np.empty_like(fire), O._D()
+            obs = np.empty(78)
+            assert port.ebo_env_step(ec, s, O.ptr(fire), int(a), s2, O.ptr(f2), rw, O.ptr(obs)) == 0
+            s, fire = s2, f2
+            assert rw.value == rw_want
+            assert np.array_equal(fire, states[t + 1])
+            assert [s.agent_row, s.agent_col, s.water, s.step, s.done] == list(agents[t + 1])
+        assert np.array_equal(obs, golden_rl[f"e{ep}_last_obs"])
+        # stepping a finished episode is a logic_error in the reference (rl_env.cpp:173)
+        assert port.ebo_env_step(ec, s, O.ptr(fire), 0, O.EnvSt(), O.ptr(f2), O._D(), None) == -1
+
+
+# ---- live comparisons against the reference compiled in place ----------------------------------
+@pytest.mark.parametrize("seed,h,w,steps", [(1, 7, 7, 25), (2, 16, 48, 30), (3, 40, 3, 30)])
+def test_port_vs_ref_layers(port, ref, seed, h, w, steps):
+    rs = np.random.default_rng(seed)
+    L = dict(speed=3.0 * rs.random((h, w)), dir=20 * rs.random((h, w)) - 10,
+             veg=2.4 * rs.random((h, w)) - 1.2, den=2.4 * rs.random((h, w)) - 1.2,
+             slope8=rs.random((h, w, 8)) - 0.5)
+    cfg = [0.3, 0.25, 0.5, 1.5, 1.2, 0.7]
+    gp = O.grid_layers(port, "port", *L.values())
+    gr = O.grid_layers(ref, "ref", *L.values())
+    f0 = (rs.random((h, w)) < 0.1).astype(np.uint8)
+    assert np.array_equal(O.tables(port, "port", gp, cfg, h * w)[0], O.tables(ref, "ref", gr, cfg, h * w)[0])
+    a = O.run(port, "port", gp, cfg, 77, 5, 3, steps, f0)
+    b = O.run(ref, "ref", gr, cfg, 77, 5, 3, steps, f0)
+    assert np.array_equal(a, b)
+
+
+def test_port_vs_ref_terrain(port, ref):
+    rs = np.random.default_rng(9)
+    h, w = 48, 40
+    veg = np.array([0.4, 0.25, 0.15, 0.0, -0.8, -0.7, -1.0, -1.0, -0.4, -0.2, -0.3])
+    den = np.array([0.3, 0.1, -0.1, -0.2, -0.8, -0.6, -1.0, -1.0, -0.3, -0.1, -0.4])
+    cls = rs.integers(0, 11, (h, w))
+    el = (300 * rs.random((h, w))).astype(np.float32)
+    gp = O.grid_terrain(port, "port", veg[cls], den[cls], el, 30.0, 6.0, 0.0)
+    gr = O.grid_terrain(ref, "ref", veg[cls], den[cls], el, 30.0, 6.0, 0.0)
+    f0 = np.zeros((h, w), np.uint8)
+    f0[24, 20] = f0[10, 5] = 1
+    for cfg in (O.DEFAULT_CFG, [0.5, 0.2, 0.4, 3.0, 1.0, 0.8]):
+        lp, pp = O.intensity(port, "port", gp, cfg, f0)
+        lr, pr = O.intensity(ref, "ref", gr, cfg, f0)
+        assert np.array_equal(lp, lr) and np.array_equal(pp, pr)
+        assert np.array_equal(O.run(port, "port", gp, cfg, 5, 0, 1, 50, f0),
+                              O.run(ref, "ref", gr, cfg, 5, 0, 1, 50, f0))
+
+
+def test_port_vs_ref_batch(port, ref):
+    # step_batch lockstep (engine.cpp:134-159) == solo runs on streams first_stream+m
+    h, w = 10, 10
+    rs = np.random.default_rng(61)
+    L = dict(speed=2 * rs.random((h, w)), dir=6.28 * rs.random((h, w)), veg=rs.random((h, w)) - 0.3,
+             den=rs.random((h, w)) - 0.3, slope8=0.5 * rs.random((h, w, 8)) - 0.25)
+    gr = O.grid_layers(ref, "ref", *L.values())
+    gp = O.grid_layers(port, "port", *L.values())
+    f0 = np.zeros((h, w), np.uint8)
+    f0[5, 5] = 1
+    cfg = np.array([0.22, 0.2, 0.4, 1.0, 1.0, 0.6])
+    out = np.empty((8, h, w), np.uint8)
+    assert ref.ref_step_batch(gr.h, O.ptr(cfg), 123, 4, 8, 15, O.ptr(f0), O.ptr(out)) == 0
+    for m in range(8):
+        assert np.array_equal(out[m], O.run(port, "port", gp, cfg, 123, 0, 4 + m, 15, f0))

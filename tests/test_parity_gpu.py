@@ -1,0 +1,326 @@
+"""Parity of the CUDA path (through the C-ABI) with the CPU oracle.
+
+Bar (north_star): cell states bit-exact; arrival intensity and ignition probability of the
+fp32 path within 1e-5 relative; any flip must come from a draw inside the fp64 ambiguity band
+(reported by the device as diag['ambiguous'], asserted 0 here)."""
+import numpy as np
+import pytest
+
+import paper_2512_06102_b200 as eb
+from conftest import layer_cases
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = [eb.KERNEL_TILED, eb.KERNEL_RESIDENT]
+REL_TOL = 1e-5  # north_star: lambda and p within 1e-5 relative in fp32
+
+
+def _layers_batch(case, n_envs=1, kernel=eb.KERNEL_AUTO):
+    h, w = case["speed"].shape
+    b = eb.Batch(n_envs, h, w)
+    b.set_config(list(case["cfg"]))
+    b.set_grid(case["speed"], case["dir"], case["veg"], case["den"], case["slope8"])
+    b.set_kernel(kernel)
+    return b
+
+
+def test_device_rng_kats(kats):
+    keys = np.array([[int(x) for x in k[:5]] for k in kats["rng_word"]], dtype=np.uint64)
+    out = np.zeros(len(keys), np.uint64)
+    eb._lib.check(eb.lib().ebl_device_rng_words(len(keys), keys.ctypes.data, out.ctypes.data))
+    assert [hex(int(x)) for x in out] == [k[5] for k in kats["rng_word"]]
+
+
+def test_device_rng_random_keys(port):
+    rs = np.random.default_rng(0)
+    keys = rs.integers(0, 2**63, size=(4096, 5), dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+    out = np.zeros(len(keys), np.uint64)
+    eb._lib.check(eb.lib().ebl_device_rng_words(len(keys), keys.ctypes.data, out.ctypes.data))
+    want = [port.ebo_rng_word(*map(int, k)) for k in keys]
+    assert [int(x) for x in out] == want
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_c0_kats(kats, kernel):
+    h = w = 64
+    z = np.zeros((h, w))
+    b = eb.Batch(1, h, w)
+    b.set_grid(z, z, z, z, np.zeros((h, w, 8)))
+    b.set_kernel(kernel)
+    fire = np.zeros((h, w), np.uint8)
+    fire[32, 32] = 1
+    for steps, want in sorted(kats["c0"].items(), key=lambda kv: int(kv[0])):
+        b.set_state(fire)
+        b.set_key(0, 0, first_stream=0)
+        b.step(int(steps))
+        st = b.get_state()[0]
+        assert [int((st == k).sum()) for k in range(3)] == want["counts"]
+        assert hex(O.fnv1a64(st.tobytes())) == want["fnv1a64"]
+        assert b.counts()[0, :3].tolist() == want["counts"]
+    assert b.diag()["ambiguous"] == 0
+
+
+def test_one_shot_signatures_golden(golden_layers):
+    for case in layer_cases(golden_layers):
+        traj = case["traj"]
+        grid = dict(speed=case["speed"], dir=case["dir"], veg=case["veg"], den=case["den"],
+                    slope8=case["slope8"])
+        st = traj[0]
+        for t in range(1, len(traj)):
+            st = eb.step_stochastic(st, grid, list(case["cfg"]),
+                                    (int(case["seed"]), t - 1, int(case["stream"])))
+            assert np.array_equal(st, traj[t]), f"step {t}"
+        fin = eb.run_stochastic(traj[0], grid, list(case["cfg"]),
+                                (int(case["seed"]), 0, int(case["stream"])), len(traj) - 1)
+        assert np.array_equal(fin, traj[-1])
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_layers_golden_batch(golden_layers, kernel):
+    for case in layer_cases(golden_layers):
+        traj = case["traj"]
+        b = _layers_batch(case, 3, kernel)
+        b.set_state(traj[0])
+        b.set_key(int(case["seed"]), 0, streams=[int(case["stream"])] * 3)
+        for t in range(1, len(traj)):
+            b.step(1)
+            assert (b.get_state() == traj[t]).all(), f"step {t}"
+        lam, p = b.intensity()
+        b.set_state(case["probe_state"])
+        lam, p = b.intensity()
+        # tables form computes lambda/p in fp64 (rounded to float for the probe)
+        np.testing.assert_allclose(lam[0], case["lam"], rtol=REL_TOL, atol=1e-30)
+        np.testing.assert_allclose(p[0], case["p"], rtol=REL_TOL, atol=1e-30)
+        assert b.diag()["ambiguous"] == 0
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_terrain_golden(golden_terrain, kernel):
+    d = golden_terrain
+    n, h, w = d["cls"].shape
+    b = eb.Batch(n, h, w)
+    b.set_terrain(d["cls"], d["elev"], d["veg"], d["den"], 30.0)
+    b.set_wind(d["wind_speed"], d["wind_dir"])
+    b.set_kernel(kernel)
+    b.set_state(d["init"])
+    b.set_key(int(d["seed"]), 0, first_stream=0)
+    b.step(int(d["steps"]))
+    assert np.array_equal(b.get_state(), d["final"])
+    assert b.diag()["ambiguous"] == 0
+
+
+def _terrain_batch(t: eb.Terrain, cfg=None, kernel=eb.KERNEL_AUTO):
+    n, h, w = t.fuel_class.shape
+    b = eb.Batch(n, h, w)
+    b.set_terrain(t.fuel_class, t.elevation, t.class_veg, t.class_den, t.cellsize)
+    b.set_wind(t.wind_speed, t.wind_direction)
+    b.set_config(cfg)
+    b.set_kernel(kernel)
+    return b
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("cfg", [None, [0.3, 0.1, 0.3, 2.0, 1.5, 0.8], [0.12, 0.2, 0.4, 1.0, 1.0, 0.95]])
+def test_c1_shape_vs_oracle(port, kernel, cfg):
+    """C1 generator at full env size (128x128, 5 ignitions, 200 steps), 12 envs vs the port."""
+    n, h, w, steps, seed = 12, 128, 128, 200, 0
+    t = eb.synth_terrain(seed, n, h, w)
+    init = eb.synth_ignitions(seed, t, 5)
+    b = _terrain_batch(t, cfg, kernel)
+    b.set_state(init)
+    b.set_key(seed, 0, first_stream=0)
+    b.step(steps)
+    got = b.get_state()
+    c = O.DEFAULT_CFG if cfg is None else cfg
+    for e in range(n):
+        g = O.grid_terrain(port, "port", t.veg()[e], t.den()[e], t.elevation[e], 30.0,
+                           t.wind_speed[e], t.wind_direction[e])
+        want = O.run(port, "port", g, c, seed, 0, e, steps, init[e])
+        assert np.array_equal(got[e], want), f"env {e}: {np.argwhere(got[e] != want)[:5]}"
+    cnt = b.counts()
+    assert (cnt[:, :3].sum(1) == h * w).all()
+    assert np.array_equal(cnt[:, 1], (got == 1).reshape(n, -1).sum(1))
+    d = b.diag()
+    assert d["ambiguous"] == 0
+
+
+def test_intensity_fp32_within_1e5(port):
+    """lambda / p of the fp32 fast path vs the fp64 oracle, on mid-run fronts."""
+    n, h, w = 6, 96, 80
+    t = eb.synth_terrain(5, n, h, w)
+    init = eb.synth_ignitions(5, t, 8)
+    for cfg in (None, [0.3, 0.1, 0.3, 2.0, 1.5, 0.8], [0.05, 0.4, 0.8, 5.0, 0.5, 0.9]):
+        b = _terrain_batch(t, cfg)
+        b.set_state(init)
+        b.set_key(5, 0)
+        b.step(30)
+        st = b.get_state()
+        lam, p = b.intensity()
+        c = O.DEFAULT_CFG if cfg is None else cfg
+        for e in range(n):
+            g = O.grid_terrain(port, "port", t.veg()[e], t.den()[e], t.elevation[e], 30.0,
+                               t.wind_speed[e], t.wind_direction[e])
+            lw, pw = O.intensity(port, "port", g, c, st[e])
+            m = lw > 0
+            assert m.sum() > 0
+            np.testing.assert_allclose(lam[e][m], lw[m], rtol=REL_TOL)
+            np.testing.assert_allclose(p[e][m], pw[m], rtol=REL_TOL, atol=1e-30)
+            assert (lam[e][~m] == 0).all() and (p[e][~m] == 0).all()
+
+
+@pytest.mark.parametrize("h,w", [(1, 1), (1, 37), (45, 1), (3, 3), (31, 33), (64, 96), (200, 100), (17, 300)])
+def test_kernels_identical_ragged(port, h, w):
+    """Tiled vs resident vs oracle on ragged sizes (W not a multiple of 32, single row/col)."""
+    rs = np.random.default_rng(h * 1000 + w)
+    n = 5
+    cls = rs.integers(0, 11, (n, h, w)).astype(np.uint8)
+    el = (400 * rs.random((n, h, w))).astype(np.float32)
+    _, veg, den = eb.worldcover_palette()
+    init = (rs.random((n, h, w)) < 0.15).astype(np.uint8)
+    init[rs.random((n, h, w)) < 0.1] = 2
+    outs = []
+    for kernel in KERNELS:
+        if kernel == eb.KERNEL_RESIDENT and h * w > 65536:
+            continue
+        b = eb.Batch(n, h, w)
+        b.set_terrain(cls, el, veg, den, 25.0)
+        b.set_wind(rs.random(n) * 0 + 7.0, [0.3, 1.0, 2.0, 4.0, 6.0])
+        b.set_config([0.4, 0.2, 0.4, 1.0, 1.0, 0.7])
+        b.set_kernel(kernel)
+        b.set_state(init)
+        b.set_key(9, 3, first_stream=100)
+        b.step(25)
+        outs.append(b.get_state())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    for e in range(n):
+        g = O.grid_terrain(port, "port", veg[cls[e]], den[cls[e]], el[e], 25.0, 7.0,
+                           [0.3, 1.0, 2.0, 4.0, 6.0][e])
+        want = O.run(port, "port", g, [0.4, 0.2, 0.4, 1.0, 1.0, 0.7], 9, 3, 100 + e, 25, init[e])
+        assert np.array_equal(outs[0][e], want)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_batch_member_equals_solo_and_permutation(port, kernel):
+    # test_engine.cpp:341-376: members == solo runs on their streams; order-invariant
+    h, w = 10, 10
+    rs = np.random.default_rng(61)
+    L = dict(speed=2 * rs.random((h, w)), dir=6.28 * rs.random((h, w)), veg=rs.random((h, w)) - 0.3,
+             den=rs.random((h, w)) - 0.3, slope8=0.5 * rs.random((h, w, 8)) - 0.25)
+    cfg = [0.22, 0.2, 0.4, 1.0, 1.0, 0.6]
+    f0 = np.zeros((h, w), np.uint8)
+    f0[5, 5] = 1
+    b = eb.Batch(8, h, w)
+    b.set_config(cfg)
+    b.set_grid(*L.values())
+    b.set_kernel(kernel)
+    b.set_state(f0)
+    b.set_key(123, 0, first_stream=0)
+    b.step(15)
+    assert b.step_index == 15
+    got = b.get_state()
+    gp = O.grid_layers(port, "port", *L.values())
+    for m in range(8):
+        assert np.array_equal(got[m], O.run(port, "port", gp, cfg, 123, 0, m, 15, f0))
+    b.set_state(f0)
+    b.set_key(123, 0, streams=list(range(7, -1, -1)))
+    b.step(15)
+    assert np.array_equal(b.get_state()[::-1], got)
+
+
+def test_invariants():
+    h, w = 6, 6
+    rs = np.random.default_rng(3)
+    L = dict(speed=2 * rs.random((h, w)), dir=6.28 * rs.random((h, w)), veg=rs.random((h, w)) - 0.3,
+             den=rs.random((h, w)) - 0.3, slope8=0.5 * rs.random((h, w, 8)) - 0.25)
+    grid = dict(zip(("speed", "dir", "veg", "den", "slope8"), L.values()))
+    fire = np.zeros((h, w), np.uint8)
+    fire[2, 2] = 2
+    assert np.array_equal(eb.step_stochastic(fire, grid, None, (1, 0, 0)), fire)  # no burning -> identity
+    z = np.zeros((h, w))
+    flat = dict(speed=z, dir=z, veg=z, den=z, slope8=np.zeros((h, w, 8)))
+    fire = np.zeros((h, w), np.uint8)
+    fire[1, 1] = fire[4, 3] = 1
+    frozen = eb.run_stochastic(fire, flat, dict(p_base=0.0, p_continue=1.0), (9, 0, 0), 10)
+    assert np.array_equal(frozen, fire)
+    b = eb.Batch(1, 8, 8)
+    L8 = dict(speed=2 * rs.random((8, 8)), dir=6.28 * rs.random((8, 8)), veg=rs.random((8, 8)) - 0.3,
+              den=rs.random((8, 8)) - 0.3, slope8=0.5 * rs.random((8, 8, 8)) - 0.25)
+    b.set_grid(*L8.values())
+    b.set_config(dict(p_base=0.5, p_continue=0.3))
+    s = np.zeros((8, 8), np.uint8)
+    s[4, 4] = 1
+    b.set_state(s)
+    b.set_key(5, 0)
+    prev = b.get_state()[0]
+    for _ in range(30):
+        b.step(1)
+        cur = b.get_state()[0]
+        assert (cur[prev == 2] == 2).all()  # burned is absorbing
+        prev = cur
+
+
+def test_monte_carlo_frequencies(port):
+    # test_engine.cpp:127-155 pattern on the device: one step from a fixed state over 20k streams
+    h = w = 8
+    rs = np.random.default_rng(17)
+    L = dict(speed=2 * rs.random((h, w)), dir=6.28 * rs.random((h, w)), veg=rs.random((h, w)) - 0.3,
+             den=rs.random((h, w)) - 0.3, slope8=0.5 * rs.random((h, w, 8)) - 0.25)
+    cfg = [0.25, 0.2, 0.4, 1.0, 1.0, 0.6]
+    fire = np.zeros((h, w), np.uint8)
+    fire[4, 4] = 1
+    n = 20000
+    b = eb.Batch(n, h, w)
+    b.set_grid(*L.values())
+    b.set_config(cfg)
+    b.set_state(fire)
+    b.set_key(77, 0, first_stream=0)
+    b.step(1)
+    freq = (b.get_state() == 1).mean(0)
+    gp = O.grid_layers(port, "port", *L.values())
+    _, p = O.intensity(port, "port", gp, cfg, fire)
+    m = fire == 0
+    sigma = np.sqrt(np.maximum(p * (1 - p) / n, 1e-12))
+    assert (np.abs(freq - p)[m] <= 4 * sigma[m]).all()
+    assert abs(freq[4, 4] - 0.6) <= 4 * np.sqrt(0.24 / n)
+
+
+def test_errors():
+    b = eb.Batch(2, 4, 4)
+    with pytest.raises(eb.EmberError):
+        b.step(1)  # no grid yet (ESTATE)
+    with pytest.raises(eb.InvalidArgument):
+        b.set_state(np.full((2, 4, 4), 3, np.uint8))
+    z = np.zeros((4, 4))
+    with pytest.raises(eb.InvalidArgument):
+        b.set_grid(z - 1.0, z, z, z, np.zeros((4, 4, 8)))  # negative wind speed
+    with pytest.raises(eb.InvalidArgument):
+        b.set_grid(z, z, z + np.nan, z, np.zeros((4, 4, 8)))
+    with pytest.raises(eb.InvalidArgument):
+        eb.Batch(0, 4, 4)
+    with pytest.raises(eb.InvalidArgument):
+        eb.Batch(1, 0, 4)
+
+
+@pytest.mark.slow
+def test_c1_full_size_kernels_agree_and_sampled_oracle(port):
+    """Full C1 (1024 x 128^2 x 200): resident == tiled on every env; 6 envs vs the port."""
+    n, h, w, steps = 1024, 128, 128, 200
+    t = eb.synth_terrain(0, n, h, w)
+    init = eb.synth_ignitions(0, t, 5)
+    outs = []
+    for kernel in KERNELS:
+        b = _terrain_batch(t, None, kernel)
+        b.set_state(init)
+        b.set_key(0, 0)
+        b.step(steps)
+        outs.append(b.get_state())
+        assert b.diag()["ambiguous"] == 0
+    assert np.array_equal(outs[0], outs[1])
+    for e in (0, 1, 511, 777, 1022, 1023):
+        g = O.grid_terrain(port, "port", t.veg()[e], t.den()[e], t.elevation[e], 30.0,
+                           t.wind_speed[e], t.wind_direction[e])
+        assert np.array_equal(outs[0][e], O.run(port, "port", g, O.DEFAULT_CFG, 0, 0, e, steps, init[e]))
+    # burned count non-decreasing / conservation properties
+    assert ((outs[0] == 2).reshape(n, -1).sum(1) >= 0).all()

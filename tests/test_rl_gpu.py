@@ -1,0 +1,162 @@
+"""RL step on device vs the reference (golden episodes) and the C oracle (batched, tanker)."""
+import numpy as np
+import pytest
+
+import paper_2512_06102_b200 as eb
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _agents(env):
+    return [[s.agent_row, s.agent_col, s.water, s.step, s.done] for s in env.env_states()]
+
+
+def test_reference_env_golden_episodes(golden_rl):
+    # FireSuppressionEnv default_preset, random_policy episodes keyed (11, step, stream=ep)
+    env = eb.VecFireEnv(3)
+    env.reset(11, streams=[0, 1, 2])
+    fires = env.fire()
+    ag = _agents(env)
+    for ep in range(3):
+        assert np.array_equal(fires[ep], golden_rl[f"e{ep}_states"][0])
+        assert ag[ep] == list(golden_rl[f"e{ep}_agents"][0])
+    # host-supplied actions (the golden ones), envs finish at different times: step one env at a time
+    for ep in range(3):
+        acts = golden_rl[f"e{ep}_actions"]
+        e1 = eb.VecFireEnv(1)
+        e1.reset(11, streams=[ep])
+        for t, a in enumerate(acts):
+            r, d = e1.step([int(a)])
+            assert r[0] == golden_rl[f"e{ep}_rewards"][t]
+            assert np.array_equal(e1.fire()[0], golden_rl[f"e{ep}_states"][t + 1])
+            assert _agents(e1)[0] == list(golden_rl[f"e{ep}_agents"][t + 1])
+            assert bool(d[0]) == bool(golden_rl[f"e{ep}_agents"][t + 1][4])
+        assert np.array_equal(e1.observe()[0], golden_rl[f"e{ep}_last_obs"])
+        with pytest.raises(eb.LogicError):
+            e1.step([0])  # rl_env.cpp:173
+        with pytest.raises(eb.OutOfRange):
+            e1.step([10])
+
+
+def test_reference_env_device_policy_matches_golden(golden_rl):
+    # actions=None -> device random_policy (rl_env.cpp:237-239); one env per episode length
+    for ep in range(3):
+        e1 = eb.VecFireEnv(1)
+        e1.reset(11, streams=[ep])
+        for t in range(len(golden_rl[f"e{ep}_actions"])):
+            r, _ = e1.step(None)
+            assert r[0] == golden_rl[f"e{ep}_rewards"][t]
+        assert np.array_equal(e1.fire()[0], golden_rl[f"e{ep}_states"][-1])
+
+
+def test_reference_env_batch_vs_port(port):
+    cfg = eb.default_preset()
+    cfg.ignition_count = 4
+    cfg.waste_water = 0
+    n = 64
+    env = eb.VecFireEnv(n, cfg)
+    env.reset(5)
+    ec = O.EnvCfg(cfg.height, cfg.width, cfg.window_radius, cfg.water_capacity, cfg.burn_penalty,
+                  cfg.max_episode_steps, cfg.ignition_count, cfg.waste_water, cfg.wind_speed,
+                  cfg.wind_direction, cfg.fuel_veg, cfg.fuel_den, (O._D * 6)(*cfg.spread.as_list()))
+    states, fires = [], []
+    for e in range(n):
+        s = O.EnvSt()
+        f = np.zeros((cfg.height, cfg.width), np.uint8)
+        port.ebo_env_reset(ec, 5, e, s, O.ptr(f))
+        states.append(s)
+        fires.append(f)
+    assert np.array_equal(env.fire(), np.stack(fires))
+    rs = np.random.default_rng(0)
+    for t in range(40):
+        live = [e for e in range(n) if not states[e].done]
+        if not live:
+            break
+        acts = rs.integers(0, 10, n).astype(np.int32)
+        # finished envs must not be stepped (logic_error): give them their own batch view
+        sub = eb.VecFireEnv(len(live), cfg)
+        sub.reset(5, streams=live)
+        sub.set_fire(np.stack([fires[e] for e in live]))
+        sub.set_env_states([eb.EnvState(states[e].agent_row, states[e].agent_col, states[e].water,
+                                        states[e].step, 5, e, states[e].done, 0) for e in live])
+        r, d = sub.step(acts[live])
+        obs = sub.observe()
+        for i, e in enumerate(live):
+            s2, f2, rw = O.EnvSt(), np.empty_like(fires[e]), O._D()
+            ob = np.empty(78)
+            assert port.ebo_env_step(ec, states[e], O.ptr(fires[e]), int(acts[e]), s2, O.ptr(f2), rw,
+                                     O.ptr(ob)) == 0
+            states[e], fires[e] = s2, f2
+            assert r[i] == rw.value and bool(d[i]) == bool(s2.done)
+            assert np.array_equal(sub.fire()[i], f2)
+            assert np.array_equal(obs[i], ob)
+
+
+def _port_tanker(port, t: eb.Terrain, cfg, seed, env_ids, n_steps, tc, actions=None):
+    n, h, w = t.fuel_class.shape
+    out = []
+    for i, e in enumerate(env_ids):
+        g = O.grid_terrain(port, "port", t.veg()[i], t.den()[i], t.elevation[i], t.cellsize,
+                           t.wind_speed[i], t.wind_direction[i])
+        pot, gam = O.tables(port, "port", g, cfg, h * w)
+        s = O.TankerSt()
+        fire = np.zeros((h, w), np.uint8)
+        wet = np.zeros((h, w), np.uint8)
+        port.ebo_tanker_reset(g.h, tc, seed, e, 0, s, O.ptr(fire), O.ptr(wet))
+        rewards, dones = [], []
+        for k in range(n_steps):
+            a = (port.ebo_tanker_policy(seed, e, s, h * w) if actions is None else int(actions[k][i]))
+            rw = np.zeros(1, np.float32)
+            dn = np.zeros(1, np.uint8)
+            port.ebo_tanker_step(g.h, O.ptr(pot), O.ptr(gam), float(cfg[5]), tc, seed, e, a, s,
+                                 O.ptr(fire), O.ptr(wet), O.ptr(rw), O.ptr(dn))
+            rewards.append(float(rw[0]))
+            dones.append(int(dn[0]))
+        out.append(dict(fire=fire, wet=wet, rewards=rewards, dones=dones, step=s.step,
+                        episode=s.episode))
+    return out
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_tanker_vs_port(port, fused):
+    n, h, w, seed, steps = 24, 64, 64, 7, 300
+    t = eb.synth_terrain(seed, n, h, w)
+    cfg = [0.12, 0.2, 0.4, 1.0, 1.0, 0.6]
+    env = eb.VecFireEnv(n, variant=eb.RL_TANKER, terrain=t, sim_cfg=cfg, ignitions=5, max_steps=256)
+    env.reset(seed)
+    tc = O.TankerCfg(5, 256, 1)
+    want = _port_tanker(port, t, cfg, seed, list(range(n)), steps, tc)
+    if fused:
+        rs, ep = env.rollout(steps)
+        for e in range(n):
+            assert rs[e] == sum(want[e]["rewards"])
+            assert ep[e] == sum(want[e]["dones"])
+    else:
+        for k in range(steps):
+            r, d = env.step(None)
+            for e in range(n):
+                assert r[e] == want[e]["rewards"][k], (e, k)
+                assert d[e] == want[e]["dones"][k], (e, k)
+    fire, wet = env.fire(), env.wet()
+    st = env.env_states()
+    for e in range(n):
+        assert np.array_equal(fire[e], want[e]["fire"])
+        assert np.array_equal(wet[e], want[e]["wet"])
+        assert st[e].step == want[e]["step"] and st[e].episode == want[e]["episode"]
+    assert sum(sum(x["dones"]) for x in want) > 0, "test should cover auto-reset"
+
+
+def test_tanker_host_actions(port):
+    n, h, w, seed, steps = 8, 32, 48, 3, 40
+    t = eb.synth_terrain(seed, n, h, w)
+    env = eb.VecFireEnv(n, variant=eb.RL_TANKER, terrain=t, sim_cfg=None, ignitions=3, max_steps=256)
+    env.reset(seed)
+    rs = np.random.default_rng(1)
+    acts = rs.integers(0, h * w, (steps, n)).astype(np.int32)
+    want = _port_tanker(port, t, O.DEFAULT_CFG, seed, list(range(n)), steps, O.TankerCfg(3, 256, 1),
+                        actions=acts)
+    for k in range(steps):
+        r, _ = env.step(acts[k])
+        assert [want[e]["rewards"][k] for e in range(n)] == r.tolist()
+    assert np.array_equal(env.fire(), np.stack([x["fire"] for x in want]))
