@@ -446,3 +446,147 @@ void ebo_det_step_tables(int h, int w, const double* pot, const double* gamma, d
       bd_o[i] = bd[i] + burned_now;
     }
 }
+
+/* ---------------------------------------------------------------- dual.hpp:21-200 (N = 6)
+ * Forward-mode dual numbers with the reference's exact per-operation formulas, used to
+ * restate run_deterministic<Dual<6>> + loss (engine.hpp:147-245, calibrate.hpp:86-146):
+ * the C4 gradient oracle. */
+typedef struct { double v, g[6]; } dual6;
+
+static dual6 d_const(double x) { dual6 r; r.v = x; for (int i = 0; i < 6; ++i) r.g[i] = 0.0; return r; }
+static dual6 d_add(dual6 a, dual6 b) { a.v += b.v; for (int i = 0; i < 6; ++i) a.g[i] += b.g[i]; return a; }
+static dual6 d_sub(dual6 a, dual6 b) { a.v -= b.v; for (int i = 0; i < 6; ++i) a.g[i] -= b.g[i]; return a; }
+static dual6 d_mul(dual6 a, dual6 b) {  /* operator*= (dual.hpp:57-61): grads first, then value */
+  for (int i = 0; i < 6; ++i) a.g[i] = a.g[i] * b.v + a.v * b.g[i];
+  a.v *= b.v;
+  return a;
+}
+static dual6 d_muls(dual6 a, double b) { a.v *= b; for (int i = 0; i < 6; ++i) a.g[i] *= b; return a; }
+static dual6 d_divs(dual6 a, double b) { a.v /= b; for (int i = 0; i < 6; ++i) a.g[i] /= b; return a; }
+static dual6 d_neg(dual6 a) { a.v = -a.v; for (int i = 0; i < 6; ++i) a.g[i] = -a.g[i]; return a; }
+static dual6 d_rsub(double a, dual6 b) {  /* double - Dual (dual.hpp:101-106) */
+  dual6 r; r.v = a - b.v; for (int i = 0; i < 6; ++i) r.g[i] = -b.g[i]; return r;
+}
+static dual6 d_subs(dual6 a, double b) { a.v -= b; return a; }
+static dual6 d_exp(dual6 a) {
+  dual6 r; r.v = exp(a.v); for (int i = 0; i < 6; ++i) r.g[i] = r.v * a.g[i]; return r;
+}
+static dual6 d_log(dual6 a) {
+  dual6 r; r.v = log(a.v); for (int i = 0; i < 6; ++i) r.g[i] = a.g[i] / a.v; return r;
+}
+
+/* Loss + d loss / d theta after `steps` deterministic steps from a discrete layer;
+ * theta = the six SimConfig fields lifted as parameters 0..5 (ParamIndex order,
+ * calibrate.hpp:21-28).  loss = bce_w * BCE + mse_w * MSE(avgpool) (calibrate.hpp:120-146). */
+void ebo_det_loss_grad(const ebo_grid* g, const double* cfg, int steps, const uint8_t* fire0,
+                       const double* mask, double bce_w, double mse_w, int pool, double* loss_out,
+                       double* grad6) {
+  const int h = g->h, w = g->w;
+  const size_t n = (size_t)h * w;
+  dual6 P[6];
+  for (int i = 0; i < 6; ++i) { P[i] = d_const(cfg[i]); P[i].g[i] = 1.0; }
+  /* SpreadTables<Dual<6>> (engine.hpp:79-110) */
+  dual6* pot = (dual6*)malloc(n * 8 * sizeof(dual6));
+  dual6* gam = (dual6*)malloc(n * sizeof(dual6));
+  for (size_t i = 0; i < n; ++i) {
+    const dual6 source = d_muls(d_muls(P[0], 1.0 + g->veg[i]), 1.0 + g->den[i]);
+    gam[i] = d_muls(d_muls(P[4], 1.0 + g->veg[i]), 1.0 + g->den[i]);
+    for (int k = 0; k < 8; ++k) {
+      const dual6 sf = d_exp(d_muls(P[3], g->slope8[i * 8 + k]));
+      const double align = cos(ebo_offset_angle(k) - g->dir[i]) - 1.0;
+      const dual6 kw = d_mul(d_exp(d_muls(P[1], g->speed[i])),
+                             d_exp(d_muls(d_muls(P[2], g->speed[i]), align)));
+      pot[i * 8 + k] = d_mul(d_mul(source, kw), sf);
+    }
+  }
+  dual6 *un = (dual6*)malloc(n * sizeof(dual6)), *bu = (dual6*)malloc(n * sizeof(dual6)),
+        *bd = (dual6*)malloc(n * sizeof(dual6));
+  dual6 *un2 = (dual6*)malloc(n * sizeof(dual6)), *bu2 = (dual6*)malloc(n * sizeof(dual6)),
+        *bd2 = (dual6*)malloc(n * sizeof(dual6));
+  for (size_t i = 0; i < n; ++i) {  /* lift_state(state_from_fire) (engine.cpp:42-52) */
+    un[i] = d_const(fire0[i] == 0 ? 1.0 : 0.0);
+    bu[i] = d_const(fire0[i] == 1 ? 1.0 : 0.0);
+    bd[i] = d_const(fire0[i] == 2 ? 1.0 : 0.0);
+  }
+  for (int t = 0; t < steps; ++t) {
+    for (int r = 0; r < h; ++r)
+      for (int c = 0; c < w; ++c) {
+        const size_t i = (size_t)r * w + c;
+        dual6 lam = d_const(0.0);
+        for (int k = 0; k < 8; ++k) {
+          const int ur = r - kDy[k], uc = c - kDx[k];
+          if (ur < 0 || ur >= h || uc < 0 || uc >= w) continue;
+          const size_t u = (size_t)ur * w + uc;
+          if (bu[u].v == 0.0) continue;
+          lam = d_add(lam, d_mul(bu[u], pot[u * 8 + k]));
+        }
+        const dual6 p_ig = d_rsub(1.0, d_exp(d_neg(d_mul(gam[i], lam))));
+        const dual6 newly = d_mul(un[i], p_ig);
+        const dual6 continuing = d_mul(bu[i], P[5]);
+        const dual6 burned_now = d_mul(bu[i], d_rsub(1.0, P[5]));
+        bu2[i] = d_add(newly, continuing);
+        un2[i] = d_sub(un[i], newly);
+        bd2[i] = d_add(bd[i], burned_now);
+      }
+    dual6* tmp;
+    tmp = un; un = un2; un2 = tmp;
+    tmp = bu; bu = bu2; bu2 = tmp;
+    tmp = bd; bd = bd2; bd2 = tmp;
+  }
+  /* pred = p_burn + p_bd (calibrate.hpp:86-91) */
+  dual6* pred = un2;
+  for (size_t i = 0; i < n; ++i) pred[i] = d_add(bu[i], bd[i]);
+  const double eps = 1e-6;  /* LossConfig::bce_epsilon */
+  dual6 bce = d_const(0.0);
+  for (size_t i = 0; i < n; ++i) {
+    dual6 p = pred[i];
+    p = p.v >= eps ? p : d_const(eps);                /* max(pred, eps): ties keep pred */
+    p = p.v <= 1.0 - eps ? p : d_const(1.0 - eps);    /* min(., 1-eps) */
+    const double m = mask[i];
+    bce = d_add(bce, d_neg(d_add(d_muls(d_log(p), m), d_muls(d_log(d_rsub(1.0, p)), 1.0 - m))));
+  }
+  bce = d_divs(bce, (double)n);
+  /* avgpool (calibrate.hpp:95-115) of pred and mask, then MSE */
+  const int oh = (h + pool - 1) / pool, ow = (w + pool - 1) / pool;
+  dual6 mse = d_const(0.0);
+  for (int pr = 0; pr < oh; ++pr)
+    for (int pc = 0; pc < ow; ++pc) {
+      dual6 s = d_const(0.0);
+      double sm = 0.0;
+      int count = 0;
+      for (int r = pr * pool; r < (pr + 1) * pool && r < h; ++r)
+        for (int c = pc * pool; c < (pc + 1) * pool && c < w; ++c) {
+          s = d_add(s, pred[(size_t)r * w + c]);
+          sm += mask[(size_t)r * w + c];
+          ++count;
+        }
+      const dual6 pp = d_divs(s, (double)count);
+      const double pm = sm / (double)count;
+      const dual6 d = d_subs(pp, pm);
+      mse = d_add(mse, d_mul(d, d));
+    }
+  mse = d_divs(mse, (double)(oh * ow));
+  const dual6 l = d_add(d_muls(bce, bce_w), d_muls(mse, mse_w));
+  *loss_out = l.v;
+  for (int i = 0; i < 6; ++i) grad6[i] = l.g[i];
+  free(pot), free(gam), free(un), free(bu), free(bd), free(un2), free(bu2), free(bd2);
+}
+
+/* Deterministic forward from a discrete layer, double (run_deterministic<double>). */
+void ebo_det_run(const ebo_grid* g, const double* cfg, int steps, double* un, double* burn,
+                 double* bd) {
+  const int h = g->h, w = g->w;
+  const size_t n = (size_t)h * w;
+  double* pot = (double*)malloc(n * 8 * sizeof(double));
+  double* gam = (double*)malloc(n * sizeof(double));
+  double *a = (double*)malloc(n * sizeof(double)), *b = (double*)malloc(n * sizeof(double)),
+         *c = (double*)malloc(n * sizeof(double));
+  ebo_tables(g, cfg, pot, gam);
+  for (int t = 0; t < steps; ++t) {
+    ebo_det_step_tables(h, w, pot, gam, cfg[5], un, burn, bd, a, b, c);
+    memcpy(un, a, n * sizeof(double));
+    memcpy(burn, b, n * sizeof(double));
+    memcpy(bd, c, n * sizeof(double));
+  }
+  free(pot), free(gam), free(a), free(b), free(c);
+}

@@ -119,6 +119,14 @@ int ebo_tanker_policy(uint64_t seed, uint32_t env_id, const ebo_tanker_state* s,
 void ebo_det_step_tables(int h, int w, const double* pot, const double* gamma, double p_continue,
                          const double* un, const double* burn, const double* bd, double* un_o,
                          double* burn_o, double* bd_o);
+/* run_deterministic<double> from an arbitrary continuous state (in place). */
+void ebo_det_run(const ebo_grid* g, const double* cfg, int steps, double* un, double* burn,
+                 double* bd);
+/* C4 gradient oracle: run_deterministic<Dual<6>> + loss (calibrate.hpp:120-146) from a discrete
+ * initial layer, theta = the 6 SimConfig fields; grad6 = d loss / d theta. */
+void ebo_det_loss_grad(const ebo_grid* g, const double* cfg, int steps, const uint8_t* fire0,
+                       const double* mask, double bce_w, double mse_w, int pool, double* loss_out,
+                       double* grad6);
 
 #ifdef __cplusplus
 }

@@ -81,6 +81,8 @@ _PORT_SIG = {
                                C.POINTER(TankerSt), _P, _P, _P, _P]),
     "ebo_tanker_policy": (_I, [_U64, _U32, C.POINTER(TankerSt), _I]),
     "ebo_det_step_tables": (None, [_I, _I, _P, _P, _D, _P, _P, _P, _P, _P, _P]),
+    "ebo_det_run": (None, [_P, _P, _I, _P, _P, _P]),
+    "ebo_det_loss_grad": (None, [_P, _P, _I, _P, _P, _D, _D, _I, C.POINTER(_D), _P]),
 }
 
 _REF_SIG = {

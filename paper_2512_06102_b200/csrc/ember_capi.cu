@@ -276,9 +276,16 @@ void ebl_batch_destroy(ebl_batch* b) {
 int ebl_batch_set_config(ebl_batch* b, const ebl_sim_config* c) {
   if (int e = check_batch(b)) return e;
   if (!c) return set_err(EBL_EINVAL, "null config");
+  // pot/gamma/kappa depend on every field but p_continue and max_steps
+  const bool statics = c->p_base != b->cfg.p_base || c->alpha_w1 != b->cfg.alpha_w1 ||
+                       c->alpha_w2 != b->cfg.alpha_w2 || c->alpha_s != b->cfg.alpha_s ||
+                       c->alpha_gamma != b->cfg.alpha_gamma ||
+                       std::memcmp(&c->p_base, &b->cfg.p_base, 5 * sizeof(double)) != 0;
   b->cfg = *c;
-  b->tables_dirty = b->mode == ebl::kStaticTables;
-  b->derived_dirty = b->mode == ebl::kStaticTerrain;
+  if (statics) {
+    b->tables_dirty = b->tables_dirty || b->mode == ebl::kStaticTables;
+    b->derived_dirty = b->derived_dirty || b->mode == ebl::kStaticTerrain;
+  }
   return EBL_OK;
 }
 

@@ -285,9 +285,9 @@ __device__ void tanker_reset(const RlArgs& g, int env, RlEnv& e, uint8_t* cur, u
     cur[i] = 0;
     wet[i] = 0;
   }
+  const uint64_t stream = tanker_stream(g.env_id0 + env, episode);
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint64_t stream = tanker_stream(g.env_id0 + env, episode);
     const uint64_t prefix = key_prefix(g.seed, stream, 0);
     uint64_t counter = 0;
     const uint64_t max_draws = 64ull * n;
@@ -298,13 +298,14 @@ __device__ void tanker_reset(const RlArgs& g, int env, RlEnv& e, uint8_t* cur, u
       cur[cell] = 1;
       ++placed;
     }
-    e.step = 0;
-    e.episode = episode;
-    e.stream = stream;
-    e.done = placed == 0;
     *s_burning = placed;
   }
   __syncthreads();
+  // every thread holds its own copy of the env record: update all copies uniformly
+  e.step = 0;
+  e.episode = episode;
+  e.stream = stream;
+  e.done = *s_burning == 0;
 }
 
 // n_steps tanker steps of one env per CTA (n_steps = 1 for the per-step API).

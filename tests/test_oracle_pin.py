@@ -157,3 +157,33 @@ def test_port_vs_ref_batch(port, ref):
     assert ref.ref_step_batch(gr.h, O.ptr(cfg), 123, 4, 8, 15, O.ptr(f0), O.ptr(out)) == 0
     for m in range(8):
         assert np.array_equal(out[m], O.run(port, "port", gp, cfg, 123, 0, 4 + m, 15, f0))
+
+
+@pytest.mark.parametrize("bce_w,mse_w,pool", [(0.0, 1.0, 1), (1.0, 1.0, 4), (0.5, 2.0, 3)])
+def test_port_vs_ref_dual_loss_grad(port, ref, bce_w, mse_w, pool):
+    # C4 gradient oracle: run_deterministic<Dual<6>> + loss, restated vs the reference, bitwise
+    rs = np.random.default_rng(int(bce_w * 10 + pool))
+    h, w = 14, 11
+    veg = np.array([0.4, 0.25, 0.15, 0.0, -0.8, -0.7, -1.0, -1.0, -0.4, -0.2, -0.3])
+    den = np.array([0.3, 0.1, -0.1, -0.2, -0.8, -0.6, -1.0, -1.0, -0.3, -0.1, -0.4])
+    cls = rs.integers(0, 11, (h, w))
+    el = (200 * rs.random((h, w))).astype(np.float32)
+    gp = O.grid_terrain(port, "port", veg[cls], den[cls], el, 30.0, 4.0, 1.0)
+    gr = O.grid_terrain(ref, "ref", veg[cls], den[cls], el, 30.0, 4.0, 1.0)
+    f0 = np.zeros((h, w), np.uint8)
+    f0[7, 5] = f0[2, 2] = 1
+    mask = (rs.random((h, w)) < 0.3).astype(np.float64)
+    mask[0, 0] = 1.0
+    cfg = O.cfg_array([0.2, 0.15, 0.3, 1.2, 0.9, 0.65])
+    out = {}
+    for L, kind in ((port, "port"), (ref, "ref")):
+        loss, g6 = O._D(), np.empty(6)
+        fn = L.ebo_det_loss_grad if kind == "port" else L.ref_loss_grad
+        (gp if kind == "port" else gr)
+        rc = fn((gp if kind == "port" else gr).h, O.ptr(cfg), 20, O.ptr(f0), O.ptr(mask), bce_w, mse_w,
+                pool, loss, O.ptr(g6))
+        assert rc in (None, 0)
+        out[kind] = (loss.value, g6)
+    assert out["port"][0] == out["ref"][0]
+    assert np.array_equal(out["port"][1], out["ref"][1])
+    assert np.abs(out["ref"][1]).max() > 0
