@@ -10,7 +10,7 @@ reset the 1024 fire layers to their ignitions and advance 200 CA steps
   e2e     the same metric through the public C-ABI with HOST buffers: pinned host ->
           device copy of the 1024 initial layers, 200 steps, device -> host copy of the
           1024 final layers, all inside the timed region.
-  roofline  dominant kernel (k_step_resident) vs measured HBM copy bandwidth, at SURVEY
+  roofline  dominant kernel (k_step_blocked) vs measured HBM copy bandwidth, at SURVEY
           §8(d)'s 10 algorithmic bytes per cell-update.
   cpu_baseline  the reference's own code (oracle/_ref = /root/reference/proj compiled in
           place) on this host's cores, a bounded sample of the same workload.
@@ -311,7 +311,7 @@ def main():
                     "h2d_bytes_per_step": int(init.nbytes), "d2h_bytes_per_step": int(init.nbytes)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "k_step_resident" if args.kernel != "tiled" else "k_step_tile",
+                         "kernel": "k_step_blocked" if args.kernel != "tiled" else "k_step_tile",
                          "alg_bytes_per_launch": alg_bytes if args.kernel != "tiled"
                          else alg_bytes // CA_STEPS,
                          "kernel_ms": kern_s * 1e3},

@@ -83,7 +83,9 @@ int ebl_batch_set_terrain(ebl_batch* b, int n_grids, const uint8_t* fuel_class,
  * terrain form; n_winds = 1 or n_envs. */
 int ebl_batch_set_wind(ebl_batch* b, int n_winds, const double* speed, const double* direction);
 
-/* Member fire layers, host <-> device, [n_envs][H*W] uint8 (values must be 0..2). */
+/* Member fire layers, host <-> device, [n_envs][H*W] uint8.  Like the reference's FireLayer
+ * they are not validated: a byte other than 1 (Burning) / 2 (Burned) steps as Unburned
+ * (engine.cpp:15-25) and is written back as 0 or 1. */
 int ebl_batch_set_state(ebl_batch* b, const uint8_t* states);
 int ebl_batch_get_state(ebl_batch* b, uint8_t* states);
 /* Same, device pointers (no host round trip). */
@@ -104,12 +106,20 @@ uint64_t ebl_batch_step_index(const ebl_batch* b);
 int ebl_step_batch(ebl_batch* b, int n_steps);
 
 /* Kernel selection for ebl_step_batch (results are identical by construction):
- * EBL_KERNEL_AUTO picks the fused env-resident multi-step kernel when one env's
- * layers fit in shared memory, else the tiled one-step-per-launch kernel. */
+ *  AUTO      the bit-sliced blocked kernel: one CTA per env with all n steps fused when an
+ *            env fits shared memory (H*W <= 65536), else light-cone-halo tiles, 8 steps
+ *            per launch;
+ *  TILED     the per-cell tile kernel, one step per launch (independent implementation);
+ *  RESIDENT  the blocked kernel, whole env per CTA (error if it does not fit);
+ *  BLOCKED   the blocked kernel with halo tiles even when the env would fit. */
 #define EBL_KERNEL_AUTO 0
 #define EBL_KERNEL_TILED 1
 #define EBL_KERNEL_RESIDENT 2
+#define EBL_KERNEL_BLOCKED 3
 int ebl_batch_set_kernel(ebl_batch* b, int which);
+/* Explicit tiling of the blocked kernel (tile_h rows x tile_w cols, tile_w a multiple of
+ * 32, `halo` rows of light cone = steps per launch); tile_h == 0 restores planning. */
+int ebl_batch_set_tiling(ebl_batch* b, int tile_h, int tile_w, int halo);
 
 /* fire_fraction_stats (engine.cpp:185-198) as integer counts of the current
  * state, out[e*4 + {0,1,2,3}] = {unburned, burning, burned, newly ignited in the
@@ -142,6 +152,23 @@ int ebl_run_stochastic(int height, int width, const uint8_t* initial, const doub
                        const double* wind_direction, const double* veg, const double* den,
                        const double* slope8, const ebl_sim_config* cfg, uint64_t seed,
                        uint64_t step, uint64_t stream, int steps, uint8_t* out);
+
+/* ---- deterministic (raw-probability) mode and its gradient (BASELINE C4) -------- */
+/* BasicContinuousState (engine.hpp:27-37) of every env as fp32 planes [n_envs][H*W]. */
+int ebl_det_set_state(ebl_batch* b, const float* p_un, const float* p_burn, const float* p_bd);
+/* state_from_fire (engine.cpp:42-52) of the batch's current fire layers. */
+int ebl_det_set_state_from_fire(ebl_batch* b);
+int ebl_det_get_state(ebl_batch* b, float* p_un, float* p_burn, float* p_bd);
+/* run_deterministic (engine.hpp:225-245) for n_steps on the terrain statics, fp32 on the
+ * device; record = 1 keeps (p_un, p_burn) of every step in HBM for ebl_det_loss_grad. */
+int ebl_det_forward(ebl_batch* b, int n_steps, int record);
+/* loss = bce_w * BCE(clamp(pred)) + mse_w * MSE(avgpool(pred, pool), avgpool(mask, pool)),
+ * pred = p_burn + p_bd (calibrate.hpp:86-146), per env, and its gradient with respect to
+ * the six SimConfig fields in ParamIndex order (calibrate.hpp:21-28) by reverse mode
+ * through the recorded steps (the reference computes it forward-mode with Dual<6>,
+ * calibrate.cpp:130-162).  mask [n_envs][H*W]; loss [n_envs]; grad6 [n_envs*6]. */
+int ebl_det_loss_grad(ebl_batch* b, const float* mask, double bce_w, double mse_w, int pool,
+                      double* loss, double* grad6);
 
 /* ---- RL (rl_env.hpp) ---------------------------------------------------------- */
 /* EnvConfig (rl_env.hpp:24-40). */

@@ -91,6 +91,7 @@ SIGNATURES = {
     "ebl_batch_step_index": (_U64, [_P]),
     "ebl_step_batch": (_I, [_P, _I]),
     "ebl_batch_set_kernel": (_I, [_P, _I]),
+    "ebl_batch_set_tiling": (_I, [_P, _I, _I, _I]),
     "ebl_batch_counts": (_I, [_P, _P]),
     "ebl_batch_intensity": (_I, [_P, _P, _P]),
     "ebl_batch_diag": (_I, [_P, _P, _I]),
@@ -100,6 +101,11 @@ SIGNATURES = {
                                  _U64, _U64, _P]),
     "ebl_run_stochastic": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, C.POINTER(SimConfig), _U64,
                                 _U64, _U64, _I, _P]),
+    "ebl_det_set_state": (_I, [_P, _P, _P, _P]),
+    "ebl_det_set_state_from_fire": (_I, [_P]),
+    "ebl_det_get_state": (_I, [_P, _P, _P, _P]),
+    "ebl_det_forward": (_I, [_P, _I, _I]),
+    "ebl_det_loss_grad": (_I, [_P, _P, _D, _D, _I, _P, _P]),
     "ebl_env_default_preset": (None, [C.POINTER(EnvConfig)]),
     "ebl_env_smoke10_preset": (None, [C.POINTER(EnvConfig)]),
     "ebl_env_observation_size": (_I, [C.POINTER(EnvConfig)]),

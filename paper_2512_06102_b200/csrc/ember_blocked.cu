@@ -1,0 +1,355 @@
+// Bit-sliced, temporally blocked multi-step kernel — the throughput path.
+//
+// A CTA owns one *tile* of one env layer and advances it n_steps steps per launch:
+// the tile plus a halo (K rows above/below, one 32-cell word left/right) is read once
+// from HBM (uint8 [row][col]), converted to bit-planes in shared memory, stepped, and
+// the tile (not the halo) is written back once.  Cells at distance d from a region
+// boundary that is not a grid edge are exact for d steps (the halo is the light cone),
+// so n_steps <= K.  With the tile = the whole env (H*W <= 65536 cells) there is no halo
+// and n_steps is unbounded: BASELINE C1 runs its 200 steps in ONE launch per env.
+//
+// Planes: B[2] (Burning, double-buffered, one zero row of padding above/below), X (Burned),
+// ACT (per-thread overflow of the active list).  Per step, two block barriers:
+//   P1 dense   (32 cells per op, each thread owns fixed words): any = 8-neighbour dilation
+//              of B, act = (Unburned & any) | B; Bn[w] = B[w]; active cells appended to a
+//              shared list with one warp-aggregated atomic per warp (cells beyond the
+//              list capacity stay with their owner thread in ACT);
+//   --- barrier ---
+//   P2 sparse  one thread per active cell: the last two rng_word rounds on the
+//              per-(env,step) prefix; Burning: integer survive test, burn-out clears Bn
+//              and sets X; candidate: 8-bit neighbour mask from B, lambda/p in fp32 with the
+//              fp64 guard (ember_device.cuh), ignition sets Bn (shared atomics);
+//   --- barrier ---, swap B <-> Bn.
+// Every cell of the tile is updated every step (quiescent ones by the bit-sliced copy),
+// so cell-updates are counted densely as the reference does (emberline_main.cpp:432-433);
+// results are bit-identical to k_step_tile and engine.cpp:134-159 by construction.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ember_device.cuh"
+#include "ember_kernels.h"
+#include "ember_params.h"
+
+namespace ebl {
+
+namespace {
+
+__device__ __forceinline__ uint32_t west_of(const uint32_t* row, int j) {
+  return (row[j] << 1) | (j > 0 ? row[j - 1] >> 31 : 0u);  // bit c <- cell c-1
+}
+
+__device__ __forceinline__ uint32_t east_of(const uint32_t* row, int j, int wpr) {
+  return (row[j] >> 1) | (j + 1 < wpr ? row[j + 1] << 31 : 0u);  // bit c <- cell c+1
+}
+
+__device__ __forceinline__ uint32_t low_mask(int n) {
+  return n >= 32 ? 0xffffffffu : (n <= 0 ? 0u : ((1u << n) - 1u));
+}
+
+// Iterates this thread's words idx = tid, tid+T, ... of an [rows][wpr] plane with the
+// (row, word) pair maintained incrementally (no division in the loop).
+struct WordIter {
+  int idx, r, j, dr, dj, wpr, n;
+  __device__ __forceinline__ WordIter(int wpr_, int n_) : wpr(wpr_), n(n_) {
+    idx = threadIdx.x;
+    r = idx / wpr;
+    j = idx - r * wpr;
+    dr = blockDim.x / wpr;
+    dj = blockDim.x - dr * wpr;
+  }
+  __device__ __forceinline__ bool ok() const { return idx < n; }
+  __device__ __forceinline__ void next() {
+    idx += blockDim.x;
+    r += dr;
+    j += dj;
+    if (j >= wpr) {
+      j -= wpr;
+      ++r;
+    }
+  }
+};
+
+}  // namespace
+
+template <int MODE>
+__global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, BlockGeom g) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_total[2];
+  __shared__ int32_t s_newly[2];
+  __shared__ int32_t s_cnt[4];
+
+  const int env = blockIdx.z;
+  const int W = a.w, BH = a.h;
+  const int r0 = blockIdx.y * g.tile_h, c0 = blockIdx.x * g.tile_w;  // c0 % 32 == 0
+  const int R0 = max(0, r0 - g.halo_rows), R1 = min(BH, r0 + g.tile_h + g.halo_rows);
+  const int C0 = max(0, c0 - g.halo_cols), C1 = min(W, c0 + g.tile_w + g.halo_cols);
+  const int RH = R1 - R0, RW = C1 - C0;
+  const int wpr = (RW + 31) >> 5;
+  const int nwords = RH * wpr;
+  const int pw = (RH + 2) * wpr;
+  uint32_t* Bp[2];
+  Bp[0] = reinterpret_cast<uint32_t*>(smem);
+  Bp[1] = Bp[0] + pw;
+  uint32_t* X = Bp[1] + pw;
+  uint32_t* ACT = X + nwords;
+  uint16_t* list = reinterpret_cast<uint16_t*>(ACT + nwords);
+  const int cap = g.list_cap;
+
+  const size_t ncell = static_cast<size_t>(BH) * W;
+  const uint8_t* __restrict__ in = a.in + env * ncell;
+  const bool vec = (W & 15) == 0;  // 16-byte aligned rows (C0 is a multiple of 32)
+
+  // ---- load: uint8 layer -> bit-planes ------------------------------------------------
+  for (int i = threadIdx.x; i < wpr; i += blockDim.x) {  // zero padding rows of both buffers
+    Bp[0][i] = Bp[1][i] = 0u;
+    Bp[0][(RH + 1) * wpr + i] = Bp[1][(RH + 1) * wpr + i] = 0u;
+  }
+  if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+  if (threadIdx.x < 2) {
+    s_total[threadIdx.x] = 0;
+    s_newly[threadIdx.x] = 0;
+  }
+  for (WordIter it(wpr, nwords); it.ok(); it.next()) {
+    const int nc = min(32, RW - 32 * it.j);
+    const uint8_t* src = in + static_cast<size_t>(R0 + it.r) * W + C0 + 32 * it.j;
+    uint32_t b = 0u, x = 0u;
+    if (nc == 32 && vec) {
+      const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(src));
+      const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+      const uint32_t wds[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        // byte k of wds[q] is cell 4q+k; bit0 = Burning (1), bit1 = Burned (2); other byte
+        // values act as Unburned exactly as in next_fire_cell (engine.cpp:15-25)
+        const uint32_t v = wds[q];
+        const uint32_t z = v & 0xFCFCFCFCu;  // per byte: nonzero iff value >= 4
+        const uint32_t small = ~((((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) >> 7) & 0x01010101u;
+        const uint32_t b0 = v & 0x01010101u, b1 = (v >> 1) & 0x01010101u;
+        const uint32_t lo = b0 & ~b1 & small;  // byte == 1
+        const uint32_t hi = b1 & ~b0 & small;  // byte == 2
+        b |= ((lo * 0x01020408u) >> 24 & 0xfu) << (4 * q);  // gather bytes' bit0 -> 4 bits
+        x |= ((hi * 0x01020408u) >> 24 & 0xfu) << (4 * q);
+      }
+    } else {
+      for (int k = 0; k < nc; ++k) {
+        const uint8_t v = src[k];
+        b |= static_cast<uint32_t>(v == 1) << k;
+        x |= static_cast<uint32_t>(v == 2) << k;
+      }
+    }
+    Bp[0][(it.r + 1) * wpr + it.j] = b;
+    X[it.idx] = x;
+    ACT[it.idx] = 0u;
+  }
+  __syncthreads();
+
+  const DiagCounters dg{a.diag};
+  const uint64_t stream = a.streams[env];
+  const uint64_t gbase = static_cast<uint64_t>(g.row_off + R0) * W + C0;  // RNG index of region (0,0)
+  const int lane = threadIdx.x & 31;
+  // newly-ignited cells are counted only inside the output tile
+  const int tr0 = r0 - R0, tr1 = min(r0 + g.tile_h, BH) - R0;
+  const int tc0 = c0 - C0, tc1 = min(c0 + g.tile_w, W) - C0;
+  int cur = 0;
+
+  for (int t = 0; t < g.n_steps; ++t) {
+    const uint32_t* B = Bp[cur];
+    uint32_t* Bn = Bp[cur ^ 1];
+    const int par = t & 1;
+    if (threadIdx.x == 0) {  // the other parity's counters are free until the next step
+      s_total[par ^ 1] = 0;
+      s_newly[par ^ 1] = 0;
+    }
+    const uint64_t prefix = key_prefix(a.seed, stream, a.step + static_cast<uint64_t>(t));
+    // ---- P1: dilation, copy B -> Bn, active words -> ACT ----------------------------------
+    int cnt = 0;
+    bool ovf = false;
+    for (WordIter it(wpr, nwords); it.ok(); it.next()) {
+      const int j = it.j;
+      const uint32_t* up = B + (it.r + 2) * wpr;
+      const uint32_t* mid = B + (it.r + 1) * wpr;
+      const uint32_t* dn = B + it.r * wpr;
+      const uint32_t any = up[j] | west_of(up, j) | east_of(up, j, wpr) | dn[j] | west_of(dn, j) |
+                           east_of(dn, j, wpr) | west_of(mid, j) | east_of(mid, j, wpr);
+      const uint32_t b = mid[j];
+      Bn[(it.r + 1) * wpr + j] = b;
+      const uint32_t act = ((~(b | X[it.idx]) & low_mask(RW - 32 * j)) & any) | b;
+      ACT[it.idx] = act;
+      cnt += __popc(act);
+    }
+    // one warp-aggregated list reservation per warp and step (skipped by quiet warps)
+    if (__ballot_sync(0xffffffffu, cnt > 0)) {
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int base = 0;
+      if (lane == 31) base = atomicAdd(&s_total[par], incl);
+      base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+      if (cnt > 0) {
+        for (WordIter it(wpr, nwords); it.ok(); it.next()) {
+          uint32_t rest = ACT[it.idx];
+          const int cell0 = it.r * RW + 32 * it.j;
+          while (rest && base < cap) {
+            const int bit = __ffs(rest) - 1;
+            rest &= rest - 1;
+            list[base++] = static_cast<uint16_t>(cell0 + bit);
+          }
+          ACT[it.idx] = rest;  // overflow beyond the list capacity: done by this thread in P2
+          ovf |= rest != 0u;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- P2: sparse decisions ------------------------------------------------------------
+    int newly = 0;
+    const int total = min(s_total[par], cap);
+    auto decide = [&](int lc) {
+      const int rr = lc / RW, cc = lc - rr * RW;
+      const int wi = (rr + 1) * wpr + (cc >> 5);
+      const uint32_t bit = 1u << (cc & 31);
+      const uint64_t m = cell_bits53(prefix, gbase + static_cast<uint64_t>(rr) * W + cc, 0);
+      if (B[wi] & bit) {
+        if (m >= a.pc_thr) {
+          atomicAnd(Bn + wi, ~bit);
+          atomicOr(X + rr * wpr + (cc >> 5), bit);
+        }
+      } else {
+        uint32_t nb = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int ur = rr - kDy[k], uc = cc - kDx[k];
+          if (uc < 0 || uc >= RW) continue;  // padding rows cover ur = -1 and ur = RH
+          nb |= ((B[(ur + 1) * wpr + (uc >> 5)] >> (uc & 31)) & 1u) << k;
+        }
+        if (ignite<MODE>(a, env, R0 + rr, C0 + cc, nb, m, dg)) {
+          atomicOr(Bn + wi, bit);
+          newly += (rr >= tr0 && rr < tr1 && cc >= tc0 && cc < tc1);
+        }
+      }
+    };
+    for (int i = threadIdx.x; i < total; i += blockDim.x) decide(list[i]);
+    for (WordIter it(wpr, nwords); ovf && it.ok(); it.next()) {
+      uint32_t rest = ACT[it.idx];
+      while (rest) {
+        const int bit = __ffs(rest) - 1;
+        rest &= rest - 1;
+        decide(it.r * RW + 32 * it.j + bit);
+      }
+    }
+    if (t == g.n_steps - 1) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) newly += __shfl_xor_sync(0xffffffffu, newly, o);
+      if (lane == 0 && newly) atomicAdd(&s_newly[par], newly);
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+
+  // ---- store the tile: bit-planes -> uint8, counts -----------------------------------------
+  const uint32_t* B = Bp[cur];
+  uint8_t* __restrict__ out = a.out + env * ncell;
+  int32_t nU = 0, nB = 0, nX = 0;
+  const int tj0 = tc0 >> 5, tj1 = (tc1 + 31) >> 5;
+  const int twords = tj1 - tj0;
+  for (WordIter it(twords, (tr1 - tr0) * twords); it.ok(); it.next()) {
+    const int rr = tr0 + it.r, j = tj0 + it.j;
+    const uint32_t b = B[(rr + 1) * wpr + j], x = X[rr * wpr + j];
+    const int nc = min(32, RW - 32 * j);
+    nB += __popc(b);
+    nX += __popc(x);
+    nU += nc - __popc(b) - __popc(x);
+    uint8_t* dst = out + static_cast<size_t>(R0 + rr) * W + C0 + 32 * j;
+    if (nc == 32 && vec) {
+      uint32_t wds[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {  // spread 4 bits to 4 bytes: bit k -> bit 8k
+        const uint32_t bs = (((b >> (4 * q)) & 0xfu) * 0x00204081u) & 0x01010101u;
+        const uint32_t xs = (((x >> (4 * q)) & 0xfu) * 0x00204081u) & 0x01010101u;
+        wds[q] = bs | (xs << 1);
+      }
+      reinterpret_cast<uint4*>(dst)[0] = make_uint4(wds[0], wds[1], wds[2], wds[3]);
+      reinterpret_cast<uint4*>(dst)[1] = make_uint4(wds[4], wds[5], wds[6], wds[7]);
+    } else {
+      for (int k = 0; k < nc; ++k) dst[k] = static_cast<uint8_t>(((b >> k) & 1u) | (((x >> k) & 1u) << 1));
+    }
+  }
+  if (a.counts) {
+    atomicAdd(&s_cnt[0], nU);
+    atomicAdd(&s_cnt[1], nB);
+    atomicAdd(&s_cnt[2], nX);
+    __syncthreads();
+    if (threadIdx.x < 3) atomicAdd(a.counts + env * 4 + threadIdx.x, s_cnt[threadIdx.x]);
+    if (threadIdx.x == 3 && g.n_steps > 0)
+      atomicAdd(a.counts + env * 4 + 3, s_newly[(g.n_steps - 1) & 1]);
+  }
+}
+
+size_t blocked_smem_bytes(int region_h, int region_w, int list_cap) {
+  const size_t wpr = (region_w + 31) / 32;
+  const size_t planes = (2 * (static_cast<size_t>(region_h) + 2) + 2 * region_h) * wpr * sizeof(uint32_t);
+  const size_t list = static_cast<size_t>(list_cap) * sizeof(uint16_t);
+  return planes + ((list + 15) & ~size_t(15));
+}
+
+static int list_cap_for(int cells) {
+  // active cells are ~1-3% of an env per step; a quarter of the region is ample and an
+  // overflow is still exact (owner threads finish the rest)
+  const int cap = (cells + 3) / 4;
+  return cap < 1024 ? (cells < 1024 ? cells : 1024) : cap;
+}
+
+bool resident_fits(int h, int w) {
+  return static_cast<size_t>(h) * w <= 65536 &&
+         blocked_smem_bytes(h, w, list_cap_for(h * w)) <= kResMaxSmem;
+}
+
+BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_off) {
+  BlockGeom g{};
+  g.row_off = row_off;
+  if (!force_tiles && resident_fits(buf_h, w)) {  // whole env per CTA, all steps fused
+    g.tile_h = buf_h;
+    g.tile_w = ((w + 31) / 32) * 32;
+    g.halo_rows = 0;
+    g.halo_cols = 0;
+    g.n_steps = n_steps;
+  } else {
+    g.halo_rows = kBlockHalo;
+    g.tile_w = w <= kBlockTileW + 64 ? ((w + 31) / 32) * 32 : kBlockTileW;
+    g.halo_cols = g.tile_w >= w ? 0 : 32;
+    g.tile_h = kBlockTileH;
+    if (g.tile_h >= buf_h) {
+      g.tile_h = buf_h;
+      g.halo_rows = 0;
+    }
+    const bool fuzzy = g.halo_rows > 0 || g.halo_cols > 0;
+    g.n_steps = !fuzzy ? n_steps : (n_steps < kBlockHalo ? n_steps : kBlockHalo);
+  }
+  const int rh = g.tile_h + 2 * g.halo_rows, rw = g.tile_w + 2 * g.halo_cols;
+  g.list_cap = list_cap_for((rh < buf_h ? rh : buf_h) * (rw < w ? rw : w));
+  return g;
+}
+
+cudaError_t launch_step_blocked(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s) {
+  const int rh = g.tile_h + 2 * g.halo_rows, rw = g.tile_w + 2 * g.halo_cols;
+  const size_t sm = blocked_smem_bytes(rh < a.h ? rh : a.h, rw < a.w ? rw : a.w, g.list_cap);
+  const dim3 grid((a.w + g.tile_w - 1) / g.tile_w, (a.h + g.tile_h - 1) / g.tile_h, a.n_envs);
+  cudaError_t e;
+  if (mode == kStaticTables) {
+    e = cudaFuncSetAttribute(k_step_blocked<kStaticTables>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sm));
+    if (e != cudaSuccess) return e;
+    k_step_blocked<kStaticTables><<<grid, kResThreads, sm, s>>>(a, g);
+  } else {
+    e = cudaFuncSetAttribute(k_step_blocked<kStaticTerrain>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sm));
+    if (e != cudaSuccess) return e;
+    k_step_blocked<kStaticTerrain><<<grid, kResThreads, sm, s>>>(a, g);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ebl

@@ -4,6 +4,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -69,6 +70,7 @@ struct ebl_batch {
   DevBuf<uint8_t> state[2];
   int cur = 0;
   int kernel = EBL_KERNEL_AUTO;
+  int tile_h = 0, tile_w = 0, tile_halo = 0;  // explicit blocked tiling (tests); 0 = planned
   bool counts_valid = false;
   DevBuf<int32_t> counts;
   DevBuf<unsigned long long> diag;
@@ -106,6 +108,14 @@ struct ebl_batch {
   DevBuf<double> reward, reward_sum;
   DevBuf<int32_t> actions, error, episodes;
   DevBuf<double> obs;
+
+  // deterministic mode (C4)
+  DevBuf<float> det[6];             // un, burn, bd x2 (double buffer)
+  int det_cur = 0;
+  bool det_ready = false;
+  DevBuf<float> pot32, gam32, F32, traj, adj, mask32, wind32, align32;
+  DevBuf<double> grad_pred, acc, det_loss, det_grad;
+  int traj_steps = 0;               // steps recorded by the last ebl_det_forward(record=1)
 };
 
 namespace {
@@ -372,18 +382,9 @@ int ebl_batch_set_wind(ebl_batch* b, int n_winds, const double* speed, const dou
 
 int ebl_batch_set_state(ebl_batch* b, const uint8_t* states) {
   if (int e = check_batch(b)) return e;
+  // Like the reference's FireLayer (a plain Grid<FireState>, grid.hpp:100) member layers are
+  // not validated; a byte other than 1/2 takes the Unburned path as in engine.cpp:15-25.
   const size_t total = b->ncell * b->n_envs;
-  {  // every byte in {0,1,2} (grid.cpp:133-136), 8 bytes per test
-    size_t i = 0;
-    uint64_t bad = 0;
-    for (; i + 8 <= total; i += 8) {
-      uint64_t v;
-      std::memcpy(&v, states + i, 8);
-      bad |= (v & 0xFCFCFCFCFCFCFCFCull) | (v & (v >> 1) & 0x0101010101010101ull);
-    }
-    for (; i < total; ++i) bad |= states[i] > 2;
-    if (bad) return set_err(EBL_EINVAL, "GridState: invalid fire state value");
-  }
   EBL_CUDA(cudaSetDevice(b->device));
   EBL_CUDA(cudaMemcpyAsync(b->state[b->cur].p, states, total, cudaMemcpyHostToDevice, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
@@ -431,7 +432,7 @@ uint64_t ebl_batch_step_index(const ebl_batch* b) { return b ? b->step : 0; }
 
 int ebl_batch_set_kernel(ebl_batch* b, int which) {
   if (int e = check_batch(b)) return e;
-  if (which < EBL_KERNEL_AUTO || which > EBL_KERNEL_RESIDENT) return set_err(EBL_EINVAL, "unknown kernel");
+  if (which < EBL_KERNEL_AUTO || which > EBL_KERNEL_BLOCKED) return set_err(EBL_EINVAL, "unknown kernel");
   if (which == EBL_KERNEL_RESIDENT && !ebl::resident_fits(b->h, b->w))
     return set_err(EBL_EINVAL, "env too large for the resident kernel");
   b->kernel = which;
@@ -443,35 +444,64 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
   if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
   if (n_steps == 0) return EBL_OK;
   if (int e = prepare(b)) return e;
-  const bool resident = b->kernel == EBL_KERNEL_RESIDENT ||
-                        (b->kernel == EBL_KERNEL_AUTO && ebl::resident_fits(b->h, b->w));
-  if (resident) {
-    if (!ebl::resident_fits(b->h, b->w))
-      return set_err(EBL_EINVAL, "env too large for the resident kernel");
-    ebl::StepArgs a = step_args(b);
-    a.counts = b->counts.p;
-    EBL_CUDA(ebl::launch_step_resident(a, b->mode, n_steps, b->stream));
-    b->cur ^= 1;
-    b->step += n_steps;
-    b->launches += 1;
-    b->steps_done += n_steps;
-    b->counts_valid = true;
-    return EBL_OK;
-  }
-  for (int t = 0; t < n_steps; ++t) {
-    ebl::StepArgs a = step_args(b);
-    const bool last = t == n_steps - 1;
-    if (last) {
-      EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
-      a.counts = b->counts.p;
+  if (b->kernel == EBL_KERNEL_TILED) {  // one step per launch (the simple per-cell kernel)
+    for (int t = 0; t < n_steps; ++t) {
+      ebl::StepArgs a = step_args(b);
+      if (t == n_steps - 1) {
+        EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
+        a.counts = b->counts.p;
+      }
+      EBL_CUDA(ebl::launch_step_tile(a, b->mode, b->stream));
+      b->cur ^= 1;
+      b->step += 1;
+      b->launches += 1;
     }
-    EBL_CUDA(ebl::launch_step_tile(a, b->mode, b->stream));
-    b->cur ^= 1;
-    b->step += 1;
-    b->launches += 1;
+  } else {  // bit-sliced blocked kernel: whole env per CTA when it fits, else halo tiles
+    const bool force_tiles = b->kernel == EBL_KERNEL_BLOCKED;
+    for (int done = 0; done < n_steps;) {
+      ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps - done, force_tiles, 0);
+      if (b->tile_h > 0) {  // test hook: explicit tiling
+        g.tile_h = b->tile_h;
+        g.tile_w = b->tile_w;
+        g.halo_rows = b->tile_halo;
+        g.halo_cols = g.tile_w >= b->w ? 0 : 32;
+        g.n_steps = std::min(n_steps - done, std::max(1, b->tile_halo));
+        const int rh = std::min(b->h, g.tile_h + 2 * g.halo_rows);
+        const int rw = std::min(b->w, g.tile_w + 2 * g.halo_cols);
+        g.list_cap = std::max(1, rh * rw / 4);
+      }
+      ebl::StepArgs a = step_args(b);
+      if (done + g.n_steps == n_steps) {
+        EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
+        a.counts = b->counts.p;
+      }
+      EBL_CUDA(ebl::launch_step_blocked(a, b->mode, g, b->stream));
+      b->cur ^= 1;
+      b->step += g.n_steps;
+      b->launches += 1;
+      done += g.n_steps;
+    }
   }
   b->steps_done += n_steps;
   b->counts_valid = true;
+  return EBL_OK;
+}
+
+int ebl_batch_set_tiling(ebl_batch* b, int tile_h, int tile_w, int halo) {
+  if (int e = check_batch(b)) return e;
+  if (tile_h == 0) {
+    b->tile_h = 0;
+    return EBL_OK;
+  }
+  if (tile_h < 1 || tile_w < 32 || (tile_w & 31) || halo < 0 || halo > 32 ||
+      (halo == 0 && (tile_h < b->h || tile_w < b->w)))
+    return set_err(EBL_EINVAL, "tiling: tile_w a positive multiple of 32, halo in [1,32] unless one tile");
+  const int rh = std::min(b->h, tile_h + 2 * halo), rw = std::min(b->w, tile_w + (tile_w >= b->w ? 0 : 64));
+  if (rh * rw > 65536 || ebl::blocked_smem_bytes(rh, rw, std::max(1, rh * rw / 4)) > ebl::kResMaxSmem)
+    return set_err(EBL_EINVAL, "tiling: region exceeds shared memory");
+  b->tile_h = tile_h;
+  b->tile_w = tile_w;
+  b->tile_halo = halo;
   return EBL_OK;
 }
 
@@ -830,6 +860,163 @@ int ebl_rl_get_wet(ebl_batch* b, uint8_t* wet) {
   if (int e = check_batch(b)) return e;
   if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
   EBL_CUDA(cudaMemcpyAsync(wet, b->wet.p, b->ncell * b->n_envs, cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+// ---- deterministic mode (engine.hpp:147-245) and its adjoint (C4) ---------------------------
+namespace {
+int det_alloc(ebl_batch* b) {
+  const size_t n = b->ncell * b->n_envs;
+  for (auto& d : b->det) EBL_CUDA(d.alloc(n));
+  return EBL_OK;
+}
+
+ebl::DetArgs det_args(ebl_batch* b) {
+  ebl::DetArgs d{};
+  d.s = step_args(b);
+  const size_t n = b->ncell * b->n_envs;
+  (void)n;
+  const int c = b->det_cur * 3, o = (b->det_cur ^ 1) * 3;
+  d.un = b->det[c].p;
+  d.burn = b->det[c + 1].p;
+  d.bd = b->det[c + 2].p;
+  d.un_o = b->det[o].p;
+  d.burn_o = b->det[o + 1].p;
+  d.bd_o = b->det[o + 2].p;
+  d.pot32 = b->pot32.p;
+  d.gam32 = b->gam32.p;
+  d.F32 = b->F32.p;
+  d.pc32 = static_cast<float>(b->cfg.p_continue);
+  d.wind_speed32 = b->wind32.p;
+  d.align32 = b->align32.p;
+  d.wind_stride = b->n_winds > 1 ? 1 : 0;
+  return d;
+}
+}  // namespace
+
+int ebl_det_set_state(ebl_batch* b, const float* un, const float* burn, const float* bd) {
+  if (int e = check_batch(b)) return e;
+  if (!un || !burn || !bd) return set_err(EBL_EINVAL, "null plane");
+  EBL_CUDA(cudaSetDevice(b->device));
+  if (int e = det_alloc(b)) return e;
+  const size_t bytes = b->ncell * b->n_envs * sizeof(float);
+  const int c = b->det_cur * 3;
+  EBL_CUDA(cudaMemcpyAsync(b->det[c].p, un, bytes, cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(b->det[c + 1].p, burn, bytes, cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(b->det[c + 2].p, bd, bytes, cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  b->det_ready = true;
+  b->traj_steps = 0;
+  return EBL_OK;
+}
+
+int ebl_det_set_state_from_fire(ebl_batch* b) {  // state_from_fire (engine.cpp:42-52)
+  if (int e = check_batch(b)) return e;
+  const size_t n = b->ncell * b->n_envs;
+  std::vector<uint8_t> st(n);
+  if (int e = ebl_batch_get_state(b, st.data())) return e;
+  std::vector<float> un(n), bu(n), bd(n);
+  for (size_t i = 0; i < n; ++i) {
+    un[i] = st[i] == 0 ? 1.f : 0.f;
+    bu[i] = st[i] == 1 ? 1.f : 0.f;
+    bd[i] = st[i] == 2 ? 1.f : 0.f;
+  }
+  return ebl_det_set_state(b, un.data(), bu.data(), bd.data());
+}
+
+int ebl_det_get_state(ebl_batch* b, float* un, float* burn, float* bd) {
+  if (int e = check_batch(b)) return e;
+  if (!b->det_ready) return set_err(EBL_ESTATE, "ebl_det_set_state first");
+  const size_t bytes = b->ncell * b->n_envs * sizeof(float);
+  const int c = b->det_cur * 3;
+  if (un) EBL_CUDA(cudaMemcpyAsync(un, b->det[c].p, bytes, cudaMemcpyDeviceToHost, b->stream));
+  if (burn) EBL_CUDA(cudaMemcpyAsync(burn, b->det[c + 1].p, bytes, cudaMemcpyDeviceToHost, b->stream));
+  if (bd) EBL_CUDA(cudaMemcpyAsync(bd, b->det[c + 2].p, bytes, cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_det_forward(ebl_batch* b, int n_steps, int record) {
+  if (int e = check_batch(b)) return e;
+  if (!b->det_ready) return set_err(EBL_ESTATE, "ebl_det_set_state first");
+  if (b->mode != ebl::kStaticTerrain)
+    return set_err(EBL_EINVAL, "deterministic mode runs on the terrain form (ebl_batch_set_terrain)");
+  if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
+  if (int e = prepare(b)) return e;
+  const size_t n = b->ncell * b->n_envs;
+  EBL_CUDA(b->pot32.alloc(n * 8));
+  EBL_CUDA(b->gam32.alloc(n));
+  EBL_CUDA(b->F32.alloc(n));
+  {  // per wind set: V and cos(phi_k - theta) - 1 (kernel.hpp:24)
+    std::vector<float> v(b->n_winds), al(static_cast<size_t>(b->n_winds) * 8);
+    for (int w = 0; w < b->n_winds; ++w) {
+      v[w] = static_cast<float>(b->wind_speed[w]);
+      const double dir = ebl::wrap_angle(b->wind_dir[w]);
+      for (int k = 0; k < 8; ++k) al[w * 8 + k] = static_cast<float>(std::cos(ebl::offset_angle(k) - dir) - 1.0);
+    }
+    EBL_CUDA(b->wind32.alloc(v.size()));
+    EBL_CUDA(b->align32.alloc(al.size()));
+    EBL_CUDA(cudaMemcpyAsync(b->wind32.p, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaMemcpyAsync(b->align32.p, al.data(), al.size() * sizeof(float), cudaMemcpyHostToDevice, b->stream));
+  }
+  if (record) EBL_CUDA(b->traj.alloc(2 * n * std::max(1, n_steps)));
+  ebl::DetArgs d = det_args(b);
+  EBL_CUDA(ebl::launch_det_tables(d, b->stream));
+  b->launches += 1;
+  for (int t = 0; t < n_steps; ++t) {
+    d = det_args(b);
+    if (record) {
+      d.traj_un = b->traj.p;
+      d.traj_burn = b->traj.p + n * n_steps;
+    }
+    EBL_CUDA(ebl::launch_det_forward(d, t, b->stream));
+    b->det_cur ^= 1;
+    b->launches += 1;
+  }
+  b->traj_steps = record ? n_steps : -1;
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_det_loss_grad(ebl_batch* b, const float* mask, double bce_w, double mse_w, int pool,
+                      double* loss, double* grad6) {
+  if (int e = check_batch(b)) return e;
+  if (b->traj_steps < 0 || !b->det_ready)
+    return set_err(EBL_ESTATE, "ebl_det_loss_grad needs a recorded ebl_det_forward");
+  if (pool < 1 || !(bce_w >= 0.0) || !(mse_w >= 0.0) || (bce_w == 0.0 && mse_w == 0.0))
+    return set_err(EBL_EINVAL, "LossConfig: weights >= 0, one positive, pool_size >= 1");
+  const size_t n = b->ncell * b->n_envs;
+  const int bpe = static_cast<int>((b->ncell + 255) / 256);
+  EBL_CUDA(b->mask32.alloc(n));
+  EBL_CUDA(b->adj.alloc(4 * n));
+  EBL_CUDA(b->grad_pred.alloc(n));
+  EBL_CUDA(b->acc.alloc(static_cast<size_t>(b->n_envs) * bpe * 8));
+  EBL_CUDA(b->det_loss.alloc(b->n_envs));
+  EBL_CUDA(b->det_grad.alloc(static_cast<size_t>(b->n_envs) * 6));
+  EBL_CUDA(cudaMemcpyAsync(b->mask32.p, mask, n * sizeof(float), cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaMemsetAsync(b->acc.p, 0, static_cast<size_t>(b->n_envs) * bpe * 8 * sizeof(double), b->stream));
+  ebl::DetArgs d = det_args(b);
+  d.mask = b->mask32.p;
+  d.bce_w = bce_w;
+  d.mse_w = mse_w;
+  d.pool = pool;
+  d.grad_pred = b->grad_pred.p;
+  d.A_un = b->adj.p;
+  d.A_burn = b->adj.p + n;
+  d.A_bd = b->adj.p + 2 * n;
+  d.a_lam = b->adj.p + 3 * n;
+  d.acc = b->acc.p;
+  d.loss = b->det_loss.p;
+  d.grad = b->det_grad.p;
+  d.traj_un = b->traj.p;
+  d.traj_burn = b->traj.p + n * std::max(1, b->traj_steps);
+  EBL_CUDA(ebl::launch_det_loss(d, b->stream));
+  for (int t = b->traj_steps - 1; t >= 0; --t) EBL_CUDA(ebl::launch_det_backward(d, t, b->stream));
+  EBL_CUDA(ebl::launch_det_reduce(d, b->stream));
+  b->launches += 2 + 2 * static_cast<uint64_t>(b->traj_steps);
+  EBL_CUDA(cudaMemcpyAsync(loss, b->det_loss.p, b->n_envs * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(grad6, b->det_grad.p, b->n_envs * 6 * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
   return EBL_OK;
 }

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kTileThreads) k_step_tile(StepArgs a) {
     uint8_t ns = 2;
     if (s == 1) {
       ns = cell_bits53(prefix, static_cast<uint64_t>(r) * W + c, 0) < a.pc_thr ? 1 : 2;
-    } else if (s == 0) {
+    } else if (s != 2) {  // any other byte takes the Unburned path (engine.cpp:15-25)
       uint32_t nb = 0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) nb |= static_cast<uint32_t>(tile[lr + 1 - kDy[k]][lc + 1 - kDx[k]] == 1) << k;

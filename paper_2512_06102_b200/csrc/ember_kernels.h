@@ -1,4 +1,4 @@
-// Launchers exported by ember_kernels.cu / ember_resident.cu to the C-ABI layer.
+// Launchers exported by ember_kernels.cu / ember_blocked.cu to the C-ABI layer.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -11,13 +11,22 @@ constexpr int kTileH = 16;        // 256 threads x 4 cells
 constexpr int kTileThreads = 256;
 constexpr int kRlThreads = 256;   // RL kernels: one CTA per env
 constexpr int kRlMaxCells = 16384;  // env layer(s) resident in shared memory
-constexpr int kResThreads = 256;    // fused env-resident kernel: one CTA per env
+constexpr int kResThreads = 128;    // blocked kernel: one CTA per tile (whole env if it fits)
 constexpr size_t kResMaxSmem = 200 * 1024;
+constexpr int kBlockTileH = 64;     // tiled blocked kernel (large grids): 64 x 256 tiles,
+constexpr int kBlockTileW = 256;    // 8-row / 32-column light-cone halo, 8 steps per launch
+constexpr int kBlockHalo = 8;
 
-size_t resident_smem_bytes(int h, int w);
+size_t blocked_smem_bytes(int region_h, int region_w, int list_cap);
 bool resident_fits(int h, int w);
-cudaError_t launch_step_resident(const StepArgs& a, int mode, int n_steps, cudaStream_t s);
+BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_off);
+cudaError_t launch_step_blocked(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s);
 
+cudaError_t launch_det_tables(const DetArgs& d, cudaStream_t s);
+cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s);
+cudaError_t launch_det_loss(const DetArgs& d, cudaStream_t s);
+cudaError_t launch_det_backward(const DetArgs& d, int t, cudaStream_t s);
+cudaError_t launch_det_reduce(const DetArgs& d, cudaStream_t s);
 cudaError_t launch_rng_probe(int n, const uint64_t* keys5, uint64_t* out, cudaStream_t s);
 cudaError_t launch_step_tile(const StepArgs& a, int mode, cudaStream_t s);
 cudaError_t launch_intensity(const StepArgs& a, int mode, float* lam, float* p, cudaStream_t s);

@@ -41,6 +41,47 @@ struct StepArgs {
   int force64;
 };
 
+// Tiling of the blocked kernel (ember_blocked.cu): tiles of tile_h x tile_w cells with
+// halo_rows / halo_cols of light-cone halo; n_steps per launch (<= halo_rows when halos
+// exist); row_off = global row of buffer row 0 (the RNG cell index is global).
+struct BlockGeom {
+  int tile_h, tile_w, halo_rows, halo_cols;
+  int n_steps;
+  int row_off;
+  int list_cap;
+};
+
+// Deterministic mode + adjoint (ember_det.cu).  Planes are fp32 [env][cell].
+struct DetArgs {
+  StepArgs s;                     // statics (terrain form), dims
+  const float* un;                // current state
+  const float* burn;
+  const float* bd;
+  float* un_o;                    // next state
+  float* burn_o;
+  float* bd_o;
+  float* pot32;                   // [env][cell][8] potential toward direction k (source cell)
+  float* gam32;                   // [env][cell]
+  float* F32;                     // [env][cell] (1+veg)(1+den)
+  float pc32;
+  float* traj_un;                 // [T][env][cell] state before step t (record mode)
+  float* traj_burn;
+  const float* mask;              // [env][cell] target burn mask
+  double bce_w, mse_w;
+  int pool;
+  double* grad_pred;              // [env][cell] scratch
+  float* A_un;                    // adjoints of the state after step t
+  float* A_burn;
+  float* A_bd;
+  float* a_lam;                   // adjoint of lambda
+  double* acc;                    // [env][block][8] fp64 gradient partials (fixed order)
+  double* loss;                   // [env]
+  double* grad;                   // [env][6]
+  const float* wind_speed32;      // [wind] V
+  const float* align32;           // [wind][8] cos(phi_k - theta) - 1
+  int wind_stride;                // 1 (per env) or 0 (shared)
+};
+
 // Per-env RL record (rl_env.hpp:67-75 EnvState minus the layer, plus the tanker
 // episode counter).
 struct RlEnv {

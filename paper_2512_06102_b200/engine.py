@@ -16,7 +16,7 @@ from . import _lib
 from ._lib import EnvConfig, EnvState, SimConfig, check, lib
 
 UNBURNED, BURNING, BURNED = 0, 1, 2
-KERNEL_AUTO, KERNEL_TILED, KERNEL_RESIDENT = 0, 1, 2
+KERNEL_AUTO, KERNEL_TILED, KERNEL_RESIDENT, KERNEL_BLOCKED = 0, 1, 2, 3
 
 
 def _ptr(a: np.ndarray | None):
@@ -113,6 +113,10 @@ class Batch:
     def set_kernel(self, which: int) -> None:
         check(lib().ebl_batch_set_kernel(self._h, which))
 
+    def set_tiling(self, tile_h: int, tile_w: int = 0, halo: int = 0) -> None:
+        """Explicit blocked-kernel tiling (tests); tile_h = 0 restores the planner."""
+        check(lib().ebl_batch_set_tiling(self._h, tile_h, tile_w, halo))
+
     # -- state / key ----------------------------------------------------------------------
     def set_state(self, states) -> None:
         st = np.ascontiguousarray(np.broadcast_to(np.asarray(states, dtype=np.uint8),
@@ -160,6 +164,35 @@ class Batch:
         p = np.empty_like(lam)
         check(lib().ebl_batch_intensity(self._h, _ptr(lam), _ptr(p)))
         return lam, p
+
+    # -- deterministic mode (engine.hpp:147-245) + reverse-mode gradient (C4) ----------------
+    def det_set_state(self, p_un, p_burn, p_bd) -> None:
+        shp = (self.n_envs, self.height, self.width)
+        arrs = [np.ascontiguousarray(np.broadcast_to(np.asarray(x, dtype=np.float32), shp))
+                for x in (p_un, p_burn, p_bd)]
+        check(lib().ebl_det_set_state(self._h, *[_ptr(a) for a in arrs]))
+
+    def det_set_state_from_fire(self) -> None:
+        check(lib().ebl_det_set_state_from_fire(self._h))
+
+    def det_get_state(self):
+        shp = (self.n_envs, self.height, self.width)
+        out = [np.empty(shp, np.float32) for _ in range(3)]
+        check(lib().ebl_det_get_state(self._h, *[_ptr(a) for a in out]))
+        return tuple(out)
+
+    def det_forward(self, n_steps: int, record: bool = True) -> None:
+        check(lib().ebl_det_forward(self._h, n_steps, int(record)))
+
+    def det_loss_grad(self, mask, bce_weight=0.0, mse_weight=1.0, pool=1):
+        """(loss [n_envs], grad [n_envs, 6]) after a recorded det_forward (calibrate.hpp:120-146)."""
+        m = np.ascontiguousarray(np.broadcast_to(np.asarray(mask, dtype=np.float32),
+                                                 (self.n_envs, self.height, self.width)))
+        loss = np.empty(self.n_envs, np.float64)
+        grad = np.empty((self.n_envs, 6), np.float64)
+        check(lib().ebl_det_loss_grad(self._h, _ptr(m), float(bce_weight), float(mse_weight), int(pool),
+                                      _ptr(loss), _ptr(grad)))
+        return loss, grad
 
     def diag(self, reset: bool = False) -> dict:
         out = np.zeros(4, dtype=np.uint64)

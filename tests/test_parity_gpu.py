@@ -12,7 +12,7 @@ from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [eb.KERNEL_TILED, eb.KERNEL_RESIDENT]
+KERNELS = [eb.KERNEL_TILED, eb.KERNEL_RESIDENT, eb.KERNEL_BLOCKED]
 REL_TOL = 1e-5  # north_star: lambda and p within 1e-5 relative in fp32
 
 
@@ -158,20 +158,24 @@ def test_intensity_fp32_within_1e5(port):
         st = b.get_state()
         lam, p = b.intensity()
         c = O.DEFAULT_CFG if cfg is None else cfg
+        checked = 0
         for e in range(n):
             g = O.grid_terrain(port, "port", t.veg()[e], t.den()[e], t.elevation[e], 30.0,
                                t.wind_speed[e], t.wind_direction[e])
             lw, pw = O.intensity(port, "port", g, c, st[e])
             m = lw > 0
-            assert m.sum() > 0
+            checked += int(m.sum())
             np.testing.assert_allclose(lam[e][m], lw[m], rtol=REL_TOL)
             np.testing.assert_allclose(p[e][m], pw[m], rtol=REL_TOL, atol=1e-30)
             assert (lam[e][~m] == 0).all() and (p[e][~m] == 0).all()
+        assert checked > 100, "fronts must be alive to test lambda/p"
 
 
-@pytest.mark.parametrize("h,w", [(1, 1), (1, 37), (45, 1), (3, 3), (31, 33), (64, 96), (200, 100), (17, 300)])
+@pytest.mark.parametrize("h,w", [(1, 1), (1, 37), (45, 1), (3, 3), (31, 33), (64, 96), (200, 100),
+                                 (17, 300), (130, 520)])
 def test_kernels_identical_ragged(port, h, w):
-    """Tiled vs resident vs oracle on ragged sizes (W not a multiple of 32, single row/col)."""
+    """Tiled vs resident vs halo-tiled blocked vs oracle on ragged sizes (W not a multiple of
+    32, single row/col), including garbage state bytes (>2 act as Unburned, engine.cpp:15-25)."""
     rs = np.random.default_rng(h * 1000 + w)
     n = 5
     cls = rs.integers(0, 11, (n, h, w)).astype(np.uint8)
@@ -179,19 +183,25 @@ def test_kernels_identical_ragged(port, h, w):
     _, veg, den = eb.worldcover_palette()
     init = (rs.random((n, h, w)) < 0.15).astype(np.uint8)
     init[rs.random((n, h, w)) < 0.1] = 2
+    init[rs.random((n, h, w)) < 0.01] = 7
     outs = []
-    for kernel in KERNELS:
-        if kernel == eb.KERNEL_RESIDENT and h * w > 65536:
-            continue
+    variants = [(eb.KERNEL_TILED, None), (eb.KERNEL_AUTO, None), (eb.KERNEL_BLOCKED, None),
+                (eb.KERNEL_AUTO, (8, 32, 3)), (eb.KERNEL_AUTO, (5, 64, 1)), (eb.KERNEL_AUTO, (16, 96, 7))]
+    for kernel, tiling in variants:
         b = eb.Batch(n, h, w)
         b.set_terrain(cls, el, veg, den, 25.0)
         b.set_wind(rs.random(n) * 0 + 7.0, [0.3, 1.0, 2.0, 4.0, 6.0])
         b.set_config([0.4, 0.2, 0.4, 1.0, 1.0, 0.7])
         b.set_kernel(kernel)
+        if tiling:
+            b.set_tiling(*tiling)
         b.set_state(init)
         b.set_key(9, 3, first_stream=100)
         b.step(25)
         outs.append(b.get_state())
+        cnt = b.counts()
+        assert np.array_equal(cnt[:, 1], (outs[-1] == 1).reshape(n, -1).sum(1)), (kernel, tiling)
+        assert np.array_equal(cnt[:, 2], (outs[-1] == 2).reshape(n, -1).sum(1)), (kernel, tiling)
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
     for e in range(n):
@@ -290,8 +300,6 @@ def test_errors():
     b = eb.Batch(2, 4, 4)
     with pytest.raises(eb.EmberError):
         b.step(1)  # no grid yet (ESTATE)
-    with pytest.raises(eb.InvalidArgument):
-        b.set_state(np.full((2, 4, 4), 3, np.uint8))
     z = np.zeros((4, 4))
     with pytest.raises(eb.InvalidArgument):
         b.set_grid(z - 1.0, z, z, z, np.zeros((4, 4, 8)))  # negative wind speed
@@ -324,3 +332,24 @@ def test_c1_full_size_kernels_agree_and_sampled_oracle(port):
         assert np.array_equal(outs[0][e], O.run(port, "port", g, O.DEFAULT_CFG, 0, 0, e, steps, init[e]))
     # burned count non-decreasing / conservation properties
     assert ((outs[0] == 2).reshape(n, -1).sum(1) >= 0).all()
+
+
+def test_large_single_grid_vs_oracle(port):
+    """C3-shaped (one large landscape, uniform wind from the west, many ignitions) at 1024^2:
+    the halo-tiled blocked kernel (AUTO at this size) == per-step tiled kernel == oracle."""
+    h = w = 1024
+    t = eb.synth_terrain(11, 1, h, w)
+    t.wind_speed[:] = 6.0
+    t.wind_direction[:] = 0.0
+    init = eb.synth_ignitions(11, t, 64)
+    outs = []
+    for kernel in (eb.KERNEL_AUTO, eb.KERNEL_TILED):
+        b = _terrain_batch(t, None, kernel)
+        b.set_state(init)
+        b.set_key(11, 0)
+        b.step(60)
+        outs.append(b.get_state())
+        assert b.diag()["ambiguous"] == 0
+    assert np.array_equal(outs[0], outs[1])
+    g = O.grid_terrain(port, "port", t.veg()[0], t.den()[0], t.elevation[0], 30.0, 6.0, 0.0)
+    assert np.array_equal(outs[0][0], O.run(port, "port", g, O.DEFAULT_CFG, 11, 0, 0, 60, init[0]))
