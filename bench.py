@@ -38,6 +38,12 @@ N_ENVS, H, W, CA_STEPS, IGNITIONS, SEED = 1024, 128, 128, 200, 5, 0
 ALG_BYTES_PER_CELL_UPDATE = 10  # 1 B state read + 1 B write + 4 B fuel + 4 B elevation
 
 
+def env_ids(rank: int) -> list:
+    """Global env ids (= RNG streams, = synthetic-terrain keys) of a rank: weak scaling,
+    each rank owns its own N_ENVS envs; no data-path collective."""
+    return list(range(rank * N_ENVS, (rank + 1) * N_ENVS))
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -178,7 +184,7 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    env0 = rank * N_ENVS  # global env ids of this rank (weak scaling)
+    env0 = env_ids(rank)[0]  # global env ids of this rank (weak scaling)
     terrain = eb.synth_terrain(SEED, N_ENVS, H, W, env_id0=env0)
     init = eb.synth_ignitions(SEED, terrain, IGNITIONS, env_id0=env0)
 

@@ -121,6 +121,19 @@ int ebl_batch_set_kernel(ebl_batch* b, int which);
  * 32, `halo` rows of light cone = steps per launch); tile_h == 0 restores planning. */
 int ebl_batch_set_tiling(ebl_batch* b, int tile_h, int tile_w, int halo);
 
+/* ---- row-sharded landscapes (BASELINE C3) ----
+ * A shard's layer holds global rows [row_off, row_off + H): its band plus light-cone halo
+ * rows.  The RNG cell index stays global ((row_off + r) * W + c), so a sharded run is
+ * bit-identical to the unsharded one. */
+int ebl_batch_set_row_offset(ebl_batch* b, int64_t row_off);
+/* Copies rows [src_row, src_row+n) of every member of `src` into rows [dst_row, ...) of `dst`
+ * (same width and member count); batches on different devices copy peer-to-peer over
+ * NVLink (cudaMemcpyPeerAsync) on dst's stream after src's stream has drained. */
+int ebl_batch_copy_rows(ebl_batch* dst, int dst_row, const ebl_batch* src, int src_row, int n_rows);
+/* Rows [row0, row0+n) of every member to (to_batch = 0) or from (1) a device buffer
+ * [n_envs][n][W] (e.g. a torch tensor exchanged with NCCL send/recv between processes). */
+int ebl_batch_rows_device(ebl_batch* b, int row0, int n_rows, void* dptr, int to_batch);
+
 /* fire_fraction_stats (engine.cpp:185-198) as integer counts of the current
  * state, out[e*4 + {0,1,2,3}] = {unburned, burning, burned, newly ignited in the
  * last step}. */
@@ -154,20 +167,21 @@ int ebl_run_stochastic(int height, int width, const uint8_t* initial, const doub
                        uint64_t step, uint64_t stream, int steps, uint8_t* out);
 
 /* ---- deterministic (raw-probability) mode and its gradient (BASELINE C4) -------- */
-/* BasicContinuousState (engine.hpp:27-37) of every env as fp32 planes [n_envs][H*W]. */
-int ebl_det_set_state(ebl_batch* b, const float* p_un, const float* p_burn, const float* p_bd);
+/* BasicContinuousState (engine.hpp:27-37) of every env as fp64 planes [n_envs][H*W]. */
+int ebl_det_set_state(ebl_batch* b, const double* p_un, const double* p_burn, const double* p_bd);
 /* state_from_fire (engine.cpp:42-52) of the batch's current fire layers. */
 int ebl_det_set_state_from_fire(ebl_batch* b);
-int ebl_det_get_state(ebl_batch* b, float* p_un, float* p_burn, float* p_bd);
-/* run_deterministic (engine.hpp:225-245) for n_steps on the terrain statics, fp32 on the
- * device; record = 1 keeps (p_un, p_burn) of every step in HBM for ebl_det_loss_grad. */
+int ebl_det_get_state(ebl_batch* b, double* p_un, double* p_burn, double* p_bd);
+/* run_deterministic (engine.hpp:225-245) for n_steps on the terrain statics, in the
+ * reference's fp64 arithmetic on the device (DESIGN.md §4 explains why not fp32); record = 1
+ * keeps (p_un, p_burn) of every step in HBM for ebl_det_loss_grad. */
 int ebl_det_forward(ebl_batch* b, int n_steps, int record);
 /* loss = bce_w * BCE(clamp(pred)) + mse_w * MSE(avgpool(pred, pool), avgpool(mask, pool)),
  * pred = p_burn + p_bd (calibrate.hpp:86-146), per env, and its gradient with respect to
  * the six SimConfig fields in ParamIndex order (calibrate.hpp:21-28) by reverse mode
  * through the recorded steps (the reference computes it forward-mode with Dual<6>,
  * calibrate.cpp:130-162).  mask [n_envs][H*W]; loss [n_envs]; grad6 [n_envs*6]. */
-int ebl_det_loss_grad(ebl_batch* b, const float* mask, double bce_w, double mse_w, int pool,
+int ebl_det_loss_grad(ebl_batch* b, const double* mask, double bce_w, double mse_w, int pool,
                       double* loss, double* grad6);
 
 /* ---- RL (rl_env.hpp) ---------------------------------------------------------- */

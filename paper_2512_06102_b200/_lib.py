@@ -92,6 +92,9 @@ SIGNATURES = {
     "ebl_step_batch": (_I, [_P, _I]),
     "ebl_batch_set_kernel": (_I, [_P, _I]),
     "ebl_batch_set_tiling": (_I, [_P, _I, _I, _I]),
+    "ebl_batch_set_row_offset": (_I, [_P, C.c_int64]),
+    "ebl_batch_copy_rows": (_I, [_P, _I, _P, _I, _I]),
+    "ebl_batch_rows_device": (_I, [_P, _I, _I, _P, _I]),
     "ebl_batch_counts": (_I, [_P, _P]),
     "ebl_batch_intensity": (_I, [_P, _P, _P]),
     "ebl_batch_diag": (_I, [_P, _P, _I]),

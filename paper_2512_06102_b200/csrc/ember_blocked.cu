@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
 
   const DiagCounters dg{a.diag};
   const uint64_t stream = a.streams[env];
-  const uint64_t gbase = static_cast<uint64_t>(g.row_off + R0) * W + C0;  // RNG index of region (0,0)
+  const uint64_t gbase = static_cast<uint64_t>(a.row_off + R0) * W + C0;  // RNG index of region (0,0)
   const int lane = threadIdx.x & 31;
   // newly-ignited cells are counted only inside the output tile
   const int tr0 = r0 - R0, tr1 = min(r0 + g.tile_h, BH) - R0;

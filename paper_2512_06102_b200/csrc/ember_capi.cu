@@ -77,6 +77,7 @@ struct ebl_batch {
   uint64_t launches = 0, steps_done = 0;
 
   uint64_t seed = 0, step = 0;
+  int64_t row_off = 0;  // global row of layer row 0 (row-sharded landscapes)
   std::vector<uint64_t> h_streams;
   DevBuf<uint64_t> streams;
 
@@ -109,13 +110,17 @@ struct ebl_batch {
   DevBuf<int32_t> actions, error, episodes;
   DevBuf<double> obs;
 
-  // deterministic mode (C4)
-  DevBuf<float> det[6];             // un, burn, bd x2 (double buffer)
+  // deterministic mode (C4), fp64
+  DevBuf<double> det[6];            // un, burn, bd x2 (double buffer)
   int det_cur = 0;
   bool det_ready = false;
-  DevBuf<float> pot32, gam32, F32, traj, adj, mask32, wind32, align32;
-  DevBuf<double> grad_pred, acc, det_loss, det_grad;
-  int traj_steps = 0;               // steps recorded by the last ebl_det_forward(record=1)
+  DevBuf<double> det_pot, det_gam, det_V, det_align, traj, adj, det_mask, acc, det_loss, det_grad;
+  int det_tables = 0;
+  bool det_tables_valid = false;
+  ebl_sim_config det_cfg{};
+  int traj_steps = -1;              // steps recorded by the last ebl_det_forward(record=1)
+  std::vector<uint8_t> h_fuel;      // host copies of the terrain (exact host-built tables)
+  std::vector<float> h_elev;
 };
 
 namespace {
@@ -148,26 +153,28 @@ int prepare(ebl_batch* b) {
   }
   if (b->mode == ebl::kStaticTerrain && b->derived_dirty) {
     if (b->n_winds == 0) return set_err(EBL_ESTATE, "terrain form needs ebl_batch_set_wind");
-    std::vector<float> p32(512, 0.f);
-    std::vector<double> p64(768, 0.0);
+    std::vector<float> p32(768, 0.f);
+    std::vector<double> p64(1024, 0.0);
     for (size_t k = 0; k < b->pal_veg.size(); ++k) {
       const double v = ebl::clamp_fuel(b->pal_veg[k]), d = ebl::clamp_fuel(b->pal_den[k]);
       p64[k] = (c.p_base * (1.0 + v)) * (1.0 + d);            // kernel.hpp:39-40
       p64[256 + k] = (c.alpha_gamma * (1.0 + v)) * (1.0 + d);  // kernel.hpp:75-76
       p64[512 + k] = (1.0 + v) * (1.0 + d) > 0.0 ? 1.0 : 0.0;
+      p64[768 + k] = (1.0 + v) * (1.0 + d);  // F, for the deterministic adjoint
       p32[k] = static_cast<float>(p64[k]);
       p32[256 + k] = static_cast<float>(p64[256 + k]);
+      p32[512 + k] = static_cast<float>((1.0 + v) * (1.0 + d));  // F = (1+veg)(1+den), deterministic adjoint
     }
     std::vector<double> k64(static_cast<size_t>(b->n_winds) * 8);
     std::vector<float> k32(k64.size());
     for (int e = 0; e < b->n_winds; ++e) ebl::kappa_wind8(b->wind_speed[e], b->wind_dir[e], c, &k64[e * 8]);
     for (size_t i = 0; i < k64.size(); ++i) k32[i] = static_cast<float>(k64[i]);
-    EBL_CUDA(b->pal32.alloc(512));
-    EBL_CUDA(b->pal64.alloc(768));
+    EBL_CUDA(b->pal32.alloc(768));
+    EBL_CUDA(b->pal64.alloc(1024));
     EBL_CUDA(b->kw32.alloc(k32.size()));
     EBL_CUDA(b->kw64.alloc(k64.size()));
-    EBL_CUDA(cudaMemcpyAsync(b->pal32.p, p32.data(), 512 * sizeof(float), cudaMemcpyHostToDevice, b->stream));
-    EBL_CUDA(cudaMemcpyAsync(b->pal64.p, p64.data(), 768 * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaMemcpyAsync(b->pal32.p, p32.data(), 768 * sizeof(float), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaMemcpyAsync(b->pal64.p, p64.data(), 1024 * sizeof(double), cudaMemcpyHostToDevice, b->stream));
     EBL_CUDA(cudaMemcpyAsync(b->kw32.p, k32.data(), k32.size() * sizeof(float), cudaMemcpyHostToDevice, b->stream));
     EBL_CUDA(cudaMemcpyAsync(b->kw64.p, k64.data(), k64.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
     EBL_CUDA(cudaStreamSynchronize(b->stream));
@@ -183,6 +190,7 @@ ebl::StepArgs step_args(const ebl_batch* b) {
   a.n_envs = b->n_envs;
   a.seed = b->seed;
   a.step = b->step;
+  a.row_off = b->row_off;
   a.streams = b->streams.p;
   a.pc_thr = ebl::continue_threshold(b->cfg.p_continue);
   a.in = b->state[b->cur].p;
@@ -350,11 +358,14 @@ int ebl_batch_set_terrain(ebl_batch* b, int n_grids, const uint8_t* fuel_class, 
   EBL_CUDA(cudaMemcpyAsync(b->elev.p, elevation, n * sizeof(float), cudaMemcpyHostToDevice, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
   b->pal_veg.assign(class_veg, class_veg + n_classes);
+  b->h_fuel.assign(fuel_class, fuel_class + n);
+  b->h_elev.assign(elevation, elevation + n);
   b->pal_den.assign(class_den, class_den + n_classes);
   b->cellsize = cellsize;
   b->mode = ebl::kStaticTerrain;
   b->n_grids = n_grids;
   b->derived_dirty = true;
+  b->det_tables_valid = false;
   b->pot.reset();
   b->gamma.reset();
   if (b->n_winds == 0) {  // calm air until set
@@ -377,6 +388,7 @@ int ebl_batch_set_wind(ebl_batch* b, int n_winds, const double* speed, const dou
   b->wind_speed.assign(speed, speed + n_winds);
   b->wind_dir.assign(dir, dir + n_winds);
   b->derived_dirty = true;
+  b->det_tables_valid = false;
   return EBL_OK;
 }
 
@@ -484,6 +496,61 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
   }
   b->steps_done += n_steps;
   b->counts_valid = true;
+  return EBL_OK;
+}
+
+int ebl_batch_set_row_offset(ebl_batch* b, int64_t row_off) {
+  if (int e = check_batch(b)) return e;
+  if (row_off < 0) return set_err(EBL_EINVAL, "row offset must be >= 0");
+  b->row_off = row_off;
+  return EBL_OK;
+}
+
+int ebl_batch_copy_rows(ebl_batch* dst, int dst_row, const ebl_batch* src, int src_row, int n_rows) {
+  if (int e = check_batch(dst)) return e;
+  if (int e = check_batch(src)) return e;
+  if (dst->w != src->w || dst->n_envs != src->n_envs) return set_err(EBL_EINVAL, "copy_rows: widths/env counts differ");
+  if (n_rows < 0 || dst_row < 0 || src_row < 0 || dst_row + n_rows > dst->h || src_row + n_rows > src->h)
+    return set_err(EBL_EINVAL, "copy_rows: row range outside a layer");
+  if (n_rows == 0) return EBL_OK;
+  EBL_CUDA(cudaSetDevice(src->device));
+  EBL_CUDA(cudaStreamSynchronize(src->stream));  // src rows final
+  EBL_CUDA(cudaSetDevice(dst->device));
+  if (dst->device != src->device) {  // direct NVLink peer access when the pair supports it
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, dst->device, src->device) == cudaSuccess && can) {
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(src->device, 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) return set_err(EBL_ECUDA, cudaGetErrorString(pe));
+      cudaGetLastError();  // clear "already enabled"
+    }
+  }
+  const size_t bytes = static_cast<size_t>(n_rows) * dst->w;
+  for (int e = 0; e < dst->n_envs; ++e) {
+    uint8_t* d = dst->state[dst->cur].p + e * dst->ncell + static_cast<size_t>(dst_row) * dst->w;
+    const uint8_t* s = src->state[src->cur].p + e * src->ncell + static_cast<size_t>(src_row) * src->w;
+    if (dst->device == src->device) {
+      EBL_CUDA(cudaMemcpyAsync(d, s, bytes, cudaMemcpyDeviceToDevice, dst->stream));
+    } else {  // NVLink peer copy
+      EBL_CUDA(cudaMemcpyPeerAsync(d, dst->device, s, src->device, bytes, dst->stream));
+    }
+  }
+  dst->counts_valid = false;
+  return EBL_OK;
+}
+
+int ebl_batch_rows_device(ebl_batch* b, int row0, int n_rows, void* dptr, int to_batch) {
+  if (int e = check_batch(b)) return e;
+  if (n_rows < 0 || row0 < 0 || row0 + n_rows > b->h) return set_err(EBL_EINVAL, "rows: range outside the layer");
+  EBL_CUDA(cudaSetDevice(b->device));
+  const size_t bytes = static_cast<size_t>(n_rows) * b->w;
+  for (int e = 0; e < b->n_envs; ++e) {
+    uint8_t* layer = b->state[b->cur].p + e * b->ncell + static_cast<size_t>(row0) * b->w;
+    uint8_t* ext = static_cast<uint8_t*>(dptr) + e * bytes;
+    if (to_batch) EBL_CUDA(cudaMemcpyAsync(layer, ext, bytes, cudaMemcpyDeviceToDevice, b->stream));
+    else EBL_CUDA(cudaMemcpyAsync(ext, layer, bytes, cudaMemcpyDeviceToDevice, b->stream));
+  }
+  if (to_batch) b->counts_valid = false;
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
   return EBL_OK;
 }
 
@@ -875,8 +942,6 @@ int det_alloc(ebl_batch* b) {
 ebl::DetArgs det_args(ebl_batch* b) {
   ebl::DetArgs d{};
   d.s = step_args(b);
-  const size_t n = b->ncell * b->n_envs;
-  (void)n;
   const int c = b->det_cur * 3, o = (b->det_cur ^ 1) * 3;
   d.un = b->det[c].p;
   d.burn = b->det[c + 1].p;
@@ -884,30 +949,61 @@ ebl::DetArgs det_args(ebl_batch* b) {
   d.un_o = b->det[o].p;
   d.burn_o = b->det[o + 1].p;
   d.bd_o = b->det[o + 2].p;
-  d.pot32 = b->pot32.p;
-  d.gam32 = b->gam32.p;
-  d.F32 = b->F32.p;
-  d.pc32 = static_cast<float>(b->cfg.p_continue);
-  d.wind_speed32 = b->wind32.p;
-  d.align32 = b->align32.p;
+  d.pot = b->det_pot.p;
+  d.gam = b->det_gam.p;
+  d.tab_stride = b->det_tables > 1 ? b->ncell : 0;
+  d.pc = b->cfg.p_continue;
+  d.V = b->det_V.p;
+  d.align = b->det_align.p;
   d.wind_stride = b->n_winds > 1 ? 1 : 0;
   return d;
 }
+
+// SpreadTables<double> for the deterministic mode, built on the host in the reference's
+// arithmetic (ember_host.cpp) and uploaded; one table per env when grids or winds differ.
+int det_tables(ebl_batch* b) {
+  const ebl::Cfg6 c = cfg6(b->cfg);
+  const int T = (b->n_grids > 1 || b->n_winds > 1) ? b->n_envs : 1;
+  const size_t n = b->ncell;
+  std::vector<double> pot(n * 8 * T), gam(n * T);
+  ebl::build_terrain_tables(T, b->h, b->w, b->h_fuel.data(), b->h_elev.data(), b->n_grids > 1 ? n : 0,
+                            b->pal_veg.data(), b->pal_den.data(), b->cellsize, b->wind_speed.data(),
+                            b->wind_dir.data(), b->n_winds > 1 ? 1 : 0, c, pot.data(), gam.data());
+  std::vector<double> V(b->n_winds), al(static_cast<size_t>(b->n_winds) * 8);
+  for (int w = 0; w < b->n_winds; ++w) {  // kernel.hpp:24: cos(phi_k - theta) - 1
+    V[w] = b->wind_speed[w];
+    const double dir = ebl::wrap_angle(b->wind_dir[w]);
+    for (int k = 0; k < 8; ++k) al[w * 8 + k] = std::cos(ebl::offset_angle(k) - dir) - 1.0;
+  }
+  EBL_CUDA(b->det_pot.alloc(pot.size()));
+  EBL_CUDA(b->det_gam.alloc(gam.size()));
+  EBL_CUDA(b->det_V.alloc(V.size()));
+  EBL_CUDA(b->det_align.alloc(al.size()));
+  EBL_CUDA(cudaMemcpyAsync(b->det_pot.p, pot.data(), pot.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(b->det_gam.p, gam.data(), gam.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(b->det_V.p, V.data(), V.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(b->det_align.p, al.data(), al.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  b->det_tables = T;
+  std::memcpy(&b->det_cfg, &b->cfg, sizeof b->cfg);
+  b->det_tables_valid = true;
+  return EBL_OK;
+}
 }  // namespace
 
-int ebl_det_set_state(ebl_batch* b, const float* un, const float* burn, const float* bd) {
+int ebl_det_set_state(ebl_batch* b, const double* un, const double* burn, const double* bd) {
   if (int e = check_batch(b)) return e;
   if (!un || !burn || !bd) return set_err(EBL_EINVAL, "null plane");
   EBL_CUDA(cudaSetDevice(b->device));
   if (int e = det_alloc(b)) return e;
-  const size_t bytes = b->ncell * b->n_envs * sizeof(float);
+  const size_t bytes = b->ncell * b->n_envs * sizeof(double);
   const int c = b->det_cur * 3;
   EBL_CUDA(cudaMemcpyAsync(b->det[c].p, un, bytes, cudaMemcpyHostToDevice, b->stream));
   EBL_CUDA(cudaMemcpyAsync(b->det[c + 1].p, burn, bytes, cudaMemcpyHostToDevice, b->stream));
   EBL_CUDA(cudaMemcpyAsync(b->det[c + 2].p, bd, bytes, cudaMemcpyHostToDevice, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
   b->det_ready = true;
-  b->traj_steps = 0;
+  b->traj_steps = -1;
   return EBL_OK;
 }
 
@@ -916,19 +1012,19 @@ int ebl_det_set_state_from_fire(ebl_batch* b) {  // state_from_fire (engine.cpp:
   const size_t n = b->ncell * b->n_envs;
   std::vector<uint8_t> st(n);
   if (int e = ebl_batch_get_state(b, st.data())) return e;
-  std::vector<float> un(n), bu(n), bd(n);
+  std::vector<double> un(n), bu(n), bd(n);
   for (size_t i = 0; i < n; ++i) {
-    un[i] = st[i] == 0 ? 1.f : 0.f;
-    bu[i] = st[i] == 1 ? 1.f : 0.f;
-    bd[i] = st[i] == 2 ? 1.f : 0.f;
+    un[i] = st[i] == 0 ? 1.0 : 0.0;
+    bu[i] = st[i] == 1 ? 1.0 : 0.0;
+    bd[i] = st[i] == 2 ? 1.0 : 0.0;
   }
   return ebl_det_set_state(b, un.data(), bu.data(), bd.data());
 }
 
-int ebl_det_get_state(ebl_batch* b, float* un, float* burn, float* bd) {
+int ebl_det_get_state(ebl_batch* b, double* un, double* burn, double* bd) {
   if (int e = check_batch(b)) return e;
   if (!b->det_ready) return set_err(EBL_ESTATE, "ebl_det_set_state first");
-  const size_t bytes = b->ncell * b->n_envs * sizeof(float);
+  const size_t bytes = b->ncell * b->n_envs * sizeof(double);
   const int c = b->det_cur * 3;
   if (un) EBL_CUDA(cudaMemcpyAsync(un, b->det[c].p, bytes, cudaMemcpyDeviceToHost, b->stream));
   if (burn) EBL_CUDA(cudaMemcpyAsync(burn, b->det[c + 1].p, bytes, cudaMemcpyDeviceToHost, b->stream));
@@ -944,28 +1040,12 @@ int ebl_det_forward(ebl_batch* b, int n_steps, int record) {
     return set_err(EBL_EINVAL, "deterministic mode runs on the terrain form (ebl_batch_set_terrain)");
   if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
   if (int e = prepare(b)) return e;
+  if (!b->det_tables_valid || std::memcmp(&b->det_cfg, &b->cfg, sizeof b->cfg) != 0)
+    if (int e = det_tables(b)) return e;
   const size_t n = b->ncell * b->n_envs;
-  EBL_CUDA(b->pot32.alloc(n * 8));
-  EBL_CUDA(b->gam32.alloc(n));
-  EBL_CUDA(b->F32.alloc(n));
-  {  // per wind set: V and cos(phi_k - theta) - 1 (kernel.hpp:24)
-    std::vector<float> v(b->n_winds), al(static_cast<size_t>(b->n_winds) * 8);
-    for (int w = 0; w < b->n_winds; ++w) {
-      v[w] = static_cast<float>(b->wind_speed[w]);
-      const double dir = ebl::wrap_angle(b->wind_dir[w]);
-      for (int k = 0; k < 8; ++k) al[w * 8 + k] = static_cast<float>(std::cos(ebl::offset_angle(k) - dir) - 1.0);
-    }
-    EBL_CUDA(b->wind32.alloc(v.size()));
-    EBL_CUDA(b->align32.alloc(al.size()));
-    EBL_CUDA(cudaMemcpyAsync(b->wind32.p, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice, b->stream));
-    EBL_CUDA(cudaMemcpyAsync(b->align32.p, al.data(), al.size() * sizeof(float), cudaMemcpyHostToDevice, b->stream));
-  }
   if (record) EBL_CUDA(b->traj.alloc(2 * n * std::max(1, n_steps)));
-  ebl::DetArgs d = det_args(b);
-  EBL_CUDA(ebl::launch_det_tables(d, b->stream));
-  b->launches += 1;
   for (int t = 0; t < n_steps; ++t) {
-    d = det_args(b);
+    ebl::DetArgs d = det_args(b);
     if (record) {
       d.traj_un = b->traj.p;
       d.traj_burn = b->traj.p + n * n_steps;
@@ -979,7 +1059,7 @@ int ebl_det_forward(ebl_batch* b, int n_steps, int record) {
   return EBL_OK;
 }
 
-int ebl_det_loss_grad(ebl_batch* b, const float* mask, double bce_w, double mse_w, int pool,
+int ebl_det_loss_grad(ebl_batch* b, const double* mask, double bce_w, double mse_w, int pool,
                       double* loss, double* grad6) {
   if (int e = check_batch(b)) return e;
   if (b->traj_steps < 0 || !b->det_ready)
@@ -988,20 +1068,18 @@ int ebl_det_loss_grad(ebl_batch* b, const float* mask, double bce_w, double mse_
     return set_err(EBL_EINVAL, "LossConfig: weights >= 0, one positive, pool_size >= 1");
   const size_t n = b->ncell * b->n_envs;
   const int bpe = static_cast<int>((b->ncell + 255) / 256);
-  EBL_CUDA(b->mask32.alloc(n));
+  EBL_CUDA(b->det_mask.alloc(n));
   EBL_CUDA(b->adj.alloc(4 * n));
-  EBL_CUDA(b->grad_pred.alloc(n));
   EBL_CUDA(b->acc.alloc(static_cast<size_t>(b->n_envs) * bpe * 8));
   EBL_CUDA(b->det_loss.alloc(b->n_envs));
   EBL_CUDA(b->det_grad.alloc(static_cast<size_t>(b->n_envs) * 6));
-  EBL_CUDA(cudaMemcpyAsync(b->mask32.p, mask, n * sizeof(float), cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(b->det_mask.p, mask, n * sizeof(double), cudaMemcpyHostToDevice, b->stream));
   EBL_CUDA(cudaMemsetAsync(b->acc.p, 0, static_cast<size_t>(b->n_envs) * bpe * 8 * sizeof(double), b->stream));
   ebl::DetArgs d = det_args(b);
-  d.mask = b->mask32.p;
+  d.mask = b->det_mask.p;
   d.bce_w = bce_w;
   d.mse_w = mse_w;
   d.pool = pool;
-  d.grad_pred = b->grad_pred.p;
   d.A_un = b->adj.p;
   d.A_burn = b->adj.p + n;
   d.A_bd = b->adj.p + 2 * n;

@@ -142,9 +142,14 @@ __device__ __forceinline__ bool ignite_terrain(const TerrainView& t, int w, int 
   const double u = bits_to_uniform(m);
   if (!t.force64) {
     const float lam = terrain_lambda32(t, w, r, c, nb);
-    const double p32 = static_cast<double>(-expm1f(-t.pal_gam32[t.fuel[r * w + c]] * lam));
-    if (u < p32 * (1.0 - kGuardRel)) return true;
-    if (u >= p32 * (1.0 + kGuardRel) + 1e-37) return false;
+    const float x = t.pal_gam32[t.fuel[r * w + c]] * lam;
+    if (x == 0.f) return false;  // gamma or lambda exactly 0: p = 1 - exp(-0) = 0, u < 0 is false
+    const double p32 = static_cast<double>(-expm1f(-x));
+    // tiny p: the reference's 1 - exp(-x) is quantised to multiples of 2^-53 there; decide in fp64
+    if (p32 > 1e-12) {
+      if (u < p32 * (1.0 - kGuardRel)) return true;
+      if (u >= p32 * (1.0 + kGuardRel)) return false;
+    }
   }
   dg.fallback();
   const double p = terrain_p64(t, w, r, c, nb);

@@ -78,6 +78,38 @@ void build_tables(size_t n, const double* speed, const double* dir, const double
   }
 }
 
+void build_terrain_tables(int n_tables, int h, int w, const uint8_t* fuel, const float* elev,
+                          size_t grid_stride, const double* class_veg, const double* class_den,
+                          double cellsize, const double* wind_speed, const double* wind_dir,
+                          int wind_stride, const Cfg6& c, double* pot, double* gamma) {
+  const size_t n = static_cast<size_t>(h) * w;
+  const double dist[2] = {cellsize * 1.0, cellsize * 1.41421356237309504880};  // geodata.cpp:222-223
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int t = 0; t < n_tables; ++t) {
+    const uint8_t* f = fuel + t * grid_stride;
+    const float* z = elev + t * grid_stride;
+    double kw[8];
+    kappa_wind8(wind_speed[t * wind_stride], wind_dir[t * wind_stride], c, kw);
+    double* P = pot + t * n * 8;
+    double* G = gamma + t * n;
+    for (int r = 0; r < h; ++r)
+      for (int col = 0; col < w; ++col) {
+        const size_t i = static_cast<size_t>(r) * w + col;
+        const double v = clamp_fuel(class_veg[f[i]]), d = clamp_fuel(class_den[f[i]]);
+        const double source = (c.p_base * (1.0 + v)) * (1.0 + d);  // engine.hpp:88
+        G[i] = (c.alpha_gamma * (1.0 + v)) * (1.0 + d);           // engine.hpp:89
+        for (int k = 0; k < 8; ++k) {
+          const int nr = r + kDy[k], nc = col + kDx[k];
+          double s = 0.0;  // slope_from_dem: 0 toward out-of-bounds neighbours
+          if (nr >= 0 && nr < h && nc >= 0 && nc < w)
+            s = std::atan((static_cast<double>(z[static_cast<size_t>(nr) * w + nc]) - static_cast<double>(z[i])) /
+                          dist[k & 1]);
+          P[i * 8 + k] = (source * kw[k]) * std::exp(c.alpha_s * s);  // engine.hpp:91,106-107
+        }
+      }
+  }
+}
+
 uint64_t continue_threshold(double pc) {
   if (!(pc > 0.0)) return 0;  // also NaN: u < NaN is false
   if (pc >= 1.0) return 1ull << 53;

@@ -20,6 +20,13 @@ void kappa_wind8(double speed, double direction, const Cfg6& c, double kw[8]);
 void build_tables(size_t n, const double* speed, const double* dir, const double* veg,
                   const double* den, const double* slope8, const Cfg6& c, double* pot,
                   double* gamma);
+// SpreadTables<double> of terrain-form statics (slope_from_dem of the fp32 elevation, palette
+// fuel, uniform wind per table): pot [n_tables][h*w][8], gamma [n_tables][h*w].  Table t uses
+// grid t*grid_stride (stride 0: shared) and wind t*wind_stride.
+void build_terrain_tables(int n_tables, int h, int w, const uint8_t* fuel, const float* elev,
+                          size_t grid_stride, const double* class_veg, const double* class_den,
+                          double cellsize, const double* wind_speed, const double* wind_dir,
+                          int wind_stride, const Cfg6& c, double* pot, double* gamma);
 // ceil(p_continue * 2^53): a Burning cell survives iff (word >> 11) < this.
 uint64_t continue_threshold(double p_continue);
 

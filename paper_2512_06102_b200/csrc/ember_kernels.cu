@@ -72,14 +72,14 @@ __global__ void __launch_bounds__(kTileThreads) k_step_tile(StepArgs a) {
     const uint8_t s = tile[lr + 1][lc + 1];
     uint8_t ns = 2;
     if (s == 1) {
-      ns = cell_bits53(prefix, static_cast<uint64_t>(r) * W + c, 0) < a.pc_thr ? 1 : 2;
+      ns = cell_bits53(prefix, static_cast<uint64_t>(a.row_off + r) * W + c, 0) < a.pc_thr ? 1 : 2;
     } else if (s != 2) {  // any other byte takes the Unburned path (engine.cpp:15-25)
       uint32_t nb = 0;
 #pragma unroll
       for (int k = 0; k < 8; ++k) nb |= static_cast<uint32_t>(tile[lr + 1 - kDy[k]][lc + 1 - kDx[k]] == 1) << k;
       ns = 0;
       if (nb) {
-        const uint64_t m = cell_bits53(prefix, static_cast<uint64_t>(r) * W + c, 0);
+        const uint64_t m = cell_bits53(prefix, static_cast<uint64_t>(a.row_off + r) * W + c, 0);
         ns = ignite<MODE>(a, env, r, c, nb, m, dg) ? 1 : 0;
         nNew += ns;
       }

@@ -22,7 +22,6 @@ bool resident_fits(int h, int w);
 BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_off);
 cudaError_t launch_step_blocked(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s);
 
-cudaError_t launch_det_tables(const DetArgs& d, cudaStream_t s);
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s);
 cudaError_t launch_det_loss(const DetArgs& d, cudaStream_t s);
 cudaError_t launch_det_backward(const DetArgs& d, int t, cudaStream_t s);

@@ -15,6 +15,7 @@ struct StepArgs {
   int h, w, n_envs;
   uint64_t seed;
   uint64_t step;                  // lockstep step index t (RngKey::step)
+  long long row_off;              // global row of layer row 0 (row shards): RNG cell = (row_off+r)*W+c
   const uint64_t* streams;        // [n_envs] Member::stream
   uint64_t pc_thr;                // Burning survives iff (word>>11) < pc_thr (= ceil(p_continue*2^53))
   const uint8_t* in;              // [n_envs][h*w]
@@ -51,34 +52,34 @@ struct BlockGeom {
   int list_cap;
 };
 
-// Deterministic mode + adjoint (ember_det.cu).  Planes are fp32 [env][cell].
+// Deterministic mode + adjoint (ember_det.cu).  fp64 planes [env][cell] (the
+// reference's trajectory is ulp-sensitive, so parity needs its exact fp64 arithmetic).
 struct DetArgs {
   StepArgs s;                     // statics (terrain form), dims
-  const float* un;                // current state
-  const float* burn;
-  const float* bd;
-  float* un_o;                    // next state
-  float* burn_o;
-  float* bd_o;
-  float* pot32;                   // [env][cell][8] potential toward direction k (source cell)
-  float* gam32;                   // [env][cell]
-  float* F32;                     // [env][cell] (1+veg)(1+den)
-  float pc32;
-  float* traj_un;                 // [T][env][cell] state before step t (record mode)
-  float* traj_burn;
-  const float* mask;              // [env][cell] target burn mask
+  const double* un;               // current state
+  const double* burn;
+  const double* bd;
+  double* un_o;                   // next state
+  double* burn_o;
+  double* bd_o;
+  const double* pot;              // [table][cell][8] SpreadTables<double>::pot (host-built, exact)
+  const double* gam;              // [table][cell]
+  size_t tab_stride;              // cells per table (0: one table for all envs)
+  double pc;
+  double* traj_un;                // [T][env][cell] state before step t (record mode)
+  double* traj_burn;
+  const double* mask;             // [env][cell] target burn mask
   double bce_w, mse_w;
   int pool;
-  double* grad_pred;              // [env][cell] scratch
-  float* A_un;                    // adjoints of the state after step t
-  float* A_burn;
-  float* A_bd;
-  float* a_lam;                   // adjoint of lambda
-  double* acc;                    // [env][block][8] fp64 gradient partials (fixed order)
+  double* A_un;                   // adjoints of the state after step t
+  double* A_burn;
+  double* A_bd;
+  double* a_lam;                  // adjoint of lambda
+  double* acc;                    // [env][block][8] gradient partials (fixed order)
   double* loss;                   // [env]
   double* grad;                   // [env][6]
-  const float* wind_speed32;      // [wind] V
-  const float* align32;           // [wind][8] cos(phi_k - theta) - 1
+  const double* V;                // [wind] wind speed
+  const double* align;            // [wind][8] cos(phi_k - theta) - 1
   int wind_stride;                // 1 (per env) or 0 (shared)
 };
 

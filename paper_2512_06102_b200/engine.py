@@ -168,7 +168,7 @@ class Batch:
     # -- deterministic mode (engine.hpp:147-245) + reverse-mode gradient (C4) ----------------
     def det_set_state(self, p_un, p_burn, p_bd) -> None:
         shp = (self.n_envs, self.height, self.width)
-        arrs = [np.ascontiguousarray(np.broadcast_to(np.asarray(x, dtype=np.float32), shp))
+        arrs = [np.ascontiguousarray(np.broadcast_to(np.asarray(x, dtype=np.float64), shp))
                 for x in (p_un, p_burn, p_bd)]
         check(lib().ebl_det_set_state(self._h, *[_ptr(a) for a in arrs]))
 
@@ -177,7 +177,7 @@ class Batch:
 
     def det_get_state(self):
         shp = (self.n_envs, self.height, self.width)
-        out = [np.empty(shp, np.float32) for _ in range(3)]
+        out = [np.empty(shp, np.float64) for _ in range(3)]
         check(lib().ebl_det_get_state(self._h, *[_ptr(a) for a in out]))
         return tuple(out)
 
@@ -186,7 +186,7 @@ class Batch:
 
     def det_loss_grad(self, mask, bce_weight=0.0, mse_weight=1.0, pool=1):
         """(loss [n_envs], grad [n_envs, 6]) after a recorded det_forward (calibrate.hpp:120-146)."""
-        m = np.ascontiguousarray(np.broadcast_to(np.asarray(mask, dtype=np.float32),
+        m = np.ascontiguousarray(np.broadcast_to(np.asarray(mask, dtype=np.float64),
                                                  (self.n_envs, self.height, self.width)))
         loss = np.empty(self.n_envs, np.float64)
         grad = np.empty((self.n_envs, 6), np.float64)

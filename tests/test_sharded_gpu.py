@@ -1,0 +1,50 @@
+"""C3 path: one landscape row-sharded into G shards with light-cone halos (here G shards on
+device 0; on G GPUs the halo copies go peer-to-peer) is bit-identical to the unsharded run
+and to the oracle, because the RNG cell index stays global (engine.cpp:17)."""
+import numpy as np
+import pytest
+
+import paper_2512_06102_b200 as eb
+from oracle import oracle as O
+from paper_2512_06102_b200.sharded import ShardedLandscape
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("g,halo", [(1, 8), (2, 8), (3, 4), (4, 8), (5, 2)])
+def test_sharded_equals_unsharded(port, g, halo):
+    h, w, steps, seed = 300, 200, 45, 3
+    t = eb.synth_terrain(seed, 1, h, w)
+    t.wind_speed[:] = 6.0
+    t.wind_direction[:] = 0.0  # "from the west": pushes east (kernel.hpp:24)
+    init = eb.synth_ignitions(seed, t, 16)
+    full = eb.Batch(1, h, w)
+    full.set_terrain(t.fuel_class, t.elevation, t.class_veg, t.class_den, 30.0)
+    full.set_wind(t.wind_speed, t.wind_direction)
+    full.set_state(init)
+    full.set_key(seed, 0, first_stream=0)
+    full.step(steps)
+    want = full.get_state()[0]
+    sh = ShardedLandscape(t, g, halo=halo)
+    sh.set_state(init[0])
+    sh.set_key(seed, 0, 0)
+    sh.step(steps)
+    got = sh.get_state()
+    assert np.array_equal(got, want), np.argwhere(got != want)[:5]
+    gp = O.grid_terrain(port, "port", t.veg()[0], t.den()[0], t.elevation[0], 30.0, 6.0, 0.0)
+    assert np.array_equal(want, O.run(port, "port", gp, O.DEFAULT_CFG, seed, 0, 0, steps, init[0]))
+
+
+def test_rows_device_roundtrip():
+    import torch
+    b = eb.Batch(2, 40, 64)
+    rs = np.random.default_rng(0)
+    st = rs.integers(0, 3, (2, 40, 64)).astype(np.uint8)
+    b.set_state(st)
+    buf = torch.empty((2, 5, 64), dtype=torch.uint8, device="cuda:0")
+    eb._lib.check(eb.lib().ebl_batch_rows_device(b.handle, 10, 5, buf.data_ptr(), 0))
+    assert np.array_equal(buf.cpu().numpy(), st[:, 10:15])
+    buf.fill_(2)
+    eb._lib.check(eb.lib().ebl_batch_rows_device(b.handle, 30, 5, buf.data_ptr(), 1))
+    st[:, 30:35] = 2
+    assert np.array_equal(b.get_state(), st)
