@@ -27,50 +27,13 @@
 
 #include <cstdint>
 
+#include "ember_bits.cuh"
 #include "ember_device.cuh"
 #include "ember_kernels.h"
 #include "ember_params.h"
 
 namespace ebl {
 
-namespace {
-
-__device__ __forceinline__ uint32_t west_of(const uint32_t* row, int j) {
-  return (row[j] << 1) | (j > 0 ? row[j - 1] >> 31 : 0u);  // bit c <- cell c-1
-}
-
-__device__ __forceinline__ uint32_t east_of(const uint32_t* row, int j, int wpr) {
-  return (row[j] >> 1) | (j + 1 < wpr ? row[j + 1] << 31 : 0u);  // bit c <- cell c+1
-}
-
-__device__ __forceinline__ uint32_t low_mask(int n) {
-  return n >= 32 ? 0xffffffffu : (n <= 0 ? 0u : ((1u << n) - 1u));
-}
-
-// Iterates this thread's words idx = tid, tid+T, ... of an [rows][wpr] plane with the
-// (row, word) pair maintained incrementally (no division in the loop).
-struct WordIter {
-  int idx, r, j, dr, dj, wpr, n;
-  __device__ __forceinline__ WordIter(int wpr_, int n_) : wpr(wpr_), n(n_) {
-    idx = threadIdx.x;
-    r = idx / wpr;
-    j = idx - r * wpr;
-    dr = blockDim.x / wpr;
-    dj = blockDim.x - dr * wpr;
-  }
-  __device__ __forceinline__ bool ok() const { return idx < n; }
-  __device__ __forceinline__ void next() {
-    idx += blockDim.x;
-    r += dr;
-    j += dj;
-    if (j >= wpr) {
-      j -= wpr;
-      ++r;
-    }
-  }
-};
-
-}  // namespace
 
 template <int MODE>
 __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, BlockGeom g) {

@@ -692,6 +692,14 @@ int validate_env(const ebl_env_config* c) {  // rl_env.cpp:80-93
   return EBL_OK;
 }
 
+// Tanker step/rollout: the bit-plane kernel, or the byte kernel when EBL_KERNEL_TILED is
+// selected (an independent implementation kept for cross-checking).
+cudaError_t tanker_launch(ebl_batch* b, const ebl::RlArgs& g) {
+  if (b->kernel != EBL_KERNEL_TILED && ebl::rl_bits_fits(b->h, b->w))
+    return ebl::launch_rl_tanker_bits(g, b->mode, b->stream);
+  return ebl::launch_rl_tanker(g, b->mode, b->stream);
+}
+
 ebl::RlArgs rl_args(ebl_batch* b) {
   ebl::RlArgs g{};
   g.s = step_args(b);
@@ -837,7 +845,7 @@ int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* d
   if (b->rl_variant == EBL_RL_REFERENCE) {
     EBL_CUDA(ebl::launch_rl_ref_step(g, b->mode, b->stream));
   } else {
-    EBL_CUDA(ebl::launch_rl_tanker(g, b->mode, b->stream));
+    EBL_CUDA(tanker_launch(b, g));
   }
   b->launches += 1;
   b->steps_done += 1;
@@ -872,7 +880,7 @@ int ebl_rl_rollout(ebl_batch* b, int n_steps, double* reward_sum, int32_t* episo
   g.n_steps = n_steps;
   g.reward_sum = b->reward_sum.p;
   g.episodes = b->episodes.p;
-  EBL_CUDA(ebl::launch_rl_tanker(g, b->mode, b->stream));
+  EBL_CUDA(tanker_launch(b, g));
   b->launches += 1;
   b->steps_done += n_steps;
   b->counts_valid = false;

@@ -34,6 +34,10 @@ cudaError_t launch_rl_ref_step(const RlArgs& g, int mode, cudaStream_t s);
 cudaError_t launch_rl_observe(const uint8_t* state, const RlEnv* envs, int n_envs, int h, int w,
                               int radius, int capacity, double* obs, cudaStream_t s);
 cudaError_t launch_rl_tanker(const RlArgs& g, int mode, cudaStream_t s);
+constexpr int kRlBitsThreads = 128;  // bit-plane tanker kernel: one CTA per env
+size_t rl_bits_smem_bytes(int h, int w);
+bool rl_bits_fits(int h, int w);
+cudaError_t launch_rl_tanker_bits(const RlArgs& g, int mode, cudaStream_t s);
 cudaError_t launch_rl_tanker_reset(const RlArgs& g, int mode, const uint8_t* mask, cudaStream_t s);
 
 }  // namespace ebl

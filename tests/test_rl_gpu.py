@@ -118,12 +118,14 @@ def _port_tanker(port, t: eb.Terrain, cfg, seed, env_ids, n_steps, tc, actions=N
     return out
 
 
+@pytest.mark.parametrize("kernel", [eb.KERNEL_AUTO, eb.KERNEL_TILED])  # bit-plane / byte kernel
 @pytest.mark.parametrize("fused", [False, True])
-def test_tanker_vs_port(port, fused):
+def test_tanker_vs_port(port, fused, kernel):
     n, h, w, seed, steps = 24, 64, 64, 7, 300
     t = eb.synth_terrain(seed, n, h, w)
     cfg = [0.12, 0.2, 0.4, 1.0, 1.0, 0.6]
     env = eb.VecFireEnv(n, variant=eb.RL_TANKER, terrain=t, sim_cfg=cfg, ignitions=5, max_steps=256)
+    env.batch.set_kernel(kernel)
     env.reset(seed)
     tc = O.TankerCfg(5, 256, 1)
     want = _port_tanker(port, t, cfg, seed, list(range(n)), steps, tc)
@@ -147,10 +149,13 @@ def test_tanker_vs_port(port, fused):
     assert sum(sum(x["dones"]) for x in want) > 0, "test should cover auto-reset"
 
 
-def test_tanker_host_actions(port):
-    n, h, w, seed, steps = 8, 32, 48, 3, 40
+@pytest.mark.parametrize("kernel,h,w", [(eb.KERNEL_AUTO, 32, 48), (eb.KERNEL_TILED, 32, 48),
+                                          (eb.KERNEL_AUTO, 17, 45)])
+def test_tanker_host_actions(port, kernel, h, w):
+    n, seed, steps = 8, 3, 40
     t = eb.synth_terrain(seed, n, h, w)
     env = eb.VecFireEnv(n, variant=eb.RL_TANKER, terrain=t, sim_cfg=None, ignitions=3, max_steps=256)
+    env.batch.set_kernel(kernel)
     env.reset(seed)
     rs = np.random.default_rng(1)
     acts = rs.integers(0, h * w, (steps, n)).astype(np.int32)
