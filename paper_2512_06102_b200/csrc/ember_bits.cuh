@@ -41,6 +41,10 @@ struct WordIter {
 };
 
 
+// Row stride (words) of a bit-plane with wpr words per row: odd, so the 32 lanes of a warp
+// each reading "its" row at the same column hit 32 distinct shared-memory banks.
+__host__ __device__ __forceinline__ int plane_stride(int wpr) { return wpr | 1; }
+
 // 32 uint8 cells (two 16-byte loads) -> Burning / Burned bits.  Bytes other than 1/2 act as
 // Unburned exactly as in next_fire_cell (engine.cpp:15-25).
 __device__ __forceinline__ void bytes_to_bits(const uint8_t* src, uint32_t& b, uint32_t& x) {

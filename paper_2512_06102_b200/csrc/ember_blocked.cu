@@ -49,15 +49,15 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
   const int C0 = max(0, c0 - g.halo_cols), C1 = min(W, c0 + g.tile_w + g.halo_cols);
   const int RH = R1 - R0, RW = C1 - C0;
   const int wpr = (RW + 31) >> 5;
-  const int nwords = RH * wpr;
-  const int pw = (RH + 2) * wpr;
+  const int S = plane_stride(wpr);  // odd row stride: a warp's 32 rows hit 32 distinct banks
   uint32_t* Bp[2];
   Bp[0] = reinterpret_cast<uint32_t*>(smem);
-  Bp[1] = Bp[0] + pw;
-  uint32_t* X = Bp[1] + pw;
-  uint32_t* ACT = X + nwords;
-  uint16_t* list = reinterpret_cast<uint16_t*>(ACT + nwords);
+  Bp[1] = Bp[0] + (RH + 2) * S;
+  uint32_t* X = Bp[1] + (RH + 2) * S;
+  uint32_t* ACT = X + RH * S;
+  uint16_t* list = reinterpret_cast<uint16_t*>(ACT + RH * S);
   const int cap = g.list_cap;
+  const uint32_t last_mask = low_mask(RW - 32 * (wpr - 1));
 
   const size_t ncell = static_cast<size_t>(BH) * W;
   const uint8_t* __restrict__ in = a.in + env * ncell;
@@ -66,34 +66,19 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
   // ---- load: uint8 layer -> bit-planes ------------------------------------------------
   for (int i = threadIdx.x; i < wpr; i += blockDim.x) {  // zero padding rows of both buffers
     Bp[0][i] = Bp[1][i] = 0u;
-    Bp[0][(RH + 1) * wpr + i] = Bp[1][(RH + 1) * wpr + i] = 0u;
+    Bp[0][(RH + 1) * S + i] = Bp[1][(RH + 1) * S + i] = 0u;
   }
   if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
   if (threadIdx.x < 2) {
     s_total[threadIdx.x] = 0;
     s_newly[threadIdx.x] = 0;
   }
-  for (WordIter it(wpr, nwords); it.ok(); it.next()) {
+  for (WordIter it(wpr, RH * wpr); it.ok(); it.next()) {
     const int nc = min(32, RW - 32 * it.j);
     const uint8_t* src = in + static_cast<size_t>(R0 + it.r) * W + C0 + 32 * it.j;
     uint32_t b = 0u, x = 0u;
     if (nc == 32 && vec) {
-      const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(src));
-      const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
-      const uint32_t wds[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        // byte k of wds[q] is cell 4q+k; bit0 = Burning (1), bit1 = Burned (2); other byte
-        // values act as Unburned exactly as in next_fire_cell (engine.cpp:15-25)
-        const uint32_t v = wds[q];
-        const uint32_t z = v & 0xFCFCFCFCu;  // per byte: nonzero iff value >= 4
-        const uint32_t small = ~((((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) >> 7) & 0x01010101u;
-        const uint32_t b0 = v & 0x01010101u, b1 = (v >> 1) & 0x01010101u;
-        const uint32_t lo = b0 & ~b1 & small;  // byte == 1
-        const uint32_t hi = b1 & ~b0 & small;  // byte == 2
-        b |= ((lo * 0x01020408u) >> 24 & 0xfu) << (4 * q);  // gather bytes' bit0 -> 4 bits
-        x |= ((hi * 0x01020408u) >> 24 & 0xfu) << (4 * q);
-      }
+      bytes_to_bits(src, b, x);
     } else {
       for (int k = 0; k < nc; ++k) {
         const uint8_t v = src[k];
@@ -101,9 +86,8 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
         x |= static_cast<uint32_t>(v == 2) << k;
       }
     }
-    Bp[0][(it.r + 1) * wpr + it.j] = b;
-    X[it.idx] = x;
-    ACT[it.idx] = 0u;
+    Bp[0][(it.r + 1) * S + it.j] = b;
+    X[it.r * S + it.j] = x;
   }
   __syncthreads();
 
@@ -125,21 +109,41 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
       s_newly[par ^ 1] = 0;
     }
     const uint64_t prefix = key_prefix(a.seed, stream, a.step + static_cast<uint64_t>(t));
-    // ---- P1: dilation, copy B -> Bn, active words -> ACT ----------------------------------
+    // ---- P1: each thread owns whole rows; the 3x3 dilation slides along the row in
+    //      registers (3 shared loads per word: north, own, south) ------------------------------
     int cnt = 0;
     bool ovf = false;
-    for (WordIter it(wpr, nwords); it.ok(); it.next()) {
-      const int j = it.j;
-      const uint32_t* up = B + (it.r + 2) * wpr;
-      const uint32_t* mid = B + (it.r + 1) * wpr;
-      const uint32_t* dn = B + it.r * wpr;
-      const uint32_t any = up[j] | west_of(up, j) | east_of(up, j, wpr) | dn[j] | west_of(dn, j) |
-                           east_of(dn, j, wpr) | west_of(mid, j) | east_of(mid, j, wpr);
-      const uint32_t b = mid[j];
-      Bn[(it.r + 1) * wpr + j] = b;
-      const uint32_t act = ((~(b | X[it.idx]) & low_mask(RW - 32 * j)) & any) | b;
-      ACT[it.idx] = act;
-      cnt += __popc(act);
+    for (int r = threadIdx.x; r < RH; r += blockDim.x) {
+      const uint32_t* up = B + (r + 2) * S;
+      const uint32_t* mid = B + (r + 1) * S;
+      const uint32_t* dn = B + r * S;
+      uint32_t* bn = Bn + (r + 1) * S;
+      const uint32_t* xr = X + r * S;
+      uint32_t* ar = ACT + r * S;
+      uint32_t vl = 0u;                            // column j-1: north | own | south
+      uint32_t uc = up[0], mc = mid[0], dc = dn[0];
+      uint32_t vc = uc | mc | dc;
+      for (int j = 0; j < wpr; ++j) {
+        uint32_t un = 0u, mn = 0u, dnn = 0u;
+        if (j + 1 < wpr) {
+          un = up[j + 1];
+          mn = mid[j + 1];
+          dnn = dn[j + 1];
+        }
+        const uint32_t vn = un | mn | dnn;
+        // west/east neighbours of all three rows, plus north/south of the own column
+        const uint32_t any = ((vc << 1) | (vl >> 31)) | ((vc >> 1) | (vn << 31)) | uc | dc;
+        bn[j] = mc;
+        const uint32_t valid = j + 1 < wpr ? 0xffffffffu : last_mask;
+        const uint32_t act = ((~(mc | xr[j]) & valid) & any) | mc;
+        ar[j] = act;
+        cnt += __popc(act);
+        vl = vc;
+        vc = vn;
+        uc = un;
+        mc = mn;
+        dc = dnn;
+      }
     }
     // one warp-aggregated list reservation per warp and step (skipped by quiet warps)
     if (__ballot_sync(0xffffffffu, cnt > 0)) {
@@ -153,16 +157,19 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
       if (lane == 31) base = atomicAdd(&s_total[par], incl);
       base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
       if (cnt > 0) {
-        for (WordIter it(wpr, nwords); it.ok(); it.next()) {
-          uint32_t rest = ACT[it.idx];
-          const int cell0 = it.r * RW + 32 * it.j;
-          while (rest && base < cap) {
-            const int bit = __ffs(rest) - 1;
-            rest &= rest - 1;
-            list[base++] = static_cast<uint16_t>(cell0 + bit);
+        for (int r = threadIdx.x; r < RH; r += blockDim.x) {
+          for (int j = 0; j < wpr; ++j) {
+            uint32_t rest = ACT[r * S + j];
+            if (!rest) continue;
+            const int cell0 = r * RW + 32 * j;
+            while (rest && base < cap) {
+              const int bit = __ffs(rest) - 1;
+              rest &= rest - 1;
+              list[base++] = static_cast<uint16_t>(cell0 + bit);
+            }
+            ACT[r * S + j] = rest;  // overflow beyond the list capacity: done by this thread in P2
+            ovf |= rest != 0u;
           }
-          ACT[it.idx] = rest;  // overflow beyond the list capacity: done by this thread in P2
-          ovf |= rest != 0u;
         }
       }
     }
@@ -172,13 +179,13 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
     const int total = min(s_total[par], cap);
     auto decide = [&](int lc) {
       const int rr = lc / RW, cc = lc - rr * RW;
-      const int wi = (rr + 1) * wpr + (cc >> 5);
+      const int wi = (rr + 1) * S + (cc >> 5);
       const uint32_t bit = 1u << (cc & 31);
       const uint64_t m = cell_bits53(prefix, gbase + static_cast<uint64_t>(rr) * W + cc, 0);
       if (B[wi] & bit) {
         if (m >= a.pc_thr) {
           atomicAnd(Bn + wi, ~bit);
-          atomicOr(X + rr * wpr + (cc >> 5), bit);
+          atomicOr(X + rr * S + (cc >> 5), bit);
         }
       } else {
         uint32_t nb = 0;
@@ -186,7 +193,7 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
         for (int k = 0; k < 8; ++k) {
           const int ur = rr - kDy[k], uc = cc - kDx[k];
           if (uc < 0 || uc >= RW) continue;  // padding rows cover ur = -1 and ur = RH
-          nb |= ((B[(ur + 1) * wpr + (uc >> 5)] >> (uc & 31)) & 1u) << k;
+          nb |= ((B[(ur + 1) * S + (uc >> 5)] >> (uc & 31)) & 1u) << k;
         }
         if (ignite<MODE>(a, env, R0 + rr, C0 + cc, nb, m, dg)) {
           atomicOr(Bn + wi, bit);
@@ -195,13 +202,16 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
       }
     };
     for (int i = threadIdx.x; i < total; i += blockDim.x) decide(list[i]);
-    for (WordIter it(wpr, nwords); ovf && it.ok(); it.next()) {
-      uint32_t rest = ACT[it.idx];
-      while (rest) {
-        const int bit = __ffs(rest) - 1;
-        rest &= rest - 1;
-        decide(it.r * RW + 32 * it.j + bit);
-      }
+    if (ovf) {
+      for (int r = threadIdx.x; r < RH; r += blockDim.x)
+        for (int j = 0; j < wpr; ++j) {
+          uint32_t rest = ACT[r * S + j];
+          while (rest) {
+            const int bit = __ffs(rest) - 1;
+            rest &= rest - 1;
+            decide(r * RW + 32 * j + bit);
+          }
+        }
     }
     if (t == g.n_steps - 1) {
 #pragma unroll
@@ -220,22 +230,14 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
   const int twords = tj1 - tj0;
   for (WordIter it(twords, (tr1 - tr0) * twords); it.ok(); it.next()) {
     const int rr = tr0 + it.r, j = tj0 + it.j;
-    const uint32_t b = B[(rr + 1) * wpr + j], x = X[rr * wpr + j];
+    const uint32_t b = B[(rr + 1) * S + j], x = X[rr * S + j];
     const int nc = min(32, RW - 32 * j);
     nB += __popc(b);
     nX += __popc(x);
     nU += nc - __popc(b) - __popc(x);
     uint8_t* dst = out + static_cast<size_t>(R0 + rr) * W + C0 + 32 * j;
     if (nc == 32 && vec) {
-      uint32_t wds[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {  // spread 4 bits to 4 bytes: bit k -> bit 8k
-        const uint32_t bs = (((b >> (4 * q)) & 0xfu) * 0x00204081u) & 0x01010101u;
-        const uint32_t xs = (((x >> (4 * q)) & 0xfu) * 0x00204081u) & 0x01010101u;
-        wds[q] = bs | (xs << 1);
-      }
-      reinterpret_cast<uint4*>(dst)[0] = make_uint4(wds[0], wds[1], wds[2], wds[3]);
-      reinterpret_cast<uint4*>(dst)[1] = make_uint4(wds[4], wds[5], wds[6], wds[7]);
+      bits_to_bytes(b, x, dst);
     } else {
       for (int k = 0; k < nc; ++k) dst[k] = static_cast<uint8_t>(((b >> k) & 1u) | (((x >> k) & 1u) << 1));
     }
@@ -252,8 +254,8 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
 }
 
 size_t blocked_smem_bytes(int region_h, int region_w, int list_cap) {
-  const size_t wpr = (region_w + 31) / 32;
-  const size_t planes = (2 * (static_cast<size_t>(region_h) + 2) + 2 * region_h) * wpr * sizeof(uint32_t);
+  const size_t S = plane_stride((region_w + 31) / 32);
+  const size_t planes = (2 * (static_cast<size_t>(region_h) + 2) + 2 * region_h) * S * sizeof(uint32_t);
   const size_t list = static_cast<size_t>(list_cap) * sizeof(uint16_t);
   return planes + ((list + 15) & ~size_t(15));
 }
