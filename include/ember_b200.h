@@ -38,6 +38,7 @@ extern "C" {
 #define EBL_ERANGE -3 /* std::out_of_range */
 #define EBL_ECUDA -4  /* device / driver failure */
 #define EBL_ESTATE -5 /* call order (e.g. stepping before a grid is set) */
+#define EBL_ENUMERIC -6 /* NumericalError (errors.hpp:14-17) */
 
 #define EBL_ABI_VERSION 1
 
@@ -183,6 +184,26 @@ int ebl_det_forward(ebl_batch* b, int n_steps, int record);
  * calibrate.cpp:130-162).  mask [n_envs][H*W]; loss [n_envs]; grad6 [n_envs*6]. */
 int ebl_det_loss_grad(ebl_batch* b, const double* mask, double bce_w, double mse_w, int pool,
                       double* loss, double* grad6);
+
+/* CalibrationOptions (calibrate.hpp:158-166). */
+typedef struct {
+  int iterations;
+  double init_theta[6]; /* constrained space, ParamIndex order */
+  int optimize[6];
+  double lr;
+  int max_horizon;
+} ebl_calib_options;
+void ebl_default_calib_options(ebl_calib_options* o);
+/* calibrate(grid, initial, target, lc, opts) (calibrate.cpp:104-167): Adam on the
+ * ThetaTransform-unconstrained parameters; every iteration a device deterministic rollout of
+ * `horizon` steps from the continuous initial state [n_envs][H*W], the loss and its reverse-mode
+ * gradient (summed over the batch's envs, which share theta; n_envs = 1 is the reference's call).
+ * loss_hist [iterations+1], theta_hist [(iterations+1)*6].  Errors as the reference:
+ * EBL_EINVAL (invalid_argument), EBL_ENUMERIC (NumericalError).  Restores the batch config. */
+int ebl_calibrate(ebl_batch* b, const double* p_un, const double* p_burn, const double* p_bd,
+                  const double* mask, int horizon, double bce_w, double mse_w, int pool,
+                  const ebl_calib_options* opt, double* loss_hist, double* theta_hist,
+                  double* best_theta, double* best_loss);
 
 /* ---- RL (rl_env.hpp) ---------------------------------------------------------- */
 /* EnvConfig (rl_env.hpp:24-40). */

@@ -478,13 +478,35 @@ static dual6 d_log(dual6 a) {
 /* Loss + d loss / d theta after `steps` deterministic steps from a discrete layer;
  * theta = the six SimConfig fields lifted as parameters 0..5 (ParamIndex order,
  * calibrate.hpp:21-28).  loss = bce_w * BCE + mse_w * MSE(avgpool) (calibrate.hpp:120-146). */
+/* run_deterministic<Dual<6>> from a continuous initial state (lift_state: constant duals) with
+ * config P[0..5], then loss; returns the Dual loss. */
+static dual6 det_loss_dual(const ebo_grid* g, const dual6* P, int steps, const double* un0,
+                           const double* bu0, const double* bd0, const double* mask, double bce_w,
+                           double mse_w, int pool);
+
 void ebo_det_loss_grad(const ebo_grid* g, const double* cfg, int steps, const uint8_t* fire0,
                        const double* mask, double bce_w, double mse_w, int pool, double* loss_out,
                        double* grad6) {
-  const int h = g->h, w = g->w;
-  const size_t n = (size_t)h * w;
+  const size_t n = (size_t)g->h * g->w;
   dual6 P[6];
   for (int i = 0; i < 6; ++i) { P[i] = d_const(cfg[i]); P[i].g[i] = 1.0; }
+  double* s0 = (double*)malloc(3 * n * sizeof(double));
+  for (size_t i = 0; i < n; ++i) {  /* state_from_fire (engine.cpp:42-52) */
+    s0[i] = fire0[i] == 0 ? 1.0 : 0.0;
+    s0[n + i] = fire0[i] == 1 ? 1.0 : 0.0;
+    s0[2 * n + i] = fire0[i] == 2 ? 1.0 : 0.0;
+  }
+  const dual6 l = det_loss_dual(g, P, steps, s0, s0 + n, s0 + 2 * n, mask, bce_w, mse_w, pool);
+  *loss_out = l.v;
+  for (int i = 0; i < 6; ++i) grad6[i] = l.g[i];
+  free(s0);
+}
+
+static dual6 det_loss_dual(const ebo_grid* g, const dual6* P, int steps, const double* un0,
+                           const double* bu0, const double* bd0, const double* mask, double bce_w,
+                           double mse_w, int pool) {
+  const int h = g->h, w = g->w;
+  const size_t n = (size_t)h * w;
   /* SpreadTables<Dual<6>> (engine.hpp:79-110) */
   dual6* pot = (dual6*)malloc(n * 8 * sizeof(dual6));
   dual6* gam = (dual6*)malloc(n * sizeof(dual6));
@@ -503,10 +525,10 @@ void ebo_det_loss_grad(const ebo_grid* g, const double* cfg, int steps, const ui
         *bd = (dual6*)malloc(n * sizeof(dual6));
   dual6 *un2 = (dual6*)malloc(n * sizeof(dual6)), *bu2 = (dual6*)malloc(n * sizeof(dual6)),
         *bd2 = (dual6*)malloc(n * sizeof(dual6));
-  for (size_t i = 0; i < n; ++i) {  /* lift_state(state_from_fire) (engine.cpp:42-52) */
-    un[i] = d_const(fire0[i] == 0 ? 1.0 : 0.0);
-    bu[i] = d_const(fire0[i] == 1 ? 1.0 : 0.0);
-    bd[i] = d_const(fire0[i] == 2 ? 1.0 : 0.0);
+  for (size_t i = 0; i < n; ++i) {  /* lift_state (engine.hpp:46-57) */
+    un[i] = d_const(un0[i]);
+    bu[i] = d_const(bu0[i]);
+    bd[i] = d_const(bd0[i]);
   }
   for (int t = 0; t < steps; ++t) {
     for (int r = 0; r < h; ++r)
@@ -567,9 +589,84 @@ void ebo_det_loss_grad(const ebo_grid* g, const double* cfg, int steps, const ui
     }
   mse = d_divs(mse, (double)(oh * ow));
   const dual6 l = d_add(d_muls(bce, bce_w), d_muls(mse, mse_w));
-  *loss_out = l.v;
-  for (int i = 0; i < 6; ++i) grad6[i] = l.g[i];
   free(pot), free(gam), free(un), free(bu), free(bd), free(un2), free(bu2), free(bd2);
+  return l;
+}
+
+/* ---------------------------------------------------------------- calibrate.cpp / .hpp */
+static dual6 d_addl(double a, dual6 b) { b.v += a; return b; } /* double + Dual (dual.hpp:90) */
+static dual6 d_div(dual6 a, dual6 b) {                          /* operator/= (dual.hpp:62-68) */
+  for (int i = 0; i < 6; ++i) a.g[i] = (a.g[i] * b.v - a.v * b.g[i]) / (b.v * b.v);
+  a.v /= b.v;
+  return a;
+}
+static dual6 softplus6(dual6 x) { /* calibrate.hpp:44-49 */
+  if (x.v > 0.0) return d_add(x, d_log(d_addl(1.0, d_exp(d_neg(x)))));
+  return d_log(d_addl(1.0, d_exp(x)));
+}
+static dual6 logistic6(dual6 x) { /* calibrate.hpp:51-57 */
+  if (x.v >= 0.0) return d_div(d_const(1.0), d_addl(1.0, d_exp(d_neg(x))));
+  const dual6 e = d_exp(x);
+  return d_div(e, d_addl(1.0, e));
+}
+
+/* calibrate (calibrate.cpp:104-167) with ThetaTransform (calibrate.hpp:59-68, calibrate.cpp:35-55)
+ * and adam_step (calibrate.cpp:84-102); returns 0, -1 on a non-finite loss or gradient
+ * (NumericalError), -2 on an init_theta outside the transform's domain (invalid_argument). */
+int ebo_calibrate(const ebo_grid* g, const double* un0, const double* bu0, const double* bd0,
+                  const double* mask, int horizon, double bce_w, double mse_w, int pool,
+                  int iterations, const double* init_theta, const int* optimize, double lr,
+                  double* loss_hist, double* theta_hist, double* best_theta, double* best_loss) {
+  double u[6];
+  for (int i = 0; i < 6; ++i) u[i] = init_theta[i];
+  const int pos[2] = {0, 4};
+  for (int j = 0; j < 2; ++j) { /* inverse_softplus */
+    const double y = init_theta[pos[j]];
+    if (!(y > 0.0)) return -2;
+    u[pos[j]] = y > 20.0 ? y : log(expm1(y));
+  }
+  {
+    const double p = init_theta[5]; /* logit */
+    if (!(p > 0.0 && p < 1.0)) return -2;
+    u[5] = log(p / (1.0 - p));
+  }
+  double m[6] = {0}, v[6] = {0};
+  int t_adam = 0;
+  const double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+  *best_loss = INFINITY;
+  for (int iter = 0; iter <= iterations; ++iter) {
+    dual6 ud[6], th[6];
+    for (int i = 0; i < 6; ++i) {
+      ud[i] = d_const(u[i]);
+      if (optimize[i]) ud[i].g[i] = 1.0;
+    }
+    th[0] = softplus6(ud[0]);
+    th[1] = ud[1];
+    th[2] = ud[2];
+    th[3] = ud[3];
+    th[4] = softplus6(ud[4]);
+    th[5] = logistic6(ud[5]);
+    const dual6 l = det_loss_dual(g, th, horizon, un0, bu0, bd0, mask, bce_w, mse_w, pool);
+    if (!isfinite(l.v)) return -1;
+    loss_hist[iter] = l.v;
+    for (int i = 0; i < 6; ++i) theta_hist[iter * 6 + i] = th[i].v;
+    if (l.v < *best_loss) {
+      *best_loss = l.v;
+      for (int i = 0; i < 6; ++i) best_theta[i] = th[i].v;
+    }
+    if (iter == iterations) break;
+    for (int i = 0; i < 6; ++i)
+      if (!isfinite(l.g[i])) return -1;
+    t_adam += 1;
+    const double bc1 = 1.0 - pow(beta1, t_adam), bc2 = 1.0 - pow(beta2, t_adam);
+    for (int i = 0; i < 6; ++i) {
+      m[i] = beta1 * m[i] + (1.0 - beta1) * l.g[i];
+      v[i] = beta2 * v[i] + (1.0 - beta2) * l.g[i] * l.g[i];
+      const double m_hat = m[i] / bc1, v_hat = v[i] / bc2;
+      u[i] = u[i] - lr * m_hat / (sqrt(v_hat) + eps);
+    }
+  }
+  return 0;
 }
 
 /* Deterministic forward from a discrete layer, double (run_deterministic<double>). */

@@ -128,6 +128,15 @@ void ebo_det_loss_grad(const ebo_grid* g, const double* cfg, int steps, const ui
                        const double* mask, double bce_w, double mse_w, int pool, double* loss_out,
                        double* grad6);
 
+/* calibrate (calibrate.cpp:104-167): Adam on ThetaTransform-unconstrained parameters, each
+ * iteration a Dual<6> deterministic rollout of `horizon` steps from the continuous initial
+ * state + loss.  loss_hist [iterations+1], theta_hist [(iterations+1)*6].  0 / -1 non-finite /
+ * -2 bad init_theta. */
+int ebo_calibrate(const ebo_grid* g, const double* un0, const double* bu0, const double* bd0,
+                  const double* mask, int horizon, double bce_w, double mse_w, int pool,
+                  int iterations, const double* init_theta, const int* optimize, double lr,
+                  double* loss_hist, double* theta_hist, double* best_theta, double* best_loss);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,7 @@ _PORT_SIG = {
     "ebo_det_step_tables": (None, [_I, _I, _P, _P, _D, _P, _P, _P, _P, _P, _P]),
     "ebo_det_run": (None, [_P, _P, _I, _P, _P, _P]),
     "ebo_det_loss_grad": (None, [_P, _P, _I, _P, _P, _D, _D, _I, C.POINTER(_D), _P]),
+    "ebo_calibrate": (_I, [_P, _P, _P, _P, _P, _I, _D, _D, _I, _I, _P, _P, _D, _P, _P, _P, C.POINTER(_D)]),
 }
 
 _REF_SIG = {
@@ -110,6 +111,7 @@ _REF_SIG = {
     "ref_random_policy": (_I, [_U64, _U64, _U64]),
     "ref_run_deterministic": (_I, [_P, _P, _I, _P, _P, _P]),
     "ref_loss_grad": (_I, [_P, _P, _I, _P, _P, _D, _D, _I, C.POINTER(_D), _P]),
+    "ref_calibrate": (_I, [_P, _P, _P, _P, _P, _I, _D, _D, _I, _I, _P, _P, _D, _P, _P, _P, C.POINTER(_D)]),
 }
 
 _port = None
@@ -225,3 +227,21 @@ def fnv1a64(data: bytes) -> int:
         h ^= b
         h = (h * 0x100000001B3) & 0xFFFFFFFFFFFFFFFF
     return h
+
+
+def calibrate(L, kind, grid: Grid, init_planes, mask, horizon, iterations, init_theta, optimize=None,
+              lr=1e-2, bce_w=1.0, mse_w=1.0, pool=4):
+    """calibrate (calibrate.cpp:104-167) on the port or the reference: (rc, loss_hist, theta_hist,
+    best_theta, best_loss)."""
+    un, bu, bd = [np.ascontiguousarray(x, dtype=np.float64) for x in init_planes]
+    m = np.ascontiguousarray(mask, dtype=np.float64)
+    th = np.ascontiguousarray(init_theta, dtype=np.float64)
+    opt = np.ascontiguousarray(np.ones(6) if optimize is None else optimize, dtype=np.int32)
+    lh = np.empty(iterations + 1)
+    thh = np.empty((iterations + 1, 6))
+    best = np.empty(6)
+    bl = _D()
+    fn = L.ebo_calibrate if kind == "port" else L.ref_calibrate
+    rc = fn(grid.h, ptr(un), ptr(bu), ptr(bd), ptr(m), horizon, bce_w, mse_w, pool, iterations, ptr(th),
+            ptr(opt), lr, ptr(lh), ptr(thh), ptr(best), bl)
+    return rc, lh, thh, best, bl.value

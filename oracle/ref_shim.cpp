@@ -397,4 +397,40 @@ int ref_loss_grad(const void* gp, const double* c, int steps, const std::uint8_t
   }
 }
 
+// calibrate(grid, initial, target, lc, opts) (calibrate.cpp:104-167).  Returns 0, or -1 with
+// ref_last_error() set (invalid_argument / NumericalError).
+int ref_calibrate(const void* gp, const double* un0, const double* bu0, const double* bd0,
+                  const double* mask, int horizon, double bce_w, double mse_w, int pool,
+                  int iterations, const double* init_theta, const int* optimize, double lr,
+                  double* loss_hist, double* theta_hist, double* best_theta, double* best_loss) {
+  try {
+    const auto& g = *static_cast<const R::GridState*>(gp);
+    const int h = g.height(), w = g.width();
+    R::ContinuousState init{grid_of(h, w, un0), grid_of(h, w, bu0), grid_of(h, w, bd0)};
+    R::CalibrationTarget tgt{grid_of(h, w, mask), horizon};
+    R::LossConfig lc;
+    lc.bce_weight = bce_w;
+    lc.mse_weight = mse_w;
+    lc.pool_size = pool;
+    R::CalibrationOptions opts;
+    opts.iterations = iterations;
+    for (int i = 0; i < 6; ++i) {
+      opts.init_theta[i] = init_theta[i];
+      opts.optimize[i] = optimize[i] != 0;
+    }
+    opts.lr = lr;
+    opts.exec = R::Exec::serial;
+    const R::CalibrationResult res = R::calibrate(g, init, tgt, lc, opts);
+    for (int i = 0; i <= iterations; ++i) {
+      loss_hist[i] = res.loss_history[i];
+      for (int k = 0; k < 6; ++k) theta_hist[i * 6 + k] = res.theta_history[i][k];
+    }
+    for (int k = 0; k < 6; ++k) best_theta[k] = res.best_theta[k];
+    *best_loss = res.best_loss;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 }  // extern "C"

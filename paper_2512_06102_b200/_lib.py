@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libember_b200.so")
 
-EBL_OK, EBL_EINVAL, EBL_ELOGIC, EBL_ERANGE, EBL_ECUDA, EBL_ESTATE = 0, -1, -2, -3, -4, -5
+EBL_OK, EBL_EINVAL, EBL_ELOGIC, EBL_ERANGE, EBL_ECUDA, EBL_ESTATE, EBL_ENUMERIC = 0, -1, -2, -3, -4, -5, -6
 RL_REFERENCE, RL_TANKER = 0, 1
 
 
@@ -47,6 +47,13 @@ class EnvState(C.Structure):
                 ("done", C.c_int32), ("episode", C.c_uint32)]
 
 
+class CalibOptions(C.Structure):
+    """CalibrationOptions (reference calibrate.hpp:158-166)."""
+
+    _fields_ = [("iterations", C.c_int), ("init_theta", C.c_double * 6), ("optimize", C.c_int * 6),
+                ("lr", C.c_double), ("max_horizon", C.c_int)]
+
+
 class EmberError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"[{code}] {msg}")
@@ -65,7 +72,12 @@ class OutOfRange(EmberError, IndexError):        # std::out_of_range
     pass
 
 
-_EXC = {EBL_EINVAL: InvalidArgument, EBL_ELOGIC: LogicError, EBL_ERANGE: OutOfRange}
+class NumericalError(EmberError, ArithmeticError):  # emberline::NumericalError
+    pass
+
+
+_EXC = {EBL_EINVAL: InvalidArgument, EBL_ELOGIC: LogicError, EBL_ERANGE: OutOfRange,
+        EBL_ENUMERIC: NumericalError}
 
 _P = C.c_void_p
 _I, _U64, _U32, _D = C.c_int, C.c_uint64, C.c_uint32, C.c_double
@@ -109,6 +121,9 @@ SIGNATURES = {
     "ebl_det_get_state": (_I, [_P, _P, _P, _P]),
     "ebl_det_forward": (_I, [_P, _I, _I]),
     "ebl_det_loss_grad": (_I, [_P, _P, _D, _D, _I, _P, _P]),
+    "ebl_default_calib_options": (None, [C.POINTER(CalibOptions)]),
+    "ebl_calibrate": (_I, [_P, _P, _P, _P, _P, _I, _D, _D, _I, C.POINTER(CalibOptions), _P, _P, _P,
+                           C.POINTER(_D)]),
     "ebl_env_default_preset": (None, [C.POINTER(EnvConfig)]),
     "ebl_env_smoke10_preset": (None, [C.POINTER(EnvConfig)]),
     "ebl_env_observation_size": (_I, [C.POINTER(EnvConfig)]),

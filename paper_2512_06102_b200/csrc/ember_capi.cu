@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <algorithm>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <string>
 #include <vector>
@@ -78,6 +79,7 @@ struct ebl_batch {
 
   uint64_t seed = 0, step = 0;
   int64_t row_off = 0;  // global row of layer row 0 (row-sharded landscapes)
+  bool streams_uploaded = false;
   std::vector<uint64_t> h_streams;
   DevBuf<uint64_t> streams;
 
@@ -114,7 +116,7 @@ struct ebl_batch {
   DevBuf<double> det[6];            // un, burn, bd x2 (double buffer)
   int det_cur = 0;
   bool det_ready = false;
-  DevBuf<double> det_pot, det_gam, det_V, det_align, traj, adj, det_mask, acc, det_loss, det_grad;
+  DevBuf<double> det_pot, det_gam, det_fac, det_V, det_align, traj, adj, det_mask, acc, det_loss, det_grad;
   int det_tables = 0;
   bool det_tables_valid = false;
   ebl_sim_config det_cfg{};
@@ -279,6 +281,7 @@ int ebl_batch_create(ebl_batch** out, int device, int n_envs, int height, int wi
   EBL_CUDA(cudaMemcpyAsync(b->streams.p, b->h_streams.data(), n_envs * sizeof(uint64_t),
                            cudaMemcpyHostToDevice, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
+  b->streams_uploaded = true;
   *out = b.release();
   return EBL_OK;
 }
@@ -330,6 +333,7 @@ int ebl_batch_set_grid(ebl_batch* b, int n_grids, const double* speed, const dou
   b->mode = ebl::kStaticTables;
   b->n_grids = n_grids;
   b->tables_dirty = true;
+  b->det_tables_valid = false;
   b->fuel.reset();
   b->elev.reset();
   return EBL_OK;
@@ -432,11 +436,18 @@ int ebl_batch_set_key(ebl_batch* b, uint64_t seed, uint64_t step, const uint64_t
   if (int e = check_batch(b)) return e;
   b->seed = seed;
   b->step = step;
-  for (int e = 0; e < b->n_envs; ++e) b->h_streams[e] = streams ? streams[e] : first_stream + e;
+  bool changed = false;
+  for (int e = 0; e < b->n_envs; ++e) {
+    const uint64_t s = streams ? streams[e] : first_stream + e;
+    changed |= b->h_streams[e] != s;
+    b->h_streams[e] = s;
+  }
+  if (!changed && b->streams_uploaded) return EBL_OK;  // seed/step travel as kernel arguments
   EBL_CUDA(cudaSetDevice(b->device));
   EBL_CUDA(cudaMemcpyAsync(b->streams.p, b->h_streams.data(), b->n_envs * sizeof(uint64_t),
                            cudaMemcpyHostToDevice, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
+  b->streams_uploaded = true;
   return EBL_OK;
 }
 
@@ -964,6 +975,14 @@ ebl::DetArgs det_args(ebl_batch* b) {
   d.V = b->det_V.p;
   d.align = b->det_align.p;
   d.wind_stride = b->n_winds > 1 ? 1 : 0;
+  if (b->det_fac.p) {  // general form
+    const size_t nt = b->ncell * b->det_tables;
+    d.fac_F = b->det_fac.p;
+    d.fac_pb = d.fac_F + nt;
+    d.fac_V = d.fac_pb + nt * 8;
+    d.fac_Va = d.fac_V + nt;
+    d.fac_S = d.fac_Va + nt * 8;
+  }
   return d;
 }
 
@@ -971,12 +990,30 @@ ebl::DetArgs det_args(ebl_batch* b) {
 // arithmetic (ember_host.cpp) and uploaded; one table per env when grids or winds differ.
 int det_tables(ebl_batch* b) {
   const ebl::Cfg6 c = cfg6(b->cfg);
-  const int T = (b->n_grids > 1 || b->n_winds > 1) ? b->n_envs : 1;
+  const bool general = b->mode == ebl::kStaticTables;
+  const int T = general ? b->n_grids : ((b->n_grids > 1 || b->n_winds > 1) ? b->n_envs : 1);
   const size_t n = b->ncell;
   std::vector<double> pot(n * 8 * T), gam(n * T);
-  ebl::build_terrain_tables(T, b->h, b->w, b->h_fuel.data(), b->h_elev.data(), b->n_grids > 1 ? n : 0,
-                            b->pal_veg.data(), b->pal_den.data(), b->cellsize, b->wind_speed.data(),
-                            b->wind_dir.data(), b->n_winds > 1 ? 1 : 0, c, pot.data(), gam.data());
+  if (general) {  // per-cell layers: the SpreadTables plus the adjoint's derivative factors
+    const size_t nt = n * T;
+    ebl::build_tables(nt, b->g_speed.data(), b->g_dir.data(), b->g_veg.data(), b->g_den.data(),
+                      b->g_slope.data(), c, pot.data(), gam.data());
+    std::vector<double> fac(nt * 26);  // F | pb[8] | V | Va[8] | S[8]
+    double* F = fac.data();
+    double* pb = F + nt;
+    double* V = pb + nt * 8;
+    double* Va = V + nt;
+    double* S = Va + nt * 8;
+    ebl::build_det_factors(nt, b->g_speed.data(), b->g_dir.data(), b->g_veg.data(), b->g_den.data(),
+                           b->g_slope.data(), c, F, pb, V, Va, S);
+    EBL_CUDA(b->det_fac.alloc(fac.size()));
+    EBL_CUDA(cudaMemcpyAsync(b->det_fac.p, fac.data(), fac.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  } else {
+    ebl::build_terrain_tables(T, b->h, b->w, b->h_fuel.data(), b->h_elev.data(), b->n_grids > 1 ? n : 0,
+                              b->pal_veg.data(), b->pal_den.data(), b->cellsize, b->wind_speed.data(),
+                              b->wind_dir.data(), b->n_winds > 1 ? 1 : 0, c, pot.data(), gam.data());
+    b->det_fac.reset();
+  }
   std::vector<double> V(b->n_winds), al(static_cast<size_t>(b->n_winds) * 8);
   for (int w = 0; w < b->n_winds; ++w) {  // kernel.hpp:24: cos(phi_k - theta) - 1
     V[w] = b->wind_speed[w];
@@ -1044,8 +1081,7 @@ int ebl_det_get_state(ebl_batch* b, double* un, double* burn, double* bd) {
 int ebl_det_forward(ebl_batch* b, int n_steps, int record) {
   if (int e = check_batch(b)) return e;
   if (!b->det_ready) return set_err(EBL_ESTATE, "ebl_det_set_state first");
-  if (b->mode != ebl::kStaticTerrain)
-    return set_err(EBL_EINVAL, "deterministic mode runs on the terrain form (ebl_batch_set_terrain)");
+  if (b->mode == ebl::kStaticNone) return set_err(EBL_ESTATE, "no grid or terrain set on the batch");
   if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
   if (int e = prepare(b)) return e;
   if (!b->det_tables_valid || std::memcmp(&b->det_cfg, &b->cfg, sizeof b->cfg) != 0)
@@ -1105,6 +1141,109 @@ int ebl_det_loss_grad(ebl_batch* b, const double* mask, double bce_w, double mse
   EBL_CUDA(cudaMemcpyAsync(grad6, b->det_grad.p, b->n_envs * 6 * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
   return EBL_OK;
+}
+
+void ebl_default_calib_options(ebl_calib_options* o) {  // calibrate.hpp:158-166
+  *o = ebl_calib_options{300, {0.12, 0.2, 0.4, 1.0, 1.0, 0.6}, {1, 1, 1, 1, 1, 1}, 1e-2, 2000};
+}
+
+// calibrate (calibrate.cpp:104-167) with every rollout, loss and gradient on the device.
+int ebl_calibrate(ebl_batch* b, const double* p_un, const double* p_burn, const double* p_bd,
+                  const double* mask, int horizon, double bce_w, double mse_w, int pool,
+                  const ebl_calib_options* opt, double* loss_hist, double* theta_hist,
+                  double* best_theta, double* best_loss) {
+  if (int e = check_batch(b)) return e;
+  if (!opt || !p_un || !p_burn || !p_bd || !mask || !loss_hist || !theta_hist || !best_theta || !best_loss)
+    return set_err(EBL_EINVAL, "null argument");
+  const size_t n = b->ncell * b->n_envs;
+  // validate_target / validate_loss_config / validate_state (calibrate.cpp:57-80, engine.cpp:54-72)
+  for (int e = 0; e < b->n_envs; ++e) {
+    bool any = false;
+    for (size_t i = e * b->ncell; i < (e + 1) * b->ncell; ++i) {
+      if (mask[i] != 0.0 && mask[i] != 1.0) return set_err(EBL_EINVAL, "CalibrationTarget: mask values must be 0 or 1");
+      any |= mask[i] == 1.0;
+    }
+    if (!any) return set_err(EBL_EINVAL, "CalibrationTarget: mask has no burned cells");
+  }
+  if (horizon < 0) return set_err(EBL_EINVAL, "CalibrationTarget: negative horizon");
+  if (!(bce_w >= 0.0) || !(mse_w >= 0.0)) return set_err(EBL_EINVAL, "LossConfig: weights must be >= 0");
+  if (bce_w == 0.0 && mse_w == 0.0) return set_err(EBL_EINVAL, "LossConfig: at least one weight must be positive");
+  if (pool < 1) return set_err(EBL_EINVAL, "LossConfig: pool_size must be >= 1");
+  for (size_t i = 0; i < n; ++i) {
+    if (!(p_un[i] >= 0.0) || !(p_burn[i] >= 0.0) || !(p_bd[i] >= 0.0))
+      return set_err(EBL_EINVAL, "ContinuousState: negative or NaN component");
+    if (std::abs(p_un[i] + p_burn[i] + p_bd[i] - 1.0) > 1e-9)
+      return set_err(EBL_EINVAL, "ContinuousState: cell probabilities do not sum to 1");
+  }
+  if (opt->iterations < 0) return set_err(EBL_EINVAL, "calibrate: negative iteration count");
+  if (horizon > opt->max_horizon) return set_err(EBL_EINVAL, "calibrate: horizon exceeds the configured maximum");
+  // ThetaTransform::unconstrain (calibrate.cpp:35-55)
+  double u[6];
+  for (int i = 0; i < 6; ++i) u[i] = opt->init_theta[i];
+  for (int i : {0, 4}) {
+    const double y = opt->init_theta[i];
+    if (!(y > 0.0)) return set_err(EBL_EINVAL, "inverse_softplus: argument must be > 0");
+    u[i] = y > 20.0 ? y : std::log(std::expm1(y));
+  }
+  {
+    const double p = opt->init_theta[5];
+    if (!(p > 0.0 && p < 1.0)) return set_err(EBL_EINVAL, "logit: argument must be in (0, 1)");
+    u[5] = std::log(p / (1.0 - p));
+  }
+  const double beta1 = 0.9, beta2 = 0.999, eps = 1e-8;  // AdamState defaults (calibrate.hpp:148-156)
+  double m[6] = {0}, v[6] = {0};
+  int t_adam = 0;
+  *best_loss = std::numeric_limits<double>::infinity();
+  const ebl_sim_config saved = b->cfg;
+  std::vector<double> loss_e(b->n_envs), grad_e(static_cast<size_t>(b->n_envs) * 6);
+  for (int iter = 0; iter <= opt->iterations; ++iter) {
+    // ThetaTransform::constrain (calibrate.hpp:59-65): softplus / identity / logistic
+    auto softplus = [](double x) { return x > 0.0 ? x + std::log(1.0 + std::exp(-x)) : std::log(1.0 + std::exp(x)); };
+    auto logistic = [](double x) {
+      if (x >= 0.0) return 1.0 / (1.0 + std::exp(-x));
+      const double e = std::exp(x);
+      return e / (1.0 + e);
+    };
+    const double th[6] = {softplus(u[0]), u[1], u[2], u[3], softplus(u[4]), logistic(u[5])};
+    // d theta / d u: softplus' = logistic, logistic' = s (1 - s), identity elsewhere
+    const double dth[6] = {logistic(u[0]), 1.0, 1.0, 1.0, logistic(u[4]), th[5] * (1.0 - th[5])};
+    ebl_sim_config c = b->cfg;
+    c.p_base = th[0], c.alpha_w1 = th[1], c.alpha_w2 = th[2], c.alpha_s = th[3], c.alpha_gamma = th[4],
+    c.p_continue = th[5];
+    if (int e = ebl_batch_set_config(b, &c)) return e;
+    if (int e = ebl_det_set_state(b, p_un, p_burn, p_bd)) return e;
+    if (int e = ebl_det_forward(b, horizon, 1)) return e;
+    if (int e = ebl_det_loss_grad(b, mask, bce_w, mse_w, pool, loss_e.data(), grad_e.data())) return e;
+    double l = 0.0, g[6] = {0};
+    for (int e = 0; e < b->n_envs; ++e) {  // the batch's envs share theta: total loss
+      l += loss_e[e];
+      for (int k = 0; k < 6; ++k) g[k] += grad_e[e * 6 + k];
+    }
+    if (!std::isfinite(l))
+      return set_err(EBL_ENUMERIC, "calibrate: loss became non-finite at iteration " + std::to_string(iter));
+    loss_hist[iter] = l;
+    for (int k = 0; k < 6; ++k) theta_hist[iter * 6 + k] = th[k];
+    if (l < *best_loss) {
+      *best_loss = l;
+      for (int k = 0; k < 6; ++k) best_theta[k] = th[k];
+    }
+    if (iter == opt->iterations) break;
+    // adam_step (calibrate.cpp:84-102) on d loss / d u
+    double gu[6];
+    for (int k = 0; k < 6; ++k) {
+      gu[k] = opt->optimize[k] ? g[k] * dth[k] : 0.0;
+      if (!std::isfinite(gu[k])) return set_err(EBL_ENUMERIC, "adam_step: non-finite gradient component");
+    }
+    t_adam += 1;
+    const double bc1 = 1.0 - std::pow(beta1, t_adam), bc2 = 1.0 - std::pow(beta2, t_adam);
+    for (int k = 0; k < 6; ++k) {
+      m[k] = beta1 * m[k] + (1.0 - beta1) * gu[k];
+      v[k] = beta2 * v[k] + (1.0 - beta2) * gu[k] * gu[k];
+      const double m_hat = m[k] / bc1, v_hat = v[k] / bc2;
+      u[k] = u[k] - opt->lr * m_hat / (std::sqrt(v_hat) + eps);
+    }
+  }
+  return ebl_batch_set_config(b, &saved);
 }
 
 // ---- inputs ----------------------------------------------------------------------------

@@ -171,8 +171,8 @@ __global__ void k_det_back1(DetArgs d, int t) {
     const double a_x = a_newly * un * e;  // dp_ig/dx = e^{-x} (Dual's exp)
     d.a_lam[base + i] = a_x * gam;
     d.A_un[base + i] = Au + a_newly * p_ig;
-    const uint8_t cls = a.fuel[static_cast<size_t>(env) * a.ter_stride + i];
-    g_gamma = a_x * lam * a.pal64[768 + cls];  // dgamma/dalpha_gamma = F(v)
+    const double F = d.fac_F ? d.fac_F[tb + i] : a.pal64[768 + a.fuel[static_cast<size_t>(env) * a.ter_stride + i]];
+    g_gamma = a_x * lam * F;  // dgamma/dalpha_gamma = F(v)
     g_pc = bu * (Ab - Ad);
   }
   g_gamma = block_sum_d(g_gamma, red);
@@ -199,7 +199,23 @@ __global__ void k_det_back2(DetArgs d, int t) {
     const int r = i / a.w, c = i - r * a.w;
     const double bu = d.traj_burn[tr + i];
     double acc_burn = d.A_burn[base + i] * d.pc + d.A_bd[base + i] * (1.0 - d.pc);
-    if (bu != 0.0) {
+    if (bu != 0.0 && d.fac_pb) {  // general form: host-built derivative factors
+      const size_t o = tb + i;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int vr = r + kDy[k], vc = c + kDx[k];
+        if (vr < 0 || vr >= a.h || vc < 0 || vc >= a.w) continue;
+        const double al = d.a_lam[base + vr * a.w + vc];
+        if (al == 0.0) continue;
+        const double pot = d.pot[o * 8 + k];
+        acc_burn += al * pot;
+        const double ab = al * bu;
+        gp += ab * d.fac_pb[o * 8 + k];
+        gw1 += ab * pot * d.fac_V[o];
+        gw2 += ab * pot * d.fac_Va[o * 8 + k];
+        gs += ab * pot * d.fac_S[o * 8 + k];
+      }
+    } else if (bu != 0.0) {
       const TerrainView tv = terrain_view(a, env);
       const double V = d.V[env * d.wind_stride];
       const double Fu = a.pal64[768 + tv.fuel[i]];

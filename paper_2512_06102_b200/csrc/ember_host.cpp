@@ -78,6 +78,27 @@ void build_tables(size_t n, const double* speed, const double* dir, const double
   }
 }
 
+void build_det_factors(size_t n, const double* speed, const double* dir, const double* veg,
+                       const double* den, const double* slope8, const Cfg6& c, double* F,
+                       double* pb, double* V, double* Va, double* S) {
+#pragma omp parallel for schedule(static) if (n > 16384)
+  for (long long ii = 0; ii < static_cast<long long>(n); ++ii) {
+    const size_t i = static_cast<size_t>(ii);
+    const double v = clamp_fuel(veg[i]), d = clamp_fuel(den[i]);
+    F[i] = (1.0 + v) * (1.0 + d);
+    V[i] = speed[i];
+    double kw[8];
+    kappa_wind8(speed[i], dir[i], c, kw);
+    const double wd = wrap_angle(dir[i]);
+    for (int k = 0; k < 8; ++k) {
+      const double s = slope8[i * 8 + k];
+      pb[i * 8 + k] = (F[i] * kw[k]) * std::exp(c.alpha_s * s);  // dpot/dp_base
+      Va[i * 8 + k] = speed[i] * (std::cos(offset_angle(k) - wd) - 1.0);
+      S[i * 8 + k] = s;
+    }
+  }
+}
+
 void build_terrain_tables(int n_tables, int h, int w, const uint8_t* fuel, const float* elev,
                           size_t grid_stride, const double* class_veg, const double* class_den,
                           double cellsize, const double* wind_speed, const double* wind_dir,

@@ -20,6 +20,11 @@ void kappa_wind8(double speed, double direction, const Cfg6& c, double kw[8]);
 void build_tables(size_t n, const double* speed, const double* dir, const double* veg,
                   const double* den, const double* slope8, const Cfg6& c, double* pot,
                   double* gamma);
+// Per-cell derivative factors of pot for the deterministic adjoint on general layers:
+// F = (1+veg)(1+den), pb[k] = dpot/dp_base = F kw ks, V, Va[k] = V (cos(phi_k - dir) - 1), S[k].
+void build_det_factors(size_t n, const double* speed, const double* dir, const double* veg,
+                       const double* den, const double* slope8, const Cfg6& c, double* F,
+                       double* pb, double* V, double* Va, double* S);
 // SpreadTables<double> of terrain-form statics (slope_from_dem of the fp32 elevation, palette
 // fuel, uniform wind per table): pot [n_tables][h*w][8], gamma [n_tables][h*w].  Table t uses
 // grid t*grid_stride (stride 0: shared) and wind t*wind_stride.

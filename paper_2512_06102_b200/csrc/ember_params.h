@@ -81,6 +81,12 @@ struct DetArgs {
   const double* V;                // [wind] wind speed
   const double* align;            // [wind][8] cos(phi_k - theta) - 1
   int wind_stride;                // 1 (per env) or 0 (shared)
+  // general form (per-cell layers): host-built derivative factors per table cell, else null
+  const double* fac_F;            // [table][cell] (1+veg)(1+den)
+  const double* fac_pb;           // [table][cell][8] dpot/dp_base = F kw ks
+  const double* fac_V;            // [table][cell] V
+  const double* fac_Va;           // [table][cell][8] V (cos(phi_k - theta) - 1)
+  const double* fac_S;            // [table][cell][8] slope S
 };
 
 // Per-env RL record (rl_env.hpp:67-75 EnvState minus the layer, plus the tanker

@@ -7,7 +7,7 @@
 //   reward -(cells ignited this step); done = no cell burning or step == max_steps;
 //   reset  on done, in place: episode+1, stream = episode << 32 | env id, ignitions drawn
 //          with rng_below(key{seed,0,stream}, counter++, kDrawEnvSetup, H*W) at burnable cells.
-// Identical semantics to the byte kernel k_rl_tanker and the oracle's ebo_tanker_step.
+// Identical semantics to the byte kernel k_rl_tanker.
 #include <cuda_runtime.h>
 
 #include <cstdint>

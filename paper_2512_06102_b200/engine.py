@@ -194,6 +194,31 @@ class Batch:
                                       _ptr(loss), _ptr(grad)))
         return loss, grad
 
+    def calibrate(self, p_un, p_burn, p_bd, mask, horizon, iterations=300, init_theta=None,
+                  optimize=None, lr=1e-2, max_horizon=2000, bce_weight=1.0, mse_weight=1.0, pool=4):
+        """calibrate (calibrate.cpp:104-167) on the device; returns dict(loss_history,
+        theta_history, best_theta, best_loss, initial_loss)."""
+        o = _lib.CalibOptions()
+        lib().ebl_default_calib_options(C.byref(o))
+        o.iterations = iterations
+        if init_theta is not None:
+            o.init_theta = (C.c_double * 6)(*init_theta)
+        if optimize is not None:
+            o.optimize = (C.c_int * 6)(*[int(x) for x in optimize])
+        o.lr, o.max_horizon = lr, max_horizon
+        shp = (self.n_envs, self.height, self.width)
+        planes = [np.ascontiguousarray(np.broadcast_to(np.asarray(x, dtype=np.float64), shp))
+                  for x in (p_un, p_burn, p_bd, mask)]
+        lh = np.empty(iterations + 1)
+        th = np.empty((iterations + 1, 6))
+        best = np.empty(6)
+        bl = C.c_double()
+        check(lib().ebl_calibrate(self._h, *[_ptr(a) for a in planes], horizon, float(bce_weight),
+                                  float(mse_weight), int(pool), C.byref(o), _ptr(lh), _ptr(th),
+                                  _ptr(best), C.byref(bl)))
+        return dict(loss_history=lh, theta_history=th, best_theta=best, best_loss=bl.value,
+                    initial_loss=lh[0])
+
     def diag(self, reset: bool = False) -> dict:
         out = np.zeros(4, dtype=np.uint64)
         check(lib().ebl_batch_diag(self._h, _ptr(out), int(reset)))

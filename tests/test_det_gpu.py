@@ -102,3 +102,61 @@ def test_c4_full_batch_runs_and_is_deterministic():
         outs.append(b.det_loss_grad(mask, 0.0, 1.0, 1))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
     assert np.isfinite(outs[0][1]).all() and (np.abs(outs[0][1]).sum(1) > 0).all()
+
+
+def _calib_case(seed=3, h=20, w=17):
+    rs = np.random.default_rng(seed)
+    L = dict(speed=np.full((h, w), 1.5), dir=np.full((h, w), 0.9), veg=rs.random((h, w)) * 0.6 + 0.1,
+             den=rs.random((h, w)) * 0.5 + 0.1, slope8=0.4 * rs.random((h, w, 8)) - 0.2)
+    fire = np.zeros((h, w), np.uint8)
+    fire[h // 2, w // 2] = 1
+    planes = [(fire == k).astype(np.float64) for k in (0, 1, 2)]
+    return L, planes
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(bce_weight=0.0, mse_weight=1.0, pool=1),
+                                dict(optimize=[1, 0, 1, 1, 0, 1])])
+def test_calibrate_on_device_matches_reference_loop(port, kw):
+    """calibrate (calibrate.cpp:104-167) with the device rollout/loss/gradient on a general
+    GridState vs the oracle's Dual<6> loop (itself bitwise equal to the reference)."""
+    L, planes = _calib_case()
+    h, w = L["veg"].shape
+    gp = O.grid_layers(port, "port", *L.values())
+    un, bu, bd = [p.copy() for p in planes]
+    port.ebo_det_run(gp.h, O.ptr(O.cfg_array([0.22, 0.15, 0.3, 0.8, 1.1, 0.7])), 12, O.ptr(un), O.ptr(bu), O.ptr(bd))
+    mask = ((bu + bd) >= 0.5).astype(np.float64)
+    init = [0.15, 0.2, 0.25, 1.1, 0.9, 0.6]
+    okw = {("bce_w" if k == "bce_weight" else "mse_w" if k == "mse_weight" else k): v for k, v in kw.items()}
+    rc, lh, thh, best, bl = O.calibrate(port, "port", gp, planes, mask, 12, 10, init, **okw)
+    assert rc == 0
+    b = eb.Batch(1, h, w)
+    b.set_grid(*L.values())
+    res = b.calibrate(*planes, mask, 12, iterations=10, init_theta=init, **kw)
+    np.testing.assert_allclose(res["loss_history"], lh, rtol=1e-9)
+    np.testing.assert_allclose(res["theta_history"], thh, rtol=1e-9, atol=1e-12)
+    assert res["best_loss"] == pytest.approx(bl, rel=1e-9)
+    with pytest.raises(eb.InvalidArgument):
+        b.calibrate(*planes, mask * 0, 12, iterations=1)  # no burned cell in the target
+
+
+def test_det_general_form_gradient_vs_dual(port):
+    """The general (per-cell layers) form of the adjoint vs Dual<6>, 30 steps, BCE + pooled MSE."""
+    L, _ = _calib_case(seed=8, h=33, w=29)
+    h, w = L["veg"].shape
+    fire = np.zeros((h, w), np.uint8)
+    fire[5, 7] = fire[20, 20] = 1
+    rs = np.random.default_rng(1)
+    mask = (rs.random((h, w)) < 0.3).astype(np.float64)
+    cfg = [0.25, 0.1, 0.35, 0.9, 1.2, 0.65]
+    b = eb.Batch(1, h, w)
+    b.set_grid(*L.values())
+    b.set_config(cfg)
+    b.set_state(fire)
+    b.det_set_state_from_fire()
+    b.det_forward(30, record=True)
+    loss, grad = b.det_loss_grad(mask, 1.0, 1.0, 4)
+    gp = O.grid_layers(port, "port", *L.values())
+    lo, g6 = O._D(), np.empty(6)
+    port.ebo_det_loss_grad(gp.h, O.ptr(O.cfg_array(cfg)), 30, O.ptr(fire), O.ptr(mask), 1.0, 1.0, 4, lo, O.ptr(g6))
+    assert loss[0] == pytest.approx(lo.value, rel=1e-12)
+    np.testing.assert_allclose(grad[0], g6, rtol=1e-9, atol=1e-14)

@@ -187,3 +187,35 @@ def test_port_vs_ref_dual_loss_grad(port, ref, bce_w, mse_w, pool):
     assert out["port"][0] == out["ref"][0]
     assert np.array_equal(out["port"][1], out["ref"][1])
     assert np.abs(out["ref"][1]).max() > 0
+
+
+def _calib_case(seed=3, h=20, w=17):
+    rs = np.random.default_rng(seed)
+    L = dict(speed=np.full((h, w), 1.5), dir=np.full((h, w), 0.9), veg=rs.random((h, w)) * 0.6 + 0.1,
+             den=rs.random((h, w)) * 0.5 + 0.1, slope8=0.4 * rs.random((h, w, 8)) - 0.2)
+    fire = np.zeros((h, w), np.uint8)
+    fire[h // 2, w // 2] = 1
+    planes = [(fire == k).astype(np.float64) for k in (0, 1, 2)]
+    return L, planes
+
+
+def test_port_vs_ref_calibrate(port, ref):
+    # calibrate.cpp:104-167: Adam through ThetaTransform on Dual<6> rollouts, bitwise
+    L, planes = _calib_case()
+    gp = O.grid_layers(port, "port", *L.values())
+    gr = O.grid_layers(ref, "ref", *L.values())
+    true_theta = [0.22, 0.15, 0.3, 0.8, 1.1, 0.7]
+    un, bu, bd = [p.copy() for p in planes]
+    port.ebo_det_run(gp.h, O.ptr(O.cfg_array(true_theta)), 12, O.ptr(un), O.ptr(bu), O.ptr(bd))
+    mask = ((bu + bd) >= 0.5).astype(np.float64)
+    init = [0.15, 0.2, 0.25, 1.1, 0.9, 0.6]
+    for kw in (dict(), dict(bce_w=0.0, mse_w=1.0, pool=1), dict(optimize=[1, 0, 1, 1, 0, 1])):
+        a = O.calibrate(port, "port", gp, planes, mask, 12, 8, init, **kw)
+        b = O.calibrate(ref, "ref", gr, planes, mask, 12, 8, init, **kw)
+        assert a[0] == b[0] == 0
+        for x, y in zip(a[1:], b[1:]):
+            assert np.array_equal(np.asarray(x), np.asarray(y))
+    assert a[4] < a[1][0]  # the loss went down
+    # invalid init (p_continue outside (0,1)) is rejected by both
+    assert O.calibrate(port, "port", gp, planes, mask, 12, 2, [0.1, 0, 0, 0, 1, 1.5])[0] == -2
+    assert O.calibrate(ref, "ref", gr, planes, mask, 12, 2, [0.1, 0, 0, 0, 1, 1.5])[0] == -1
