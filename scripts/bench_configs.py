@@ -24,6 +24,7 @@ from oracle import oracle as O  # noqa: E402
 PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 FLUSH = None
+STREAM = None  # the stream every timed batch launches on (set in main)
 
 
 def flush_l2():
@@ -42,9 +43,9 @@ def timed(fn, iters, warmup=3):
     for _ in range(iters):
         flush_l2()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
+        s.record(STREAM)
         fn()
-        e.record()
+        e.record(STREAM)
         e.synchronize()
         out.append(s.elapsed_time(e))
     return out
@@ -64,7 +65,7 @@ def line(cfg, metric, value, unit, ms, alg_bytes, extra=None):
 def bench_c0(iters):
     h = w = 64
     z = np.zeros((h, w))
-    stream = torch.cuda.current_stream()
+    stream = STREAM  # a real stream: the legacy default (0) would make the batch use its own
     b = eb.Batch(1, h, w, stream=stream.cuda_stream)
     b.set_grid(z, z, z, z, np.zeros((h, w, 8)))
     fire = np.zeros((1, h, w), np.uint8)
@@ -162,7 +163,7 @@ def bench_c3(iters, size):
     t.wind_speed[:] = 6.0
     t.wind_direction[:] = 0.0
     init = eb.synth_ignitions(0, t, 64)
-    stream = torch.cuda.current_stream()
+    stream = STREAM
     b = eb.Batch(1, h, w, stream=stream.cuda_stream)
     b.set_terrain(t.fuel_class, t.elevation, t.class_veg, t.class_den, 30.0)
     b.set_wind(t.wind_speed, t.wind_direction)
@@ -242,6 +243,8 @@ def main():
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     torch.cuda.set_device(0)
+    global STREAM
+    STREAM = torch.cuda.Stream()
     res = []
     for c in a.configs.split(","):
         if c == "c0":
