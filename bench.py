@@ -38,6 +38,16 @@ N_ENVS, H, W, CA_STEPS, IGNITIONS, SEED = 1024, 128, 128, 200, 5, 0
 ALG_BYTES_PER_CELL_UPDATE = 10  # 1 B state read + 1 B write + 4 B fuel + 4 B elevation
 
 
+def config_json(world: int, kernel: str) -> dict:
+    """The workload description shared by both arms (BASELINE.json configs[1])."""
+    return {"workload": "C1: 1024 envs x 128x128 per GPU, per-env value-noise landcover "
+                        "(11 WorldCover classes) + fractal elevation 0-500 m + wind "
+                        "U(0,10)/U(0,2pi), 5 ignitions, 200 CA steps",
+            "global_batch": N_ENVS * world, "grid": [H, W], "ca_steps": CA_STEPS,
+            "parallelism": f"env-sharded x{world}", "kernel": kernel,
+            "l2": "flushed between timed iterations (256 MiB write)"}
+
+
 def env_ids(rank: int) -> list:
     """Global env ids (= RNG streams, = synthetic-terrain keys) of a rank: weak scaling,
     each rank owns its own N_ENVS envs; no data-path collective."""
@@ -129,8 +139,7 @@ def cpu_reference_sample(n_envs: int, threads: int = 0):
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
-    cfgj = {"workload": "C1: 1024 envs x 128x128, 5 ignitions, 200 CA steps (per-env terrain+wind)",
-            "global_batch": N_ENVS, "grid": [H, W], "ca_steps": CA_STEPS}
+    cfgj = config_json(world, "reference CPU (emberline run_stochastic)")
     # each bench step = a bounded sample of the workload, sized to ~2-4 s of CPU work
     secs, cells, kind, cores, _ = cpu_reference_sample(4)
     n_sample = int(max(4, min(N_ENVS, 4 * 3.0 / max(secs, 1e-3))))
@@ -306,12 +315,7 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_max * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": "C1: 1024 envs x 128x128 per GPU, per-env value-noise landcover "
-                                   "(11 WorldCover classes) + fractal elevation 0-500 m + wind "
-                                   "U(0,10)/U(0,2pi), 5 ignitions, 200 CA steps",
-                       "global_batch": N_ENVS * world, "grid": [H, W], "ca_steps": CA_STEPS,
-                       "parallelism": f"env-sharded x{world}", "kernel": args.kernel,
-                       "l2": "flushed between timed iterations (256 MiB write)"},
+            "config": config_json(world, args.kernel),
             "env_steps_per_sec": value / (H * W),
             "e2e": {"value": e2e_value, "unit": "cell-updates/s",
                     "h2d_bytes_per_step": int(init.nbytes), "d2h_bytes_per_step": int(init.nbytes)},
