@@ -261,6 +261,88 @@ class DeviceBatch {
   int n_, h_, w_;
 };
 
+// ---- engine.hpp (deterministic path, double) + calibrate.hpp -------------------------------
+template <class S>
+struct BasicContinuousState {
+  Grid<S> p_un, p_burn, p_bd;
+  int height() const { return p_un.height(); }
+  int width() const { return p_un.width(); }
+};
+using ContinuousState = BasicContinuousState<double>;
+
+ContinuousState state_from_fire(const FireLayer& fire);
+void validate_state(const ContinuousState& state, double tol = 1e-9);
+FireFractions fire_fraction_stats(const ContinuousState& state);
+
+// step_deterministic / run_deterministic (engine.hpp:147-245) for S = double, on the device in
+// the reference's fp64 arithmetic.
+ContinuousState step_deterministic(const ContinuousState& state, const GridState& grid,
+                                   const SimConfig& cfg, Exec exec = Exec::parallel);
+struct DeterministicRun {
+  ContinuousState final_state;
+  std::vector<ContinuousState> trajectory;
+};
+DeterministicRun run_deterministic(const ContinuousState& initial, const GridState& grid,
+                                   const SimConfig& cfg, int steps, bool record = false,
+                                   const WindSchedule* schedule = nullptr, Exec exec = Exec::parallel);
+
+struct DeterministicBatch {
+  std::uint64_t step = 0;
+  std::vector<ContinuousState> members;
+};
+void step_batch(DeterministicBatch& batch, const GridState& grid, const SimConfig& cfg,
+                Exec exec = Exec::parallel);
+
+inline constexpr std::size_t kParamCount = 6;
+using ParamArray = std::array<double, kParamCount>;
+enum ParamIndex : std::size_t {
+  kParamPBase = 0, kParamAlphaW1 = 1, kParamAlphaW2 = 2, kParamAlphaS = 3, kParamAlphaGamma = 4,
+  kParamPContinue = 5,
+};
+ParamArray params_of(const SimConfig& cfg);
+SimConfig config_from_params(const ParamArray& theta, int max_steps = 200);
+
+struct CalibrationTarget {
+  Grid<double> burn_mask;
+  int horizon = 0;
+};
+struct LossConfig {
+  double bce_weight = 1.0;
+  double mse_weight = 1.0;
+  int pool_size = 4;
+  double bce_epsilon = 1e-6;
+};
+struct CalibrationOptions {
+  int iterations = 300;
+  ParamArray init_theta = params_of(SimConfig{});
+  std::array<bool, kParamCount> optimize = {true, true, true, true, true, true};
+  double lr = 1e-2;
+  int max_horizon = 2000;
+  Exec exec = Exec::parallel;
+};
+struct CalibrationResult {
+  ParamArray best_theta{};
+  double best_loss = 0.0;
+  double initial_loss = 0.0;
+  std::vector<double> loss_history;
+  std::vector<ParamArray> theta_history;
+};
+
+// Loss value and d loss / d theta (ParamIndex order) after `horizon` deterministic steps:
+// the reference gets these from Dual<6> (calibrate.cpp:130-151); here reverse mode on device.
+std::pair<double, ParamArray> loss_and_gradient(const GridState& grid, const ContinuousState& initial,
+                                                const CalibrationTarget& target, const LossConfig& lc,
+                                                const SimConfig& cfg);
+// calibrate (calibrate.cpp:104-167); throws NumericalError on a non-finite loss/gradient.
+CalibrationResult calibrate(const GridState& grid, const ContinuousState& initial,
+                            const CalibrationTarget& target, const LossConfig& lc,
+                            const CalibrationOptions& opts);
+
+class NumericalError : public std::runtime_error {  // errors.hpp:14-17
+ public:
+  using std::runtime_error::runtime_error;
+};
+
 // ---- rl_env.hpp ---------------------------------------------------------------------------
 struct EnvConfig {
   int height = 20, width = 20, window_radius = 2, water_capacity = 30;

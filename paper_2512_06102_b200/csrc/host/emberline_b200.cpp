@@ -17,6 +17,7 @@ namespace {
     case EBL_EINVAL: throw std::invalid_argument(msg);
     case EBL_ELOGIC: throw std::logic_error(msg);
     case EBL_ERANGE: throw std::out_of_range(msg);
+    case EBL_ENUMERIC: throw NumericalError(msg);
     default: throw std::runtime_error("ember_b200: " + msg);
   }
 }
@@ -362,6 +363,170 @@ std::vector<FireFractions> DeviceBatch::fractions() const {
   const double n = static_cast<double>(h_) * w_;
   for (int m = 0; m < n_; ++m) out[m] = {c[m * 4] / n, c[m * 4 + 1] / n, c[m * 4 + 2] / n};
   return out;
+}
+
+// ---- deterministic path + calibrate -----------------------------------------------------------------
+ContinuousState state_from_fire(const FireLayer& fire) {
+  const int h = fire.height(), w = fire.width();
+  ContinuousState s{Grid<double>(h, w), Grid<double>(h, w), Grid<double>(h, w)};
+  for (int i = 0; i < h * w; ++i) {
+    s.p_un[i] = fire[i] == FireState::Unburned ? 1.0 : 0.0;
+    s.p_burn[i] = fire[i] == FireState::Burning ? 1.0 : 0.0;
+    s.p_bd[i] = fire[i] == FireState::Burned ? 1.0 : 0.0;
+  }
+  return s;
+}
+
+void validate_state(const ContinuousState& s, double tol) {
+  const int h = s.height(), w = s.width();
+  if (s.p_burn.height() != h || s.p_burn.width() != w || s.p_bd.height() != h || s.p_bd.width() != w)
+    throw std::invalid_argument("ContinuousState: component dimensions differ");
+  for (int i = 0; i < h * w; ++i) {
+    if (!(s.p_un[i] >= 0.0) || !(s.p_burn[i] >= 0.0) || !(s.p_bd[i] >= 0.0))
+      throw std::invalid_argument("ContinuousState: negative or NaN component");
+    if (std::abs(s.p_un[i] + s.p_burn[i] + s.p_bd[i] - 1.0) > tol)
+      throw std::invalid_argument("ContinuousState: cell probabilities do not sum to 1");
+  }
+}
+
+FireFractions fire_fraction_stats(const ContinuousState& s) {
+  FireFractions f;
+  const double n = s.p_un.size();
+  for (int i = 0; i < s.p_un.size(); ++i) {
+    f.unburned += s.p_un[i];
+    f.burning += s.p_burn[i];
+    f.burned += s.p_bd[i];
+  }
+  f.unburned /= n;
+  f.burning /= n;
+  f.burned /= n;
+  return f;
+}
+
+namespace {
+std::shared_ptr<ebl_batch> det_batch(int members, const GridState& grid, const SimConfig& cfg) {
+  auto b = make_batch(members, grid.height(), grid.width());
+  const ebl_sim_config c = to_c(cfg);
+  ok(ebl_batch_set_config(b.get(), &c));
+  upload_grid(b.get(), grid);
+  return b;
+}
+
+void push_planes(ebl_batch* b, const std::vector<ContinuousState>& states) {
+  const size_t n = static_cast<size_t>(states[0].height()) * states[0].width();
+  std::vector<double> un(n * states.size()), bu(un.size()), bd(un.size());
+  for (size_t m = 0; m < states.size(); ++m) {
+    std::memcpy(un.data() + m * n, states[m].p_un.data().data(), n * sizeof(double));
+    std::memcpy(bu.data() + m * n, states[m].p_burn.data().data(), n * sizeof(double));
+    std::memcpy(bd.data() + m * n, states[m].p_bd.data().data(), n * sizeof(double));
+  }
+  ok(ebl_det_set_state(b, un.data(), bu.data(), bd.data()));
+}
+
+std::vector<ContinuousState> pull_planes(ebl_batch* b, int members, int h, int w) {
+  const size_t n = static_cast<size_t>(h) * w;
+  std::vector<double> un(n * members), bu(un.size()), bd(un.size());
+  ok(ebl_det_get_state(b, un.data(), bu.data(), bd.data()));
+  std::vector<ContinuousState> out;
+  for (int m = 0; m < members; ++m) {
+    ContinuousState s{Grid<double>(h, w), Grid<double>(h, w), Grid<double>(h, w)};
+    std::memcpy(s.p_un.data().data(), un.data() + m * n, n * sizeof(double));
+    std::memcpy(s.p_burn.data().data(), bu.data() + m * n, n * sizeof(double));
+    std::memcpy(s.p_bd.data().data(), bd.data() + m * n, n * sizeof(double));
+    out.push_back(std::move(s));
+  }
+  return out;
+}
+}  // namespace
+
+DeterministicRun run_deterministic(const ContinuousState& initial, const GridState& grid,
+                                   const SimConfig& cfg, int steps, bool record,
+                                   const WindSchedule* schedule, Exec) {
+  DeterministicRun out;
+  const int h = initial.height(), w = initial.width();
+  auto b = det_batch(1, grid, cfg);
+  push_planes(b.get(), {initial});
+  if (record) out.trajectory.push_back(initial);
+  const bool sched = schedule != nullptr && !schedule->empty();
+  if (!record && !sched) {
+    ok(ebl_det_forward(b.get(), steps, 0));
+  } else {
+    for (int t = 0; t < steps; ++t) {
+      if (sched) upload_grid(b.get(), grid.with_wind(schedule->at_step(static_cast<std::uint64_t>(t))));
+      ok(ebl_det_forward(b.get(), 1, 0));
+      if (record) out.trajectory.push_back(pull_planes(b.get(), 1, h, w)[0]);
+    }
+  }
+  out.final_state = pull_planes(b.get(), 1, h, w)[0];
+  return out;
+}
+
+ContinuousState step_deterministic(const ContinuousState& state, const GridState& grid,
+                                   const SimConfig& cfg, Exec exec) {
+  return run_deterministic(state, grid, cfg, 1, false, nullptr, exec).final_state;
+}
+
+void step_batch(DeterministicBatch& batch, const GridState& grid, const SimConfig& cfg, Exec) {
+  if (batch.members.empty()) return;
+  const int h = batch.members[0].height(), w = batch.members[0].width();
+  auto b = det_batch(static_cast<int>(batch.members.size()), grid, cfg);
+  push_planes(b.get(), batch.members);
+  ok(ebl_det_forward(b.get(), 1, 0));
+  batch.members = pull_planes(b.get(), static_cast<int>(batch.members.size()), h, w);
+  batch.step += 1;
+}
+
+ParamArray params_of(const SimConfig& c) {
+  return {c.p_base, c.alpha_w1, c.alpha_w2, c.alpha_s, c.alpha_gamma, c.p_continue};
+}
+
+SimConfig config_from_params(const ParamArray& t, int max_steps) {
+  return SimConfig{t[0], t[1], t[2], t[3], t[4], t[5], max_steps};
+}
+
+std::pair<double, ParamArray> loss_and_gradient(const GridState& grid, const ContinuousState& initial,
+                                                const CalibrationTarget& target, const LossConfig& lc,
+                                                const SimConfig& cfg) {
+  auto b = det_batch(1, grid, cfg);
+  push_planes(b.get(), {initial});
+  ok(ebl_det_forward(b.get(), target.horizon, 1));
+  double l = 0.0;
+  ParamArray g{};
+  ok(ebl_det_loss_grad(b.get(), target.burn_mask.data().data(), lc.bce_weight, lc.mse_weight,
+                       lc.pool_size, &l, g.data()));
+  return {l, g};
+}
+
+CalibrationResult calibrate(const GridState& grid, const ContinuousState& initial,
+                            const CalibrationTarget& target, const LossConfig& lc,
+                            const CalibrationOptions& opts) {
+  if (target.burn_mask.height() != grid.height() || target.burn_mask.width() != grid.width())
+    throw std::invalid_argument("CalibrationTarget: mask dimensions differ from the grid");
+  if (opts.iterations < 0) throw std::invalid_argument("calibrate: negative iteration count");
+  auto b = det_batch(1, grid, SimConfig{});
+  ebl_calib_options o{};
+  ebl_default_calib_options(&o);
+  o.iterations = opts.iterations;
+  for (std::size_t i = 0; i < kParamCount; ++i) {
+    o.init_theta[i] = opts.init_theta[i];
+    o.optimize[i] = opts.optimize[i] ? 1 : 0;
+  }
+  o.lr = opts.lr;
+  o.max_horizon = opts.max_horizon;
+  CalibrationResult r;
+  r.loss_history.resize(opts.iterations + 1);
+  std::vector<double> th((opts.iterations + 1) * kParamCount);
+  ok(ebl_calibrate(b.get(), initial.p_un.data().data(), initial.p_burn.data().data(),
+                   initial.p_bd.data().data(), target.burn_mask.data().data(), target.horizon,
+                   lc.bce_weight, lc.mse_weight, lc.pool_size, &o, r.loss_history.data(), th.data(),
+                   r.best_theta.data(), &r.best_loss));
+  for (int i = 0; i <= opts.iterations; ++i) {
+    ParamArray t;
+    for (std::size_t k = 0; k < kParamCount; ++k) t[k] = th[i * kParamCount + k];
+    r.theta_history.push_back(t);
+  }
+  r.initial_loss = r.loss_history.front();
+  return r;
 }
 
 // ---- rl_env.hpp ----------------------------------------------------------------------------------

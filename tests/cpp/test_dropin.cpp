@@ -3,6 +3,7 @@
 // (include/emberline_b200.hpp, every step on the GPU), compared bit for bit.
 // Mirrors the reference's own checks: test_engine.cpp:265-376, test_rl_env.cpp:234-253.
 #define emberline ebl_ref
+#include "emberline/calibrate.hpp"
 #include "emberline/engine.hpp"
 #include "emberline/reference.hpp"
 #include "emberline/rl_env.hpp"
@@ -222,6 +223,74 @@ static void test_rl_env() {
   CHECK(D::observation_size(D::default_preset()) == R::observation_size(R::default_preset()));
 }
 
+template <class A, class B>
+static double max_rel(const A& a, const B& b) {
+  double m = 0.0;
+  for (int i = 0; i < a.size(); ++i) {
+    const double d = std::abs(a[i] - b[i]) / std::max(1e-300, std::max(std::abs(a[i]), std::abs(b[i])));
+    if (std::abs(a[i] - b[i]) > 1e-15) m = std::max(m, d);
+  }
+  return m;
+}
+
+static void test_deterministic_and_calibrate() {
+  // run_deterministic<double> (engine.hpp:225-245): the device runs the reference's fp64 arithmetic
+  const Layers L = varied(29, 16, 16);
+  R::SimConfig rc;
+  D::SimConfig dc;
+  R::FireLayer f(16, 16, R::FireState::Unburned);
+  f(8, 8) = f(3, 12) = R::FireState::Burning;
+  const R::ContinuousState rs = R::state_from_fire(f);
+  const D::ContinuousState ds = D::state_from_fire(to_dev(f));
+  const auto ra = R::run_deterministic(rs, ref_grid(L), rc, 60, true);
+  const auto da = D::run_deterministic(ds, dev_grid(L), dc, 60, true);
+  CHECK(da.trajectory.size() == ra.trajectory.size());
+  CHECK(max_rel(ra.final_state.p_burn, da.final_state.p_burn) < 1e-12);
+  CHECK(max_rel(ra.final_state.p_un, da.final_state.p_un) < 1e-12);
+  CHECK(max_rel(ra.trajectory[30].p_bd, da.trajectory[30].p_bd) < 1e-12);
+  const auto rf = R::fire_fraction_stats(ra.final_state);
+  const auto df = D::fire_fraction_stats(da.final_state);
+  CHECK(std::abs(rf.burning - df.burning) < 1e-12 && std::abs(rf.burned - df.burned) < 1e-12);
+  const auto r1 = R::step_deterministic(rs, ref_grid(L), rc);
+  const auto d1 = D::step_deterministic(ds, dev_grid(L), dc);
+  CHECK(max_rel(r1.p_burn, d1.p_burn) == 0.0);
+  R::DeterministicBatch rb;
+  rb.members.assign(3, rs);
+  D::DeterministicBatch db;
+  db.members.assign(3, ds);
+  for (int t = 0; t < 5; ++t) {
+    R::step_batch(rb, ref_grid(L), rc);
+    D::step_batch(db, dev_grid(L), dc);
+  }
+  CHECK(db.step == 5 && max_rel(rb.members[2].p_burn, db.members[2].p_burn) < 1e-12);
+  CHECK(throws<std::invalid_argument>([&] {
+    D::ContinuousState bad = ds;
+    bad.p_un[0] = 0.5;
+    D::validate_state(bad);
+  }));
+  // calibrate (calibrate.cpp:104-167): reference Dual<6> forward mode vs device reverse mode
+  R::Grid<double> mask_r(16, 16);
+  D::Grid<double> mask_d(16, 16);
+  const auto tgt_run = R::run_deterministic(rs, ref_grid(L), R::config_from_params({0.22, 0.15, 0.3, 0.8, 1.1, 0.7}), 12);
+  for (int i = 0; i < 256; ++i)
+    mask_r[i] = mask_d[i] = (tgt_run.final_state.p_burn[i] + tgt_run.final_state.p_bd[i]) >= 0.5 ? 1.0 : 0.0;
+  const R::CalibrationTarget rt{mask_r, 12};
+  const D::CalibrationTarget dt{mask_d, 12};
+  R::CalibrationOptions ro;
+  D::CalibrationOptions dop;
+  ro.iterations = dop.iterations = 8;
+  ro.init_theta = {0.15, 0.2, 0.25, 1.1, 0.9, 0.6};
+  dop.init_theta = {0.15, 0.2, 0.25, 1.1, 0.9, 0.6};
+  const auto rres = R::calibrate(ref_grid(L), rs, rt, R::LossConfig{}, ro);
+  const auto dres = D::calibrate(dev_grid(L), ds, dt, D::LossConfig{}, dop);
+  CHECK(dres.loss_history.size() == rres.loss_history.size());
+  for (std::size_t i = 0; i < rres.loss_history.size(); ++i)
+    CHECK(std::abs(rres.loss_history[i] - dres.loss_history[i]) <= 1e-9 * std::abs(rres.loss_history[i]));
+  for (int k = 0; k < 6; ++k) CHECK(std::abs(rres.best_theta[k] - dres.best_theta[k]) <= 1e-9);
+  const auto lg = D::loss_and_gradient(dev_grid(L), ds, dt, D::LossConfig{}, D::config_from_params(dop.init_theta));
+  CHECK(std::abs(lg.first - rres.loss_history[0]) <= 1e-12 * rres.loss_history[0]);
+}
+
 static void test_validation() {
   CHECK(throws<std::invalid_argument>([] { D::Grid<double>(0, 3); }));
   CHECK(throws<std::invalid_argument>([] { D::WindField::uniform(2, 2, -1.0, 0.0); }));
@@ -244,6 +313,7 @@ int main() {
   test_wind_schedule();
   test_batches();
   test_rl_env();
+  test_deterministic_and_calibrate();
   std::printf("dropin: %d checks, %d failures\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
