@@ -106,6 +106,22 @@ uint64_t ebl_batch_step_index(const ebl_batch* b);
  * {seed, step+t, stream[e]}; the batch step counter advances by n_steps. */
 int ebl_step_batch(ebl_batch* b, int n_steps);
 
+/* run_stochastic(record=true) (engine.cpp:108,116): ebl_step_batch that also stores the layers
+ * after every step into traj [n_steps][n_envs][H*W] (device pointer when on_device, else host;
+ * the initial layers are the caller's).  The blocked kernel writes them from shared memory as
+ * it goes: no per-step launches or host syncs. */
+int ebl_step_batch_record(ebl_batch* b, int n_steps, void* traj, int on_device);
+
+/* WindSchedule (engine.hpp:188-199, engine.cpp:74-86) on the device: step t of a run uses the
+ * entry min(t, n_sched - 1) of the absolute step index t (run_stochastic, engine.cpp:110-112).
+ * Terrain form: uniform winds speed/dir [n_sched][n_winds] (n_winds = 1 or n_envs); n_sched = 0
+ * sets a constant wind.  General form: per-cell WindFields [n_sched][n_grids][H*W]; the fp64
+ * SpreadTables are built once per entry. */
+int ebl_batch_set_wind_schedule(ebl_batch* b, int n_sched, int n_winds, const double* speed,
+                                const double* direction);
+int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* speed,
+                                     const double* direction);
+
 /* Kernel selection for ebl_step_batch (results are identical by construction):
  *  AUTO      the bit-sliced blocked kernel: one CTA per env with all n steps fused when an
  *            env fits shared memory (H*W <= 65536), else light-cone-halo tiles, 8 steps

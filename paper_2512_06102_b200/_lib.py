@@ -103,6 +103,9 @@ SIGNATURES = {
     "ebl_batch_step_index": (_U64, [_P]),
     "ebl_step_batch": (_I, [_P, _I]),
     "ebl_batch_set_kernel": (_I, [_P, _I]),
+    "ebl_step_batch_record": (_I, [_P, _I, _P, _I]),
+    "ebl_batch_set_wind_schedule": (_I, [_P, _I, _I, _P, _P]),
+    "ebl_batch_set_grid_wind_schedule": (_I, [_P, _I, _P, _P]),
     "ebl_batch_set_tiling": (_I, [_P, _I, _I, _I]),
     "ebl_batch_set_row_offset": (_I, [_P, C.c_int64]),
     "ebl_batch_copy_rows": (_I, [_P, _I, _P, _I, _I]),

@@ -99,6 +99,27 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
   const int tr0 = r0 - R0, tr1 = min(r0 + g.tile_h, BH) - R0;
   const int tc0 = c0 - C0, tc1 = min(c0 + g.tile_w, W) - C0;
   int cur = 0;
+  const int tj0 = tc0 >> 5, tj1 = (tc1 + 31) >> 5;
+  const int twords = tj1 - tj0;
+  // bit-planes of the output tile -> uint8 layer at `layer` (+ U/B/X counts when cnt3)
+  auto store_tile = [&](const uint32_t* Bs, uint8_t* __restrict__ layer, int32_t* cnt3) {
+    for (WordIter it(twords, (tr1 - tr0) * twords); it.ok(); it.next()) {
+      const int rr = tr0 + it.r, j = tj0 + it.j;
+      const uint32_t b = Bs[(rr + 1) * S + j], x = X[rr * S + j];
+      const int nc = min(32, RW - 32 * j);
+      if (cnt3) {
+        cnt3[0] += nc - __popc(b) - __popc(x);
+        cnt3[1] += __popc(b);
+        cnt3[2] += __popc(x);
+      }
+      uint8_t* dst = layer + static_cast<size_t>(R0 + rr) * W + C0 + 32 * j;
+      if (nc == 32 && vec) {
+        bits_to_bytes(b, x, dst);
+      } else {
+        for (int k = 0; k < nc; ++k) dst[k] = static_cast<uint8_t>(((b >> k) & 1u) | (((x >> k) & 1u) << 1));
+      }
+    }
+  };
 
   for (int t = 0; t < g.n_steps; ++t) {
     const uint32_t* B = Bp[cur];
@@ -109,6 +130,7 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
       s_newly[par ^ 1] = 0;
     }
     const uint64_t prefix = key_prefix(a.seed, stream, a.step + static_cast<uint64_t>(t));
+    const int srow = sched_row(a, a.step + static_cast<uint64_t>(t));  // wind in force
     // ---- P1: each thread owns whole rows; the 3x3 dilation slides along the row in
     //      registers (3 shared loads per word: north, own, south) ------------------------------
     int cnt = 0;
@@ -195,7 +217,7 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
           if (uc < 0 || uc >= RW) continue;  // padding rows cover ur = -1 and ur = RH
           nb |= ((B[(ur + 1) * S + (uc >> 5)] >> (uc & 31)) & 1u) << k;
         }
-        if (ignite<MODE>(a, env, R0 + rr, C0 + cc, nb, m, dg)) {
+        if (ignite<MODE>(a, env, R0 + rr, C0 + cc, nb, m, dg, srow)) {
           atomicOr(Bn + wi, bit);
           newly += (rr >= tr0 && rr < tr1 && cc >= tc0 && cc < tc1);
         }
@@ -220,28 +242,14 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
     }
     __syncthreads();
     cur ^= 1;
+    if (a.traj)  // record (run_stochastic(record=true), engine.cpp:116): this step's tile
+      store_tile(Bp[cur], a.traj + ((a.traj_t0 + t) * a.n_envs + env) * ncell, nullptr);
   }
 
   // ---- store the tile: bit-planes -> uint8, counts -----------------------------------------
-  const uint32_t* B = Bp[cur];
-  uint8_t* __restrict__ out = a.out + env * ncell;
-  int32_t nU = 0, nB = 0, nX = 0;
-  const int tj0 = tc0 >> 5, tj1 = (tc1 + 31) >> 5;
-  const int twords = tj1 - tj0;
-  for (WordIter it(twords, (tr1 - tr0) * twords); it.ok(); it.next()) {
-    const int rr = tr0 + it.r, j = tj0 + it.j;
-    const uint32_t b = B[(rr + 1) * S + j], x = X[rr * S + j];
-    const int nc = min(32, RW - 32 * j);
-    nB += __popc(b);
-    nX += __popc(x);
-    nU += nc - __popc(b) - __popc(x);
-    uint8_t* dst = out + static_cast<size_t>(R0 + rr) * W + C0 + 32 * j;
-    if (nc == 32 && vec) {
-      bits_to_bytes(b, x, dst);
-    } else {
-      for (int k = 0; k < nc; ++k) dst[k] = static_cast<uint8_t>(((b >> k) & 1u) | (((x >> k) & 1u) << 1));
-    }
-  }
+  int32_t cnt3[3] = {0, 0, 0};
+  store_tile(Bp[cur], a.out + env * ncell, cnt3);
+  const int32_t nU = cnt3[0], nB = cnt3[1], nX = cnt3[2];
   if (a.counts) {
     atomicAdd(&s_cnt[0], nU);
     atomicAdd(&s_cnt[1], nB);

@@ -79,6 +79,9 @@ struct ebl_batch {
 
   uint64_t seed = 0, step = 0;
   int64_t row_off = 0;  // global row of layer row 0 (row-sharded landscapes)
+  int sched_len = 0;    // wind schedule entries (0: constant wind)
+  uint8_t* traj_out = nullptr;  // device trajectory of the ebl_step_batch in flight (record)
+  std::vector<double> g_sched_speed, g_sched_dir;  // general form: [S][grid][cell]
   bool streams_uploaded = false;
   std::vector<uint64_t> h_streams;
   DevBuf<uint64_t> streams;
@@ -143,12 +146,17 @@ int prepare(ebl_batch* b) {
   const Cfg6 c = cfg6(b->cfg);
   if (b->mode == ebl::kStaticTables && b->tables_dirty) {
     const size_t n = b->ncell * b->n_grids;
-    std::vector<double> pot(n * 8), gam(n);
-    ebl::build_tables(n, b->g_speed.data(), b->g_dir.data(), b->g_veg.data(), b->g_den.data(),
-                      b->g_slope.data(), c, pot.data(), gam.data());
-    EBL_CUDA(b->pot.alloc(n * 8));
+    const int S = std::max(1, b->sched_len);  // one table per wind-schedule entry
+    std::vector<double> pot(n * 8 * S), gam(n);
+    for (int s = 0; s < S; ++s) {
+      const double* sp = b->sched_len ? b->g_sched_speed.data() + s * n : b->g_speed.data();
+      const double* dr = b->sched_len ? b->g_sched_dir.data() + s * n : b->g_dir.data();
+      ebl::build_tables(n, sp, dr, b->g_veg.data(), b->g_den.data(), b->g_slope.data(), c,
+                        pot.data() + s * n * 8, gam.data());
+    }
+    EBL_CUDA(b->pot.alloc(n * 8 * S));
     EBL_CUDA(b->gamma.alloc(n));
-    EBL_CUDA(cudaMemcpyAsync(b->pot.p, pot.data(), n * 8 * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaMemcpyAsync(b->pot.p, pot.data(), pot.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
     EBL_CUDA(cudaMemcpyAsync(b->gamma.p, gam.data(), n * sizeof(double), cudaMemcpyHostToDevice, b->stream));
     EBL_CUDA(cudaStreamSynchronize(b->stream));
     b->tables_dirty = false;
@@ -167,9 +175,11 @@ int prepare(ebl_batch* b) {
       p32[256 + k] = static_cast<float>(p64[256 + k]);
       p32[512 + k] = static_cast<float>((1.0 + v) * (1.0 + d));  // F = (1+veg)(1+den), deterministic adjoint
     }
-    std::vector<double> k64(static_cast<size_t>(b->n_winds) * 8);
+    // kappa_wind of every wind [schedule entry][wind set] (wind_speed holds S * n_winds entries)
+    const size_t nw = b->wind_speed.size();
+    std::vector<double> k64(nw * 8);
     std::vector<float> k32(k64.size());
-    for (int e = 0; e < b->n_winds; ++e) ebl::kappa_wind8(b->wind_speed[e], b->wind_dir[e], c, &k64[e * 8]);
+    for (size_t e = 0; e < nw; ++e) ebl::kappa_wind8(b->wind_speed[e], b->wind_dir[e], c, &k64[e * 8]);
     for (size_t i = 0; i < k64.size(); ++i) k32[i] = static_cast<float>(k64[i]);
     EBL_CUDA(b->pal32.alloc(768));
     EBL_CUDA(b->pal64.alloc(1024));
@@ -209,6 +219,9 @@ ebl::StepArgs step_args(const ebl_batch* b) {
   a.kw32 = b->kw32.p;
   a.kw64 = b->kw64.p;
   a.kw_stride = b->n_winds > 1 ? 8 : 0;
+  a.sched_len = b->sched_len;
+  a.kw_sched_stride = static_cast<size_t>(b->n_winds) * 8;
+  a.pot_sched_stride = b->ncell * b->n_grids * 8;
   a.alpha_s = b->cfg.alpha_s;
   a.alpha_s32 = static_cast<float>(b->cfg.alpha_s);
   const double d0 = b->cellsize * 1.0, d1 = b->cellsize * 1.41421356237309504880;  // geodata.cpp:222-223
@@ -332,6 +345,9 @@ int ebl_batch_set_grid(ebl_batch* b, int n_grids, const double* speed, const dou
   b->g_slope.assign(slope8, slope8 + n * 8);
   b->mode = ebl::kStaticTables;
   b->n_grids = n_grids;
+  b->sched_len = 0;
+  b->g_sched_speed.clear();
+  b->g_sched_dir.clear();
   b->tables_dirty = true;
   b->det_tables_valid = false;
   b->fuel.reset();
@@ -389,10 +405,71 @@ int ebl_batch_set_wind(ebl_batch* b, int n_winds, const double* speed, const dou
     if (!std::isfinite(dir[i])) return set_err(EBL_EINVAL, "WindField: non-finite direction");
   }
   b->n_winds = n_winds;
+  b->sched_len = 0;
   b->wind_speed.assign(speed, speed + n_winds);
   b->wind_dir.assign(dir, dir + n_winds);
   b->derived_dirty = true;
   b->det_tables_valid = false;
+  return EBL_OK;
+}
+
+int ebl_batch_set_wind_schedule(ebl_batch* b, int n_sched, int n_winds, const double* speed,
+                                const double* dir) {
+  if (int e = check_batch(b)) return e;
+  if (n_sched == 0) return ebl_batch_set_wind(b, n_winds, speed, dir);  // constant wind
+  if (n_sched < 0) return set_err(EBL_EINVAL, "schedule length must be >= 0");
+  if (n_winds != 1 && n_winds != b->n_envs) return set_err(EBL_EINVAL, "n_winds must be 1 or n_envs");
+  const size_t m = static_cast<size_t>(n_sched) * n_winds;
+  for (size_t i = 0; i < m; ++i) {
+    if (!std::isfinite(speed[i])) return set_err(EBL_EINVAL, "WindField: non-finite speed");
+    if (speed[i] < 0.0) return set_err(EBL_EINVAL, "WindField: negative speed");
+    if (!std::isfinite(dir[i])) return set_err(EBL_EINVAL, "WindField: non-finite direction");
+  }
+  b->n_winds = n_winds;
+  b->sched_len = n_sched;
+  b->wind_speed.assign(speed, speed + m);
+  b->wind_dir.assign(dir, dir + m);
+  b->derived_dirty = true;
+  b->det_tables_valid = false;
+  return EBL_OK;
+}
+
+int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* speed, const double* dir) {
+  if (int e = check_batch(b)) return e;
+  if (b->mode != ebl::kStaticTables) return set_err(EBL_ESTATE, "a per-cell wind schedule needs ebl_batch_set_grid first");
+  if (n_sched < 0) return set_err(EBL_EINVAL, "schedule length must be >= 0");
+  const size_t m = static_cast<size_t>(n_sched) * b->ncell * b->n_grids;
+  for (size_t i = 0; i < m; ++i) {  // WindSchedule of WindFields (engine.cpp:74-86, grid.cpp:49-62)
+    if (!std::isfinite(speed[i])) return set_err(EBL_EINVAL, "WindField: non-finite speed");
+    if (speed[i] < 0.0) return set_err(EBL_EINVAL, "WindField: negative speed");
+    if (!std::isfinite(dir[i])) return set_err(EBL_EINVAL, "WindField: non-finite direction");
+  }
+  b->sched_len = n_sched;
+  b->g_sched_speed.assign(speed, speed + m);
+  b->g_sched_dir.assign(dir, dir + m);
+  b->tables_dirty = true;
+  return EBL_OK;
+}
+
+int ebl_step_batch_record(ebl_batch* b, int n_steps, void* traj, int on_device) {
+  if (int e = check_batch(b)) return e;
+  if (n_steps < 0 || (n_steps > 0 && !traj)) return set_err(EBL_EINVAL, "bad trajectory arguments");
+  if (n_steps == 0) return EBL_OK;
+  const size_t bytes = static_cast<size_t>(n_steps) * b->n_envs * b->ncell;
+  DevBuf<uint8_t> tmp;
+  uint8_t* dst = static_cast<uint8_t*>(traj);
+  if (!on_device) {
+    EBL_CUDA(tmp.alloc(bytes));
+    dst = tmp.p;
+  }
+  b->traj_out = dst;
+  const int rc = ebl_step_batch(b, n_steps);
+  b->traj_out = nullptr;
+  if (rc) return rc;
+  if (!on_device) {
+    EBL_CUDA(cudaMemcpyAsync(traj, tmp.p, bytes, cudaMemcpyDeviceToHost, b->stream));
+    EBL_CUDA(cudaStreamSynchronize(b->stream));
+  }
   return EBL_OK;
 }
 
@@ -478,6 +555,11 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
       b->cur ^= 1;
       b->step += 1;
       b->launches += 1;
+      if (b->traj_out) {  // record: this step's layers
+        const size_t layer = b->ncell * b->n_envs;
+        EBL_CUDA(cudaMemcpyAsync(b->traj_out + t * layer, b->state[b->cur].p, layer,
+                                 cudaMemcpyDeviceToDevice, b->stream));
+      }
     }
   } else {  // bit-sliced blocked kernel: whole env per CTA when it fits, else halo tiles
     const bool force_tiles = b->kernel == EBL_KERNEL_BLOCKED;
@@ -498,6 +580,8 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
         EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
         a.counts = b->counts.p;
       }
+      a.traj = b->traj_out;  // record: the kernel stores every step's tile (no extra launches)
+      a.traj_t0 = static_cast<size_t>(done);
       EBL_CUDA(ebl::launch_step_blocked(a, b->mode, g, b->stream));
       b->cur ^= 1;
       b->step += g.n_steps;

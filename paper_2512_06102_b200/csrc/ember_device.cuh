@@ -157,7 +157,14 @@ __device__ __forceinline__ bool ignite_terrain(const TerrainView& t, int w, int 
   return u < p;
 }
 
-__device__ __forceinline__ TerrainView terrain_view(const StepArgs& a, int env) {
+// Row of a wind schedule in force at absolute step `step` (WindSchedule::at_step clamps to the
+// last entry, engine.cpp:81-86); 0 without a schedule.
+__device__ __forceinline__ int sched_row(const StepArgs& a, uint64_t step) {
+  return a.sched_len > 1 ? static_cast<int>(step < static_cast<uint64_t>(a.sched_len - 1) ? step : a.sched_len - 1)
+                         : 0;
+}
+
+__device__ __forceinline__ TerrainView terrain_view(const StepArgs& a, int env, int srow = 0) {
   TerrainView t;
   const size_t base = static_cast<size_t>(env) * a.ter_stride;
   t.fuel = a.fuel + base;
@@ -166,8 +173,8 @@ __device__ __forceinline__ TerrainView terrain_view(const StepArgs& a, int env) 
   t.pal_gam32 = a.pal32 + 256;
   t.pal_src64 = a.pal64;
   t.pal_gam64 = a.pal64 + 256;
-  t.kw32 = a.kw32 + env * a.kw_stride;
-  t.kw64 = a.kw64 + env * a.kw_stride;
+  t.kw32 = a.kw32 + static_cast<size_t>(srow) * a.kw_sched_stride + env * a.kw_stride;
+  t.kw64 = a.kw64 + static_cast<size_t>(srow) * a.kw_sched_stride + env * a.kw_stride;
   t.alpha_s32 = a.alpha_s32;
   t.alpha_s = a.alpha_s;
   t.inv_dist32[0] = a.inv_dist32[0];
@@ -179,14 +186,16 @@ __device__ __forceinline__ TerrainView terrain_view(const StepArgs& a, int env) 
 }
 
 // Decision for an Unburned cell with burning-neighbour mask nb != 0.
+// `srow` selects the wind-schedule entry in force (sched_row).
 template <int MODE>
 __device__ __forceinline__ bool ignite(const StepArgs& a, int env, int r, int c, uint32_t nb,
-                                       uint64_t m, const DiagCounters& dg) {
+                                       uint64_t m, const DiagCounters& dg, int srow = 0) {
   if constexpr (MODE == kStaticTables) {
     const size_t base = static_cast<size_t>(env) * a.tab_stride;
-    return ignite_tables(a.pot + base * 8, a.gamma + base, a.w, r, c, nb, m, dg);
+    return ignite_tables(a.pot + static_cast<size_t>(srow) * a.pot_sched_stride + base * 8,
+                         a.gamma + base, a.w, r, c, nb, m, dg);
   } else {
-    return ignite_terrain(terrain_view(a, env), a.w, r, c, nb, m, dg);
+    return ignite_terrain(terrain_view(a, env, srow), a.w, r, c, nb, m, dg);
   }
 }
 

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kTileThreads) k_step_tile(StepArgs a) {
       ns = 0;
       if (nb) {
         const uint64_t m = cell_bits53(prefix, static_cast<uint64_t>(a.row_off + r) * W + c, 0);
-        ns = ignite<MODE>(a, env, r, c, nb, m, dg) ? 1 : 0;
+        ns = ignite<MODE>(a, env, r, c, nb, m, dg, sched_row(a, a.step)) ? 1 : 0;
         nNew += ns;
       }
     }
@@ -113,14 +113,15 @@ __global__ void k_intensity(StepArgs a, float* lam_out, float* p_out) {
     float lam = 0.f, p = 0.f;
     if constexpr (MODE == kStaticTables) {
       const size_t base = static_cast<size_t>(env) * a.tab_stride;
+      const double* pot = a.pot + static_cast<size_t>(sched_row(a, a.step)) * a.pot_sched_stride;
       double l = 0.0;
       for (int k = 0; k < 8; ++k)
         if (nb & (1u << k))
-          l = __dadd_rn(l, a.pot[(base + (r - kDy[k]) * a.w + (c - kDx[k])) * 8 + k]);
+          l = __dadd_rn(l, pot[(base + (r - kDy[k]) * a.w + (c - kDx[k])) * 8 + k]);
       lam = static_cast<float>(l);
       p = static_cast<float>(__dsub_rn(1.0, exp(-__dmul_rn(a.gamma[base + i], l))));
     } else {
-      const TerrainView t = terrain_view(a, env);
+      const TerrainView t = terrain_view(a, env, sched_row(a, a.step));
       lam = terrain_lambda32(t, a.w, r, c, nb);
       p = -expm1f(-t.pal_gam32[t.fuel[i]] * lam);
     }

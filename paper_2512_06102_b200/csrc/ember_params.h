@@ -35,6 +35,11 @@ struct StepArgs {
   const float* kw32;              // [wind][8]
   const double* kw64;
   int kw_stride;                  // 8 or 0
+  int sched_len;                  // wind schedule entries (0/1: constant wind)
+  size_t kw_sched_stride;         // kw elements per schedule entry (terrain form)
+  size_t pot_sched_stride;        // pot elements per schedule entry (general form)
+  uint8_t* traj;                  // [step][env][cell] states after each step (record), or null
+  size_t traj_t0;                 // trajectory slot of this launch's first step
   float alpha_s32;
   double alpha_s;
   float inv_dist32[2];

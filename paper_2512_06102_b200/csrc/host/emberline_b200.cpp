@@ -250,17 +250,27 @@ StochasticRun run_stochastic(const FireLayer& initial, const GridState& grid, co
   ok(ebl_batch_set_state(b.get(), v.data()));
   ok(ebl_batch_set_key(b.get(), key.seed, key.step, &key.stream, 0));
   if (record) out.trajectory.push_back(initial);
-  const bool sched = schedule != nullptr && !schedule->empty();
-  if (!record && !sched) {
-    if (steps > 0) ok(ebl_step_batch(b.get(), steps));  // one fused launch on the device
-  } else {
-    for (int t = 0; t < steps; ++t) {
-      if (sched) upload_grid(b.get(), grid.with_wind(schedule->at_step(key.step + t)));
-      ok(ebl_step_batch(b.get(), 1));
-      if (record) {
-        ok(ebl_batch_get_state(b.get(), v.data()));
-        out.trajectory.push_back(layer_of(h, w, v.data()));
-      }
+  if (schedule != nullptr && !schedule->empty() && steps > 0) {
+    // the entries a run of `steps` from key.step can reach (engine.cpp:110-112), uploaded once;
+    // the device indexes them by absolute step
+    const std::uint64_t last = std::min<std::uint64_t>(key.step + steps - 1, schedule->size() - 1);
+    const std::size_t n = static_cast<std::size_t>(h) * w;
+    std::vector<double> sp((last + 1) * n), dr((last + 1) * n);
+    for (std::uint64_t s = 0; s <= last; ++s) {
+      const WindField& wf = schedule->at_step(s);
+      std::memcpy(sp.data() + s * n, wf.speed_layer().data().data(), n * sizeof(double));
+      std::memcpy(dr.data() + s * n, wf.direction_layer().data().data(), n * sizeof(double));
+    }
+    ok(ebl_batch_set_grid_wind_schedule(b.get(), static_cast<int>(last + 1), sp.data(), dr.data()));
+  }
+  if (steps > 0) {
+    if (record) {  // every step's layer, written by the kernel as it goes
+      std::vector<std::uint8_t> traj(static_cast<std::size_t>(steps) * h * w);
+      ok(ebl_step_batch_record(b.get(), steps, traj.data(), 0));
+      for (int t = 0; t < steps; ++t)
+        out.trajectory.push_back(layer_of(h, w, traj.data() + static_cast<std::size_t>(t) * h * w));
+    } else {
+      ok(ebl_step_batch(b.get(), steps));  // one fused launch on the device
     }
   }
   ok(ebl_batch_get_state(b.get(), v.data()));

@@ -145,6 +145,25 @@ class Batch:
         """step_batch (engine.cpp:134-159) n_steps times, asynchronously on the batch stream."""
         check(lib().ebl_step_batch(self._h, n_steps))
 
+    def step_record(self, n_steps: int) -> np.ndarray:
+        """step(n_steps) keeping every step's layers (run_stochastic record=true, engine.cpp:116):
+        [n_steps, n_envs, H, W] uint8 (the initial layers are not included)."""
+        out = np.empty((n_steps, self.n_envs, self.height, self.width), dtype=np.uint8)
+        check(lib().ebl_step_batch_record(self._h, n_steps, _ptr(out), 0))
+        return out
+
+    def set_wind_schedule(self, speed, direction) -> None:
+        """Terrain-form WindSchedule: speed/direction [n_sched, n_winds] (n_winds 1 or n_envs)."""
+        sp = np.ascontiguousarray(np.atleast_2d(speed), dtype=np.float64)
+        dr = np.ascontiguousarray(np.atleast_2d(direction), dtype=np.float64)
+        check(lib().ebl_batch_set_wind_schedule(self._h, sp.shape[0], sp.shape[1], _ptr(sp), _ptr(dr)))
+
+    def set_grid_wind_schedule(self, speed, direction) -> None:
+        """General-form WindSchedule of per-cell WindFields: [n_sched, n_grids, H, W]."""
+        sp = np.ascontiguousarray(speed, dtype=np.float64)
+        dr = np.ascontiguousarray(direction, dtype=np.float64)
+        check(lib().ebl_batch_set_grid_wind_schedule(self._h, sp.shape[0], _ptr(sp), _ptr(dr)))
+
     def sync(self) -> None:
         check(lib().ebl_batch_sync(self._h))
 

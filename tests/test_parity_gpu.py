@@ -353,3 +353,73 @@ def test_large_single_grid_vs_oracle(port):
     assert np.array_equal(outs[0], outs[1])
     g = O.grid_terrain(port, "port", t.veg()[0], t.den()[0], t.elevation[0], 30.0, 6.0, 0.0)
     assert np.array_equal(outs[0][0], O.run(port, "port", g, O.DEFAULT_CFG, 11, 0, 0, 60, init[0]))
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_record_trajectory_vs_oracle(port, kernel):
+    """run_stochastic(record=true) (engine.cpp:108,116) on the device: every step's layers."""
+    n, h, w, steps = 3, 96, 64, 40
+    t = eb.synth_terrain(2, n, h, w)
+    init = eb.synth_ignitions(2, t, 6)
+    b = _terrain_batch(t, None, kernel)
+    b.set_state(init)
+    b.set_key(2, 5, first_stream=7)
+    traj = b.step_record(steps)
+    assert np.array_equal(traj[-1], b.get_state())
+    for e in range(n):
+        g = O.grid_terrain(port, "port", t.veg()[e], t.den()[e], t.elevation[e], 30.0,
+                           t.wind_speed[e], t.wind_direction[e])
+        st = init[e]
+        for s in range(steps):
+            st = O.run(port, "port", g, O.DEFAULT_CFG, 2, 5 + s, 7 + e, 1, st)
+            assert np.array_equal(traj[s, e], st), (e, s)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_wind_schedule_terrain_vs_oracle(port, kernel):
+    """WindSchedule (engine.hpp:188-199) on the device: per-step winds, held past the end."""
+    n, h, w, steps = 4, 64, 80, 30
+    t = eb.synth_terrain(4, n, h, w)
+    init = eb.synth_ignitions(4, t, 5)
+    rs = np.random.default_rng(0)
+    S = 7
+    sp = 8 * rs.random((S, n))
+    dr = 6.3 * rs.random((S, n))
+    b = _terrain_batch(t, None, kernel)
+    b.set_wind_schedule(sp, dr)
+    b.set_state(init)
+    b.set_key(4, 2, first_stream=0)  # absolute steps 2.. -> entries 2..6 then 6 held
+    b.step(steps)
+    got = b.get_state()
+    for e in range(n):
+        st = init[e]
+        for s in range(steps):
+            row = min(2 + s, S - 1)
+            g = O.grid_terrain(port, "port", t.veg()[e], t.den()[e], t.elevation[e], 30.0, sp[row, e], dr[row, e])
+            st = O.run(port, "port", g, O.DEFAULT_CFG, 4, 2 + s, e, 1, st)
+        assert np.array_equal(got[e], st)
+
+
+def test_wind_schedule_general_form_vs_oracle(port):
+    h, w, steps, S = 12, 10, 12, 4
+    rs = np.random.default_rng(5)
+    L = dict(speed=2 * rs.random((h, w)), dir=6.28 * rs.random((h, w)), veg=rs.random((h, w)) - 0.3,
+             den=rs.random((h, w)) - 0.3, slope8=0.5 * rs.random((h, w, 8)) - 0.25)
+    sp = 3 * rs.random((S, 1, h, w))
+    dr = 6.28 * rs.random((S, 1, h, w))
+    f0 = np.zeros((h, w), np.uint8)
+    f0[6, 5] = 1
+    cfg = [0.3, 0.2, 0.4, 1.0, 1.0, 0.7]
+    b = eb.Batch(1, h, w)
+    b.set_config(cfg)
+    b.set_grid(*L.values())
+    b.set_grid_wind_schedule(sp, dr)
+    b.set_state(f0)
+    b.set_key(21, 0)
+    traj = b.step_record(steps)
+    st = f0
+    for s in range(steps):
+        row = min(s, S - 1)
+        g = O.grid_layers(port, "port", sp[row, 0], dr[row, 0], L["veg"], L["den"], L["slope8"])
+        st = O.run(port, "port", g, cfg, 21, s, 0, 1, st)
+        assert np.array_equal(traj[s, 0], st), s
