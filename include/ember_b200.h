@@ -39,6 +39,7 @@ extern "C" {
 #define EBL_ECUDA -4  /* device / driver failure */
 #define EBL_ESTATE -5 /* call order (e.g. stepping before a grid is set) */
 #define EBL_ENUMERIC -6 /* NumericalError (errors.hpp:14-17) */
+#define EBL_EFILE -7    /* FileError (errors.hpp:9-12), e.g. an unmapped landcover code */
 
 #define EBL_ABI_VERSION 1
 
@@ -76,10 +77,36 @@ int ebl_batch_set_grid(ebl_batch* b, int n_grids, const double* wind_speed,
 /* Static layers, form 2 — terrain (the north-star layout): per-cell uint8 fuel
  * class into a palette of (veg, den) pairs (FuelTable, geodata.hpp:63-86), fp32
  * elevation in metres from which the 8 slopes are derived on the fly exactly as
- * slope_from_dem does (geodata.cpp:209-229) at `cellsize`.  n_grids = 1 or n_envs. */
+ * slope_from_dem does (geodata.cpp:209-229) at `cellsize`.  n_grids = 1 or n_envs.
+ * A NaN elevation is a DEM nodata cell: slope 0 from and toward it (geodata.cpp:214,220). */
 int ebl_batch_set_terrain(ebl_batch* b, int n_grids, const uint8_t* fuel_class,
                           const float* elevation, int n_classes, const double* class_veg,
                           const double* class_den, double cellsize);
+/* fuel_from_landcover / grid_from_rasters (geodata.cpp:324-369) on the device: int32
+ * landcover codes [n_grids][H*W] (model order) are mapped through a FuelTable (codes[k] ->
+ * (veg[k], den[k]); a repeated code keeps its last entry; optional fallback for unknown
+ * codes) into the terrain form's palette.  Landcover nodata (has_nodata && code ==
+ * nodata_code) and DEM nodata (NaN elevation) cells become inert (-1, -1) and the latter get
+ * slope 0.  Errors: EBL_EINVAL for modifiers outside [-1, 1] (FuelTable::set), EBL_EFILE
+ * naming the first unmapped code when there is no fallback (FuelTable::lookup). */
+int ebl_batch_set_landcover(ebl_batch* b, int n_grids, const int32_t* landcover,
+                            const float* elevation, int has_nodata, int32_t nodata_code,
+                            int n_codes, const int32_t* codes, const double* veg,
+                            const double* den, int has_fallback, double fallback_veg,
+                            double fallback_den, double cellsize);
+/* The C1 generator (ebl_synth_terrain below) run on the device straight into the batch:
+ * per-env terrain (n_grids = n_envs, env e on stream env_id0 + e), the WorldCover palette,
+ * per-env wind; bit-identical to ebl_synth_terrain.  n_envs <= 65535. */
+int ebl_batch_synth_terrain(ebl_batch* b, uint64_t seed, uint32_t env_id0, double elev_max,
+                            double wind_max, double cellsize);
+/* ebl_synth_ignitions on the device into the batch state (terrain form; every env zeroed
+ * first).  *placed_total (may be NULL) receives the number of ignitions placed. */
+int ebl_batch_synth_ignitions(ebl_batch* b, uint64_t seed, uint32_t env_id0, int count,
+                              int* placed_total);
+/* Terrain-form layers back to the host: fuel_class / elevation [n_grids][H*W]; either may
+ * be NULL. */
+int ebl_batch_get_terrain(ebl_batch* b, uint8_t* fuel_class, float* elevation);
+
 /* Spatially uniform wind per env (WindField::uniform, grid.cpp:64-66) for the
  * terrain form; n_winds = 1 or n_envs. */
 int ebl_batch_set_wind(ebl_batch* b, int n_winds, const double* speed, const double* direction);

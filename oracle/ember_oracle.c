@@ -89,7 +89,7 @@ ebo_grid* ebo_grid_layers(int h, int w, const double* speed, const double* dir, 
 }
 
 /* slope_from_dem (geodata.cpp:209-229) on model-order fp32 elevation widened
- * exactly to double; no nodata cells. */
+ * exactly to double; a NaN elevation marks a DEM nodata cell. */
 ebo_grid* ebo_grid_terrain(int h, int w, const double* veg, const double* den, const float* elev,
                            double cellsize, double speed, double dir) {
   ebo_grid* g = grid_alloc(h, w);
@@ -105,6 +105,7 @@ ebo_grid* ebo_grid_terrain(int h, int w, const double* veg, const double* den, c
         const int nr = r + kDy[k], nc = c + kDx[k];
         if (nr < 0 || nr >= h || nc < 0 || nc >= w) continue;
         const double dist = cellsize * ((kDx[k] != 0 && kDy[k] != 0) ? SQRT2 : 1.0);
+        if (isnan(elev[i]) || isnan(elev[(size_t)nr * w + nc])) continue; /* nodata: slope 0 (:214,220) */
         g->slope8[i * 8 + k] = atan(((double)elev[(size_t)nr * w + nc] - (double)elev[i]) / dist);
       }
     }

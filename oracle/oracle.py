@@ -93,6 +93,8 @@ _REF_SIG = {
     "ref_rng_below": (_U64, [_U64] * 6),
     "ref_grid_layers": (_P, [_I, _I, _P, _P, _P, _P, _P]),
     "ref_grid_terrain": (_P, [_I, _I, _P, _P, _P, _D, _D, _D]),
+    "ref_grid_from_rasters": (_P, [_I, _I, _P, _P, _I, _P, _P, _P, _I, _D, _D, _D, _D, _D]),
+    "ref_grid_fuel": (_I, [_P, _P, _P]),
     "ref_grid_free": (None, [_P]),
     "ref_grid_slope": (_I, [_P, _P]),
     "ref_tables": (_I, [_P, _P, _P, _P]),
@@ -190,6 +192,29 @@ def grid_terrain(L, kind, veg, den, elev, cellsize, speed, direction) -> Grid:
     g = fn(h, w, ptr(v), ptr(d), ptr(e), float(cellsize), float(speed), float(direction))
     assert g, "oracle rejected the grid"
     return Grid(L, kind, g)
+
+
+def grid_from_rasters(L, elev, landcover, table: dict, fallback=None, cellsize=30.0, speed=0.0,
+                      direction=0.0):
+    """Reference grid_from_rasters (geodata.cpp:351-369) -> (Grid, veg, den), or raises
+    RuntimeError carrying the reference's message (FileError / invalid_argument)."""
+    e = np.ascontiguousarray(elev, dtype=np.float32)
+    lc = np.ascontiguousarray(landcover, dtype=np.float64)
+    h, w = e.shape
+    codes = np.ascontiguousarray(list(table.keys()), dtype=np.int32)
+    veg = np.ascontiguousarray([v for v, _ in table.values()], dtype=np.float64)
+    den = np.ascontiguousarray([d for _, d in table.values()], dtype=np.float64)
+    fb = (0.0, 0.0) if fallback is None else fallback
+    g = L.ref_grid_from_rasters(h, w, ptr(e), ptr(lc), codes.size, ptr(codes), ptr(veg), ptr(den),
+                                int(fallback is not None), float(fb[0]), float(fb[1]), float(cellsize),
+                                float(speed), float(direction))
+    if not g:
+        raise RuntimeError(L.ref_last_error().decode())
+    grid = Grid(L, "ref", g)
+    v = np.empty((h, w))
+    d = np.empty((h, w))
+    L.ref_grid_fuel(g, ptr(v), ptr(d))
+    return grid, v, d
 
 
 def run(L, kind, grid: Grid, cfg, seed, step0, stream, steps, state) -> np.ndarray:

@@ -10,6 +10,7 @@
 // oracle/ember_oracle.c), tests/golden/make_golden.py, and bench.py's
 // `--impl reference` / cpu_baseline leg.
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -62,6 +63,28 @@ R::Grid<double> grid_of(int h, int w, const double* v) {
   for (int i = 0; i < h * w; ++i) g[i] = v[i];
   return g;
 }
+
+// Model-order values -> Raster; NaN cells become NODATA (has_nodata, sentinel, flag), as
+// parse_ascii_grid marks them (geodata.hpp:19-35).
+R::Raster raster_of(int h, int w, const double* v, double cellsize) {
+  R::Grid<double> z(h, w);
+  bool any = false;
+  for (int i = 0; i < h * w; ++i) {
+    z[i] = v[i];
+    any = any || std::isnan(v[i]);
+  }
+  R::Raster r = R::raster_from_model(z, cellsize);
+  if (any) {
+    r.has_nodata = true;
+    for (int mr = 0; mr < h; ++mr)
+      for (int c = 0; c < w; ++c)
+        if (std::isnan(z(mr, c))) {
+          r.values(h - 1 - mr, c) = r.nodata;
+          r.nodata_flag(h - 1 - mr, c) = 1;
+        }
+  }
+  return r;
+}
 }  // namespace
 
 extern "C" {
@@ -103,15 +126,46 @@ void* ref_grid_layers(int h, int w, const double* speed, const double* dir, cons
 void* ref_grid_terrain(int h, int w, const double* veg, const double* den, const float* elev,
                        double cellsize, double speed, double dir) {
   try {
-    R::Grid<double> z(h, w);
+    std::vector<double> z(static_cast<size_t>(h) * w);
     for (int i = 0; i < h * w; ++i) z[i] = static_cast<double>(elev[i]);
-    const R::SlopeField slope = R::slope_from_dem(R::raster_from_model(z, cellsize));
+    const R::SlopeField slope = R::slope_from_dem(raster_of(h, w, z.data(), cellsize));
     return new R::GridState(R::FireLayer(h, w), R::WindField::uniform(h, w, speed, dir),
                             R::FuelField(grid_of(h, w, veg), grid_of(h, w, den)), slope);
   } catch (const std::exception& e) {
     fail(e);
     return nullptr;
   }
+}
+
+// grid_from_rasters (geodata.cpp:351-369): DEM (fp32 widened, NaN = nodata) + landcover codes
+// (NaN = nodata) through a FuelTable {codes -> (veg, den)} with an optional fallback.
+// Returns null with ref_last_error() on FileError / invalid_argument.
+void* ref_grid_from_rasters(int h, int w, const float* elev, const double* landcover, int n_codes,
+                            const int* codes, const double* veg, const double* den, int has_fallback,
+                            double fb_veg, double fb_den, double cellsize, double speed, double dir) {
+  try {
+    std::vector<double> z(static_cast<size_t>(h) * w);
+    for (int i = 0; i < h * w; ++i) z[i] = static_cast<double>(elev[i]);
+    R::FuelTable table;
+    for (int k = 0; k < n_codes; ++k) table.set(codes[k], R::FuelTable::Entry{veg[k], den[k]});
+    if (has_fallback) table.set_fallback(R::FuelTable::Entry{fb_veg, fb_den});
+    return new R::GridState(R::grid_from_rasters(raster_of(h, w, z.data(), cellsize),
+                                                 raster_of(h, w, landcover, cellsize), table, speed, dir));
+  } catch (const std::exception& e) {
+    fail(e);
+    return nullptr;
+  }
+}
+
+// Per-cell FuelField of a GridState (model order).
+int ref_grid_fuel(const void* gp, double* veg, double* den) {
+  const auto& g = *static_cast<const R::GridState*>(gp);
+  const int w = g.width();
+  for (int i = 0; i < g.height() * w; ++i) {
+    veg[i] = g.fuel().veg(i / w, i % w);
+    den[i] = g.fuel().den(i / w, i % w);
+  }
+  return 0;
 }
 
 void ref_grid_free(void* g) { delete static_cast<R::GridState*>(g); }

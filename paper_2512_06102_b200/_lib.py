@@ -12,7 +12,8 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libember_b200.so")
 
-EBL_OK, EBL_EINVAL, EBL_ELOGIC, EBL_ERANGE, EBL_ECUDA, EBL_ESTATE, EBL_ENUMERIC = 0, -1, -2, -3, -4, -5, -6
+EBL_OK, EBL_EINVAL, EBL_ELOGIC, EBL_ERANGE, EBL_ECUDA, EBL_ESTATE, EBL_ENUMERIC, EBL_EFILE = \
+    0, -1, -2, -3, -4, -5, -6, -7
 RL_REFERENCE, RL_TANKER = 0, 1
 
 
@@ -76,8 +77,12 @@ class NumericalError(EmberError, ArithmeticError):  # emberline::NumericalError
     pass
 
 
+class FileError(EmberError):                      # emberline::FileError
+    pass
+
+
 _EXC = {EBL_EINVAL: InvalidArgument, EBL_ELOGIC: LogicError, EBL_ERANGE: OutOfRange,
-        EBL_ENUMERIC: NumericalError}
+        EBL_ENUMERIC: NumericalError, EBL_EFILE: FileError}
 
 _P = C.c_void_p
 _I, _U64, _U32, _D = C.c_int, C.c_uint64, C.c_uint32, C.c_double
@@ -93,6 +98,10 @@ SIGNATURES = {
     "ebl_batch_set_config": (_I, [_P, C.POINTER(SimConfig)]),
     "ebl_batch_set_grid": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "ebl_batch_set_terrain": (_I, [_P, _I, _P, _P, _I, _P, _P, _D]),
+    "ebl_batch_set_landcover": (_I, [_P, _I, _P, _P, _I, C.c_int32, _I, _P, _P, _P, _I, _D, _D, _D]),
+    "ebl_batch_synth_terrain": (_I, [_P, _U64, _U32, _D, _D, _D]),
+    "ebl_batch_synth_ignitions": (_I, [_P, _U64, _U32, _I, C.POINTER(_I)]),
+    "ebl_batch_get_terrain": (_I, [_P, _P, _P]),
     "ebl_batch_set_wind": (_I, [_P, _I, _P, _P]),
     "ebl_batch_set_state": (_I, [_P, _P]),
     "ebl_batch_get_state": (_I, [_P, _P]),

@@ -126,6 +126,7 @@ struct ebl_batch {
   int traj_steps = -1;              // steps recorded by the last ebl_det_forward(record=1)
   std::vector<uint8_t> h_fuel;      // host copies of the terrain (exact host-built tables)
   std::vector<float> h_elev;
+  bool h_terrain_stale = false;     // device terrain newer than h_fuel/h_elev (device-built)
 };
 
 namespace {
@@ -369,7 +370,7 @@ int ebl_batch_set_terrain(ebl_batch* b, int n_grids, const uint8_t* fuel_class, 
   const size_t n = b->ncell * n_grids;
   for (size_t i = 0; i < n; ++i) {
     if (fuel_class[i] >= n_classes) return set_err(EBL_EINVAL, "fuel class outside the palette");
-    if (!std::isfinite(elevation[i])) return set_err(EBL_EINVAL, "elevation must be finite");
+    if (std::isinf(elevation[i])) return set_err(EBL_EINVAL, "elevation must be finite or NaN (nodata)");
   }
   EBL_CUDA(cudaSetDevice(b->device));
   EBL_CUDA(b->fuel.alloc(n));
@@ -380,6 +381,7 @@ int ebl_batch_set_terrain(ebl_batch* b, int n_grids, const uint8_t* fuel_class, 
   b->pal_veg.assign(class_veg, class_veg + n_classes);
   b->h_fuel.assign(fuel_class, fuel_class + n);
   b->h_elev.assign(elevation, elevation + n);
+  b->h_terrain_stale = false;
   b->pal_den.assign(class_den, class_den + n_classes);
   b->cellsize = cellsize;
   b->mode = ebl::kStaticTerrain;
@@ -393,6 +395,208 @@ int ebl_batch_set_terrain(ebl_batch* b, int n_grids, const uint8_t* fuel_class, 
     b->wind_speed.assign(1, 0.0);
     b->wind_dir.assign(1, 0.0);
   }
+  return EBL_OK;
+}
+
+namespace {
+// Terrain-form bookkeeping once fuel/elev hold device-built layers for n_grids grids.
+void adopt_device_terrain(ebl_batch* b, int n_grids, std::vector<double> veg, std::vector<double> den,
+                          double cellsize) {
+  b->pal_veg = std::move(veg);
+  b->pal_den = std::move(den);
+  b->h_fuel.clear();
+  b->h_elev.clear();
+  b->h_terrain_stale = true;
+  b->cellsize = cellsize;
+  b->mode = ebl::kStaticTerrain;
+  b->n_grids = n_grids;
+  b->derived_dirty = true;
+  b->det_tables_valid = false;
+  b->pot.reset();
+  b->gamma.reset();
+  if (b->n_winds == 0) {
+    b->n_winds = 1;
+    b->wind_speed.assign(1, 0.0);
+    b->wind_dir.assign(1, 0.0);
+  }
+}
+}  // namespace
+
+int ebl_batch_synth_terrain(ebl_batch* b, uint64_t seed, uint32_t env_id0, double elev_max,
+                            double wind_max, double cellsize) {
+  if (int e = check_batch(b)) return e;
+  if (!(cellsize > 0.0) || !std::isfinite(cellsize))
+    return set_err(EBL_EINVAL, "raster_from_model: cellsize must be positive");
+  if (!std::isfinite(elev_max)) return set_err(EBL_EINVAL, "elev_max must be finite");
+  if (!std::isfinite(wind_max)) return set_err(EBL_EINVAL, "WindField: non-finite speed");
+  if (wind_max < 0.0) return set_err(EBL_EINVAL, "WindField: negative speed");
+  if (b->h < 2 || b->w < 2) return set_err(EBL_EINVAL, "synth_terrain: need n_envs >= 1, dims >= 2");
+  if (b->n_envs > 65535) return set_err(EBL_EINVAL, "device terrain synthesis supports at most 65535 envs per batch");
+  EBL_CUDA(cudaSetDevice(b->device));
+  const size_t n = b->ncell * b->n_envs;
+  EBL_CUDA(b->fuel.alloc(n));
+  EBL_CUDA(b->elev.alloc(n));
+  DevBuf<double> scratch;
+  DevBuf<unsigned long long> mm;
+  DevBuf<unsigned int> hist;
+  DevBuf<int> thr;
+  EBL_CUDA(scratch.alloc(n));
+  EBL_CUDA(mm.alloc(static_cast<size_t>(b->n_envs) * 4));
+  EBL_CUDA(hist.alloc(static_cast<size_t>(b->n_envs) * 4096));
+  EBL_CUDA(thr.alloc(static_cast<size_t>(b->n_envs) * 10));
+  ebl::SynthArgs a{};
+  a.seed = seed;
+  a.env_id0 = env_id0;
+  a.n_envs = b->n_envs;
+  a.h = b->h;
+  a.w = b->w;
+  a.lc_base = std::min(64, std::max(4, std::min(b->h, b->w) / 4));   // ember_host.cpp synth_one
+  a.el_base = std::min(128, std::max(8, std::min(b->h, b->w) / 2));
+  a.elev_max = elev_max;
+  a.fuel = b->fuel.p;
+  a.elev = b->elev.p;
+  a.scratch = scratch.p;
+  a.mm = mm.p;
+  a.hist = hist.p;
+  a.thr = thr.p;
+  EBL_CUDA(ebl::launch_synth_terrain(a, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  std::vector<double> veg(11), den(11);
+  ebl::worldcover_palette(nullptr, veg.data(), den.data());
+  adopt_device_terrain(b, b->n_envs, std::move(veg), std::move(den), cellsize);
+  // per-env wind exactly as the host generator draws it
+  std::vector<double> speed(b->n_envs), dir(b->n_envs);
+  for (int e = 0; e < b->n_envs; ++e) {
+    const uint64_t stream = env_id0 + static_cast<uint64_t>(e);
+    speed[e] = wind_max * ebl::rng_uniform(seed, 3000, stream, 0, 3);
+    dir[e] = 2.0 * 3.14159265358979323846 * ebl::rng_uniform(seed, 3000, stream, 1, 3);
+  }
+  b->n_winds = b->n_envs;
+  b->sched_len = 0;
+  b->wind_speed = std::move(speed);
+  b->wind_dir = std::move(dir);
+  return EBL_OK;
+}
+
+int ebl_batch_synth_ignitions(ebl_batch* b, uint64_t seed, uint32_t env_id0, int count, int* placed_total) {
+  if (int e = check_batch(b)) return e;
+  if (b->mode != ebl::kStaticTerrain) return set_err(EBL_ESTATE, "ignitions need terrain-form static layers");
+  if (count < 0) return set_err(EBL_EINVAL, "EnvConfig: ignition_count must be >= 0");
+  if (int e = prepare(b)) return e;  // burnable flags live in pal64[512..767]
+  DevBuf<int> placed;
+  EBL_CUDA(placed.alloc(b->n_envs));
+  ebl::IgniteArgs a{};
+  a.seed = seed;
+  a.env_id0 = env_id0;
+  a.n_envs = b->n_envs;
+  a.h = b->h;
+  a.w = b->w;
+  a.count = count;
+  a.fuel = b->fuel.p;
+  a.fuel_stride = b->n_grids > 1 ? b->ncell : 0;
+  a.burnable = b->pal64.p + 512;
+  a.states = b->state[b->cur].p;
+  a.placed = placed.p;
+  EBL_CUDA(ebl::launch_synth_ignitions(a, b->stream));
+  std::vector<int> h(b->n_envs);
+  EBL_CUDA(cudaMemcpyAsync(h.data(), placed.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  b->counts_valid = false;
+  if (placed_total) {
+    long long t = 0;
+    for (int v : h) t += v;
+    *placed_total = static_cast<int>(t);
+  }
+  return EBL_OK;
+}
+
+int ebl_batch_get_terrain(ebl_batch* b, uint8_t* fuel_class, float* elevation) {
+  if (int e = check_batch(b)) return e;
+  if (b->mode != ebl::kStaticTerrain) return set_err(EBL_ESTATE, "no terrain-form static layers on the batch");
+  EBL_CUDA(cudaSetDevice(b->device));
+  const size_t n = b->ncell * b->n_grids;
+  if (fuel_class) EBL_CUDA(cudaMemcpyAsync(fuel_class, b->fuel.p, n, cudaMemcpyDeviceToHost, b->stream));
+  if (elevation) EBL_CUDA(cudaMemcpyAsync(elevation, b->elev.p, n * sizeof(float), cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_batch_set_landcover(ebl_batch* b, int n_grids, const int32_t* landcover, const float* elevation,
+                            int has_nodata, int32_t nodata_code, int n_codes, const int32_t* codes,
+                            const double* veg, const double* den, int has_fallback, double fallback_veg,
+                            double fallback_den, double cellsize) {
+  if (int e = check_batch(b)) return e;
+  if (n_grids != 1 && n_grids != b->n_envs) return set_err(EBL_EINVAL, "n_grids must be 1 or n_envs");
+  if (!landcover || !elevation) return set_err(EBL_EINVAL, "null layer");
+  if (n_codes < 0 || n_codes > 254) return set_err(EBL_EINVAL, "a fuel table holds at most 254 codes");
+  if (n_codes > 0 && (!codes || !veg || !den)) return set_err(EBL_EINVAL, "null fuel table");
+  if (!(cellsize > 0.0) || !std::isfinite(cellsize))
+    return set_err(EBL_EINVAL, "raster_from_model: cellsize must be positive");
+  auto in_range = [](double v) { return std::isfinite(v) && v >= -1.0 && v <= 1.0; };
+  // FuelTable::set / set_fallback (geodata.cpp:231-247); a repeated code keeps the last entry
+  std::vector<std::pair<int32_t, int>> order;
+  for (int k = 0; k < n_codes; ++k) {
+    if (!in_range(veg[k]) || !in_range(den[k]))
+      return set_err(EBL_EINVAL, "FuelTable: modifiers for code " + std::to_string(codes[k]) +
+                                     " must lie in [-1, 1]");
+    order.emplace_back(codes[k], k);
+  }
+  if (has_fallback && (!in_range(fallback_veg) || !in_range(fallback_den)))
+    return set_err(EBL_EINVAL, "FuelTable: fallback modifiers must lie in [-1, 1]");
+  std::stable_sort(order.begin(), order.end(), [](auto& x, auto& y) { return x.first < y.first; });
+  std::vector<int32_t> sorted;
+  std::vector<double> pv, pd;
+  for (size_t i = 0; i < order.size(); ++i) {
+    if (i + 1 < order.size() && order[i + 1].first == order[i].first) continue;  // last set wins
+    sorted.push_back(order[i].first);
+    pv.push_back(veg[order[i].second]);
+    pd.push_back(den[order[i].second]);
+  }
+  const int nc = static_cast<int>(sorted.size());
+  const int fallback_index = has_fallback ? nc : -1;
+  if (has_fallback) {
+    pv.push_back(fallback_veg);
+    pd.push_back(fallback_den);
+  }
+  const int nodata_index = static_cast<int>(pv.size());
+  pv.push_back(-1.0);  // nodata cells are inert (geodata.cpp:330-334)
+  pd.push_back(-1.0);
+  const size_t n = b->ncell * n_grids;
+  for (size_t i = 0; i < n; ++i)
+    if (std::isinf(elevation[i])) return set_err(EBL_EINVAL, "elevation must be finite or NaN (nodata)");
+  EBL_CUDA(cudaSetDevice(b->device));
+  DevBuf<int32_t> lc, dcodes;
+  DevBuf<unsigned long long> missing;
+  EBL_CUDA(lc.alloc(n));
+  EBL_CUDA(dcodes.alloc(std::max(1, nc)));
+  EBL_CUDA(missing.alloc(1));
+  EBL_CUDA(b->fuel.alloc(n));
+  EBL_CUDA(b->elev.alloc(n));
+  EBL_CUDA(cudaMemcpyAsync(lc.p, landcover, n * sizeof(int32_t), cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(b->elev.p, elevation, n * sizeof(float), cudaMemcpyHostToDevice, b->stream));
+  if (nc) EBL_CUDA(cudaMemcpyAsync(dcodes.p, sorted.data(), nc * sizeof(int32_t), cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaMemsetAsync(missing.p, 0xff, sizeof(unsigned long long), b->stream));
+  ebl::LandcoverArgs a{};
+  a.n = n;
+  a.landcover = lc.p;
+  a.elev = b->elev.p;
+  a.codes = dcodes.p;
+  a.n_codes = nc;
+  a.fallback_index = fallback_index;
+  a.nodata_index = nodata_index;
+  a.has_nodata = has_nodata;
+  a.nodata_code = nodata_code;
+  a.fuel = b->fuel.p;
+  a.missing = missing.p;
+  EBL_CUDA(ebl::launch_landcover_map(a, b->stream));
+  unsigned long long miss = 0;
+  EBL_CUDA(cudaMemcpyAsync(&miss, missing.p, sizeof(miss), cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  if (miss != ~0ull) {
+    b->mode = ebl::kStaticNone;  // layers half-built: the batch has no usable statics
+    return set_err(EBL_EFILE, "fuel table has no entry for landcover code " + std::to_string(landcover[miss]));
+  }
+  adopt_device_terrain(b, n_grids, std::move(pv), std::move(pd), cellsize);
   return EBL_OK;
 }
 
@@ -1093,6 +1297,15 @@ int det_tables(ebl_batch* b) {
     EBL_CUDA(b->det_fac.alloc(fac.size()));
     EBL_CUDA(cudaMemcpyAsync(b->det_fac.p, fac.data(), fac.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
   } else {
+    if (b->h_terrain_stale) {  // terrain built on the device: fetch the host copy once
+      const size_t m = n * b->n_grids;
+      b->h_fuel.resize(m);
+      b->h_elev.resize(m);
+      EBL_CUDA(cudaMemcpyAsync(b->h_fuel.data(), b->fuel.p, m, cudaMemcpyDeviceToHost, b->stream));
+      EBL_CUDA(cudaMemcpyAsync(b->h_elev.data(), b->elev.p, m * sizeof(float), cudaMemcpyDeviceToHost, b->stream));
+      EBL_CUDA(cudaStreamSynchronize(b->stream));
+      b->h_terrain_stale = false;
+    }
     ebl::build_terrain_tables(T, b->h, b->w, b->h_fuel.data(), b->h_elev.data(), b->n_grids > 1 ? n : 0,
                               b->pal_veg.data(), b->pal_den.data(), b->cellsize, b->wind_speed.data(),
                               b->wind_dir.data(), b->n_winds > 1 ? 1 : 0, c, pot.data(), gam.data());

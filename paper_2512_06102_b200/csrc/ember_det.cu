@@ -230,7 +230,8 @@ __global__ void k_det_back2(DetArgs d, int t) {
         acc_burn += al * pot;
         // pot = p_base F kw ks (kernel.hpp:21-45): dpot/dp_base = F kw ks, dpot/dalpha_w1 = pot V,
         // dpot/dalpha_w2 = pot V (cos - 1), dpot/dalpha_s = pot S
-        const double S = atan((static_cast<double>(tv.elev[vr * a.w + vc]) - zu) / tv.dist64[k & 1]);
+        const double dz = static_cast<double>(tv.elev[vr * a.w + vc]) - zu;
+        const double S = dz == dz ? atan(dz / tv.dist64[k & 1]) : 0.0;  // DEM nodata: slope 0
         const double ab = al * bu;
         gp += ab * (Fu * tv.kw64[k] * exp(tv.alpha_s * S));
         gw1 += ab * pot * V;

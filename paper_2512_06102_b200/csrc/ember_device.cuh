@@ -109,8 +109,9 @@ static __device__ __noinline__ double terrain_p64(const TerrainView& t, int w, i
   for (int k = 0; k < 8; ++k) {
     if (nb & (1u << k)) {
       const int u = (r - kDy[k]) * w + (c - kDx[k]);
-      const double s = atan(__ddiv_rn(__dsub_rn(zv, static_cast<double>(t.elev[u])),
-                                      t.dist64[k & 1]));
+      const double dz = __dsub_rn(zv, static_cast<double>(t.elev[u]));
+      // DEM nodata (NaN) on either end: slope 0 (geodata.cpp:214,220)
+      const double s = dz == dz ? atan(__ddiv_rn(dz, t.dist64[k & 1])) : 0.0;
       const double ks = exp(__dmul_rn(t.alpha_s, s));
       const double pot = __dmul_rn(__dmul_rn(t.pal_src64[t.fuel[u]], t.kw64[k]), ks);
       lam = __dadd_rn(lam, pot);
@@ -128,7 +129,8 @@ __device__ __forceinline__ float terrain_lambda32(const TerrainView& t, int w, i
   for (int k = 0; k < 8; ++k) {
     if (nb & (1u << k)) {
       const int u = (r - kDy[k]) * w + (c - kDx[k]);
-      const float s = atanf((zv - t.elev[u]) * t.inv_dist32[k & 1]);
+      const float dz = zv - t.elev[u];
+      const float s = dz == dz ? atanf(dz * t.inv_dist32[k & 1]) : 0.f;  // nodata: slope 0
       lam += t.pal_src32[t.fuel[u]] * t.kw32[k] * expf(t.alpha_s32 * s);
     }
   }

@@ -122,9 +122,10 @@ void build_terrain_tables(int n_tables, int h, int w, const uint8_t* fuel, const
         for (int k = 0; k < 8; ++k) {
           const int nr = r + kDy[k], nc = col + kDx[k];
           double s = 0.0;  // slope_from_dem: 0 toward out-of-bounds neighbours
-          if (nr >= 0 && nr < h && nc >= 0 && nc < w)
-            s = std::atan((static_cast<double>(z[static_cast<size_t>(nr) * w + nc]) - static_cast<double>(z[i])) /
-                          dist[k & 1]);
+          if (nr >= 0 && nr < h && nc >= 0 && nc < w) {
+            const double dz = static_cast<double>(z[static_cast<size_t>(nr) * w + nc]) - static_cast<double>(z[i]);
+            if (dz == dz) s = std::atan(dz / dist[k & 1]);  // NaN = DEM nodata: slope 0 (geodata.cpp:214,220)
+          }
           P[i * 8 + k] = (source * kw[k]) * std::exp(c.alpha_s * s);  // engine.hpp:91,106-107
         }
       }

@@ -40,4 +40,44 @@ bool rl_bits_fits(int h, int w);
 cudaError_t launch_rl_tanker_bits(const RlArgs& g, int mode, cudaStream_t s);
 cudaError_t launch_rl_tanker_reset(const RlArgs& g, int mode, const uint8_t* mask, cudaStream_t s);
 
+// ---- environment construction (ember_synth.cu) ----
+struct SynthArgs {
+  uint64_t seed;
+  uint32_t env_id0;
+  int n_envs, h, w;       // n_envs <= 65535 (grid.y)
+  int lc_base, el_base;   // lattice periods (ember_host.cpp synth_one)
+  double elev_max;
+  uint8_t* fuel;          // [n_envs][h*w] palette index 0..10
+  float* elev;            // [n_envs][h*w]
+  double* scratch;        // [n_envs][h*w]
+  unsigned long long* mm; // [n_envs][4] landcover lo, hi, elevation lo, hi (IEEE bits)
+  unsigned int* hist;     // [n_envs][4096]
+  int* thr;               // [n_envs][10]
+};
+cudaError_t launch_synth_terrain(const SynthArgs& a, cudaStream_t s);
+
+struct IgniteArgs {
+  uint64_t seed;
+  uint32_t env_id0;
+  int n_envs, h, w, count;
+  const uint8_t* fuel;
+  size_t fuel_stride;      // 0 (shared terrain) or h*w
+  const double* burnable;  // [256] 1.0 / 0.0 per palette entry
+  uint8_t* states;         // [n_envs][h*w], zeroed by the launcher
+  int* placed;             // [n_envs]
+};
+cudaError_t launch_synth_ignitions(const IgniteArgs& a, cudaStream_t s);
+
+struct LandcoverArgs {
+  size_t n;
+  const int32_t* landcover;  // [n] codes
+  const float* elev;         // [n] or null; NaN = DEM nodata
+  const int32_t* codes;      // sorted FuelTable codes, n_codes <= 254
+  int n_codes, fallback_index, nodata_index, has_nodata;
+  int32_t nodata_code;
+  uint8_t* fuel;             // [n] palette index
+  unsigned long long* missing;  // first cell with an unmapped code (init ~0)
+};
+cudaError_t launch_landcover_map(const LandcoverArgs& a, cudaStream_t s);
+
 }  // namespace ebl

@@ -105,6 +105,44 @@ class Batch:
         check(lib().ebl_batch_set_terrain(self._h, n_grids, _ptr(fc), _ptr(el), cv.size, _ptr(cv),
                                           _ptr(cd), float(cellsize)))
 
+    def set_landcover(self, landcover, elevation, table, fallback=None, nodata_code=None,
+                      cellsize=30.0) -> None:
+        """grid_from_rasters / fuel_from_landcover (geodata.cpp:324-369) on the device.
+
+        landcover: int codes [G,H,W]; elevation: fp32 [G,H,W] (NaN = DEM nodata);
+        table: {code: (veg, den)}; fallback: (veg, den) for unknown codes or None."""
+        lc = np.ascontiguousarray(landcover, dtype=np.int32)
+        el = np.ascontiguousarray(elevation, dtype=np.float32)
+        codes = np.ascontiguousarray(list(table.keys()), dtype=np.int32)
+        veg = np.ascontiguousarray([v for v, _ in table.values()], dtype=np.float64)
+        den = np.ascontiguousarray([d for _, d in table.values()], dtype=np.float64)
+        n_grids = lc.size // (self.height * self.width)
+        fb = (0.0, 0.0) if fallback is None else fallback
+        check(lib().ebl_batch_set_landcover(
+            self._h, n_grids, _ptr(lc), _ptr(el), int(nodata_code is not None),
+            0 if nodata_code is None else int(nodata_code), codes.size, _ptr(codes), _ptr(veg),
+            _ptr(den), int(fallback is not None), float(fb[0]), float(fb[1]), float(cellsize)))
+
+    def synth_terrain(self, seed: int, env_id0: int = 0, elev_max: float = 500.0,
+                      wind_max: float = 10.0, cellsize: float = 30.0) -> None:
+        """The C1 generator run on the device (bit-identical to synth_terrain below)."""
+        check(lib().ebl_batch_synth_terrain(self._h, seed, env_id0, float(elev_max), float(wind_max),
+                                            float(cellsize)))
+
+    def synth_ignitions(self, seed: int, count: int, env_id0: int = 0) -> int:
+        """Seeded ignitions on the device into the state (bit-identical to synth_ignitions)."""
+        placed = C.c_int()
+        check(lib().ebl_batch_synth_ignitions(self._h, seed, env_id0, count, C.byref(placed)))
+        return placed.value
+
+    def get_terrain(self):
+        """(fuel_class uint8 [G,H,W], elevation fp32 [G,H,W]) of the terrain form."""
+        n = self.n_envs  # G = n_envs or 1; the C-ABI copies n_grids grids
+        fc = np.zeros((n, self.height, self.width), np.uint8)
+        el = np.zeros((n, self.height, self.width), np.float32)
+        check(lib().ebl_batch_get_terrain(self._h, _ptr(fc), _ptr(el)))
+        return fc, el
+
     def set_wind(self, speed, direction) -> None:
         sp = np.ascontiguousarray(np.atleast_1d(speed), dtype=np.float64)
         dr = np.ascontiguousarray(np.atleast_1d(direction), dtype=np.float64)

@@ -219,3 +219,57 @@ def test_port_vs_ref_calibrate(port, ref):
     # invalid init (p_continue outside (0,1)) is rejected by both
     assert O.calibrate(port, "port", gp, planes, mask, 12, 2, [0.1, 0, 0, 0, 1, 1.5])[0] == -2
     assert O.calibrate(ref, "ref", gr, planes, mask, 12, 2, [0.1, 0, 0, 0, 1, 1.5])[0] == -1
+
+
+def test_port_vs_ref_dem_nodata(port, ref):
+    # slope_from_dem (geodata.cpp:209-229): NaN elevation = nodata, slope 0 from and toward it
+    rs = np.random.default_rng(71)
+    h, w = 13, 9
+    el = (300 * rs.random((h, w))).astype(np.float32)
+    el[0, 0] = el[6, 4] = el[12, 8] = el[3, 8] = np.nan
+    veg, den = rs.random((h, w)) - 0.3, rs.random((h, w)) - 0.3
+    gp = O.grid_terrain(port, "port", veg, den, el, 25.0, 3.0, 2.0)
+    gr = O.grid_terrain(ref, "ref", veg, den, el, 25.0, 3.0, 2.0)
+    cfg = np.array([0.3, 0.2, 0.4, 1.5, 1.0, 0.6])
+    pp, gmp = O.tables(port, "port", gp, cfg, h * w)
+    pr, gmr = O.tables(ref, "ref", gr, cfg, h * w)
+    assert np.array_equal(pp, pr) and np.array_equal(gmp, gmr)
+    s = np.empty(h * w * 8)
+    ref.ref_grid_slope(gr.h, O.ptr(s))
+    s = s.reshape(h, w, 8)
+    assert (s[6, 4] == 0).all() and s[5, 4, 2] == 0.0 and s[7, 4, 6] == 0.0  # N of / S of nodata
+    f0 = np.zeros((h, w), np.uint8)
+    f0[6, 3] = f0[1, 1] = 1
+    assert np.array_equal(O.run(port, "port", gp, cfg, 9, 0, 2, 40, f0),
+                          O.run(ref, "ref", gr, cfg, 9, 0, 2, 40, f0))
+
+
+def landcover_restated(lc, elev, table, fallback):
+    """fuel_layers (geodata.cpp:324-345) in numpy: nodata (NaN landcover or DEM) -> (-1, -1)."""
+    veg = np.full(lc.shape, -1.0)
+    den = np.full(lc.shape, -1.0)
+    for idx in np.ndindex(lc.shape):
+        if np.isnan(lc[idx]) or np.isnan(elev[idx]):
+            continue
+        v, d = table.get(int(lc[idx]), fallback)
+        veg[idx], den[idx] = v, d
+    return veg, den
+
+
+def test_ref_landcover_mapping(ref):
+    rs = np.random.default_rng(72)
+    h, w = 12, 10
+    el = (100 * rs.random((h, w))).astype(np.float32)
+    el[2, 2] = np.nan
+    lc = rs.choice([10, 20, 30, 40, 50, 60, 70, 80, 90, 95, 100, 7], (h, w)).astype(np.float64)
+    lc[5, 5] = np.nan
+    tab = {10: (0.4, 0.3), 20: (0.25, 0.1), 30: (0.15, -0.1), 40: (0.0, -0.2), 50: (-0.8, -0.8),
+           60: (-0.7, -0.6), 70: (-1.0, -1.0), 80: (-1.0, -1.0), 90: (-0.4, -0.3), 95: (-0.2, -0.1),
+           100: (-0.3, -0.4)}
+    with pytest.raises(RuntimeError, match="no entry for landcover code 7"):
+        O.grid_from_rasters(ref, el, lc, tab)
+    _, v, d = O.grid_from_rasters(ref, el, lc, tab, fallback=(0.05, -0.05))
+    rv, rd = landcover_restated(lc, el, tab, (0.05, -0.05))
+    assert np.array_equal(v, rv) and np.array_equal(d, rd)
+    with pytest.raises(RuntimeError, match="must lie in"):
+        O.grid_from_rasters(ref, el, lc, {10: (1.5, 0.0)}, fallback=(0, 0))
