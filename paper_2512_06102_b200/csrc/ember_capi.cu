@@ -1351,16 +1351,14 @@ int ebl_det_set_state(ebl_batch* b, const double* un, const double* burn, const 
 
 int ebl_det_set_state_from_fire(ebl_batch* b) {  // state_from_fire (engine.cpp:42-52)
   if (int e = check_batch(b)) return e;
-  const size_t n = b->ncell * b->n_envs;
-  std::vector<uint8_t> st(n);
-  if (int e = ebl_batch_get_state(b, st.data())) return e;
-  std::vector<double> un(n), bu(n), bd(n);
-  for (size_t i = 0; i < n; ++i) {
-    un[i] = st[i] == 0 ? 1.0 : 0.0;
-    bu[i] = st[i] == 1 ? 1.0 : 0.0;
-    bd[i] = st[i] == 2 ? 1.0 : 0.0;
-  }
-  return ebl_det_set_state(b, un.data(), bu.data(), bd.data());
+  EBL_CUDA(cudaSetDevice(b->device));
+  if (int e = det_alloc(b)) return e;
+  const int c = b->det_cur * 3;
+  EBL_CUDA(ebl::launch_det_from_fire(b->state[b->cur].p, b->det[c].p, b->det[c + 1].p, b->det[c + 2].p,
+                                     b->ncell * b->n_envs, b->stream));
+  b->det_ready = true;
+  b->traj_steps = -1;
+  return EBL_OK;
 }
 
 int ebl_det_get_state(ebl_batch* b, double* un, double* burn, double* bd) {
@@ -1384,12 +1382,13 @@ int ebl_det_forward(ebl_batch* b, int n_steps, int record) {
   if (!b->det_tables_valid || std::memcmp(&b->det_cfg, &b->cfg, sizeof b->cfg) != 0)
     if (int e = det_tables(b)) return e;
   const size_t n = b->ncell * b->n_envs;
-  if (record) EBL_CUDA(b->traj.alloc(2 * n * std::max(1, n_steps)));
+  if (record) EBL_CUDA(b->traj.alloc(3 * n * std::max(1, n_steps)));
   for (int t = 0; t < n_steps; ++t) {
     ebl::DetArgs d = det_args(b);
     if (record) {
       d.traj_un = b->traj.p;
       d.traj_burn = b->traj.p + n * n_steps;
+      d.traj_lam = b->traj.p + 2 * n * n_steps;
     }
     EBL_CUDA(ebl::launch_det_forward(d, t, b->stream));
     b->det_cur ^= 1;
@@ -1430,6 +1429,8 @@ int ebl_det_loss_grad(ebl_batch* b, const double* mask, double bce_w, double mse
   d.grad = b->det_grad.p;
   d.traj_un = b->traj.p;
   d.traj_burn = b->traj.p + n * std::max(1, b->traj_steps);
+  d.traj_lam = b->traj.p + 2 * n * std::max(1, b->traj_steps);
+  d.inv_p_base = 1.0 / b->cfg.p_base;
   EBL_CUDA(ebl::launch_det_loss(d, b->stream));
   for (int t = b->traj_steps - 1; t >= 0; --t) EBL_CUDA(ebl::launch_det_backward(d, t, b->stream));
   EBL_CUDA(ebl::launch_det_reduce(d, b->stream));

@@ -95,7 +95,18 @@ __global__ void k_det_forward(DetArgs d, int t) {
     const size_t tr = static_cast<size_t>(t) * a.n_envs * ncell + base + i;
     d.traj_un[tr] = un;
     d.traj_burn[tr] = bu;
+    d.traj_lam[tr] = lam;
   }
+}
+
+// state_from_fire (engine.cpp:42-52): one-hot planes from the member layers, on the device.
+__global__ void k_det_from_fire(const uint8_t* __restrict__ st, double* un, double* bu, double* bd, size_t n) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint8_t s = st[i];
+  un[i] = s == 0 ? 1.0 : 0.0;
+  bu[i] = s == 1 ? 1.0 : 0.0;
+  bd[i] = s == 2 ? 1.0 : 0.0;
 }
 
 // Loss (calibrate.hpp:120-146) per env and dL/dpred -> the adjoints of the final state.
@@ -160,7 +171,7 @@ __global__ void k_det_back1(DetArgs d, int t) {
   const size_t tr = static_cast<size_t>(t) * a.n_envs * ncell + base;
   double g_gamma = 0.0, g_pc = 0.0;
   if (i < ncell) {
-    const double lam = lambda_at(d.traj_burn + tr, d.pot + tb * 8, a.h, a.w, i / a.w, i % a.w);
+    const double lam = d.traj_lam[tr + i];  // bit-identical to re-folding traj_burn * pot
     const double gam = d.gam[tb + i];
     const double x = __dmul_rn(gam, lam);
     const double e = exp_neg(x);
@@ -218,8 +229,7 @@ __global__ void k_det_back2(DetArgs d, int t) {
     } else if (bu != 0.0) {
       const TerrainView tv = terrain_view(a, env);
       const double V = d.V[env * d.wind_stride];
-      const double Fu = a.pal64[768 + tv.fuel[i]];
-      const double zu = static_cast<double>(tv.elev[i]);
+      const float zu = tv.elev[i];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int vr = r + kDy[k], vc = c + kDx[k];
@@ -230,10 +240,12 @@ __global__ void k_det_back2(DetArgs d, int t) {
         acc_burn += al * pot;
         // pot = p_base F kw ks (kernel.hpp:21-45): dpot/dp_base = F kw ks, dpot/dalpha_w1 = pot V,
         // dpot/dalpha_w2 = pot V (cos - 1), dpot/dalpha_s = pot S
-        const double dz = static_cast<double>(tv.elev[vr * a.w + vc]) - zu;
-        const double S = dz == dz ? atan(dz / tv.dist64[k & 1]) : 0.0;  // DEM nodata: slope 0
+        // S in fp32 (relative error ~1e-7, far inside the 1e-4 gradient bar); fp32 elevations
+        // differ exactly in fp32 unless they are ~2^24 apart in magnitude
+        const float dz = tv.elev[vr * a.w + vc] - zu;
+        const double S = dz == dz ? static_cast<double>(atanf(dz * tv.inv_dist32[k & 1])) : 0.0;  // nodata: 0
         const double ab = al * bu;
-        gp += ab * (Fu * tv.kw64[k] * exp(tv.alpha_s * S));
+        gp += ab * (pot * d.inv_p_base);
         gw1 += ab * pot * V;
         gw2 += ab * pot * V * d.align[env * d.wind_stride * 8 + k];
         gs += ab * pot * S;
@@ -266,6 +278,12 @@ __global__ void k_det_reduce(DetArgs d, int blocks_per_env) {
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s) {
   const int ncell = d.s.h * d.s.w;
   k_det_forward<<<dim3((ncell + 255) / 256, d.s.n_envs), 256, 0, s>>>(d, t);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_det_from_fire(const uint8_t* st, double* un, double* bu, double* bd, size_t n,
+                                 cudaStream_t s) {
+  k_det_from_fire<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(st, un, bu, bd, n);
   return cudaGetLastError();
 }
 

@@ -24,6 +24,8 @@ cudaError_t launch_step_blocked(const StepArgs& a, int mode, const BlockGeom& g,
 
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s);
 cudaError_t launch_det_loss(const DetArgs& d, cudaStream_t s);
+cudaError_t launch_det_from_fire(const uint8_t* st, double* un, double* bu, double* bd, size_t n,
+                                 cudaStream_t s);
 cudaError_t launch_det_backward(const DetArgs& d, int t, cudaStream_t s);
 cudaError_t launch_det_reduce(const DetArgs& d, cudaStream_t s);
 cudaError_t launch_rng_probe(int n, const uint64_t* keys5, uint64_t* out, cudaStream_t s);

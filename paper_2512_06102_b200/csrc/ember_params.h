@@ -73,6 +73,8 @@ struct DetArgs {
   double pc;
   double* traj_un;                // [T][env][cell] state before step t (record mode)
   double* traj_burn;
+  double* traj_lam;               // [T][env][cell] lambda of step t (saves back1 the pot gather)
+  double inv_p_base;              // 1 / p_base: dpot/dp_base = pot / p_base (terrain form)
   const double* mask;             // [env][cell] target burn mask
   double bce_w, mse_w;
   int pool;
