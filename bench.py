@@ -172,7 +172,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "tiled", "resident"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "tiled", "resident", "paired"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -202,7 +202,7 @@ def main():
     b.set_terrain(terrain.fuel_class, terrain.elevation, terrain.class_veg, terrain.class_den, 30.0)
     b.set_wind(terrain.wind_speed, terrain.wind_direction)
     b.set_config(None)
-    b.set_kernel({"auto": 0, "tiled": 1, "resident": 2}[args.kernel])
+    b.set_kernel({"auto": 0, "tiled": 1, "resident": 2, "paired": 4}[args.kernel])
     b.set_key(SEED, 0, first_stream=env0)
 
     init_dev = torch.from_numpy(init).to(f"cuda:{local}")

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libember_b200.so")
+# EBL_LIB overrides the library path (A/B timing of two builds of the same ABI)
+LIB_PATH = os.environ.get("EBL_LIB") or os.path.join(_HERE, "libember_b200.so")
 
 EBL_OK, EBL_EINVAL, EBL_ELOGIC, EBL_ERANGE, EBL_ECUDA, EBL_ESTATE, EBL_ENUMERIC, EBL_EFILE = \
     0, -1, -2, -3, -4, -5, -6, -7

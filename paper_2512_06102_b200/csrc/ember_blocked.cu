@@ -35,14 +35,18 @@
 namespace ebl {
 
 
-template <int MODE>
-__global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, BlockGeom g) {
+// E envs per CTA (E = 1, or 2 for whole-env residency of envs <= 32768 cells): 128 threads per
+// env in P1, one pooled active list in P2, so a heavy env shares its CTA's 128*E threads with a
+// lighter one (the batch's kernel time is set by its slowest CTA: measured, scripts/imbalance.py).
+template <int MODE, int E>
+__global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArgs a, BlockGeom g) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_total[2];
-  __shared__ int32_t s_newly[2];
-  __shared__ int32_t s_cnt[4];
+  __shared__ int32_t s_newly[2][E];
+  __shared__ int32_t s_cnt[E][4];
+  __shared__ uint64_t s_prefix[2][E];  // rng key prefix of step t in slot t & 1 (one thread computes it)
 
-  const int env = blockIdx.z;
+  const int env0 = blockIdx.z * E;
   const int W = a.w, BH = a.h;
   const int r0 = blockIdx.y * g.tile_h, c0 = blockIdx.x * g.tile_w;  // c0 % 32 == 0
   const int R0 = max(0, r0 - g.halo_rows), R1 = min(BH, r0 + g.tile_h + g.halo_rows);
@@ -50,51 +54,61 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
   const int RH = R1 - R0, RW = C1 - C0;
   const int wpr = (RW + 31) >> 5;
   const int S = plane_stride(wpr);  // odd row stride: a warp's 32 rows hit 32 distinct banks
-  uint32_t* Bp[2];
-  Bp[0] = reinterpret_cast<uint32_t*>(smem);
-  Bp[1] = Bp[0] + (RH + 2) * S;
-  uint32_t* X = Bp[1] + (RH + 2) * S;
-  uint32_t* ACT = X + RH * S;
-  uint16_t* list = reinterpret_cast<uint16_t*>(ACT + RH * S);
+  const int PB = (2 * (RH + 2) + 2 * RH) * S;  // words of one env's planes: B[2], X, ACT
+  uint32_t* const planes = reinterpret_cast<uint32_t*>(smem);
+  // env s's planes: B[c] = planes + s*PB + c*(RH+2)*S, X = + 2*(RH+2)*S, ACT = X + RH*S
+  auto Bplane = [&](int sub, int c) { return planes + sub * PB + c * (RH + 2) * S; };
+  auto Xplane = [&](int sub) { return planes + sub * PB + 2 * (RH + 2) * S; };
+  auto Aplane = [&](int sub) { return planes + sub * PB + (2 * (RH + 2) + RH) * S; };
+  uint16_t* list = reinterpret_cast<uint16_t*>(planes + E * PB);
   const int cap = g.list_cap;
   const uint32_t last_mask = low_mask(RW - 32 * (wpr - 1));
 
   const size_t ncell = static_cast<size_t>(BH) * W;
-  const uint8_t* __restrict__ in = a.in + env * ncell;
   const bool vec = (W & 15) == 0;  // 16-byte aligned rows (C0 is a multiple of 32)
 
-  // ---- load: uint8 layer -> bit-planes ------------------------------------------------
-  for (int i = threadIdx.x; i < wpr; i += blockDim.x) {  // zero padding rows of both buffers
-    Bp[0][i] = Bp[1][i] = 0u;
-    Bp[0][(RH + 1) * S + i] = Bp[1][(RH + 1) * S + i] = 0u;
-  }
-  if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
-  if (threadIdx.x < 2) {
-    s_total[threadIdx.x] = 0;
-    s_newly[threadIdx.x] = 0;
-  }
-  for (WordIter it(wpr, RH * wpr); it.ok(); it.next()) {
-    const int nc = min(32, RW - 32 * it.j);
-    const uint8_t* src = in + static_cast<size_t>(R0 + it.r) * W + C0 + 32 * it.j;
-    uint32_t b = 0u, x = 0u;
-    if (nc == 32 && vec) {
-      bytes_to_bits(src, b, x);
-    } else {
-      for (int k = 0; k < nc; ++k) {
-        const uint8_t v = src[k];
-        b |= static_cast<uint32_t>(v == 1) << k;
-        x |= static_cast<uint32_t>(v == 2) << k;
-      }
+  // ---- load: uint8 layers -> bit-planes ------------------------------------------------
+  for (int sub = 0; sub < E; ++sub) {
+    uint32_t* B0 = Bplane(sub, 0);
+    uint32_t* B1 = Bplane(sub, 1);
+    uint32_t* X = Xplane(sub);
+    for (int i = threadIdx.x; i < wpr; i += blockDim.x) {  // zero padding rows of both buffers
+      B0[i] = B1[i] = 0u;
+      B0[(RH + 1) * S + i] = B1[(RH + 1) * S + i] = 0u;
     }
-    Bp[0][(it.r + 1) * S + it.j] = b;
-    X[it.r * S + it.j] = x;
+    const bool live = env0 + sub < a.n_envs;
+    const uint8_t* __restrict__ in = a.in + (env0 + sub) * ncell;
+    for (WordIter it(wpr, RH * wpr); it.ok(); it.next()) {
+      const int nc = min(32, RW - 32 * it.j);
+      uint32_t b = 0u, x = 0u;
+      if (live) {
+        const uint8_t* src = in + static_cast<size_t>(R0 + it.r) * W + C0 + 32 * it.j;
+        if (nc == 32 && vec) {
+          bytes_to_bits(src, b, x);
+        } else {
+          for (int k = 0; k < nc; ++k) {
+            const uint8_t v = src[k];
+            b |= static_cast<uint32_t>(v == 1) << k;
+            x |= static_cast<uint32_t>(v == 2) << k;
+          }
+        }
+      }
+      B0[(it.r + 1) * S + it.j] = b;
+      X[it.r * S + it.j] = x;
+    }
   }
+  if (threadIdx.x < 4 * E) s_cnt[threadIdx.x >> 2][threadIdx.x & 3] = 0;
+  if (threadIdx.x < 2) s_total[threadIdx.x] = 0;
+  if (threadIdx.x < 2 * E) s_newly[threadIdx.x / E][threadIdx.x % E] = 0;
+  if (threadIdx.x < E)
+    s_prefix[0][threadIdx.x] = key_prefix(a.seed, a.streams[min(env0 + static_cast<int>(threadIdx.x), a.n_envs - 1)], a.step);
   __syncthreads();
 
   const DiagCounters dg{a.diag};
-  const uint64_t stream = a.streams[env];
   const uint64_t gbase = static_cast<uint64_t>(a.row_off + R0) * W + C0;  // RNG index of region (0,0)
   const int lane = threadIdx.x & 31;
+  const int my_sub = E > 1 ? static_cast<int>(threadIdx.x) / kResThreads : 0;  // P1 ownership
+  const int lt = E > 1 ? static_cast<int>(threadIdx.x) % kResThreads : static_cast<int>(threadIdx.x);
   // newly-ignited cells are counted only inside the output tile
   const int tr0 = r0 - R0, tr1 = min(r0 + g.tile_h, BH) - R0;
   const int tc0 = c0 - C0, tc1 = min(c0 + g.tile_w, W) - C0;
@@ -102,7 +116,7 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
   const int tj0 = tc0 >> 5, tj1 = (tc1 + 31) >> 5;
   const int twords = tj1 - tj0;
   // bit-planes of the output tile -> uint8 layer at `layer` (+ U/B/X counts when cnt3)
-  auto store_tile = [&](const uint32_t* Bs, uint8_t* __restrict__ layer, int32_t* cnt3) {
+  auto store_tile = [&](const uint32_t* Bs, const uint32_t* X, uint8_t* __restrict__ layer, int32_t* cnt3) {
     for (WordIter it(twords, (tr1 - tr0) * twords); it.ok(); it.next()) {
       const int rr = tr0 + it.r, j = tj0 + it.j;
       const uint32_t b = Bs[(rr + 1) * S + j], x = X[rr * S + j];
@@ -122,92 +136,103 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
   };
 
   for (int t = 0; t < g.n_steps; ++t) {
-    const uint32_t* B = Bp[cur];
-    uint32_t* Bn = Bp[cur ^ 1];
     const int par = t & 1;
-    if (threadIdx.x == 0) {  // the other parity's counters are free until the next step
-      s_total[par ^ 1] = 0;
-      s_newly[par ^ 1] = 0;
-    }
-    const uint64_t prefix = key_prefix(a.seed, stream, a.step + static_cast<uint64_t>(t));
+    if (threadIdx.x == 0) s_total[par ^ 1] = 0;  // the other parity's counters are free until the next step
+    if (threadIdx.x < E) s_newly[par ^ 1][threadIdx.x] = 0;
     const int srow = sched_row(a, a.step + static_cast<uint64_t>(t));  // wind in force
-    // ---- P1: each thread owns whole rows; the 3x3 dilation slides along the row in
+    // ---- P1: each thread owns whole rows of one env; the 3x3 dilation slides along the row in
     //      registers (3 shared loads per word: north, own, south) ------------------------------
     int cnt = 0;
     bool ovf = false;
-    for (int r = threadIdx.x; r < RH; r += blockDim.x) {
-      const uint32_t* up = B + (r + 2) * S;
-      const uint32_t* mid = B + (r + 1) * S;
-      const uint32_t* dn = B + r * S;
-      uint32_t* bn = Bn + (r + 1) * S;
-      const uint32_t* xr = X + r * S;
-      uint32_t* ar = ACT + r * S;
-      uint32_t vl = 0u;                            // column j-1: north | own | south
-      uint32_t uc = up[0], mc = mid[0], dc = dn[0];
-      uint32_t vc = uc | mc | dc;
-      for (int j = 0; j < wpr; ++j) {
-        uint32_t un = 0u, mn = 0u, dnn = 0u;
-        if (j + 1 < wpr) {
-          un = up[j + 1];
-          mn = mid[j + 1];
-          dnn = dn[j + 1];
+    {
+      const uint32_t* B = Bplane(my_sub, cur);
+      uint32_t* Bn = Bplane(my_sub, cur ^ 1);
+      const uint32_t* X = Xplane(my_sub);
+      uint32_t* ACT = Aplane(my_sub);
+      for (int r = lt; r < RH; r += kResThreads) {
+        const uint32_t* up = B + (r + 2) * S;
+        const uint32_t* mid = B + (r + 1) * S;
+        const uint32_t* dn = B + r * S;
+        uint32_t* bn = Bn + (r + 1) * S;
+        const uint32_t* xr = X + r * S;
+        uint32_t* ar = ACT + r * S;
+        uint32_t vl = 0u;                            // column j-1: north | own | south
+        uint32_t uc = up[0], mc = mid[0], dc = dn[0];
+        uint32_t vc = uc | mc | dc;
+        for (int j = 0; j < wpr; ++j) {
+          uint32_t un = 0u, mn = 0u, dnn = 0u;
+          if (j + 1 < wpr) {
+            un = up[j + 1];
+            mn = mid[j + 1];
+            dnn = dn[j + 1];
+          }
+          const uint32_t vn = un | mn | dnn;
+          // west/east neighbours of all three rows, plus north/south of the own column
+          const uint32_t any = ((vc << 1) | (vl >> 31)) | ((vc >> 1) | (vn << 31)) | uc | dc;
+          bn[j] = mc;
+          const uint32_t valid = j + 1 < wpr ? 0xffffffffu : last_mask;
+          const uint32_t act = ((~(mc | xr[j]) & valid) & any) | mc;
+          ar[j] = act;
+          cnt += __popc(act);
+          vl = vc;
+          vc = vn;
+          uc = un;
+          mc = mn;
+          dc = dnn;
         }
-        const uint32_t vn = un | mn | dnn;
-        // west/east neighbours of all three rows, plus north/south of the own column
-        const uint32_t any = ((vc << 1) | (vl >> 31)) | ((vc >> 1) | (vn << 31)) | uc | dc;
-        bn[j] = mc;
-        const uint32_t valid = j + 1 < wpr ? 0xffffffffu : last_mask;
-        const uint32_t act = ((~(mc | xr[j]) & valid) & any) | mc;
-        ar[j] = act;
-        cnt += __popc(act);
-        vl = vc;
-        vc = vn;
-        uc = un;
-        mc = mn;
-        dc = dnn;
       }
-    }
-    // one warp-aggregated list reservation per warp and step (skipped by quiet warps)
-    if (__ballot_sync(0xffffffffu, cnt > 0)) {
-      int incl = cnt;
+      // one warp-aggregated list reservation per warp and step (skipped by quiet warps)
+      if (__ballot_sync(0xffffffffu, cnt > 0)) {
+        int incl = cnt;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      int base = 0;
-      if (lane == 31) base = atomicAdd(&s_total[par], incl);
-      base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
-      if (cnt > 0) {
-        for (int r = threadIdx.x; r < RH; r += blockDim.x) {
-          for (int j = 0; j < wpr; ++j) {
-            uint32_t rest = ACT[r * S + j];
-            if (!rest) continue;
-            const int cell0 = r * RW + 32 * j;
-            while (rest && base < cap) {
-              const int bit = __ffs(rest) - 1;
-              rest &= rest - 1;
-              list[base++] = static_cast<uint16_t>(cell0 + bit);
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        int base = 0;
+        if (lane == 31) base = atomicAdd(&s_total[par], incl);
+        base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
+        if (cnt > 0) {
+          const int tag = E > 1 ? (my_sub << 15) : 0;
+          for (int r = lt; r < RH; r += kResThreads) {
+            for (int j = 0; j < wpr; ++j) {
+              uint32_t rest = ACT[r * S + j];
+              if (!rest) continue;
+              const int cell0 = r * RW + 32 * j;
+              while (rest && base < cap) {
+                const int bit = __ffs(rest) - 1;
+                rest &= rest - 1;
+                list[base++] = static_cast<uint16_t>((cell0 + bit) | tag);
+              }
+              ACT[r * S + j] = rest;  // overflow beyond the list capacity: done by this thread in P2
+              ovf |= rest != 0u;
             }
-            ACT[r * S + j] = rest;  // overflow beyond the list capacity: done by this thread in P2
-            ovf |= rest != 0u;
           }
         }
       }
     }
     __syncthreads();
-    // ---- P2: sparse decisions ------------------------------------------------------------
-    int newly = 0;
+    // ---- P2: sparse decisions over the pooled list ------------------------------------------
+    int newly[E];
+#pragma unroll
+    for (int q = 0; q < E; ++q) newly[q] = 0;
     const int total = min(s_total[par], cap);
-    auto decide = [&](int lc) {
+    if (threadIdx.x >= blockDim.x - E) {  // next step's prefixes, published by the end-of-step barrier
+      const int q = static_cast<int>(threadIdx.x) - static_cast<int>(blockDim.x - E);
+      s_prefix[par ^ 1][q] = key_prefix(a.seed, a.streams[min(env0 + q, a.n_envs - 1)],
+                                        a.step + static_cast<uint64_t>(t + 1));
+    }
+    auto decide = [&](int sub, int lc) {
+      const uint32_t* B = Bplane(sub, cur);
+      uint32_t* Bn = Bplane(sub, cur ^ 1);
       const int rr = lc / RW, cc = lc - rr * RW;
       const int wi = (rr + 1) * S + (cc >> 5);
       const uint32_t bit = 1u << (cc & 31);
-      const uint64_t m = cell_bits53(prefix, gbase + static_cast<uint64_t>(rr) * W + cc, 0);
+      const uint64_t m = cell_bits53(s_prefix[par][sub], gbase + static_cast<uint64_t>(rr) * W + cc, 0);
       if (B[wi] & bit) {
         if (m >= a.pc_thr) {
           atomicAnd(Bn + wi, ~bit);
-          atomicOr(X + rr * S + (cc >> 5), bit);
+          atomicOr(Xplane(sub) + rr * S + (cc >> 5), bit);
         }
       } else {
         uint32_t nb = 0;
@@ -217,55 +242,78 @@ __global__ void __launch_bounds__(kResThreads, 8) k_step_blocked(StepArgs a, Blo
           if (uc < 0 || uc >= RW) continue;  // padding rows cover ur = -1 and ur = RH
           nb |= ((B[(ur + 1) * S + (uc >> 5)] >> (uc & 31)) & 1u) << k;
         }
-        if (ignite<MODE>(a, env, R0 + rr, C0 + cc, nb, m, dg, srow)) {
+        if (ignite<MODE>(a, env0 + sub, R0 + rr, C0 + cc, nb, m, dg, srow)) {
           atomicOr(Bn + wi, bit);
-          newly += (rr >= tr0 && rr < tr1 && cc >= tc0 && cc < tc1);
+          const int in_tile = (rr >= tr0 && rr < tr1 && cc >= tc0 && cc < tc1);
+#pragma unroll
+          for (int q = 0; q < E; ++q) newly[q] += (q == sub) ? in_tile : 0;
         }
       }
     };
-    for (int i = threadIdx.x; i < total; i += blockDim.x) decide(list[i]);
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int e = list[i];
+      if (E > 1) decide(e >> 15, e & 0x7fff);
+      else decide(0, e);
+    }
     if (ovf) {
-      for (int r = threadIdx.x; r < RH; r += blockDim.x)
+      uint32_t* ACT = Aplane(my_sub);
+      for (int r = lt; r < RH; r += kResThreads)
         for (int j = 0; j < wpr; ++j) {
           uint32_t rest = ACT[r * S + j];
           while (rest) {
             const int bit = __ffs(rest) - 1;
             rest &= rest - 1;
-            decide(r * RW + 32 * j + bit);
+            decide(my_sub, r * RW + 32 * j + bit);
           }
         }
     }
     if (t == g.n_steps - 1) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) newly += __shfl_xor_sync(0xffffffffu, newly, o);
-      if (lane == 0 && newly) atomicAdd(&s_newly[par], newly);
+      for (int q = 0; q < E; ++q) {
+        int v = newly[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && v) atomicAdd(&s_newly[par][q], v);
+      }
     }
     __syncthreads();
     cur ^= 1;
-    if (a.traj)  // record (run_stochastic(record=true), engine.cpp:116): this step's tile
-      store_tile(Bp[cur], a.traj + ((a.traj_t0 + t) * a.n_envs + env) * ncell, nullptr);
+    if (a.traj) {  // record (run_stochastic(record=true), engine.cpp:116): this step's tile
+      for (int sub = 0; sub < E; ++sub)
+        if (env0 + sub < a.n_envs)
+          store_tile(Bplane(sub, cur), Xplane(sub), a.traj + ((a.traj_t0 + t) * a.n_envs + env0 + sub) * ncell,
+                     nullptr);
+    }
   }
 
-  // ---- store the tile: bit-planes -> uint8, counts -----------------------------------------
-  int32_t cnt3[3] = {0, 0, 0};
-  store_tile(Bp[cur], a.out + env * ncell, cnt3);
-  const int32_t nU = cnt3[0], nB = cnt3[1], nX = cnt3[2];
+  // ---- store the tiles: bit-planes -> uint8, counts -----------------------------------------
+  for (int sub = 0; sub < E; ++sub) {
+    if (env0 + sub >= a.n_envs) break;
+    int32_t cnt3[3] = {0, 0, 0};
+    store_tile(Bplane(sub, cur), Xplane(sub), a.out + (env0 + sub) * ncell, cnt3);
+    if (a.counts) {
+      atomicAdd(&s_cnt[sub][0], cnt3[0]);
+      atomicAdd(&s_cnt[sub][1], cnt3[1]);
+      atomicAdd(&s_cnt[sub][2], cnt3[2]);
+    }
+  }
   if (a.counts) {
-    atomicAdd(&s_cnt[0], nU);
-    atomicAdd(&s_cnt[1], nB);
-    atomicAdd(&s_cnt[2], nX);
     __syncthreads();
-    if (threadIdx.x < 3) atomicAdd(a.counts + env * 4 + threadIdx.x, s_cnt[threadIdx.x]);
-    if (threadIdx.x == 3 && g.n_steps > 0)
-      atomicAdd(a.counts + env * 4 + 3, s_newly[(g.n_steps - 1) & 1]);
+    if (threadIdx.x < 4 * E) {
+      const int sub = threadIdx.x >> 2, k = threadIdx.x & 3;
+      if (env0 + sub < a.n_envs) {
+        if (k < 3) atomicAdd(a.counts + (env0 + sub) * 4 + k, s_cnt[sub][k]);
+        else if (g.n_steps > 0) atomicAdd(a.counts + (env0 + sub) * 4 + 3, s_newly[(g.n_steps - 1) & 1][sub]);
+      }
+    }
   }
 }
 
-size_t blocked_smem_bytes(int region_h, int region_w, int list_cap) {
+size_t blocked_smem_bytes(int region_h, int region_w, int list_cap, int envs_per_cta) {
   const size_t S = plane_stride((region_w + 31) / 32);
   const size_t planes = (2 * (static_cast<size_t>(region_h) + 2) + 2 * region_h) * S * sizeof(uint32_t);
   const size_t list = static_cast<size_t>(list_cap) * sizeof(uint16_t);
-  return planes + ((list + 15) & ~size_t(15));
+  return envs_per_cta * planes + ((list + 15) & ~size_t(15));
 }
 
 static int list_cap_for(int cells) {
@@ -277,18 +325,25 @@ static int list_cap_for(int cells) {
 
 bool resident_fits(int h, int w) {
   return static_cast<size_t>(h) * w <= 65536 &&
-         blocked_smem_bytes(h, w, list_cap_for(h * w)) <= kResMaxSmem;
+         blocked_smem_bytes(h, w, list_cap_for(h * w), 1) <= kResMaxSmem;
 }
 
-BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_off) {
+BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_off, int n_envs,
+                      int envs_per_cta) {
   BlockGeom g{};
   g.row_off = row_off;
+  g.envs_per_cta = 1;
   if (!force_tiles && resident_fits(buf_h, w)) {  // whole env per CTA, all steps fused
     g.tile_h = buf_h;
     g.tile_w = ((w + 31) / 32) * 32;
     g.halo_rows = 0;
     g.halo_cols = 0;
     g.n_steps = n_steps;
+    // pooled pairs: only when the cells fit the list tag and the batch still fills the GPU
+    // (>= 2 CTAs per SM at E = 2); envs_per_cta 1/2 forces, 0 = auto
+    const bool pair_ok = static_cast<size_t>(buf_h) * w <= 32768;
+    if (envs_per_cta == 2 && pair_ok) g.envs_per_cta = 2;
+    if (envs_per_cta == 0 && pair_ok && n_envs >= kPairMinEnvs) g.envs_per_cta = 2;
   } else {
     g.halo_rows = kBlockHalo;
     g.tile_w = w <= kBlockTileW + 64 ? ((w + 31) / 32) * 32 : kBlockTileW;
@@ -302,27 +357,27 @@ BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_o
     g.n_steps = !fuzzy ? n_steps : (n_steps < kBlockHalo ? n_steps : kBlockHalo);
   }
   const int rh = g.tile_h + 2 * g.halo_rows, rw = g.tile_w + 2 * g.halo_cols;
-  g.list_cap = list_cap_for((rh < buf_h ? rh : buf_h) * (rw < w ? rw : w));
+  g.list_cap = g.envs_per_cta * list_cap_for((rh < buf_h ? rh : buf_h) * (rw < w ? rw : w));
   return g;
+}
+
+template <int MODE, int E>
+static cudaError_t launch_blocked_t(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k_step_blocked<MODE, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sm));
+  if (e != cudaSuccess) return e;
+  const dim3 grid((a.w + g.tile_w - 1) / g.tile_w, (a.h + g.tile_h - 1) / g.tile_h, (a.n_envs + E - 1) / E);
+  k_step_blocked<MODE, E><<<grid, kResThreads * E, sm, s>>>(a, g);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_step_blocked(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s) {
   const int rh = g.tile_h + 2 * g.halo_rows, rw = g.tile_w + 2 * g.halo_cols;
-  const size_t sm = blocked_smem_bytes(rh < a.h ? rh : a.h, rw < a.w ? rw : a.w, g.list_cap);
-  const dim3 grid((a.w + g.tile_w - 1) / g.tile_w, (a.h + g.tile_h - 1) / g.tile_h, a.n_envs);
-  cudaError_t e;
-  if (mode == kStaticTables) {
-    e = cudaFuncSetAttribute(k_step_blocked<kStaticTables>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sm));
-    if (e != cudaSuccess) return e;
-    k_step_blocked<kStaticTables><<<grid, kResThreads, sm, s>>>(a, g);
-  } else {
-    e = cudaFuncSetAttribute(k_step_blocked<kStaticTerrain>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sm));
-    if (e != cudaSuccess) return e;
-    k_step_blocked<kStaticTerrain><<<grid, kResThreads, sm, s>>>(a, g);
-  }
-  return cudaGetLastError();
+  const int E = g.envs_per_cta == 2 ? 2 : 1;
+  const size_t sm = blocked_smem_bytes(rh < a.h ? rh : a.h, rw < a.w ? rw : a.w, g.list_cap, E);
+  if (mode == kStaticTables)
+    return E == 2 ? launch_blocked_t<kStaticTables, 2>(a, g, sm, s) : launch_blocked_t<kStaticTables, 1>(a, g, sm, s);
+  return E == 2 ? launch_blocked_t<kStaticTerrain, 2>(a, g, sm, s) : launch_blocked_t<kStaticTerrain, 1>(a, g, sm, s);
 }
 
 }  // namespace ebl

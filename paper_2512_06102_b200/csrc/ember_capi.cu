@@ -72,6 +72,7 @@ struct ebl_batch {
   int cur = 0;
   int kernel = EBL_KERNEL_AUTO;
   int tile_h = 0, tile_w = 0, tile_halo = 0;  // explicit blocked tiling (tests); 0 = planned
+  int envs_per_cta = 0;                         // blocked kernel env pooling: 0 auto, 1, 2 (set_kernel)
   bool counts_valid = false;
   DevBuf<int32_t> counts;
   DevBuf<unsigned long long> diag;
@@ -736,10 +737,13 @@ uint64_t ebl_batch_step_index(const ebl_batch* b) { return b ? b->step : 0; }
 
 int ebl_batch_set_kernel(ebl_batch* b, int which) {
   if (int e = check_batch(b)) return e;
-  if (which < EBL_KERNEL_AUTO || which > EBL_KERNEL_BLOCKED) return set_err(EBL_EINVAL, "unknown kernel");
-  if (which == EBL_KERNEL_RESIDENT && !ebl::resident_fits(b->h, b->w))
+  if (which < EBL_KERNEL_AUTO || which > EBL_KERNEL_PAIRED) return set_err(EBL_EINVAL, "unknown kernel");
+  if ((which == EBL_KERNEL_RESIDENT || which == EBL_KERNEL_PAIRED) && !ebl::resident_fits(b->h, b->w))
     return set_err(EBL_EINVAL, "env too large for the resident kernel");
+  if (which == EBL_KERNEL_PAIRED && b->ncell > 32768)
+    return set_err(EBL_EINVAL, "paired residency needs H*W <= 32768");
   b->kernel = which;
+  b->envs_per_cta = which == EBL_KERNEL_AUTO ? 0 : (which == EBL_KERNEL_PAIRED ? 2 : 1);
   return EBL_OK;
 }
 
@@ -768,8 +772,10 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
   } else {  // bit-sliced blocked kernel: whole env per CTA when it fits, else halo tiles
     const bool force_tiles = b->kernel == EBL_KERNEL_BLOCKED;
     for (int done = 0; done < n_steps;) {
-      ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps - done, force_tiles, 0);
+      ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps - done, force_tiles, 0, b->n_envs,
+                                          b->envs_per_cta);
       if (b->tile_h > 0) {  // test hook: explicit tiling
+        g.envs_per_cta = 1;
         g.tile_h = b->tile_h;
         g.tile_w = b->tile_w;
         g.halo_rows = b->tile_halo;
@@ -863,7 +869,7 @@ int ebl_batch_set_tiling(ebl_batch* b, int tile_h, int tile_w, int halo) {
       (halo == 0 && (tile_h < b->h || tile_w < b->w)))
     return set_err(EBL_EINVAL, "tiling: tile_w a positive multiple of 32, halo in [1,32] unless one tile");
   const int rh = std::min(b->h, tile_h + 2 * halo), rw = std::min(b->w, tile_w + (tile_w >= b->w ? 0 : 64));
-  if (rh * rw > 65536 || ebl::blocked_smem_bytes(rh, rw, std::max(1, rh * rw / 4)) > ebl::kResMaxSmem)
+  if (rh * rw > 65536 || ebl::blocked_smem_bytes(rh, rw, std::max(1, rh * rw / 4), 1) > ebl::kResMaxSmem)
     return set_err(EBL_EINVAL, "tiling: region exceeds shared memory");
   b->tile_h = tile_h;
   b->tile_w = tile_w;

@@ -131,7 +131,8 @@ __device__ __forceinline__ float terrain_lambda32(const TerrainView& t, int w, i
       const int u = (r - kDy[k]) * w + (c - kDx[k]);
       const float dz = zv - t.elev[u];
       const float s = dz == dz ? atanf(dz * t.inv_dist32[k & 1]) : 0.f;  // nodata: slope 0
-      lam += t.pal_src32[t.fuel[u]] * t.kw32[k] * expf(t.alpha_s32 * s);
+      // ex2.approx: relative error ~1e-7 for |alpha_s * s| <= 80 (force64 beyond), far inside the guard
+      lam += t.pal_src32[t.fuel[u]] * t.kw32[k] * __expf(t.alpha_s32 * s);
     }
   }
   return lam;

@@ -17,9 +17,14 @@ constexpr int kBlockTileH = 64;     // tiled blocked kernel (large grids): 64 x 
 constexpr int kBlockTileW = 256;    // 8-row / 32-column light-cone halo, 8 steps per launch
 constexpr int kBlockHalo = 8;
 
-size_t blocked_smem_bytes(int region_h, int region_w, int list_cap);
+// AUTO never pairs: measured on C1 (1024 x 128^2 x 200, scripts/ab_pair.sh) pairs ran 1.14 ms vs
+// 1.07 ms unpaired -- the heavy envs' step latency is not P2-throughput bound.  EBL_KERNEL_PAIRED
+// keeps the pooled form selectable.
+constexpr int kPairMinEnvs = 1 << 30;
+size_t blocked_smem_bytes(int region_h, int region_w, int list_cap, int envs_per_cta);
 bool resident_fits(int h, int w);
-BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_off);
+BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_off, int n_envs,
+                      int envs_per_cta);
 cudaError_t launch_step_blocked(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s);
 
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s);

@@ -54,7 +54,8 @@ struct BlockGeom {
   int tile_h, tile_w, halo_rows, halo_cols;
   int n_steps;
   int row_off;
-  int list_cap;
+  int list_cap;      // active-list entries per CTA (all its envs)
+  int envs_per_cta;  // 1, or 2 (whole-env residency, pooled P2 list)
 };
 
 // Deterministic mode + adjoint (ember_det.cu).  fp64 planes [env][cell] (the

@@ -16,7 +16,7 @@ from . import _lib
 from ._lib import EnvConfig, EnvState, SimConfig, check, lib
 
 UNBURNED, BURNING, BURNED = 0, 1, 2
-KERNEL_AUTO, KERNEL_TILED, KERNEL_RESIDENT, KERNEL_BLOCKED = 0, 1, 2, 3
+KERNEL_AUTO, KERNEL_TILED, KERNEL_RESIDENT, KERNEL_BLOCKED, KERNEL_PAIRED = 0, 1, 2, 3, 4
 
 
 def _ptr(a: np.ndarray | None):

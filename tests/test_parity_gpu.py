@@ -12,7 +12,7 @@ from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [eb.KERNEL_TILED, eb.KERNEL_RESIDENT, eb.KERNEL_BLOCKED]
+KERNELS = [eb.KERNEL_TILED, eb.KERNEL_RESIDENT, eb.KERNEL_BLOCKED, eb.KERNEL_PAIRED]
 REL_TOL = 1e-5  # north_star: lambda and p within 1e-5 relative in fp32
 
 
@@ -187,6 +187,8 @@ def test_kernels_identical_ragged(port, h, w):
     outs = []
     variants = [(eb.KERNEL_TILED, None), (eb.KERNEL_AUTO, None), (eb.KERNEL_BLOCKED, None),
                 (eb.KERNEL_AUTO, (8, 32, 3)), (eb.KERNEL_AUTO, (5, 64, 1)), (eb.KERNEL_AUTO, (16, 96, 7))]
+    if h * w <= 32768:  # two envs per CTA (5 envs: the last CTA carries one)
+        variants.append((eb.KERNEL_PAIRED, None))
     for kernel, tiling in variants:
         b = eb.Batch(n, h, w)
         b.set_terrain(cls, el, veg, den, 25.0)

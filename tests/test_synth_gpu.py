@@ -15,7 +15,7 @@ from test_oracle_pin import landcover_restated
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [eb.KERNEL_TILED, eb.KERNEL_RESIDENT, eb.KERNEL_BLOCKED]
+KERNELS = [eb.KERNEL_TILED, eb.KERNEL_RESIDENT, eb.KERNEL_BLOCKED, eb.KERNEL_PAIRED]
 WORLDCOVER = {10: (0.4, 0.3), 20: (0.25, 0.1), 30: (0.15, -0.1), 40: (0.0, -0.2), 50: (-0.8, -0.8),
               60: (-0.7, -0.6), 70: (-1.0, -1.0), 80: (-1.0, -1.0), 90: (-0.4, -0.3),
               95: (-0.2, -0.1), 100: (-0.3, -0.4)}
