@@ -7,9 +7,10 @@ reset the 1024 fire layers to their ignitions and advance 200 CA steps
 
   value   device throughput, inputs resident in HBM, CUDA events on the launch stream,
           L2 flushed (256 MiB write) between timed iterations, max over ranks.
-  e2e     the same metric through the public C-ABI with HOST buffers: pinned host ->
-          device copy of the 1024 initial layers, 200 steps, device -> host copy of the
-          1024 final layers, all inside the timed region.
+  e2e     the same metric through the public C-ABI with HOST buffers (ebl_batch_run):
+          pinned host -> device copy of the 1024 initial layers, 200 steps, device -> host
+          copy of the 1024 final layers, all inside the timed region; the library pipelines
+          the copies against the compute over env chunks.
   roofline  dominant kernel (k_step_blocked) vs measured HBM copy bandwidth, at SURVEY
           §8(d)'s 10 algorithmic bytes per cell-update.
   cpu_baseline  the reference's own code (oracle/_ref = /root/reference/proj compiled in
@@ -93,7 +94,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            time.sleep(0.05)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.nv:
@@ -174,6 +175,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "tiled", "resident", "paired"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pipeline", type=int, default=0,
+                    help="env chunks of the e2e host-buffer pipeline (0 = library default)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -228,19 +231,19 @@ def main():
     kern_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
     b.diag(reset=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        for i in range(args.steps):
-            with torch.cuda.stream(stream):
-                flush.zero_()                       # untimed L2 flush between iterations
-                ev[i][0].record(stream)
-                eb._lib.check(eb.lib().ebl_batch_set_state_device(b.handle, init_dev.data_ptr()))
-                b.set_key(SEED, 0, first_stream=env0)
-                kern_ev[i][0].record(stream)
-                b.step(CA_STEPS)
-                kern_ev[i][1].record(stream)
-                ev[i][1].record(stream)
-        barrier()
+    clk = ClockSampler(local).__enter__()   # sampled over both timed regions (device and e2e)
+    barrier()
+    for i in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()                       # untimed L2 flush between iterations
+            ev[i][0].record(stream)
+            eb._lib.check(eb.lib().ebl_batch_set_state_device(b.handle, init_dev.data_ptr()))
+            b.set_key(SEED, 0, first_stream=env0)
+            kern_ev[i][0].record(stream)
+            b.step(CA_STEPS)
+            kern_ev[i][1].record(stream)
+            ev[i][1].record(stream)
+    barrier()
     diag = b.diag()
     step_ms = [s.elapsed_time(e) for s, e in ev]
     kern_ms = [s.elapsed_time(e) for s, e in kern_ev]
@@ -258,11 +261,11 @@ def main():
     L = eb.lib()
     in_ptr, out_ptr = h_in.data_ptr(), h_out.data_ptr()
 
-    def e2e_step():
-        eb._lib.check(L.ebl_batch_set_state(b.handle, in_ptr))
+    eb._lib.check(L.ebl_batch_set_pipeline(b.handle, args.pipeline))
+
+    def e2e_step():  # the public host-buffer call: copy in, 200 fused steps, copy out (pipelined)
         eb._lib.check(L.ebl_batch_set_key(b.handle, SEED, 0, None, env0))
-        eb._lib.check(L.ebl_step_batch(b.handle, CA_STEPS))
-        eb._lib.check(L.ebl_batch_get_state(b.handle, out_ptr))
+        eb._lib.check(L.ebl_batch_run(b.handle, in_ptr, CA_STEPS, out_ptr))
 
     for _ in range(2):
         e2e_step()
@@ -278,6 +281,7 @@ def main():
         e1.record(stream)
         e1.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
+    clk.__exit__(None, None, None)
     te = torch.tensor([sum(e2e_ms) / 1e3], dtype=torch.float64, device=f"cuda:{local}")
     if dist_on:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)

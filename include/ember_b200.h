@@ -133,6 +133,16 @@ uint64_t ebl_batch_step_index(const ebl_batch* b);
  * {seed, step+t, stream[e]}; the batch step counter advances by n_steps. */
 int ebl_step_batch(ebl_batch* b, int n_steps);
 
+/* make_stochastic_batch + step_batch x n_steps + reading the members back (engine.cpp:122-159,
+ * emberline_main.cpp:417-424), from and to HOST buffers [n_envs][H*W]: identical to
+ * ebl_batch_set_state + ebl_step_batch + ebl_batch_get_state, but pipelined over env chunks
+ * (chunk c's host->device copy, its fused launch and its device->host copy overlap the other
+ * chunks' work).  Returns when final_states is written.  Pinned host memory makes the copies
+ * asynchronous. */
+int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* final_states);
+/* Number of env chunks ebl_batch_run pipelines over (0 = auto, 8; 1 = no pipelining). */
+int ebl_batch_set_pipeline(ebl_batch* b, int chunks);
+
 /* run_stochastic(record=true) (engine.cpp:108,116): ebl_step_batch that also stores the layers
  * after every step into traj [n_steps][n_envs][H*W] (device pointer when on_device, else host;
  * the initial layers are the caller's).  The blocked kernel writes them from shared memory as

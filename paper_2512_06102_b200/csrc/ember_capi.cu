@@ -128,6 +128,23 @@ struct ebl_batch {
   std::vector<uint8_t> h_fuel;      // host copies of the terrain (exact host-built tables)
   std::vector<float> h_elev;
   bool h_terrain_stale = false;     // device terrain newer than h_fuel/h_elev (device-built)
+
+  // host-buffer pipeline (ebl_batch_run): copy-in stream, per-chunk compute streams, copy-out
+  int pipe_chunks = 0;              // 0 = auto
+  cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
+  std::vector<cudaStream_t> pipe_comp;
+  std::vector<cudaEvent_t> pipe_ev_in, pipe_ev_done;
+  cudaEvent_t pipe_ev_start = nullptr, pipe_ev_end = nullptr;
+
+  ~ebl_batch() {
+    for (cudaStream_t s : pipe_comp) cudaStreamDestroy(s);
+    for (cudaEvent_t e : pipe_ev_in) cudaEventDestroy(e);
+    for (cudaEvent_t e : pipe_ev_done) cudaEventDestroy(e);
+    if (pipe_in) cudaStreamDestroy(pipe_in);
+    if (pipe_out) cudaStreamDestroy(pipe_out);
+    if (pipe_ev_start) cudaEventDestroy(pipe_ev_start);
+    if (pipe_ev_end) cudaEventDestroy(pipe_ev_end);
+  }
 };
 
 namespace {
@@ -234,6 +251,49 @@ ebl::StepArgs step_args(const ebl_batch* b) {
   // the fp32 guard band (1e-4 relative) holds while |alpha_s * slope| stays O(10)
   a.force64 = !(std::fabs(b->cfg.alpha_s) <= 50.0);
   return a;
+}
+
+// StepArgs of the env sub-range [off, off + n) of a batch (per-env pointers advanced).
+ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
+  const size_t o = static_cast<size_t>(off);
+  a.n_envs = n;
+  a.in += o * b->ncell;
+  a.out += o * b->ncell;
+  a.streams += o;
+  if (a.counts) a.counts += o * 4;
+  if (a.tab_stride) {
+    a.pot += o * a.tab_stride * 8;
+    a.gamma += o * a.tab_stride;
+  }
+  if (a.ter_stride) {
+    a.fuel += o * a.ter_stride;
+    a.elev += o * a.ter_stride;
+  }
+  if (a.kw_stride) {
+    a.kw32 += o * a.kw_stride;
+    a.kw64 += o * a.kw_stride;
+  }
+  return a;
+}
+
+int ensure_pipeline(ebl_batch* b, int chunks) {
+  if (!b->pipe_in) {
+    EBL_CUDA(cudaStreamCreateWithFlags(&b->pipe_in, cudaStreamNonBlocking));
+    EBL_CUDA(cudaStreamCreateWithFlags(&b->pipe_out, cudaStreamNonBlocking));
+    EBL_CUDA(cudaEventCreateWithFlags(&b->pipe_ev_start, cudaEventDisableTiming));
+    EBL_CUDA(cudaEventCreateWithFlags(&b->pipe_ev_end, cudaEventDisableTiming));
+  }
+  while (static_cast<int>(b->pipe_comp.size()) < chunks) {
+    cudaStream_t s;
+    cudaEvent_t e0, e1;
+    EBL_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    EBL_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    EBL_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+    b->pipe_comp.push_back(s);
+    b->pipe_ev_in.push_back(e0);
+    b->pipe_ev_done.push_back(e1);
+  }
+  return EBL_OK;
 }
 
 }  // namespace
@@ -799,6 +859,79 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
       done += g.n_steps;
     }
   }
+  b->steps_done += n_steps;
+  b->counts_valid = true;
+  return EBL_OK;
+}
+
+int ebl_batch_set_pipeline(ebl_batch* b, int chunks) {
+  if (int e = check_batch(b)) return e;
+  if (chunks < 0 || chunks > 256) return set_err(EBL_EINVAL, "pipeline chunks must be in [0, 256]");
+  b->pipe_chunks = chunks;
+  return EBL_OK;
+}
+
+// set_state + step_batch x n_steps + get_state from/to HOST buffers, pipelined over env chunks:
+// chunk c's H2D copy (copy-in stream, in order), its fused n-step launch (own stream, after the
+// copy), its D2H copy (copy-out stream, after the launch) -- transfers of later/earlier chunks
+// overlap the compute of the others.  Identical results to the unpipelined sequence (envs are
+// independent; the RNG is keyed by stream, not by launch).  Pinned host buffers are needed for
+// the copies to be asynchronous.
+int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* final_states) {
+  if (int e = check_batch(b)) return e;
+  if (!initial || !final_states) return set_err(EBL_EINVAL, "null state buffer");
+  if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
+  if (int e = prepare(b)) return e;
+  const bool resident = b->kernel != EBL_KERNEL_TILED && b->kernel != EBL_KERNEL_BLOCKED &&
+                        b->tile_h == 0 && ebl::resident_fits(b->h, b->w);
+  int chunks = b->pipe_chunks > 0 ? b->pipe_chunks : 8;
+  chunks = std::min(chunks, b->n_envs);
+  if (!resident || n_steps == 0 || chunks <= 1) {  // one launch per step set: plain sequence
+    int rc;
+    if ((rc = ebl_batch_set_state(b, initial))) return rc;
+    if ((rc = ebl_step_batch(b, n_steps))) return rc;
+    return ebl_batch_get_state(b, final_states);
+  }
+  EBL_CUDA(cudaSetDevice(b->device));
+  if (int e = ensure_pipeline(b, chunks)) return e;
+  const ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps, false, 0, b->n_envs, b->envs_per_cta);
+  ebl::StepArgs a = step_args(b);
+  a.counts = b->counts.p;
+  // everything earlier on the batch stream (state/key uploads, statics) happens first
+  EBL_CUDA(cudaEventRecord(b->pipe_ev_start, b->stream));
+  EBL_CUDA(cudaStreamWaitEvent(b->pipe_in, b->pipe_ev_start, 0));
+  for (int c = 0; c < chunks; ++c) EBL_CUDA(cudaStreamWaitEvent(b->pipe_comp[c], b->pipe_ev_start, 0));
+  const int per = (b->n_envs + chunks - 1) / chunks;
+  for (int c = 0; c < chunks; ++c) {
+    const int off = c * per, n = std::min(per, b->n_envs - off);
+    if (n <= 0) break;
+    const size_t bytes = static_cast<size_t>(n) * b->ncell, boff = static_cast<size_t>(off) * b->ncell;
+    EBL_CUDA(cudaMemcpyAsync(b->state[b->cur].p + boff, initial + boff, bytes, cudaMemcpyHostToDevice, b->pipe_in));
+    EBL_CUDA(cudaEventRecord(b->pipe_ev_in[c], b->pipe_in));
+  }
+  for (int c = 0; c < chunks; ++c) {
+    const int off = c * per, n = std::min(per, b->n_envs - off);
+    if (n <= 0) break;
+    cudaStream_t s = b->pipe_comp[c];
+    EBL_CUDA(cudaStreamWaitEvent(s, b->pipe_ev_in[c], 0));
+    EBL_CUDA(cudaMemsetAsync(b->counts.p + static_cast<size_t>(off) * 4, 0, static_cast<size_t>(n) * 4 * sizeof(int32_t), s));
+    EBL_CUDA(ebl::launch_step_blocked(chunk_args(b, a, off, n), b->mode, g, s));
+    EBL_CUDA(cudaEventRecord(b->pipe_ev_done[c], s));
+  }
+  for (int c = 0; c < chunks; ++c) {
+    const int off = c * per, n = std::min(per, b->n_envs - off);
+    if (n <= 0) break;
+    const size_t bytes = static_cast<size_t>(n) * b->ncell, boff = static_cast<size_t>(off) * b->ncell;
+    EBL_CUDA(cudaStreamWaitEvent(b->pipe_out, b->pipe_ev_done[c], 0));
+    EBL_CUDA(cudaMemcpyAsync(final_states + boff, b->state[b->cur ^ 1].p + boff, bytes, cudaMemcpyDeviceToHost,
+                             b->pipe_out));
+  }
+  EBL_CUDA(cudaEventRecord(b->pipe_ev_end, b->pipe_out));
+  EBL_CUDA(cudaStreamWaitEvent(b->stream, b->pipe_ev_end, 0));  // later batch work follows the run
+  EBL_CUDA(cudaStreamSynchronize(b->pipe_out));
+  b->cur ^= 1;
+  b->step += n_steps;
+  b->launches += chunks;
   b->steps_done += n_steps;
   b->counts_valid = true;
   return EBL_OK;

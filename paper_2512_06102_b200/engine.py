@@ -183,6 +183,19 @@ class Batch:
         """step_batch (engine.cpp:134-159) n_steps times, asynchronously on the batch stream."""
         check(lib().ebl_step_batch(self._h, n_steps))
 
+    def run(self, initial, n_steps: int, out=None) -> np.ndarray:
+        """set_state(initial) + step(n_steps) + get_state() from/to host buffers, pipelined over
+        env chunks (ebl_batch_run); pass pinned arrays for overlapped copies."""
+        st = np.ascontiguousarray(np.broadcast_to(np.asarray(initial, dtype=np.uint8),
+                                                  (self.n_envs, self.height, self.width)))
+        if out is None:
+            out = np.empty((self.n_envs, self.height, self.width), dtype=np.uint8)
+        check(lib().ebl_batch_run(self._h, _ptr(st), n_steps, _ptr(out)))
+        return out
+
+    def set_pipeline(self, chunks: int) -> None:
+        check(lib().ebl_batch_set_pipeline(self._h, chunks))
+
     def step_record(self, n_steps: int) -> np.ndarray:
         """step(n_steps) keeping every step's layers (run_stochastic record=true, engine.cpp:116):
         [n_steps, n_envs, H, W] uint8 (the initial layers are not included)."""

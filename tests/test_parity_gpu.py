@@ -425,3 +425,32 @@ def test_wind_schedule_general_form_vs_oracle(port):
         g = O.grid_layers(port, "port", sp[row, 0], dr[row, 0], L["veg"], L["den"], L["slope8"])
         st = O.run(port, "port", g, cfg, 21, s, 0, 1, st)
         assert np.array_equal(traj[s, 0], st), s
+
+
+@pytest.mark.parametrize("n_envs,chunks", [(13, 4), (64, 8), (7, 7), (5, 1), (3, 16)])
+def test_pipelined_host_run_equals_sequence(n_envs, chunks):
+    """ebl_batch_run (chunked H2D / fused launch / D2H pipeline) == set_state + step + get_state,
+    counts included, and the batch continues from the run's result."""
+    h, w, steps, seed = 64, 96, 40, 3
+    t = eb.synth_terrain(seed, n_envs, h, w, env_id0=100)
+    init = eb.synth_ignitions(seed, t, 4, env_id0=100)
+    out = {}
+    for mode in ("seq", "run"):
+        with eb.Batch(n_envs, h, w) as b:
+            b.set_terrain(t.fuel_class, t.elevation, t.class_veg, t.class_den, 30.0)
+            b.set_wind(t.wind_speed, t.wind_direction)
+            b.set_key(seed, 5, first_stream=100)
+            if mode == "seq":
+                b.set_state(init)
+                b.step(steps)
+                fin = b.get_state()
+            else:
+                b.set_pipeline(chunks)
+                fin = b.run(init, steps)
+            counts = b.counts().copy()
+            b.step(3)  # continues from the run's final layers and step index
+            out[mode] = (fin, counts, b.get_state(), b.step_index)
+    assert np.array_equal(out["seq"][0], out["run"][0])
+    assert np.array_equal(out["seq"][1], out["run"][1])
+    assert np.array_equal(out["seq"][2], out["run"][2])
+    assert out["seq"][3] == out["run"][3] == 5 + steps + 3
