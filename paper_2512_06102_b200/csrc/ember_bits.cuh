@@ -41,6 +41,16 @@ struct WordIter {
 };
 
 
+// Bulk L2 prefetch (cp.async.bulk.prefetch, sm_90+): a hint, `bytes` a multiple of 16, 16-byte
+// aligned address; no completion to wait for.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uintptr_t lo = (a + 15) & ~uintptr_t(15);
+  if (bytes < 32) return;
+  const uint32_t n = (bytes - static_cast<uint32_t>(lo - a)) & ~15u;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(n) : "memory");
+}
+
 // Row stride (words) of a bit-plane with wpr words per row: odd, so the 32 lanes of a warp
 // each reading "its" row at the same column hit 32 distinct shared-memory banks.
 __host__ __device__ __forceinline__ int plane_stride(int wpr) { return wpr | 1; }

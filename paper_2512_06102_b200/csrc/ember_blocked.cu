@@ -32,6 +32,16 @@
 #include "ember_kernels.h"
 #include "ember_params.h"
 
+#ifndef EBL_PREFETCH
+#define EBL_PREFETCH 0    // bulk L2 prefetch of the region's static layers at launch
+#endif
+#ifndef EBL_PHASE_PROF
+#define EBL_PHASE_PROF 0  // per-phase clock64 profile (diagnostic builds: scripts/build_variant.sh)
+#endif
+#ifndef EBL_LAMBDA_ALL
+#define EBL_LAMBDA_ALL 1  // slope-table, branch-free 8-direction lambda (terrain form)
+#endif
+
 namespace ebl {
 
 
@@ -45,6 +55,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   __shared__ int32_t s_newly[2][E];
   __shared__ int32_t s_cnt[E][4];
   __shared__ uint64_t s_prefix[2][E];  // rng key prefix of step t in slot t & 1 (one thread computes it)
+  __shared__ float s_pal[MODE == kStaticTerrain ? 512 : 1];  // terrain palette: fp32 src, gam
 
   const int env0 = blockIdx.z * E;
   const int W = a.w, BH = a.h;
@@ -97,6 +108,23 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
       X[it.r * S + it.j] = x;
     }
   }
+  if constexpr (MODE == kStaticTerrain) {
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) s_pal[i] = __ldg(a.pal32 + i);
+#if EBL_PREFETCH
+    // the region's static layers are touched only along the fire front: one bulk L2 prefetch per
+    // region row (whole env = one contiguous range) hides their first-touch DRAM latency
+    const bool whole = RW == W;
+    const int n_pf = whole ? E : E * RH;
+    for (int i = threadIdx.x; i < n_pf; i += blockDim.x) {
+      const int sub = whole ? i : i / RH, rr = whole ? 0 : i % RH;
+      if (env0 + sub >= a.n_envs) continue;
+      const size_t base = static_cast<size_t>(env0 + sub) * a.ter_stride + static_cast<size_t>(R0 + rr) * W + C0;
+      const uint32_t cells = whole ? static_cast<uint32_t>(RH) * W : static_cast<uint32_t>(RW);
+      prefetch_l2(a.elev + base, (cells * 4u) & ~15u);
+      prefetch_l2(a.fuel + base, cells & ~15u);
+    }
+#endif
+  }
   if (threadIdx.x < 4 * E) s_cnt[threadIdx.x >> 2][threadIdx.x & 3] = 0;
   if (threadIdx.x < 2) s_total[threadIdx.x] = 0;
   if (threadIdx.x < 2 * E) s_newly[threadIdx.x / E][threadIdx.x % E] = 0;
@@ -135,8 +163,24 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
     }
   };
 
+#if EBL_PHASE_PROF
+  // phase profile: thread 0 times the barrier-to-barrier phases; each warp's lane 0 times its own
+  // dense pass, list build and P2 work; the slowest warp's times are accumulated
+  __shared__ long long s_pw[3][kResThreads * E / 32];
+  __shared__ int s_ncand;
+  long long pr_t0 = 0, pr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pw0 = 0, pw1 = 0;
+  if (threadIdx.x == 0) s_ncand = 0;
+#define EBL_PW_MARK(v) \
+  if (a.prof && lane == 0) v = clock64();
+#else
+#define EBL_PW_MARK(v)
+#endif
   for (int t = 0; t < g.n_steps; ++t) {
     const int par = t & 1;
+#if EBL_PHASE_PROF
+    if (a.prof && threadIdx.x == 0) pr_t0 = clock64();
+    EBL_PW_MARK(pw0)
+#endif
     if (threadIdx.x == 0) s_total[par ^ 1] = 0;  // the other parity's counters are free until the next step
     if (threadIdx.x < E) s_newly[par ^ 1][threadIdx.x] = 0;
     const int srow = sched_row(a, a.step + static_cast<uint64_t>(t));  // wind in force
@@ -181,6 +225,9 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
           dc = dnn;
         }
       }
+#if EBL_PHASE_PROF
+      if (a.prof && lane == 0) { pw1 = clock64(); s_pw[0][threadIdx.x >> 5] = pw1 - pw0; }
+#endif
       // one warp-aggregated list reservation per warp and step (skipped by quiet warps)
       if (__ballot_sync(0xffffffffu, cnt > 0)) {
         int incl = cnt;
@@ -211,7 +258,29 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
         }
       }
     }
+#if EBL_PHASE_PROF
+    if (a.prof) {
+      __syncwarp();
+      if (lane == 0) s_pw[1][threadIdx.x >> 5] = clock64() - pw1;
+    }
+#endif
     __syncthreads();
+#if EBL_PHASE_PROF
+    if (a.prof && threadIdx.x == 0) {
+      const long long t1 = clock64();
+      pr[0] += t1 - pr_t0;
+      pr_t0 = t1;
+      pr[2] += s_total[par];
+      long long m0 = 0, m1 = 0;
+      for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) {
+        m0 = max(m0, s_pw[0][q]);
+        m1 = max(m1, s_pw[1][q]);
+      }
+      pr[4] += m0;
+      pr[5] += m1;
+    }
+    EBL_PW_MARK(pw0)
+#endif
     // ---- P2: sparse decisions over the pooled list ------------------------------------------
     int newly[E];
 #pragma unroll
@@ -242,7 +311,17 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
           if (uc < 0 || uc >= RW) continue;  // padding rows cover ur = -1 and ur = RH
           nb |= ((B[(ur + 1) * S + (uc >> 5)] >> (uc & 31)) & 1u) << k;
         }
-        if (ignite<MODE>(a, env0 + sub, R0 + rr, C0 + cc, nb, m, dg, srow)) {
+#if EBL_PHASE_PROF
+        if (a.prof) atomicAdd(&s_ncand, 1);
+#endif
+        bool ig;
+        if constexpr (MODE == kStaticTerrain && EBL_LAMBDA_ALL)
+          ig = ignite_terrain_tab(terrain_view(a, env0 + sub, srow),
+                                  a.slope32 + static_cast<size_t>(env0 + sub) * a.ter_stride * 8, s_pal, W, BH,
+                                  R0 + rr, C0 + cc, nb, m, dg);
+        else
+          ig = ignite<MODE>(a, env0 + sub, R0 + rr, C0 + cc, nb, m, dg, srow);
+        if (ig) {
           atomicOr(Bn + wi, bit);
           const int in_tile = (rr >= tr0 && rr < tr1 && cc >= tc0 && cc < tc1);
 #pragma unroll
@@ -276,7 +355,21 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
         if (lane == 0 && v) atomicAdd(&s_newly[par][q], v);
       }
     }
+#if EBL_PHASE_PROF
+    if (a.prof) {
+      __syncwarp();
+      if (lane == 0) s_pw[2][threadIdx.x >> 5] = clock64() - pw0;
+    }
+#endif
     __syncthreads();
+#if EBL_PHASE_PROF
+    if (a.prof && threadIdx.x == 0) {
+      pr[1] += clock64() - pr_t0;
+      long long m2 = 0;
+      for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) m2 = max(m2, s_pw[2][q]);
+      pr[6] += m2;
+    }
+#endif
     cur ^= 1;
     if (a.traj) {  // record (run_stochastic(record=true), engine.cpp:116): this step's tile
       for (int sub = 0; sub < E; ++sub)
@@ -286,6 +379,13 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
     }
   }
 
+#if EBL_PHASE_PROF
+  if (a.prof && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+    pr[3] = g.n_steps;
+    pr[7] = s_ncand;
+    for (int q = 0; q < 8; ++q) a.prof[env0 * 8 + q] = pr[q];
+  }
+#endif
   // ---- store the tiles: bit-planes -> uint8, counts -----------------------------------------
   for (int sub = 0; sub < E; ++sub) {
     if (env0 + sub >= a.n_envs) break;
@@ -308,6 +408,8 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
     }
   }
 }
+
+bool phase_prof_built() { return EBL_PHASE_PROF != 0; }
 
 size_t blocked_smem_bytes(int region_h, int region_w, int list_cap, int envs_per_cta) {
   const size_t S = plane_stride((region_w + 31) / 32);

@@ -76,6 +76,8 @@ struct ebl_batch {
   bool counts_valid = false;
   DevBuf<int32_t> counts;
   DevBuf<unsigned long long> diag;
+  DevBuf<long long> prof;           // phase profile of the blocked kernel (ebl_batch_set_profiling)
+  bool profiling = false;
   uint64_t launches = 0, steps_done = 0;
 
   uint64_t seed = 0, step = 0;
@@ -96,6 +98,8 @@ struct ebl_batch {
   // terrain form
   DevBuf<uint8_t> fuel;
   DevBuf<float> elev;
+  DevBuf<float> slope32;            // [grid][cell][8] fp32 slopes of the layers (built by prepare)
+  bool slope_dirty = false;
   std::vector<double> pal_veg, pal_den;
   double cellsize = 30.0;
   int n_winds = 0;
@@ -211,6 +215,13 @@ int prepare(ebl_batch* b) {
     EBL_CUDA(cudaStreamSynchronize(b->stream));
     b->derived_dirty = false;
   }
+  if (b->mode == ebl::kStaticTerrain && b->slope_dirty) {  // slope_from_dem of the layers (GridState)
+    const double d0 = b->cellsize * 1.0, d1 = b->cellsize * 1.41421356237309504880;
+    EBL_CUDA(b->slope32.alloc(b->ncell * b->n_grids * 8));
+    EBL_CUDA(ebl::launch_slope_table(b->elev.p, b->n_grids, b->h, b->w, static_cast<float>(1.0 / d0),
+                                     static_cast<float>(1.0 / d1), b->slope32.p, b->stream));
+    b->slope_dirty = false;
+  }
   return EBL_OK;
 }
 
@@ -232,6 +243,7 @@ ebl::StepArgs step_args(const ebl_batch* b) {
   a.tab_stride = b->n_grids > 1 ? b->ncell : 0;
   a.fuel = b->fuel.p;
   a.elev = b->elev.p;
+  a.slope32 = b->mode == ebl::kStaticTerrain ? b->slope32.p : nullptr;
   a.ter_stride = b->n_grids > 1 ? b->ncell : 0;
   a.pal32 = b->pal32.p;
   a.pal64 = b->pal64.p;
@@ -250,6 +262,7 @@ ebl::StepArgs step_args(const ebl_batch* b) {
   a.inv_dist32[1] = static_cast<float>(1.0 / d1);
   // the fp32 guard band (1e-4 relative) holds while |alpha_s * slope| stays O(10)
   a.force64 = !(std::fabs(b->cfg.alpha_s) <= 50.0);
+  a.prof = b->profiling ? b->prof.p : nullptr;
   return a;
 }
 
@@ -261,6 +274,7 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
   a.out += o * b->ncell;
   a.streams += o;
   if (a.counts) a.counts += o * 4;
+  if (a.prof) a.prof += o * 8;
   if (a.tab_stride) {
     a.pot += o * a.tab_stride * 8;
     a.gamma += o * a.tab_stride;
@@ -268,6 +282,7 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
   if (a.ter_stride) {
     a.fuel += o * a.ter_stride;
     a.elev += o * a.ter_stride;
+    if (a.slope32) a.slope32 += o * a.ter_stride * 8;
   }
   if (a.kw_stride) {
     a.kw32 += o * a.kw_stride;
@@ -448,6 +463,7 @@ int ebl_batch_set_terrain(ebl_batch* b, int n_grids, const uint8_t* fuel_class, 
   b->mode = ebl::kStaticTerrain;
   b->n_grids = n_grids;
   b->derived_dirty = true;
+  b->slope_dirty = true;
   b->det_tables_valid = false;
   b->pot.reset();
   b->gamma.reset();
@@ -472,6 +488,7 @@ void adopt_device_terrain(ebl_batch* b, int n_grids, std::vector<double> veg, st
   b->mode = ebl::kStaticTerrain;
   b->n_grids = n_grids;
   b->derived_dirty = true;
+  b->slope_dirty = true;
   b->det_tables_valid = false;
   b->pot.reset();
   b->gamma.reset();
@@ -1034,6 +1051,28 @@ int ebl_batch_intensity(ebl_batch* b, float* lambda, float* p) {
   EBL_CUDA(ebl::launch_intensity(a, b->mode, dl.p, dp.p, b->stream));
   EBL_CUDA(cudaMemcpyAsync(lambda, dl.p, total * sizeof(float), cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaMemcpyAsync(p, dp.p, total * sizeof(float), cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_batch_set_profiling(ebl_batch* b, int on) {
+  if (int e = check_batch(b)) return e;
+  EBL_CUDA(cudaSetDevice(b->device));
+  if (on && !ebl::phase_prof_built())
+    return set_err(EBL_ESTATE, "library built without EBL_PHASE_PROF (scripts/build_variant.sh)");
+  if (on) {
+    EBL_CUDA(b->prof.alloc(static_cast<size_t>(b->n_envs) * 8));
+    EBL_CUDA(cudaMemsetAsync(b->prof.p, 0, static_cast<size_t>(b->n_envs) * 8 * sizeof(long long), b->stream));
+  }
+  b->profiling = on != 0;
+  return EBL_OK;
+}
+
+int ebl_batch_profile(ebl_batch* b, int64_t* out) {
+  if (int e = check_batch(b)) return e;
+  if (!b->profiling) return set_err(EBL_ESTATE, "profiling is off (ebl_batch_set_profiling)");
+  EBL_CUDA(cudaMemcpyAsync(out, b->prof.p, static_cast<size_t>(b->n_envs) * 8 * sizeof(long long),
+                           cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
   return EBL_OK;
 }

@@ -138,6 +138,37 @@ __device__ __forceinline__ float terrain_lambda32(const TerrainView& t, int w, i
   return lam;
 }
 
+// terrain_lambda32 over the fp32 slope table (launch_slope_table: slope_from_dem of the layers,
+// built once with them like the reference's SlopeField): the candidate's 8 slopes are one 32-byte
+// record, the 8 sources' fuel classes are loaded unconditionally (indices clamped into the h x w
+// layer) -- one memory round trip, no atan -- and the directions without a burning source are
+// selected away.  Same per-direction fp32 expression as terrain_lambda32.  pal_src: the palette's
+// fp32 source values (shared memory).
+__device__ __forceinline__ float terrain_lambda32_tab(const TerrainView& t, const float* __restrict__ slope32,
+                                                      const float* pal_src, int w, int h, int r, int c,
+                                                      uint32_t nb, uint8_t* fuel_v) {
+  const int rs = r > 0 ? r - 1 : 0, rn = r + 1 < h ? r + 1 : h - 1;
+  const int cw = c > 0 ? c - 1 : 0, ce = c + 1 < w ? c + 1 : w - 1;
+  // u_k = (r - dy_k, c - dx_k), k = E NE N NW W SW S SE (kDx/kDy)
+  const int ur[8] = {r, rs, rs, rs, r, rn, rn, rn};
+  const int uc[8] = {cw, cw, c, ce, ce, ce, c, cw};
+  const int v = r * w + c;
+  const float4 s0 = __ldg(reinterpret_cast<const float4*>(slope32) + 2 * v);
+  const float4 s1 = __ldg(reinterpret_cast<const float4*>(slope32) + 2 * v + 1);
+  const float s[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+  *fuel_v = __ldg(t.fuel + v);
+  uint8_t f[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) f[k] = __ldg(t.fuel + ur[k] * w + uc[k]);
+  float lam = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float contrib = pal_src[f[k]] * t.kw32[k] * __expf(t.alpha_s32 * s[k]);
+    lam += (nb >> k) & 1u ? contrib : 0.f;
+  }
+  return lam;
+}
+
 constexpr double kGuardRel = 1e-4;
 
 __device__ __forceinline__ bool ignite_terrain(const TerrainView& t, int w, int r, int c,
@@ -149,6 +180,30 @@ __device__ __forceinline__ bool ignite_terrain(const TerrainView& t, int w, int 
     if (x == 0.f) return false;  // gamma or lambda exactly 0: p = 1 - exp(-0) = 0, u < 0 is false
     const double p32 = static_cast<double>(-expm1f(-x));
     // tiny p: the reference's 1 - exp(-x) is quantised to multiples of 2^-53 there; decide in fp64
+    if (p32 > 1e-12) {
+      if (u < p32 * (1.0 - kGuardRel)) return true;
+      if (u >= p32 * (1.0 + kGuardRel)) return false;
+    }
+  }
+  dg.fallback();
+  const double p = terrain_p64(t, w, r, c, nb);
+  if (fabs(u - p) < kAmbiguousBand) dg.ambiguous();
+  return u < p;
+}
+
+// ignite_terrain with the slope-table fp32 lambda (blocked kernel); pal32s = [src 256][gam 256] in
+// shared memory.  Same decisions as ignite_terrain (same fp32 values to rounding, same guard band,
+// same fp64 path).
+__device__ __forceinline__ bool ignite_terrain_tab(const TerrainView& t, const float* slope32, const float* pal32s,
+                                                   int w, int h, int r, int c, uint32_t nb, uint64_t m,
+                                                   const DiagCounters& dg) {
+  const double u = bits_to_uniform(m);
+  if (!t.force64) {
+    uint8_t fv;
+    const float lam = terrain_lambda32_tab(t, slope32, pal32s, w, h, r, c, nb, &fv);
+    const float x = pal32s[256 + fv] * lam;
+    if (x == 0.f) return false;  // gamma or lambda exactly 0: p = 1 - exp(-0) = 0, u < 0 is false
+    const double p32 = static_cast<double>(-expm1f(-x));
     if (p32 > 1e-12) {
       if (u < p32 * (1.0 - kGuardRel)) return true;
       if (u >= p32 * (1.0 + kGuardRel)) return false;

@@ -21,6 +21,7 @@ constexpr int kBlockHalo = 8;
 // 1.07 ms unpaired -- the heavy envs' step latency is not P2-throughput bound.  EBL_KERNEL_PAIRED
 // keeps the pooled form selectable.
 constexpr int kPairMinEnvs = 1 << 30;
+bool phase_prof_built();
 size_t blocked_smem_bytes(int region_h, int region_w, int list_cap, int envs_per_cta);
 bool resident_fits(int h, int w);
 BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_off, int n_envs,
@@ -86,5 +87,8 @@ struct LandcoverArgs {
   unsigned long long* missing;  // first cell with an unmapped code (init ~0)
 };
 cudaError_t launch_landcover_map(const LandcoverArgs& a, cudaStream_t s);
+// fp32 slope table [grid][cell][8] (terrain form, built with the layers; ember_synth.cu)
+cudaError_t launch_slope_table(const float* elev, size_t n_grids, int h, int w, float inv_d0, float inv_d1,
+                               float* out, cudaStream_t s);
 
 }  // namespace ebl

@@ -29,6 +29,7 @@ struct StepArgs {
   // terrain form
   const uint8_t* fuel;            // [grid][h*w]
   const float* elev;              // [grid][h*w]
+  const float* slope32;           // [grid][h*w][8] fp32 slope table (terrain form) or null
   size_t ter_stride;
   const float* pal32;             // [2][256] src32, gam32
   const double* pal64;            // [2][256] src64, gam64
@@ -45,6 +46,7 @@ struct StepArgs {
   float inv_dist32[2];
   double dist64[2];
   int force64;
+  long long* prof;                // [n_envs][4] phase profile (P1 cycles, P2 cycles, active, -), or null
 };
 
 // Tiling of the blocked kernel (ember_blocked.cu): tiles of tile_h x tile_w cells with

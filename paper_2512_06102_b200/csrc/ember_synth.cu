@@ -243,6 +243,36 @@ __global__ void __launch_bounds__(kSynthThreads) k_landcover_map(LandcoverArgs a
   a.fuel[i] = static_cast<uint8_t>(k);
 }
 
+// slope_from_dem (geodata.cpp:209-229) in the fp32 fast-path form: S[cell][k] = atan((z(v) - z(u_k)) /
+// dist_k) for target v and source u_k = v - d_k, the same fp32 expression terrain_lambda32 evaluates
+// on the fly (so the tabulated and the on-the-fly lambda are bit-identical).  Sources outside the
+// layer and DEM nodata (NaN) on either end give 0.
+__global__ void __launch_bounds__(kSynthThreads) k_slope_table(const float* __restrict__ elev, size_t n_cells,
+                                                                int h, int w, float inv_d0, float inv_d1,
+                                                                float4* __restrict__ out) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n_cells) return;
+  const size_t layer = static_cast<size_t>(h) * w;
+  const size_t g = i / layer;
+  const int v = static_cast<int>(i - g * layer);
+  const int r = v / w, c = v - r * w;
+  const float* z = elev + g * layer;
+  const float zv = z[v];
+  float s[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int ur = r - kDy[k], uc = c - kDx[k];
+    float sk = 0.f;
+    if (ur >= 0 && ur < h && uc >= 0 && uc < w) {
+      const float dz = zv - z[ur * w + uc];
+      sk = dz == dz ? atanf(dz * (k & 1 ? inv_d1 : inv_d0)) : 0.f;
+    }
+    s[k] = sk;
+  }
+  out[2 * i] = make_float4(s[0], s[1], s[2], s[3]);
+  out[2 * i + 1] = make_float4(s[4], s[5], s[6], s[7]);
+}
+
 inline unsigned grid_x(size_t n) { return static_cast<unsigned>((n + kSynthThreads - 1) / kSynthThreads); }
 
 }  // namespace
@@ -264,6 +294,13 @@ cudaError_t launch_synth_ignitions(const IgniteArgs& a, cudaStream_t s) {
   cudaError_t e = cudaMemsetAsync(a.states, 0, static_cast<size_t>(a.n_envs) * a.h * a.w, s);
   if (e != cudaSuccess) return e;
   k_synth_ignitions<<<(a.n_envs + 63) / 64, 64, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slope_table(const float* elev, size_t n_grids, int h, int w, float inv_d0, float inv_d1,
+                               float* out, cudaStream_t s) {
+  const size_t n = n_grids * h * w;
+  k_slope_table<<<grid_x(n), kSynthThreads, 0, s>>>(elev, n, h, w, inv_d0, inv_d1, reinterpret_cast<float4*>(out));
   return cudaGetLastError();
 }
 
