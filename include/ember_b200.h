@@ -206,9 +206,10 @@ int ebl_batch_intensity(ebl_batch* b, float* lambda, float* p);
 int ebl_batch_diag(ebl_batch* b, uint64_t* out4, int reset);
 /* Phase profile of the resident blocked kernel (diagnostic builds with -DEBL_PHASE_PROF=1 only;
  * otherwise set_profiling(on) fails with EBL_ESTATE): each launch stores per env int64
- * [n_envs][8] = {P1 cycles (to the first barrier), P2 cycles (to the second), active cells,
+ * [n_envs][10] = {P1 cycles (to the first barrier), P2 cycles (to the second), active cells,
  * steps, slowest warp's dense-pass cycles, slowest warp's list-build cycles, slowest warp's P2
- * work cycles, candidate decisions}, summed over the launch's steps (clock64, the env's CTA). */
+ * work cycles, candidate decisions, list build: count done, reservation done}, summed over the
+ * launch's steps (clock64, the env's CTA). */
 int ebl_batch_set_profiling(ebl_batch* b, int on);
 int ebl_batch_profile(ebl_batch* b, int64_t* out);
 /* rng_word (rng.hpp:38-46) evaluated ON THE DEVICE for n keys

@@ -51,6 +51,10 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(n) : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 // Row stride (words) of a bit-plane with wpr words per row: odd, so the 32 lanes of a warp
 // each reading "its" row at the same column hit 32 distinct shared-memory banks.
 __host__ __device__ __forceinline__ int plane_stride(int wpr) { return wpr | 1; }

@@ -35,6 +35,9 @@
 #ifndef EBL_PREFETCH
 #define EBL_PREFETCH 0    // bulk L2 prefetch of the region's static layers at launch
 #endif
+#ifndef EBL_PREFETCH_FRONT
+#define EBL_PREFETCH_FRONT 0  // prefetch next step's candidate statics at each ignition
+#endif
 #ifndef EBL_PHASE_PROF
 #define EBL_PHASE_PROF 0  // per-phase clock64 profile (diagnostic builds: scripts/build_variant.sh)
 #endif
@@ -48,14 +51,18 @@ namespace ebl {
 // E envs per CTA (E = 1, or 2 for whole-env residency of envs <= 32768 cells): 128 threads per
 // env in P1, one pooled active list in P2, so a heavy env shares its CTA's 128*E threads with a
 // lighter one (the batch's kernel time is set by its slowest CTA: measured, scripts/imbalance.py).
-template <int MODE, int E>
+// WPRC: words per region row when known at compile time (2: 64-wide, 4: 128-wide envs), else 0.
+template <int MODE, int E, int WPRC>
 __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArgs a, BlockGeom g) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_total[2];
   __shared__ int32_t s_newly[2][E];
   __shared__ int32_t s_cnt[E][4];
-  __shared__ uint64_t s_prefix[2][E];  // rng key prefix of step t in slot t & 1 (one thread computes it)
+  // rng key prefixes (3 of rng_word's 5 rounds) of steps t .. t+63 in a ring, slot t & 127: 64 are
+  // computed in parallel every 64 steps instead of one per step on the critical path
+  __shared__ uint64_t s_prefix[E][128];
   __shared__ float s_pal[MODE == kStaticTerrain ? 512 : 1];  // terrain palette: fp32 src, gam
+  __shared__ float s_kw[MODE == kStaticTerrain ? E : 1][8];    // kappa_wind of the wind in force
 
   const int env0 = blockIdx.z * E;
   const int W = a.w, BH = a.h;
@@ -63,7 +70,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   const int R0 = max(0, r0 - g.halo_rows), R1 = min(BH, r0 + g.tile_h + g.halo_rows);
   const int C0 = max(0, c0 - g.halo_cols), C1 = min(W, c0 + g.tile_w + g.halo_cols);
   const int RH = R1 - R0, RW = C1 - C0;
-  const int wpr = (RW + 31) >> 5;
+  const int wpr = WPRC ? WPRC : (RW + 31) >> 5;
   const int S = plane_stride(wpr);  // odd row stride: a warp's 32 rows hit 32 distinct banks
   const int PB = (2 * (RH + 2) + 2 * RH) * S;  // words of one env's planes: B[2], X, ACT
   uint32_t* const planes = reinterpret_cast<uint32_t*>(smem);
@@ -74,6 +81,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   uint16_t* list = reinterpret_cast<uint16_t*>(planes + E * PB);
   const int cap = g.list_cap;
   const uint32_t last_mask = low_mask(RW - 32 * (wpr - 1));
+  const int rot = wpr >= 32 ? 1 : 32 / wpr;  // list-build word rotation (see P1)
 
   const size_t ncell = static_cast<size_t>(BH) * W;
   const bool vec = (W & 15) == 0;  // 16-byte aligned rows (C0 is a multiple of 32)
@@ -128,8 +136,10 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   if (threadIdx.x < 4 * E) s_cnt[threadIdx.x >> 2][threadIdx.x & 3] = 0;
   if (threadIdx.x < 2) s_total[threadIdx.x] = 0;
   if (threadIdx.x < 2 * E) s_newly[threadIdx.x / E][threadIdx.x % E] = 0;
-  if (threadIdx.x < E)
-    s_prefix[0][threadIdx.x] = key_prefix(a.seed, a.streams[min(env0 + static_cast<int>(threadIdx.x), a.n_envs - 1)], a.step);
+  for (int i = threadIdx.x; i < 64 * E; i += blockDim.x) {
+    const int q = i >> 6, k = i & 63;
+    s_prefix[q][k] = key_prefix(a.seed, a.streams[min(env0 + q, a.n_envs - 1)], a.step + static_cast<uint64_t>(k));
+  }
   __syncthreads();
 
   const DiagCounters dg{a.diag};
@@ -166,10 +176,11 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
 #if EBL_PHASE_PROF
   // phase profile: thread 0 times the barrier-to-barrier phases; each warp's lane 0 times its own
   // dense pass, list build and P2 work; the slowest warp's times are accumulated
-  __shared__ long long s_pw[3][kResThreads * E / 32];
+  __shared__ long long s_pw[5][kResThreads * E / 32];
   __shared__ int s_ncand;
-  long long pr_t0 = 0, pr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pw0 = 0, pw1 = 0;
+  long long pr_t0 = 0, pr[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, pw0 = 0, pw1 = 0;
   if (threadIdx.x == 0) s_ncand = 0;
+  if (threadIdx.x < 5 * (kResThreads * E / 32)) (&s_pw[0][0])[threadIdx.x] = 0;
 #define EBL_PW_MARK(v) \
   if (a.prof && lane == 0) v = clock64();
 #else
@@ -184,6 +195,14 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
     if (threadIdx.x == 0) s_total[par ^ 1] = 0;  // the other parity's counters are free until the next step
     if (threadIdx.x < E) s_newly[par ^ 1][threadIdx.x] = 0;
     const int srow = sched_row(a, a.step + static_cast<uint64_t>(t));  // wind in force
+    if constexpr (MODE == kStaticTerrain) {  // read by P2, after the first barrier
+      if ((t == 0 || a.sched_len > 1) && threadIdx.x < 8 * E) {
+        const int q = threadIdx.x >> 3;
+        s_kw[q][threadIdx.x & 7] = __ldg(a.kw32 + static_cast<size_t>(srow) * a.kw_sched_stride +
+                                         static_cast<size_t>(min(env0 + q, a.n_envs - 1)) * a.kw_stride +
+                                         (threadIdx.x & 7));
+      }
+    }
     // ---- P1: each thread owns whole rows of one env; the 3x3 dilation slides along the row in
     //      registers (3 shared loads per word: north, own, south) ------------------------------
     int cnt = 0;
@@ -193,6 +212,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
       uint32_t* Bn = Bplane(my_sub, cur ^ 1);
       const uint32_t* X = Xplane(my_sub);
       uint32_t* ACT = Aplane(my_sub);
+      uint32_t* const ACT_P1 = ACT;
       for (int r = lt; r < RH; r += kResThreads) {
         const uint32_t* up = B + (r + 2) * S;
         const uint32_t* mid = B + (r + 1) * S;
@@ -203,6 +223,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
         uint32_t vl = 0u;                            // column j-1: north | own | south
         uint32_t uc = up[0], mc = mid[0], dc = dn[0];
         uint32_t vc = uc | mc | dc;
+#pragma unroll 4
         for (int j = 0; j < wpr; ++j) {
           uint32_t un = 0u, mn = 0u, dnn = 0u;
           if (j + 1 < wpr) {
@@ -228,9 +249,22 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
 #if EBL_PHASE_PROF
       if (a.prof && lane == 0) { pw1 = clock64(); s_pw[0][threadIdx.x >> 5] = pw1 - pw0; }
 #endif
-      // one warp-aggregated list reservation per warp and step (skipped by quiet warps)
+      // List build, one warp-aggregated reservation per warp and step (skipped by quiet warps).
+      // The warp's ACT words are re-dealt to its lanes so that a row with a long front is spread
+      // over several lanes: in 128-row block rb, lane l extracts word j of row rb + ((l + rot*j) & 31)
+      // (a rotation per word column: every (row, word) exactly once).  ovf words stay with that lane.
       if (__ballot_sync(0xffffffffu, cnt > 0)) {
-        int incl = cnt;
+        __syncwarp();  // the warp's ACT rows (its own dense-pass output) are visible to all lanes
+        int c2 = 0;
+        for (int rb = lt & ~31; rb < RH; rb += kResThreads)
+          for (int j = 0; j < wpr; ++j) {
+            const int r = rb + ((lane + rot * j) & 31);
+            if (r < RH) c2 += __popc(ACT_P1[r * S + j]);
+          }
+#if EBL_PHASE_PROF
+        if (a.prof && lane == 0) s_pw[3][threadIdx.x >> 5] = clock64() - pw1;
+#endif
+        int incl = c2;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -238,12 +272,17 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
         }
         int base = 0;
         if (lane == 31) base = atomicAdd(&s_total[par], incl);
-        base = __shfl_sync(0xffffffffu, base, 31) + incl - cnt;
-        if (cnt > 0) {
+        base = __shfl_sync(0xffffffffu, base, 31) + incl - c2;
+#if EBL_PHASE_PROF
+        if (a.prof && lane == 0) s_pw[4][threadIdx.x >> 5] = clock64() - pw1;
+#endif
+        if (c2 > 0) {
           const int tag = E > 1 ? (my_sub << 15) : 0;
-          for (int r = lt; r < RH; r += kResThreads) {
+          for (int rb = lt & ~31; rb < RH; rb += kResThreads)
             for (int j = 0; j < wpr; ++j) {
-              uint32_t rest = ACT[r * S + j];
+              const int r = rb + ((lane + rot * j) & 31);
+              if (r >= RH) continue;
+              uint32_t rest = ACT_P1[r * S + j];
               if (!rest) continue;
               const int cell0 = r * RW + 32 * j;
               while (rest && base < cap) {
@@ -251,10 +290,9 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
                 rest &= rest - 1;
                 list[base++] = static_cast<uint16_t>((cell0 + bit) | tag);
               }
-              ACT[r * S + j] = rest;  // overflow beyond the list capacity: done by this thread in P2
+              ACT_P1[r * S + j] = rest;  // overflow beyond the list capacity: done by this lane in P2
               ovf |= rest != 0u;
             }
-          }
         }
       }
     }
@@ -271,13 +309,18 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
       pr[0] += t1 - pr_t0;
       pr_t0 = t1;
       pr[2] += s_total[par];
-      long long m0 = 0, m1 = 0;
+      long long m0 = 0, m1 = 0, m3 = 0, m4 = 0;
       for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) {
         m0 = max(m0, s_pw[0][q]);
         m1 = max(m1, s_pw[1][q]);
+        m3 = max(m3, s_pw[3][q]);
+        m4 = max(m4, s_pw[4][q]);
+        s_pw[3][q] = s_pw[4][q] = 0;
       }
       pr[4] += m0;
       pr[5] += m1;
+      pr[8] += m3;
+      pr[9] += m4;
     }
     EBL_PW_MARK(pw0)
 #endif
@@ -286,10 +329,12 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
 #pragma unroll
     for (int q = 0; q < E; ++q) newly[q] = 0;
     const int total = min(s_total[par], cap);
-    if (threadIdx.x >= blockDim.x - E) {  // next step's prefixes, published by the end-of-step barrier
-      const int q = static_cast<int>(threadIdx.x) - static_cast<int>(blockDim.x - E);
-      s_prefix[par ^ 1][q] = key_prefix(a.seed, a.streams[min(env0 + q, a.n_envs - 1)],
-                                        a.step + static_cast<uint64_t>(t + 1));
+    if ((t & 63) == 63 && t + 1 < g.n_steps) {  // refill the ring with steps t+1 .. t+64
+      for (int i = threadIdx.x; i < 64 * E; i += blockDim.x) {
+        const int q = i >> 6, k = i & 63;
+        s_prefix[q][(t + 1 + k) & 127] = key_prefix(a.seed, a.streams[min(env0 + q, a.n_envs - 1)],
+                                                   a.step + static_cast<uint64_t>(t + 1 + k));
+      }
     }
     auto decide = [&](int sub, int lc) {
       const uint32_t* B = Bplane(sub, cur);
@@ -297,32 +342,63 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
       const int rr = lc / RW, cc = lc - rr * RW;
       const int wi = (rr + 1) * S + (cc >> 5);
       const uint32_t bit = 1u << (cc & 31);
-      const uint64_t m = cell_bits53(s_prefix[par][sub], gbase + static_cast<uint64_t>(rr) * W + cc, 0);
-      if (B[wi] & bit) {
+      const uint64_t m = cell_bits53(s_prefix[sub][t & 127], gbase + static_cast<uint64_t>(rr) * W + cc, 0);
+      // 3-cell windows (columns cc-1, cc, cc+1 -> bits 0..2) of the rows below, at and above the
+      // cell; padding rows cover rr-1 = -1 and rr+1 = RH, bits past RW are never set
+      const int j = cc >> 5, b = cc & 31;
+      auto win3 = [&](const uint32_t* row) -> uint32_t {
+        const uint32_t wj = row[j];
+        uint32_t v = b > 0 ? wj >> (b - 1) : ((j > 0 ? row[j - 1] >> 31 : 0u) | (wj << 1));
+        if (b == 31) v = (v & 3u) | ((j + 1 < wpr ? row[j + 1] & 1u : 0u) << 2);
+        return v & 7u;
+      };
+      const uint32_t mid = win3(B + (rr + 1) * S);
+      if (mid & 2u) {
         if (m >= a.pc_thr) {
           atomicAnd(Bn + wi, ~bit);
           atomicOr(Xplane(sub) + rr * S + (cc >> 5), bit);
         }
       } else {
-        uint32_t nb = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int ur = rr - kDy[k], uc = cc - kDx[k];
-          if (uc < 0 || uc >= RW) continue;  // padding rows cover ur = -1 and ur = RH
-          nb |= ((B[(ur + 1) * S + (uc >> 5)] >> (uc & 31)) & 1u) << k;
-        }
+        // burning-source mask in kNeighborOffsets order (u_k = v - d_k): E <- (r, c-1),
+        // NE <- (r-1, c-1), N <- (r-1, c), NW <- (r-1, c+1), W <- (r, c+1), SW <- (r+1, c+1),
+        // S <- (r+1, c), SE <- (r+1, c-1)
+        const uint32_t dnw = win3(B + rr * S), upw = win3(B + (rr + 2) * S);
+        const uint32_t nb = (mid & 1u) | (dnw << 1) | ((mid >> 2) << 4) | ((upw >> 2) << 5) |
+                            ((upw & 2u) << 5) | ((upw & 1u) << 7);
 #if EBL_PHASE_PROF
         if (a.prof) atomicAdd(&s_ncand, 1);
 #endif
         bool ig;
         if constexpr (MODE == kStaticTerrain && EBL_LAMBDA_ALL)
           ig = ignite_terrain_tab(terrain_view(a, env0 + sub, srow),
-                                  a.slope32 + static_cast<size_t>(env0 + sub) * a.ter_stride * 8, s_pal, W, BH,
-                                  R0 + rr, C0 + cc, nb, m, dg);
+                                  a.slope32 + static_cast<size_t>(env0 + sub) * a.ter_stride * 8, s_pal, s_kw[sub],
+                                  W, BH, R0 + rr, C0 + cc, nb, m, dg);
         else
           ig = ignite<MODE>(a, env0 + sub, R0 + rr, C0 + cc, nb, m, dg, srow);
         if (ig) {
           atomicOr(Bn + wi, bit);
+#if EBL_PREFETCH_FRONT
+          if constexpr (MODE == kStaticTerrain) {
+            // the ignited cell's unburned neighbours are next step's candidates: pull their slope
+            // records (rows r-1..r+1, 3 records each) and the fuel of their sources (rows r-2..r+2)
+            // toward the SM while this step finishes
+            const int gr = R0 + rr, gc = C0 + cc;
+            const size_t eb = static_cast<size_t>(env0 + sub) * a.ter_stride;
+            const int c0 = max(gc - 1, 0), c1 = min(gc + 1, W - 1);
+#pragma unroll
+            for (int d = -1; d <= 1; ++d) {
+              const int rowp = min(max(gr + d, 0), BH - 1);
+              const float* sp = a.slope32 + (eb + static_cast<size_t>(rowp) * W) * 8;
+              prefetch_l1(sp + c0 * 8);
+              prefetch_l1(sp + c1 * 8 + 7);
+            }
+#pragma unroll
+            for (int d = -2; d <= 2; ++d) {
+              const int rowp = min(max(gr + d, 0), BH - 1);
+              prefetch_l1(a.fuel + eb + static_cast<size_t>(rowp) * W + max(gc - 2, 0));
+            }
+          }
+#endif
           const int in_tile = (rr >= tr0 && rr < tr1 && cc >= tc0 && cc < tc1);
 #pragma unroll
           for (int q = 0; q < E; ++q) newly[q] += (q == sub) ? in_tile : 0;
@@ -336,8 +412,10 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
     }
     if (ovf) {
       uint32_t* ACT = Aplane(my_sub);
-      for (int r = lt; r < RH; r += kResThreads)
+      for (int rb = lt & ~31; rb < RH; rb += kResThreads)
         for (int j = 0; j < wpr; ++j) {
+          const int r = rb + ((lane + rot * j) & 31);
+          if (r >= RH) continue;
           uint32_t rest = ACT[r * S + j];
           while (rest) {
             const int bit = __ffs(rest) - 1;
@@ -383,7 +461,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   if (a.prof && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
     pr[3] = g.n_steps;
     pr[7] = s_ncand;
-    for (int q = 0; q < 8; ++q) a.prof[env0 * 8 + q] = pr[q];
+    for (int q = 0; q < 10; ++q) a.prof[env0 * 10 + q] = pr[q];
   }
 #endif
   // ---- store the tiles: bit-planes -> uint8, counts -----------------------------------------
@@ -463,14 +541,23 @@ BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_o
   return g;
 }
 
-template <int MODE, int E>
-static cudaError_t launch_blocked_t(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(k_step_blocked<MODE, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <int MODE, int E, int WPRC>
+static cudaError_t launch_blocked_w(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k_step_blocked<MODE, E, WPRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
   const dim3 grid((a.w + g.tile_w - 1) / g.tile_w, (a.h + g.tile_h - 1) / g.tile_h, (a.n_envs + E - 1) / E);
-  k_step_blocked<MODE, E><<<grid, kResThreads * E, sm, s>>>(a, g);
+  k_step_blocked<MODE, E, WPRC><<<grid, kResThreads * E, sm, s>>>(a, g);
   return cudaGetLastError();
+}
+
+template <int MODE, int E>
+static cudaError_t launch_blocked_t(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStream_t s) {
+  const int rw = g.tile_w + 2 * g.halo_cols;
+  const int wpr = ((rw < a.w ? rw : a.w) + 31) / 32;
+  if (wpr == 4) return launch_blocked_w<MODE, E, 4>(a, g, sm, s);
+  if (wpr == 2) return launch_blocked_w<MODE, E, 2>(a, g, sm, s);
+  return launch_blocked_w<MODE, E, 0>(a, g, sm, s);
 }
 
 cudaError_t launch_step_blocked(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s) {

@@ -274,7 +274,7 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
   a.out += o * b->ncell;
   a.streams += o;
   if (a.counts) a.counts += o * 4;
-  if (a.prof) a.prof += o * 8;
+  if (a.prof) a.prof += o * 10;
   if (a.tab_stride) {
     a.pot += o * a.tab_stride * 8;
     a.gamma += o * a.tab_stride;
@@ -1061,8 +1061,8 @@ int ebl_batch_set_profiling(ebl_batch* b, int on) {
   if (on && !ebl::phase_prof_built())
     return set_err(EBL_ESTATE, "library built without EBL_PHASE_PROF (scripts/build_variant.sh)");
   if (on) {
-    EBL_CUDA(b->prof.alloc(static_cast<size_t>(b->n_envs) * 8));
-    EBL_CUDA(cudaMemsetAsync(b->prof.p, 0, static_cast<size_t>(b->n_envs) * 8 * sizeof(long long), b->stream));
+    EBL_CUDA(b->prof.alloc(static_cast<size_t>(b->n_envs) * 10));
+    EBL_CUDA(cudaMemsetAsync(b->prof.p, 0, static_cast<size_t>(b->n_envs) * 10 * sizeof(long long), b->stream));
   }
   b->profiling = on != 0;
   return EBL_OK;
@@ -1071,7 +1071,7 @@ int ebl_batch_set_profiling(ebl_batch* b, int on) {
 int ebl_batch_profile(ebl_batch* b, int64_t* out) {
   if (int e = check_batch(b)) return e;
   if (!b->profiling) return set_err(EBL_ESTATE, "profiling is off (ebl_batch_set_profiling)");
-  EBL_CUDA(cudaMemcpyAsync(out, b->prof.p, static_cast<size_t>(b->n_envs) * 8 * sizeof(long long),
+  EBL_CUDA(cudaMemcpyAsync(out, b->prof.p, static_cast<size_t>(b->n_envs) * 10 * sizeof(long long),
                            cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
   return EBL_OK;

@@ -145,8 +145,8 @@ __device__ __forceinline__ float terrain_lambda32(const TerrainView& t, int w, i
 // selected away.  Same per-direction fp32 expression as terrain_lambda32.  pal_src: the palette's
 // fp32 source values (shared memory).
 __device__ __forceinline__ float terrain_lambda32_tab(const TerrainView& t, const float* __restrict__ slope32,
-                                                      const float* pal_src, int w, int h, int r, int c,
-                                                      uint32_t nb, uint8_t* fuel_v) {
+                                                      const float* pal_src, const float* kw, int w, int h,
+                                                      int r, int c, uint32_t nb, uint8_t* fuel_v) {
   const int rs = r > 0 ? r - 1 : 0, rn = r + 1 < h ? r + 1 : h - 1;
   const int cw = c > 0 ? c - 1 : 0, ce = c + 1 < w ? c + 1 : w - 1;
   // u_k = (r - dy_k, c - dx_k), k = E NE N NW W SW S SE (kDx/kDy)
@@ -163,7 +163,7 @@ __device__ __forceinline__ float terrain_lambda32_tab(const TerrainView& t, cons
   float lam = 0.f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const float contrib = pal_src[f[k]] * t.kw32[k] * __expf(t.alpha_s32 * s[k]);
+    const float contrib = pal_src[f[k]] * kw[k] * __expf(t.alpha_s32 * s[k]);
     lam += (nb >> k) & 1u ? contrib : 0.f;
   }
   return lam;
@@ -195,12 +195,12 @@ __device__ __forceinline__ bool ignite_terrain(const TerrainView& t, int w, int 
 // shared memory.  Same decisions as ignite_terrain (same fp32 values to rounding, same guard band,
 // same fp64 path).
 __device__ __forceinline__ bool ignite_terrain_tab(const TerrainView& t, const float* slope32, const float* pal32s,
-                                                   int w, int h, int r, int c, uint32_t nb, uint64_t m,
-                                                   const DiagCounters& dg) {
+                                                   const float* kw, int w, int h, int r, int c, uint32_t nb,
+                                                   uint64_t m, const DiagCounters& dg) {
   const double u = bits_to_uniform(m);
   if (!t.force64) {
     uint8_t fv;
-    const float lam = terrain_lambda32_tab(t, slope32, pal32s, w, h, r, c, nb, &fv);
+    const float lam = terrain_lambda32_tab(t, slope32, pal32s, kw, w, h, r, c, nb, &fv);
     const float x = pal32s[256 + fv] * lam;
     if (x == 0.f) return false;  // gamma or lambda exactly 0: p = 1 - exp(-0) = 0, u < 0 is false
     const double p32 = static_cast<double>(-expm1f(-x));

@@ -23,7 +23,7 @@ def prof(idx):
         b.set_state(init[idx])
         b.set_key(0, 0, streams=np.asarray(idx, dtype=np.uint64))
         b.step(STEPS)
-    pr = np.zeros((n, 8), np.int64)
+    pr = np.zeros((n, 10), np.int64)
     eb._lib.check(eb.lib().ebl_batch_profile(b.handle, pr.ctypes.data))
     fin = b.get_state()
     b.close()
@@ -39,4 +39,4 @@ for name, e in (("heaviest", order[-1]), ("p90", order[int(0.9 * N)]), ("median"
     for k in (148, 1184):
         p, _ = prof(np.full(k, e))
         print(f"{name:8s} x{k:4d}: P1 {p[0]:6.0f} (dense {p[4]:5.0f} build {p[5]:5.0f})  P2 {p[1]:6.0f} "
-              f"(work {p[6]:5.0f})  active {p[2]:6.1f} cand {p[7] / 1:6.0f}/launch")
+              f"(work {p[6]:5.0f})  active {p[2]:6.1f} cand {p[7]:5.0f}  [build: count {p[8]:5.0f} reserve {p[9]:5.0f}]")

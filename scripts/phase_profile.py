@@ -34,7 +34,7 @@ for prof in (0, 1):
         e1.synchronize()
         ms.append(e0.elapsed_time(e1))
     print(f"profiling={prof}: kernel {np.median(ms[1:]):.3f} ms (median of 4)")
-pr = np.zeros((N, 8), np.int64)
+pr = np.zeros((N, 10), np.int64)
 eb._lib.check(eb.lib().ebl_batch_profile(b.handle, pr.ctypes.data))
 p1, p2, act = pr[:, 0] / STEPS, pr[:, 1] / STEPS, pr[:, 2] / STEPS
 dense, build, work, cand = pr[:, 4] / STEPS, pr[:, 5] / STEPS, pr[:, 6] / STEPS, pr[:, 7] / STEPS
