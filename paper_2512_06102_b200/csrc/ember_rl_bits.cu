@@ -24,6 +24,8 @@ __global__ void __launch_bounds__(kRlBitsThreads) k_rl_tanker_bits(RlArgs g) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_total[2], s_newly[2], s_burn[2];
   __shared__ int s_action, s_placed;
+  __shared__ float s_pal[MODE == kStaticTerrain ? 512 : 1];  // terrain palette: fp32 src, gam
+  __shared__ float s_kw[8];                                   // kappa_wind of this env
 
   const StepArgs& a = g.s;
   const int env = blockIdx.x;
@@ -49,6 +51,10 @@ __global__ void __launch_bounds__(kRlBitsThreads) k_rl_tanker_bits(RlArgs g) {
     Bp[0][(H + 1) * wpr + i] = Bp[1][(H + 1) * wpr + i] = 0u;
   }
   if (threadIdx.x < 2) s_total[threadIdx.x] = s_newly[threadIdx.x] = s_burn[threadIdx.x] = 0;
+  if constexpr (MODE == kStaticTerrain) {
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) s_pal[i] = __ldg(a.pal32 + i);
+    if (threadIdx.x < 8) s_kw[threadIdx.x] = __ldg(a.kw32 + static_cast<size_t>(env) * a.kw_stride + threadIdx.x);
+  }
   for (WordIter it(wpr, nwords); it.ok(); it.next()) {
     const uint8_t* src = st + it.r * W + 32 * it.j;
     const uint8_t* wsrc = wt + it.r * W + 32 * it.j;
@@ -158,14 +164,24 @@ __global__ void __launch_bounds__(kRlBitsThreads) k_rl_tanker_bits(RlArgs g) {
           atomicOr(X + r * wpr + (c >> 5), bit);
         }
       } else {
-        uint32_t nb = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int ur = r - kDy[k], uc = c - kDx[k];
-          if (uc < 0 || uc >= W) continue;
-          nb |= ((B[(ur + 1) * wpr + (uc >> 5)] >> (uc & 31)) & 1u) << k;
-        }
-        if (ignite<MODE>(a, env, r, c, nb, m, dg)) {
+        // burning-source mask from 3-cell windows of the rows below / at / above (ember_blocked.cu)
+        const int j = c >> 5, b = c & 31;
+        auto win3 = [&](const uint32_t* row) -> uint32_t {
+          const uint32_t wj = row[j];
+          uint32_t v = b > 0 ? wj >> (b - 1) : ((j > 0 ? row[j - 1] >> 31 : 0u) | (wj << 1));
+          if (b == 31) v = (v & 3u) | ((j + 1 < wpr ? row[j + 1] & 1u : 0u) << 2);
+          return v & 7u;
+        };
+        const uint32_t mid = win3(B + (r + 1) * wpr), dnw = win3(B + r * wpr), upw = win3(B + (r + 2) * wpr);
+        const uint32_t nb = (mid & 1u) | (dnw << 1) | ((mid >> 2) << 4) | ((upw >> 2) << 5) |
+                            ((upw & 2u) << 5) | ((upw & 1u) << 7);
+        bool ig;
+        if constexpr (MODE == kStaticTerrain)
+          ig = ignite_terrain_tab(terrain_view(a, env), a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
+                                  s_pal, s_kw, W, H, r, c, nb, m, dg);
+        else
+          ig = ignite<MODE>(a, env, r, c, nb, m, dg);
+        if (ig) {
           atomicOr(Bn + wi, bit);
           ++newly;
         }
