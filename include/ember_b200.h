@@ -171,7 +171,8 @@ int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* sp
 #define EBL_KERNEL_RESIDENT 2
 #define EBL_KERNEL_BLOCKED 3
 #define EBL_KERNEL_PAIRED 4 /* resident, two envs per CTA sharing 256 threads and one pooled
-                               active list (H*W <= 32768); AUTO picks it for large batches */
+                               active list (H*W <= 32768); selectable only (AUTO does not pair:
+                               slower on C1, ember_kernels.h) */
 int ebl_batch_set_kernel(ebl_batch* b, int which);
 /* Explicit tiling of the blocked kernel (tile_h rows x tile_w cols, tile_w a multiple of
  * 32, `halo` rows of light cone = steps per launch); tile_h == 0 restores planning. */
