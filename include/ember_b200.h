@@ -163,6 +163,10 @@ int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* sp
  *  AUTO      the bit-sliced blocked kernel: one CTA per env with all n steps fused when an
  *            env fits shared memory (H*W <= 65536), else light-cone-halo tiles, 8 steps
  *            per launch;
+ *  FRONTIER  whole env per CTA (H*W <= 16384), all steps fused, each step touching only its
+ *            active list (the next list built from this step's decisions, no dense pass); envs
+ *            whose list outgrows its capacity are continued by the blocked kernel in a second
+ *            launch.  Faster per step for small fires, not for the heaviest;
  *  TILED     the per-cell tile kernel, one step per launch (independent implementation);
  *  RESIDENT  the blocked kernel, whole env per CTA (error if it does not fit);
  *  BLOCKED   the blocked kernel with halo tiles even when the env would fit. */
@@ -170,6 +174,7 @@ int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* sp
 #define EBL_KERNEL_TILED 1
 #define EBL_KERNEL_RESIDENT 2
 #define EBL_KERNEL_BLOCKED 3
+#define EBL_KERNEL_FRONTIER 5
 #define EBL_KERNEL_PAIRED 4 /* resident, two envs per CTA sharing 256 threads and one pooled
                                active list (H*W <= 32768); selectable only (AUTO does not pair:
                                slower on C1, ember_kernels.h) */
@@ -205,6 +210,9 @@ int ebl_batch_intensity(ebl_batch* b, float* lambda, float* p);
  * CPU reference is only possible here), [2] steps, [3] kernel
  * launches issued. */
 int ebl_batch_diag(ebl_batch* b, uint64_t* out4, int reset);
+/* Number of envs the last FRONTIER run handed over to the blocked kernel (active list over its
+ * capacity; diagnostics and tests). */
+int ebl_batch_frontier_handovers(ebl_batch* b, int* count);
 /* Phase profile of the resident blocked kernel (diagnostic builds with -DEBL_PHASE_PROF=1 only;
  * otherwise set_profiling(on) fails with EBL_ESTATE): each launch stores per env int64
  * [n_envs][10] = {P1 cycles (to the first barrier), P2 cycles (to the second), active cells,

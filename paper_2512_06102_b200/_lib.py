@@ -114,6 +114,7 @@ SIGNATURES = {
     "ebl_step_batch": (_I, [_P, _I]),
     "ebl_batch_run": (_I, [_P, _P, _I, _P]),
     "ebl_batch_set_profiling": (_I, [_P, _I]),
+    "ebl_batch_frontier_handovers": (_I, [_P, _P]),
     "ebl_batch_profile": (_I, [_P, _P]),
     "ebl_batch_set_pipeline": (_I, [_P, _I]),
     "ebl_batch_set_kernel": (_I, [_P, _I]),

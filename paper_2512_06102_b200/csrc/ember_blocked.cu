@@ -65,6 +65,9 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   __shared__ float s_kw[MODE == kStaticTerrain ? E : 1][8];    // kappa_wind of the wind in force
 
   const int env0 = blockIdx.z * E;
+  // hand-over from the frontier kernel (E == 1): this env resumes at step t_start of the launch
+  const int t_start = a.resume ? a.resume[env0] : 0;
+  if (t_start >= g.n_steps) return;
   const int W = a.w, BH = a.h;
   const int r0 = blockIdx.y * g.tile_h, c0 = blockIdx.x * g.tile_w;  // c0 % 32 == 0
   const int R0 = max(0, r0 - g.halo_rows), R1 = min(BH, r0 + g.tile_h + g.halo_rows);
@@ -137,8 +140,8 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   if (threadIdx.x < 2) s_total[threadIdx.x] = 0;
   if (threadIdx.x < 2 * E) s_newly[threadIdx.x / E][threadIdx.x % E] = 0;
   for (int i = threadIdx.x; i < 64 * E; i += blockDim.x) {
-    const int q = i >> 6, k = i & 63;
-    s_prefix[q][k] = key_prefix(a.seed, a.streams[min(env0 + q, a.n_envs - 1)], a.step + static_cast<uint64_t>(k));
+    const int q = i >> 6, k = t_start + (i & 63);
+    s_prefix[q][k & 127] = key_prefix(a.seed, a.streams[min(env0 + q, a.n_envs - 1)], a.step + static_cast<uint64_t>(k));
   }
   __syncthreads();
 
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
 #else
 #define EBL_PW_MARK(v)
 #endif
-  for (int t = 0; t < g.n_steps; ++t) {
+  for (int t = t_start; t < g.n_steps; ++t) {
     const int par = t & 1;
 #if EBL_PHASE_PROF
     if (a.prof && threadIdx.x == 0) pr_t0 = clock64();
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
     if (threadIdx.x < E) s_newly[par ^ 1][threadIdx.x] = 0;
     const int srow = sched_row(a, a.step + static_cast<uint64_t>(t));  // wind in force
     if constexpr (MODE == kStaticTerrain) {  // read by P2, after the first barrier
-      if ((t == 0 || a.sched_len > 1) && threadIdx.x < 8 * E) {
+      if ((t == t_start || a.sched_len > 1) && threadIdx.x < 8 * E) {
         const int q = threadIdx.x >> 3;
         s_kw[q][threadIdx.x & 7] = __ldg(a.kw32 + static_cast<size_t>(srow) * a.kw_sched_stride +
                                          static_cast<size_t>(min(env0 + q, a.n_envs - 1)) * a.kw_stride +
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
 #pragma unroll
     for (int q = 0; q < E; ++q) newly[q] = 0;
     const int total = min(s_total[par], cap);
-    if ((t & 63) == 63 && t + 1 < g.n_steps) {  // refill the ring with steps t+1 .. t+64
+    if (((t - t_start) & 63) == 63 && t + 1 < g.n_steps) {  // refill the ring with steps t+1 .. t+64
       for (int i = threadIdx.x; i < 64 * E; i += blockDim.x) {
         const int q = i >> 6, k = i & 63;
         s_prefix[q][(t + 1 + k) & 127] = key_prefix(a.seed, a.streams[min(env0 + q, a.n_envs - 1)],

@@ -77,6 +77,8 @@ struct ebl_batch {
   DevBuf<int32_t> counts;
   DevBuf<unsigned long long> diag;
   DevBuf<long long> prof;           // phase profile of the blocked kernel (ebl_batch_set_profiling)
+  DevBuf<int> resume;               // frontier -> blocked hand-over step per env
+  int frontier_steps = 0;           // n_steps of the last frontier launch (0: none)
   bool profiling = false;
   uint64_t launches = 0, steps_done = 0;
 
@@ -275,6 +277,7 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
   a.streams += o;
   if (a.counts) a.counts += o * 4;
   if (a.prof) a.prof += o * 10;
+  if (a.resume) a.resume += o;
   if (a.tab_stride) {
     a.pot += o * a.tab_stride * 8;
     a.gamma += o * a.tab_stride;
@@ -289,6 +292,13 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
     a.kw64 += o * a.kw_stride;
   }
   return a;
+}
+
+// The frontier kernel only on request: measured on C1 (1024 x 128^2 x 200) it runs light envs
+// ~4x faster per step than the blocked kernel but the heaviest envs -- which set the batch time --
+// no faster (its apply phase's shared atomics cost what the dense pass saves), 0.94 vs 0.78 ms.
+bool use_frontier(const ebl_batch* b) {
+  return b->kernel == EBL_KERNEL_FRONTIER && b->tile_h == 0 && ebl::frontier_fits(b->h, b->w);
 }
 
 int ensure_pipeline(ebl_batch* b, int chunks) {
@@ -814,13 +824,15 @@ uint64_t ebl_batch_step_index(const ebl_batch* b) { return b ? b->step : 0; }
 
 int ebl_batch_set_kernel(ebl_batch* b, int which) {
   if (int e = check_batch(b)) return e;
-  if (which < EBL_KERNEL_AUTO || which > EBL_KERNEL_PAIRED) return set_err(EBL_EINVAL, "unknown kernel");
+  if (which < EBL_KERNEL_AUTO || which > EBL_KERNEL_FRONTIER) return set_err(EBL_EINVAL, "unknown kernel");
+  if (which == EBL_KERNEL_FRONTIER && !ebl::frontier_fits(b->h, b->w))
+    return set_err(EBL_EINVAL, "the frontier kernel needs a resident env with H*W <= 16384");
   if ((which == EBL_KERNEL_RESIDENT || which == EBL_KERNEL_PAIRED) && !ebl::resident_fits(b->h, b->w))
     return set_err(EBL_EINVAL, "env too large for the resident kernel");
   if (which == EBL_KERNEL_PAIRED && b->ncell > 32768)
     return set_err(EBL_EINVAL, "paired residency needs H*W <= 32768");
   b->kernel = which;
-  b->envs_per_cta = which == EBL_KERNEL_AUTO ? 0 : (which == EBL_KERNEL_PAIRED ? 2 : 1);
+  b->envs_per_cta = which == EBL_KERNEL_PAIRED ? 2 : (which == EBL_KERNEL_AUTO ? 0 : 1);
   return EBL_OK;
 }
 
@@ -846,6 +858,19 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
                                  cudaMemcpyDeviceToDevice, b->stream));
       }
     }
+  } else if (use_frontier(b)) {  // frontier kernel, all steps in one launch (+ hand-over launch)
+    EBL_CUDA(b->resume.alloc(b->n_envs));
+    ebl::StepArgs a = step_args(b);
+    EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
+    a.counts = b->counts.p;
+    a.resume = b->resume.p;
+    a.traj = b->traj_out;
+    a.traj_t0 = 0;
+    EBL_CUDA(ebl::launch_step_frontier(a, b->mode, n_steps, b->stream));
+    b->frontier_steps = n_steps;
+    b->cur ^= 1;
+    b->step += n_steps;
+    b->launches += 2;
   } else {  // bit-sliced blocked kernel: whole env per CTA when it fits, else halo tiles
     const bool force_tiles = b->kernel == EBL_KERNEL_BLOCKED;
     for (int done = 0; done < n_steps;) {
@@ -901,6 +926,7 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
   if (int e = prepare(b)) return e;
   const bool resident = b->kernel != EBL_KERNEL_TILED && b->kernel != EBL_KERNEL_BLOCKED &&
                         b->tile_h == 0 && ebl::resident_fits(b->h, b->w);
+  const bool frontier = use_frontier(b);
   int chunks = b->pipe_chunks > 0 ? b->pipe_chunks : 8;
   chunks = std::min(chunks, b->n_envs);
   if (!resident || n_steps == 0 || chunks <= 1) {  // one launch per step set: plain sequence
@@ -914,6 +940,10 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
   const ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps, false, 0, b->n_envs, b->envs_per_cta);
   ebl::StepArgs a = step_args(b);
   a.counts = b->counts.p;
+  if (frontier) {
+    EBL_CUDA(b->resume.alloc(b->n_envs));
+    a.resume = b->resume.p;
+  }
   // everything earlier on the batch stream (state/key uploads, statics) happens first
   EBL_CUDA(cudaEventRecord(b->pipe_ev_start, b->stream));
   EBL_CUDA(cudaStreamWaitEvent(b->pipe_in, b->pipe_ev_start, 0));
@@ -932,7 +962,8 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
     cudaStream_t s = b->pipe_comp[c];
     EBL_CUDA(cudaStreamWaitEvent(s, b->pipe_ev_in[c], 0));
     EBL_CUDA(cudaMemsetAsync(b->counts.p + static_cast<size_t>(off) * 4, 0, static_cast<size_t>(n) * 4 * sizeof(int32_t), s));
-    EBL_CUDA(ebl::launch_step_blocked(chunk_args(b, a, off, n), b->mode, g, s));
+    if (frontier) EBL_CUDA(ebl::launch_step_frontier(chunk_args(b, a, off, n), b->mode, n_steps, s));
+    else EBL_CUDA(ebl::launch_step_blocked(chunk_args(b, a, off, n), b->mode, g, s));
     EBL_CUDA(cudaEventRecord(b->pipe_ev_done[c], s));
   }
   for (int c = 0; c < chunks; ++c) {
@@ -948,7 +979,8 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
   EBL_CUDA(cudaStreamSynchronize(b->pipe_out));
   b->cur ^= 1;
   b->step += n_steps;
-  b->launches += chunks;
+  b->launches += frontier ? 2 * chunks : chunks;
+  if (frontier) b->frontier_steps = n_steps;
   b->steps_done += n_steps;
   b->counts_valid = true;
   return EBL_OK;
@@ -1074,6 +1106,18 @@ int ebl_batch_profile(ebl_batch* b, int64_t* out) {
   EBL_CUDA(cudaMemcpyAsync(out, b->prof.p, static_cast<size_t>(b->n_envs) * 10 * sizeof(long long),
                            cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_batch_frontier_handovers(ebl_batch* b, int* count) {
+  if (int e = check_batch(b)) return e;
+  if (!count) return set_err(EBL_EINVAL, "null count");
+  *count = 0;
+  if (b->frontier_steps == 0) return EBL_OK;
+  std::vector<int> r(b->n_envs);
+  EBL_CUDA(cudaMemcpyAsync(r.data(), b->resume.p, r.size() * sizeof(int), cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  for (int v : r) *count += v < b->frontier_steps;
   return EBL_OK;
 }
 

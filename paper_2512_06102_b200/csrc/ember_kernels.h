@@ -27,6 +27,12 @@ bool resident_fits(int h, int w);
 BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_off, int n_envs,
                       int envs_per_cta);
 cudaError_t launch_step_blocked(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s);
+// frontier kernel (ember_frontier.cu): resident envs with H*W <= 16384; hands envs whose active
+// list outgrows its capacity over to the blocked kernel (a.resume: n_envs device ints)
+int frontier_cap(int h, int w);
+size_t frontier_smem_bytes(int h, int w);
+bool frontier_fits(int h, int w);
+cudaError_t launch_step_frontier(const StepArgs& a, int mode, int n_steps, cudaStream_t s);
 
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s);
 cudaError_t launch_det_loss(const DetArgs& d, cudaStream_t s);

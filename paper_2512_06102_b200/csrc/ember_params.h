@@ -46,7 +46,8 @@ struct StepArgs {
   float inv_dist32[2];
   double dist64[2];
   int force64;
-  long long* prof;                // [n_envs][4] phase profile (P1 cycles, P2 cycles, active, -), or null
+  long long* prof;                // [n_envs][10] phase profile (EBL_PHASE_PROF builds), or null
+  int* resume;                    // [n_envs] first step of this launch per env (frontier hand-over), or null
 };
 
 // Tiling of the blocked kernel (ember_blocked.cu): tiles of tile_h x tile_w cells with

@@ -16,7 +16,7 @@ from . import _lib
 from ._lib import EnvConfig, EnvState, SimConfig, check, lib
 
 UNBURNED, BURNING, BURNED = 0, 1, 2
-KERNEL_AUTO, KERNEL_TILED, KERNEL_RESIDENT, KERNEL_BLOCKED, KERNEL_PAIRED = 0, 1, 2, 3, 4
+KERNEL_AUTO, KERNEL_TILED, KERNEL_RESIDENT, KERNEL_BLOCKED, KERNEL_PAIRED, KERNEL_FRONTIER = 0, 1, 2, 3, 4, 5
 
 
 def _ptr(a: np.ndarray | None):
@@ -192,6 +192,12 @@ class Batch:
             out = np.empty((self.n_envs, self.height, self.width), dtype=np.uint8)
         check(lib().ebl_batch_run(self._h, _ptr(st), n_steps, _ptr(out)))
         return out
+
+    def frontier_handovers(self) -> int:
+        """Envs of the last FRONTIER run continued by the blocked kernel (list over capacity)."""
+        n = C.c_int()
+        check(lib().ebl_batch_frontier_handovers(self._h, C.byref(n)))
+        return n.value
 
     def set_pipeline(self, chunks: int) -> None:
         check(lib().ebl_batch_set_pipeline(self._h, chunks))

@@ -12,7 +12,7 @@ from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [eb.KERNEL_TILED, eb.KERNEL_RESIDENT, eb.KERNEL_BLOCKED, eb.KERNEL_PAIRED]
+KERNELS = [eb.KERNEL_TILED, eb.KERNEL_RESIDENT, eb.KERNEL_BLOCKED, eb.KERNEL_PAIRED, eb.KERNEL_FRONTIER]
 REL_TOL = 1e-5  # north_star: lambda and p within 1e-5 relative in fp32
 
 
@@ -189,6 +189,8 @@ def test_kernels_identical_ragged(port, h, w):
                 (eb.KERNEL_AUTO, (8, 32, 3)), (eb.KERNEL_AUTO, (5, 64, 1)), (eb.KERNEL_AUTO, (16, 96, 7))]
     if h * w <= 32768:  # two envs per CTA (5 envs: the last CTA carries one)
         variants.append((eb.KERNEL_PAIRED, None))
+    if h * w <= 16384:
+        variants.append((eb.KERNEL_FRONTIER, None))
     for kernel, tiling in variants:
         b = eb.Batch(n, h, w)
         b.set_terrain(cls, el, veg, den, 25.0)
@@ -327,7 +329,8 @@ def test_c1_full_size_kernels_agree_and_sampled_oracle(port):
         b.step(steps)
         outs.append(b.get_state())
         assert b.diag()["ambiguous"] == 0
-    assert np.array_equal(outs[0], outs[1])
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
     for e in (0, 1, 511, 777, 1022, 1023):
         g = O.grid_terrain(port, "port", t.veg()[e], t.den()[e], t.elevation[e], 30.0,
                            t.wind_speed[e], t.wind_direction[e])
@@ -454,3 +457,39 @@ def test_pipelined_host_run_equals_sequence(n_envs, chunks):
     assert np.array_equal(out["seq"][1], out["run"][1])
     assert np.array_equal(out["seq"][2], out["run"][2])
     assert out["seq"][3] == out["run"][3] == 5 + steps + 3
+
+
+@pytest.mark.parametrize("case", ["initial", "midrun"])
+def test_frontier_handover_vs_blocked_and_oracle(port, case):
+    """Envs whose active list outgrows the frontier kernel's capacity (2048 at 128^2) are
+    continued by the blocked kernel: at launch (a dense initial fire) or mid-run (persistent
+    burning, p_continue 0.97).  Bit-identical to the blocked kernel and the oracle, counts and
+    recorded trajectories included."""
+    n, h, w, steps, seed = 6, 128, 128, 60, 5
+    t = eb.synth_terrain(seed, n, h, w)
+    rs = np.random.default_rng(3)
+    if case == "initial":
+        init = (rs.random((n, h, w)) < 0.2).astype(np.uint8)
+        init[0] = eb.synth_ignitions(seed, t, 5)[0]  # one env stays on the frontier path
+        cfg = None
+    else:
+        init = eb.synth_ignitions(seed, t, 40)
+        cfg = [0.45, 0.2, 0.4, 1.0, 1.0, 0.97]
+    res = {}
+    for kernel in (eb.KERNEL_FRONTIER, eb.KERNEL_RESIDENT):
+        b = _terrain_batch(t, cfg, kernel)
+        b.set_state(init)
+        b.set_key(seed, 0, first_stream=0)
+        traj = b.step_record(steps)
+        res[kernel] = (b.get_state(), b.counts().copy(), traj)
+        if kernel == eb.KERNEL_FRONTIER:
+            ho = b.frontier_handovers()
+            assert 1 <= ho <= n - (1 if case == "initial" else 0), ho
+        assert b.diag()["ambiguous"] == 0
+    f, r = res[eb.KERNEL_FRONTIER], res[eb.KERNEL_RESIDENT]
+    assert np.array_equal(f[0], r[0]) and np.array_equal(f[1], r[1]) and np.array_equal(f[2], r[2])
+    c = O.DEFAULT_CFG if cfg is None else cfg
+    for e in (0, n - 1):
+        g = O.grid_terrain(port, "port", t.veg()[e], t.den()[e], t.elevation[e], 30.0,
+                           t.wind_speed[e], t.wind_direction[e])
+        assert np.array_equal(f[0][e], O.run(port, "port", g, c, seed, 0, e, steps, init[e]))
