@@ -33,6 +33,25 @@ namespace ebl {
 
 namespace {
 
+// Fixed-order block sums of N values at once (one shared round trip instead of N).
+template <int N>
+__device__ __forceinline__ void block_sum_n(double (&v)[N], double* red) {
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int q = 0; q < N; ++q) red[q * 32 + (threadIdx.x >> 5)] = v[q];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    double t = 0.0;
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) t += red[q * 32 + i];  // fixed order
+    v[q] = t;
+  }
+}
+
 __device__ __forceinline__ double block_sum_d(double v, double* red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -161,7 +180,7 @@ __global__ void k_det_loss(DetArgs d) {
 
 // back1: lambda, a_lambda, A_un update, gamma / p_continue gradients.
 __global__ void k_det_back1(DetArgs d, int t) {
-  __shared__ double red[32];
+  __shared__ double red[2 * 32];
   const StepArgs& a = d.s;
   const int ncell = a.h * a.w;
   const int env = blockIdx.y;
@@ -186,18 +205,18 @@ __global__ void k_det_back1(DetArgs d, int t) {
     g_gamma = a_x * lam * F;  // dgamma/dalpha_gamma = F(v)
     g_pc = bu * (Ab - Ad);
   }
-  g_gamma = block_sum_d(g_gamma, red);
-  g_pc = block_sum_d(g_pc, red);
+  double g2[2] = {g_gamma, g_pc};
+  block_sum_n<2>(g2, red);
   if (threadIdx.x == 0) {
     double* acc = d.acc + (static_cast<size_t>(env) * gridDim.x + blockIdx.x) * 8;
-    acc[4] += g_gamma;
-    acc[5] += g_pc;
+    acc[4] += g2[0];
+    acc[5] += g2[1];
   }
 }
 
 // back2: A_burn update and the pot-parameter gradients (gather over each source cell's targets).
 __global__ void k_det_back2(DetArgs d, int t) {
-  __shared__ double red[32];
+  __shared__ double red[4 * 32];
   const StepArgs& a = d.s;
   const int ncell = a.h * a.w;
   const int env = blockIdx.y;
@@ -228,6 +247,7 @@ __global__ void k_det_back2(DetArgs d, int t) {
       }
     } else if (bu != 0.0) {
       const TerrainView tv = terrain_view(a, env);
+      const float* slope = a.slope32 ? a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8 : nullptr;
       const double V = d.V[env * d.wind_stride];
       const float zu = tv.elev[i];
 #pragma unroll
@@ -242,8 +262,14 @@ __global__ void k_det_back2(DetArgs d, int t) {
         // dpot/dalpha_w2 = pot V (cos - 1), dpot/dalpha_s = pot S
         // S in fp32 (relative error ~1e-7, far inside the 1e-4 gradient bar); fp32 elevations
         // differ exactly in fp32 unless they are ~2^24 apart in magnitude
-        const float dz = tv.elev[vr * a.w + vc] - zu;
-        const double S = dz == dz ? static_cast<double>(atanf(dz * tv.inv_dist32[k & 1])) : 0.0;  // nodata: 0
+        // the slope table holds exactly this fp32 value (record of the target v, direction k)
+        double S;
+        if (slope) {
+          S = static_cast<double>(slope[static_cast<size_t>(vr * a.w + vc) * 8 + k]);
+        } else {
+          const float dz = tv.elev[vr * a.w + vc] - zu;
+          S = dz == dz ? static_cast<double>(atanf(dz * tv.inv_dist32[k & 1])) : 0.0;  // nodata: 0
+        }
         const double ab = al * bu;
         gp += ab * (pot * d.inv_p_base);
         gw1 += ab * pot * V;
@@ -253,16 +279,14 @@ __global__ void k_det_back2(DetArgs d, int t) {
     }
     d.A_burn[base + i] = acc_burn;  // A_bd is unchanged (bd' = bd + ...)
   }
-  gp = block_sum_d(gp, red);
-  gw1 = block_sum_d(gw1, red);
-  gw2 = block_sum_d(gw2, red);
-  gs = block_sum_d(gs, red);
+  double g4[4] = {gp, gw1, gw2, gs};
+  block_sum_n<4>(g4, red);
   if (threadIdx.x == 0) {
     double* acc = d.acc + (static_cast<size_t>(env) * gridDim.x + blockIdx.x) * 8;
-    acc[0] += gp;
-    acc[1] += gw1;
-    acc[2] += gw2;
-    acc[3] += gs;
+    acc[0] += g4[0];
+    acc[1] += g4[1];
+    acc[2] += g4[2];
+    acc[3] += g4[3];
   }
 }
 
