@@ -63,6 +63,9 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   __shared__ uint64_t s_prefix[E][128];
   __shared__ float s_pal[MODE == kStaticTerrain ? 512 : 1];  // terrain palette: fp32 src, gam
   __shared__ float s_kw[MODE == kStaticTerrain ? E : 1][8];    // kappa_wind of the wind in force
+  // src32(class) * kappa_wind32(k) of the wind in force, palettes of <= 32 classes
+  __shared__ float s_srckw[MODE == kStaticTerrain ? E : 1][MODE == kStaticTerrain ? 32 * 8 : 1];
+  const bool use_rec = MODE == kStaticTerrain && a.nfuel && a.n_pal <= 32;
 
   const int env0 = blockIdx.z * E;
   // hand-over from the frontier kernel (E == 1): this env resumes at step t_start of the launch
@@ -85,6 +88,8 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   const int cap = g.list_cap;
   const uint32_t last_mask = low_mask(RW - 32 * (wpr - 1));
   const int rot = wpr >= 32 ? 1 : 32 / wpr;  // list-build word rotation (see P1)
+  // list entry -> region row: exact reciprocal division (entry * RW < 2^32)
+  const uint32_t rw_magic = RW > 1 ? static_cast<uint32_t>((0x100000000ull + RW - 1) / RW) : 0u;
 
   const size_t ncell = static_cast<size_t>(BH) * W;
   const bool vec = (W & 15) == 0;  // 16-byte aligned rows (C0 is a multiple of 32)
@@ -204,6 +209,14 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
         s_kw[q][threadIdx.x & 7] = __ldg(a.kw32 + static_cast<size_t>(srow) * a.kw_sched_stride +
                                          static_cast<size_t>(min(env0 + q, a.n_envs - 1)) * a.kw_stride +
                                          (threadIdx.x & 7));
+      }
+      if (use_rec && (t == t_start || a.sched_len > 1)) {
+        for (int i = threadIdx.x; i < E * a.n_pal * 8; i += blockDim.x) {
+          const int q = i / (a.n_pal * 8), ck = i - q * a.n_pal * 8;
+          const float kw = __ldg(a.kw32 + static_cast<size_t>(srow) * a.kw_sched_stride +
+                                 static_cast<size_t>(min(env0 + q, a.n_envs - 1)) * a.kw_stride + (ck & 7));
+          s_srckw[q][ck] = s_pal[ck >> 3] * kw;  // the same product terrain_lambda32 forms
+        }
       }
     }
     // ---- P1: each thread owns whole rows of one env; the 3x3 dilation slides along the row in
@@ -342,7 +355,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
     auto decide = [&](int sub, int lc) {
       const uint32_t* B = Bplane(sub, cur);
       uint32_t* Bn = Bplane(sub, cur ^ 1);
-      const int rr = lc / RW, cc = lc - rr * RW;
+      const int rr = RW > 1 ? static_cast<int>(__umulhi(static_cast<uint32_t>(lc), rw_magic)) : lc, cc = lc - rr * RW;
       const int wi = (rr + 1) * S + (cc >> 5);
       const uint32_t bit = 1u << (cc & 31);
       const uint64_t m = cell_bits53(s_prefix[sub][t & 127], gbase + static_cast<uint64_t>(rr) * W + cc, 0);
@@ -372,7 +385,12 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
         if (a.prof) atomicAdd(&s_ncand, 1);
 #endif
         bool ig;
-        if constexpr (MODE == kStaticTerrain && EBL_LAMBDA_ALL)
+        if (use_rec)
+          ig = ignite_terrain_rec(terrain_view(a, env0 + sub, srow),
+                                  a.slope32 + static_cast<size_t>(env0 + sub) * a.ter_stride * 8,
+                                  a.nfuel + static_cast<size_t>(env0 + sub) * a.ter_stride, s_srckw[sub], s_pal + 256,
+                                  a.alpha_s_l2, W, R0 + rr, C0 + cc, nb, m, dg);
+        else if constexpr (MODE == kStaticTerrain && EBL_LAMBDA_ALL)
           ig = ignite_terrain_tab(terrain_view(a, env0 + sub, srow),
                                   a.slope32 + static_cast<size_t>(env0 + sub) * a.ter_stride * 8, s_pal, s_kw[sub],
                                   W, BH, R0 + rr, C0 + cc, nb, m, dg);
@@ -556,10 +574,13 @@ static cudaError_t launch_blocked_w(const StepArgs& a, const BlockGeom& g, size_
 
 template <int MODE, int E>
 static cudaError_t launch_blocked_t(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStream_t s) {
-  const int rw = g.tile_w + 2 * g.halo_cols;
-  const int wpr = ((rw < a.w ? rw : a.w) + 31) / 32;
-  if (wpr == 4) return launch_blocked_w<MODE, E, 4>(a, g, sm, s);
-  if (wpr == 2) return launch_blocked_w<MODE, E, 2>(a, g, sm, s);
+  // compile-time words per row only when every region spans the full width (edge tiles of a
+  // column-tiled grid are narrower; their last-word mask depends on the true word count)
+  if (g.tile_w >= a.w) {
+    const int wpr = (a.w + 31) / 32;
+    if (wpr == 4) return launch_blocked_w<MODE, E, 4>(a, g, sm, s);
+    if (wpr == 2) return launch_blocked_w<MODE, E, 2>(a, g, sm, s);
+  }
   return launch_blocked_w<MODE, E, 0>(a, g, sm, s);
 }
 

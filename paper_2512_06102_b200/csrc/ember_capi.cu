@@ -101,6 +101,7 @@ struct ebl_batch {
   DevBuf<uint8_t> fuel;
   DevBuf<float> elev;
   DevBuf<float> slope32;            // [grid][cell][8] fp32 slopes of the layers (built by prepare)
+  DevBuf<uint2> nfuel;              // [grid][cell] fuel classes of the 8 sources (built with slope32)
   bool slope_dirty = false;
   std::vector<double> pal_veg, pal_den;
   double cellsize = 30.0;
@@ -220,8 +221,9 @@ int prepare(ebl_batch* b) {
   if (b->mode == ebl::kStaticTerrain && b->slope_dirty) {  // slope_from_dem of the layers (GridState)
     const double d0 = b->cellsize * 1.0, d1 = b->cellsize * 1.41421356237309504880;
     EBL_CUDA(b->slope32.alloc(b->ncell * b->n_grids * 8));
-    EBL_CUDA(ebl::launch_slope_table(b->elev.p, b->n_grids, b->h, b->w, static_cast<float>(1.0 / d0),
-                                     static_cast<float>(1.0 / d1), b->slope32.p, b->stream));
+    EBL_CUDA(b->nfuel.alloc(b->ncell * b->n_grids));
+    EBL_CUDA(ebl::launch_slope_table(b->elev.p, b->fuel.p, b->n_grids, b->h, b->w, static_cast<float>(1.0 / d0),
+                                     static_cast<float>(1.0 / d1), b->slope32.p, b->nfuel.p, b->stream));
     b->slope_dirty = false;
   }
   return EBL_OK;
@@ -246,6 +248,9 @@ ebl::StepArgs step_args(const ebl_batch* b) {
   a.fuel = b->fuel.p;
   a.elev = b->elev.p;
   a.slope32 = b->mode == ebl::kStaticTerrain ? b->slope32.p : nullptr;
+  a.nfuel = b->mode == ebl::kStaticTerrain ? b->nfuel.p : nullptr;
+  a.n_pal = static_cast<int>(b->pal_veg.size());
+  a.alpha_s_l2 = static_cast<float>(b->cfg.alpha_s * 1.4426950408889634);
   a.ter_stride = b->n_grids > 1 ? b->ncell : 0;
   a.pal32 = b->pal32.p;
   a.pal64 = b->pal64.p;
@@ -286,6 +291,7 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
     a.fuel += o * a.ter_stride;
     a.elev += o * a.ter_stride;
     if (a.slope32) a.slope32 += o * a.ter_stride * 8;
+    if (a.nfuel) a.nfuel += o * a.ter_stride;
   }
   if (a.kw_stride) {
     a.kw32 += o * a.kw_stride;

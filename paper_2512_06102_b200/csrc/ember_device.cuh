@@ -169,6 +169,31 @@ __device__ __forceinline__ float terrain_lambda32_tab(const TerrainView& t, cons
   return lam;
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {  // 2^x, rel. error ~2^-22 (MUFU.EX2)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// The leanest fp32 lambda: the candidate's slope record, its sources' class record, and a
+// shared-memory table srckw[class * 8 + k] = src32(class) * kappa_wind32(k) of the wind in force;
+// kappa_slope = 2^(alpha_s log2e * S).  Within ~3e-7 relative of terrain_lambda32 (guard 1e-4).
+__device__ __forceinline__ float terrain_lambda32_rec(const float* __restrict__ slope32, const uint2* __restrict__ nfuel,
+                                                      const float* srckw, float alpha_l2, int v, uint32_t nb) {
+  const float4 s0 = __ldg(reinterpret_cast<const float4*>(slope32) + 2 * v);
+  const float4 s1 = __ldg(reinterpret_cast<const float4*>(slope32) + 2 * v + 1);
+  const uint2 nf = __ldg(nfuel + v);
+  const float s[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+  float lam = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t f = ((k < 4 ? nf.x : nf.y) >> (8 * (k & 3))) & 0xffu;
+    const float contrib = srckw[f * 8 + k] * ex2_approx(alpha_l2 * s[k]);
+    lam += (nb >> k) & 1u ? contrib : 0.f;
+  }
+  return lam;
+}
+
 constexpr double kGuardRel = 1e-4;
 
 __device__ __forceinline__ bool ignite_terrain(const TerrainView& t, int w, int r, int c,
@@ -202,6 +227,29 @@ __device__ __forceinline__ bool ignite_terrain_tab(const TerrainView& t, const f
     uint8_t fv;
     const float lam = terrain_lambda32_tab(t, slope32, pal32s, kw, w, h, r, c, nb, &fv);
     const float x = pal32s[256 + fv] * lam;
+    if (x == 0.f) return false;  // gamma or lambda exactly 0: p = 1 - exp(-0) = 0, u < 0 is false
+    const double p32 = static_cast<double>(-expm1f(-x));
+    if (p32 > 1e-12) {
+      if (u < p32 * (1.0 - kGuardRel)) return true;
+      if (u >= p32 * (1.0 + kGuardRel)) return false;
+    }
+  }
+  dg.fallback();
+  const double p = terrain_p64(t, w, r, c, nb);
+  if (fabs(u - p) < kAmbiguousBand) dg.ambiguous();
+  return u < p;
+}
+
+// ignite_terrain over terrain_lambda32_rec (blocked / tanker kernels when the palette has <= 32
+// classes); pal_gam: the palette's fp32 gamma values (shared memory).
+__device__ __forceinline__ bool ignite_terrain_rec(const TerrainView& t, const float* slope32, const uint2* nfuel,
+                                                   const float* srckw, const float* pal_gam, float alpha_l2, int w,
+                                                   int r, int c, uint32_t nb, uint64_t m, const DiagCounters& dg) {
+  const double u = bits_to_uniform(m);
+  if (!t.force64) {
+    const int v = r * w + c;
+    const float lam = terrain_lambda32_rec(slope32, nfuel, srckw, alpha_l2, v, nb);
+    const float x = pal_gam[__ldg(t.fuel + v)] * lam;
     if (x == 0.f) return false;  // gamma or lambda exactly 0: p = 1 - exp(-0) = 0, u < 0 is false
     const double p32 = static_cast<double>(-expm1f(-x));
     if (p32 > 1e-12) {

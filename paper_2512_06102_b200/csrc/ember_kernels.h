@@ -94,7 +94,7 @@ struct LandcoverArgs {
 };
 cudaError_t launch_landcover_map(const LandcoverArgs& a, cudaStream_t s);
 // fp32 slope table [grid][cell][8] (terrain form, built with the layers; ember_synth.cu)
-cudaError_t launch_slope_table(const float* elev, size_t n_grids, int h, int w, float inv_d0, float inv_d1,
-                               float* out, cudaStream_t s);
+cudaError_t launch_slope_table(const float* elev, const uint8_t* fuel, size_t n_grids, int h, int w, float inv_d0,
+                               float inv_d1, float* out, uint2* nfuel, cudaStream_t s);
 
 }  // namespace ebl

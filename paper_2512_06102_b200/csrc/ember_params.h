@@ -30,6 +30,9 @@ struct StepArgs {
   const uint8_t* fuel;            // [grid][h*w]
   const float* elev;              // [grid][h*w]
   const float* slope32;           // [grid][h*w][8] fp32 slope table (terrain form) or null
+  const uint2* nfuel;             // [grid][h*w] fuel classes of the 8 sources u_k = v - d_k (bytes k)
+  int n_pal;                      // palette entries in use (terrain form)
+  float alpha_s_l2;               // alpha_s * log2(e): kappa_slope = 2^(alpha_s_l2 * S)
   size_t ter_stride;
   const float* pal32;             // [2][256] src32, gam32
   const double* pal64;            // [2][256] src64, gam64

@@ -243,13 +243,16 @@ __global__ void __launch_bounds__(kSynthThreads) k_landcover_map(LandcoverArgs a
   a.fuel[i] = static_cast<uint8_t>(k);
 }
 
+// Also the fuel classes of each cell's 8 sources (one 8-byte record), so a candidate's lambda needs
+// one slope record + one source-class record.
 // slope_from_dem (geodata.cpp:209-229) in the fp32 fast-path form: S[cell][k] = atan((z(v) - z(u_k)) /
 // dist_k) for target v and source u_k = v - d_k, the same fp32 expression terrain_lambda32 evaluates
 // on the fly (so the tabulated and the on-the-fly lambda are bit-identical).  Sources outside the
 // layer and DEM nodata (NaN) on either end give 0.
-__global__ void __launch_bounds__(kSynthThreads) k_slope_table(const float* __restrict__ elev, size_t n_cells,
+__global__ void __launch_bounds__(kSynthThreads) k_slope_table(const float* __restrict__ elev,
+                                                                const uint8_t* __restrict__ fuel, size_t n_cells,
                                                                 int h, int w, float inv_d0, float inv_d1,
-                                                                float4* __restrict__ out) {
+                                                                float4* __restrict__ out, uint2* __restrict__ nf) {
   const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n_cells) return;
   const size_t layer = static_cast<size_t>(h) * w;
@@ -258,19 +261,26 @@ __global__ void __launch_bounds__(kSynthThreads) k_slope_table(const float* __re
   const int r = v / w, c = v - r * w;
   const float* z = elev + g * layer;
   const float zv = z[v];
+  const uint8_t* f = fuel + g * layer;
   float s[8];
+  uint32_t nf0 = 0u, nf1 = 0u;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int ur = r - kDy[k], uc = c - kDx[k];
     float sk = 0.f;
+    uint32_t fk = 0u;  // outside the layer: class 0 (never weighted: no burning source there)
     if (ur >= 0 && ur < h && uc >= 0 && uc < w) {
       const float dz = zv - z[ur * w + uc];
       sk = dz == dz ? atanf(dz * (k & 1 ? inv_d1 : inv_d0)) : 0.f;
+      fk = f[ur * w + uc];
     }
     s[k] = sk;
+    if (k < 4) nf0 |= fk << (8 * k);
+    else nf1 |= fk << (8 * (k - 4));
   }
   out[2 * i] = make_float4(s[0], s[1], s[2], s[3]);
   out[2 * i + 1] = make_float4(s[4], s[5], s[6], s[7]);
+  nf[i] = make_uint2(nf0, nf1);
 }
 
 inline unsigned grid_x(size_t n) { return static_cast<unsigned>((n + kSynthThreads - 1) / kSynthThreads); }
@@ -297,10 +307,11 @@ cudaError_t launch_synth_ignitions(const IgniteArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_slope_table(const float* elev, size_t n_grids, int h, int w, float inv_d0, float inv_d1,
-                               float* out, cudaStream_t s) {
+cudaError_t launch_slope_table(const float* elev, const uint8_t* fuel, size_t n_grids, int h, int w, float inv_d0,
+                               float inv_d1, float* out, uint2* nfuel, cudaStream_t s) {
   const size_t n = n_grids * h * w;
-  k_slope_table<<<grid_x(n), kSynthThreads, 0, s>>>(elev, n, h, w, inv_d0, inv_d1, reinterpret_cast<float4*>(out));
+  k_slope_table<<<grid_x(n), kSynthThreads, 0, s>>>(elev, fuel, n, h, w, inv_d0, inv_d1, reinterpret_cast<float4*>(out),
+                                                    nfuel);
   return cudaGetLastError();
 }
 
