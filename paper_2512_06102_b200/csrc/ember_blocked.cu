@@ -64,8 +64,13 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   __shared__ float s_pal[MODE == kStaticTerrain ? 512 : 1];  // terrain palette: fp32 src, gam
   __shared__ float s_kw[MODE == kStaticTerrain ? E : 1][8];    // kappa_wind of the wind in force
   // src32(class) * kappa_wind32(k) of the wind in force, palettes of <= 32 classes
-  __shared__ float s_srckw[MODE == kStaticTerrain ? E : 1][MODE == kStaticTerrain ? 32 * 8 : 1];
-  const bool use_rec = MODE == kStaticTerrain && a.nfuel && a.n_pal <= 32;
+  // (only in the whole-width instantiations: the extra 1 KB costs halo-tile launches occupancy)
+  constexpr bool kRec = MODE == kStaticTerrain && WPRC != 0;
+  __shared__ float s_srckw[kRec ? E : 1][kRec ? 32 * 8 : 1];
+  // source-class records for whole-env regions (C1-like batches: measured faster); halo tiles of
+  // large landscapes keep the fuel-byte gathers (their statics stream from DRAM; C3 measured
+  // 22.5 ms vs 24.1 ms with the 8-byte records)
+  const bool use_rec = kRec && a.nfuel && a.n_pal <= 32 && g.halo_rows == 0 && g.halo_cols == 0;
 
   const int env0 = blockIdx.z * E;
   // hand-over from the frontier kernel (E == 1): this env resumes at step t_start of the launch
