@@ -188,6 +188,15 @@ int ebl_batch_set_tiling(ebl_batch* b, int tile_h, int tile_w, int halo);
  * rows.  The RNG cell index stays global ((row_off + r) * W + c), so a sharded run is
  * bit-identical to the unsharded one. */
 int ebl_batch_set_row_offset(ebl_batch* b, int64_t row_off);
+/* Layer rows [row_lo, row_hi) this shard owns (its band; the rest of its layer is halo). */
+int ebl_batch_set_band(ebl_batch* b, int row_lo, int row_hi);
+/* Steps n_shards row shards of one landscape (bands in order, one env each, halo-tiled blocked
+ * kernel with `halo` rows of light cone) by n_steps, `halo` steps per launch, with the halo
+ * exchange fused into the kernels: each launch stores the band rows its neighbours hold as halo
+ * straight into their output layers (peer stores over NVLink between GPUs), and each shard's
+ * stream waits on its neighbours' previous launch (events, no host synchronisation).
+ * Bit-identical to the unsharded run.  Replaces the step + ebl_batch_copy_rows loop. */
+int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo);
 /* Copies rows [src_row, src_row+n) of every member of `src` into rows [dst_row, ...) of `dst`
  * (same width and member count); batches on different devices copy peer-to-peer over
  * NVLink (cudaMemcpyPeerAsync) on dst's stream after src's stream has drained. */

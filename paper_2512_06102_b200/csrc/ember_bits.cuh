@@ -54,6 +54,9 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 __device__ __forceinline__ void prefetch_l1(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 // Row stride (words) of a bit-plane with wpr words per row: odd, so the 32 lanes of a warp
 // each reading "its" row at the same column hit 32 distinct shared-memory banks.

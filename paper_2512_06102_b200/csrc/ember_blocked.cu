@@ -38,6 +38,9 @@
 #ifndef EBL_PREFETCH_FRONT
 #define EBL_PREFETCH_FRONT 0  // prefetch next step's candidate statics at each ignition
 #endif
+#ifndef EBL_PF
+#define EBL_PF prefetch_l2
+#endif
 #ifndef EBL_PHASE_PROF
 #define EBL_PHASE_PROF 0  // per-phase clock64 profile (diagnostic builds: scripts/build_variant.sh)
 #endif
@@ -167,9 +170,14 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   const int tj0 = tc0 >> 5, tj1 = (tc1 + 31) >> 5;
   const int twords = tj1 - tj0;
   // bit-planes of the output tile -> uint8 layer at `layer` (+ U/B/X counts when cnt3)
-  auto store_tile = [&](const uint32_t* Bs, const uint32_t* X, uint8_t* __restrict__ layer, int32_t* cnt3) {
+  // bit-planes of the output tile -> uint8 layer at `layer` (+ U/B/X counts when cnt3); rows
+  // outside [row_lo, row_hi) (layer rows) are skipped
+  auto store_tile = [&](const uint32_t* Bs, const uint32_t* X, uint8_t* __restrict__ layer, int32_t* cnt3,
+                        int row_lo, int row_hi, int dst_shift) {
     for (WordIter it(twords, (tr1 - tr0) * twords); it.ok(); it.next()) {
       const int rr = tr0 + it.r, j = tj0 + it.j;
+      const int lrow = R0 + rr;
+      if (lrow < row_lo || lrow >= row_hi) continue;
       const uint32_t b = Bs[(rr + 1) * S + j], x = X[rr * S + j];
       const int nc = min(32, RW - 32 * j);
       if (cnt3) {
@@ -177,7 +185,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
         cnt3[1] += __popc(b);
         cnt3[2] += __popc(x);
       }
-      uint8_t* dst = layer + static_cast<size_t>(R0 + rr) * W + C0 + 32 * j;
+      uint8_t* dst = layer + static_cast<size_t>(lrow + dst_shift) * W + C0 + 32 * j;
       if (nc == 32 && vec) {
         bits_to_bytes(b, x, dst);
       } else {
@@ -404,24 +412,19 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
         if (ig) {
           atomicOr(Bn + wi, bit);
 #if EBL_PREFETCH_FRONT
-          if constexpr (MODE == kStaticTerrain) {
+          if (use_rec) {
             // the ignited cell's unburned neighbours are next step's candidates: pull their slope
-            // records (rows r-1..r+1, 3 records each) and the fuel of their sources (rows r-2..r+2)
-            // toward the SM while this step finishes
+            // and source-class records (rows r-1..r+1, 3 cells each) toward the SM meanwhile
             const int gr = R0 + rr, gc = C0 + cc;
             const size_t eb = static_cast<size_t>(env0 + sub) * a.ter_stride;
             const int c0 = max(gc - 1, 0), c1 = min(gc + 1, W - 1);
 #pragma unroll
             for (int d = -1; d <= 1; ++d) {
               const int rowp = min(max(gr + d, 0), BH - 1);
-              const float* sp = a.slope32 + (eb + static_cast<size_t>(rowp) * W) * 8;
-              prefetch_l1(sp + c0 * 8);
-              prefetch_l1(sp + c1 * 8 + 7);
-            }
-#pragma unroll
-            for (int d = -2; d <= 2; ++d) {
-              const int rowp = min(max(gr + d, 0), BH - 1);
-              prefetch_l1(a.fuel + eb + static_cast<size_t>(rowp) * W + max(gc - 2, 0));
+              const size_t rb = eb + static_cast<size_t>(rowp) * W;
+              EBL_PF(a.slope32 + (rb + c0) * 8);
+              EBL_PF(a.slope32 + (rb + c1) * 8 + 7);
+              EBL_PF(a.nfuel + rb + c0);
             }
           }
 #endif
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
       for (int sub = 0; sub < E; ++sub)
         if (env0 + sub < a.n_envs)
           store_tile(Bplane(sub, cur), Xplane(sub), a.traj + ((a.traj_t0 + t) * a.n_envs + env0 + sub) * ncell,
-                     nullptr);
+                     nullptr, 0, BH, 0);
     }
   }
 
@@ -494,7 +497,10 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   for (int sub = 0; sub < E; ++sub) {
     if (env0 + sub >= a.n_envs) break;
     int32_t cnt3[3] = {0, 0, 0};
-    store_tile(Bplane(sub, cur), Xplane(sub), a.out + (env0 + sub) * ncell, cnt3);
+    store_tile(Bplane(sub, cur), Xplane(sub), a.out + (env0 + sub) * ncell, cnt3, a.store_lo, a.store_hi, 0);
+    for (int p = 0; p < a.n_peers; ++p)  // fused halo exchange: owned rows straight into the neighbour
+      store_tile(Bplane(sub, cur), Xplane(sub), a.peer_out[p], nullptr,
+                 a.peer_lo[p], a.peer_hi[p], a.peer_dst[p] - a.peer_lo[p]);
     if (a.counts) {
       atomicAdd(&s_cnt[sub][0], cnt3[0]);
       atomicAdd(&s_cnt[sub][1], cnt3[1]);

@@ -79,6 +79,8 @@ struct ebl_batch {
   DevBuf<long long> prof;           // phase profile of the blocked kernel (ebl_batch_set_profiling)
   DevBuf<int> resume;               // frontier -> blocked hand-over step per env
   int frontier_steps = 0;           // n_steps of the last frontier launch (0: none)
+  int band_lo = -1, band_hi = -1;   // layer rows owned by this row shard (ebl_batch_set_band)
+  cudaEvent_t shard_ev[2] = {nullptr, nullptr};  // completion of this shard's launch of chunk c, slot c & 1
   bool profiling = false;
   uint64_t launches = 0, steps_done = 0;
 
@@ -151,6 +153,8 @@ struct ebl_batch {
     if (pipe_out) cudaStreamDestroy(pipe_out);
     if (pipe_ev_start) cudaEventDestroy(pipe_ev_start);
     if (pipe_ev_end) cudaEventDestroy(pipe_ev_end);
+    for (cudaEvent_t e : shard_ev)
+      if (e) cudaEventDestroy(e);
   }
 };
 
@@ -270,6 +274,9 @@ ebl::StepArgs step_args(const ebl_batch* b) {
   // the fp32 guard band (1e-4 relative) holds while |alpha_s * slope| stays O(10)
   a.force64 = !(std::fabs(b->cfg.alpha_s) <= 50.0);
   a.prof = b->profiling ? b->prof.p : nullptr;
+  a.store_lo = 0;
+  a.store_hi = b->h;
+  a.n_peers = 0;
   return a;
 }
 
@@ -1028,6 +1035,118 @@ int ebl_batch_copy_rows(ebl_batch* dst, int dst_row, const ebl_batch* src, int s
     }
   }
   dst->counts_valid = false;
+  return EBL_OK;
+}
+
+int ebl_batch_set_band(ebl_batch* b, int row_lo, int row_hi) {
+  if (int e = check_batch(b)) return e;
+  if (row_lo < 0 || row_hi > b->h || row_lo >= row_hi) return set_err(EBL_EINVAL, "band outside the layer");
+  b->band_lo = row_lo;
+  b->band_hi = row_hi;
+  return EBL_OK;
+}
+
+// Row shards stepped together with the halo exchange fused into the kernels: every K-step launch
+// of shard s stores its band rows that neighbour s+-1 holds as halo straight into the neighbour's
+// output layer (peer stores over NVLink when the shards sit on different GPUs); shard s waits
+// (stream events, no host sync) for its neighbours' previous launches before the next one.
+int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
+  if (!shards || n_shards < 1) return set_err(EBL_EINVAL, "no shards");
+  if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
+  if (halo < 1) return set_err(EBL_EINVAL, "halo must be >= 1");
+  for (int s = 0; s < n_shards; ++s) {
+    ebl_batch* b = shards[s];
+    if (int e = check_batch(b)) return e;
+    if (b->n_envs != 1 || b->w != shards[0]->w) return set_err(EBL_EINVAL, "shards: one env each, equal widths");
+    if (b->band_lo < 0) return set_err(EBL_ESTATE, "shards: ebl_batch_set_band first");
+    if (b->kernel == EBL_KERNEL_TILED || b->kernel == EBL_KERNEL_FRONTIER)
+      return set_err(EBL_EINVAL, "shards: blocked kernel only");
+    if (s > 0 && b->row_off + b->band_lo != shards[s - 1]->row_off + shards[s - 1]->band_hi)
+      return set_err(EBL_EINVAL, "shards: bands must tile the landscape in order");
+    if (int e = prepare(b)) return e;
+    EBL_CUDA(cudaSetDevice(b->device));
+    for (cudaEvent_t& e : b->shard_ev)
+      if (!e) EBL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (int q = s - 1; q <= s + 1; q += 2) {  // NVLink peer access to the neighbours' layers
+      if (q < 0 || q >= n_shards || shards[q]->device == b->device) continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, b->device, shards[q]->device) != cudaSuccess || !can)
+        return set_err(EBL_ECUDA, "shards: no peer access between neighbour GPUs");
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(shards[q]->device, 0);
+      if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) return set_err(EBL_ECUDA, cudaGetErrorString(pe));
+      cudaGetLastError();
+    }
+  }
+  std::vector<uint8_t*> outs(n_shards);
+  std::vector<ebl::BlockGeom> geo(n_shards);
+  int chunk = 0;
+  for (int done = 0; done < n_steps; ++chunk) {
+    int k = n_shards > 1 ? std::min(halo, n_steps - done) : n_steps - done;
+    for (int s = 0; s < n_shards; ++s) {  // tiling per shard; a chunk never outruns a light cone
+      const ebl_batch* b = shards[s];
+      ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, k, b->kernel == EBL_KERNEL_BLOCKED, 0, 1, 1);
+      if (b->tile_h > 0) {
+        g.envs_per_cta = 1;
+        g.tile_h = b->tile_h;
+        g.tile_w = b->tile_w;
+        g.halo_rows = b->tile_halo;
+        g.halo_cols = g.tile_w >= b->w ? 0 : 32;
+        const int rh = std::min(b->h, g.tile_h + 2 * g.halo_rows);
+        const int rw = std::min(b->w, g.tile_w + 2 * g.halo_cols);
+        g.list_cap = std::max(1, rh * rw / 4);
+      }
+      if (g.halo_rows > 0 || g.halo_cols > 0) k = std::min(k, std::max(1, g.halo_rows));
+      geo[s] = g;
+    }
+    for (int s = 0; s < n_shards; ++s) outs[s] = shards[s]->state[shards[s]->cur ^ 1].p;
+    for (int s = 0; s < n_shards; ++s) {
+      ebl_batch* b = shards[s];
+      EBL_CUDA(cudaSetDevice(b->device));
+      // the neighbours' launches of the previous chunk (slot (chunk-1) & 1: a neighbour processed
+      // earlier in this loop has already re-recorded the other slot)
+      if (chunk > 0)
+        for (int q = s - 1; q <= s + 1; q += 2)
+          if (q >= 0 && q < n_shards)
+            EBL_CUDA(cudaStreamWaitEvent(b->stream, shards[q]->shard_ev[(chunk - 1) & 1], 0));
+      ebl::BlockGeom g = geo[s];
+      g.n_steps = k;
+      ebl::StepArgs a = step_args(b);
+      EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, 4 * sizeof(int32_t), b->stream));
+      a.counts = b->counts.p;
+      a.store_lo = b->band_lo;
+      a.store_hi = b->band_hi;
+      const int64_t g0 = b->row_off + b->band_lo, g1 = b->row_off + b->band_hi;
+      for (int q = s - 1; q <= s + 1; q += 2) {
+        if (q < 0 || q >= n_shards) continue;
+        const ebl_batch* nb = shards[q];
+        const int64_t lo = std::max(g0, nb->row_off), hi = std::min(g1, nb->row_off + static_cast<int64_t>(nb->h));
+        if (hi <= lo) continue;
+        a.peer_out[a.n_peers] = outs[q];
+        a.peer_lo[a.n_peers] = static_cast<int>(lo - b->row_off);
+        a.peer_hi[a.n_peers] = static_cast<int>(hi - b->row_off);
+        a.peer_dst[a.n_peers] = static_cast<int>(lo - nb->row_off);
+        ++a.n_peers;
+      }
+      EBL_CUDA(ebl::launch_step_blocked(a, b->mode, g, b->stream));
+      EBL_CUDA(cudaEventRecord(b->shard_ev[chunk & 1], b->stream));
+    }
+    for (int s = 0; s < n_shards; ++s) {
+      ebl_batch* b = shards[s];
+      b->cur ^= 1;
+      b->step += k;
+      b->launches += 1;
+      b->steps_done += k;
+      b->counts_valid = true;
+    }
+    done += k;
+  }
+  // the last launches' peer rows land before anything else on each shard's stream
+  for (int s = 0; s < n_shards && chunk > 0; ++s) {
+    EBL_CUDA(cudaSetDevice(shards[s]->device));
+    for (int q = s - 1; q <= s + 1; q += 2)
+      if (q >= 0 && q < n_shards)
+        EBL_CUDA(cudaStreamWaitEvent(shards[s]->stream, shards[q]->shard_ev[(chunk - 1) & 1], 0));
+  }
   return EBL_OK;
 }
 

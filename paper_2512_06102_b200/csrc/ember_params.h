@@ -51,6 +51,14 @@ struct StepArgs {
   int force64;
   long long* prof;                // [n_envs][10] phase profile (EBL_PHASE_PROF builds), or null
   int* resume;                    // [n_envs] first step of this launch per env (frontier hand-over), or null
+  // row shards (ebl_shards_step): the layer rows this launch writes back, and up to two peer
+  // layers (a neighbour shard's output buffer, possibly on another GPU over NVLink) that receive
+  // rows [peer_lo, peer_hi) of this layer at their row peer_dst -- the halo exchange fused into
+  // the producing kernel's store
+  int store_lo, store_hi;
+  int n_peers;
+  uint8_t* peer_out[2];
+  int peer_lo[2], peer_hi[2], peer_dst[2];
 };
 
 // Tiling of the blocked kernel (ember_blocked.cu): tiles of tile_h x tile_w cells with

@@ -7,13 +7,17 @@ sharded trajectory is bit-identical to the unsharded one.  A run advances every 
 steps (one launch of the blocked kernel: the halo is exactly the light cone), then swaps
 K boundary rows with each neighbour:
 
-  * single process, G devices (or G shards on one device for testing): `ShardedLandscape`,
-    exchanges with ebl_batch_copy_rows (cudaMemcpyPeerAsync over NVLink between devices);
+  * single process, G devices (or G shards on one device for testing): `ShardedLandscape`;
+    fused=True (default): ebl_shards_step, the exchange fused into the kernels -- each launch
+    stores the rows its neighbours hold as halo straight into their layers (peer stores over
+    NVLink), neighbours ordered by stream events, no host synchronisation; fused=False: a launch
+    per shard then ebl_batch_copy_rows (cudaMemcpyPeerAsync) per halo;
   * one process per GPU: `exchange_halos` on torch.distributed (NCCL send/recv of the K-row
     halo tensors; gloo on CPU in tests).
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -65,10 +69,12 @@ def halo_copies(shards: list[Shard]) -> list[tuple]:
 class ShardedLandscape:
     """C3 driver: G shards on `devices` (default: all on device 0) of one terrain."""
 
-    def __init__(self, terrain: Terrain, n_shards: int, devices=None, halo: int = 8, cfg=None):
+    def __init__(self, terrain: Terrain, n_shards: int, devices=None, halo: int = 8, cfg=None,
+                 fused: bool = True):
         assert terrain.fuel_class.shape[0] == 1, "one landscape"
         _, self.height, self.width = terrain.fuel_class.shape
         self.halo = halo
+        self.fused = fused
         self.shards = plan_shards(self.height, n_shards, halo)
         self.copies = halo_copies(self.shards)
         devices = devices or [0] * n_shards
@@ -83,7 +89,9 @@ class ShardedLandscape:
             check(lib().ebl_batch_set_row_offset(b.handle, g0))
             if g1 - g0 < self.height:  # halo tiles: never more steps per launch than halo rows
                 b.set_tiling(min(64, g1 - g0), min(256, -(-self.width // 32) * 32), halo)
+            check(lib().ebl_batch_set_band(b.handle, sh.band[0] - g0, sh.band[1] - g0))
             self.batches.append(b)
+        self._handles = (C.c_void_p * len(self.batches))(*[b.handle.value for b in self.batches])
 
     def set_state(self, state: np.ndarray) -> None:
         state = np.asarray(state, dtype=np.uint8).reshape(self.height, self.width)
@@ -106,6 +114,9 @@ class ShardedLandscape:
             check(lib().ebl_batch_copy_rows(self.batches[d].handle, drow, self.batches[s].handle, srow, n))
 
     def step(self, n_steps: int) -> None:
+        if self.fused:
+            check(lib().ebl_shards_step(self._handles, len(self.batches), n_steps, self.halo))
+            return
         done = 0
         while done < n_steps:
             k = min(self.halo, n_steps - done) if len(self.batches) > 1 else n_steps - done

@@ -11,8 +11,9 @@ from paper_2512_06102_b200.sharded import ShardedLandscape
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("g,halo", [(1, 8), (2, 8), (3, 4), (4, 8), (5, 2)])
-def test_sharded_equals_unsharded(port, g, halo):
+def test_sharded_equals_unsharded(port, g, halo, fused):
     h, w, steps, seed = 300, 200, 45, 3
     t = eb.synth_terrain(seed, 1, h, w)
     t.wind_speed[:] = 6.0
@@ -25,11 +26,15 @@ def test_sharded_equals_unsharded(port, g, halo):
     full.set_key(seed, 0, first_stream=0)
     full.step(steps)
     want = full.get_state()[0]
-    sh = ShardedLandscape(t, g, halo=halo)
+    sh = ShardedLandscape(t, g, halo=halo, fused=fused)
     sh.set_state(init[0])
     sh.set_key(seed, 0, 0)
-    sh.step(steps)
+    sh.step(steps - 7)
+    sh.step(7)  # a second call continues from the first (halo rows already exchanged)
     got = sh.get_state()
+    counts = sum(b.counts()[0] for b in sh.batches) if fused else None
+    if fused:  # band rows only: the shards' counts add up to the landscape's
+        assert counts[:3].tolist() == [int((want == k).sum()) for k in range(3)]
     assert np.array_equal(got, want), np.argwhere(got != want)[:5]
     gp = O.grid_terrain(port, "port", t.veg()[0], t.den()[0], t.elevation[0], 30.0, 6.0, 0.0)
     assert np.array_equal(want, O.run(port, "port", gp, O.DEFAULT_CFG, seed, 0, 0, steps, init[0]))
