@@ -498,6 +498,8 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
     if (env0 + sub >= a.n_envs) break;
     int32_t cnt3[3] = {0, 0, 0};
     store_tile(Bplane(sub, cur), Xplane(sub), a.out + (env0 + sub) * ncell, cnt3, a.store_lo, a.store_hi, 0);
+    if (a.out2)  // the host's buffer directly (mapped pinned memory): no device -> host copy after the launch
+      store_tile(Bplane(sub, cur), Xplane(sub), a.out2 + (env0 + sub) * ncell, nullptr, a.store_lo, a.store_hi, 0);
     for (int p = 0; p < a.n_peers; ++p)  // fused halo exchange: owned rows straight into the neighbour
       store_tile(Bplane(sub, cur), Xplane(sub), a.peer_out[p], nullptr,
                  a.peer_lo[p], a.peer_hi[p], a.peer_dst[p] - a.peer_lo[p]);

@@ -290,6 +290,7 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
   if (a.counts) a.counts += o * 4;
   if (a.prof) a.prof += o * 10;
   if (a.resume) a.resume += o;
+  if (a.out2) a.out2 += o * b->ncell;
   if (a.tab_stride) {
     a.pot += o * a.tab_stride * 8;
     a.gamma += o * a.tab_stride;
@@ -961,17 +962,38 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
   EBL_CUDA(cudaEventRecord(b->pipe_ev_start, b->stream));
   EBL_CUDA(cudaStreamWaitEvent(b->pipe_in, b->pipe_ev_start, 0));
   for (int c = 0; c < chunks; ++c) EBL_CUDA(cudaStreamWaitEvent(b->pipe_comp[c], b->pipe_ev_start, 0));
-  const int per = (b->n_envs + chunks - 1) / chunks;
+  // chunk boundaries: decreasing sizes (the first chunks start computing early; the last ones,
+  // whose copies finish last, are small), weights chunks, chunks-1, ..., 1
+  std::vector<int> bound(chunks + 1, 0);
+  {
+    const double tot = 0.5 * chunks * (chunks + 1);
+    double acc = 0.0;
+    for (int c = 0; c < chunks; ++c) {
+      acc += chunks - c;
+      bound[c + 1] = std::min(b->n_envs, static_cast<int>(std::lround(acc / tot * b->n_envs)));
+    }
+    bound[chunks] = b->n_envs;
+  }
+  // the final layers straight into the caller's buffer when it is mapped pinned memory: each CTA
+  // writes its env as it finishes, no device -> host copy after the chunk's launch
+  uint8_t* host_dev = nullptr;
+  if (!frontier) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, final_states) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+      host_dev = static_cast<uint8_t*>(pa.devicePointer);
+    cudaGetLastError();
+  }
+  a.out2 = host_dev;
   for (int c = 0; c < chunks; ++c) {
-    const int off = c * per, n = std::min(per, b->n_envs - off);
-    if (n <= 0) break;
+    const int off = bound[c], n = bound[c + 1] - off;
+    if (n <= 0) continue;
     const size_t bytes = static_cast<size_t>(n) * b->ncell, boff = static_cast<size_t>(off) * b->ncell;
     EBL_CUDA(cudaMemcpyAsync(b->state[b->cur].p + boff, initial + boff, bytes, cudaMemcpyHostToDevice, b->pipe_in));
     EBL_CUDA(cudaEventRecord(b->pipe_ev_in[c], b->pipe_in));
   }
   for (int c = 0; c < chunks; ++c) {
-    const int off = c * per, n = std::min(per, b->n_envs - off);
-    if (n <= 0) break;
+    const int off = bound[c], n = bound[c + 1] - off;
+    if (n <= 0) continue;
     cudaStream_t s = b->pipe_comp[c];
     EBL_CUDA(cudaStreamWaitEvent(s, b->pipe_ev_in[c], 0));
     EBL_CUDA(cudaMemsetAsync(b->counts.p + static_cast<size_t>(off) * 4, 0, static_cast<size_t>(n) * 4 * sizeof(int32_t), s));
@@ -980,12 +1002,13 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
     EBL_CUDA(cudaEventRecord(b->pipe_ev_done[c], s));
   }
   for (int c = 0; c < chunks; ++c) {
-    const int off = c * per, n = std::min(per, b->n_envs - off);
-    if (n <= 0) break;
+    const int off = bound[c], n = bound[c + 1] - off;
+    if (n <= 0) continue;
     const size_t bytes = static_cast<size_t>(n) * b->ncell, boff = static_cast<size_t>(off) * b->ncell;
     EBL_CUDA(cudaStreamWaitEvent(b->pipe_out, b->pipe_ev_done[c], 0));
-    EBL_CUDA(cudaMemcpyAsync(final_states + boff, b->state[b->cur ^ 1].p + boff, bytes, cudaMemcpyDeviceToHost,
-                             b->pipe_out));
+    if (!host_dev)
+      EBL_CUDA(cudaMemcpyAsync(final_states + boff, b->state[b->cur ^ 1].p + boff, bytes, cudaMemcpyDeviceToHost,
+                               b->pipe_out));
   }
   EBL_CUDA(cudaEventRecord(b->pipe_ev_end, b->pipe_out));
   EBL_CUDA(cudaStreamWaitEvent(b->stream, b->pipe_ev_end, 0));  // later batch work follows the run

@@ -51,6 +51,7 @@ struct StepArgs {
   int force64;
   long long* prof;                // [n_envs][10] phase profile (EBL_PHASE_PROF builds), or null
   int* resume;                    // [n_envs] first step of this launch per env (frontier hand-over), or null
+  uint8_t* out2;                  // [n_envs][h*w] second copy of the output (e.g. mapped pinned host memory), or null
   // row shards (ebl_shards_step): the layer rows this launch writes back, and up to two peer
   // layers (a neighbour shard's output buffer, possibly on another GPU over NVLink) that receive
   // rows [peer_lo, peer_hi) of this layer at their row peer_dst -- the halo exchange fused into

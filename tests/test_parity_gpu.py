@@ -493,3 +493,27 @@ def test_frontier_handover_vs_blocked_and_oracle(port, case):
         g = O.grid_terrain(port, "port", t.veg()[e], t.den()[e], t.elevation[e], 30.0,
                            t.wind_speed[e], t.wind_direction[e])
         assert np.array_equal(f[0][e], O.run(port, "port", g, c, seed, 0, e, steps, init[e]))
+
+
+@pytest.mark.parametrize("chunks", [0, 3, 8])
+def test_pipelined_run_pinned_zero_copy(chunks):
+    """ebl_batch_run with pinned host buffers: the kernels write the final layers straight into
+    the mapped output buffer (no device -> host copy); identical to the sequence."""
+    import torch
+    n_envs, h, w, steps, seed = 37, 128, 128, 50, 4
+    t = eb.synth_terrain(seed, n_envs, h, w)
+    init = eb.synth_ignitions(seed, t, 5)
+    with eb.Batch(n_envs, h, w) as b:
+        b.set_terrain(t.fuel_class, t.elevation, t.class_veg, t.class_den, 30.0)
+        b.set_wind(t.wind_speed, t.wind_direction)
+        b.set_key(seed, 0)
+        b.set_state(init)
+        b.step(steps)
+        want = b.get_state()
+        h_in = torch.from_numpy(init.copy()).pin_memory()
+        h_out = torch.full_like(h_in, 9).pin_memory()
+        b.set_pipeline(chunks)
+        b.set_key(seed, 0)
+        eb._lib.check(eb.lib().ebl_batch_run(b.handle, h_in.data_ptr(), steps, h_out.data_ptr()))
+        assert np.array_equal(h_out.numpy(), want)
+        assert np.array_equal(b.get_state(), want)  # the device copy is kept as well
