@@ -1,0 +1,317 @@
+// Warp-local resident kernel: whole env per CTA, all steps fused, ONE block barrier per step.
+//
+// Same transition as k_step_blocked (engine.cpp:12-38, next_fire_cell) and the same bit-planes
+// (B double-buffered with zero padding rows, X), but no CTA-wide active list: rows are dealt to
+// warps interleaved (block rb, lane l of warp w owns row rb + 4l + w, so a front spanning a few
+// rows is shared by all four warps), and each warp decides the active cells of its own rows:
+//   dense   per lane, its row: 8-neighbour dilation of B, Bn = B, act = (Unburned & any) | B
+//           (stored to the lane's ACT row), cnt = popc(act);
+//   warp    inclusive scan of cnt; pass p: lane l takes the warp's active cell p*32 + l, finds
+//           the owning lane by a 5-step shuffle search of the exclusive counts and the bit by
+//           popc over that row's ACT words + fns; decides it (survive test / slope-table lambda
+//           with the fp64 guard, ember_device.cuh) and updates Bn / X of that row (only this
+//           warp writes those words in this step);
+//   --- one barrier ---, swap B / Bn.
+// The pooled list of k_step_blocked costs a barrier and a per-bit list build per step; here a
+// warp only waits for itself until the end of the step.  Bit-identical results (decisions are
+// per cell; the RNG is counter-based).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ember_bits.cuh"
+#include "ember_device.cuh"
+#include "ember_kernels.h"
+#include "ember_params.h"
+
+namespace ebl {
+
+namespace {
+
+constexpr int kWpThreads = 128;  // 4 warps
+
+template <int MODE, int WPRC>
+__global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_steps) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int32_t s_cnt[3];
+  __shared__ int32_t s_newly;
+  __shared__ uint64_t s_prefix[128];  // rng key prefixes, slot t & 127, refilled 64 steps at a time
+  constexpr bool kTer = MODE == kStaticTerrain;
+  __shared__ float s_pal[kTer ? 512 : 1];
+  __shared__ float s_kw[8];
+  __shared__ float s_srckw[kTer ? 32 * 8 : 1];
+
+  const int env = blockIdx.x;
+  const int H = a.h, W = a.w;
+  const int wpr = WPRC ? WPRC : (W + 31) >> 5;
+  const int S = plane_stride(wpr);
+  // plane row R starts at word R*S + (R >> 2): the 32 lanes of a warp own rows 4 apart, and the
+  // extra word every 4 rows makes their stride 4S+1 (odd) -> 32 distinct banks
+  auto ro = [S](int R) { return R * S + (R >> 2); };
+  const int PH = ro(H + 2) + 1;  // words of a B plane (H + 2 rows)
+  uint32_t* const Bp0 = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* const Bp1 = Bp0 + PH;
+  uint32_t* const X = Bp1 + PH;
+  uint32_t* const ACT = X + PH;
+  const size_t ncell = static_cast<size_t>(H) * W;
+  const bool vec = (W & 15) == 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t last_mask = low_mask(W - 32 * (wpr - 1));
+
+  // ---- load ----------------------------------------------------------------------------------
+  for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
+    Bp0[i] = Bp1[i] = 0u;
+    Bp0[ro(H + 1) + i] = Bp1[ro(H + 1) + i] = 0u;
+  }
+  const uint8_t* __restrict__ in = a.in + env * ncell;
+  for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
+    const int nc = min(32, W - 32 * it.j);
+    uint32_t b = 0u, x = 0u;
+    const uint8_t* src = in + static_cast<size_t>(it.r) * W + 32 * it.j;
+    if (nc == 32 && vec) {
+      bytes_to_bits(src, b, x);
+    } else {
+      for (int k = 0; k < nc; ++k) {
+        const uint8_t v = src[k];
+        b |= static_cast<uint32_t>(v == 1) << k;
+        x |= static_cast<uint32_t>(v == 2) << k;
+      }
+    }
+    Bp0[ro(it.r + 1) + it.j] = b;
+    X[ro(it.r) + it.j] = x;
+  }
+  const bool use_rec = kTer && a.nfuel && a.n_pal <= 32;
+  auto load_wind = [&](int srow) {  // kappa_wind of the wind in force (+ the src * kappa_wind table)
+    if constexpr (kTer) {
+      if (threadIdx.x < 8)
+        s_kw[threadIdx.x] = __ldg(a.kw32 + static_cast<size_t>(srow) * a.kw_sched_stride +
+                                  static_cast<size_t>(env) * a.kw_stride + threadIdx.x);
+      if (use_rec)
+        for (int i = threadIdx.x; i < a.n_pal * 8; i += blockDim.x)
+          s_srckw[i] = __ldg(a.pal32 + (i >> 3)) *
+                       __ldg(a.kw32 + static_cast<size_t>(srow) * a.kw_sched_stride +
+                             static_cast<size_t>(env) * a.kw_stride + (i & 7));
+    }
+  };
+  if constexpr (kTer)
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) s_pal[i] = __ldg(a.pal32 + i);
+  load_wind(sched_row(a, a.step));
+  if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_newly = 0;
+  const uint64_t stream = a.streams[env];
+  for (int k = threadIdx.x; k < 64; k += blockDim.x) s_prefix[k] = key_prefix(a.seed, stream, a.step + k);
+  __syncthreads();
+
+  const DiagCounters dg{a.diag};
+  const uint64_t gbase = static_cast<uint64_t>(a.row_off) * W;
+  auto win3 = [&](const uint32_t* row, int j, int b) -> uint32_t {  // columns c-1, c, c+1 -> bits 0..2
+    const uint32_t wj = row[j];
+    uint32_t v = b > 0 ? wj >> (b - 1) : ((j > 0 ? row[j - 1] >> 31 : 0u) | (wj << 1));
+    if (b == 31) v = (v & 3u) | ((j + 1 < wpr ? row[j + 1] & 1u : 0u) << 2);
+    return v & 7u;
+  };
+
+  int cur = 0;
+  int newly = 0;
+  for (int t = 0; t < n_steps; ++t) {
+    const uint32_t* B = cur ? Bp1 : Bp0;
+    uint32_t* Bn = cur ? Bp0 : Bp1;
+    const int srow = sched_row(a, a.step + static_cast<uint64_t>(t));
+    if (t > 0 && a.sched_len > 1) {  // CTA-uniform: time-varying wind
+      load_wind(srow);
+      __syncthreads();
+    }
+    const uint64_t prefix = s_prefix[t & 127];
+    const bool last = t == n_steps - 1;
+    for (int rb = 0; rb < H; rb += kWpThreads) {
+      // ---- dense pass over the lane's row ------------------------------------------------------
+      const int r = rb + 4 * lane + warp;
+      int cnt = 0;
+      if (r < H) {
+        const uint32_t* up = B + ro(r + 2);
+        const uint32_t* mid = B + ro(r + 1);
+        const uint32_t* dn = B + ro(r);
+        uint32_t* bn = Bn + ro(r + 1);
+        const uint32_t* xr = X + ro(r);
+        uint32_t* ar = ACT + ro(r);
+        uint32_t vl = 0u;
+        uint32_t uc = up[0], mc = mid[0], dc = dn[0];
+        uint32_t vc = uc | mc | dc;
+#pragma unroll 4
+        for (int j = 0; j < wpr; ++j) {
+          uint32_t un = 0u, mn = 0u, dnn = 0u;
+          if (j + 1 < wpr) {
+            un = up[j + 1];
+            mn = mid[j + 1];
+            dnn = dn[j + 1];
+          }
+          const uint32_t vn = un | mn | dnn;
+          const uint32_t any = ((vc << 1) | (vl >> 31)) | ((vc >> 1) | (vn << 31)) | uc | dc;
+          bn[j] = mc;
+          const uint32_t valid = j + 1 < wpr ? 0xffffffffu : last_mask;
+          const uint32_t act = ((~(mc | xr[j]) & valid) & any) | mc;
+          ar[j] = act;
+          cnt += __popc(act);
+          vl = vc;
+          vc = vn;
+          uc = un;
+          mc = mn;
+          dc = dnn;
+        }
+      }
+      if (!__ballot_sync(0xffffffffu, cnt > 0)) continue;  // quiet rows of this warp
+      __syncwarp();  // ACT / Bn rows of the warp visible to all its lanes
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int excl = incl - cnt;
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      // ---- this warp's active cells, 32 per pass ----------------------------------------------------
+      for (int p = 0; p < total; p += 32) {
+        const int idx = p + lane;
+        int L = 0;  // the last lane whose exclusive count is <= idx (counts are non-decreasing)
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+          const int cand = L + st;
+          const int v = __shfl_sync(0xffffffffu, excl, cand & 31);
+          if (cand < 32 && v <= idx) L = cand;
+        }
+        int q = idx - __shfl_sync(0xffffffffu, excl, L);
+        if (idx >= total) continue;
+        const int rr = rb + 4 * L + warp;
+        const uint32_t* ar = ACT + ro(rr);
+        int jj = 0;
+        uint32_t wv = ar[0];
+        for (;;) {  // the word holding the q-th active cell of row rr
+          const int pc = __popc(wv);
+          if (q < pc) break;
+          q -= pc;
+          wv = ar[++jj];
+        }
+        const int cc = 32 * jj + static_cast<int>(__fns(wv, 0u, q + 1));
+        // ---- decide (engine.cpp:12-26) ----
+        const int j = cc >> 5, b = cc & 31;
+        const uint32_t bit = 1u << b;
+        const int wi = ro(rr + 1) + j;
+        const uint64_t m = cell_bits53(prefix, gbase + static_cast<uint64_t>(rr) * W + cc, 0);
+        const uint32_t midw = win3(B + ro(rr + 1), j, b);
+        if (midw & 2u) {  // Burning: u < p_continue, integer form
+          if (m >= a.pc_thr) {
+            atomicAnd(Bn + wi, ~bit);
+            atomicOr(X + ro(rr) + j, bit);
+          }
+        } else {  // Unburned with a burning neighbour
+          const uint32_t dnw = win3(B + ro(rr), j, b), upw = win3(B + ro(rr + 2), j, b);
+          const uint32_t nb = (midw & 1u) | (dnw << 1) | ((midw >> 2) << 4) | ((upw >> 2) << 5) |
+                              ((upw & 2u) << 5) | ((upw & 1u) << 7);
+          bool ig;
+          if (use_rec)
+            ig = ignite_terrain_rec(terrain_view(a, env, srow), a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
+                                    a.nfuel + static_cast<size_t>(env) * a.ter_stride, s_srckw, s_pal + 256,
+                                    a.alpha_s_l2, W, rr, cc, nb, m, dg);
+          else if constexpr (kTer)
+            ig = ignite_terrain_tab(terrain_view(a, env, srow), a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
+                                    s_pal, s_kw, W, H, rr, cc, nb, m, dg);
+          else
+            ig = ignite<MODE>(a, env, rr, cc, nb, m, dg, srow);
+          if (ig) {
+            atomicOr(Bn + wi, bit);
+            newly += last;
+          }
+        }
+      }
+    }
+    if (((t & 63) == 63) && t + 1 < n_steps) {  // refill the prefix ring with steps t+1 .. t+64
+      for (int k = threadIdx.x; k < 64; k += blockDim.x)
+        s_prefix[(t + 1 + k) & 127] = key_prefix(a.seed, stream, a.step + static_cast<uint64_t>(t + 1 + k));
+    }
+    __syncthreads();  // Bn / X complete: the next step reads them
+    cur ^= 1;
+    if (a.traj) {  // record (run_stochastic(record=true), engine.cpp:116): the layer after this step
+      const uint32_t* Bs = cur ? Bp1 : Bp0;
+      uint8_t* dst = a.traj + ((a.traj_t0 + t) * a.n_envs + env) * ncell;
+      for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
+        const uint32_t bb = Bs[ro(it.r + 1) + it.j], xx = X[ro(it.r) + it.j];
+        uint8_t* o = dst + static_cast<size_t>(it.r) * W + 32 * it.j;
+        const int nc = min(32, W - 32 * it.j);
+        if (nc == 32 && vec) bits_to_bytes(bb, xx, o);
+        else
+          for (int k = 0; k < nc; ++k) o[k] = static_cast<uint8_t>(((bb >> k) & 1u) | (((xx >> k) & 1u) << 1));
+      }
+    }
+  }
+
+  // ---- store + counts ----------------------------------------------------------------------------
+  const uint32_t* Bs = cur ? Bp1 : Bp0;
+  int cu = 0, cb = 0, cx = 0;
+  for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
+    const uint32_t bb = Bs[ro(it.r + 1) + it.j], xx = X[ro(it.r) + it.j];
+    const int nc = min(32, W - 32 * it.j);
+    cu += nc - __popc(bb) - __popc(xx);
+    cb += __popc(bb);
+    cx += __popc(xx);
+    for (int o = 0; o < 2; ++o) {
+      uint8_t* base = o == 0 ? a.out : a.out2;
+      if (!base) continue;
+      uint8_t* dst = base + env * ncell + static_cast<size_t>(it.r) * W + 32 * it.j;
+      if (nc == 32 && vec) bits_to_bytes(bb, xx, dst);
+      else
+        for (int k = 0; k < nc; ++k) dst[k] = static_cast<uint8_t>(((bb >> k) & 1u) | (((xx >> k) & 1u) << 1));
+    }
+  }
+  if (!a.counts) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    cu += __shfl_xor_sync(0xffffffffu, cu, o);
+    cb += __shfl_xor_sync(0xffffffffu, cb, o);
+    cx += __shfl_xor_sync(0xffffffffu, cx, o);
+    newly += __shfl_xor_sync(0xffffffffu, newly, o);
+  }
+  if (lane == 0) {
+    atomicAdd(&s_cnt[0], cu);
+    atomicAdd(&s_cnt[1], cb);
+    atomicAdd(&s_cnt[2], cx);
+    atomicAdd(&s_newly, newly);
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) atomicAdd(a.counts + env * 4 + threadIdx.x, s_cnt[threadIdx.x]);
+  if (threadIdx.x == 3) atomicAdd(a.counts + env * 4 + 3, s_newly);
+}
+
+template <int MODE, int WPRC>
+cudaError_t launch_wp(const StepArgs& a, int n_steps, size_t sm, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k_step_warp<MODE, WPRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sm));
+  if (e != cudaSuccess) return e;
+  k_step_warp<MODE, WPRC><<<a.n_envs, kWpThreads, sm, s>>>(a, n_steps);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t warp_smem_bytes(int h, int w) {
+  const size_t S = plane_stride((w + 31) / 32);
+  const size_t R = static_cast<size_t>(h) + 2;
+  return 4 * (R * S + (R >> 2) + 1) * sizeof(uint32_t);  // B x2, X, ACT (ro() layout, ember_warp.cu)
+}
+
+bool warp_fits(int h, int w) {
+  return static_cast<size_t>(h) * w <= 65536 && warp_smem_bytes(h, w) <= kResMaxSmem;
+}
+
+cudaError_t launch_step_warp(const StepArgs& a, int mode, int n_steps, cudaStream_t s) {
+  const size_t sm = warp_smem_bytes(a.h, a.w);
+  const int wpr = (a.w + 31) / 32;
+  if (mode == kStaticTables)
+    return wpr == 4 ? launch_wp<kStaticTables, 4>(a, n_steps, sm, s)
+                    : (wpr == 2 ? launch_wp<kStaticTables, 2>(a, n_steps, sm, s)
+                                : launch_wp<kStaticTables, 0>(a, n_steps, sm, s));
+  return wpr == 4 ? launch_wp<kStaticTerrain, 4>(a, n_steps, sm, s)
+                  : (wpr == 2 ? launch_wp<kStaticTerrain, 2>(a, n_steps, sm, s)
+                              : launch_wp<kStaticTerrain, 0>(a, n_steps, sm, s));
+}
+
+}  // namespace ebl

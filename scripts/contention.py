@@ -10,6 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_06102_b200 as eb  # noqa: E402
 
 N, H, W, STEPS = 1024, 128, 128, 200
+KERNEL = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # ebl kernel id (0 auto, 5 frontier, 6 warp)
 t = eb.synth_terrain(0, N, H, W)
 init = eb.synth_ignitions(0, t, 5)
 
@@ -19,6 +20,7 @@ def run(idx, reps=4):
     b = eb.Batch(n, H, W)
     b.set_terrain(t.fuel_class[idx], t.elevation[idx], t.class_veg, t.class_den, 30.0)
     b.set_wind(t.wind_speed[idx], t.wind_direction[idx])
+    b.set_kernel(KERNEL)
     ms = []
     for i in range(reps + 1):
         b.set_state(init[idx])
