@@ -20,7 +20,7 @@
 namespace ebl {
 
 template <int MODE>
-__global__ void __launch_bounds__(kRlBitsThreads) k_rl_tanker_bits(RlArgs g) {
+__global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_bits(RlArgs g) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_total[2], s_newly[2], s_burn[2];
   __shared__ int s_action, s_placed;
