@@ -217,6 +217,10 @@ int ebl_batch_counts(ebl_batch* b, int32_t* out);
 /* Per-cell arrival intensity and ignition probability of the current state
  * (kernel.hpp:53-78, the fp32 fast path): lambda/p [n_envs][H*W] float. */
 int ebl_batch_intensity(ebl_batch* b, float* lambda, float* p);
+/* The same probe for one fp32 form of the terrain path: record_form = 1 the slope / source-class
+ * record form the resident kernels use (the ebl_batch_intensity default when the palette has <= 32
+ * classes), 0 the on-the-fly form from the elevation layer (halo tiles, tiled kernel). */
+int ebl_batch_intensity_form(ebl_batch* b, int record_form, float* lambda, float* p);
 
 /* Diagnostics since the last reset: [0] draws decided in the fp64 guard band,
  * [1] draws within 1e-12 of their fp64 threshold ("ambiguous": a flip vs the

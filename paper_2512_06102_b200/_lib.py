@@ -113,6 +113,7 @@ SIGNATURES = {
     "ebl_batch_step_index": (_U64, [_P]),
     "ebl_step_batch": (_I, [_P, _I]),
     "ebl_batch_run": (_I, [_P, _P, _I, _P]),
+    "ebl_batch_intensity_form": (_I, [_P, _I, _P, _P]),
     "ebl_batch_set_band": (_I, [_P, _I, _I]),
     "ebl_shards_step": (_I, [_P, _I, _I, _I]),
     "ebl_batch_set_profiling": (_I, [_P, _I]),

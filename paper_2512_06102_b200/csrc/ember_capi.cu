@@ -1242,6 +1242,10 @@ int ebl_batch_counts(ebl_batch* b, int32_t* out) {
 }
 
 int ebl_batch_intensity(ebl_batch* b, float* lambda, float* p) {
+  return ebl_batch_intensity_form(b, 1, lambda, p);
+}
+
+int ebl_batch_intensity_form(ebl_batch* b, int record_form, float* lambda, float* p) {
   if (int e = check_batch(b)) return e;
   if (int e = prepare(b)) return e;
   const size_t total = b->ncell * b->n_envs;
@@ -1249,6 +1253,7 @@ int ebl_batch_intensity(ebl_batch* b, float* lambda, float* p) {
   EBL_CUDA(dl.alloc(total));
   EBL_CUDA(dp.alloc(total));
   ebl::StepArgs a = step_args(b);
+  a.rec_probe = record_form;
   EBL_CUDA(ebl::launch_intensity(a, b->mode, dl.p, dp.p, b->stream));
   EBL_CUDA(cudaMemcpyAsync(lambda, dl.p, total * sizeof(float), cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaMemcpyAsync(p, dp.p, total * sizeof(float), cudaMemcpyDeviceToHost, b->stream));

@@ -122,7 +122,16 @@ __global__ void k_intensity(StepArgs a, float* lam_out, float* p_out) {
       p = static_cast<float>(__dsub_rn(1.0, exp(-__dmul_rn(a.gamma[base + i], l))));
     } else {
       const TerrainView t = terrain_view(a, env, sched_row(a, a.step));
-      lam = terrain_lambda32(t, a.w, r, c, nb);
+      if (a.nfuel && a.slope32 && a.n_pal <= 32 && a.rec_probe) {
+        // the resident kernels' form (ember_device.cuh terrain_lambda32_rec): slope + source-class
+        // records, src32 * kappa_wind32 products, 2^(alpha_s log2e S)
+        float srckw[32 * 8];
+        for (int q = 0; q < a.n_pal * 8; ++q) srckw[q] = t.pal_src32[q >> 3] * t.kw32[q & 7];
+        lam = terrain_lambda32_rec(a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
+                                   a.nfuel + static_cast<size_t>(env) * a.ter_stride, srckw, a.alpha_s_l2, i, nb);
+      } else {
+        lam = terrain_lambda32(t, a.w, r, c, nb);
+      }
       p = -expm1f(-t.pal_gam32[t.fuel[i]] * lam);
     }
     lam_out[g] = lam;

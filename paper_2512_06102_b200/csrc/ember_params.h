@@ -33,6 +33,7 @@ struct StepArgs {
   const uint2* nfuel;             // [grid][h*w] fuel classes of the 8 sources u_k = v - d_k (bytes k)
   int n_pal;                      // palette entries in use (terrain form)
   float alpha_s_l2;               // alpha_s * log2(e): kappa_slope = 2^(alpha_s_l2 * S)
+  int rec_probe;                  // k_intensity: report the record form (1) or the elevation form (0)
   size_t ter_stride;
   const float* pal32;             // [2][256] src32, gam32
   const double* pal64;            // [2][256] src64, gam64

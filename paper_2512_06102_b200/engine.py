@@ -235,10 +235,12 @@ class Batch:
         c = self.counts()[:, :3].astype(np.float64)
         return c / float(self.height * self.width)
 
-    def intensity(self):
+    def intensity(self, record_form: bool = True):
+        """lambda and p_ignite (fp32) of the current layers; record_form: the slope-record form of
+        the resident kernels, else the on-the-fly elevation form (terrain layers)."""
         lam = np.empty((self.n_envs, self.height, self.width), dtype=np.float32)
         p = np.empty_like(lam)
-        check(lib().ebl_batch_intensity(self._h, _ptr(lam), _ptr(p)))
+        check(lib().ebl_batch_intensity_form(self._h, int(record_form), _ptr(lam), _ptr(p)))
         return lam, p
 
     # -- deterministic mode (engine.hpp:147-245) + reverse-mode gradient (C4) ----------------

@@ -157,19 +157,20 @@ def test_intensity_fp32_within_1e5(port):
         b.set_key(5, 0)
         b.step(30)
         st = b.get_state()
-        lam, p = b.intensity()
         c = O.DEFAULT_CFG if cfg is None else cfg
-        checked = 0
-        for e in range(n):
-            g = O.grid_terrain(port, "port", t.veg()[e], t.den()[e], t.elevation[e], 30.0,
-                               t.wind_speed[e], t.wind_direction[e])
-            lw, pw = O.intensity(port, "port", g, c, st[e])
-            m = lw > 0
-            checked += int(m.sum())
-            np.testing.assert_allclose(lam[e][m], lw[m], rtol=REL_TOL)
-            np.testing.assert_allclose(p[e][m], pw[m], rtol=REL_TOL, atol=1e-30)
-            assert (lam[e][~m] == 0).all() and (p[e][~m] == 0).all()
-        assert checked > 100, "fronts must be alive to test lambda/p"
+        for form in (True, False):  # slope-record form (resident kernels) and elevation form
+            lam, p = b.intensity(record_form=form)
+            checked = 0
+            for e in range(n):
+                g = O.grid_terrain(port, "port", t.veg()[e], t.den()[e], t.elevation[e], 30.0,
+                                   t.wind_speed[e], t.wind_direction[e])
+                lw, pw = O.intensity(port, "port", g, c, st[e])
+                m = lw > 0
+                checked += int(m.sum())
+                np.testing.assert_allclose(lam[e][m], lw[m], rtol=REL_TOL)
+                np.testing.assert_allclose(p[e][m], pw[m], rtol=REL_TOL, atol=1e-30)
+                assert (lam[e][~m] == 0).all() and (p[e][~m] == 0).all()
+            assert checked > 100, "fronts must be alive to test lambda/p"
 
 
 @pytest.mark.parametrize("h,w", [(1, 1), (1, 37), (45, 1), (3, 3), (31, 33), (64, 96), (200, 100),
