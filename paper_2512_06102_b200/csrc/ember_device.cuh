@@ -240,6 +240,48 @@ __device__ __forceinline__ bool ignite_terrain_tab(const TerrainView& t, const f
   return u < p;
 }
 
+// The same decision with the candidate's records already loaded (loads hoisted by the caller).
+struct CellRec {
+  float4 s0, s1;
+  uint2 nf;
+  uint32_t fv;
+};
+__device__ __forceinline__ CellRec load_rec(const float* __restrict__ slope32, const uint2* __restrict__ nfuel,
+                                            const uint8_t* __restrict__ fuel, int v) {
+  CellRec c;
+  c.s0 = __ldg(reinterpret_cast<const float4*>(slope32) + 2 * v);
+  c.s1 = __ldg(reinterpret_cast<const float4*>(slope32) + 2 * v + 1);
+  c.nf = __ldg(nfuel + v);
+  c.fv = __ldg(fuel + v);
+  return c;
+}
+__device__ __forceinline__ bool ignite_terrain_rec_pre(const TerrainView& t, const CellRec& rc, const float* srckw,
+                                                       const float* pal_gam, float alpha_l2, int w, int r, int c,
+                                                       uint32_t nb, uint64_t m, const DiagCounters& dg) {
+  const double u = bits_to_uniform(m);
+  if (!t.force64) {
+    const float s[8] = {rc.s0.x, rc.s0.y, rc.s0.z, rc.s0.w, rc.s1.x, rc.s1.y, rc.s1.z, rc.s1.w};
+    float lam = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t f = ((k < 4 ? rc.nf.x : rc.nf.y) >> (8 * (k & 3))) & 0xffu;
+      const float contrib = srckw[f * 8 + k] * ex2_approx(alpha_l2 * s[k]);
+      lam += (nb >> k) & 1u ? contrib : 0.f;
+    }
+    const float x = pal_gam[rc.fv] * lam;
+    if (x == 0.f) return false;  // gamma or lambda exactly 0: p = 1 - exp(-0) = 0, u < 0 is false
+    const double p32 = static_cast<double>(-expm1f(-x));
+    if (p32 > 1e-12) {
+      if (u < p32 * (1.0 - kGuardRel)) return true;
+      if (u >= p32 * (1.0 + kGuardRel)) return false;
+    }
+  }
+  dg.fallback();
+  const double p = terrain_p64(t, w, r, c, nb);
+  if (fabs(u - p) < kAmbiguousBand) dg.ambiguous();
+  return u < p;
+}
+
 // ignite_terrain over terrain_lambda32_rec (blocked / tanker kernels when the palette has <= 32
 // classes); pal_gam: the palette's fp32 gamma values (shared memory).
 __device__ __forceinline__ bool ignite_terrain_rec(const TerrainView& t, const float* slope32, const uint2* nfuel,

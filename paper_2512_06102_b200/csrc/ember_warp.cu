@@ -24,11 +24,17 @@
 #include "ember_kernels.h"
 #include "ember_params.h"
 
+#ifndef EBL_PHASE_PROF
+#define EBL_PHASE_PROF 0
+#endif
+
 namespace ebl {
 
 namespace {
 
 constexpr int kWpThreads = 128;  // 4 warps
+
+__device__ __forceinline__ long long pw_wait_dummy(long long v) { return v; }
 
 template <int MODE, int WPRC>
 __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_steps) {
@@ -113,7 +119,16 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
 
   int cur = 0;
   int newly = 0;
+#if EBL_PHASE_PROF
+  // per warp (lane 0): dense-pass cycles, decide-pass cycles, passes, cells; CTA: step cycles
+  long long pw_dense = 0, pw_dec = 0, pw_pass = 0, pw_cells = 0, pw_t0 = 0, p_step = 0, p_wait = 0;
+  __shared__ long long s_wd[4][4];
+#endif
   for (int t = 0; t < n_steps; ++t) {
+#if EBL_PHASE_PROF
+    const long long st0 = clock64();
+    pw_t0 = st0;
+#endif
     const uint32_t* B = cur ? Bp1 : Bp0;
     uint32_t* Bn = cur ? Bp0 : Bp1;
     const int srow = sched_row(a, a.step + static_cast<uint64_t>(t));
@@ -159,6 +174,13 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
           dc = dnn;
         }
       }
+#if EBL_PHASE_PROF
+      if (lane == 0) {
+        const long long c = clock64();
+        pw_dense += c - pw_t0;
+        pw_t0 = c;
+      }
+#endif
       if (!__ballot_sync(0xffffffffu, cnt > 0)) continue;  // quiet rows of this warp
       __syncwarp();  // ACT / Bn rows of the warp visible to all its lanes
       int incl = cnt;
@@ -170,6 +192,12 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
       const int excl = incl - cnt;
       const int total = __shfl_sync(0xffffffffu, incl, 31);
       // ---- this warp's active cells, 32 per pass ----------------------------------------------------
+#if EBL_PHASE_PROF
+      if (lane == 0) {
+        pw_pass += (total + 31) / 32;
+        pw_cells += total;
+      }
+#endif
       for (int p = 0; p < total; p += 32) {
         const int idx = p + lane;
         int L = 0;  // the last lane whose exclusive count is <= idx (counts are non-decreasing)
@@ -192,6 +220,13 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
           wv = ar[++jj];
         }
         const int cc = 32 * jj + static_cast<int>(__fns(wv, 0u, q + 1));
+        // the candidate records are requested first (burning cells waste one), so their latency
+        // overlaps the RNG rounds and the neighbour masks below
+        CellRec rec{};
+        if (use_rec)
+          rec = load_rec(a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
+                         a.nfuel + static_cast<size_t>(env) * a.ter_stride, a.fuel + static_cast<size_t>(env) * a.ter_stride,
+                         rr * W + cc);
         // ---- decide (engine.cpp:12-26) ----
         const int j = cc >> 5, b = cc & 31;
         const uint32_t bit = 1u << b;
@@ -209,9 +244,8 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
                               ((upw & 2u) << 5) | ((upw & 1u) << 7);
           bool ig;
           if (use_rec)
-            ig = ignite_terrain_rec(terrain_view(a, env, srow), a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
-                                    a.nfuel + static_cast<size_t>(env) * a.ter_stride, s_srckw, s_pal + 256,
-                                    a.alpha_s_l2, W, rr, cc, nb, m, dg);
+            ig = ignite_terrain_rec_pre(terrain_view(a, env, srow), rec, s_srckw, s_pal + 256, a.alpha_s_l2, W, rr, cc,
+                                        nb, m, dg);
           else if constexpr (kTer)
             ig = ignite_terrain_tab(terrain_view(a, env, srow), a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
                                     s_pal, s_kw, W, H, rr, cc, nb, m, dg);
@@ -228,7 +262,19 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
       for (int k = threadIdx.x; k < 64; k += blockDim.x)
         s_prefix[(t + 1 + k) & 127] = key_prefix(a.seed, stream, a.step + static_cast<uint64_t>(t + 1 + k));
     }
+#if EBL_PHASE_PROF
+    __syncwarp();
+    if (lane == 0) {
+      const long long c = clock64();
+      pw_dec += c - pw_t0;
+      pw_t0 = c;
+    }
+#endif
     __syncthreads();  // Bn / X complete: the next step reads them
+#if EBL_PHASE_PROF
+    if (lane == 0) p_wait += clock64() - pw_t0;
+    if (threadIdx.x == 0) p_step += clock64() - st0;
+#endif
     cur ^= 1;
     if (a.traj) {  // record (run_stochastic(record=true), engine.cpp:116): the layer after this step
       const uint32_t* Bs = cur ? Bp1 : Bp0;
@@ -244,6 +290,33 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
     }
   }
 
+#if EBL_PHASE_PROF
+  if (a.prof) {
+    if (lane == 0) {
+      s_wd[warp][0] = pw_dense;
+      s_wd[warp][1] = pw_dec;
+      s_wd[warp][2] = pw_pass;
+      s_wd[warp][3] = pw_wait_dummy(p_wait);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long mx[4] = {0, 0, 0, 0}, passes = 0;
+      for (int q = 0; q < 4; ++q) {
+        for (int k = 0; k < 4; ++k) mx[k] = max(mx[k], s_wd[q][k]);
+        passes += s_wd[q][2];
+      }
+      long long* o = a.prof + static_cast<size_t>(env) * 10;
+      o[0] = mx[0];      // slowest warp: dense-pass cycles (sum over steps)
+      o[1] = mx[1];      // slowest warp: decide cycles
+      o[2] = pw_cells;   // warp 0's cells (for reference)
+      o[3] = n_steps;
+      o[4] = mx[2];      // max passes of a warp (sum over steps)
+      o[5] = passes;     // passes of all warps
+      o[6] = p_step;     // CTA step cycles (thread 0)
+      o[7] = mx[3];      // max barrier wait
+    }
+  }
+#endif
   // ---- store + counts ----------------------------------------------------------------------------
   const uint32_t* Bs = cur ? Bp1 : Bp0;
   int cu = 0, cb = 0, cx = 0;
