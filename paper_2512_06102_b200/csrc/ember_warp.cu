@@ -27,6 +27,12 @@
 #ifndef EBL_PHASE_PROF
 #define EBL_PHASE_PROF 0
 #endif
+#ifndef EBL_WARP_PF
+#define EBL_WARP_PF 0
+#endif
+#ifndef EBL_WPF
+#define EBL_WPF prefetch_l1
+#endif
 
 namespace ebl {
 
@@ -35,6 +41,21 @@ namespace {
 constexpr int kWpThreads = 128;  // 4 warps
 
 __device__ __forceinline__ long long pw_wait_dummy(long long v) { return v; }
+
+// Position of the q-th (0-based) set bit of v (q < popc(v)): popc binary search, 5 levels.
+__device__ __forceinline__ int nth_set_bit(uint32_t v, int q) {
+  int pos = 0;
+#pragma unroll
+  for (int half = 16; half > 0; half >>= 1) {
+    const int c = __popc(v & ((1u << half) - 1u));
+    if (q >= c) {
+      q -= c;
+      pos += half;
+      v >>= half;
+    }
+  }
+  return pos;
+}
 
 template <int MODE, int WPRC>
 __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_steps) {
@@ -142,6 +163,7 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
       // ---- dense pass over the lane's row ------------------------------------------------------
       const int r = rb + 4 * lane + warp;
       int cnt = 0;
+      uint32_t cum = 0xffffffffu;  // (WPRC <= 4) exclusive per-word counts of the row, a byte each
       if (r < H) {
         const uint32_t* up = B + ro(r + 2);
         const uint32_t* mid = B + ro(r + 1);
@@ -166,6 +188,8 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
           const uint32_t valid = j + 1 < wpr ? 0xffffffffu : last_mask;
           const uint32_t act = ((~(mc | xr[j]) & valid) & any) | mc;
           ar[j] = act;
+          if (WPRC != 0 && WPRC <= 4 && j + 1 < 4)
+            cum = (cum & ~(0xffu << (8 * (j + 1)))) | (static_cast<uint32_t>(cnt + __popc(act)) << (8 * (j + 1)));
           cnt += __popc(act);
           vl = vc;
           vc = vn;
@@ -208,18 +232,27 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
           if (cand < 32 && v <= idx) L = cand;
         }
         int q = idx - __shfl_sync(0xffffffffu, excl, L);
+        const uint32_t cumL = __shfl_sync(0xffffffffu, cum, L);
         if (idx >= total) continue;
         const int rr = rb + 4 * L + warp;
         const uint32_t* ar = ACT + ro(rr);
         int jj = 0;
-        uint32_t wv = ar[0];
-        for (;;) {  // the word holding the q-th active cell of row rr
-          const int pc = __popc(wv);
-          if (q < pc) break;
-          q -= pc;
-          wv = ar[++jj];
+        uint32_t wv;
+        if (WPRC != 0 && WPRC <= 4) {  // the word from the packed exclusive counts: no search loop
+          const uint32_t qq = static_cast<uint32_t>(q);
+          jj = (qq >= ((cumL >> 8) & 0xffu)) + (qq >= ((cumL >> 16) & 0xffu)) + (qq >= (cumL >> 24));
+          q -= jj ? static_cast<int>((cumL >> (8 * jj)) & 0xffu) : 0;
+          wv = ar[jj];
+        } else {
+          wv = ar[0];
+          for (;;) {  // the word holding the q-th active cell of row rr
+            const int pc = __popc(wv);
+            if (q < pc) break;
+            q -= pc;
+            wv = ar[++jj];
+          }
         }
-        const int cc = 32 * jj + static_cast<int>(__fns(wv, 0u, q + 1));
+        const int cc = 32 * jj + nth_set_bit(wv, q);
         // the candidate records are requested first (burning cells waste one), so their latency
         // overlaps the RNG rounds and the neighbour masks below
         CellRec rec{};
@@ -254,6 +287,20 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
           if (ig) {
             atomicOr(Bn + wi, bit);
             newly += last;
+#if EBL_WARP_PF
+            if (use_rec) {  // next step's new candidates: the ignited cell's neighbourhood records
+              const size_t eb = static_cast<size_t>(env) * a.ter_stride;
+              const int c0 = max(cc - 1, 0), c1 = min(cc + 1, W - 1);
+#pragma unroll
+              for (int d = -1; d <= 1; ++d) {
+                const int rp = min(max(rr + d, 0), H - 1);
+                const size_t rb2 = eb + static_cast<size_t>(rp) * W;
+                EBL_WPF(a.slope32 + (rb2 + c0) * 8);
+                EBL_WPF(a.slope32 + (rb2 + c1) * 8 + 7);
+                EBL_WPF(a.nfuel + rb2 + c0);
+              }
+            }
+#endif
           }
         }
       }
