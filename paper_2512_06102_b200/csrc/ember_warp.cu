@@ -57,7 +57,9 @@ __device__ __forceinline__ int nth_set_bit(uint32_t v, int q) {
   return pos;
 }
 
-template <int MODE, int WPRC>
+// DIMC: the env's side when the env is a DIMC x DIMC square known at compile time (128: C1, 64:
+// C2-sized), else 0; WPRC: words per row when known (2, 4), else 0.
+template <int MODE, int WPRC, int DIMC>
 __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_steps) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int32_t s_cnt[3];
@@ -69,7 +71,7 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
   __shared__ float s_srckw[kTer ? 32 * 8 : 1];
 
   const int env = blockIdx.x;
-  const int H = a.h, W = a.w;
+  const int H = DIMC ? DIMC : a.h, W = DIMC ? DIMC : a.w;
   const int wpr = WPRC ? WPRC : (W + 31) >> 5;
   const int S = plane_stride(wpr);
   // plane row R starts at word R*S + (R >> 2): the 32 lanes of a warp own rows 4 apart, and the
@@ -401,12 +403,12 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
   if (threadIdx.x == 3) atomicAdd(a.counts + env * 4 + 3, s_newly);
 }
 
-template <int MODE, int WPRC>
+template <int MODE, int WPRC, int DIMC = 0>
 cudaError_t launch_wp(const StepArgs& a, int n_steps, size_t sm, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(k_step_warp<MODE, WPRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_step_warp<MODE, WPRC, DIMC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
-  k_step_warp<MODE, WPRC><<<a.n_envs, kWpThreads, sm, s>>>(a, n_steps);
+  k_step_warp<MODE, WPRC, DIMC><<<a.n_envs, kWpThreads, sm, s>>>(a, n_steps);
   return cudaGetLastError();
 }
 
@@ -429,6 +431,8 @@ cudaError_t launch_step_warp(const StepArgs& a, int mode, int n_steps, cudaStrea
     return wpr == 4 ? launch_wp<kStaticTables, 4>(a, n_steps, sm, s)
                     : (wpr == 2 ? launch_wp<kStaticTables, 2>(a, n_steps, sm, s)
                                 : launch_wp<kStaticTables, 0>(a, n_steps, sm, s));
+  if (a.h == 128 && a.w == 128) return launch_wp<kStaticTerrain, 4, 128>(a, n_steps, sm, s);  // C1
+  if (a.h == 64 && a.w == 64) return launch_wp<kStaticTerrain, 2, 64>(a, n_steps, sm, s);
   return wpr == 4 ? launch_wp<kStaticTerrain, 4>(a, n_steps, sm, s)
                   : (wpr == 2 ? launch_wp<kStaticTerrain, 2>(a, n_steps, sm, s)
                               : launch_wp<kStaticTerrain, 0>(a, n_steps, sm, s));
