@@ -52,11 +52,6 @@ struct DevBuf {
   }
 };
 
-bool finite_all(const double* v, size_t n) {
-  for (size_t i = 0; i < n; ++i)
-    if (!std::isfinite(v[i])) return false;
-  return true;
-}
 
 }  // namespace
 
@@ -1390,8 +1385,12 @@ int validate_env(const ebl_env_config* c) {  // rl_env.cpp:80-93
 // Tanker step/rollout: the bit-plane kernel, or the byte kernel when EBL_KERNEL_TILED is
 // selected (an independent implementation kept for cross-checking).
 cudaError_t tanker_launch(ebl_batch* b, const ebl::RlArgs& g) {
-  if (b->kernel != EBL_KERNEL_TILED && ebl::rl_bits_fits(b->h, b->w))
+  if (b->kernel != EBL_KERNEL_TILED && ebl::rl_bits_fits(b->h, b->w)) {
+    // the warp-local kernel (two barriers per step) unless the pooled-list one is requested
+    if (b->kernel != EBL_KERNEL_RESIDENT && ebl::rl_warp_smem_bytes(b->h, b->w) <= ebl::kResMaxSmem)
+      return ebl::launch_rl_tanker_warp(g, b->mode, b->stream);
     return ebl::launch_rl_tanker_bits(g, b->mode, b->stream);
+  }
   return ebl::launch_rl_tanker(g, b->mode, b->stream);
 }
 

@@ -56,6 +56,8 @@ constexpr int kRlBitsThreads = 128;  // bit-plane tanker kernel: one CTA per env
 size_t rl_bits_smem_bytes(int h, int w);
 bool rl_bits_fits(int h, int w);
 cudaError_t launch_rl_tanker_bits(const RlArgs& g, int mode, cudaStream_t s);
+size_t rl_warp_smem_bytes(int h, int w);
+cudaError_t launch_rl_tanker_warp(const RlArgs& g, int mode, cudaStream_t s);
 cudaError_t launch_rl_tanker_reset(const RlArgs& g, int mode, const uint8_t* mask, cudaStream_t s);
 
 // ---- environment construction (ember_synth.cu) ----

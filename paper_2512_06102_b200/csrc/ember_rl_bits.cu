@@ -39,8 +39,7 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_bits(RlArgs g) 
   uint32_t* X = Bp[1] + pw;
   uint32_t* WET = X + nwords;
   uint32_t* ACT = WET + nwords;
-  uint16_t* list = reinterpret_cast<uint16_t*>(ACT + nwords);
-  const int cap = n;
+  uint16_t* list = reinterpret_cast<uint16_t*>(ACT + nwords);  // capacity n: every cell fits
   const int lane = threadIdx.x & 31;
   const bool vec = (W & 31) == 0;
 
@@ -287,6 +286,358 @@ cudaError_t launch_rl_tanker_bits(const RlArgs& g, int mode, cudaStream_t s) {
     k_rl_tanker_bits<kStaticTerrain><<<g.s.n_envs, kRlBitsThreads, sm, s>>>(g);
   }
   return cudaGetLastError();
+}
+
+
+
+// ---- warp-local tanker kernel -----------------------------------------------------------------
+// The same env step as k_rl_tanker_bits, with the CA step of k_step_warp (ember_warp.cu): rows
+// dealt to warps interleaved (row 4l + w), each warp deciding its own rows' active cells, so a
+// step needs two block barriers (after the drop, at the end) instead of five: every thread draws
+// the action itself, and the Burning count is kept incrementally (burning(t+1) = burning(t) -
+// extinguished - burnt out + ignited) instead of a popc pass.
+namespace {
+
+__device__ __forceinline__ int nth_set_bit32(uint32_t v, int q) {
+  int pos = 0;
+#pragma unroll
+  for (int half = 16; half > 0; half >>= 1) {
+    const int c = __popc(v & ((1u << half) - 1u));
+    if (q >= c) {
+      q -= c;
+      pos += half;
+      v >>= half;
+    }
+  }
+  return pos;
+}
+
+}  // namespace
+
+template <int MODE, int DIMC>
+__global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_newly[2], s_gone[2];  // per step parity: ignitions, Burning cells lost
+  __shared__ int s_burning[2];           // Burning cells at the start of step t (slot t & 1)
+  __shared__ int s_placed;
+  constexpr bool kTer = MODE == kStaticTerrain;
+  __shared__ float s_pal[kTer ? 512 : 1];
+  __shared__ float s_kw[8];
+  __shared__ float s_srckw[kTer ? 32 * 8 : 1];
+
+  const StepArgs& a = g.s;
+  const int env = blockIdx.x;
+  const int H = DIMC ? DIMC : a.h, W = DIMC ? DIMC : a.w, n = H * W;
+  const int wpr = (W + 31) >> 5;
+  const int S = plane_stride(wpr);
+  auto ro = [S](int R) { return R * S + (R >> 2); };  // conflict-free rows 4 apart (ember_warp.cu)
+  const int PH = ro(H + 2) + 1;
+  uint32_t* const Bp0 = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* const Bp1 = Bp0 + PH;
+  uint32_t* const X = Bp1 + PH;
+  uint32_t* const WET = X + PH;
+  uint32_t* const ACT = WET + PH;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec = (W & 31) == 0;
+  const uint32_t last_mask = low_mask(W - 32 * (wpr - 1));
+
+  uint8_t* st = g.state + static_cast<size_t>(env) * n;
+  uint8_t* wt = g.wet + static_cast<size_t>(env) * n;
+  for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
+    Bp0[i] = Bp1[i] = 0u;
+    Bp0[ro(H + 1) + i] = Bp1[ro(H + 1) + i] = 0u;
+  }
+  if (threadIdx.x < 2) s_newly[threadIdx.x] = s_gone[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_burning[0] = 0;
+  const bool use_rec = kTer && a.nfuel && a.n_pal <= 32;
+  if constexpr (kTer) {
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) s_pal[i] = __ldg(a.pal32 + i);
+    if (threadIdx.x < 8) s_kw[threadIdx.x] = __ldg(a.kw32 + static_cast<size_t>(env) * a.kw_stride + threadIdx.x);
+    if (use_rec)
+      for (int i = threadIdx.x; i < a.n_pal * 8; i += blockDim.x)
+        s_srckw[i] = __ldg(a.pal32 + (i >> 3)) * __ldg(a.kw32 + static_cast<size_t>(env) * a.kw_stride + (i & 7));
+  }
+  int burning0 = 0;
+  for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
+    const uint8_t* src = st + it.r * W + 32 * it.j;
+    const uint8_t* wsrc = wt + it.r * W + 32 * it.j;
+    const int nc = min(32, W - 32 * it.j);
+    uint32_t b = 0u, x = 0u, wb = 0u;
+    if (vec) {
+      bytes_to_bits(src, b, x);
+      uint32_t w1, w2;
+      bytes_to_bits(wsrc, w1, w2);  // wet bytes are 0/1
+      wb = w1;
+    } else {
+      for (int k = 0; k < nc; ++k) {
+        b |= static_cast<uint32_t>(src[k] == 1) << k;
+        x |= static_cast<uint32_t>(src[k] == 2) << k;
+        wb |= static_cast<uint32_t>(wsrc[k] != 0) << k;
+      }
+    }
+    Bp0[ro(it.r + 1) + it.j] = b;
+    X[ro(it.r) + it.j] = x;
+    WET[ro(it.r) + it.j] = wb;
+    burning0 += __popc(b);
+  }
+  __syncthreads();  // s_burning zeroed, planes loaded
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) burning0 += __shfl_xor_sync(0xffffffffu, burning0, o);
+  if (lane == 0 && burning0) atomicAdd(&s_burning[0], burning0);
+
+  RlEnv e = g.env[env];
+  const DiagCounters dg{a.diag};
+  double rsum = 0.0;
+  int32_t finished = 0;
+  int cur = 0;
+  auto win3 = [&](const uint32_t* row, int j, int b) -> uint32_t {
+    const uint32_t wj = row[j];
+    uint32_t v = b > 0 ? wj >> (b - 1) : ((j > 0 ? row[j - 1] >> 31 : 0u) | (wj << 1));
+    if (b == 31) v = (v & 3u) | ((j + 1 < wpr ? row[j + 1] & 1u : 0u) << 2);
+    return v & 7u;
+  };
+  for (int t = 0; t < g.n_steps; ++t) {
+    const int par = t & 1;
+    uint32_t* B = cur ? Bp1 : Bp0;
+    uint32_t* Bn = cur ? Bp0 : Bp1;
+    // ---- action (every thread) + drop ----------------------------------------------------------
+    const uint64_t prefix = key_prefix(g.seed, e.stream, static_cast<uint64_t>(e.step));
+    const int action = g.actions ? g.actions[env] : static_cast<int>(below(cell_bits53(prefix, 0, 2), n));
+    if (threadIdx.x < 9) {
+      const int r = action / W + static_cast<int>(threadIdx.x) / 3 - 1;
+      const int c = action % W + static_cast<int>(threadIdx.x) % 3 - 1;
+      if (r >= 0 && r < H && c >= 0 && c < W) {
+        const uint32_t bit = 1u << (c & 31);
+        uint32_t* bw = B + ro(r + 1) + (c >> 5);
+        if (*bw & bit) {  // extinguish
+          atomicAnd(bw, ~bit);
+          atomicOr(X + ro(r) + (c >> 5), bit);
+          atomicAdd(&s_gone[par], 1);
+        } else if (!(X[ro(r) + (c >> 5)] & bit)) {  // wet
+          atomicOr(WET + ro(r) + (c >> 5), bit);
+        }
+      }
+    }
+    if (threadIdx.x == 0) s_newly[par ^ 1] = s_gone[par ^ 1] = 0;  // the next step's counters
+    __syncthreads();
+    // ---- warp-local CA step (k_step_warp) -----------------------------------------------------------
+    int newly = 0, burnt = 0;
+    for (int rb = 0; rb < H; rb += kRlBitsThreads) {
+      const int r = rb + 4 * lane + warp;
+      int cnt = 0;
+      uint32_t cum = 0xffffffffu;
+      if (r < H) {
+        const uint32_t* up = B + ro(r + 2);
+        const uint32_t* mid = B + ro(r + 1);
+        const uint32_t* dn = B + ro(r);
+        uint32_t* bn = Bn + ro(r + 1);
+        const uint32_t* xr = X + ro(r);
+        const uint32_t* wr = WET + ro(r);
+        uint32_t* ar = ACT + ro(r);
+        uint32_t vl = 0u;
+        uint32_t uc = up[0], mc = mid[0], dc = dn[0];
+        uint32_t vc = uc | mc | dc;
+        for (int j = 0; j < wpr; ++j) {
+          uint32_t un = 0u, mn = 0u, dnn = 0u;
+          if (j + 1 < wpr) {
+            un = up[j + 1];
+            mn = mid[j + 1];
+            dnn = dn[j + 1];
+          }
+          const uint32_t vn = un | mn | dnn;
+          const uint32_t any = ((vc << 1) | (vl >> 31)) | ((vc >> 1) | (vn << 31)) | uc | dc;
+          bn[j] = mc;
+          const uint32_t valid = j + 1 < wpr ? 0xffffffffu : last_mask;
+          const uint32_t act = ((~(mc | xr[j] | wr[j]) & valid) & any) | mc;  // wet cells never ignite
+          ar[j] = act;
+          if (j + 1 < 4) cum = (cum & ~(0xffu << (8 * (j + 1)))) | (static_cast<uint32_t>(cnt + __popc(act)) << (8 * (j + 1)));
+          cnt += __popc(act);
+          vl = vc;
+          vc = vn;
+          uc = un;
+          mc = mn;
+          dc = dnn;
+        }
+      }
+      if (!__ballot_sync(0xffffffffu, cnt > 0)) continue;
+      __syncwarp();
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int excl = incl - cnt;
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      for (int p = 0; p < total; p += 32) {
+        const int idx = p + lane;
+        int L = 0;
+#pragma unroll
+        for (int stp = 16; stp > 0; stp >>= 1) {
+          const int cand = L + stp;
+          const int v = __shfl_sync(0xffffffffu, excl, cand & 31);
+          if (cand < 32 && v <= idx) L = cand;
+        }
+        int q = idx - __shfl_sync(0xffffffffu, excl, L);
+        const uint32_t cumL = __shfl_sync(0xffffffffu, cum, L);
+        if (idx >= total) continue;
+        const int rr = rb + 4 * L + warp;
+        const uint32_t* ar = ACT + ro(rr);
+        int jj = 0;
+        uint32_t wv;
+        if (wpr <= 4) {
+          const uint32_t qq = static_cast<uint32_t>(q);
+          jj = (qq >= ((cumL >> 8) & 0xffu)) + (qq >= ((cumL >> 16) & 0xffu)) + (qq >= (cumL >> 24));
+          q -= jj ? static_cast<int>((cumL >> (8 * jj)) & 0xffu) : 0;
+          wv = ar[jj];
+        } else {
+          wv = ar[0];
+          for (;;) {
+            const int pc = __popc(wv);
+            if (q < pc) break;
+            q -= pc;
+            wv = ar[++jj];
+          }
+        }
+        const int cc = 32 * jj + nth_set_bit32(wv, q);
+        CellRec rec{};
+        if (use_rec)
+          rec = load_rec(a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
+                         a.nfuel + static_cast<size_t>(env) * a.ter_stride, a.fuel + static_cast<size_t>(env) * a.ter_stride,
+                         rr * W + cc);
+        const int j = cc >> 5, b = cc & 31;
+        const uint32_t bit = 1u << b;
+        const int wi = ro(rr + 1) + j;
+        const uint64_t m = cell_bits53(prefix, static_cast<uint64_t>(rr * W + cc), 0);
+        const uint32_t midw = win3(B + ro(rr + 1), j, b);
+        if (midw & 2u) {
+          if (m >= a.pc_thr) {
+            atomicAnd(Bn + wi, ~bit);
+            atomicOr(X + ro(rr) + j, bit);
+            ++burnt;
+          }
+        } else {
+          const uint32_t dnw = win3(B + ro(rr), j, b), upw = win3(B + ro(rr + 2), j, b);
+          const uint32_t nb = (midw & 1u) | (dnw << 1) | ((midw >> 2) << 4) | ((upw >> 2) << 5) |
+                              ((upw & 2u) << 5) | ((upw & 1u) << 7);
+          bool ig;
+          if (use_rec)
+            ig = ignite_terrain_rec_pre(terrain_view(a, env), rec, s_srckw, s_pal + 256, a.alpha_s_l2, W, rr, cc, nb, m, dg);
+          else if constexpr (kTer)
+            ig = ignite_terrain_tab(terrain_view(a, env), a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
+                                    s_pal, s_kw, W, H, rr, cc, nb, m, dg);
+          else
+            ig = ignite<MODE>(a, env, rr, cc, nb, m, dg);
+          if (ig) {
+            atomicOr(Bn + wi, bit);
+            ++newly;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      newly += __shfl_xor_sync(0xffffffffu, newly, o);
+      burnt += __shfl_xor_sync(0xffffffffu, burnt, o);
+    }
+    if (lane == 0 && newly) atomicAdd(&s_newly[par], newly);
+    if (lane == 0 && burnt) atomicAdd(&s_gone[par], burnt);
+    __syncthreads();
+    cur ^= 1;
+    // ---- reward, done (Burning count kept incrementally) --------------------------------------------
+    const int burning = s_burning[par] - s_gone[par] + s_newly[par];
+    e.step += 1;
+    const double reward = -static_cast<double>(s_newly[par]);
+    const bool done = burning == 0 || e.step >= g.max_steps;
+    rsum += reward;
+    if (g.n_steps == 1 && threadIdx.x == 0) {
+      if (g.reward) g.reward[env] = reward;
+      if (g.done) g.done[env] = done ? 1 : 0;
+    }
+    if (done) {  // auto-reset in place (block-uniform branch)
+      ++finished;
+      uint32_t* Bnew = cur ? Bp1 : Bp0;
+      for (int i = threadIdx.x; i < PH; i += blockDim.x) {
+        Bnew[i] = 0u;
+        X[i] = 0u;
+        WET[i] = 0u;
+      }
+      const uint32_t episode = e.episode + 1;
+      const uint64_t stream = (static_cast<uint64_t>(episode) << 32) | (g.env_id0 + env);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const uint64_t pre = key_prefix(g.seed, stream, 0);
+        const uint8_t* fuel = a.fuel + static_cast<size_t>(env) * a.ter_stride;
+        uint64_t counter = 0;
+        int placed = 0;
+        while (placed < g.ignitions && counter < 64ull * n) {
+          const int cell = static_cast<int>(below(cell_bits53(pre, counter++, 1), n));
+          const int cr = cell / W, cc2 = cell % W;
+          uint32_t* bw = Bnew + ro(cr + 1) + (cc2 >> 5);
+          const uint32_t bit = 1u << (cc2 & 31);
+          const bool burnable = kTer ? a.pal64[512 + fuel[cell]] > 0.5
+                                     : a.gamma[static_cast<size_t>(env) * a.tab_stride + cell] > 0.0;
+          if ((*bw & bit) || !burnable) continue;
+          *bw |= bit;
+          ++placed;
+        }
+        s_placed = placed;
+        s_burning[par ^ 1] = placed;
+      }
+      __syncthreads();
+      e.step = 0;
+      e.episode = episode;
+      e.stream = stream;
+      e.done = s_placed == 0;
+    } else if (threadIdx.x == 0) {
+      s_burning[par ^ 1] = burning;  // read after the next step's barriers
+    }
+  }
+  // ---- store ----------------------------------------------------------------------------------
+  __syncthreads();
+  const uint32_t* Bs = cur ? Bp1 : Bp0;
+  for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
+    const uint32_t b = Bs[ro(it.r + 1) + it.j], x = X[ro(it.r) + it.j], wb = WET[ro(it.r) + it.j];
+    uint8_t* dst = st + it.r * W + 32 * it.j;
+    uint8_t* wdst = wt + it.r * W + 32 * it.j;
+    if (vec) {
+      bits_to_bytes(b, x, dst);
+      bits_to_bytes(wb, 0u, wdst);
+    } else {
+      const int nc = min(32, W - 32 * it.j);
+      for (int k = 0; k < nc; ++k) {
+        dst[k] = static_cast<uint8_t>(((b >> k) & 1u) | (((x >> k) & 1u) << 1));
+        wdst[k] = static_cast<uint8_t>((wb >> k) & 1u);
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    g.env[env] = e;
+    if (g.reward_sum) g.reward_sum[env] += rsum;
+    if (g.episodes) g.episodes[env] += finished;
+  }
+}
+
+size_t rl_warp_smem_bytes(int h, int w) {
+  const size_t S = plane_stride((w + 31) / 32);
+  const size_t R = static_cast<size_t>(h) + 2;
+  return 5 * (R * S + (R >> 2) + 1) * sizeof(uint32_t);  // B x2, X, WET, ACT (ro() layout)
+}
+
+template <int MODE, int DIMC>
+static cudaError_t launch_rl_warp_t(const RlArgs& g, size_t sm, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k_rl_tanker_warp<MODE, DIMC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(sm));
+  if (e != cudaSuccess) return e;
+  k_rl_tanker_warp<MODE, DIMC><<<g.s.n_envs, kRlBitsThreads, sm, s>>>(g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rl_tanker_warp(const RlArgs& g, int mode, cudaStream_t s) {
+  const size_t sm = rl_warp_smem_bytes(g.s.h, g.s.w);
+  if (mode == kStaticTables) return launch_rl_warp_t<kStaticTables, 0>(g, sm, s);
+  if (g.s.h == 64 && g.s.w == 64) return launch_rl_warp_t<kStaticTerrain, 64>(g, sm, s);
+  return launch_rl_warp_t<kStaticTerrain, 0>(g, sm, s);
 }
 
 }  // namespace ebl

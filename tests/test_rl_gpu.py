@@ -118,7 +118,8 @@ def _port_tanker(port, t: eb.Terrain, cfg, seed, env_ids, n_steps, tc, actions=N
     return out
 
 
-@pytest.mark.parametrize("kernel", [eb.KERNEL_AUTO, eb.KERNEL_TILED])  # bit-plane / byte kernel
+# warp-local bit-plane (AUTO) / pooled-list bit-plane (RESIDENT) / byte kernel (TILED)
+@pytest.mark.parametrize("kernel", [eb.KERNEL_AUTO, eb.KERNEL_RESIDENT, eb.KERNEL_TILED])
 @pytest.mark.parametrize("fused", [False, True])
 def test_tanker_vs_port(port, fused, kernel):
     n, h, w, seed, steps = 24, 64, 64, 7, 300
@@ -150,7 +151,8 @@ def test_tanker_vs_port(port, fused, kernel):
 
 
 @pytest.mark.parametrize("kernel,h,w", [(eb.KERNEL_AUTO, 32, 48), (eb.KERNEL_TILED, 32, 48),
-                                          (eb.KERNEL_AUTO, 17, 45)])
+                                          (eb.KERNEL_AUTO, 17, 45), (eb.KERNEL_RESIDENT, 17, 45),
+                                          (eb.KERNEL_AUTO, 140, 33)])
 def test_tanker_host_actions(port, kernel, h, w):
     n, seed, steps = 8, 3, 40
     t = eb.synth_terrain(seed, n, h, w)
