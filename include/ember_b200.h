@@ -160,25 +160,24 @@ int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* sp
                                      const double* direction);
 
 /* Kernel selection for ebl_step_batch (results are identical by construction):
- *  AUTO      WARP when an env fits shared memory (H*W <= 65536), else the bit-sliced
- *            blocked kernel with light-cone-halo tiles, 8 steps per launch;
- *  WARP      whole env per CTA, all n steps fused, rows dealt to warps and each warp deciding
- *            its own rows' active cells: one block barrier per step;
+ *  AUTO      the warp-local kernel: one CTA per env with all n steps fused when an env fits
+ *            shared memory (H*W <= 65536), else light-cone-halo tiles, 8 steps per launch;
+ *            rows dealt to warps, each warp deciding its own rows' active cells, one block
+ *            barrier per step;
+ *  WARP      the same as AUTO;
  *  FRONTIER  whole env per CTA (H*W <= 16384), all steps fused, each step touching only its
  *            active list (the next list built from this step's decisions, no dense pass); envs
  *            whose list outgrows its capacity are continued by the blocked kernel in a second
  *            launch.  Faster per step for small fires, not for the heaviest;
  *  TILED     the per-cell tile kernel, one step per launch (independent implementation);
- *  RESIDENT  the blocked kernel, whole env per CTA with a pooled active list (error if it
- *            does not fit);
- *  BLOCKED   the blocked kernel with halo tiles even when the env would fit. */
+ *  RESIDENT  the pooled-list blocked kernel, whole env per CTA (error if it does not fit);
+ *  BLOCKED   the pooled-list blocked kernel with halo tiles even when the env would fit. */
 #define EBL_KERNEL_AUTO 0
 #define EBL_KERNEL_TILED 1
 #define EBL_KERNEL_RESIDENT 2
 #define EBL_KERNEL_BLOCKED 3
 #define EBL_KERNEL_FRONTIER 5
-#define EBL_KERNEL_WARP 6 /* resident, rows dealt to warps, each warp decides its own rows'
-                             active cells: one block barrier per step, no list build */
+#define EBL_KERNEL_WARP 6
 #define EBL_KERNEL_PAIRED 4 /* resident, two envs per CTA sharing 256 threads and one pooled
                                active list (H*W <= 32768); selectable only (AUTO does not pair:
                                slower on C1, ember_kernels.h) */

@@ -310,11 +310,14 @@ bool use_frontier(const ebl_batch* b) {
   return b->kernel == EBL_KERNEL_FRONTIER && b->tile_h == 0 && ebl::frontier_fits(b->h, b->w);
 }
 
-// The warp-local kernel runs resident envs under AUTO (measured on C1: 0.74 ms vs 0.77 ms for the
-// pooled-list blocked kernel; EBL_KERNEL_RESIDENT keeps the latter selectable).
-bool use_warp(const ebl_batch* b) {
-  return (b->kernel == EBL_KERNEL_WARP || b->kernel == EBL_KERNEL_AUTO) && b->tile_h == 0 &&
-         ebl::warp_fits(b->h, b->w);
+// The warp-local kernel runs every one-env-per-CTA geometry (whole env or halo tiles) under AUTO
+// (C1: 0.63 ms vs 0.77 ms for the pooled-list blocked kernel, which EBL_KERNEL_RESIDENT /
+// EBL_KERNEL_BLOCKED / EBL_KERNEL_PAIRED keep selectable).
+bool use_warp(const ebl_batch* b) { return b->kernel == EBL_KERNEL_WARP || b->kernel == EBL_KERNEL_AUTO; }
+
+cudaError_t launch_ca(const ebl_batch* b, const ebl::StepArgs& a, const ebl::BlockGeom& g, cudaStream_t s) {
+  if (use_warp(b) && g.envs_per_cta == 1) return ebl::launch_step_warp(a, b->mode, g, s);
+  return ebl::launch_step_blocked(a, b->mode, g, s);
 }
 
 int ensure_pipeline(ebl_batch* b, int chunks) {
@@ -841,8 +844,6 @@ uint64_t ebl_batch_step_index(const ebl_batch* b) { return b ? b->step : 0; }
 int ebl_batch_set_kernel(ebl_batch* b, int which) {
   if (int e = check_batch(b)) return e;
   if (which < EBL_KERNEL_AUTO || which > EBL_KERNEL_WARP) return set_err(EBL_EINVAL, "unknown kernel");
-  if (which == EBL_KERNEL_WARP && !ebl::warp_fits(b->h, b->w))
-    return set_err(EBL_EINVAL, "the warp-local kernel needs a resident env (H*W <= 65536)");
   if (which == EBL_KERNEL_FRONTIER && !ebl::frontier_fits(b->h, b->w))
     return set_err(EBL_EINVAL, "the frontier kernel needs a resident env with H*W <= 16384");
   if ((which == EBL_KERNEL_RESIDENT || which == EBL_KERNEL_PAIRED) && !ebl::resident_fits(b->h, b->w))
@@ -876,16 +877,6 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
                                  cudaMemcpyDeviceToDevice, b->stream));
       }
     }
-  } else if (use_warp(b)) {  // warp-local resident kernel, all steps in one launch
-    ebl::StepArgs a = step_args(b);
-    EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
-    a.counts = b->counts.p;
-    a.traj = b->traj_out;
-    a.traj_t0 = 0;
-    EBL_CUDA(ebl::launch_step_warp(a, b->mode, n_steps, b->stream));
-    b->cur ^= 1;
-    b->step += n_steps;
-    b->launches += 1;
   } else if (use_frontier(b)) {  // frontier kernel, all steps in one launch (+ hand-over launch)
     EBL_CUDA(b->resume.alloc(b->n_envs));
     ebl::StepArgs a = step_args(b);
@@ -922,7 +913,7 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
       }
       a.traj = b->traj_out;  // record: the kernel stores every step's tile (no extra launches)
       a.traj_t0 = static_cast<size_t>(done);
-      EBL_CUDA(ebl::launch_step_blocked(a, b->mode, g, b->stream));
+      EBL_CUDA(launch_ca(b, a, g, b->stream));
       b->cur ^= 1;
       b->step += g.n_steps;
       b->launches += 1;
@@ -955,7 +946,6 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
   const bool resident = b->kernel != EBL_KERNEL_TILED && b->kernel != EBL_KERNEL_BLOCKED &&
                         b->tile_h == 0 && ebl::resident_fits(b->h, b->w);
   const bool frontier = use_frontier(b);
-  const bool warpk = use_warp(b);
   int chunks = b->pipe_chunks > 0 ? b->pipe_chunks : 8;
   chunks = std::min(chunks, b->n_envs);
   if (!resident || n_steps == 0 || chunks <= 1) {  // one launch per step set: plain sequence
@@ -1013,8 +1003,7 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
     EBL_CUDA(cudaStreamWaitEvent(s, b->pipe_ev_in[c], 0));
     EBL_CUDA(cudaMemsetAsync(b->counts.p + static_cast<size_t>(off) * 4, 0, static_cast<size_t>(n) * 4 * sizeof(int32_t), s));
     if (frontier) EBL_CUDA(ebl::launch_step_frontier(chunk_args(b, a, off, n), b->mode, n_steps, s));
-    else if (warpk) EBL_CUDA(ebl::launch_step_warp(chunk_args(b, a, off, n), b->mode, n_steps, s));
-    else EBL_CUDA(ebl::launch_step_blocked(chunk_args(b, a, off, n), b->mode, g, s));
+    else EBL_CUDA(launch_ca(b, chunk_args(b, a, off, n), g, s));
     EBL_CUDA(cudaEventRecord(b->pipe_ev_done[c], s));
   }
   for (int c = 0; c < chunks; ++c) {
@@ -1166,7 +1155,7 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
         a.peer_dst[a.n_peers] = static_cast<int>(lo - nb->row_off);
         ++a.n_peers;
       }
-      EBL_CUDA(ebl::launch_step_blocked(a, b->mode, g, b->stream));
+      EBL_CUDA(launch_ca(b, a, g, b->stream));
       EBL_CUDA(cudaEventRecord(b->shard_ev[chunk & 1], b->stream));
     }
     for (int s = 0; s < n_shards; ++s) {

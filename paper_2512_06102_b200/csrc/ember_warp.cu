@@ -60,7 +60,7 @@ __device__ __forceinline__ int nth_set_bit(uint32_t v, int q) {
 // DIMC: the env's side when the env is a DIMC x DIMC square known at compile time (128: C1, 64:
 // C2-sized), else 0; WPRC: words per row when known (2, 4), else 0.
 template <int MODE, int WPRC, int DIMC>
-__global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_steps) {
+__global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGeom g) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int32_t s_cnt[3];
   __shared__ int32_t s_newly;
@@ -70,9 +70,16 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
   __shared__ float s_kw[8];
   __shared__ float s_srckw[kTer ? 32 * 8 : 1];
 
-  const int env = blockIdx.x;
-  const int H = DIMC ? DIMC : a.h, W = DIMC ? DIMC : a.w;
-  const int wpr = WPRC ? WPRC : (W + 31) >> 5;
+  // region of this CTA: one tile of one env's layer plus its light-cone halo (the whole env for
+  // resident launches); H x RW region cells, layer BH x W
+  const int env = blockIdx.z;
+  const int n_steps = g.n_steps;
+  const int BH = DIMC ? DIMC : a.h, W = DIMC ? DIMC : a.w;
+  const int r0 = DIMC ? 0 : blockIdx.y * g.tile_h, c0 = DIMC ? 0 : blockIdx.x * g.tile_w;  // c0 % 32 == 0
+  const int R0 = DIMC ? 0 : max(0, r0 - g.halo_rows), R1 = DIMC ? BH : min(BH, r0 + g.tile_h + g.halo_rows);
+  const int C0 = DIMC ? 0 : max(0, c0 - g.halo_cols), C1 = DIMC ? W : min(W, c0 + g.tile_w + g.halo_cols);
+  const int H = R1 - R0, RW = C1 - C0;
+  const int wpr = WPRC ? WPRC : (RW + 31) >> 5;
   const int S = plane_stride(wpr);
   // plane row R starts at word R*S + (R >> 2): the 32 lanes of a warp own rows 4 apart, and the
   // extra word every 4 rows makes their stride 4S+1 (odd) -> 32 distinct banks
@@ -82,10 +89,14 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
   uint32_t* const Bp1 = Bp0 + PH;
   uint32_t* const X = Bp1 + PH;
   uint32_t* const ACT = X + PH;
-  const size_t ncell = static_cast<size_t>(H) * W;
+  const size_t ncell = static_cast<size_t>(BH) * W;
   const bool vec = (W & 15) == 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t last_mask = low_mask(W - 32 * (wpr - 1));
+  const uint32_t last_mask = low_mask(RW - 32 * (wpr - 1));
+  // the output tile inside the region (rows tr0..tr1, words tj0..tj1)
+  const int tr0 = r0 - R0, tr1 = (DIMC ? BH : min(r0 + g.tile_h, BH)) - R0;
+  const int tc0 = c0 - C0, tc1 = (DIMC ? W : min(c0 + g.tile_w, W)) - C0;
+  const int tj0 = tc0 >> 5, tj1 = (tc1 + 31) >> 5, twords = tj1 - tj0;
 
   // ---- load ----------------------------------------------------------------------------------
   for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
@@ -94,9 +105,9 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
   }
   const uint8_t* __restrict__ in = a.in + env * ncell;
   for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
-    const int nc = min(32, W - 32 * it.j);
+    const int nc = min(32, RW - 32 * it.j);
     uint32_t b = 0u, x = 0u;
-    const uint8_t* src = in + static_cast<size_t>(it.r) * W + 32 * it.j;
+    const uint8_t* src = in + static_cast<size_t>(R0 + it.r) * W + C0 + 32 * it.j;
     if (nc == 32 && vec) {
       bytes_to_bits(src, b, x);
     } else {
@@ -132,12 +143,34 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
   __syncthreads();
 
   const DiagCounters dg{a.diag};
-  const uint64_t gbase = static_cast<uint64_t>(a.row_off) * W;
+  const uint64_t gbase = static_cast<uint64_t>(a.row_off + R0) * W + C0;  // RNG index of region (0, 0)
   auto win3 = [&](const uint32_t* row, int j, int b) -> uint32_t {  // columns c-1, c, c+1 -> bits 0..2
     const uint32_t wj = row[j];
     uint32_t v = b > 0 ? wj >> (b - 1) : ((j > 0 ? row[j - 1] >> 31 : 0u) | (wj << 1));
     if (b == 31) v = (v & 3u) | ((j + 1 < wpr ? row[j + 1] & 1u : 0u) << 2);
     return v & 7u;
+  };
+
+  // output tile -> uint8 layer at `layer` (+ U/B/X counts when cnt3); layer rows outside
+  // [row_lo, row_hi) skipped, rows shifted by dst_shift (peer layers)
+  auto store_tile = [&](const uint32_t* Bs, uint8_t* __restrict__ layer, int* cnt3, int row_lo, int row_hi,
+                        int dst_shift) {
+    for (WordIter it(twords, (tr1 - tr0) * twords); it.ok(); it.next()) {
+      const int rr = tr0 + it.r, j = tj0 + it.j;
+      const int lrow = R0 + rr;
+      if (lrow < row_lo || lrow >= row_hi) continue;
+      const uint32_t bb = Bs[ro(rr + 1) + j], xx = X[ro(rr) + j];
+      const int nc = min(32, RW - 32 * j);
+      if (cnt3) {
+        cnt3[0] += nc - __popc(bb) - __popc(xx);
+        cnt3[1] += __popc(bb);
+        cnt3[2] += __popc(xx);
+      }
+      uint8_t* dst = layer + static_cast<size_t>(lrow + dst_shift) * W + C0 + 32 * j;
+      if (nc == 32 && vec) bits_to_bytes(bb, xx, dst);
+      else
+        for (int k = 0; k < nc; ++k) dst[k] = static_cast<uint8_t>(((bb >> k) & 1u) | (((xx >> k) & 1u) << 1));
+    }
   };
 
   int cur = 0;
@@ -255,13 +288,14 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
           }
         }
         const int cc = 32 * jj + nth_set_bit(wv, q);
+        const int gr = R0 + rr, gc = C0 + cc;  // layer coordinates
         // the candidate records are requested first (burning cells waste one), so their latency
         // overlaps the RNG rounds and the neighbour masks below
         CellRec rec{};
         if (use_rec)
           rec = load_rec(a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
                          a.nfuel + static_cast<size_t>(env) * a.ter_stride, a.fuel + static_cast<size_t>(env) * a.ter_stride,
-                         rr * W + cc);
+                         gr * W + gc);
         // ---- decide (engine.cpp:12-26) ----
         const int j = cc >> 5, b = cc & 31;
         const uint32_t bit = 1u << b;
@@ -279,30 +313,16 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
                               ((upw & 2u) << 5) | ((upw & 1u) << 7);
           bool ig;
           if (use_rec)
-            ig = ignite_terrain_rec_pre(terrain_view(a, env, srow), rec, s_srckw, s_pal + 256, a.alpha_s_l2, W, rr, cc,
+            ig = ignite_terrain_rec_pre(terrain_view(a, env, srow), rec, s_srckw, s_pal + 256, a.alpha_s_l2, W, gr, gc,
                                         nb, m, dg);
           else if constexpr (kTer)
             ig = ignite_terrain_tab(terrain_view(a, env, srow), a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
-                                    s_pal, s_kw, W, H, rr, cc, nb, m, dg);
+                                    s_pal, s_kw, W, BH, gr, gc, nb, m, dg);
           else
-            ig = ignite<MODE>(a, env, rr, cc, nb, m, dg, srow);
+            ig = ignite<MODE>(a, env, gr, gc, nb, m, dg, srow);
           if (ig) {
             atomicOr(Bn + wi, bit);
-            newly += last;
-#if EBL_WARP_PF
-            if (use_rec) {  // next step's new candidates: the ignited cell's neighbourhood records
-              const size_t eb = static_cast<size_t>(env) * a.ter_stride;
-              const int c0 = max(cc - 1, 0), c1 = min(cc + 1, W - 1);
-#pragma unroll
-              for (int d = -1; d <= 1; ++d) {
-                const int rp = min(max(rr + d, 0), H - 1);
-                const size_t rb2 = eb + static_cast<size_t>(rp) * W;
-                EBL_WPF(a.slope32 + (rb2 + c0) * 8);
-                EBL_WPF(a.slope32 + (rb2 + c1) * 8 + 7);
-                EBL_WPF(a.nfuel + rb2 + c0);
-              }
-            }
-#endif
+            newly += last && rr >= tr0 && rr < tr1 && cc >= tc0 && cc < tc1;  // counted in the tile only
           }
         }
       }
@@ -325,17 +345,9 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
     if (threadIdx.x == 0) p_step += clock64() - st0;
 #endif
     cur ^= 1;
-    if (a.traj) {  // record (run_stochastic(record=true), engine.cpp:116): the layer after this step
+    if (a.traj) {  // record (run_stochastic(record=true), engine.cpp:116): the tile after this step
       const uint32_t* Bs = cur ? Bp1 : Bp0;
-      uint8_t* dst = a.traj + ((a.traj_t0 + t) * a.n_envs + env) * ncell;
-      for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
-        const uint32_t bb = Bs[ro(it.r + 1) + it.j], xx = X[ro(it.r) + it.j];
-        uint8_t* o = dst + static_cast<size_t>(it.r) * W + 32 * it.j;
-        const int nc = min(32, W - 32 * it.j);
-        if (nc == 32 && vec) bits_to_bytes(bb, xx, o);
-        else
-          for (int k = 0; k < nc; ++k) o[k] = static_cast<uint8_t>(((bb >> k) & 1u) | (((xx >> k) & 1u) << 1));
-      }
+      store_tile(Bs, a.traj + ((a.traj_t0 + t) * a.n_envs + env) * ncell, nullptr, 0, BH, 0);
     }
   }
 
@@ -368,22 +380,12 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
 #endif
   // ---- store + counts ----------------------------------------------------------------------------
   const uint32_t* Bs = cur ? Bp1 : Bp0;
-  int cu = 0, cb = 0, cx = 0;
-  for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
-    const uint32_t bb = Bs[ro(it.r + 1) + it.j], xx = X[ro(it.r) + it.j];
-    const int nc = min(32, W - 32 * it.j);
-    cu += nc - __popc(bb) - __popc(xx);
-    cb += __popc(bb);
-    cx += __popc(xx);
-    for (int o = 0; o < 2; ++o) {
-      uint8_t* base = o == 0 ? a.out : a.out2;
-      if (!base) continue;
-      uint8_t* dst = base + env * ncell + static_cast<size_t>(it.r) * W + 32 * it.j;
-      if (nc == 32 && vec) bits_to_bytes(bb, xx, dst);
-      else
-        for (int k = 0; k < nc; ++k) dst[k] = static_cast<uint8_t>(((bb >> k) & 1u) | (((xx >> k) & 1u) << 1));
-    }
-  }
+  int c3[3] = {0, 0, 0};
+  store_tile(Bs, a.out + env * ncell, c3, a.store_lo, a.store_hi, 0);
+  if (a.out2) store_tile(Bs, a.out2 + env * ncell, nullptr, a.store_lo, a.store_hi, 0);
+  for (int p = 0; p < a.n_peers; ++p)  // fused halo exchange: owned rows straight into the neighbour
+    store_tile(Bs, a.peer_out[p], nullptr, a.peer_lo[p], a.peer_hi[p], a.peer_dst[p] - a.peer_lo[p]);
+  int cu = c3[0], cb = c3[1], cx = c3[2];
   if (!a.counts) return;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -404,11 +406,12 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, int n_s
 }
 
 template <int MODE, int WPRC, int DIMC = 0>
-cudaError_t launch_wp(const StepArgs& a, int n_steps, size_t sm, cudaStream_t s) {
+cudaError_t launch_wp(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k_step_warp<MODE, WPRC, DIMC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
-  k_step_warp<MODE, WPRC, DIMC><<<a.n_envs, kWpThreads, sm, s>>>(a, n_steps);
+  const dim3 grid((a.w + g.tile_w - 1) / g.tile_w, (a.h + g.tile_h - 1) / g.tile_h, a.n_envs);
+  k_step_warp<MODE, WPRC, DIMC><<<grid, kWpThreads, sm, s>>>(a, g);
   return cudaGetLastError();
 }
 
@@ -424,18 +427,23 @@ bool warp_fits(int h, int w) {
   return static_cast<size_t>(h) * w <= 65536 && warp_smem_bytes(h, w) <= kResMaxSmem;
 }
 
-cudaError_t launch_step_warp(const StepArgs& a, int mode, int n_steps, cudaStream_t s) {
-  const size_t sm = warp_smem_bytes(a.h, a.w);
+// Any geometry plan_blocks produces with one env per CTA (whole env, or halo tiles).
+cudaError_t launch_step_warp(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s) {
+  const int rh = a.h < g.tile_h + 2 * g.halo_rows ? a.h : g.tile_h + 2 * g.halo_rows;
+  const int rw = a.w < g.tile_w + 2 * g.halo_cols ? a.w : g.tile_w + 2 * g.halo_cols;
+  const size_t sm = warp_smem_bytes(rh, rw);
+  const bool whole_width = g.tile_w >= a.w, whole = whole_width && g.tile_h >= a.h;
   const int wpr = (a.w + 31) / 32;
-  if (mode == kStaticTables)
-    return wpr == 4 ? launch_wp<kStaticTables, 4>(a, n_steps, sm, s)
-                    : (wpr == 2 ? launch_wp<kStaticTables, 2>(a, n_steps, sm, s)
-                                : launch_wp<kStaticTables, 0>(a, n_steps, sm, s));
-  if (a.h == 128 && a.w == 128) return launch_wp<kStaticTerrain, 4, 128>(a, n_steps, sm, s);  // C1
-  if (a.h == 64 && a.w == 64) return launch_wp<kStaticTerrain, 2, 64>(a, n_steps, sm, s);
-  return wpr == 4 ? launch_wp<kStaticTerrain, 4>(a, n_steps, sm, s)
-                  : (wpr == 2 ? launch_wp<kStaticTerrain, 2>(a, n_steps, sm, s)
-                              : launch_wp<kStaticTerrain, 0>(a, n_steps, sm, s));
+  if (mode == kStaticTables) {
+    if (whole_width && wpr == 4) return launch_wp<kStaticTables, 4>(a, g, sm, s);
+    if (whole_width && wpr == 2) return launch_wp<kStaticTables, 2>(a, g, sm, s);
+    return launch_wp<kStaticTables, 0>(a, g, sm, s);
+  }
+  if (whole && a.h == 128 && a.w == 128) return launch_wp<kStaticTerrain, 4, 128>(a, g, sm, s);  // C1
+  if (whole && a.h == 64 && a.w == 64) return launch_wp<kStaticTerrain, 2, 64>(a, g, sm, s);
+  if (whole_width && wpr == 4) return launch_wp<kStaticTerrain, 4>(a, g, sm, s);
+  if (whole_width && wpr == 2) return launch_wp<kStaticTerrain, 2>(a, g, sm, s);
+  return launch_wp<kStaticTerrain, 0>(a, g, sm, s);
 }
 
 }  // namespace ebl
