@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <algorithm>
 #include <cstring>
@@ -968,13 +969,19 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
   EBL_CUDA(cudaStreamWaitEvent(b->pipe_in, b->pipe_ev_start, 0));
   for (int c = 0; c < chunks; ++c) EBL_CUDA(cudaStreamWaitEvent(b->pipe_comp[c], b->pipe_ev_start, 0));
   // chunk boundaries: decreasing sizes (the first chunks start computing early; the last ones,
-  // whose copies finish last, are small), weights chunks, chunks-1, ..., 1
+  // whose copies finish last, are small): weight of chunk c = ratio^c (EBL_PIPE_RATIO overrides the
+  // default for tuning runs; 1 = equal chunks)
   std::vector<int> bound(chunks + 1, 0);
   {
-    const double tot = 0.5 * chunks * (chunks + 1);
-    double acc = 0.0;
+    static const double ratio = [] {
+      const char* e = std::getenv("EBL_PIPE_RATIO");
+      return e ? std::atof(e) : 0.7;
+    }();
+    std::vector<double> wgt(chunks);
+    double tot = 0.0, acc = 0.0;
+    for (int c = 0; c < chunks; ++c) tot += (wgt[c] = std::pow(ratio, c));
     for (int c = 0; c < chunks; ++c) {
-      acc += chunks - c;
+      acc += wgt[c];
       bound[c + 1] = std::min(b->n_envs, static_cast<int>(std::lround(acc / tot * b->n_envs)));
     }
     bound[chunks] = b->n_envs;
