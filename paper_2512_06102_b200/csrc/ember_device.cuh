@@ -240,6 +240,14 @@ __device__ __forceinline__ bool ignite_terrain_tab(const TerrainView& t, const f
   return u < p;
 }
 
+// p = 1 - e^-x in fp32 for the record form: a 4-term Taylor series below x = 0.03 (relative error
+// < 1e-8), 1 - 2^(-x log2e) with MUFU.EX2 above (< 6e-6: the 2^-22 error of ex2 on e^-x, divided by
+// p >= 0.03); within the 1e-5 bar and far inside the decision guard (kGuardRel = 1e-4).
+__device__ __forceinline__ float p_ignite32(float x) {
+  if (x < 0.03f) return x * (1.f - x * (0.5f - x * (1.f / 6.f - x * (1.f / 24.f))));
+  return 1.f - ex2_approx(-x * 1.44269504088896341f);
+}
+
 // The same decision with the candidate's records already loaded (loads hoisted by the caller).
 struct CellRec {
   float4 s0, s1;
@@ -258,7 +266,6 @@ __device__ __forceinline__ CellRec load_rec(const float* __restrict__ slope32, c
 __device__ __forceinline__ bool ignite_terrain_rec_pre(const TerrainView& t, const CellRec& rc, const float* srckw,
                                                        const float* pal_gam, float alpha_l2, int w, int r, int c,
                                                        uint32_t nb, uint64_t m, const DiagCounters& dg) {
-  const double u = bits_to_uniform(m);
   if (!t.force64) {
     const float s[8] = {rc.s0.x, rc.s0.y, rc.s0.z, rc.s0.w, rc.s1.x, rc.s1.y, rc.s1.z, rc.s1.w};
     float lam = 0.f;
@@ -270,13 +277,18 @@ __device__ __forceinline__ bool ignite_terrain_rec_pre(const TerrainView& t, con
     }
     const float x = pal_gam[rc.fv] * lam;
     if (x == 0.f) return false;  // gamma or lambda exactly 0: p = 1 - exp(-0) = 0, u < 0 is false
-    const double p32 = static_cast<double>(-expm1f(-x));
-    if (p32 > 1e-12) {
-      if (u < p32 * (1.0 - kGuardRel)) return true;
-      if (u >= p32 * (1.0 + kGuardRel)) return false;
+    const float p32 = p_ignite32(x);
+    if (p32 > 1e-12f) {
+      // u < p (1 -+ guard)  <=>  m < p (1 -+ guard) 2^53: the thresholds in fp32 (relative rounding
+      // 6e-8, inside the 1e-4 guard) and the 53-bit draw compared as an integer
+      const uint64_t lo = static_cast<uint64_t>(p32 * static_cast<float>((1.0 - kGuardRel) * 0x1p53));
+      const uint64_t hi = static_cast<uint64_t>(p32 * static_cast<float>((1.0 + kGuardRel) * 0x1p53));
+      if (m < lo) return true;
+      if (m >= hi) return false;
     }
   }
   dg.fallback();
+  const double u = bits_to_uniform(m);
   const double p = terrain_p64(t, w, r, c, nb);
   if (fabs(u - p) < kAmbiguousBand) dg.ambiguous();
   return u < p;

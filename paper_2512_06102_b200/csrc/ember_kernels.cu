@@ -129,10 +129,11 @@ __global__ void k_intensity(StepArgs a, float* lam_out, float* p_out) {
         for (int q = 0; q < a.n_pal * 8; ++q) srckw[q] = t.pal_src32[q >> 3] * t.kw32[q & 7];
         lam = terrain_lambda32_rec(a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
                                    a.nfuel + static_cast<size_t>(env) * a.ter_stride, srckw, a.alpha_s_l2, i, nb);
+        p = p_ignite32(t.pal_gam32[t.fuel[i]] * lam);  // the warp kernels' p
       } else {
         lam = terrain_lambda32(t, a.w, r, c, nb);
+        p = -expm1f(-t.pal_gam32[t.fuel[i]] * lam);
       }
-      p = -expm1f(-t.pal_gam32[t.fuel[i]] * lam);
     }
     lam_out[g] = lam;
     p_out[g] = p;
