@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
     }
   }
   if constexpr (MODE == kStaticTerrain) {
-    for (int i = threadIdx.x; i < 512; i += blockDim.x) s_pal[i] = __ldg(a.pal32 + i);
+    for (int i = threadIdx.x; i < 2 * a.n_pal; i += blockDim.x)  // the palette entries in use: src, gam
+      s_pal[i < a.n_pal ? i : 256 + i - a.n_pal] = __ldg(a.pal32 + (i < a.n_pal ? i : 256 + i - a.n_pal));
 #if EBL_PREFETCH
     // the region's static layers are touched only along the fire front: one bulk L2 prefetch per
     // region row (whole env = one contiguous range) hides their first-touch DRAM latency

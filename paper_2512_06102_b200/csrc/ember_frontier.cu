@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(kFrThreads, 8) k_step_frontier(StepArgs a, int
     X[it.r * S + it.j] = x;
   }
   if constexpr (MODE == kStaticTerrain) {
-    for (int i = threadIdx.x; i < 512; i += blockDim.x) s_pal[i] = __ldg(a.pal32 + i);
+    for (int i = threadIdx.x; i < 2 * a.n_pal; i += blockDim.x)  // the palette entries in use: src, gam
+      s_pal[i < a.n_pal ? i : 256 + i - a.n_pal] = __ldg(a.pal32 + (i < a.n_pal ? i : 256 + i - a.n_pal));
     if (threadIdx.x < 8)  // the wind of step 0; a wind schedule reloads it per step
       s_kw[threadIdx.x] = __ldg(a.kw32 + static_cast<size_t>(sched_row(a, a.step)) * a.kw_sched_stride +
                                 static_cast<size_t>(env) * a.kw_stride + threadIdx.x);

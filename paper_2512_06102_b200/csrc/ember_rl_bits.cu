@@ -51,7 +51,8 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_bits(RlArgs g) 
   }
   if (threadIdx.x < 2) s_total[threadIdx.x] = s_newly[threadIdx.x] = s_burn[threadIdx.x] = 0;
   if constexpr (MODE == kStaticTerrain) {
-    for (int i = threadIdx.x; i < 512; i += blockDim.x) s_pal[i] = __ldg(a.pal32 + i);
+    for (int i = threadIdx.x; i < 2 * a.n_pal; i += blockDim.x)  // the palette entries in use: src, gam
+      s_pal[i < a.n_pal ? i : 256 + i - a.n_pal] = __ldg(a.pal32 + (i < a.n_pal ? i : 256 + i - a.n_pal));
     if (threadIdx.x < 8) s_kw[threadIdx.x] = __ldg(a.kw32 + static_cast<size_t>(env) * a.kw_stride + threadIdx.x);
   }
   for (WordIter it(wpr, nwords); it.ok(); it.next()) {
@@ -351,7 +352,8 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
   if (threadIdx.x == 0) s_burning[0] = 0;
   const bool use_rec = kTer && a.nfuel && a.n_pal <= 32;
   if constexpr (kTer) {
-    for (int i = threadIdx.x; i < 512; i += blockDim.x) s_pal[i] = __ldg(a.pal32 + i);
+    for (int i = threadIdx.x; i < 2 * a.n_pal; i += blockDim.x)  // the palette entries in use: src, gam
+      s_pal[i < a.n_pal ? i : 256 + i - a.n_pal] = __ldg(a.pal32 + (i < a.n_pal ? i : 256 + i - a.n_pal));
     if (threadIdx.x < 8) s_kw[threadIdx.x] = __ldg(a.kw32 + static_cast<size_t>(env) * a.kw_stride + threadIdx.x);
     if (use_rec)
       for (int i = threadIdx.x; i < a.n_pal * 8; i += blockDim.x)

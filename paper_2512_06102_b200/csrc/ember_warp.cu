@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
     }
   };
   if constexpr (kTer)
-    for (int i = threadIdx.x; i < 512; i += blockDim.x) s_pal[i] = __ldg(a.pal32 + i);
+    for (int i = threadIdx.x; i < 2 * a.n_pal; i += blockDim.x)  // the palette entries in use: src, gam
+      s_pal[i < a.n_pal ? i : 256 + i - a.n_pal] = __ldg(a.pal32 + (i < a.n_pal ? i : 256 + i - a.n_pal));
   load_wind(sched_row(a, a.step));
   if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_newly = 0;
