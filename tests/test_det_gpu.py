@@ -160,3 +160,30 @@ def test_det_general_form_gradient_vs_dual(port):
     port.ebo_det_loss_grad(gp.h, O.ptr(O.cfg_array(cfg)), 30, O.ptr(fire), O.ptr(mask), 1.0, 1.0, 4, lo, O.ptr(g6))
     assert loss[0] == pytest.approx(lo.value, rel=1e-12)
     np.testing.assert_allclose(grad[0], g6, rtol=1e-9, atol=1e-14)
+
+
+def test_c4_env_shards_sum_to_the_whole():
+    """C4 sharded by env (one process per GPU in production): two halves of the batch, run as
+    separate batches, give per-env losses / gradients identical to the whole batch, and their
+    fixed-order sum equals the whole batch's (distributed.reduce_loss_grad's contract)."""
+    from paper_2512_06102_b200.distributed import env_range, sum_loss_grad
+    n, h, w, steps, seed = 6, 48, 48, 25, 4
+    t = eb.synth_terrain(seed, n, h, w)
+    init = eb.synth_ignitions(seed, t, 4)
+    mask = (np.random.default_rng(1).random((n, h, w)) < 0.2).astype(np.float64)
+
+    def run(ids):
+        b = eb.Batch(len(ids), h, w)
+        b.set_terrain(t.fuel_class[ids], t.elevation[ids], t.class_veg, t.class_den, 30.0)
+        b.set_wind(t.wind_speed[ids], t.wind_direction[ids])
+        b.set_state(init[ids])
+        b.det_set_state_from_fire()
+        b.det_forward(steps, record=True)
+        return b.det_loss_grad(mask[ids])
+
+    loss_all, grad_all = run(list(range(n)))
+    parts = [run(list(range(*env_range(r, 2, n)))) for r in range(2)]
+    assert np.array_equal(np.concatenate([p[0] for p in parts]), loss_all)
+    assert np.array_equal(np.concatenate([p[1] for p in parts]), grad_all)
+    assert sum_loss_grad(loss_all, grad_all)[0] == sum_loss_grad(
+        np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts]))[0]

@@ -101,3 +101,43 @@ def test_gloo_env_sharding_weak_scaling():
         p.join(timeout=60)
     for rank, ids, tmax in res:
         assert ids == list(range(world * 1024)) and tmax == float(world)
+
+
+def _grad_worker(rank, world, port, n_envs, q):
+    from paper_2512_06102_b200.distributed import env_range, reduce_loss_grad
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rs = np.random.default_rng(7)
+    loss_all = rs.random(n_envs)
+    grad_all = rs.standard_normal((n_envs, 6))
+    f, l = env_range(rank, world, n_envs)
+    loss, grad = reduce_loss_grad(dist, loss_all[f:l], grad_all[f:l], n_envs)
+    q.put((rank, loss, grad.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_envs", [(2, 7), (3, 10), (2, 1)])
+def test_c4_gradient_allreduce_gloo(world, n_envs):
+    """C4 env sharding: each rank's per-env loss/gradient rows are gathered and summed in global
+    env order -- bit-identical to the one-process sum, for any rank count."""
+    from paper_2512_06102_b200.distributed import env_range, sum_loss_grad
+    rs = np.random.default_rng(7)
+    loss_all = rs.random(n_envs)
+    grad_all = rs.standard_normal((n_envs, 6))
+    want_loss, want_grad = sum_loss_grad(loss_all, grad_all)
+    covered = []
+    for r in range(world):
+        covered += list(range(*env_range(r, world, n_envs)))
+    assert covered == list(range(n_envs))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grad_worker, args=(r, world, port, n_envs, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for _, loss, grad in res:
+        assert loss == want_loss and grad == want_grad.tolist()
