@@ -173,7 +173,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "tiled", "resident", "paired", "frontier", "warp"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "tiled", "resident", "paired", "frontier", "warp", "warp2"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pipeline", type=int, default=0,
                     help="env chunks of the e2e host-buffer pipeline (0 = library default)")
@@ -205,7 +205,7 @@ def main():
     b.set_terrain(terrain.fuel_class, terrain.elevation, terrain.class_veg, terrain.class_den, 30.0)
     b.set_wind(terrain.wind_speed, terrain.wind_direction)
     b.set_config(None)
-    b.set_kernel({"auto": 0, "tiled": 1, "resident": 2, "paired": 4, "frontier": 5, "warp": 6}[args.kernel])
+    b.set_kernel({"auto": 0, "tiled": 1, "resident": 2, "paired": 4, "frontier": 5, "warp": 6, "warp2": 7}[args.kernel])
     b.set_key(SEED, 0, first_stream=env0)
 
     init_dev = torch.from_numpy(init).to(f"cuda:{local}")
@@ -326,7 +326,8 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": {"tiled": "k_step_tile", "frontier": "k_step_frontier", "resident": "k_step_blocked",
-                                    "paired": "k_step_blocked"}.get(args.kernel, "k_step_warp"),
+                                    "paired": "k_step_blocked", "warp2": "k_step_warp2"}.get(
+                             args.kernel, "k_step_warp"),
                          "alg_bytes_per_launch": alg_bytes if args.kernel != "tiled"
                          else alg_bytes // CA_STEPS,
                          "kernel_ms": kern_s * 1e3},

@@ -178,6 +178,7 @@ int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* sp
 #define EBL_KERNEL_BLOCKED 3
 #define EBL_KERNEL_FRONTIER 5
 #define EBL_KERNEL_WARP 6
+#define EBL_KERNEL_WARP2 7 /* warp-local, two whole envs per 256-thread CTA */
 #define EBL_KERNEL_PAIRED 4 /* resident, two envs per CTA sharing 256 threads and one pooled
                                active list (H*W <= 32768); selectable only (AUTO does not pair:
                                slower on C1, ember_kernels.h) */

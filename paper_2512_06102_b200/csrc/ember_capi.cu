@@ -317,7 +317,10 @@ bool use_frontier(const ebl_batch* b) {
 bool use_warp(const ebl_batch* b) { return b->kernel == EBL_KERNEL_WARP || b->kernel == EBL_KERNEL_AUTO; }
 
 cudaError_t launch_ca(const ebl_batch* b, const ebl::StepArgs& a, const ebl::BlockGeom& g, cudaStream_t s) {
-  if (use_warp(b) && g.envs_per_cta == 1) return ebl::launch_step_warp(a, b->mode, g, s);
+  const bool whole = g.halo_rows == 0 && g.halo_cols == 0 && g.tile_h >= b->h && g.tile_w >= b->w;
+  if (b->kernel == EBL_KERNEL_WARP2 && whole && a.store_lo == 0 && a.store_hi == b->h && a.n_peers == 0)
+    return ebl::launch_step_warp2(a, b->mode, g.n_steps, s);
+  if ((use_warp(b) || b->kernel == EBL_KERNEL_WARP2) && g.envs_per_cta == 1) return ebl::launch_step_warp(a, b->mode, g, s);
   return ebl::launch_step_blocked(a, b->mode, g, s);
 }
 
@@ -844,7 +847,9 @@ uint64_t ebl_batch_step_index(const ebl_batch* b) { return b ? b->step : 0; }
 
 int ebl_batch_set_kernel(ebl_batch* b, int which) {
   if (int e = check_batch(b)) return e;
-  if (which < EBL_KERNEL_AUTO || which > EBL_KERNEL_WARP) return set_err(EBL_EINVAL, "unknown kernel");
+  if (which < EBL_KERNEL_AUTO || which > EBL_KERNEL_WARP2) return set_err(EBL_EINVAL, "unknown kernel");
+  if (which == EBL_KERNEL_WARP2 && (!ebl::resident_fits(b->h, b->w) || ebl::warp2_smem_bytes(b->h, b->w) > ebl::kResMaxSmem))
+    return set_err(EBL_EINVAL, "two envs per CTA need resident envs whose pair fits shared memory");
   if (which == EBL_KERNEL_FRONTIER && !ebl::frontier_fits(b->h, b->w))
     return set_err(EBL_EINVAL, "the frontier kernel needs a resident env with H*W <= 16384");
   if ((which == EBL_KERNEL_RESIDENT || which == EBL_KERNEL_PAIRED) && !ebl::resident_fits(b->h, b->w))

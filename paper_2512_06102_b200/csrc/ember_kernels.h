@@ -37,6 +37,8 @@ cudaError_t launch_step_frontier(const StepArgs& a, int mode, int n_steps, cudaS
 size_t warp_smem_bytes(int h, int w);
 bool warp_fits(int h, int w);
 cudaError_t launch_step_warp(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s);
+size_t warp2_smem_bytes(int h, int w);
+cudaError_t launch_step_warp2(const StepArgs& a, int mode, int n_steps, cudaStream_t s);
 
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s);
 cudaError_t launch_det_loss(const DetArgs& d, cudaStream_t s);

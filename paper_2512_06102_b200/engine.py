@@ -17,6 +17,7 @@ from ._lib import EnvConfig, EnvState, SimConfig, check, lib
 
 UNBURNED, BURNING, BURNED = 0, 1, 2
 KERNEL_AUTO, KERNEL_TILED, KERNEL_RESIDENT, KERNEL_BLOCKED, KERNEL_PAIRED, KERNEL_FRONTIER, KERNEL_WARP = 0, 1, 2, 3, 4, 5, 6
+KERNEL_WARP2 = 7
 
 
 def _ptr(a: np.ndarray | None):

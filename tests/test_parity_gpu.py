@@ -13,7 +13,7 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 KERNELS = [eb.KERNEL_TILED, eb.KERNEL_RESIDENT, eb.KERNEL_BLOCKED, eb.KERNEL_PAIRED, eb.KERNEL_FRONTIER,
-           eb.KERNEL_WARP]
+           eb.KERNEL_WARP, eb.KERNEL_WARP2]
 REL_TOL = 1e-5  # north_star: lambda and p within 1e-5 relative in fp32
 
 
@@ -195,6 +195,8 @@ def test_kernels_identical_ragged(port, h, w):
         variants.append((eb.KERNEL_FRONTIER, None))
     if h * w <= 65536:
         variants.append((eb.KERNEL_WARP, None))
+    if h * w <= 16384:
+        variants.append((eb.KERNEL_WARP2, None))
     for kernel, tiling in variants:
         b = eb.Batch(n, h, w)
         b.set_terrain(cls, el, veg, den, 25.0)
