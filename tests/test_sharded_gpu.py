@@ -53,3 +53,42 @@ def test_rows_device_roundtrip():
     eb._lib.check(eb.lib().ebl_batch_rows_device(b.handle, 30, 5, buf.data_ptr(), 1))
     st[:, 30:35] = 2
     assert np.array_equal(b.get_state(), st)
+
+
+@pytest.mark.slow
+def test_c3_full_size_shards_equal_unsharded():
+    """BASELINE C3 at full size (one 16384 x 16384 landscape, wind 6 from the west, 64 ignitions,
+    500 steps): 4 fused row shards == the unsharded run, bit for bit, and the size-independent
+    properties hold -- cells conserved, burnt only grows, every burnt or burning cell is burnable
+    or an ignition, the shard counts add up to the landscape's."""
+    h = w = 16384
+    steps = 500
+    t = eb.synth_terrain(0, 1, h, w)
+    t.wind_speed[:] = 6.0
+    t.wind_direction[:] = 0.0
+    init = eb.synth_ignitions(0, t, 64)
+    full = eb.Batch(1, h, w)
+    full.set_terrain(t.fuel_class, t.elevation, t.class_veg, t.class_den, 30.0)
+    full.set_wind(t.wind_speed, t.wind_direction)
+    full.set_state(init)
+    full.set_key(0, 0, first_stream=0)
+    full.step(200)
+    mid = full.get_state()[0]
+    full.step(steps - 200)
+    want = full.get_state()[0]
+    cnt = full.counts()[0]
+    full.close()
+    assert cnt[:3].tolist() == [int((want == k).sum()) for k in range(3)]
+    assert cnt[:3].sum() == h * w
+    assert ((want == 2) | (mid != 2)).all(), "a burnt cell never changes"
+    assert (want != 0).sum() >= (mid != 0).sum() >= (init[0] != 0).sum()
+    burnable = t.class_veg[t.fuel_class[0]] > -1.0
+    assert ((want == 0) | burnable | (init[0] != 0)).all()
+    sh = ShardedLandscape(t, 4, halo=8, fused=True)
+    sh.set_state(init[0])
+    sh.set_key(0, 0, 0)
+    sh.step(steps)
+    got = sh.get_state()
+    assert np.array_equal(got, want)
+    total = sum(b.counts()[0] for b in sh.batches)
+    assert total[:3].tolist() == cnt[:3].tolist()
