@@ -89,7 +89,6 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_bits(RlArgs g) 
     uint32_t* Bn = Bp[cur ^ 1];
     // ---- action + drop -------------------------------------------------------------------
     if (threadIdx.x == 0) {
-      s_total[par ^ 1] = s_newly[par ^ 1] = s_burn[par ^ 1] = 0;
       s_action = g.actions ? g.actions[env]
                            : static_cast<int>(below(cell_bits53(key_prefix(g.seed, e.stream,
                                                                            static_cast<uint64_t>(e.step)),
@@ -97,6 +96,9 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_bits(RlArgs g) 
                                                     n));
     }
     __syncthreads();
+    // the next step's counters: every thread has read this slot (as the previous step's) before
+    // the barrier above; the next step writes it after this step's last barrier
+    if (threadIdx.x == 0) s_total[par ^ 1] = s_newly[par ^ 1] = s_burn[par ^ 1] = 0;
     if (threadIdx.x < 9) {
       const int r = s_action / W + static_cast<int>(threadIdx.x) / 3 - 1;
       const int c = s_action % W + static_cast<int>(threadIdx.x) % 3 - 1;
@@ -420,8 +422,10 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
         }
       }
     }
-    if (threadIdx.x == 0) s_newly[par ^ 1] = s_gone[par ^ 1] = 0;  // the next step's counters
     __syncthreads();
+    // the next step's counters (read as the previous step's before the barrier above, written by
+    // the next step after this step's last barrier)
+    if (threadIdx.x == 0) s_newly[par ^ 1] = s_gone[par ^ 1] = 0;
     // ---- warp-local CA step (k_step_warp) -----------------------------------------------------------
     int newly = 0, burnt = 0;
     for (int rb = 0; rb < H; rb += kRlBitsThreads) {

@@ -167,3 +167,34 @@ def test_tanker_host_actions(port, kernel, h, w):
         r, _ = env.step(acts[k])
         assert [want[e]["rewards"][k] for e in range(n)] == r.tolist()
     assert np.array_equal(env.fire(), np.stack([x["fire"] for x in want]))
+
+
+@pytest.mark.slow
+def test_c2_full_size_rollout(port):
+    """BASELINE C2 at full size (16384 envs of 64 x 64, device random (x, y) policy, 256-step cap,
+    auto-reset): the warp-local and the pooled-list tanker kernels agree bit for bit over a 300-step
+    fused rollout (layers, wet layers, episode counters, reward sums), and envs sampled across the
+    batch match the C restatement step for step."""
+    n, h, w, seed, steps = 16384, 64, 64, 11, 300
+    t = eb.synth_terrain(seed, n, h, w)
+    cfg = [0.12, 0.2, 0.4, 1.0, 1.0, 0.6]
+    res = {}
+    for kernel in (eb.KERNEL_AUTO, eb.KERNEL_RESIDENT):
+        env = eb.VecFireEnv(n, variant=eb.RL_TANKER, terrain=t, sim_cfg=cfg, ignitions=5, max_steps=256)
+        env.batch.set_kernel(kernel)
+        env.reset(seed)
+        rs, ep = env.rollout(steps)
+        st = env.env_states()
+        res[kernel] = (env.fire(), env.wet(), rs, ep, [(s.step, s.episode) for s in st])
+    a, b = res[eb.KERNEL_AUTO], res[eb.KERNEL_RESIDENT]
+    for x, y in zip(a[:4], b[:4]):
+        assert np.array_equal(x, y)
+    assert a[4] == b[4]
+    assert a[3].sum() > n // 2, "most envs should finish an episode within 300 steps"
+    ids = [0, 5000, 16383]
+    sub = eb.Terrain(t.fuel_class[ids], t.elevation[ids], t.wind_speed[ids], t.wind_direction[ids],
+                     t.class_veg, t.class_den, t.cellsize)
+    want = _port_tanker(port, sub, cfg, seed, ids, steps, O.TankerCfg(5, 256, 1))
+    for i, e in enumerate(ids):
+        assert np.array_equal(a[0][e], want[i]["fire"]) and np.array_equal(a[1][e], want[i]["wet"])
+        assert a[2][e] == sum(want[i]["rewards"]) and a[3][e] == sum(want[i]["dones"])
