@@ -40,6 +40,7 @@ __device__ __forceinline__ void block_sum_n(double (&v)[N], double* red) {
   for (int q = 0; q < N; ++q)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+  __syncthreads();  // red[] may still be read by a previous call
   if ((threadIdx.x & 31) == 0)
 #pragma unroll
     for (int q = 0; q < N; ++q) red[q * 32 + (threadIdx.x >> 5)] = v[q];
