@@ -116,6 +116,10 @@ struct ebl_batch {
   uint32_t env_id0 = 0;
   uint64_t rl_seed = 0;
   DevBuf<ebl::RlEnv> rl_env;
+  // bit-resident tanker state (warp-local tanker kernel): rl_bits_valid = the bits equal the
+  // current layers; rl_bits_truth = the bits are newer than the byte layers (rebuilt on demand)
+  DevBuf<uint32_t> rl_bits;
+  bool rl_bits_valid = false, rl_bits_truth = false;
   DevBuf<uint8_t> wet, done, mask;
   DevBuf<double> reward, reward_sum;
   DevBuf<int32_t> actions, error, episodes;
@@ -163,6 +167,26 @@ Cfg6 cfg6(const ebl_sim_config& c) {
 int check_batch(const ebl_batch* b) {
   if (!b) return set_err(EBL_EINVAL, "null batch");
   return EBL_OK;
+}
+
+// Byte layers up to date before any access other than the warp-local tanker kernel: rebuild them
+// from the bit-resident tanker state when that is newer, and treat the bits as stale afterwards
+// (the caller may write the bytes).
+int rl_sync_bytes(ebl_batch* b) {
+  if (b->rl_bits_truth) {
+    EBL_CUDA(cudaSetDevice(b->device));
+    EBL_CUDA(ebl::launch_rl_bits_to_bytes(b->rl_bits.p, b->state[b->cur].p, b->wet.p, b->n_envs, b->h, b->w,
+                                          b->stream));
+    b->rl_bits_truth = false;
+  }
+  b->rl_bits_valid = false;
+  return EBL_OK;
+}
+
+// check_batch + rl_sync_bytes: the entry of every public call that touches the layers
+int check_sync(ebl_batch* b) {
+  if (int e = check_batch(b)) return e;
+  return rl_sync_bytes(b);
 }
 
 // Brings the derived device-side statics in line with (config, layers).
@@ -590,7 +614,7 @@ int ebl_batch_synth_terrain(ebl_batch* b, uint64_t seed, uint32_t env_id0, doubl
 }
 
 int ebl_batch_synth_ignitions(ebl_batch* b, uint64_t seed, uint32_t env_id0, int count, int* placed_total) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   if (b->mode != ebl::kStaticTerrain) return set_err(EBL_ESTATE, "ignitions need terrain-form static layers");
   if (count < 0) return set_err(EBL_EINVAL, "EnvConfig: ignition_count must be >= 0");
   if (int e = prepare(b)) return e;  // burnable flags live in pal64[512..767]
@@ -767,7 +791,7 @@ int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* sp
 }
 
 int ebl_step_batch_record(ebl_batch* b, int n_steps, void* traj, int on_device) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   if (n_steps < 0 || (n_steps > 0 && !traj)) return set_err(EBL_EINVAL, "bad trajectory arguments");
   if (n_steps == 0) return EBL_OK;
   const size_t bytes = static_cast<size_t>(n_steps) * b->n_envs * b->ncell;
@@ -789,7 +813,7 @@ int ebl_step_batch_record(ebl_batch* b, int n_steps, void* traj, int on_device) 
 }
 
 int ebl_batch_set_state(ebl_batch* b, const uint8_t* states) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   // Like the reference's FireLayer (a plain Grid<FireState>, grid.hpp:100) member layers are
   // not validated; a byte other than 1/2 takes the Unburned path as in engine.cpp:15-25.
   const size_t total = b->ncell * b->n_envs;
@@ -801,7 +825,7 @@ int ebl_batch_set_state(ebl_batch* b, const uint8_t* states) {
 }
 
 int ebl_batch_get_state(ebl_batch* b, uint8_t* states) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   EBL_CUDA(cudaSetDevice(b->device));
   EBL_CUDA(cudaMemcpyAsync(states, b->state[b->cur].p, b->ncell * b->n_envs, cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
@@ -809,19 +833,22 @@ int ebl_batch_get_state(ebl_batch* b, uint8_t* states) {
 }
 
 int ebl_batch_set_state_device(ebl_batch* b, const void* d) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   EBL_CUDA(cudaMemcpyAsync(b->state[b->cur].p, d, b->ncell * b->n_envs, cudaMemcpyDeviceToDevice, b->stream));
   b->counts_valid = false;
   return EBL_OK;
 }
 
 int ebl_batch_get_state_device(ebl_batch* b, void* d) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   EBL_CUDA(cudaMemcpyAsync(d, b->state[b->cur].p, b->ncell * b->n_envs, cudaMemcpyDeviceToDevice, b->stream));
   return EBL_OK;
 }
 
-void* ebl_batch_state_device_ptr(ebl_batch* b) { return b ? b->state[b->cur].p : nullptr; }
+void* ebl_batch_state_device_ptr(ebl_batch* b) {
+  if (!b || rl_sync_bytes(b) != EBL_OK) return nullptr;
+  return b->state[b->cur].p;
+}
 
 int ebl_batch_set_key(ebl_batch* b, uint64_t seed, uint64_t step, const uint64_t* streams,
                       uint64_t first_stream) {
@@ -862,7 +889,7 @@ int ebl_batch_set_kernel(ebl_batch* b, int which) {
 }
 
 int ebl_step_batch(ebl_batch* b, int n_steps) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
   if (n_steps == 0) return EBL_OK;
   if (int e = prepare(b)) return e;
@@ -945,7 +972,7 @@ int ebl_batch_set_pipeline(ebl_batch* b, int chunks) {
 // independent; the RNG is keyed by stream, not by launch).  Pinned host buffers are needed for
 // the copies to be asynchronous.
 int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* final_states) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   if (!initial || !final_states) return set_err(EBL_EINVAL, "null state buffer");
   if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
   if (int e = prepare(b)) return e;
@@ -1047,8 +1074,8 @@ int ebl_batch_set_row_offset(ebl_batch* b, int64_t row_off) {
 }
 
 int ebl_batch_copy_rows(ebl_batch* dst, int dst_row, const ebl_batch* src, int src_row, int n_rows) {
-  if (int e = check_batch(dst)) return e;
-  if (int e = check_batch(src)) return e;
+  if (int e = check_sync(dst)) return e;
+  if (int e = check_sync(const_cast<ebl_batch*>(src))) return e;
   if (dst->w != src->w || dst->n_envs != src->n_envs) return set_err(EBL_EINVAL, "copy_rows: widths/env counts differ");
   if (n_rows < 0 || dst_row < 0 || src_row < 0 || dst_row + n_rows > dst->h || src_row + n_rows > src->h)
     return set_err(EBL_EINVAL, "copy_rows: row range outside a layer");
@@ -1096,7 +1123,7 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
   if (halo < 1) return set_err(EBL_EINVAL, "halo must be >= 1");
   for (int s = 0; s < n_shards; ++s) {
     ebl_batch* b = shards[s];
-    if (int e = check_batch(b)) return e;
+    if (int e = check_sync(b)) return e;
     if (b->n_envs != 1 || b->w != shards[0]->w) return set_err(EBL_EINVAL, "shards: one env each, equal widths");
     if (b->band_lo < 0) return set_err(EBL_ESTATE, "shards: ebl_batch_set_band first");
     if (b->kernel == EBL_KERNEL_TILED || b->kernel == EBL_KERNEL_FRONTIER)
@@ -1191,7 +1218,7 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
 }
 
 int ebl_batch_rows_device(ebl_batch* b, int row0, int n_rows, void* dptr, int to_batch) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   if (n_rows < 0 || row0 < 0 || row0 + n_rows > b->h) return set_err(EBL_EINVAL, "rows: range outside the layer");
   EBL_CUDA(cudaSetDevice(b->device));
   const size_t bytes = static_cast<size_t>(n_rows) * b->w;
@@ -1225,7 +1252,7 @@ int ebl_batch_set_tiling(ebl_batch* b, int tile_h, int tile_w, int halo) {
 }
 
 int ebl_batch_counts(ebl_batch* b, int32_t* out) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   EBL_CUDA(cudaSetDevice(b->device));
   if (!b->counts_valid) {
     EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
@@ -1242,7 +1269,7 @@ int ebl_batch_intensity(ebl_batch* b, float* lambda, float* p) {
 }
 
 int ebl_batch_intensity_form(ebl_batch* b, int record_form, float* lambda, float* p) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   if (int e = prepare(b)) return e;
   const size_t total = b->ncell * b->n_envs;
   DevBuf<float> dl, dp;
@@ -1385,14 +1412,24 @@ int validate_env(const ebl_env_config* c) {  // rl_env.cpp:80-93
 
 // Tanker step/rollout: the bit-plane kernel, or the byte kernel when EBL_KERNEL_TILED is
 // selected (an independent implementation kept for cross-checking).
-cudaError_t tanker_launch(ebl_batch* b, const ebl::RlArgs& g) {
-  if (b->kernel != EBL_KERNEL_TILED && ebl::rl_bits_fits(b->h, b->w)) {
-    // the warp-local kernel (two barriers per step) unless the pooled-list one is requested
-    if (b->kernel != EBL_KERNEL_RESIDENT && ebl::rl_warp_smem_bytes(b->h, b->w) <= ebl::kResMaxSmem)
-      return ebl::launch_rl_tanker_warp(g, b->mode, b->stream);
-    return ebl::launch_rl_tanker_bits(g, b->mode, b->stream);
+int tanker_launch(ebl_batch* b, ebl::RlArgs g) {
+  if (b->kernel != EBL_KERNEL_TILED && ebl::rl_bits_fits(b->h, b->w) && b->kernel != EBL_KERNEL_RESIDENT &&
+      ebl::rl_warp_smem_bytes(b->h, b->w) <= ebl::kResMaxSmem) {
+    // the warp-local kernel (two barriers per step); its state stays bit-resident between launches
+    const size_t words = static_cast<size_t>(b->n_envs) * 3 * b->h * ((b->w + 31) / 32);
+    EBL_CUDA(b->rl_bits.alloc(words));
+    g.bits = b->rl_bits.p;
+    g.bits_in = b->rl_bits_valid ? 1 : 0;
+    EBL_CUDA(ebl::launch_rl_tanker_warp(g, b->mode, b->stream));
+    b->rl_bits_valid = b->rl_bits_truth = true;
+    return EBL_OK;
   }
-  return ebl::launch_rl_tanker(g, b->mode, b->stream);
+  if (int e = rl_sync_bytes(b)) return e;
+  if (b->kernel != EBL_KERNEL_TILED && ebl::rl_bits_fits(b->h, b->w))
+    EBL_CUDA(ebl::launch_rl_tanker_bits(g, b->mode, b->stream));  // pooled-list kernel (RESIDENT)
+  else
+    EBL_CUDA(ebl::launch_rl_tanker(g, b->mode, b->stream));
+  return EBL_OK;
 }
 
 ebl::RlArgs rl_args(ebl_batch* b) {
@@ -1417,7 +1454,7 @@ ebl::RlArgs rl_args(ebl_batch* b) {
 
 int ebl_rl_configure(ebl_batch* b, int variant, const ebl_env_config* c, int tanker_ignitions,
                      int tanker_max_steps, uint32_t env_id0) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   if (variant != EBL_RL_REFERENCE && variant != EBL_RL_TANKER) return set_err(EBL_EINVAL, "unknown RL variant");
   if (b->ncell > static_cast<size_t>(ebl::kRlMaxCells))
     return set_err(EBL_EINVAL, "RL envs must have at most 16384 cells (layer resident in shared memory)");
@@ -1460,7 +1497,7 @@ int ebl_rl_configure(ebl_batch* b, int variant, const ebl_env_config* c, int tan
 }
 
 int ebl_rl_reset(ebl_batch* b, uint64_t seed, const uint64_t* streams, const uint8_t* mask) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
   if (int e = prepare(b)) return e;
   EBL_CUDA(cudaSetDevice(b->device));
@@ -1538,9 +1575,10 @@ int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* d
   g.reward = device_io && reward ? reward : b->reward.p;
   g.done = device_io && done ? done : b->done.p;
   if (b->rl_variant == EBL_RL_REFERENCE) {
+    if (int e = rl_sync_bytes(b)) return e;
     EBL_CUDA(ebl::launch_rl_ref_step(g, b->mode, b->stream));
   } else {
-    EBL_CUDA(tanker_launch(b, g));
+    if (int e = tanker_launch(b, g)) return e;
   }
   b->launches += 1;
   b->steps_done += 1;
@@ -1575,7 +1613,7 @@ int ebl_rl_rollout(ebl_batch* b, int n_steps, double* reward_sum, int32_t* episo
   g.n_steps = n_steps;
   g.reward_sum = b->reward_sum.p;
   g.episodes = b->episodes.p;
-  EBL_CUDA(tanker_launch(b, g));
+  if (int e = tanker_launch(b, g)) return e;
   b->launches += 1;
   b->steps_done += n_steps;
   b->counts_valid = false;
@@ -1586,7 +1624,7 @@ int ebl_rl_rollout(ebl_batch* b, int n_steps, double* reward_sum, int32_t* episo
 }
 
 int ebl_rl_observe(ebl_batch* b, double* obs) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   if (b->rl_variant != EBL_RL_REFERENCE) return set_err(EBL_ESTATE, "observe needs the reference variant");
   const int osz = ebl_env_observation_size(&b->env_cfg);
   const size_t total = static_cast<size_t>(b->n_envs) * osz;
@@ -1627,7 +1665,7 @@ int ebl_rl_set_env_states(ebl_batch* b, const ebl_env_state* in) {
 }
 
 int ebl_rl_get_wet(ebl_batch* b, uint8_t* wet) {
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
   EBL_CUDA(cudaMemcpyAsync(wet, b->wet.p, b->ncell * b->n_envs, cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
@@ -1746,7 +1784,7 @@ int ebl_det_set_state(ebl_batch* b, const double* un, const double* burn, const 
 }
 
 int ebl_det_set_state_from_fire(ebl_batch* b) {  // state_from_fire (engine.cpp:42-52)
-  if (int e = check_batch(b)) return e;
+  if (int e = check_sync(b)) return e;
   EBL_CUDA(cudaSetDevice(b->device));
   if (int e = det_alloc(b)) return e;
   const int c = b->det_cur * 3;

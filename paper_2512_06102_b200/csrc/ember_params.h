@@ -141,6 +141,10 @@ struct RlArgs {
   int n_steps;                    // fused rollout length (tanker)
   double* reward_sum;             // [n_envs] (rollout)
   int32_t* episodes;              // [n_envs] (rollout)
+  // bit-resident tanker state (warp-local tanker kernel): [n_envs][3 planes B, X, WET][h][wpr] words;
+  // bits_in: load from it (else from the byte layers); the kernel always stores it (not the bytes)
+  uint32_t* bits;
+  int bits_in;
 };
 
 }  // namespace ebl

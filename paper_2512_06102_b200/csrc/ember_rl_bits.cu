@@ -10,6 +10,7 @@
 // Identical semantics to the byte kernel k_rl_tanker.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "ember_bits.cuh"
@@ -362,21 +363,29 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
         s_srckw[i] = __ldg(a.pal32 + (i >> 3)) * __ldg(a.kw32 + static_cast<size_t>(env) * a.kw_stride + (i & 7));
   }
   int burning0 = 0;
+  const size_t plane_words = static_cast<size_t>(H) * wpr;
+  uint32_t* const gbits = g.bits ? g.bits + static_cast<size_t>(env) * 3 * plane_words : nullptr;
   for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
-    const uint8_t* src = st + it.r * W + 32 * it.j;
-    const uint8_t* wsrc = wt + it.r * W + 32 * it.j;
-    const int nc = min(32, W - 32 * it.j);
     uint32_t b = 0u, x = 0u, wb = 0u;
-    if (vec) {
-      bytes_to_bits(src, b, x);
-      uint32_t w1, w2;
-      bytes_to_bits(wsrc, w1, w2);  // wet bytes are 0/1
-      wb = w1;
+    if (g.bits_in) {  // bit-resident state of the previous launch: 1/8 of the byte traffic
+      b = gbits[it.idx];
+      x = gbits[plane_words + it.idx];
+      wb = gbits[2 * plane_words + it.idx];
     } else {
-      for (int k = 0; k < nc; ++k) {
-        b |= static_cast<uint32_t>(src[k] == 1) << k;
-        x |= static_cast<uint32_t>(src[k] == 2) << k;
-        wb |= static_cast<uint32_t>(wsrc[k] != 0) << k;
+      const uint8_t* src = st + it.r * W + 32 * it.j;
+      const uint8_t* wsrc = wt + it.r * W + 32 * it.j;
+      const int nc = min(32, W - 32 * it.j);
+      if (vec) {
+        bytes_to_bits(src, b, x);
+        uint32_t w1, w2;
+        bytes_to_bits(wsrc, w1, w2);  // wet bytes are 0/1
+        wb = w1;
+      } else {
+        for (int k = 0; k < nc; ++k) {
+          b |= static_cast<uint32_t>(src[k] == 1) << k;
+          x |= static_cast<uint32_t>(src[k] == 2) << k;
+          wb |= static_cast<uint32_t>(wsrc[k] != 0) << k;
+        }
       }
     }
     Bp0[ro(it.r + 1) + it.j] = b;
@@ -604,6 +613,12 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
   const uint32_t* Bs = cur ? Bp1 : Bp0;
   for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
     const uint32_t b = Bs[ro(it.r + 1) + it.j], x = X[ro(it.r) + it.j], wb = WET[ro(it.r) + it.j];
+    if (gbits) {  // bit-resident (the byte layers are rebuilt on demand, ebl_rl_bits_to_bytes)
+      gbits[it.idx] = b;
+      gbits[plane_words + it.idx] = x;
+      gbits[2 * plane_words + it.idx] = wb;
+      continue;
+    }
     uint8_t* dst = st + it.r * W + 32 * it.j;
     uint8_t* wdst = wt + it.r * W + 32 * it.j;
     if (vec) {
@@ -622,6 +637,41 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
     if (g.reward_sum) g.reward_sum[env] += rsum;
     if (g.episodes) g.episodes[env] += finished;
   }
+}
+
+// Bit-resident tanker state -> byte layers (state, wet): one thread per (env, row, word).
+__global__ void k_rl_bits_to_bytes(const uint32_t* __restrict__ bits, uint8_t* state, uint8_t* wet, int n_envs, int H,
+                                   int W) {
+  const int wpr = (W + 31) >> 5;
+  const size_t plane = static_cast<size_t>(H) * wpr;
+  const size_t total = plane * n_envs;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t env = i / plane, k = i - env * plane;
+    const int r = static_cast<int>(k / wpr), j = static_cast<int>(k - static_cast<size_t>(r) * wpr);
+    const uint32_t* eb = bits + env * 3 * plane;
+    const uint32_t b = eb[k], x = eb[plane + k], wb = eb[2 * plane + k];
+    uint8_t* dst = state + env * H * W + static_cast<size_t>(r) * W + 32 * j;
+    uint8_t* wdst = wet + env * H * W + static_cast<size_t>(r) * W + 32 * j;
+    const int nc = min(32, W - 32 * j);
+    if (nc == 32 && (W & 15) == 0) {
+      bits_to_bytes(b, x, dst);
+      bits_to_bytes(wb, 0u, wdst);
+    } else {
+      for (int c = 0; c < nc; ++c) {
+        dst[c] = static_cast<uint8_t>(((b >> c) & 1u) | (((x >> c) & 1u) << 1));
+        wdst[c] = static_cast<uint8_t>((wb >> c) & 1u);
+      }
+    }
+  }
+}
+
+cudaError_t launch_rl_bits_to_bytes(const uint32_t* bits, uint8_t* state, uint8_t* wet, int n_envs, int h, int w,
+                                    cudaStream_t s) {
+  const size_t total = static_cast<size_t>(n_envs) * h * ((w + 31) / 32);
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 16));
+  k_rl_bits_to_bytes<<<blocks, 256, 0, s>>>(bits, state, wet, n_envs, h, w);
+  return cudaGetLastError();
 }
 
 size_t rl_warp_smem_bytes(int h, int w) {
