@@ -1673,6 +1673,9 @@ int ebl_rl_get_wet(ebl_batch* b, uint8_t* wet) {
 }
 
 // ---- deterministic mode (engine.hpp:147-245) and its adjoint (C4) ---------------------------
+#ifndef EBL_DET_FUSED  // one fused backward kernel per step (0: back1 + back2)
+#define EBL_DET_FUSED 1
+#endif
 namespace {
 int det_alloc(ebl_batch* b) {
   const size_t n = b->ncell * b->n_envs;
@@ -1817,12 +1820,26 @@ int ebl_det_forward(ebl_batch* b, int n_steps, int record) {
     if (int e = det_tables(b)) return e;
   const size_t n = b->ncell * b->n_envs;
   if (record) EBL_CUDA(b->traj.alloc(3 * n * std::max(1, n_steps)));
+  double* const tu = b->traj.p;
+  double* const tbn = b->traj.p + n * std::max(1, n_steps);
   for (int t = 0; t < n_steps; ++t) {
     ebl::DetArgs d = det_args(b);
     if (record) {
-      d.traj_un = b->traj.p;
-      d.traj_burn = b->traj.p + n * n_steps;
+      // the trajectory slots are the states: step t reads slot t (step 0: the state buffers, which
+      // it copies into slot 0) and writes slot t+1 (the last step: the state buffers); bd and the
+      // output state ping-pong as without recording
       d.traj_lam = b->traj.p + 2 * n * n_steps;
+      if (t == 0) {
+        d.traj_un = tu;
+        d.traj_burn = tbn;
+      } else {
+        d.un = tu + t * n;
+        d.burn = tbn + t * n;
+      }
+      if (t + 1 < n_steps) {
+        d.un_o = tu + (t + 1) * n;
+        d.burn_o = tbn + (t + 1) * n;
+      }
     }
     EBL_CUDA(ebl::launch_det_forward(d, t, b->stream));
     b->det_cur ^= 1;
@@ -1841,9 +1858,9 @@ int ebl_det_loss_grad(ebl_batch* b, const double* mask, double bce_w, double mse
   if (pool < 1 || !(bce_w >= 0.0) || !(mse_w >= 0.0) || (bce_w == 0.0 && mse_w == 0.0))
     return set_err(EBL_EINVAL, "LossConfig: weights >= 0, one positive, pool_size >= 1");
   const size_t n = b->ncell * b->n_envs;
-  const int bpe = static_cast<int>((b->ncell + 255) / 256);
+  const int bpe = std::max(static_cast<int>((b->ncell + 255) / 256), ebl::det_blocks_per_env(b->h, b->w));
   EBL_CUDA(b->det_mask.alloc(n));
-  EBL_CUDA(b->adj.alloc(4 * n));
+  EBL_CUDA(b->adj.alloc(6 * n));
   EBL_CUDA(b->acc.alloc(static_cast<size_t>(b->n_envs) * bpe * 8));
   EBL_CUDA(b->det_loss.alloc(b->n_envs));
   EBL_CUDA(b->det_grad.alloc(static_cast<size_t>(b->n_envs) * 6));
@@ -1866,9 +1883,19 @@ int ebl_det_loss_grad(ebl_batch* b, const double* mask, double bce_w, double mse
   d.traj_lam = b->traj.p + 2 * n * std::max(1, b->traj_steps);
   d.inv_p_base = 1.0 / b->cfg.p_base;
   EBL_CUDA(ebl::launch_det_loss(d, b->stream));
-  for (int t = b->traj_steps - 1; t >= 0; --t) EBL_CUDA(ebl::launch_det_backward(d, t, b->stream));
+#if EBL_DET_FUSED
+  d.A_un_o = b->adj.p + 4 * n;  // fused backward: adjoints double-buffered
+  d.A_burn_o = b->adj.p + 5 * n;
+#endif
+  for (int t = b->traj_steps - 1; t >= 0; --t) {
+    EBL_CUDA(ebl::launch_det_backward(d, t, b->stream));
+    if (d.A_un_o) {
+      std::swap(d.A_un, d.A_un_o);
+      std::swap(d.A_burn, d.A_burn_o);
+    }
+  }
   EBL_CUDA(ebl::launch_det_reduce(d, b->stream));
-  b->launches += 2 + 2 * static_cast<uint64_t>(b->traj_steps);
+  b->launches += 2 + (d.A_un_o ? 1 : 2) * static_cast<uint64_t>(b->traj_steps);
   EBL_CUDA(cudaMemcpyAsync(loss, b->det_loss.p, b->n_envs * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaMemcpyAsync(grad6, b->det_grad.p, b->n_envs * 6 * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));

@@ -33,7 +33,8 @@ namespace ebl {
 
 namespace {
 
-// Fixed-order block sums of N values at once (one shared round trip instead of N).
+// Fixed-order block sums of N values at once (one shared round trip instead of N); the result
+// is valid in thread 0 only (the callers' only reader).
 template <int N>
 __device__ __forceinline__ void block_sum_n(double (&v)[N], double* red) {
 #pragma unroll
@@ -45,12 +46,13 @@ __device__ __forceinline__ void block_sum_n(double (&v)[N], double* red) {
 #pragma unroll
     for (int q = 0; q < N; ++q) red[q * 32 + (threadIdx.x >> 5)] = v[q];
   __syncthreads();
+  if (threadIdx.x == 0)
 #pragma unroll
-  for (int q = 0; q < N; ++q) {
-    double t = 0.0;
-    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) t += red[q * 32 + i];  // fixed order
-    v[q] = t;
-  }
+    for (int q = 0; q < N; ++q) {
+      double t = 0.0;
+      for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) t += red[q * 32 + i];  // fixed order
+      v[q] = t;
+    }
 }
 
 __device__ __forceinline__ double block_sum_d(double v, double* red) {
@@ -111,12 +113,14 @@ __global__ void k_det_forward(DetArgs d, int t) {
   d.burn_o[base + i] = __dadd_rn(newly, __dmul_rn(bu, d.pc));
   d.un_o[base + i] = __dsub_rn(un, newly);
   d.bd_o[base + i] = __dadd_rn(bd, __dmul_rn(bu, __dsub_rn(1.0, d.pc)));
+  // record mode: the states of steps >= 1 are written straight into their trajectory slots (the
+  // host points un_o / burn_o there), so only step 0 copies its input; lambda every step
+  const size_t tr = static_cast<size_t>(t) * a.n_envs * ncell + base + i;
   if (d.traj_un) {
-    const size_t tr = static_cast<size_t>(t) * a.n_envs * ncell + base + i;
     d.traj_un[tr] = un;
     d.traj_burn[tr] = bu;
-    d.traj_lam[tr] = lam;
   }
+  if (d.traj_lam) d.traj_lam[tr] = lam;
 }
 
 // state_from_fire (engine.cpp:42-52): one-hot planes from the member layers, on the device.
@@ -291,6 +295,158 @@ __global__ void k_det_back2(DetArgs d, int t) {
   }
 }
 
+
+// back1 + back2 fused per 32 x 8 tile (one launch per step): a_lambda of the tile and its 1-cell
+// ring in shared memory (the ring's back1 is recomputed from the same inputs, bit-identical), then
+// the gather of back2.  The adjoints are double-buffered (A_un / A_burn read, A_un_o / A_burn_o
+// written) because neighbouring tiles read the old values of this tile's ring.  The slope of the
+// direction-k pot derivative is the source's own record of the opposite direction, negated
+// (atan is odd and fp32 negation exact): 32 contiguous bytes instead of 8 scattered records.
+constexpr int kBackTx = 32, kBackTy = 8;
+
+__device__ __forceinline__ double back1_alam(const DetArgs& d, size_t base, size_t tb, size_t tr, int i, double& lam,
+                                             double& e, double& p_ig, double& a_newly, double& un) {
+  lam = d.traj_lam[tr + i];
+  const double gam = d.gam[tb + i];
+  const double x = __dmul_rn(gam, lam);
+  e = exp_neg(x);
+  p_ig = __dsub_rn(1.0, e);
+  un = d.traj_un[tr + i];
+  a_newly = d.A_burn[base + i] - d.A_un[base + i];
+  const double a_x = a_newly * un * e;  // dp_ig/dx = e^{-x} (Dual's exp)
+  return a_x * gam;
+}
+
+#ifndef EBL_DET_BACK_MINB
+#define EBL_DET_BACK_MINB 5  // 48 registers: 5 CTAs per SM (88 without the bound: 2)
+#endif
+__global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_back(DetArgs d, int t) {
+  __shared__ double red[6 * 32];
+  __shared__ double s_al[kBackTy + 2][kBackTx + 2];
+  const StepArgs& a = d.s;
+  const int h = a.h, w = a.w, ncell = h * w;
+  const int env = blockIdx.y;
+  const int tiles_x = (w + kBackTx - 1) / kBackTx;
+  const int c0 = (blockIdx.x % tiles_x) * kBackTx, r0 = (blockIdx.x / tiles_x) * kBackTy;
+  const int tx = threadIdx.x & (kBackTx - 1), ty = threadIdx.x / kBackTx;
+  const int r = r0 + ty, c = c0 + tx;
+  const bool in = r < h && c < w;
+  const int i = r * w + c;
+  const size_t base = static_cast<size_t>(env) * ncell;
+  const size_t tb = static_cast<size_t>(env) * d.tab_stride;
+  const size_t tr = static_cast<size_t>(t) * a.n_envs * ncell + base;
+  double g_gamma = 0.0, g_pc = 0.0, bu = 0.0, Ab = 0.0, Ad = 0.0;
+  // ---- back1 of the own cell ----
+  {
+    double al = 0.0;
+    if (in) {
+      double lam, e, p_ig, a_newly, un;
+      al = back1_alam(d, base, tb, tr, i, lam, e, p_ig, a_newly, un);
+      bu = d.traj_burn[tr + i];
+      Ab = d.A_burn[base + i];
+      Ad = d.A_bd[base + i];
+      d.A_un_o[base + i] = d.A_un[base + i] + a_newly * p_ig;
+      const double F = d.fac_F ? d.fac_F[tb + i] : a.pal64[768 + a.fuel[static_cast<size_t>(env) * a.ter_stride + i]];
+      g_gamma = (a_newly * un * e) * lam * F;  // dgamma/dalpha_gamma = F(v)
+      g_pc = bu * (Ab - Ad);
+    }
+    s_al[ty + 1][tx + 1] = al;
+  }
+  // ---- back1 of the ring (a_lambda only) ----
+  constexpr int kRing = 2 * (kBackTx + 2) + 2 * kBackTy;
+  for (int q = threadIdx.x; q < kRing; q += blockDim.x) {
+    int sy, sx;
+    if (q < kBackTx + 2) sy = 0, sx = q;
+    else if (q < 2 * (kBackTx + 2)) sy = kBackTy + 1, sx = q - (kBackTx + 2);
+    else sy = 1 + ((q - 2 * (kBackTx + 2)) >> 1), sx = ((q - 2 * (kBackTx + 2)) & 1) ? kBackTx + 1 : 0;
+    const int vr = r0 + sy - 1, vc = c0 + sx - 1;
+    double al = 0.0;
+    if (vr >= 0 && vr < h && vc >= 0 && vc < w) {
+      double lam, e, p_ig, a_newly, un;
+      al = back1_alam(d, base, tb, tr, vr * w + vc, lam, e, p_ig, a_newly, un);
+    }
+    s_al[sy][sx] = al;
+  }
+  __syncthreads();
+  // ---- back2 of the own cell (source u = (r, c), targets u + d_k) ----
+  double gp = 0.0, gw1 = 0.0, gw2 = 0.0, gs = 0.0;
+  if (in) {
+    double acc_burn = Ab * d.pc + Ad * (1.0 - d.pc);
+    if (bu != 0.0 && d.fac_pb) {  // general form: host-built derivative factors
+      const size_t o = tb + i;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int vr = r + kDy[k], vc = c + kDx[k];
+        if (vr < 0 || vr >= h || vc < 0 || vc >= w) continue;
+        const double al = s_al[ty + 1 + kDy[k]][tx + 1 + kDx[k]];
+        if (al == 0.0) continue;
+        const double pot = d.pot[o * 8 + k];
+        acc_burn += al * pot;
+        const double ab = al * bu;
+        gp += ab * d.fac_pb[o * 8 + k];
+        gw1 += ab * pot * d.fac_V[o];
+        gw2 += ab * pot * d.fac_Va[o * 8 + k];
+        gs += ab * pot * d.fac_S[o * 8 + k];
+      }
+    } else if (bu != 0.0) {
+      const TerrainView tv = terrain_view(a, env);
+      const float* slope = a.slope32 ? a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8 : nullptr;
+      const double V = d.V[env * d.wind_stride];
+      const float zu = tv.elev[i];
+      double potk[8];  // the source's 8 pot entries, 64 contiguous bytes requested at once
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        const double2 pp = *reinterpret_cast<const double2*>(d.pot + (tb + i) * 8 + k);
+        potk[k] = pp.x;
+        potk[k + 1] = pp.y;
+      }
+      float sown[8];
+      if (slope) {
+        const float4 s0 = *reinterpret_cast<const float4*>(slope + static_cast<size_t>(i) * 8);
+        const float4 s1 = *reinterpret_cast<const float4*>(slope + static_cast<size_t>(i) * 8 + 4);
+        sown[0] = s0.x, sown[1] = s0.y, sown[2] = s0.z, sown[3] = s0.w;
+        sown[4] = s1.x, sown[5] = s1.y, sown[6] = s1.z, sown[7] = s1.w;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int vr = r + kDy[k], vc = c + kDx[k];
+        if (vr < 0 || vr >= h || vc < 0 || vc >= w) continue;
+        const double al = s_al[ty + 1 + kDy[k]][tx + 1 + kDx[k]];
+        if (al == 0.0) continue;
+        const double pot = potk[k];
+        acc_burn += al * pot;
+        // pot = p_base F kw ks (kernel.hpp:21-45): dpot/dp_base = F kw ks, dpot/dalpha_w1 = pot V,
+        // dpot/dalpha_w2 = pot V (cos - 1), dpot/dalpha_s = pot S; S in fp32 (relative error ~1e-7,
+        // far inside the 1e-4 gradient bar)
+        double S;
+        if (slope) {
+          S = -static_cast<double>(sown[(k + 4) & 7]);  // u's record, direction k+4: source v
+        } else {
+          const float dz = tv.elev[vr * w + vc] - zu;
+          S = dz == dz ? static_cast<double>(atanf(dz * tv.inv_dist32[k & 1])) : 0.0;  // nodata: 0
+        }
+        const double ab = al * bu;
+        gp += ab * (pot * d.inv_p_base);
+        gw1 += ab * pot * V;
+        gw2 += ab * pot * V * d.align[env * d.wind_stride * 8 + k];
+        gs += ab * pot * S;
+      }
+    }
+    d.A_burn_o[base + i] = acc_burn;  // A_bd is unchanged (bd' = bd + ...)
+  }
+  double g6[6] = {gp, gw1, gw2, gs, g_gamma, g_pc};
+  block_sum_n<6>(g6, red);
+  if (threadIdx.x == 0) {
+    double* acc = d.acc + (static_cast<size_t>(env) * gridDim.x + blockIdx.x) * 8;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) acc[k] += g6[k];
+  }
+}
+
+int det_blocks_per_env(int h, int w) {
+  return ((w + kBackTx - 1) / kBackTx) * ((h + kBackTy - 1) / kBackTy);
+}
+
 __global__ void k_det_reduce(DetArgs d, int blocks_per_env) {
   const int env = blockIdx.x;
   const int k = threadIdx.x;
@@ -320,6 +476,10 @@ cudaError_t launch_det_loss(const DetArgs& d, cudaStream_t s) {
 cudaError_t launch_det_backward(const DetArgs& d, int t, cudaStream_t s) {
   const int ncell = d.s.h * d.s.w;
   const dim3 grid((ncell + 255) / 256, d.s.n_envs);
+  if (d.A_un_o) {  // fused, double-buffered adjoints
+    k_det_back<<<dim3(det_blocks_per_env(d.s.h, d.s.w), d.s.n_envs), kBackTx * kBackTy, 0, s>>>(d, t);
+    return cudaGetLastError();
+  }
   k_det_back1<<<grid, 256, 0, s>>>(d, t);
   k_det_back2<<<grid, 256, 0, s>>>(d, t);
   return cudaGetLastError();
@@ -327,7 +487,7 @@ cudaError_t launch_det_backward(const DetArgs& d, int t, cudaStream_t s) {
 
 cudaError_t launch_det_reduce(const DetArgs& d, cudaStream_t s) {
   const int ncell = d.s.h * d.s.w;
-  k_det_reduce<<<d.s.n_envs, 32, 0, s>>>(d, (ncell + 255) / 256);
+  k_det_reduce<<<d.s.n_envs, 32, 0, s>>>(d, d.A_un_o ? det_blocks_per_env(d.s.h, d.s.w) : (ncell + 255) / 256);
   return cudaGetLastError();
 }
 

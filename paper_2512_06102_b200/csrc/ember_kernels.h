@@ -46,6 +46,7 @@ cudaError_t launch_det_from_fire(const uint8_t* st, double* un, double* bu, doub
                                  cudaStream_t s);
 cudaError_t launch_det_backward(const DetArgs& d, int t, cudaStream_t s);
 cudaError_t launch_det_reduce(const DetArgs& d, cudaStream_t s);
+int det_blocks_per_env(int h, int w);  // gradient partials per env of the fused backward
 cudaError_t launch_rng_probe(int n, const uint64_t* keys5, uint64_t* out, cudaStream_t s);
 cudaError_t launch_step_tile(const StepArgs& a, int mode, cudaStream_t s);
 cudaError_t launch_intensity(const StepArgs& a, int mode, float* lam, float* p, cudaStream_t s);

@@ -98,7 +98,9 @@ struct DetArgs {
   double* A_un;                   // adjoints of the state after step t
   double* A_burn;
   double* A_bd;
-  double* a_lam;                  // adjoint of lambda
+  double* a_lam;                  // adjoint of lambda (unused by the fused k_det_back)
+  double* A_un_o;                 // adjoints of the state before step t (k_det_back writes these;
+  double* A_burn_o;               // the A_* above are read only: neighbours' tiles read them too)
   double* acc;                    // [env][block][8] gradient partials (fixed order)
   double* loss;                   // [env]
   double* grad;                   // [env][6]

@@ -169,6 +169,38 @@ def test_tanker_host_actions(port, kernel, h, w):
     assert np.array_equal(env.fire(), np.stack([x["fire"] for x in want]))
 
 
+def test_tanker_bit_resident_state_sync():
+    """The warp-local tanker keeps its layers bit-resident between ebl_rl_step calls: every other
+    entry point (state read/write, wet read, observe-free reset with a mask) must see and overwrite
+    the current layers.  Interleaved with those calls, AUTO matches the byte-layer RESIDENT kernel
+    step for step, including a host edit of the fire layer mid-run."""
+    n, h, w, seed = 16, 64, 64, 5
+    t = eb.synth_terrain(seed, n, h, w)
+    runs = {}
+    for kernel in (eb.KERNEL_AUTO, eb.KERNEL_RESIDENT):
+        env = eb.VecFireEnv(n, variant=eb.RL_TANKER, terrain=t, sim_cfg=None, ignitions=4, max_steps=256)
+        env.batch.set_kernel(kernel)
+        env.reset(seed)
+        log = []
+        for k in range(60):
+            r, d = env.step(None)
+            log.append((r.copy(), d.copy()))
+            if k % 7 == 3:
+                log.append((env.fire(), env.wet()))
+            if k == 20:  # host edit: ignite a burnable-agnostic corner cell in every env
+                f = env.fire()
+                f[:, 0, 0] = np.where(f[:, 0, 0] == 0, 1, f[:, 0, 0])
+                env.set_fire(f)
+            if k == 40:
+                mask = np.zeros(n, np.uint8)
+                mask[::3] = 1
+                env.reset(seed + 1, mask=mask)
+        log.append((env.fire(), env.wet()))
+        runs[kernel] = log
+    for x, y in zip(runs[eb.KERNEL_AUTO], runs[eb.KERNEL_RESIDENT]):
+        assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
+
+
 @pytest.mark.slow
 def test_c2_full_size_rollout(port):
     """BASELINE C2 at full size (16384 envs of 64 x 64, device random (x, y) policy, 256-step cap,
