@@ -270,7 +270,11 @@ int ebl_det_forward(ebl_batch* b, int n_steps, int record);
  * pred = p_burn + p_bd (calibrate.hpp:86-146), per env, and its gradient with respect to
  * the six SimConfig fields in ParamIndex order (calibrate.hpp:21-28) by reverse mode
  * through the recorded steps (the reference computes it forward-mode with Dual<6>,
- * calibrate.cpp:130-162).  mask [n_envs][H*W]; loss [n_envs]; grad6 [n_envs*6]. */
+ * calibrate.cpp:130-162).  mask [n_envs][H*W], or NULL for the target ebl_det_set_mask made
+ * resident (a calibration's fixed target: uploaded once, not per iteration); loss [n_envs];
+ * grad6 [n_envs*6]. */
+/* Upload the target burn mask [n_envs][H*W] (CalibrationTarget::burn_mask) once. */
+int ebl_det_set_mask(ebl_batch* b, const double* mask);
 int ebl_det_loss_grad(ebl_batch* b, const double* mask, double bce_w, double mse_w, int pool,
                       double* loss, double* grad6);
 

@@ -141,6 +141,7 @@ SIGNATURES = {
     "ebl_det_set_state_from_fire": (_I, [_P]),
     "ebl_det_get_state": (_I, [_P, _P, _P, _P]),
     "ebl_det_forward": (_I, [_P, _I, _I]),
+    "ebl_det_set_mask": (_I, [_P, _P]),
     "ebl_det_loss_grad": (_I, [_P, _P, _D, _D, _I, _P, _P]),
     "ebl_default_calib_options": (None, [C.POINTER(CalibOptions)]),
     "ebl_calibrate": (_I, [_P, _P, _P, _P, _P, _I, _D, _D, _I, C.POINTER(CalibOptions), _P, _P, _P,

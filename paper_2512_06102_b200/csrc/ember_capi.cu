@@ -129,10 +129,11 @@ struct ebl_batch {
   DevBuf<double> det[6];            // un, burn, bd x2 (double buffer)
   int det_cur = 0;
   bool det_ready = false;
-  DevBuf<double> det_pot, det_gam, det_fac, det_V, det_align, traj, adj, det_mask, acc, det_loss, det_grad;
+  DevBuf<double> det_pot, det_gam, det_fac, det_V, det_align, traj, adj, det_mask, acc, det_loss, det_grad, det_init;
   int det_tables = 0;
   bool det_tables_valid = false;
   ebl_sim_config det_cfg{};
+  bool det_mask_set = false;        // det_mask holds the ebl_det_set_mask target
   int traj_steps = -1;              // steps recorded by the last ebl_det_forward(record=1)
   std::vector<uint8_t> h_fuel;      // host copies of the terrain (exact host-built tables)
   std::vector<float> h_elev;
@@ -1850,6 +1851,18 @@ int ebl_det_forward(ebl_batch* b, int n_steps, int record) {
   return EBL_OK;
 }
 
+int ebl_det_set_mask(ebl_batch* b, const double* mask) {
+  if (int e = check_batch(b)) return e;
+  if (!mask) return set_err(EBL_EINVAL, "mask is NULL");
+  EBL_CUDA(cudaSetDevice(b->device));
+  const size_t n = b->ncell * b->n_envs;
+  EBL_CUDA(b->det_mask.alloc(n));
+  EBL_CUDA(cudaMemcpyAsync(b->det_mask.p, mask, n * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  b->det_mask_set = true;
+  return EBL_OK;
+}
+
 int ebl_det_loss_grad(ebl_batch* b, const double* mask, double bce_w, double mse_w, int pool,
                       double* loss, double* grad6) {
   if (int e = check_batch(b)) return e;
@@ -1859,12 +1872,16 @@ int ebl_det_loss_grad(ebl_batch* b, const double* mask, double bce_w, double mse
     return set_err(EBL_EINVAL, "LossConfig: weights >= 0, one positive, pool_size >= 1");
   const size_t n = b->ncell * b->n_envs;
   const int bpe = std::max(static_cast<int>((b->ncell + 255) / 256), ebl::det_blocks_per_env(b->h, b->w));
+  if (!mask && !b->det_mask_set) return set_err(EBL_ESTATE, "mask = NULL needs ebl_det_set_mask first");
   EBL_CUDA(b->det_mask.alloc(n));
   EBL_CUDA(b->adj.alloc(6 * n));
   EBL_CUDA(b->acc.alloc(static_cast<size_t>(b->n_envs) * bpe * 8));
   EBL_CUDA(b->det_loss.alloc(b->n_envs));
   EBL_CUDA(b->det_grad.alloc(static_cast<size_t>(b->n_envs) * 6));
-  EBL_CUDA(cudaMemcpyAsync(b->det_mask.p, mask, n * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  if (mask) {
+    EBL_CUDA(cudaMemcpyAsync(b->det_mask.p, mask, n * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+    b->det_mask_set = false;  // a per-call mask replaces the resident one
+  }
   EBL_CUDA(cudaMemsetAsync(b->acc.p, 0, static_cast<size_t>(b->n_envs) * bpe * 8 * sizeof(double), b->stream));
   ebl::DetArgs d = det_args(b);
   d.mask = b->det_mask.p;
@@ -1970,9 +1987,20 @@ int ebl_calibrate(ebl_batch* b, const double* p_un, const double* p_burn, const 
     c.p_base = th[0], c.alpha_w1 = th[1], c.alpha_w2 = th[2], c.alpha_s = th[3], c.alpha_gamma = th[4],
     c.p_continue = th[5];
     if (int e = ebl_batch_set_config(b, &c)) return e;
-    if (int e = ebl_det_set_state(b, p_un, p_burn, p_bd)) return e;
+    if (iter == 0) {  // initial state and target uploaded once, copied on the device afterwards
+      if (int e = ebl_det_set_state(b, p_un, p_burn, p_bd)) return e;
+      if (int e = ebl_det_set_mask(b, mask)) return e;
+      EBL_CUDA(b->det_init.alloc(3 * n));
+      for (int k = 0; k < 3; ++k)
+        EBL_CUDA(cudaMemcpyAsync(b->det_init.p + k * n, b->det[b->det_cur * 3 + k].p, n * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, b->stream));
+    } else {
+      for (int k = 0; k < 3; ++k)
+        EBL_CUDA(cudaMemcpyAsync(b->det[b->det_cur * 3 + k].p, b->det_init.p + k * n, n * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, b->stream));
+    }
     if (int e = ebl_det_forward(b, horizon, 1)) return e;
-    if (int e = ebl_det_loss_grad(b, mask, bce_w, mse_w, pool, loss_e.data(), grad_e.data())) return e;
+    if (int e = ebl_det_loss_grad(b, nullptr, bce_w, mse_w, pool, loss_e.data(), grad_e.data())) return e;
     double l = 0.0, g[6] = {0};
     for (int e = 0; e < b->n_envs; ++e) {  // the batch's envs share theta: total loss
       l += loss_e[e];

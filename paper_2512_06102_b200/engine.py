@@ -263,10 +263,17 @@ class Batch:
     def det_forward(self, n_steps: int, record: bool = True) -> None:
         check(lib().ebl_det_forward(self._h, n_steps, int(record)))
 
-    def det_loss_grad(self, mask, bce_weight=0.0, mse_weight=1.0, pool=1):
-        """(loss [n_envs], grad [n_envs, 6]) after a recorded det_forward (calibrate.hpp:120-146)."""
+    def det_set_mask(self, mask) -> None:
+        """Make the target burn mask resident (det_loss_grad(None, ...) then reuses it)."""
         m = np.ascontiguousarray(np.broadcast_to(np.asarray(mask, dtype=np.float64),
                                                  (self.n_envs, self.height, self.width)))
+        check(lib().ebl_det_set_mask(self._h, _ptr(m)))
+
+    def det_loss_grad(self, mask, bce_weight=0.0, mse_weight=1.0, pool=1):
+        """(loss [n_envs], grad [n_envs, 6]) after a recorded det_forward (calibrate.hpp:120-146);
+        mask None: the det_set_mask target."""
+        m = None if mask is None else np.ascontiguousarray(
+            np.broadcast_to(np.asarray(mask, dtype=np.float64), (self.n_envs, self.height, self.width)))
         loss = np.empty(self.n_envs, np.float64)
         grad = np.empty((self.n_envs, 6), np.float64)
         check(lib().ebl_det_loss_grad(self._h, _ptr(m), float(bce_weight), float(mse_weight), int(pool),

@@ -94,12 +94,16 @@ def test_c4_full_batch_runs_and_is_deterministic():
     init = eb.synth_ignitions(seed, t, 5)
     _, mask = _hidden_target(t, init, seed, steps)
     outs = []
-    for _ in range(2):
+    for resident in (False, True):  # per-call mask, then the det_set_mask target
         b = _batch(t, None)
         b.set_state(init)
         b.det_set_state_from_fire()
         b.det_forward(steps, record=True)
-        outs.append(b.det_loss_grad(mask, 0.0, 1.0, 1))
+        if resident:
+            with pytest.raises(eb.EmberError, match="ebl_det_set_mask"):
+                b.det_loss_grad(None)  # no resident target yet
+            b.det_set_mask(mask)
+        outs.append(b.det_loss_grad(None if resident else mask, 0.0, 1.0, 1))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
     assert np.isfinite(outs[0][1]).all() and (np.abs(outs[0][1]).sum(1) > 0).all()
 
