@@ -242,6 +242,12 @@ int ebl_batch_profile(ebl_batch* b, int64_t* out);
  * keys5[i*5 + {0..4}] = {seed, step, stream, cell, draw}; the parity probe of the
  * device generator (device 0). */
 int ebl_device_rng_words(int n, const uint64_t* keys5, uint64_t* out);
+
+/* Pinned, mapped host staging memory in 2 MiB transparent huge pages for the host-buffer entry
+ * points (ebl_batch_run, set/get_state): robust full-rate DMA, and ebl_batch_run writes the final
+ * layers into it straight from the kernel.  No reference counterpart (the reference is host-only). */
+int ebl_host_alloc(size_t bytes, void** out);
+int ebl_host_free(void* p);
 int ebl_batch_sync(ebl_batch* b);
 
 /* ---- one-shot entry points (exact reference signatures, host buffers) ---- */

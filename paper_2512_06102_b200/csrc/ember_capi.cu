@@ -1,6 +1,7 @@
 // C-ABI implementation (include/ember_b200.h): the device-resident batch object,
 // static-layer management, launch sequencing and error convention.
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
 #include <cmath>
 #include <cstdlib>
@@ -9,6 +10,8 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -1333,6 +1336,53 @@ int ebl_batch_diag(ebl_batch* b, uint64_t* out4, int reset) {
     b->steps_done = 0;
     b->launches = 0;
   }
+  return EBL_OK;
+}
+
+// Host staging buffers for the host-buffer entry points: anonymous memory in 2 MiB transparent
+// huge pages, faulted in, then page-locked and mapped (cudaHostRegister).  Huge pages make the
+// DMA path robust: on the measured VM some 4 KiB-page pinned buffers copy at 14 GB/s instead of
+// 54 GB/s; mapped, so ebl_batch_run writes results into them straight from the kernel.
+namespace {
+std::mutex g_host_mu;
+std::unordered_map<void*, std::pair<void*, size_t>> g_host;  // user ptr -> (mapping, length)
+}  // namespace
+
+int ebl_host_alloc(size_t bytes, void** out) {
+  if (!out || bytes == 0) return set_err(EBL_EINVAL, "ebl_host_alloc: bytes > 0 and an out pointer");
+  constexpr size_t kHuge = size_t{2} << 20;
+  const size_t len = (bytes + kHuge - 1) / kHuge * kHuge;
+  void* base = mmap(nullptr, len + kHuge, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (base == MAP_FAILED) return set_err(EBL_ECUDA, "ebl_host_alloc: mmap failed");
+  char* p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(base) + kHuge - 1) & ~(kHuge - 1));
+  madvise(p, len, MADV_HUGEPAGE);  // a hint: 4 KiB pages when THP is off
+  std::memset(p, 0, len);          // fault the pages in before they are pinned
+  const cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterPortable | cudaHostRegisterMapped);
+  if (e != cudaSuccess) {
+    munmap(base, len + kHuge);
+    return set_err(EBL_ECUDA, std::string("ebl_host_alloc: ") + cudaGetErrorString(e));
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    g_host[p] = {base, len + kHuge};
+  }
+  *out = p;
+  return EBL_OK;
+}
+
+int ebl_host_free(void* p) {
+  if (!p) return EBL_OK;
+  std::pair<void*, size_t> m;
+  {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    auto it = g_host.find(p);
+    if (it == g_host.end()) return set_err(EBL_EINVAL, "ebl_host_free: not an ebl_host_alloc pointer");
+    m = it->second;
+    g_host.erase(it);
+  }
+  const cudaError_t e = cudaHostUnregister(p);
+  munmap(m.first, m.second);
+  if (e != cudaSuccess) return set_err(EBL_ECUDA, std::string("ebl_host_free: ") + cudaGetErrorString(e));
   return EBL_OK;
 }
 

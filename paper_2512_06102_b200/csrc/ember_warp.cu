@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
 #if EBL_PHASE_PROF
   // per warp (lane 0): dense-pass cycles, decide-pass cycles, passes, cells; CTA: step cycles
   long long pw_dense = 0, pw_dec = 0, pw_pass = 0, pw_cells = 0, pw_t0 = 0, p_step = 0, p_wait = 0;
-  __shared__ long long s_wd[4][4];
+  long long pw_loc = 0, pw_body = 0, pw_ts = 0;
+  __shared__ long long s_wd[4][6];
 #endif
   for (int t = 0; t < n_steps; ++t) {
 #if EBL_PHASE_PROF
@@ -259,6 +260,10 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
       }
 #endif
       for (int p = 0; p < total; p += 32) {
+#if EBL_PHASE_PROF
+        __syncwarp();
+        pw_ts = clock64();
+#endif
         const int idx = p + lane;
         int L = 0;  // the last lane whose exclusive count is <= idx (counts are non-decreasing)
 #pragma unroll
@@ -289,6 +294,15 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
           }
         }
         const int cc = 32 * jj + nth_set_bit(wv, q);
+#if EBL_PHASE_PROF
+        {
+          const unsigned msk = __activemask();
+          const int ccs = __shfl_sync(msk, cc, __ffs(msk) - 1);  // the warp's lanes have located
+          __syncwarp(msk);
+          if (lane == 0) pw_loc += clock64() - pw_ts + (ccs & 0);
+          pw_ts = clock64();
+        }
+#endif
         const int gr = R0 + rr, gc = C0 + cc;  // layer coordinates
         // the candidate records are requested first (burning cells waste one), so their latency
         // overlaps the RNG rounds and the neighbour masks below
@@ -321,6 +335,9 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
                                     s_pal, s_kw, W, BH, gr, gc, nb, m, dg);
           else
             ig = ignite<MODE>(a, env, gr, gc, nb, m, dg, srow);
+#if EBL_PHASE_PROF
+          if (lane == 0) pw_body += clock64() - pw_ts + (ig & 0);
+#endif
           if (ig) {
             atomicOr(Bn + wi, bit);
             newly += last && rr >= tr0 && rr < tr1 && cc >= tc0 && cc < tc1;  // counted in the tile only
@@ -359,12 +376,14 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
       s_wd[warp][1] = pw_dec;
       s_wd[warp][2] = pw_pass;
       s_wd[warp][3] = pw_wait_dummy(p_wait);
+      s_wd[warp][4] = pw_loc;
+      s_wd[warp][5] = pw_body;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      long long mx[4] = {0, 0, 0, 0}, passes = 0;
+      long long mx[6] = {0, 0, 0, 0, 0, 0}, passes = 0;
       for (int q = 0; q < 4; ++q) {
-        for (int k = 0; k < 4; ++k) mx[k] = max(mx[k], s_wd[q][k]);
+        for (int k = 0; k < 6; ++k) mx[k] = max(mx[k], s_wd[q][k]);
         passes += s_wd[q][2];
       }
       long long* o = a.prof + static_cast<size_t>(env) * 10;
@@ -376,6 +395,8 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
       o[5] = passes;     // passes of all warps
       o[6] = p_step;     // CTA step cycles (thread 0)
       o[7] = mx[3];      // max barrier wait
+      o[8] = mx[4];      // max warp: locate cycles (pass start -> cell found)
+      o[9] = mx[5];      // max warp: lane 0's decide body (cell found -> ignition decided)
     }
   }
 #endif

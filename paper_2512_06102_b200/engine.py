@@ -27,6 +27,32 @@ def _ptr(a: np.ndarray | None):
     return a.ctypes.data_as(C.c_void_p)
 
 
+class _HostMem:
+    """Owner of an ebl_host_alloc block (freed with the last array viewing it)."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        check(lib().ebl_host_alloc(nbytes, C.byref(p)))
+        self.ptr, self.nbytes = p.value, nbytes
+        self.buf = (C.c_char * nbytes).from_address(self.ptr)
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib().ebl_host_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+
+def host_buffer(shape, dtype=np.uint8) -> np.ndarray:
+    """A numpy array in pinned, mapped, huge-page host memory (ebl_host_alloc): the host buffers
+    to hand Batch.run / set_state / get_state for full-rate transfers."""
+    shape = (shape,) if isinstance(shape, int) else tuple(shape)
+    nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    mem = _HostMem(max(nbytes, 1))
+    arr = np.frombuffer(mem.buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+    mem.buf._owner = mem  # the ctypes buffer (the arrays' base) keeps the allocation alive
+    return arr
+
+
 def default_config(**overrides) -> SimConfig:
     """SimConfig{} (grid.hpp:173-179) with keyword overrides."""
     c = SimConfig()

@@ -40,6 +40,9 @@ b.set_wind(t.wind_speed, t.wind_direction)
 L = eb.lib()
 
 
+d.copy_(h_in)
+
+
 def dev():
     eb._lib.check(L.ebl_batch_set_state_device(b.handle, d.data_ptr()))
     b.set_key(0, 0)
@@ -54,3 +57,32 @@ for c in (1, 2, 4, 8, 16):
         b.set_key(0, 0)
         eb._lib.check(L.ebl_batch_run(b.handle, h_in.data_ptr(), STEPS, h_out.data_ptr()))
     print(f"ebl_batch_run chunks={c}: {tm(run):.3f} ms")
+
+# Upper bound of ordering the host->device chunks by work: the same envs permuted heaviest-first
+# (work proxy: cells touched by the fire at the end of the run) vs lightest-first.
+b.set_pipeline(0)
+b.set_key(0, 0)
+eb._lib.check(L.ebl_batch_run(b.handle, h_in.data_ptr(), STEPS, h_out.data_ptr()))
+work = (h_out.numpy().reshape(N, -1) != 0).sum(1)
+for name, order in (("identity", np.arange(N)), ("heaviest-first", np.argsort(-work, kind="stable")),
+                    ("lightest-first", np.argsort(work, kind="stable"))):
+    bp = eb.Batch(N, H, W, stream=torch.cuda.current_stream().cuda_stream)
+    bp.set_terrain(t.fuel_class[order], t.elevation[order], t.class_veg, t.class_den, 30.0)
+    bp.set_wind(t.wind_speed[order], t.wind_direction[order])
+    hp = torch.from_numpy(init[order].copy()).pin_memory()
+    streams = order.astype(np.uint64)
+    dp = hp.cuda()
+
+    def devp():
+        eb._lib.check(L.ebl_batch_set_state_device(bp.handle, dp.data_ptr()))
+        bp.set_key(0, 0, streams=streams)
+        bp.step(STEPS)
+    print(f"{name} device run: {tm(devp):.3f} ms")
+    for c in (8, 16, 32):
+        bp.set_pipeline(c)
+
+        def runp():
+            bp.set_key(0, 0, streams=streams)
+            eb._lib.check(L.ebl_batch_run(bp.handle, hp.data_ptr(), STEPS, h_out.data_ptr()))
+        print(f"{name} ebl_batch_run chunks={c}: {tm(runp):.3f} ms")
+    bp.close()

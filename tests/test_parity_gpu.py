@@ -501,10 +501,12 @@ def test_frontier_handover_vs_blocked_and_oracle(port, case):
         assert np.array_equal(f[0][e], O.run(port, "port", g, c, seed, 0, e, steps, init[e]))
 
 
+@pytest.mark.parametrize("huge", [False, True])
 @pytest.mark.parametrize("chunks", [0, 3, 8])
-def test_pipelined_run_pinned_zero_copy(chunks):
-    """ebl_batch_run with pinned host buffers: the kernels write the final layers straight into
-    the mapped output buffer (no device -> host copy); identical to the sequence."""
+def test_pipelined_run_pinned_zero_copy(chunks, huge):
+    """ebl_batch_run with pinned host buffers (torch's, or ebl_host_alloc's huge-page mapped
+    buffers): the kernels write the final layers straight into the mapped output buffer (no
+    device -> host copy); identical to the sequence."""
     import torch
     n_envs, h, w, steps, seed = 37, 128, 128, 50, 4
     t = eb.synth_terrain(seed, n_envs, h, w)
@@ -516,10 +518,17 @@ def test_pipelined_run_pinned_zero_copy(chunks):
         b.set_state(init)
         b.step(steps)
         want = b.get_state()
-        h_in = torch.from_numpy(init.copy()).pin_memory()
-        h_out = torch.full_like(h_in, 9).pin_memory()
+        if huge:
+            h_in, h_out = eb.host_buffer(init.shape), eb.host_buffer(init.shape)
+            h_in[:] = init
+            h_out[:] = 9
+            pi, po = h_in.ctypes.data, h_out.ctypes.data
+        else:
+            h_in = torch.from_numpy(init.copy()).pin_memory()
+            h_out = torch.full_like(h_in, 9).pin_memory()
+            pi, po = h_in.data_ptr(), h_out.data_ptr()
         b.set_pipeline(chunks)
         b.set_key(seed, 0)
-        eb._lib.check(eb.lib().ebl_batch_run(b.handle, h_in.data_ptr(), steps, h_out.data_ptr()))
-        assert np.array_equal(h_out.numpy(), want)
+        eb._lib.check(eb.lib().ebl_batch_run(b.handle, pi, steps, po))
+        assert np.array_equal(np.asarray(h_out), want)
         assert np.array_equal(b.get_state(), want)  # the device copy is kept as well
