@@ -140,7 +140,7 @@ int ebl_step_batch(ebl_batch* b, int n_steps);
  * chunks' work).  Returns when final_states is written.  Pinned host memory makes the copies
  * asynchronous. */
 int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* final_states);
-/* Number of env chunks ebl_batch_run pipelines over (0 = auto, 8; 1 = no pipelining). */
+/* Number of env chunks ebl_batch_run pipelines over (0 = auto, 4; 1 = no pipelining). */
 int ebl_batch_set_pipeline(ebl_batch* b, int chunks);
 
 /* run_stochastic(record=true) (engine.cpp:108,116): ebl_step_batch that also stores the layers

@@ -103,6 +103,8 @@ struct ebl_batch {
   DevBuf<float> elev;
   DevBuf<float> slope32;            // [grid][cell][8] fp32 slopes of the layers (built by prepare)
   DevBuf<uint2> nfuel;              // [grid][cell] fuel classes of the 8 sources (built with slope32)
+  DevBuf<float> pot32t;             // [env or 1][cell][8] fp32 lambda terms (built by prepare)
+  bool pot32t_valid = false;
   bool slope_dirty = false;
   std::vector<double> pal_veg, pal_den;
   double cellsize = 30.0;
@@ -198,6 +200,7 @@ int prepare(ebl_batch* b) {
   if (b->mode == ebl::kStaticNone) return set_err(EBL_ESTATE, "no grid or terrain set on the batch");
   EBL_CUDA(cudaSetDevice(b->device));
   const Cfg6 c = cfg6(b->cfg);
+  const bool pot32t_stale = b->mode == ebl::kStaticTerrain && (b->derived_dirty || b->slope_dirty);
   if (b->mode == ebl::kStaticTables && b->tables_dirty) {
     const size_t n = b->ncell * b->n_grids;
     const int S = std::max(1, b->sched_len);  // one table per wind-schedule entry
@@ -254,6 +257,18 @@ int prepare(ebl_batch* b) {
                                      static_cast<float>(1.0 / d1), b->slope32.p, b->nfuel.p, b->stream));
     b->slope_dirty = false;
   }
+  if (pot32t_stale) {  // the per-candidate lambda terms (one wind per env; none under a schedule)
+    b->pot32t_valid = false;
+    if (b->sched_len <= 1) {
+      const bool per_env = b->n_grids > 1 || b->n_winds > 1;
+      const int n_tab = per_env ? b->n_envs : 1;
+      EBL_CUDA(b->pot32t.alloc(b->ncell * n_tab * 8));
+      EBL_CUDA(ebl::launch_pot32t(b->slope32.p, b->nfuel.p, b->pal32.p, b->kw32.p, n_tab, b->ncell,
+                                  b->n_grids > 1 ? b->ncell : 0, b->n_winds > 1 ? 8 : 0,
+                                  static_cast<float>(b->cfg.alpha_s * 1.4426950408889634), b->pot32t.p, b->stream));
+      b->pot32t_valid = true;
+    }
+  }
   return EBL_OK;
 }
 
@@ -277,6 +292,8 @@ ebl::StepArgs step_args(const ebl_batch* b) {
   a.elev = b->elev.p;
   a.slope32 = b->mode == ebl::kStaticTerrain ? b->slope32.p : nullptr;
   a.nfuel = b->mode == ebl::kStaticTerrain ? b->nfuel.p : nullptr;
+  a.pot32t = b->mode == ebl::kStaticTerrain && b->pot32t_valid && b->sched_len <= 1 ? b->pot32t.p : nullptr;
+  a.pot32t_stride = b->n_grids > 1 || b->n_winds > 1 ? b->ncell * 8 : 0;
   a.n_pal = static_cast<int>(b->pal_veg.size());
   a.alpha_s_l2 = static_cast<float>(b->cfg.alpha_s * 1.4426950408889634);
   a.ter_stride = b->n_grids > 1 ? b->ncell : 0;
@@ -329,6 +346,7 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
     a.kw32 += o * a.kw_stride;
     a.kw64 += o * a.kw_stride;
   }
+  if (a.pot32t) a.pot32t += o * a.pot32t_stride;
   return a;
 }
 
@@ -983,7 +1001,7 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
   const bool resident = b->kernel != EBL_KERNEL_TILED && b->kernel != EBL_KERNEL_BLOCKED &&
                         b->tile_h == 0 && ebl::resident_fits(b->h, b->w);
   const bool frontier = use_frontier(b);
-  int chunks = b->pipe_chunks > 0 ? b->pipe_chunks : 8;
+  int chunks = b->pipe_chunks > 0 ? b->pipe_chunks : 4;  // C1 e2e: 4 chunks 0.84 ms, 8: 0.92, 2: 0.89
   chunks = std::min(chunks, b->n_envs);
   if (!resident || n_steps == 0 || chunks <= 1) {  // one launch per step set: plain sequence
     int rc;

@@ -31,6 +31,9 @@ struct StepArgs {
   const float* elev;              // [grid][h*w]
   const float* slope32;           // [grid][h*w][8] fp32 slope table (terrain form) or null
   const uint2* nfuel;             // [grid][h*w] fuel classes of the 8 sources u_k = v - d_k (bytes k)
+  const float* pot32t;            // [env][h*w][8] fp32 pot of source u_k into target v (terrain form,
+                                  // one wind per env; null with a wind schedule): the lambda terms
+  size_t pot32t_stride;           // floats per env of pot32t (0: one table for all envs)
   int n_pal;                      // palette entries in use (terrain form)
   float alpha_s_l2;               // alpha_s * log2(e): kappa_slope = 2^(alpha_s_l2 * S)
   int rec_probe;                  // k_intensity: report the record form (1) or the elevation form (0)

@@ -34,6 +34,10 @@
 #define EBL_WPF prefetch_l1
 #endif
 
+#ifndef EBL_WARP_POT  // lambda terms from the pot32t table (0: slope + source-class records)
+#define EBL_WARP_POT 1
+#endif
+
 namespace ebl {
 
 namespace {
@@ -120,6 +124,7 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
     Bp0[ro(it.r + 1) + it.j] = b;
     X[ro(it.r) + it.j] = x;
   }
+  const bool use_tab = kTer && a.pot32t && EBL_WARP_POT;  // one wind for all steps: precomputed terms
   const bool use_rec = kTer && a.nfuel && a.n_pal <= 32;
   auto load_wind = [&](int srow) {  // kappa_wind of the wind in force (+ the src * kappa_wind table)
     if constexpr (kTer) {
@@ -307,10 +312,17 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
         // the candidate records are requested first (burning cells waste one), so their latency
         // overlaps the RNG rounds and the neighbour masks below
         CellRec rec{};
-        if (use_rec)
+        if (use_tab) {  // the candidate's 8 lambda terms (pot32t) and fuel class
+          const float4* tp = reinterpret_cast<const float4*>(a.pot32t + static_cast<size_t>(env) * a.pot32t_stride) +
+                             2 * (gr * W + gc);
+          rec.s0 = __ldg(tp);
+          rec.s1 = __ldg(tp + 1);
+          rec.fv = __ldg(a.fuel + static_cast<size_t>(env) * a.ter_stride + gr * W + gc);
+        } else if (use_rec) {
           rec = load_rec(a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
                          a.nfuel + static_cast<size_t>(env) * a.ter_stride, a.fuel + static_cast<size_t>(env) * a.ter_stride,
                          gr * W + gc);
+        }
         // ---- decide (engine.cpp:12-26) ----
         const int j = cc >> 5, b = cc & 31;
         const uint32_t bit = 1u << b;
@@ -327,7 +339,10 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
           const uint32_t nb = (midw & 1u) | (dnw << 1) | ((midw >> 2) << 4) | ((upw >> 2) << 5) |
                               ((upw & 2u) << 5) | ((upw & 1u) << 7);
           bool ig;
-          if (use_rec)
+          if (use_tab)
+            ig = ignite_terrain_pot_pre(terrain_view(a, env, srow), rec.s0, rec.s1, rec.fv, s_pal + 256, W, gr, gc, nb, m,
+                                        dg);
+          else if (use_rec)
             ig = ignite_terrain_rec_pre(terrain_view(a, env, srow), rec, s_srckw, s_pal + 256, a.alpha_s_l2, W, gr, gc,
                                         nb, m, dg);
           else if constexpr (kTer)
