@@ -353,6 +353,7 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
   }
   if (threadIdx.x < 2) s_newly[threadIdx.x] = s_gone[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_burning[0] = 0;
+  const bool use_tab = kTer && a.pot32t != nullptr;  // precomputed lambda terms (one wind per env)
   const bool use_rec = kTer && a.nfuel && a.n_pal <= 32;
   if constexpr (kTer) {
     for (int i = threadIdx.x; i < 2 * a.n_pal; i += blockDim.x)  // the palette entries in use: src, gam
@@ -516,10 +517,17 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
         }
         const int cc = 32 * jj + nth_set_bit32(wv, q);
         CellRec rec{};
-        if (use_rec)
+        if (use_tab) {  // the candidate's 8 lambda terms (pot32t) and fuel class
+          const float4* tp = reinterpret_cast<const float4*>(a.pot32t + static_cast<size_t>(env) * a.pot32t_stride) +
+                             2 * (rr * W + cc);
+          rec.s0 = __ldg(tp);
+          rec.s1 = __ldg(tp + 1);
+          rec.fv = __ldg(a.fuel + static_cast<size_t>(env) * a.ter_stride + rr * W + cc);
+        } else if (use_rec) {
           rec = load_rec(a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
                          a.nfuel + static_cast<size_t>(env) * a.ter_stride, a.fuel + static_cast<size_t>(env) * a.ter_stride,
                          rr * W + cc);
+        }
         const int j = cc >> 5, b = cc & 31;
         const uint32_t bit = 1u << b;
         const int wi = ro(rr + 1) + j;
@@ -536,7 +544,9 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
           const uint32_t nb = (midw & 1u) | (dnw << 1) | ((midw >> 2) << 4) | ((upw >> 2) << 5) |
                               ((upw & 2u) << 5) | ((upw & 1u) << 7);
           bool ig;
-          if (use_rec)
+          if (use_tab)
+            ig = ignite_terrain_pot_pre(terrain_view(a, env), rec.s0, rec.s1, rec.fv, s_pal + 256, W, rr, cc, nb, m, dg);
+          else if (use_rec)
             ig = ignite_terrain_rec_pre(terrain_view(a, env), rec, s_srckw, s_pal + 256, a.alpha_s_l2, W, rr, cc, nb, m, dg);
           else if constexpr (kTer)
             ig = ignite_terrain_tab(terrain_view(a, env), a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
