@@ -263,7 +263,7 @@ int prepare(ebl_batch* b) {
       const bool per_env = b->n_grids > 1 || b->n_winds > 1;
       const int n_tab = per_env ? b->n_envs : 1;
       EBL_CUDA(b->pot32t.alloc(b->ncell * n_tab * 8));
-      EBL_CUDA(ebl::launch_pot32t(b->slope32.p, b->nfuel.p, b->pal32.p, b->kw32.p, n_tab, b->ncell,
+      EBL_CUDA(ebl::launch_pot32t(b->slope32.p, b->nfuel.p, b->fuel.p, b->pal32.p, b->kw32.p, n_tab, b->ncell,
                                   b->n_grids > 1 ? b->ncell : 0, b->n_winds > 1 ? 8 : 0,
                                   static_cast<float>(b->cfg.alpha_s * 1.4426950408889634), b->pot32t.p, b->stream));
       b->pot32t_valid = true;

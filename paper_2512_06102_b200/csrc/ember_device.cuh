@@ -294,17 +294,16 @@ __device__ __forceinline__ bool ignite_terrain_rec_pre(const TerrainView& t, con
   return u < p;
 }
 
-// The same decision from the candidate's pot32t row (T0, T1: the 8 source terms) and fuel class:
-// lambda = the k-ordered sum of the burning sources' terms, no per-candidate exponentials.
-__device__ __forceinline__ bool ignite_terrain_pot_pre(const TerrainView& t, float4 T0, float4 T1, uint32_t fv,
-                                                       const float* pal_gam, int w, int r, int c, uint32_t nb,
-                                                       uint64_t m, const DiagCounters& dg) {
+// The same decision from the candidate's pot32t row (T0, T1: its 8 source terms gamma(v) * pot32,
+// built by k_pot32t): x = gamma(v) lambda(v) is the k-ordered sum of the burning sources' terms --
+// no exponentials, class lookups or fuel load per candidate.
+__device__ __forceinline__ bool ignite_terrain_pot_pre(const TerrainView& t, float4 T0, float4 T1, int w, int r, int c,
+                                                       uint32_t nb, uint64_t m, const DiagCounters& dg) {
   if (!t.force64) {
     const float T[8] = {T0.x, T0.y, T0.z, T0.w, T1.x, T1.y, T1.z, T1.w};
-    float lam = 0.f;
+    float x = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) lam += (nb >> k) & 1u ? T[k] : 0.f;
-    const float x = pal_gam[fv] * lam;
+    for (int k = 0; k < 8; ++k) x += (nb >> k) & 1u ? T[k] : 0.f;
     if (x == 0.f) return false;  // gamma or lambda exactly 0: p = 0, u < 0 is false
     const float p32 = p_ignite32(x);
     if (p32 > 1e-12f) {

@@ -105,8 +105,9 @@ struct LandcoverArgs {
 };
 cudaError_t launch_landcover_map(const LandcoverArgs& a, cudaStream_t s);
 // fp32 slope table [grid][cell][8] (terrain form, built with the layers; ember_synth.cu)
-cudaError_t launch_pot32t(const float* slope32, const uint2* nfuel, const float* pal32, const float* kw32, int n_envs,
-                          size_t ncell, size_t ter_stride, int kw_stride, float alpha_l2, float* out, cudaStream_t s);
+cudaError_t launch_pot32t(const float* slope32, const uint2* nfuel, const uint8_t* fuel, const float* pal32,
+                          const float* kw32, int n_envs, size_t ncell, size_t ter_stride, int kw_stride, float alpha_l2,
+                          float* out, cudaStream_t s);
 cudaError_t launch_slope_table(const float* elev, const uint8_t* fuel, size_t n_grids, int h, int w, float inv_d0,
                                float inv_d1, float* out, uint2* nfuel, cudaStream_t s);
 

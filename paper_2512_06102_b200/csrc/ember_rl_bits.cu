@@ -517,12 +517,11 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
         }
         const int cc = 32 * jj + nth_set_bit32(wv, q);
         CellRec rec{};
-        if (use_tab) {  // the candidate's 8 lambda terms (pot32t) and fuel class
+        if (use_tab) {  // the candidate's 8 terms of gamma * lambda (pot32t)
           const float4* tp = reinterpret_cast<const float4*>(a.pot32t + static_cast<size_t>(env) * a.pot32t_stride) +
                              2 * (rr * W + cc);
           rec.s0 = __ldg(tp);
           rec.s1 = __ldg(tp + 1);
-          rec.fv = __ldg(a.fuel + static_cast<size_t>(env) * a.ter_stride + rr * W + cc);
         } else if (use_rec) {
           rec = load_rec(a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
                          a.nfuel + static_cast<size_t>(env) * a.ter_stride, a.fuel + static_cast<size_t>(env) * a.ter_stride,
@@ -545,7 +544,7 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
                               ((upw & 2u) << 5) | ((upw & 1u) << 7);
           bool ig;
           if (use_tab)
-            ig = ignite_terrain_pot_pre(terrain_view(a, env), rec.s0, rec.s1, rec.fv, s_pal + 256, W, rr, cc, nb, m, dg);
+            ig = ignite_terrain_pot_pre(terrain_view(a, env), rec.s0, rec.s1, W, rr, cc, nb, m, dg);
           else if (use_rec)
             ig = ignite_terrain_rec_pre(terrain_view(a, env), rec, s_srckw, s_pal + 256, a.alpha_s_l2, W, rr, cc, nb, m, dg);
           else if constexpr (kTer)

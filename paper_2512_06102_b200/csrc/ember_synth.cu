@@ -283,13 +283,15 @@ __global__ void __launch_bounds__(kSynthThreads) k_slope_table(const float* __re
   nf[i] = make_uint2(nf0, nf1);
 }
 
-// pot32t[env][v][k] = src32(class of u_k) kappa_wind32(k) 2^(alpha_s log2e S(v, k)): the fp32
-// lambda term of source u_k = v - d_k, the same product the record form evaluates per candidate
-// (terrain_lambda32_rec), built once per (terrain, wind, config).
+// pot32t[env][v][k] = gamma32(v) (src32(class of u_k) kappa_wind32(k) 2^(alpha_s log2e S(v, k))):
+// the fp32 term of source u_k = v - d_k in x = gamma(v) lambda(v) -- the product the record form
+// evaluates per candidate (terrain_lambda32_rec), scaled by the target's gamma -- built once per
+// (terrain, wind, config).
 __global__ void __launch_bounds__(kSynthThreads) k_pot32t(const float4* __restrict__ slope32, const uint2* __restrict__ nfuel,
-                                                        const float* __restrict__ pal32, const float* __restrict__ kw32,
-                                                        int n_envs, size_t ncell, size_t ter_stride, int kw_stride,
-                                                        float alpha_l2, float4* __restrict__ out) {
+                                                        const uint8_t* __restrict__ fuel, const float* __restrict__ pal32,
+                                                        const float* __restrict__ kw32, int n_envs, size_t ncell,
+                                                        size_t ter_stride, int kw_stride, float alpha_l2,
+                                                        float4* __restrict__ out) {
   const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= ncell * n_envs) return;
   const size_t env = i / ncell, v = i - env * ncell;
@@ -298,12 +300,13 @@ __global__ void __launch_bounds__(kSynthThreads) k_pot32t(const float4* __restri
   const uint2 nf = nfuel[g];
   const float s[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
   const float* kw = kw32 + env * kw_stride;
+  const float gam = pal32[256 + fuel[g]];  // the target's gamma32 (0 for non-burnable targets)
   float o[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint32_t f = ((k < 4 ? nf.x : nf.y) >> (8 * (k & 3))) & 0xffu;
     const float srckw = pal32[f] * kw[k];
-    o[k] = srckw * ex2_approx(alpha_l2 * s[k]);
+    o[k] = gam * (srckw * ex2_approx(alpha_l2 * s[k]));
   }
   out[2 * i] = make_float4(o[0], o[1], o[2], o[3]);
   out[2 * i + 1] = make_float4(o[4], o[5], o[6], o[7]);
@@ -341,10 +344,11 @@ cudaError_t launch_slope_table(const float* elev, const uint8_t* fuel, size_t n_
   return cudaGetLastError();
 }
 
-cudaError_t launch_pot32t(const float* slope32, const uint2* nfuel, const float* pal32, const float* kw32, int n_envs,
-                          size_t ncell, size_t ter_stride, int kw_stride, float alpha_l2, float* out, cudaStream_t s) {
+cudaError_t launch_pot32t(const float* slope32, const uint2* nfuel, const uint8_t* fuel, const float* pal32,
+                          const float* kw32, int n_envs, size_t ncell, size_t ter_stride, int kw_stride, float alpha_l2,
+                          float* out, cudaStream_t s) {
   const size_t n = ncell * n_envs;
-  k_pot32t<<<grid_x(n), kSynthThreads, 0, s>>>(reinterpret_cast<const float4*>(slope32), nfuel, pal32, kw32, n_envs,
+  k_pot32t<<<grid_x(n), kSynthThreads, 0, s>>>(reinterpret_cast<const float4*>(slope32), nfuel, fuel, pal32, kw32, n_envs,
                                                ncell, ter_stride, kw_stride, alpha_l2, reinterpret_cast<float4*>(out));
   return cudaGetLastError();
 }
