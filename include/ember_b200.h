@@ -243,6 +243,20 @@ int ebl_batch_profile(ebl_batch* b, int64_t* out);
  * device generator (device 0). */
 int ebl_device_rng_words(int n, const uint64_t* keys5, uint64_t* out);
 
+/* serialize_snapshot (snapshot.cpp:55-70) of n layers, concatenated: "emberline-snapshot v1 H W
+ * step", H lines of W chars from {U,B,X} (northmost row first; other byte values '?'), then
+ * "agent row col water" when agents[3*i] >= 0.  layers_dev: n_layers device layers of the batch's
+ * H x W (e.g. an ebl_step_batch_record trajectory), or NULL for the batch's current layers
+ * (n_layers ignored).  steps[i] (NULL: the batch step).  *len = the text's bytes; out = NULL
+ * queries the size; cap < *len is EBL_ERANGE.  Bodies are rendered on the device. */
+int ebl_batch_snapshot_text(ebl_batch* b, const void* layers_dev, int n_layers, const uint64_t* steps,
+                            const int32_t* agents, char* out, size_t cap, size_t* len);
+/* parse_snapshot (snapshot.cpp:74-121) of one snapshot text: dimensions, step, layer (row 0 =
+ * south; NULL to validate only), agent (has_agent).  FileError cases -> EBL_EFILE with the
+ * reference's messages. */
+int ebl_snapshot_parse(const char* text, size_t text_len, int* h, int* w, uint64_t* step, uint8_t* layer,
+                       size_t layer_cap, int32_t* agent3, int* has_agent);
+
 /* Pinned, mapped host staging memory in 2 MiB transparent huge pages for the host-buffer entry
  * points (ebl_batch_run, set/get_state): robust full-rate DMA, and ebl_batch_run writes the final
  * layers into it straight from the kernel.  No reference counterpart (the reference is host-only). */

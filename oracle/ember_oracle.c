@@ -7,6 +7,7 @@
 #include "ember_oracle.h"
 
 #include <math.h>
+#include <stdio.h>
 #include <omp.h>
 #include <stdlib.h>
 #include <string.h>
@@ -687,4 +688,26 @@ void ebo_det_run(const ebo_grid* g, const double* cfg, int steps, double* un, do
     memcpy(bd, c, n * sizeof(double));
   }
   free(pot), free(gam), free(a), free(b), free(c);
+}
+
+/* ---- snapshot.cpp:55-70 serialize_snapshot ------------------------------------------------- */
+long ebo_snapshot_text(int h, int w, const uint8_t* fire, uint64_t step, int ar, int ac, int water, char* out,
+                       long cap) {
+  char hdr[96], ag[96];
+  const int hl = snprintf(hdr, sizeof hdr, "emberline-snapshot v1 %d %d %llu\n", h, w, (unsigned long long)step);
+  const int al = ar >= 0 ? snprintf(ag, sizeof ag, "agent %d %d %d\n", ar, ac, water) : 0;
+  const long total = hl + (long)h * (w + 1) + al;
+  long o = 0;
+#define EBO_PUT(ch) do { if (out && o < cap) out[o] = (ch); ++o; } while (0)
+  for (int k = 0; k < hl; ++k) EBO_PUT(hdr[k]);
+  for (int row = h - 1; row >= 0; --row) { /* state_char, snapshot.cpp:14-21 */
+    for (int col = 0; col < w; ++col) {
+      const uint8_t v = fire[(size_t)row * w + col];
+      EBO_PUT(v == 0 ? 'U' : v == 1 ? 'B' : v == 2 ? 'X' : '?');
+    }
+    EBO_PUT('\n');
+  }
+  for (int k = 0; k < al; ++k) EBO_PUT(ag[k]);
+#undef EBO_PUT
+  return total;
 }

@@ -132,6 +132,10 @@ void ebo_det_loss_grad(const ebo_grid* g, const double* cfg, int steps, const ui
  * iteration a Dual<6> deterministic rollout of `horizon` steps from the continuous initial
  * state + loss.  loss_hist [iterations+1], theta_hist [(iterations+1)*6].  0 / -1 non-finite /
  * -2 bad init_theta. */
+/* serialize_snapshot (snapshot.cpp:55-70): header, H lines northmost first ({U,B,X}, other
+ * bytes '?'), optional agent line (ar < 0: none).  Returns the length; writes at most cap bytes. */
+long ebo_snapshot_text(int h, int w, const uint8_t* fire, uint64_t step, int ar, int ac, int water, char* out,
+                       long cap);
 int ebo_calibrate(const ebo_grid* g, const double* un0, const double* bu0, const double* bd0,
                   const double* mask, int horizon, double bce_w, double mse_w, int pool,
                   int iterations, const double* init_theta, const int* optimize, double lr,

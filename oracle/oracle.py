@@ -84,6 +84,7 @@ _PORT_SIG = {
     "ebo_det_run": (None, [_P, _P, _I, _P, _P, _P]),
     "ebo_det_loss_grad": (None, [_P, _P, _I, _P, _P, _D, _D, _I, C.POINTER(_D), _P]),
     "ebo_calibrate": (_I, [_P, _P, _P, _P, _P, _I, _D, _D, _I, _I, _P, _P, _D, _P, _P, _P, C.POINTER(_D)]),
+    "ebo_snapshot_text": (C.c_long, [_I, _I, _P, _U64, _I, _I, _I, C.c_char_p, C.c_long]),
 }
 
 _REF_SIG = {
@@ -114,6 +115,9 @@ _REF_SIG = {
     "ref_run_deterministic": (_I, [_P, _P, _I, _P, _P, _P]),
     "ref_loss_grad": (_I, [_P, _P, _I, _P, _P, _D, _D, _I, C.POINTER(_D), _P]),
     "ref_calibrate": (_I, [_P, _P, _P, _P, _P, _I, _D, _D, _I, _I, _P, _P, _D, _P, _P, _P, C.POINTER(_D)]),
+    "ref_serialize_snapshot": (C.c_long, [_I, _I, _P, _U64, _I, _I, _I, C.c_char_p, C.c_long]),
+    "ref_parse_snapshot": (_I, [C.c_char_p, C.c_long, C.POINTER(_I), C.POINTER(_I), C.POINTER(_U64), _P, C.c_long,
+                                _P, C.POINTER(_I)]),
 }
 
 _port = None
@@ -270,3 +274,15 @@ def calibrate(L, kind, grid: Grid, init_planes, mask, horizon, iterations, init_
     rc = fn(grid.h, ptr(un), ptr(bu), ptr(bd), ptr(m), horizon, bce_w, mse_w, pool, iterations, ptr(th),
             ptr(opt), lr, ptr(lh), ptr(thh), ptr(best), bl)
     return rc, lh, thh, best, bl.value
+
+
+def snapshot_text(L, kind, fire, step, agent=None) -> bytes:
+    """serialize_snapshot of one layer through the port (kind "port") or the reference ("ref")."""
+    fire = np.ascontiguousarray(fire, dtype=np.uint8)
+    h, w = fire.shape
+    ar, ac, wt = agent if agent is not None else (-1, 0, 0)
+    fn = L.ebo_snapshot_text if kind == "port" else L.ref_serialize_snapshot
+    n = fn(h, w, ptr(fire), step, ar, ac, wt, None, 0)
+    buf = C.create_string_buffer(n)
+    fn(h, w, ptr(fire), step, ar, ac, wt, buf, n)
+    return buf.raw[:n]

@@ -26,6 +26,7 @@
 #include "emberline/reference.hpp"
 #include "emberline/rl_env.hpp"
 #include "emberline/rng.hpp"
+#include "emberline/snapshot.hpp"
 
 namespace R = ::emberline;  // expands to ::ebl_ref under -Demberline=ebl_ref
 
@@ -484,6 +485,50 @@ int ref_calibrate(const void* gp, const double* un0, const double* bu0, const do
     return 0;
   } catch (const std::exception& e) {
     return fail(e);
+  }
+}
+
+// ---- snapshot.hpp ----------------------------------------------------------
+// serialize_snapshot of one layer (agent row < 0: none); returns the text length, writes at most
+// cap bytes.
+long ref_serialize_snapshot(int h, int w, const std::uint8_t* fire, std::uint64_t step, int ar, int ac, int water,
+                            char* out, long cap) {
+  try {
+    R::Snapshot snap;
+    snap.fire = R::FireLayer(h, w);
+    for (int r = 0; r < h; ++r)
+      for (int c = 0; c < w; ++c) snap.fire(r, c) = static_cast<R::FireState>(fire[r * w + c]);
+    snap.step = step;
+    if (ar >= 0) snap.agent = R::AgentMark{R::CellIndex{ar, ac}, water};
+    const std::string t = R::serialize_snapshot(snap);
+    if (out) std::memcpy(out, t.data(), std::min<long>(cap, static_cast<long>(t.size())));
+    return static_cast<long>(t.size());
+  } catch (const std::exception& e) {
+    fail(e);
+    return -1;
+  }
+}
+// parse_snapshot: 0 ok (dims, step, layer up to cap bytes, agent), -1 with ref_last_error().
+int ref_parse_snapshot(const char* text, long len, int* h, int* w, std::uint64_t* step, std::uint8_t* layer, long cap,
+                       int* agent3, int* has_agent) {
+  try {
+    const R::Snapshot snap = R::parse_snapshot(std::string(text, static_cast<size_t>(len)));
+    *h = snap.fire.height();
+    *w = snap.fire.width();
+    *step = snap.step;
+    for (int r = 0; r < *h; ++r)
+      for (int c = 0; c < *w; ++c)
+        if (r * *w + c < cap) layer[r * *w + c] = static_cast<std::uint8_t>(snap.fire(r, c));
+    *has_agent = snap.agent.has_value() ? 1 : 0;
+    if (snap.agent) {
+      agent3[0] = snap.agent->cell.row;
+      agent3[1] = snap.agent->cell.col;
+      agent3[2] = snap.agent->water;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    fail(e);
+    return -1;
   }
 }
 

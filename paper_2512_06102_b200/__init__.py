@@ -8,7 +8,7 @@ from ._lib import (CalibOptions, EmberError, EnvConfig, EnvState, InvalidArgumen
                    RL_REFERENCE, RL_TANKER, SimConfig, lib)
 from .engine import (BURNED, BURNING, KERNEL_AUTO, KERNEL_BLOCKED, KERNEL_FRONTIER, KERNEL_PAIRED, KERNEL_WARP, KERNEL_WARP2, KERNEL_RESIDENT, KERNEL_TILED, UNBURNED, Batch,
                      Terrain, VecFireEnv, as_config, default_config, default_preset,
-                     host_buffer, observation_size, run_stochastic, smoke10_preset, step_stochastic,
+                     host_buffer, observation_size, parse_snapshot, run_stochastic, smoke10_preset, step_stochastic,
                      synth_ignitions, synth_terrain, validate_config, worldcover_palette)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -157,6 +157,9 @@ SIGNATURES = {
     "ebl_rl_get_env_states": (_I, [_P, _P]),
     "ebl_rl_set_env_states": (_I, [_P, _P]),
     "ebl_rl_get_wet": (_I, [_P, _P]),
+    "ebl_batch_snapshot_text": (_I, [_P, _P, _I, _P, _P, _P, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "ebl_snapshot_parse": (_I, [C.c_char_p, C.c_size_t, C.POINTER(_I), C.POINTER(_I), C.POINTER(_U64), _P,
+                                C.c_size_t, _P, C.POINTER(_I)]),
     "ebl_host_alloc": (_I, [C.c_size_t, C.POINTER(_P)]),
     "ebl_host_free": (_I, [_P]),
     "ebl_synth_terrain": (_I, [_U64, _U32, _I, _I, _I, _D, _D, _P, _P, _P, _P]),

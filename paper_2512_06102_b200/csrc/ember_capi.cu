@@ -10,7 +10,9 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <charconv>
 #include <mutex>
+#include <sstream>
 #include <unordered_map>
 #include <string>
 #include <vector>
@@ -104,6 +106,8 @@ struct ebl_batch {
   DevBuf<float> slope32;            // [grid][cell][8] fp32 slopes of the layers (built by prepare)
   DevBuf<uint2> nfuel;              // [grid][cell] fuel classes of the 8 sources (built with slope32)
   DevBuf<float> pot32t;             // [env or 1][cell][8] fp32 lambda terms (built by prepare)
+  DevBuf<char> snap_text, snap_meta;  // snapshot rendering staging (grow-only)
+  DevBuf<unsigned long long> snap_off;
   bool pot32t_valid = false;
   bool slope_dirty = false;
   std::vector<double> pal_veg, pal_den;
@@ -1353,6 +1357,144 @@ int ebl_batch_diag(ebl_batch* b, uint64_t* out4, int reset) {
     EBL_CUDA(cudaMemsetAsync(b->diag.p, 0, sizeof d, b->stream));
     b->steps_done = 0;
     b->launches = 0;
+  }
+  return EBL_OK;
+}
+
+// ---- snapshots (snapshot.hpp / snapshot.cpp) --------------------------------------------------
+int ebl_batch_snapshot_text(ebl_batch* b, const void* layers_dev, int n_layers, const uint64_t* steps,
+                            const int32_t* agents, char* out, size_t cap, size_t* len) {
+  if (int e = check_sync(b)) return e;
+  if (!len) return set_err(EBL_EINVAL, "ebl_batch_snapshot_text: len is NULL");
+  const int n = layers_dev ? n_layers : b->n_envs;
+  if (n < 0) return set_err(EBL_EINVAL, "ebl_batch_snapshot_text: negative layer count");
+  // headers and agent lines formatted here (serialize_snapshot, snapshot.cpp:55-70), the bodies
+  // rendered on the device
+  std::string meta;
+  std::vector<unsigned long long> off(4 * static_cast<size_t>(n));
+  size_t total = 0;
+  const size_t body = static_cast<size_t>(b->h) * (b->w + 1);
+  for (int i = 0; i < n; ++i) {
+    const std::string hdr = "emberline-snapshot v1 " + std::to_string(b->h) + " " + std::to_string(b->w) + " " +
+                            std::to_string(steps ? steps[i] : b->step) + "\n";
+    std::string ag;
+    if (agents && agents[3 * i] >= 0)
+      ag = "agent " + std::to_string(agents[3 * i]) + " " + std::to_string(agents[3 * i + 1]) + " " +
+           std::to_string(agents[3 * i + 2]) + "\n";
+    off[4 * i] = total;
+    off[4 * i + 1] = meta.size();
+    off[4 * i + 2] = hdr.size();
+    off[4 * i + 3] = ag.size();
+    meta += hdr;
+    meta += ag;
+    total += hdr.size() + body + ag.size();
+  }
+  *len = total;
+  if (!out) return EBL_OK;  // size query
+  if (cap < total) return set_err(EBL_ERANGE, "ebl_batch_snapshot_text: the text needs " + std::to_string(total) + " bytes");
+  if (n == 0) return EBL_OK;
+  EBL_CUDA(cudaSetDevice(b->device));
+  if (b->snap_text.n < total) EBL_CUDA(b->snap_text.alloc(total));
+  if (b->snap_meta.n < meta.size()) EBL_CUDA(b->snap_meta.alloc(meta.size()));
+  if (b->snap_off.n < off.size()) EBL_CUDA(b->snap_off.alloc(off.size()));
+  EBL_CUDA(cudaMemcpyAsync(b->snap_meta.p, meta.data(), meta.size(), cudaMemcpyHostToDevice, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(b->snap_off.p, off.data(), off.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                           b->stream));
+  const uint8_t* L = layers_dev ? static_cast<const uint8_t*>(layers_dev) : b->state[b->cur].p;
+  EBL_CUDA(ebl::launch_snapshot_text(L, n, b->h, b->w, b->snap_meta.p, b->snap_off.p, b->snap_text.p, b->stream));
+  EBL_CUDA(cudaMemcpyAsync(out, b->snap_text.p, total, cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  b->launches += 1;
+  return EBL_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// parse_snapshot's token rules (snapshot.cpp:34-53): whitespace split; integers by from_chars over
+// the whole token
+std::vector<std::string> snap_split_ws(const std::string& line) {
+  std::vector<std::string> out;
+  std::istringstream iss(line);
+  std::string tok;
+  while (iss >> tok) out.push_back(tok);
+  return out;
+}
+template <class T>
+bool snap_int(const std::string& tok, const char* what, T* v) {
+  const char* e = tok.data() + tok.size();
+  const auto r = std::from_chars(tok.data(), e, *v);
+  if (r.ec != std::errc() || r.ptr != e) return set_err(EBL_EFILE, std::string("snapshot: invalid ") + what + " '" + tok + "'"), false;
+  return true;
+}
+}  // namespace
+
+extern "C" {
+
+int ebl_snapshot_parse(const char* text, size_t text_len, int* h, int* w, uint64_t* step, uint8_t* layer,
+                       size_t layer_cap, int32_t* agent3, int* has_agent) {
+  if (!text || !h || !w || !step) return set_err(EBL_EINVAL, "ebl_snapshot_parse: null argument");
+  // parse_snapshot (snapshot.cpp:74-121), line by line as std::getline
+  size_t pos = 0;
+  auto getline = [&](std::string& line) -> bool {
+    if (pos >= text_len) return false;
+    const void* nl = std::memchr(text + pos, '\n', text_len - pos);
+    const size_t end = nl ? static_cast<size_t>(static_cast<const char*>(nl) - text) : text_len;
+    line.assign(text + pos, end - pos);
+    pos = nl ? end + 1 : text_len;
+    return true;
+  };
+  std::string line;
+  if (!getline(line)) return set_err(EBL_EFILE, "snapshot: empty input");
+  const auto header = snap_split_ws(line);
+  if (header.size() != 5 || header[0] != "emberline-snapshot" || header[1] != "v1")
+    return set_err(EBL_EFILE, "snapshot: bad header '" + line + "'");
+  int hh = 0, ww = 0;
+  uint64_t st = 0;
+  if (!snap_int(header[2], "height", &hh) || !snap_int(header[3], "width", &ww)) return EBL_EFILE;
+  if (hh < 1 || ww < 1) return set_err(EBL_EFILE, "snapshot: dimensions must be positive");
+  if (!snap_int(header[4], "step", &st)) return EBL_EFILE;
+  const size_t need = static_cast<size_t>(hh) * ww;
+  if (layer && layer_cap < need)
+    return set_err(EBL_ERANGE, "ebl_snapshot_parse: the layer needs " + std::to_string(need) + " bytes");
+  for (int row = hh - 1; row >= 0; --row) {
+    if (!getline(line))
+      return set_err(EBL_EFILE, "snapshot: expected " + std::to_string(hh) + " rows, input ended early");
+    while (!line.empty() && (line.back() == '\r' || line.back() == ' ')) line.pop_back();
+    if (static_cast<int>(line.size()) != ww)
+      return set_err(EBL_EFILE, "snapshot: row has " + std::to_string(line.size()) + " cells, expected " +
+                                    std::to_string(ww));
+    for (int col = 0; col < ww; ++col) {
+      const char c = line[col];
+      const int v = c == 'U' ? 0 : c == 'B' ? 1 : c == 'X' ? 2 : -1;
+      if (v < 0) return set_err(EBL_EFILE, std::string("snapshot: invalid fire-state character '") + c + "'");
+      if (layer) layer[static_cast<size_t>(row) * ww + col] = static_cast<uint8_t>(v);
+    }
+  }
+  bool agent = false;
+  int32_t ar = 0, ac = 0, aw = 0;
+  while (getline(line)) {
+    const auto toks = snap_split_ws(line);
+    if (toks.empty()) continue;
+    if (toks[0] == "agent" && toks.size() == 4 && !agent) {
+      if (!snap_int(toks[1], "agent row", &ar) || !snap_int(toks[2], "agent col", &ac) ||
+          !snap_int(toks[3], "agent water", &aw))
+        return EBL_EFILE;
+      if (ar < 0 || ar >= hh || ac < 0 || ac >= ww) return set_err(EBL_EFILE, "snapshot: agent position out of bounds");
+      if (aw < 0) return set_err(EBL_EFILE, "snapshot: negative agent water");
+      agent = true;
+      continue;
+    }
+    return set_err(EBL_EFILE, "snapshot: unexpected trailing line '" + line + "'");
+  }
+  *h = hh;
+  *w = ww;
+  *step = st;
+  if (has_agent) *has_agent = agent ? 1 : 0;
+  if (agent3 && agent) {
+    agent3[0] = ar;
+    agent3[1] = ac;
+    agent3[2] = aw;
   }
   return EBL_OK;
 }

@@ -105,6 +105,8 @@ struct LandcoverArgs {
 };
 cudaError_t launch_landcover_map(const LandcoverArgs& a, cudaStream_t s);
 // fp32 slope table [grid][cell][8] (terrain form, built with the layers; ember_synth.cu)
+cudaError_t launch_snapshot_text(const uint8_t* layers, int n, int h, int w, const char* meta,
+                                 const unsigned long long* off, char* out, cudaStream_t s);
 cudaError_t launch_pot32t(const float* slope32, const uint2* nfuel, const uint8_t* fuel, const float* pal32,
                           const float* kw32, int n_envs, size_t ncell, size_t ter_stride, int kw_stride, float alpha_l2,
                           float* out, cudaStream_t s);

@@ -312,6 +312,34 @@ __global__ void __launch_bounds__(kSynthThreads) k_pot32t(const float4* __restri
   out[2 * i + 1] = make_float4(o[4], o[5], o[6], o[7]);
 }
 
+// Snapshot text (serialize_snapshot, snapshot.cpp:55-70) of n layers: one CTA per layer writes
+// its header, the H lines of W characters from {U, B, X} (northmost row first; other byte values
+// '?', as state_char), and its optional agent line, at the layer's offset of the concatenation.
+// meta holds the host-formatted header and agent strings; off[i] = {text offset, meta offset,
+// header length, agent length}.
+__global__ void k_snapshot_text(const uint8_t* __restrict__ layers, int h, int w, const char* __restrict__ meta,
+                                const unsigned long long* __restrict__ off, char* __restrict__ out) {
+  const int i = blockIdx.x;
+  const unsigned long long o = off[4 * i], mo = off[4 * i + 1], hl = off[4 * i + 2], al = off[4 * i + 3];
+  char* t = out + o;
+  for (unsigned long long k = threadIdx.x; k < hl; k += blockDim.x) t[k] = meta[mo + k];
+  t += hl;
+  const uint8_t* L = layers + static_cast<size_t>(i) * h * w;
+  const int line = w + 1;
+  const size_t body = static_cast<size_t>(h) * line;
+  for (size_t k = threadIdx.x; k < body; k += blockDim.x) {
+    const int ln = static_cast<int>(k / line), col = static_cast<int>(k - static_cast<size_t>(ln) * line);
+    char ch = '\n';
+    if (col < w) {
+      const uint8_t v = L[static_cast<size_t>(h - 1 - ln) * w + col];
+      ch = v == 0 ? 'U' : v == 1 ? 'B' : v == 2 ? 'X' : '?';
+    }
+    t[k] = ch;
+  }
+  t += body;
+  for (unsigned long long k = threadIdx.x; k < al; k += blockDim.x) t[k] = meta[mo + hl + k];
+}
+
 inline unsigned grid_x(size_t n) { return static_cast<unsigned>((n + kSynthThreads - 1) / kSynthThreads); }
 
 }  // namespace
@@ -350,6 +378,12 @@ cudaError_t launch_pot32t(const float* slope32, const uint2* nfuel, const uint8_
   const size_t n = ncell * n_envs;
   k_pot32t<<<grid_x(n), kSynthThreads, 0, s>>>(reinterpret_cast<const float4*>(slope32), nfuel, fuel, pal32, kw32, n_envs,
                                                ncell, ter_stride, kw_stride, alpha_l2, reinterpret_cast<float4*>(out));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_snapshot_text(const uint8_t* layers, int n, int h, int w, const char* meta,
+                                 const unsigned long long* off, char* out, cudaStream_t s) {
+  if (n > 0) k_snapshot_text<<<n, kSynthThreads, 0, s>>>(layers, h, w, meta, off, out);
   return cudaGetLastError();
 }
 

@@ -53,6 +53,19 @@ def host_buffer(shape, dtype=np.uint8) -> np.ndarray:
     return arr
 
 
+def parse_snapshot(text: str | bytes):
+    """parse_snapshot (snapshot.cpp:74-121): (layer [H, W] uint8, step, agent (row, col, water) or
+    None); malformed text raises FileError with the reference's message."""
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    h, w, step, ha = C.c_int(), C.c_int(), C.c_uint64(), C.c_int()
+    check(lib().ebl_snapshot_parse(b, len(b), C.byref(h), C.byref(w), C.byref(step), None, 0, None, C.byref(ha)))
+    layer = np.empty((h.value, w.value), np.uint8)
+    ag = np.zeros(3, np.int32)
+    check(lib().ebl_snapshot_parse(b, len(b), C.byref(h), C.byref(w), C.byref(step), _ptr(layer), layer.size,
+                                   _ptr(ag), C.byref(ha)))
+    return layer, step.value, (tuple(int(x) for x in ag) if ha.value else None)
+
+
 def default_config(**overrides) -> SimConfig:
     """SimConfig{} (grid.hpp:173-179) with keyword overrides."""
     c = SimConfig()
@@ -228,6 +241,21 @@ class Batch:
 
     def set_pipeline(self, chunks: int) -> None:
         check(lib().ebl_batch_set_pipeline(self._h, chunks))
+
+    def snapshot_text(self, layers_dev: int | None = None, n_layers: int = 0, steps=None, agents=None) -> str:
+        """serialize_snapshot (snapshot.cpp:55-70) of the batch's current layers (or n_layers device
+        layers at layers_dev, e.g. a recorded trajectory), concatenated; steps [n] (default: the
+        batch step); agents [n, 3] (row, col, water; row < 0: no agent line).  Rendered on the
+        device."""
+        n = self.n_envs if layers_dev is None else n_layers
+        st = None if steps is None else np.ascontiguousarray(np.broadcast_to(steps, (n,)), dtype=np.uint64)
+        ag = None if agents is None else np.ascontiguousarray(agents, dtype=np.int32).reshape(n, 3)
+        ln = C.c_size_t()
+        args = (self._h, layers_dev, n, _ptr(st), _ptr(ag))
+        check(lib().ebl_batch_snapshot_text(*args, None, 0, C.byref(ln)))
+        buf = C.create_string_buffer(max(ln.value, 1))
+        check(lib().ebl_batch_snapshot_text(*args, buf, ln.value, C.byref(ln)))
+        return buf.raw[:ln.value].decode()
 
     def step_record(self, n_steps: int) -> np.ndarray:
         """step(n_steps) keeping every step's layers (run_stochastic record=true, engine.cpp:116):

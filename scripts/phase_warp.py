@@ -28,5 +28,6 @@ for name, e in (("heaviest", 338), ("median", 809), ("light", 760)):
         eb._lib.check(eb.lib().ebl_batch_profile(b.handle, pr.ctypes.data))
         p = pr.mean(0) / STEPS
         print(f"{name:8s} x{k:4d}: step {p[6]:6.0f}  dense(max warp) {p[0]:5.0f}  decide(max warp) {p[1]:6.0f}  "
-              f"barrier wait(max) {p[7]:5.0f}  passes/step: max-warp {p[4]:4.2f} all {p[5]:4.2f}", flush=True)
+              f"barrier wait(max) {p[7]:5.0f}  passes/step: max-warp {p[4]:4.2f} all {p[5]:4.2f}  "
+              f"locate {p[8]:5.0f} body(lane 0, candidates) {p[9]:5.0f}", flush=True)
         b.close()
