@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
     Bp0[ro(H + 1) + i] = Bp1[ro(H + 1) + i] = 0u;
   }
   const uint8_t* __restrict__ in = a.in + env * ncell;
+  uint32_t any_b = 0u;  // a burning cell anywhere in the region
   for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
     const int nc = min(32, RW - 32 * it.j);
     uint32_t b = 0u, x = 0u;
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
     }
     Bp0[ro(it.r + 1) + it.j] = b;
     X[ro(it.r) + it.j] = x;
+    any_b |= b;
   }
   const bool use_tab = kTer && a.pot32t && EBL_WARP_POT;  // one wind for all steps: precomputed terms
   const bool use_rec = kTer && a.nfuel && a.n_pal <= 32;
@@ -146,7 +148,10 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
   if (threadIdx.x == 0) s_newly = 0;
   const uint64_t stream = a.streams[env];
   for (int k = threadIdx.x; k < 64; k += blockDim.x) s_prefix[k] = key_prefix(a.seed, stream, a.step + k);
-  __syncthreads();
+  // a region without a burning cell does not change in n_steps <= halo steps (no draw can flip an
+  // Unburned cell without a burning neighbour; the light cone of outside fire stays in the halo):
+  // straight to the store (which maps other byte values to Unburned as a step does)
+  const int n_run = __syncthreads_or(any_b != 0u) || a.traj ? n_steps : 0;
 
   const DiagCounters dg{a.diag};
   const uint64_t gbase = static_cast<uint64_t>(a.row_off + R0) * W + C0;  // RNG index of region (0, 0)
@@ -187,7 +192,7 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
   long long pw_loc = 0, pw_body = 0, pw_ts = 0;
   __shared__ long long s_wd[4][6];
 #endif
-  for (int t = 0; t < n_steps; ++t) {
+  for (int t = 0; t < n_run; ++t) {
 #if EBL_PHASE_PROF
     const long long st0 = clock64();
     pw_t0 = st0;
