@@ -106,6 +106,7 @@ struct ebl_batch {
   DevBuf<float> slope32;            // [grid][cell][8] fp32 slopes of the layers (built by prepare)
   DevBuf<uint2> nfuel;              // [grid][cell] fuel classes of the 8 sources (built with slope32)
   DevBuf<float> pot32t;             // [env or 1][cell][8] fp32 lambda terms (built by prepare)
+  DevBuf<int32_t> tflags[2];           // per-tile activity records of halo-tiled runs (ping-pong)
   DevBuf<char> snap_text, snap_meta;  // snapshot rendering staging (grow-only)
   DevBuf<unsigned long long> snap_off;
   bool pot32t_valid = false;
@@ -951,6 +952,7 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
     b->launches += 2;
   } else {  // bit-sliced blocked kernel: whole env per CTA when it fits, else halo tiles
     const bool force_tiles = b->kernel == EBL_KERNEL_BLOCKED;
+    int tf_par = 0, tf_tiles = -1;  // tile activity records: valid from the 2nd launch of this call
     for (int done = 0; done < n_steps;) {
       ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps - done, force_tiles, 0, b->n_envs,
                                           b->envs_per_cta);
@@ -972,6 +974,22 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
       }
       a.traj = b->traj_out;  // record: the kernel stores every step's tile (no extra launches)
       a.traj_t0 = static_cast<size_t>(done);
+      {  // quiet-tile skipping (warp-local kernel, halo inside the 8 neighbour tiles, no recording)
+        const int tx = (b->w + g.tile_w - 1) / g.tile_w, ty = (b->h + g.tile_h - 1) / g.tile_h;
+        const bool tiled = tx * ty > 1 && g.halo_rows <= g.tile_h && g.halo_cols <= g.tile_w && !a.traj &&
+                           use_warp(b) && g.envs_per_cta == 1;
+        if (tiled) {
+          const size_t n = static_cast<size_t>(tx) * ty * b->n_envs * 4;
+          for (auto& f : b->tflags)
+            if (f.n < n) EBL_CUDA(f.alloc(n));
+          a.tflag_in = tf_tiles == tx * ty ? b->tflags[tf_par].p : nullptr;
+          a.tflag_out = b->tflags[tf_par ^ 1].p;
+          tf_par ^= 1;
+          tf_tiles = tx * ty;
+        } else {
+          tf_tiles = -1;
+        }
+      }
       EBL_CUDA(launch_ca(b, a, g, b->stream));
       b->cur ^= 1;
       b->step += g.n_steps;

@@ -21,6 +21,11 @@ struct StepArgs {
   const uint8_t* in;              // [n_envs][h*w]
   uint8_t* out;
   int32_t* counts;                // [n_envs][4] U,B,X,newly (nullable)
+  // halo-tiled launches of one ebl_step_batch call: per-tile activity records [env][tile]
+  // {bit0 burning in the output tile, bits 1-2 quiet streak (saturating at 2), U, B, X}; read
+  // from the previous launch (null: first launch), written for the next
+  const int32_t* tflag_in;        // int4 records
+  int32_t* tflag_out;
   unsigned long long* diag;       // [2]
   // general form (SpreadTables)
   const double* pot;              // [grid][h*w*8]

@@ -102,6 +102,38 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
   const int tc0 = c0 - C0, tc1 = (DIMC ? W : min(c0 + g.tile_w, W)) - C0;
   const int tj0 = tc0 >> 5, tj1 = (tc1 + 31) >> 5, twords = tj1 - tj0;
 
+  // ---- quiet tiles of a halo-tiled run: skipped outright -----------------------------------------
+  // A tile whose own and 8 neighbours' output tiles had no burning cell after the previous launch
+  // has a quiet region (the halo lies in the neighbours); after two quiet launches both layer
+  // buffers hold its (canonical) bytes, so there is nothing to load, step or store.
+  const size_t tile_id = (static_cast<size_t>(env) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  int streak0 = 0;
+  const int4* const tf_in = reinterpret_cast<const int4*>(a.tflag_in);
+  int4* const tf_out = reinterpret_cast<int4*>(a.tflag_out);
+  if (tf_in) {
+    __shared__ int s_skip;
+    if (threadIdx.x == 0) {
+      const int4 me = tf_in[tile_id];
+      bool quiet = true;
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int ty = static_cast<int>(blockIdx.y) + dy, tx = static_cast<int>(blockIdx.x) + dx;
+          if (ty >= 0 && ty < static_cast<int>(gridDim.y) && tx >= 0 && tx < static_cast<int>(gridDim.x))
+            quiet &= !(tf_in[(static_cast<size_t>(env) * gridDim.y + ty) * gridDim.x + tx].x & 1);
+        }
+      s_skip = quiet && ((me.x >> 1) & 3) >= 2;
+      if (s_skip) {
+        tf_out[tile_id] = me;
+        if (a.counts) {
+          atomicAdd(a.counts + env * 4 + 0, me.y);
+          atomicAdd(a.counts + env * 4 + 2, me.w);
+        }
+      }
+    }
+    __syncthreads();
+    if (s_skip) return;
+    streak0 = (tf_in[tile_id].x >> 1) & 3;
+  }
   // ---- load ----------------------------------------------------------------------------------
   for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
     Bp0[i] = Bp1[i] = 0u;
@@ -426,7 +458,7 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
   for (int p = 0; p < a.n_peers; ++p)  // fused halo exchange: owned rows straight into the neighbour
     store_tile(Bs, a.peer_out[p], nullptr, a.peer_lo[p], a.peer_hi[p], a.peer_dst[p] - a.peer_lo[p]);
   int cu = c3[0], cb = c3[1], cx = c3[2];
-  if (!a.counts) return;
+  if (!a.counts && !a.tflag_out) return;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     cu += __shfl_xor_sync(0xffffffffu, cu, o);
@@ -441,8 +473,14 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
     atomicAdd(&s_newly, newly);
   }
   __syncthreads();
-  if (threadIdx.x < 3) atomicAdd(a.counts + env * 4 + threadIdx.x, s_cnt[threadIdx.x]);
-  if (threadIdx.x == 3) atomicAdd(a.counts + env * 4 + 3, s_newly);
+  if (a.counts) {
+    if (threadIdx.x < 3) atomicAdd(a.counts + env * 4 + threadIdx.x, s_cnt[threadIdx.x]);
+    if (threadIdx.x == 3) atomicAdd(a.counts + env * 4 + 3, s_newly);
+  }
+  if (tf_out && threadIdx.x == 0) {
+    const int streak = n_run == 0 ? min(streak0 + 1, 2) : 0;  // output == input this launch
+    tf_out[tile_id] = make_int4((s_cnt[1] > 0 ? 1 : 0) | (streak << 1), s_cnt[0], s_cnt[1], s_cnt[2]);
+  }
 }
 
 template <int MODE, int WPRC, int DIMC = 0>

@@ -366,6 +366,38 @@ def test_large_single_grid_vs_oracle(port):
     assert np.array_equal(outs[0][0], O.run(port, "port", g, O.DEFAULT_CFG, 11, 0, 0, 60, init[0]))
 
 
+def test_quiet_tiles_skipped_landscape_vs_oracle(port):
+    """One call of many halo-tiled launches over a landscape that is mostly quiet (3 ignitions far
+    apart, 240 steps = 30 launches): tiles without fire in their 3x3 neighbourhood for two launches
+    are skipped outright (no load, step or store).  Final layers == per-step kernel == oracle,
+    fire_fraction counts == the layers' counts, garbage bytes in never-burning tiles canonicalised
+    as by a step."""
+    h, w, steps = 512, 2048, 240
+    t = eb.synth_terrain(12, 1, h, w)
+    t.wind_speed[:] = 8.0
+    t.wind_direction[:] = 0.0
+    init = np.zeros((1, h, w), np.uint8)
+    for r, c in ((40, 100), (300, 1000), (480, 1900)):
+        init[0, r, c] = 1
+    init[0, 200, 1500] = 7   # not a FireState: steps as Unburned (-> 0)
+    init[0, 10, 10:20] = 2   # already burned cells far from the fire
+    outs = []
+    for kernel in (eb.KERNEL_AUTO, eb.KERNEL_TILED):
+        b = _terrain_batch(t, None, kernel)
+        b.set_state(init)
+        b.set_key(12, 0)
+        b.step(steps)
+        outs.append(b.get_state())
+        if kernel == eb.KERNEL_AUTO:
+            cnt = b.counts()
+            f = outs[-1][0]
+            assert [int(cnt[0][k]) for k in range(3)] == [int((f == v).sum()) for v in (0, 1, 2)]
+    assert np.array_equal(outs[0], outs[1])
+    assert outs[0][0, 200, 1500] == 0 and (outs[0][0, 10, 10:20] == 2).all()
+    g = O.grid_terrain(port, "port", t.veg()[0], t.den()[0], t.elevation[0], 30.0, 8.0, 0.0)
+    assert np.array_equal(outs[0][0], O.run(port, "port", g, O.DEFAULT_CFG, 12, 0, 0, steps, init[0]))
+
+
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_record_trajectory_vs_oracle(port, kernel):
     """run_stochastic(record=true) (engine.cpp:108,116) on the device: every step's layers."""
