@@ -302,7 +302,10 @@ __global__ void k_det_back2(DetArgs d, int t) {
 // written) because neighbouring tiles read the old values of this tile's ring.  The slope of the
 // direction-k pot derivative is the source's own record of the opposite direction, negated
 // (atan is odd and fp32 negation exact): 32 contiguous bytes instead of 8 scattered records.
-constexpr int kBackTx = 32, kBackTy = 8;
+#ifndef EBL_DET_CPT
+#define EBL_DET_CPT 2  // cells per thread (rows kBackTy apart): more loads in flight, a thinner ring
+#endif
+constexpr int kBackTx = 32, kBackTy = 8, kCpt = EBL_DET_CPT, kBackRows = kBackTy * kCpt;
 
 __device__ __forceinline__ double back1_alam(const DetArgs& d, size_t base, size_t tb, size_t tr, int i, double& lam,
                                              double& e, double& p_ig, double& a_newly, double& un) {
@@ -318,46 +321,49 @@ __device__ __forceinline__ double back1_alam(const DetArgs& d, size_t base, size
 }
 
 #ifndef EBL_DET_BACK_MINB
-#define EBL_DET_BACK_MINB 5  // 48 registers: 5 CTAs per SM (88 without the bound: 2)
+#define EBL_DET_BACK_MINB 5  // 48 registers: 5 CTAs per SM (kCpt 2: a few spilled bytes, still faster than 4 CTAs)
 #endif
+// Tile of 32 x (8 kCpt) cells, 256 threads; thread (tx, ty) owns rows ty, ty + 8, ... (C4 backward:
+// kCpt 1 23.3 ms, 2 20.8 ms, 4 21.0 ms per run)
 __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_back(DetArgs d, int t) {
   __shared__ double red[6 * 32];
-  __shared__ double s_al[kBackTy + 2][kBackTx + 2];
+  __shared__ double s_al[kBackRows + 2][kBackTx + 2];
   const StepArgs& a = d.s;
   const int h = a.h, w = a.w, ncell = h * w;
   const int env = blockIdx.y;
   const int tiles_x = (w + kBackTx - 1) / kBackTx;
-  const int c0 = (blockIdx.x % tiles_x) * kBackTx, r0 = (blockIdx.x / tiles_x) * kBackTy;
+  const int c0 = (blockIdx.x % tiles_x) * kBackTx, r0 = (blockIdx.x / tiles_x) * kBackRows;
   const int tx = threadIdx.x & (kBackTx - 1), ty = threadIdx.x / kBackTx;
-  const int r = r0 + ty, c = c0 + tx;
-  const bool in = r < h && c < w;
-  const int i = r * w + c;
+  const int c = c0 + tx;
   const size_t base = static_cast<size_t>(env) * ncell;
   const size_t tb = static_cast<size_t>(env) * d.tab_stride;
   const size_t tr = static_cast<size_t>(t) * a.n_envs * ncell + base;
-  double g_gamma = 0.0, g_pc = 0.0, bu = 0.0, Ab = 0.0, Ad = 0.0;
-  // ---- back1 of the own cell ----
-  {
+  double g_gamma = 0.0, g_pc = 0.0, bu[kCpt], Ab[kCpt], Ad[kCpt];
+  // ---- back1 of the own cells ----
+#pragma unroll
+  for (int q = 0; q < kCpt; ++q) {
+    const int r = r0 + ty + kBackTy * q, i = r * w + c;
     double al = 0.0;
-    if (in) {
+    bu[q] = Ab[q] = Ad[q] = 0.0;
+    if (r < h && c < w) {
       double lam, e, p_ig, a_newly, un;
       al = back1_alam(d, base, tb, tr, i, lam, e, p_ig, a_newly, un);
-      bu = d.traj_burn[tr + i];
-      Ab = d.A_burn[base + i];
-      Ad = d.A_bd[base + i];
+      bu[q] = d.traj_burn[tr + i];
+      Ab[q] = d.A_burn[base + i];
+      Ad[q] = d.A_bd[base + i];
       d.A_un_o[base + i] = d.A_un[base + i] + a_newly * p_ig;
       const double F = d.fac_F ? d.fac_F[tb + i] : a.pal64[768 + a.fuel[static_cast<size_t>(env) * a.ter_stride + i]];
-      g_gamma = (a_newly * un * e) * lam * F;  // dgamma/dalpha_gamma = F(v)
-      g_pc = bu * (Ab - Ad);
+      g_gamma += (a_newly * un * e) * lam * F;  // dgamma/dalpha_gamma = F(v)
+      g_pc += bu[q] * (Ab[q] - Ad[q]);
     }
-    s_al[ty + 1][tx + 1] = al;
+    s_al[ty + kBackTy * q + 1][tx + 1] = al;
   }
   // ---- back1 of the ring (a_lambda only) ----
-  constexpr int kRing = 2 * (kBackTx + 2) + 2 * kBackTy;
+  constexpr int kRing = 2 * (kBackTx + 2) + 2 * kBackRows;
   for (int q = threadIdx.x; q < kRing; q += blockDim.x) {
     int sy, sx;
     if (q < kBackTx + 2) sy = 0, sx = q;
-    else if (q < 2 * (kBackTx + 2)) sy = kBackTy + 1, sx = q - (kBackTx + 2);
+    else if (q < 2 * (kBackTx + 2)) sy = kBackRows + 1, sx = q - (kBackTx + 2);
     else sy = 1 + ((q - 2 * (kBackTx + 2)) >> 1), sx = ((q - 2 * (kBackTx + 2)) & 1) ? kBackTx + 1 : 0;
     const int vr = r0 + sy - 1, vc = c0 + sx - 1;
     double al = 0.0;
@@ -368,31 +374,33 @@ __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_ba
     s_al[sy][sx] = al;
   }
   __syncthreads();
-  // ---- back2 of the own cell (source u = (r, c), targets u + d_k) ----
+  // ---- back2 of the own cells (source u = (r, c), targets u + d_k) ----
   double gp = 0.0, gw1 = 0.0, gw2 = 0.0, gs = 0.0;
-  if (in) {
-    double acc_burn = Ab * d.pc + Ad * (1.0 - d.pc);
-    if (bu != 0.0 && d.fac_pb) {  // general form: host-built derivative factors
+#pragma unroll
+  for (int q = 0; q < kCpt; ++q) {
+    const int r = r0 + ty + kBackTy * q, i = r * w + c, sy = ty + kBackTy * q + 1, sx = tx + 1;
+    if (r >= h || c >= w) continue;
+    double acc_burn = Ab[q] * d.pc + Ad[q] * (1.0 - d.pc);
+    if (bu[q] != 0.0 && d.fac_pb) {  // general form: host-built derivative factors
       const size_t o = tb + i;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int vr = r + kDy[k], vc = c + kDx[k];
         if (vr < 0 || vr >= h || vc < 0 || vc >= w) continue;
-        const double al = s_al[ty + 1 + kDy[k]][tx + 1 + kDx[k]];
+        const double al = s_al[sy + kDy[k]][sx + kDx[k]];
         if (al == 0.0) continue;
         const double pot = d.pot[o * 8 + k];
         acc_burn += al * pot;
-        const double ab = al * bu;
+        const double ab = al * bu[q];
         gp += ab * d.fac_pb[o * 8 + k];
         gw1 += ab * pot * d.fac_V[o];
         gw2 += ab * pot * d.fac_Va[o * 8 + k];
         gs += ab * pot * d.fac_S[o * 8 + k];
       }
-    } else if (bu != 0.0) {
+    } else if (bu[q] != 0.0) {
       const TerrainView tv = terrain_view(a, env);
       const float* slope = a.slope32 ? a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8 : nullptr;
       const double V = d.V[env * d.wind_stride];
-      const float zu = tv.elev[i];
       double potk[8];  // the source's 8 pot entries, 64 contiguous bytes requested at once
 #pragma unroll
       for (int k = 0; k < 8; k += 2) {
@@ -411,7 +419,7 @@ __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_ba
       for (int k = 0; k < 8; ++k) {
         const int vr = r + kDy[k], vc = c + kDx[k];
         if (vr < 0 || vr >= h || vc < 0 || vc >= w) continue;
-        const double al = s_al[ty + 1 + kDy[k]][tx + 1 + kDx[k]];
+        const double al = s_al[sy + kDy[k]][sx + kDx[k]];
         if (al == 0.0) continue;
         const double pot = potk[k];
         acc_burn += al * pot;
@@ -422,10 +430,10 @@ __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_ba
         if (slope) {
           S = -static_cast<double>(sown[(k + 4) & 7]);  // u's record, direction k+4: source v
         } else {
-          const float dz = tv.elev[vr * w + vc] - zu;
+          const float dz = tv.elev[vr * w + vc] - tv.elev[i];
           S = dz == dz ? static_cast<double>(atanf(dz * tv.inv_dist32[k & 1])) : 0.0;  // nodata: 0
         }
-        const double ab = al * bu;
+        const double ab = al * bu[q];
         gp += ab * (pot * d.inv_p_base);
         gw1 += ab * pot * V;
         gw2 += ab * pot * V * d.align[env * d.wind_stride * 8 + k];
@@ -444,7 +452,7 @@ __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_ba
 }
 
 int det_blocks_per_env(int h, int w) {
-  return ((w + kBackTx - 1) / kBackTx) * ((h + kBackTy - 1) / kBackTy);
+  return ((w + kBackTx - 1) / kBackTx) * ((h + kBackRows - 1) / kBackRows);
 }
 
 __global__ void k_det_reduce(DetArgs d, int blocks_per_env) {
