@@ -366,6 +366,35 @@ def test_large_single_grid_vs_oracle(port):
     assert np.array_equal(outs[0][0], O.run(port, "port", g, O.DEFAULT_CFG, 11, 0, 0, 60, init[0]))
 
 
+def test_derived_tables_follow_config_wind_and_terrain_changes(port):
+    """The per-candidate pot32t rows (and slope records) are derived from the terrain, the wind
+    and the config: changing each on a live batch rebuilds them -- every run matches a fresh
+    oracle grid with the new inputs."""
+    n, h, w, steps, seed = 4, 64, 96, 60, 9
+    t = eb.synth_terrain(seed, n, h, w)
+    t2 = eb.synth_terrain(seed + 1, n, h, w)
+    init = eb.synth_ignitions(seed, t, 5)
+    b = _terrain_batch(t, None)
+    cfgs = [None, [0.3, 0.1, 0.3, 2.0, 1.5, 0.8], [0.3, 0.1, 0.3, 2.0, 1.5, 0.8], None]
+    winds = [(t.wind_speed, t.wind_direction), (t.wind_speed, t.wind_direction),
+             (t.wind_speed[::-1].copy(), (t.wind_direction + 1.0) % 6.28), (t.wind_speed, t.wind_direction)]
+    terrains = [t, t, t, t2]
+    for cfg, (ws, wd), tt in zip(cfgs, winds, terrains):
+        if tt is not t:
+            b.set_terrain(tt.fuel_class, tt.elevation, tt.class_veg, tt.class_den, tt.cellsize)
+        b.set_config(cfg)
+        b.set_wind(ws, wd)
+        b.set_state(init)
+        b.set_key(seed, 0)
+        b.step(steps)
+        got = b.get_state()
+        c = O.DEFAULT_CFG if cfg is None else cfg
+        for e in (0, n - 1):
+            g = O.grid_terrain(port, "port", tt.veg()[e], tt.den()[e], tt.elevation[e], tt.cellsize, ws[e], wd[e])
+            assert np.array_equal(got[e], O.run(port, "port", g, c, seed, 0, e, steps, init[e]))
+    b.close()
+
+
 def test_quiet_tiles_skipped_landscape_vs_oracle(port):
     """One call of many halo-tiled launches over a landscape that is mostly quiet (3 ignitions far
     apart, 240 steps = 30 launches): tiles without fire in their 3x3 neighbourhood for two launches
