@@ -163,7 +163,8 @@ int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* sp
  *  AUTO      the warp-local kernel: one CTA per env with all n steps fused when an env fits
  *            shared memory (H*W <= 65536), else light-cone-halo tiles, 8 steps per launch;
  *            rows dealt to warps, each warp deciding its own rows' active cells, one block
- *            barrier per step;
+ *            barrier per step; regions without a burning cell skip their steps, and tiles
+ *            quiet for two launches of one call are skipped outright;
  *  WARP      the same as AUTO;
  *  FRONTIER  whole env per CTA (H*W <= 16384), all steps fused, each step touching only its
  *            active list (the next list built from this step's decisions, no dense pass); envs
@@ -357,7 +358,8 @@ int ebl_rl_reset(ebl_batch* b, uint64_t seed, const uint64_t* streams, const uin
  * TANKER row*W+col.  actions == NULL: the device-side random policy
  * (random_policy, rl_env.cpp:237-239 / uniform (x,y) for TANKER).  reward/done
  * may be NULL; host pointers unless `device_io` is 1.  Returns EBL_ELOGIC if a
- * REFERENCE env is already done (rl_env.cpp:173). */
+ * REFERENCE env is already done (rl_env.cpp:173).  TANKER: the layers stay bit-resident
+ * between consecutive calls; any other call that reads or writes them rebuilds the bytes. */
 int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* done, int device_io);
 /* Tanker fused rollout: n_steps random-policy steps on device, rewards summed
  * into reward_sum[e] (host), episodes finished counted into episodes[e]. */
