@@ -371,6 +371,32 @@ __device__ __forceinline__ TerrainView terrain_view(const StepArgs& a, int env, 
   return t;
 }
 
+// ignite_terrain_pot_pre with the terrain view built only on the fp64 fallback path (the common
+// fp32 decision needs none of its pointers).
+__device__ __forceinline__ bool ignite_pot(const StepArgs& a, int env, int srow, float4 T0, float4 T1, int w, int r,
+                                           int c, uint32_t nb, uint64_t m, const DiagCounters& dg) {
+  if (!a.force64) {
+    const float T[8] = {T0.x, T0.y, T0.z, T0.w, T1.x, T1.y, T1.z, T1.w};
+    float x = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x += (nb >> k) & 1u ? T[k] : 0.f;
+    if (x == 0.f) return false;  // gamma or lambda exactly 0: p = 0, u < 0 is false
+    const float p32 = p_ignite32(x);
+    if (p32 > 1e-12f) {
+      const uint64_t lo = static_cast<uint64_t>(p32 * static_cast<float>((1.0 - kGuardRel) * 0x1p53));
+      const uint64_t hi = static_cast<uint64_t>(p32 * static_cast<float>((1.0 + kGuardRel) * 0x1p53));
+      if (m < lo) return true;
+      if (m >= hi) return false;
+    }
+  }
+  const TerrainView t = terrain_view(a, env, srow);
+  dg.fallback();
+  const double u = bits_to_uniform(m);
+  const double p = terrain_p64(t, w, r, c, nb);
+  if (fabs(u - p) < kAmbiguousBand) dg.ambiguous();
+  return u < p;
+}
+
 // Decision for an Unburned cell with burning-neighbour mask nb != 0.
 // `srow` selects the wind-schedule entry in force (sched_row).
 template <int MODE>

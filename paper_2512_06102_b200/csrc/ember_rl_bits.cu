@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
                               ((upw & 2u) << 5) | ((upw & 1u) << 7);
           bool ig;
           if (use_tab)
-            ig = ignite_terrain_pot_pre(terrain_view(a, env), rec.s0, rec.s1, W, rr, cc, nb, m, dg);
+            ig = ignite_pot(a, env, 0, rec.s0, rec.s1, W, rr, cc, nb, m, dg);
           else if (use_rec)
             ig = ignite_terrain_rec_pre(terrain_view(a, env), rec, s_srckw, s_pal + 256, a.alpha_s_l2, W, rr, cc, nb, m, dg);
           else if constexpr (kTer)

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
 #endif
     const uint32_t* B = cur ? Bp1 : Bp0;
     uint32_t* Bn = cur ? Bp0 : Bp1;
-    const int srow = sched_row(a, a.step + static_cast<uint64_t>(t));
+    const int srow = a.sched_len > 1 ? sched_row(a, a.step + static_cast<uint64_t>(t)) : 0;
     if (t > 0 && a.sched_len > 1) {  // CTA-uniform: time-varying wind
       load_wind(srow);
       __syncthreads();
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGe
                               ((upw & 2u) << 5) | ((upw & 1u) << 7);
           bool ig;
           if (use_tab)
-            ig = ignite_terrain_pot_pre(terrain_view(a, env, srow), rec.s0, rec.s1, W, gr, gc, nb, m, dg);
+            ig = ignite_pot(a, env, srow, rec.s0, rec.s1, W, gr, gc, nb, m, dg);
           else if (use_rec)
             ig = ignite_terrain_rec_pre(terrain_view(a, env, srow), rec, s_srckw, s_pal + 256, a.alpha_s_l2, W, gr, gc,
                                         nb, m, dg);
