@@ -1044,14 +1044,13 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
   EBL_CUDA(cudaEventRecord(b->pipe_ev_start, b->stream));
   EBL_CUDA(cudaStreamWaitEvent(b->pipe_in, b->pipe_ev_start, 0));
   for (int c = 0; c < chunks; ++c) EBL_CUDA(cudaStreamWaitEvent(b->pipe_comp[c], b->pipe_ev_start, 0));
-  // chunk boundaries: decreasing sizes (the first chunks start computing early; the last ones,
-  // whose copies finish last, are small): weight of chunk c = ratio^c (EBL_PIPE_RATIO overrides the
-  // default for tuning runs; 1 = equal chunks)
+  // chunk boundaries: weight of chunk c = ratio^c, equal chunks by default (measured best:
+  // scripts/pipeline_ratio_sweep.sh; EBL_PIPE_RATIO < 1 makes the later chunks smaller)
   std::vector<int> bound(chunks + 1, 0);
   {
     static const double ratio = [] {
       const char* e = std::getenv("EBL_PIPE_RATIO");
-      return e ? std::atof(e) : 0.7;
+      return e ? std::atof(e) : 1.0;  // C1 e2e, 4 chunks: equal 4.12e12, 0.7: 3.95e12, 0.5: 3.79e12
     }();
     std::vector<double> wgt(chunks);
     double tot = 0.0, acc = 0.0;
