@@ -1071,6 +1071,14 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
     cudaGetLastError();
   }
   a.out2 = host_dev;
+  // trailing chunks with zero-copy output: the later half by default (C1 e2e, 4 chunks: all 4.07e12,
+  // last 1 4.11e12, last 2 4.29e12; scripts/pipeline_zc_sweep.sh); EBL_PIPE_ZC overrides
+  static const int zc_env = [] {
+    const char* e = std::getenv("EBL_PIPE_ZC");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int zc_keep = zc_env >= 0 ? zc_env : (chunks + 1) / 2;
+  const int zc_from = host_dev ? std::max(0, chunks - zc_keep) : chunks;
   for (int c = 0; c < chunks; ++c) {
     const int off = bound[c], n = bound[c + 1] - off;
     if (n <= 0) continue;
@@ -1084,16 +1092,23 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
     cudaStream_t s = b->pipe_comp[c];
     EBL_CUDA(cudaStreamWaitEvent(s, b->pipe_ev_in[c], 0));
     EBL_CUDA(cudaMemsetAsync(b->counts.p + static_cast<size_t>(off) * 4, 0, static_cast<size_t>(n) * 4 * sizeof(int32_t), s));
-    if (frontier) EBL_CUDA(ebl::launch_step_frontier(chunk_args(b, a, off, n), b->mode, n_steps, s));
-    else EBL_CUDA(launch_ca(b, chunk_args(b, a, off, n), g, s));
+    // mapped output: only the chunks whose envs can still be running after the last input copy
+    // write their layers over PCIe from the kernel (zero_copy_from on); earlier chunks are copied
+    // back by DMA once the inputs are all in, so their results do not share the link with the
+    // input stream
+    ebl::StepArgs ca = chunk_args(b, a, off, n);
+    if (c < zc_from) ca.out2 = nullptr;
+    if (frontier) EBL_CUDA(ebl::launch_step_frontier(ca, b->mode, n_steps, s));
+    else EBL_CUDA(launch_ca(b, ca, g, s));
     EBL_CUDA(cudaEventRecord(b->pipe_ev_done[c], s));
   }
+  EBL_CUDA(cudaStreamWaitEvent(b->pipe_out, b->pipe_ev_in[chunks - 1], 0));
   for (int c = 0; c < chunks; ++c) {
     const int off = bound[c], n = bound[c + 1] - off;
     if (n <= 0) continue;
     const size_t bytes = static_cast<size_t>(n) * b->ncell, boff = static_cast<size_t>(off) * b->ncell;
     EBL_CUDA(cudaStreamWaitEvent(b->pipe_out, b->pipe_ev_done[c], 0));
-    if (!host_dev)
+    if (!host_dev || c < zc_from)
       EBL_CUDA(cudaMemcpyAsync(final_states + boff, b->state[b->cur ^ 1].p + boff, bytes, cudaMemcpyDeviceToHost,
                                b->pipe_out));
   }
