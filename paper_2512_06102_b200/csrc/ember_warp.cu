@@ -66,8 +66,11 @@ __device__ __forceinline__ int nth_set_bit(uint32_t v, int q) {
 
 // DIMC: the env's side when the env is a DIMC x DIMC square known at compile time (128: C1, 64:
 // C2-sized), else 0; WPRC: words per row when known (2, 4), else 0.
+#ifndef EBL_WARP_MINB
+#define EBL_WARP_MINB 8  // 64 registers; 7 (72 registers, still one wave for C1): same C1, slower C3
+#endif
 template <int MODE, int WPRC, int DIMC>
-__global__ void __launch_bounds__(kWpThreads, 8) k_step_warp(StepArgs a, BlockGeom g) {
+__global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArgs a, BlockGeom g) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int32_t s_cnt[3];
   __shared__ int32_t s_newly;
