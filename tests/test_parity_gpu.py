@@ -593,3 +593,22 @@ def test_pipelined_run_pinned_zero_copy(chunks, huge):
         eb._lib.check(eb.lib().ebl_batch_run(b.handle, pi, steps, po))
         assert np.array_equal(np.asarray(h_out), want)
         assert np.array_equal(b.get_state(), want)  # the device copy is kept as well
+
+
+@pytest.mark.slow
+def test_bench_c1_workload_every_env_vs_reference():
+    """The exact bench.py C1 workload (1024 envs x 128^2 x 200 steps, seed, 5 ignitions): every
+    env's final layer from the device equals the reference engine's own run_stochastic
+    (oracle/_ref, OpenMP over envs; the C restatement where the reference is not built)."""
+    import bench
+    t = eb.synth_terrain(bench.SEED, bench.N_ENVS, bench.H, bench.W)
+    init = eb.synth_ignitions(bench.SEED, t, bench.IGNITIONS)
+    b = _terrain_batch(t, None)
+    b.set_state(init)
+    b.set_key(bench.SEED, 0)
+    b.step(bench.CA_STEPS)
+    got = b.get_state()
+    assert b.diag()["ambiguous"] == 0
+    b.close()
+    _, _, kind, _, want = bench.cpu_reference_sample(bench.N_ENVS)
+    assert np.array_equal(got, want.reshape(got.shape)), kind
