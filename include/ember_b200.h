@@ -166,10 +166,6 @@ int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* sp
  *            barrier per step; regions without a burning cell skip their steps, and tiles
  *            quiet for two launches of one call are skipped outright;
  *  WARP      the same as AUTO;
- *  FRONTIER  whole env per CTA (H*W <= 16384), all steps fused, each step touching only its
- *            active list (the next list built from this step's decisions, no dense pass); envs
- *            whose list outgrows its capacity are continued by the blocked kernel in a second
- *            launch.  Faster per step for small fires, not for the heaviest;
  *  TILED     the per-cell tile kernel, one step per launch (independent implementation);
  *  RESIDENT  the pooled-list blocked kernel, whole env per CTA (error if it does not fit);
  *  BLOCKED   the pooled-list blocked kernel with halo tiles even when the env would fit. */
@@ -177,12 +173,9 @@ int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* sp
 #define EBL_KERNEL_TILED 1
 #define EBL_KERNEL_RESIDENT 2
 #define EBL_KERNEL_BLOCKED 3
-#define EBL_KERNEL_FRONTIER 5
 #define EBL_KERNEL_WARP 6
-#define EBL_KERNEL_WARP2 7 /* warp-local, two whole envs per 256-thread CTA */
-#define EBL_KERNEL_PAIRED 4 /* resident, two envs per CTA sharing 256 threads and one pooled
-                               active list (H*W <= 32768); selectable only (AUTO does not pair:
-                               slower on C1, ember_kernels.h) */
+/* (4, 5 and 7 named kernel variants measured slower than WARP and removed; set_kernel rejects
+ * them with EBL_EINVAL) */
 int ebl_batch_set_kernel(ebl_batch* b, int which);
 /* Explicit tiling of the blocked kernel (tile_h rows x tile_w cols, tile_w a multiple of
  * 32, `halo` rows of light cone = steps per launch); tile_h == 0 restores planning. */
@@ -228,9 +221,10 @@ int ebl_batch_intensity_form(ebl_batch* b, int record_form, float* lambda, float
  * CPU reference is only possible here), [2] steps, [3] kernel
  * launches issued. */
 int ebl_batch_diag(ebl_batch* b, uint64_t* out4, int reset);
-/* Number of envs the last FRONTIER run handed over to the blocked kernel (active list over its
- * capacity; diagnostics and tests). */
-int ebl_batch_frontier_handovers(ebl_batch* b, int* count);
+/* Tile statistics of the warp-local kernel since the last reset: [0] regions (CTAs) that loaded
+ * and stepped or stored their tile, [1] regions launched (the rest were quiet tiles skipped
+ * outright).  Their ratio is the share of the dense cell-updates actually visited. */
+int ebl_batch_tile_stats(ebl_batch* b, uint64_t* out2, int reset);
 /* Phase profile of the resident blocked kernel (diagnostic builds with -DEBL_PHASE_PROF=1 only;
  * otherwise set_profiling(on) fails with EBL_ESTATE): each launch stores per env int64
  * [n_envs][10] = {P1 cycles (to the first barrier), P2 cycles (to the second), active cells,

@@ -711,3 +711,204 @@ long ebo_snapshot_text(int h, int w, const uint8_t* fire, uint64_t step, int ar,
 #undef EBO_PUT
   return total;
 }
+
+/* ---------------------------------------------------------------- synthetic C1 inputs
+ * The benchmark's own input generator (not a reference function), restated
+ * here so the CPU arms of bench.py build their inputs without the product library.  Pinned
+ * bit-for-bit against ebl_synth_terrain / ebl_synth_ignitions by tests/test_oracle_pin.py.
+ * Lattice values and wind are keyed by the reference RNG (rng.hpp:38-58) with draw domain
+ * kDrawSynthesis = 3; ignitions by kDrawEnvSetup = 1 (rng.hpp:22-25).  The palette is
+ * default_worldcover_table (geodata.cpp:305-319). */
+enum { DRAW_SYNTH = 3 };
+
+static void noise2d(uint64_t seed, uint64_t layer, uint64_t stream, int h, int w, int octaves,
+                    int period, double* out) {
+  memset(out, 0, sizeof(double) * (size_t)h * w);
+  double amp = 1.0;
+  for (int o = 0; o < octaves; ++o) {
+    int L = period >> o;
+    if (L < 1) L = 1;
+    const int gh = h / L + 2, gw = w / L + 2;
+    double* lat = (double*)malloc(sizeof(double) * (size_t)gh * gw);
+    for (size_t i = 0; i < (size_t)gh * gw; ++i)
+      lat[i] = ebo_rng_uniform(seed, layer + (uint64_t)o, stream, i, DRAW_SYNTH);
+    for (int r = 0; r < h; ++r) {
+      const int gy = r / L;
+      double ty = (r - gy * L + 0.5) / L;
+      ty = ty * ty * (3.0 - 2.0 * ty); /* smoothstep */
+      for (int c = 0; c < w; ++c) {
+        const int gx = c / L;
+        double tx = (c - gx * L + 0.5) / L;
+        tx = tx * tx * (3.0 - 2.0 * tx);
+        const double* a = lat + (size_t)gy * gw + gx;
+        const double* b = a + gw;
+        const double s0 = a[0] + (a[1] - a[0]) * tx;
+        const double s1 = b[0] + (b[1] - b[0]) * tx;
+        out[(size_t)r * w + c] += amp * (s0 + (s1 - s0) * ty);
+      }
+    }
+    free(lat);
+    amp *= 0.5;
+  }
+}
+
+static void minmax(const double* v, size_t n, double* lo, double* hi) {
+  *lo = *hi = v[0];
+  for (size_t i = 0; i < n; ++i) {
+    if (v[i] < *lo) *lo = v[i];
+    if (v[i] > *hi) *hi = v[i];
+  }
+}
+
+#define SYNTH_BINS 4096
+static int imin(int a, int b) { return a < b ? a : b; }
+static int imax(int a, int b) { return a > b ? a : b; }
+
+static void synth_env(uint64_t seed, uint64_t stream, int h, int w, double elev_max, uint8_t* cls,
+                      float* elev, double* scratch) {
+  const size_t n = (size_t)h * w;
+  double lo, hi;
+  /* landcover: 4 octaves, period clamp(min(h,w)/4, 4, 64), 11 equal-count classes by a
+   * 4096-bin histogram of the noise */
+  noise2d(seed, 1000, stream, h, w, 4, imin(64, imax(4, imin(h, w) / 4)), scratch);
+  minmax(scratch, n, &lo, &hi);
+  const double scale = hi > lo ? SYNTH_BINS / (hi - lo) : 0.0;
+  static __thread uint64_t hist[SYNTH_BINS];
+  memset(hist, 0, sizeof hist);
+  for (size_t i = 0; i < n; ++i) hist[imin(SYNTH_BINS - 1, (int)((scratch[i] - lo) * scale))]++;
+  int cut[10], j = 0;
+  uint64_t acc = 0;
+  for (int b = 0; b < SYNTH_BINS && j < 10; ++b) {
+    acc += hist[b];
+    while (j < 10 && acc * 11 >= (uint64_t)(j + 1) * n) cut[j++] = b + 1;
+  }
+  while (j < 10) cut[j++] = SYNTH_BINS;
+  for (size_t i = 0; i < n; ++i) {
+    const int b = imin(SYNTH_BINS - 1, (int)((scratch[i] - lo) * scale));
+    int k = 0;
+    while (k < 10 && b >= cut[k]) ++k;
+    cls[i] = (uint8_t)k;
+  }
+  /* elevation: 6 octaves, period clamp(min(h,w)/2, 8, 128), affinely mapped to [0, elev_max] */
+  noise2d(seed, 2000, stream, h, w, 6, imin(128, imax(8, imin(h, w) / 2)), scratch);
+  minmax(scratch, n, &lo, &hi);
+  const double es = hi > lo ? elev_max / (hi - lo) : 0.0;
+  for (size_t i = 0; i < n; ++i) elev[i] = (float)((scratch[i] - lo) * es);
+}
+
+void ebo_synth_terrain(uint64_t seed, uint32_t env_id0, int n_envs, int h, int w, double elev_max,
+                       double wind_max, uint8_t* fuel_class, float* elevation, double* wind_speed,
+                       double* wind_direction) {
+  const size_t n = (size_t)h * w;
+#pragma omp parallel
+  {
+    double* scratch = (double*)malloc(sizeof(double) * n);
+#pragma omp for schedule(dynamic, 1)
+    for (int e = 0; e < n_envs; ++e) {
+      const uint64_t stream = (uint64_t)env_id0 + (uint64_t)e;
+      synth_env(seed, stream, h, w, elev_max, fuel_class + e * n, elevation + e * n, scratch);
+      if (wind_speed) wind_speed[e] = wind_max * ebo_rng_uniform(seed, 3000, stream, 0, DRAW_SYNTH);
+      if (wind_direction) wind_direction[e] = TWO_PI * ebo_rng_uniform(seed, 3000, stream, 1, DRAW_SYNTH);
+    }
+    free(scratch);
+  }
+}
+
+void ebo_worldcover_palette(int32_t* codes, double* veg, double* den) {
+  /* default_worldcover_table (geodata.cpp:305-319), dense in code order */
+  static const int32_t kc[11] = {10, 20, 30, 40, 50, 60, 70, 80, 90, 95, 100};
+  static const double kv[11] = {0.4, 0.25, 0.15, 0.0, -0.8, -0.7, -1.0, -1.0, -0.4, -0.2, -0.3};
+  static const double kd[11] = {0.3, 0.1, -0.1, -0.2, -0.8, -0.6, -1.0, -1.0, -0.3, -0.1, -0.4};
+  for (int i = 0; i < 11; ++i) {
+    if (codes) codes[i] = kc[i];
+    if (veg) veg[i] = kv[i];
+    if (den) den[i] = kd[i];
+  }
+}
+
+int ebo_synth_ignitions(uint64_t seed, uint32_t env_id0, int n_envs, int h, int w,
+                        const uint8_t* fuel_class, const double* class_veg, const double* class_den,
+                        int count, uint8_t* states) {
+  const uint64_t n = (uint64_t)h * w;
+  int total = 0;
+#pragma omp parallel for schedule(static) reduction(+ : total)
+  for (int e = 0; e < n_envs; ++e) {
+    uint8_t* st = states + e * n;
+    const uint8_t* fc = fuel_class + e * n;
+    memset(st, 0, n);
+    const uint64_t stream = (uint64_t)env_id0 + (uint64_t)e;
+    int placed = 0;
+    /* uniform cells until `count` distinct burnable ones ((1+veg)(1+den) > 0, veg/den clamped
+     * as FuelField does, grid.cpp:75-76); at most 64 n draws */
+    for (uint64_t k = 0; placed < count && k < 64 * n; ++k) {
+      const uint64_t cell = ebo_rng_below(seed, 0, stream, k, DRAW_SETUP, n);
+      const double v = clamp1(class_veg[fc[cell]]), d = clamp1(class_den[fc[cell]]);
+      if (st[cell] == 1 || !((1.0 + v) * (1.0 + d) > 0.0)) continue;
+      st[cell] = 1;
+      ++placed;
+    }
+    total += placed;
+  }
+  return total;
+}
+
+/* ---------------------------------------------------------------- CPU-baseline harnesses
+ * C2: the tanker step (ebo_tanker_step) over n envs, OpenMP over envs, random device policy
+ * (ebo_tanker_policy), auto-reset.  Tables per env are built before the clock starts (the
+ * reference's FireSuppressionEnv likewise holds its tables for the whole episode).  Env e has id
+ * env_ids[e] (null: env_id0 + e).  Returns the wall seconds of `steps` steps of every env;
+ * optional outputs: *reward_sum (all envs), per env the final fire / wet layers [n][h*w], the
+ * reward sum and the number of finished episodes. */
+double ebo_tanker_run_envs(ebo_grid* const* grids, int n_envs, const double* cfg,
+                           const ebo_tanker_cfg* tc, uint64_t seed, uint32_t env_id0,
+                           const uint32_t* env_ids, int steps, int threads, double* reward_sum,
+                           uint8_t* fire_out, uint8_t* wet_out, double* env_reward, int32_t* env_episodes) {
+  if (threads > 0) omp_set_num_threads(threads);
+  const size_t n = (size_t)grids[0]->h * grids[0]->w;
+  double** pots = (double**)malloc(sizeof(double*) * n_envs);
+  double** gams = (double**)malloc(sizeof(double*) * n_envs);
+  uint8_t* fire = fire_out ? fire_out : (uint8_t*)malloc(n * n_envs);
+  uint8_t* wet = wet_out ? wet_out : (uint8_t*)malloc(n * n_envs);
+  ebo_tanker_state* st = (ebo_tanker_state*)malloc(sizeof(ebo_tanker_state) * n_envs);
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int e = 0; e < n_envs; ++e) {
+    const uint32_t id = env_ids ? env_ids[e] : env_id0 + (uint32_t)e;
+    pots[e] = (double*)malloc(sizeof(double) * n * 8);
+    gams[e] = (double*)malloc(sizeof(double) * n);
+    ebo_tables(grids[e], cfg, pots[e], gams[e]);
+    ebo_tanker_reset(grids[e], tc, seed, id, 0, st + e, fire + e * n, wet + e * n);
+  }
+  double total = 0.0;
+  struct timespec t0, t1;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : total)
+  for (int e = 0; e < n_envs; ++e) {
+    const uint32_t id = env_ids ? env_ids[e] : env_id0 + (uint32_t)e;
+    double mine = 0.0;
+    int32_t eps = 0;
+    for (int t = 0; t < steps; ++t) {
+      float rw;
+      uint8_t dn;
+      const int a = ebo_tanker_policy(seed, id, st + e, (int)n);
+      ebo_tanker_step(grids[e], pots[e], gams[e], cfg[5], tc, seed, id, a, st + e, fire + e * n,
+                      wet + e * n, &rw, &dn);
+      mine += rw;
+      eps += dn;
+    }
+    if (env_reward) env_reward[e] = mine;
+    if (env_episodes) env_episodes[e] = eps;
+    total += mine;
+  }
+  clock_gettime(CLOCK_MONOTONIC, &t1);
+  for (int e = 0; e < n_envs; ++e) {
+    free(pots[e]);
+    free(gams[e]);
+  }
+  free(pots);
+  free(gams);
+  if (!fire_out) free(fire);
+  if (!wet_out) free(wet);
+  free(st);
+  if (reward_sum) *reward_sum = total;
+  return (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+}

@@ -141,6 +141,22 @@ int ebo_calibrate(const ebo_grid* g, const double* un0, const double* bu0, const
                   int iterations, const double* init_theta, const int* optimize, double lr,
                   double* loss_hist, double* theta_hist, double* best_theta, double* best_loss);
 
+/* The benchmark's synthetic inputs (not a reference function), restated so
+ * the CPU arms never load the product library; pinned to ebl_synth_terrain/_ignitions. */
+void ebo_synth_terrain(uint64_t seed, uint32_t env_id0, int n_envs, int h, int w, double elev_max,
+                       double wind_max, uint8_t* fuel_class, float* elevation, double* wind_speed,
+                       double* wind_direction);
+void ebo_worldcover_palette(int32_t* codes, double* veg, double* den);
+int ebo_synth_ignitions(uint64_t seed, uint32_t env_id0, int n_envs, int h, int w,
+                        const uint8_t* fuel_class, const double* class_veg, const double* class_den,
+                        int count, uint8_t* states);
+
+/* CPU-baseline harness for C2: the tanker step over n envs, OpenMP over envs (see .c). */
+double ebo_tanker_run_envs(ebo_grid* const* grids, int n_envs, const double* cfg,
+                           const ebo_tanker_cfg* tc, uint64_t seed, uint32_t env_id0,
+                           const uint32_t* env_ids, int steps, int threads, double* reward_sum,
+                           uint8_t* fire_out, uint8_t* wet_out, double* env_reward, int32_t* env_episodes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,6 +85,11 @@ _PORT_SIG = {
     "ebo_det_loss_grad": (None, [_P, _P, _I, _P, _P, _D, _D, _I, C.POINTER(_D), _P]),
     "ebo_calibrate": (_I, [_P, _P, _P, _P, _P, _I, _D, _D, _I, _I, _P, _P, _D, _P, _P, _P, C.POINTER(_D)]),
     "ebo_snapshot_text": (C.c_long, [_I, _I, _P, _U64, _I, _I, _I, C.c_char_p, C.c_long]),
+    "ebo_synth_terrain": (None, [_U64, _U32, _I, _I, _I, _D, _D, _P, _P, _P, _P]),
+    "ebo_worldcover_palette": (None, [_P, _P, _P]),
+    "ebo_synth_ignitions": (_I, [_U64, _U32, _I, _I, _I, _P, _P, _P, _I, _P]),
+    "ebo_tanker_run_envs": (_D, [_P, _I, _P, C.POINTER(TankerCfg), _U64, _U32, _P, _I, _I, C.POINTER(_D),
+                                 _P, _P, _P, _P]),
 }
 
 _REF_SIG = {
@@ -105,6 +110,8 @@ _REF_SIG = {
     "ref_step_batch": (_I, [_P, _P, _U64, _U64, _I, _I, _P, _P]),
     "ref_run_envs": (_D, [_P, _I, _P, _U64, _P, _I, _P, _I]),
     "ref_max_threads": (_I, []),
+    "ref_loss_grad_envs": (_D, [_P, _I, _P, _I, _P, _P, _D, _D, _I, _P, _P, _I]),
+    "ref_env_batch": (_D, [C.POINTER(EnvCfg), _I, _U64, _U64, _I, _I, C.POINTER(C.c_longlong), C.POINTER(_D)]),
     "ref_worldcover": (_I, [_I, C.POINTER(_D), C.POINTER(_D)]),
     "ref_env_preset": (_I, [_I, C.POINTER(EnvCfg)]),
     "ref_env_reset": (_I, [C.POINTER(EnvCfg), _U64, _U64, C.POINTER(EnvSt), _P]),
@@ -286,3 +293,57 @@ def snapshot_text(L, kind, fire, step, agent=None) -> bytes:
     buf = C.create_string_buffer(n)
     fn(h, w, ptr(fire), step, ar, ac, wt, buf, n)
     return buf.raw[:n]
+
+
+class SynthTerrain:
+    """The benchmark's synthetic inputs from the port (no product library): same fields as
+    paper_2512_06102_b200.Terrain, bit-identical to ebl_synth_terrain (tests/test_oracle_pin.py)."""
+
+    def __init__(self, seed, n_envs, h, w, env_id0=0, elev_max=500.0, wind_max=10.0):
+        L = port()
+        self.fuel_class = np.empty((n_envs, h, w), dtype=np.uint8)
+        self.elevation = np.empty((n_envs, h, w), dtype=np.float32)
+        self.wind_speed = np.empty(n_envs)
+        self.wind_direction = np.empty(n_envs)
+        L.ebo_synth_terrain(seed, env_id0, n_envs, h, w, elev_max, wind_max, ptr(self.fuel_class),
+                            ptr(self.elevation), ptr(self.wind_speed), ptr(self.wind_direction))
+        self.class_veg = np.empty(11)
+        self.class_den = np.empty(11)
+        L.ebo_worldcover_palette(None, ptr(self.class_veg), ptr(self.class_den))
+        self.cellsize = 30.0
+        self.seed, self.env_id0 = seed, env_id0
+
+    def veg(self):
+        return self.class_veg[self.fuel_class]
+
+    def den(self):
+        return self.class_den[self.fuel_class]
+
+    def ignitions(self, count, seed=None):
+        n, h, w = self.fuel_class.shape
+        st = np.empty((n, h, w), dtype=np.uint8)
+        port().ebo_synth_ignitions(self.seed if seed is None else seed, self.env_id0, n, h, w,
+                                   ptr(self.fuel_class), ptr(self.class_veg), ptr(self.class_den),
+                                   count, ptr(st))
+        return st
+
+
+def tanker_run_envs(terrain, env_ids, cfg, seed, steps, ignitions=5, max_steps=256, threads=0):
+    """The C restatement of the C2 tanker env over the given env ids (OpenMP over envs): returns
+    dict(fire, wet [n, h, w], reward [n], episodes [n], seconds)."""
+    L = port()
+    ids = np.ascontiguousarray(env_ids, dtype=np.uint32)
+    n = ids.size
+    _, h, w = terrain.fuel_class.shape
+    grids = [grid_terrain(L, "port", terrain.class_veg[terrain.fuel_class[e]],
+                          terrain.class_den[terrain.fuel_class[e]], terrain.elevation[e], terrain.cellsize,
+                          terrain.wind_speed[e], terrain.wind_direction[e]) for e in ids]
+    hs = (_P * n)(*[g.h for g in grids])
+    fire = np.empty((n, h, w), np.uint8)
+    wet = np.empty((n, h, w), np.uint8)
+    rw = np.empty(n)
+    ep = np.empty(n, np.int32)
+    tc = TankerCfg(ignitions, max_steps, 1)
+    secs = L.ebo_tanker_run_envs(hs, n, ptr(cfg_array(cfg)), C.byref(tc), seed, 0, ptr(ids), steps, threads,
+                                 None, ptr(fire), ptr(wet), ptr(rw), ptr(ep))
+    return dict(fire=fire, wet=wet, reward=rw, episodes=ep, seconds=secs)

@@ -277,6 +277,30 @@ double ref_run_envs(void* const* grids, int n_envs, const double* c, std::uint64
 
 int ref_max_threads() { return omp_get_max_threads(); }
 
+// C4 CPU-baseline harness: run_deterministic<Dual<6>> + loss per env, OpenMP
+// over envs, the body of ref_loss_grad (calibrate.cpp:144-146 per env).  fire0s/masks
+// [n_envs][h*w]; losses [n_envs], grads [n_envs][6].  Returns wall seconds (-1 on error).
+int ref_loss_grad(const void* gp, const double* c, int steps, const std::uint8_t* fire0,
+                  const double* mask, double bce_w, double mse_w, int pool, double* loss_out,
+                  double* grad6);
+double ref_loss_grad_envs(void* const* grids, int n_envs, const double* c, int steps,
+                          const std::uint8_t* fire0s, const double* masks, double bce_w, double mse_w,
+                          int pool, double* losses, double* grads, int threads) {
+  const auto* g0 = static_cast<const R::GridState*>(grids[0]);
+  const std::size_t n = static_cast<std::size_t>(g0->height()) * g0->width();
+  if (threads > 0) omp_set_num_threads(threads);
+  int bad = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : bad)
+  for (int e = 0; e < n_envs; ++e)
+    bad += ref_loss_grad(grids[e], c, steps, fire0s + e * n, masks + e * n, bce_w, mse_w, pool, losses + e,
+                         grads + 6 * e) != 0;
+  const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return bad ? -1.0 : s;
+}
+
+
+
 // ---- fuel table (geodata.cpp default_worldcover_table) -----------------------
 int ref_worldcover(int code, double* veg, double* den) {
   try {
@@ -530,6 +554,40 @@ int ref_parse_snapshot(const char* text, long len, int* h, int* w, std::uint64_t
     fail(e);
     return -1;
   }
+}
+
+// C2 reference CPU baseline: FireSuppressionEnv (rl_env.cpp:125-210) over n envs with OpenMP
+// over envs (the parallel form of run_batch_episodes, rl_env.cpp:263-285), random_policy
+// actions, an env that finishes is reset with the next stream (first_stream + k * n_envs).
+// `steps` env-steps per env; returns wall seconds, *env_steps and *reward_sum.
+double ref_env_batch(const RefEnvCfg* c, int n_envs, std::uint64_t seed, std::uint64_t first_stream,
+                     int steps, int threads, long long* env_steps, double* reward_sum) {
+  const R::EnvConfig ec = env_cfg_of(*c);
+  const R::FireSuppressionEnv env(ec);
+  if (threads > 0) omp_set_num_threads(threads);
+  long long cnt = 0;
+  double total = 0.0;
+  const auto t0 = std::chrono::steady_clock::now();
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : cnt, total)
+  for (int e = 0; e < n_envs; ++e) {
+    std::uint64_t stream = first_stream + static_cast<std::uint64_t>(e);
+    R::EnvState st = env.reset(seed, stream);
+    for (int t = 0; t < steps; ++t) {
+      if (st.done) {
+        stream += static_cast<std::uint64_t>(n_envs);
+        st = env.reset(seed, stream);
+      }
+      const R::Action a = R::random_policy(R::RngKey{seed, static_cast<std::uint64_t>(st.step), stream});
+      R::StepResult r = env.step(st, a);
+      total += r.reward;
+      st = std::move(r.state);
+      ++cnt;
+    }
+  }
+  const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (env_steps) *env_steps = cnt;
+  if (reward_sum) *reward_sum = total;
+  return s;
 }
 
 }  // extern "C"

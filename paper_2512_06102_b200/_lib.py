@@ -117,7 +117,6 @@ SIGNATURES = {
     "ebl_batch_set_band": (_I, [_P, _I, _I]),
     "ebl_shards_step": (_I, [_P, _I, _I, _I]),
     "ebl_batch_set_profiling": (_I, [_P, _I]),
-    "ebl_batch_frontier_handovers": (_I, [_P, _P]),
     "ebl_batch_profile": (_I, [_P, _P]),
     "ebl_batch_set_pipeline": (_I, [_P, _I]),
     "ebl_batch_set_kernel": (_I, [_P, _I]),
@@ -131,6 +130,7 @@ SIGNATURES = {
     "ebl_batch_counts": (_I, [_P, _P]),
     "ebl_batch_intensity": (_I, [_P, _P, _P]),
     "ebl_batch_diag": (_I, [_P, _P, _I]),
+    "ebl_batch_tile_stats": (_I, [_P, _P, _I]),
     "ebl_batch_sync": (_I, [_P]),
     "ebl_device_rng_words": (_I, [_I, _P, _P]),
     "ebl_step_stochastic": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, C.POINTER(SimConfig), _U64,

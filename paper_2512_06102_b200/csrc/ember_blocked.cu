@@ -76,9 +76,7 @@ __global__ void __launch_bounds__(kResThreads * E, 8 / E) k_step_blocked(StepArg
   const bool use_rec = kRec && a.nfuel && a.n_pal <= 32 && g.halo_rows == 0 && g.halo_cols == 0;
 
   const int env0 = blockIdx.z * E;
-  // hand-over from the frontier kernel (E == 1): this env resumes at step t_start of the launch
-  const int t_start = a.resume ? a.resume[env0] : 0;
-  if (t_start >= g.n_steps) return;
+  constexpr int t_start = 0;
   const int W = a.w, BH = a.h;
   const int r0 = blockIdx.y * g.tile_h, c0 = blockIdx.x * g.tile_w;  // c0 % 32 == 0
   const int R0 = max(0, r0 - g.halo_rows), R1 = min(BH, r0 + g.tile_h + g.halo_rows);
@@ -554,11 +552,6 @@ BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_o
     g.halo_rows = 0;
     g.halo_cols = 0;
     g.n_steps = n_steps;
-    // pooled pairs: only when the cells fit the list tag and the batch still fills the GPU
-    // (>= 2 CTAs per SM at E = 2); envs_per_cta 1/2 forces, 0 = auto
-    const bool pair_ok = static_cast<size_t>(buf_h) * w <= 32768;
-    if (envs_per_cta == 2 && pair_ok) g.envs_per_cta = 2;
-    if (envs_per_cta == 0 && pair_ok && n_envs >= kPairMinEnvs) g.envs_per_cta = 2;
   } else {
     g.halo_rows = kBlockHalo;
     g.tile_w = w <= kBlockTileW + 64 ? ((w + 31) / 32) * 32 : kBlockTileW;
@@ -600,11 +593,9 @@ static cudaError_t launch_blocked_t(const StepArgs& a, const BlockGeom& g, size_
 
 cudaError_t launch_step_blocked(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s) {
   const int rh = g.tile_h + 2 * g.halo_rows, rw = g.tile_w + 2 * g.halo_cols;
-  const int E = g.envs_per_cta == 2 ? 2 : 1;
-  const size_t sm = blocked_smem_bytes(rh < a.h ? rh : a.h, rw < a.w ? rw : a.w, g.list_cap, E);
-  if (mode == kStaticTables)
-    return E == 2 ? launch_blocked_t<kStaticTables, 2>(a, g, sm, s) : launch_blocked_t<kStaticTables, 1>(a, g, sm, s);
-  return E == 2 ? launch_blocked_t<kStaticTerrain, 2>(a, g, sm, s) : launch_blocked_t<kStaticTerrain, 1>(a, g, sm, s);
+  const size_t sm = blocked_smem_bytes(rh < a.h ? rh : a.h, rw < a.w ? rw : a.w, g.list_cap, 1);
+  if (mode == kStaticTables) return launch_blocked_t<kStaticTables, 1>(a, g, sm, s);
+  return launch_blocked_t<kStaticTerrain, 1>(a, g, sm, s);
 }
 
 }  // namespace ebl

@@ -73,13 +73,10 @@ struct ebl_batch {
   int cur = 0;
   int kernel = EBL_KERNEL_AUTO;
   int tile_h = 0, tile_w = 0, tile_halo = 0;  // explicit blocked tiling (tests); 0 = planned
-  int envs_per_cta = 0;                         // blocked kernel env pooling: 0 auto, 1, 2 (set_kernel)
   bool counts_valid = false;
   DevBuf<int32_t> counts;
   DevBuf<unsigned long long> diag;
   DevBuf<long long> prof;           // phase profile of the blocked kernel (ebl_batch_set_profiling)
-  DevBuf<int> resume;               // frontier -> blocked hand-over step per env
-  int frontier_steps = 0;           // n_steps of the last frontier launch (0: none)
   int band_lo = -1, band_hi = -1;   // layer rows owned by this row shard (ebl_batch_set_band)
   cudaEvent_t shard_ev[2] = {nullptr, nullptr};  // completion of this shard's launch of chunk c, slot c & 1
   bool profiling = false;
@@ -175,6 +172,28 @@ Cfg6 cfg6(const ebl_sim_config& c) {
   return Cfg6{c.p_base, c.alpha_w1, c.alpha_w2, c.alpha_s, c.alpha_gamma, c.p_continue};
 }
 
+// Every entry point that works on a batch makes the batch's device current for the call and
+// restores the caller's device on return (a process may drive batches on several GPUs, and the
+// caller's own CUDA context -- e.g. torch's current device -- must not move under it).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (dev < 0 || cudaGetDevice(&prev) != cudaSuccess) {
+      prev = -1;
+      cudaGetLastError();
+      return;
+    }
+    if (prev == dev) prev = -1;
+    else if (cudaSetDevice(dev) != cudaSuccess) cudaGetLastError();
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+#define EBL_DEVICE_GUARD(b) DeviceGuard ebl_device_guard_((b) ? (b)->device : -1)
+
 int check_batch(const ebl_batch* b) {
   if (!b) return set_err(EBL_EINVAL, "null batch");
   return EBL_OK;
@@ -196,6 +215,7 @@ int rl_sync_bytes(ebl_batch* b) {
 
 // check_batch + rl_sync_bytes: the entry of every public call that touches the layers
 int check_sync(ebl_batch* b) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   return rl_sync_bytes(b);
 }
@@ -335,7 +355,6 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
   a.streams += o;
   if (a.counts) a.counts += o * 4;
   if (a.prof) a.prof += o * 10;
-  if (a.resume) a.resume += o;
   if (a.out2) a.out2 += o * b->ncell;
   if (a.tab_stride) {
     a.pot += o * a.tab_stride * 8;
@@ -355,23 +374,13 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
   return a;
 }
 
-// The frontier kernel only on request: measured on C1 (1024 x 128^2 x 200) it runs light envs
-// ~4x faster per step than the blocked kernel but the heaviest envs -- which set the batch time --
-// no faster (its apply phase's shared atomics cost what the dense pass saves), 0.94 vs 0.78 ms.
-bool use_frontier(const ebl_batch* b) {
-  return b->kernel == EBL_KERNEL_FRONTIER && b->tile_h == 0 && ebl::frontier_fits(b->h, b->w);
-}
-
 // The warp-local kernel runs every one-env-per-CTA geometry (whole env or halo tiles) under AUTO
 // (C1: 0.63 ms vs 0.77 ms for the pooled-list blocked kernel, which EBL_KERNEL_RESIDENT /
-// EBL_KERNEL_BLOCKED / EBL_KERNEL_PAIRED keep selectable).
+// EBL_KERNEL_BLOCKED keep selectable).
 bool use_warp(const ebl_batch* b) { return b->kernel == EBL_KERNEL_WARP || b->kernel == EBL_KERNEL_AUTO; }
 
 cudaError_t launch_ca(const ebl_batch* b, const ebl::StepArgs& a, const ebl::BlockGeom& g, cudaStream_t s) {
-  const bool whole = g.halo_rows == 0 && g.halo_cols == 0 && g.tile_h >= b->h && g.tile_w >= b->w;
-  if (b->kernel == EBL_KERNEL_WARP2 && whole && a.store_lo == 0 && a.store_hi == b->h && a.n_peers == 0)
-    return ebl::launch_step_warp2(a, b->mode, g.n_steps, s);
-  if ((use_warp(b) || b->kernel == EBL_KERNEL_WARP2) && g.envs_per_cta == 1) return ebl::launch_step_warp(a, b->mode, g, s);
+  if (use_warp(b)) return ebl::launch_step_warp(a, b->mode, g, s);
   return ebl::launch_step_blocked(a, b->mode, g, s);
 }
 
@@ -428,7 +437,7 @@ int ebl_batch_create(ebl_batch** out, int device, int n_envs, int height, int wi
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return set_err(EBL_ECUDA, "no CUDA device available (the engine has no CPU path)");
   if (device < 0 || device >= ndev) return set_err(EBL_EINVAL, "device ordinal out of range");
-  EBL_CUDA(cudaSetDevice(device));
+  DeviceGuard guard(device);
   auto b = std::make_unique<ebl_batch>();
   b->device = device;
   b->n_envs = n_envs;
@@ -447,8 +456,8 @@ int ebl_batch_create(ebl_batch** out, int device, int n_envs, int height, int wi
   EBL_CUDA(b->state[1].alloc(total));
   EBL_CUDA(cudaMemsetAsync(b->state[0].p, 0, total, b->stream));
   EBL_CUDA(b->counts.alloc(static_cast<size_t>(n_envs) * 4));
-  EBL_CUDA(b->diag.alloc(2));
-  EBL_CUDA(cudaMemsetAsync(b->diag.p, 0, 2 * sizeof(unsigned long long), b->stream));
+  EBL_CUDA(b->diag.alloc(4));  // fp64 fallbacks, ambiguous draws, tiles processed, tiles launched
+  EBL_CUDA(cudaMemsetAsync(b->diag.p, 0, 4 * sizeof(unsigned long long), b->stream));
   EBL_CUDA(b->streams.alloc(n_envs));
   b->h_streams.resize(n_envs);
   for (int e = 0; e < n_envs; ++e) b->h_streams[e] = static_cast<uint64_t>(e);
@@ -462,13 +471,14 @@ int ebl_batch_create(ebl_batch** out, int device, int n_envs, int height, int wi
 
 void ebl_batch_destroy(ebl_batch* b) {
   if (!b) return;
-  cudaSetDevice(b->device);
+  EBL_DEVICE_GUARD(b);
   cudaStreamSynchronize(b->stream);
   if (b->own_stream) cudaStreamDestroy(b->stream);
   delete b;
 }
 
 int ebl_batch_set_config(ebl_batch* b, const ebl_sim_config* c) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (!c) return set_err(EBL_EINVAL, "null config");
   // pot/gamma/kappa depend on every field but p_continue and max_steps
@@ -486,6 +496,7 @@ int ebl_batch_set_config(ebl_batch* b, const ebl_sim_config* c) {
 
 int ebl_batch_set_grid(ebl_batch* b, int n_grids, const double* speed, const double* dir,
                        const double* veg, const double* den, const double* slope8) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (n_grids != 1 && n_grids != b->n_envs) return set_err(EBL_EINVAL, "n_grids must be 1 or n_envs");
   if (!speed || !dir || !veg || !den || !slope8) return set_err(EBL_EINVAL, "null layer");
@@ -519,6 +530,7 @@ int ebl_batch_set_grid(ebl_batch* b, int n_grids, const double* speed, const dou
 int ebl_batch_set_terrain(ebl_batch* b, int n_grids, const uint8_t* fuel_class, const float* elevation,
                           int n_classes, const double* class_veg, const double* class_den,
                           double cellsize) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (n_grids != 1 && n_grids != b->n_envs) return set_err(EBL_EINVAL, "n_grids must be 1 or n_envs");
   if (n_classes < 1 || n_classes > 256) return set_err(EBL_EINVAL, "n_classes must be in [1, 256]");
@@ -586,6 +598,7 @@ void adopt_device_terrain(ebl_batch* b, int n_grids, std::vector<double> veg, st
 
 int ebl_batch_synth_terrain(ebl_batch* b, uint64_t seed, uint32_t env_id0, double elev_max,
                             double wind_max, double cellsize) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (!(cellsize > 0.0) || !std::isfinite(cellsize))
     return set_err(EBL_EINVAL, "raster_from_model: cellsize must be positive");
@@ -641,6 +654,7 @@ int ebl_batch_synth_terrain(ebl_batch* b, uint64_t seed, uint32_t env_id0, doubl
 }
 
 int ebl_batch_synth_ignitions(ebl_batch* b, uint64_t seed, uint32_t env_id0, int count, int* placed_total) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   if (b->mode != ebl::kStaticTerrain) return set_err(EBL_ESTATE, "ignitions need terrain-form static layers");
   if (count < 0) return set_err(EBL_EINVAL, "EnvConfig: ignition_count must be >= 0");
@@ -673,6 +687,7 @@ int ebl_batch_synth_ignitions(ebl_batch* b, uint64_t seed, uint32_t env_id0, int
 }
 
 int ebl_batch_get_terrain(ebl_batch* b, uint8_t* fuel_class, float* elevation) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (b->mode != ebl::kStaticTerrain) return set_err(EBL_ESTATE, "no terrain-form static layers on the batch");
   EBL_CUDA(cudaSetDevice(b->device));
@@ -687,6 +702,7 @@ int ebl_batch_set_landcover(ebl_batch* b, int n_grids, const int32_t* landcover,
                             int has_nodata, int32_t nodata_code, int n_codes, const int32_t* codes,
                             const double* veg, const double* den, int has_fallback, double fallback_veg,
                             double fallback_den, double cellsize) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (n_grids != 1 && n_grids != b->n_envs) return set_err(EBL_EINVAL, "n_grids must be 1 or n_envs");
   if (!landcover || !elevation) return set_err(EBL_EINVAL, "null layer");
@@ -763,6 +779,7 @@ int ebl_batch_set_landcover(ebl_batch* b, int n_grids, const int32_t* landcover,
 }
 
 int ebl_batch_set_wind(ebl_batch* b, int n_winds, const double* speed, const double* dir) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (n_winds != 1 && n_winds != b->n_envs) return set_err(EBL_EINVAL, "n_winds must be 1 or n_envs");
   for (int i = 0; i < n_winds; ++i) {
@@ -781,6 +798,7 @@ int ebl_batch_set_wind(ebl_batch* b, int n_winds, const double* speed, const dou
 
 int ebl_batch_set_wind_schedule(ebl_batch* b, int n_sched, int n_winds, const double* speed,
                                 const double* dir) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (n_sched == 0) return ebl_batch_set_wind(b, n_winds, speed, dir);  // constant wind
   if (n_sched < 0) return set_err(EBL_EINVAL, "schedule length must be >= 0");
@@ -801,6 +819,7 @@ int ebl_batch_set_wind_schedule(ebl_batch* b, int n_sched, int n_winds, const do
 }
 
 int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* speed, const double* dir) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (b->mode != ebl::kStaticTables) return set_err(EBL_ESTATE, "a per-cell wind schedule needs ebl_batch_set_grid first");
   if (n_sched < 0) return set_err(EBL_EINVAL, "schedule length must be >= 0");
@@ -818,6 +837,7 @@ int ebl_batch_set_grid_wind_schedule(ebl_batch* b, int n_sched, const double* sp
 }
 
 int ebl_step_batch_record(ebl_batch* b, int n_steps, void* traj, int on_device) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   if (n_steps < 0 || (n_steps > 0 && !traj)) return set_err(EBL_EINVAL, "bad trajectory arguments");
   if (n_steps == 0) return EBL_OK;
@@ -840,6 +860,7 @@ int ebl_step_batch_record(ebl_batch* b, int n_steps, void* traj, int on_device) 
 }
 
 int ebl_batch_set_state(ebl_batch* b, const uint8_t* states) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   // Like the reference's FireLayer (a plain Grid<FireState>, grid.hpp:100) member layers are
   // not validated; a byte other than 1/2 takes the Unburned path as in engine.cpp:15-25.
@@ -852,6 +873,7 @@ int ebl_batch_set_state(ebl_batch* b, const uint8_t* states) {
 }
 
 int ebl_batch_get_state(ebl_batch* b, uint8_t* states) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   EBL_CUDA(cudaSetDevice(b->device));
   EBL_CUDA(cudaMemcpyAsync(states, b->state[b->cur].p, b->ncell * b->n_envs, cudaMemcpyDeviceToHost, b->stream));
@@ -860,6 +882,7 @@ int ebl_batch_get_state(ebl_batch* b, uint8_t* states) {
 }
 
 int ebl_batch_set_state_device(ebl_batch* b, const void* d) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   EBL_CUDA(cudaMemcpyAsync(b->state[b->cur].p, d, b->ncell * b->n_envs, cudaMemcpyDeviceToDevice, b->stream));
   b->counts_valid = false;
@@ -867,6 +890,7 @@ int ebl_batch_set_state_device(ebl_batch* b, const void* d) {
 }
 
 int ebl_batch_get_state_device(ebl_batch* b, void* d) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   EBL_CUDA(cudaMemcpyAsync(d, b->state[b->cur].p, b->ncell * b->n_envs, cudaMemcpyDeviceToDevice, b->stream));
   return EBL_OK;
@@ -879,6 +903,7 @@ void* ebl_batch_state_device_ptr(ebl_batch* b) {
 
 int ebl_batch_set_key(ebl_batch* b, uint64_t seed, uint64_t step, const uint64_t* streams,
                       uint64_t first_stream) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   b->seed = seed;
   b->step = step;
@@ -900,22 +925,18 @@ int ebl_batch_set_key(ebl_batch* b, uint64_t seed, uint64_t step, const uint64_t
 uint64_t ebl_batch_step_index(const ebl_batch* b) { return b ? b->step : 0; }
 
 int ebl_batch_set_kernel(ebl_batch* b, int which) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
-  if (which < EBL_KERNEL_AUTO || which > EBL_KERNEL_WARP2) return set_err(EBL_EINVAL, "unknown kernel");
-  if (which == EBL_KERNEL_WARP2 && (!ebl::resident_fits(b->h, b->w) || ebl::warp2_smem_bytes(b->h, b->w) > ebl::kResMaxSmem))
-    return set_err(EBL_EINVAL, "two envs per CTA need resident envs whose pair fits shared memory");
-  if (which == EBL_KERNEL_FRONTIER && !ebl::frontier_fits(b->h, b->w))
-    return set_err(EBL_EINVAL, "the frontier kernel needs a resident env with H*W <= 16384");
-  if ((which == EBL_KERNEL_RESIDENT || which == EBL_KERNEL_PAIRED) && !ebl::resident_fits(b->h, b->w))
+  if (which < EBL_KERNEL_AUTO || which > EBL_KERNEL_WARP || which == 4 || which == 5)
+    return set_err(EBL_EINVAL, "unknown kernel");
+  if (which == EBL_KERNEL_RESIDENT && !ebl::resident_fits(b->h, b->w))
     return set_err(EBL_EINVAL, "env too large for the resident kernel");
-  if (which == EBL_KERNEL_PAIRED && b->ncell > 32768)
-    return set_err(EBL_EINVAL, "paired residency needs H*W <= 32768");
   b->kernel = which;
-  b->envs_per_cta = which == EBL_KERNEL_PAIRED ? 2 : (which == EBL_KERNEL_AUTO ? 0 : 1);
   return EBL_OK;
 }
 
 int ebl_step_batch(ebl_batch* b, int n_steps) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
   if (n_steps == 0) return EBL_OK;
@@ -937,25 +958,11 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
                                  cudaMemcpyDeviceToDevice, b->stream));
       }
     }
-  } else if (use_frontier(b)) {  // frontier kernel, all steps in one launch (+ hand-over launch)
-    EBL_CUDA(b->resume.alloc(b->n_envs));
-    ebl::StepArgs a = step_args(b);
-    EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
-    a.counts = b->counts.p;
-    a.resume = b->resume.p;
-    a.traj = b->traj_out;
-    a.traj_t0 = 0;
-    EBL_CUDA(ebl::launch_step_frontier(a, b->mode, n_steps, b->stream));
-    b->frontier_steps = n_steps;
-    b->cur ^= 1;
-    b->step += n_steps;
-    b->launches += 2;
   } else {  // bit-sliced blocked kernel: whole env per CTA when it fits, else halo tiles
     const bool force_tiles = b->kernel == EBL_KERNEL_BLOCKED;
     int tf_par = 0, tf_tiles = -1;  // tile activity records: valid from the 2nd launch of this call
     for (int done = 0; done < n_steps;) {
-      ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps - done, force_tiles, 0, b->n_envs,
-                                          b->envs_per_cta);
+      ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps - done, force_tiles, 0, b->n_envs, 1);
       if (b->tile_h > 0) {  // test hook: explicit tiling
         g.envs_per_cta = 1;
         g.tile_h = b->tile_h;
@@ -977,7 +984,7 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
       {  // quiet-tile skipping (warp-local kernel, halo inside the 8 neighbour tiles, no recording)
         const int tx = (b->w + g.tile_w - 1) / g.tile_w, ty = (b->h + g.tile_h - 1) / g.tile_h;
         const bool tiled = tx * ty > 1 && g.halo_rows <= g.tile_h && g.halo_cols <= g.tile_w && !a.traj &&
-                           use_warp(b) && g.envs_per_cta == 1;
+                           use_warp(b);
         if (tiled) {
           const size_t n = static_cast<size_t>(tx) * ty * b->n_envs * 4;
           for (auto& f : b->tflags)
@@ -1003,6 +1010,7 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
 }
 
 int ebl_batch_set_pipeline(ebl_batch* b, int chunks) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (chunks < 0 || chunks > 256) return set_err(EBL_EINVAL, "pipeline chunks must be in [0, 256]");
   b->pipe_chunks = chunks;
@@ -1016,13 +1024,13 @@ int ebl_batch_set_pipeline(ebl_batch* b, int chunks) {
 // independent; the RNG is keyed by stream, not by launch).  Pinned host buffers are needed for
 // the copies to be asynchronous.
 int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* final_states) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   if (!initial || !final_states) return set_err(EBL_EINVAL, "null state buffer");
   if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
   if (int e = prepare(b)) return e;
   const bool resident = b->kernel != EBL_KERNEL_TILED && b->kernel != EBL_KERNEL_BLOCKED &&
                         b->tile_h == 0 && ebl::resident_fits(b->h, b->w);
-  const bool frontier = use_frontier(b);
   int chunks = b->pipe_chunks > 0 ? b->pipe_chunks : 4;  // C1 e2e: 4 chunks 0.84 ms, 8: 0.92, 2: 0.89
   chunks = std::min(chunks, b->n_envs);
   if (!resident || n_steps == 0 || chunks <= 1) {  // one launch per step set: plain sequence
@@ -1033,13 +1041,9 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
   }
   EBL_CUDA(cudaSetDevice(b->device));
   if (int e = ensure_pipeline(b, chunks)) return e;
-  const ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps, false, 0, b->n_envs, b->envs_per_cta);
+  const ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps, false, 0, b->n_envs, 1);
   ebl::StepArgs a = step_args(b);
   a.counts = b->counts.p;
-  if (frontier) {
-    EBL_CUDA(b->resume.alloc(b->n_envs));
-    a.resume = b->resume.p;
-  }
   // everything earlier on the batch stream (state/key uploads, statics) happens first
   EBL_CUDA(cudaEventRecord(b->pipe_ev_start, b->stream));
   EBL_CUDA(cudaStreamWaitEvent(b->pipe_in, b->pipe_ev_start, 0));
@@ -1063,10 +1067,12 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
   }
   // the final layers straight into the caller's buffer when it is mapped pinned memory: each CTA
   // writes its env as it finishes, no device -> host copy after the chunk's launch
+  // (the kernels store 16-byte vectors: an unaligned mapping falls back to the DMA copy)
   uint8_t* host_dev = nullptr;
-  if (!frontier) {
+  {
     cudaPointerAttributes pa{};
-    if (cudaPointerGetAttributes(&pa, final_states) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+    if (cudaPointerGetAttributes(&pa, final_states) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer && (reinterpret_cast<uintptr_t>(pa.devicePointer) & 15) == 0)
       host_dev = static_cast<uint8_t*>(pa.devicePointer);
     cudaGetLastError();
   }
@@ -1098,8 +1104,7 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
     // input stream
     ebl::StepArgs ca = chunk_args(b, a, off, n);
     if (c < zc_from) ca.out2 = nullptr;
-    if (frontier) EBL_CUDA(ebl::launch_step_frontier(ca, b->mode, n_steps, s));
-    else EBL_CUDA(launch_ca(b, ca, g, s));
+    EBL_CUDA(launch_ca(b, ca, g, s));
     EBL_CUDA(cudaEventRecord(b->pipe_ev_done[c], s));
   }
   EBL_CUDA(cudaStreamWaitEvent(b->pipe_out, b->pipe_ev_in[chunks - 1], 0));
@@ -1117,14 +1122,14 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
   EBL_CUDA(cudaStreamSynchronize(b->pipe_out));
   b->cur ^= 1;
   b->step += n_steps;
-  b->launches += frontier ? 2 * chunks : chunks;
-  if (frontier) b->frontier_steps = n_steps;
+  b->launches += chunks;
   b->steps_done += n_steps;
   b->counts_valid = true;
   return EBL_OK;
 }
 
 int ebl_batch_set_row_offset(ebl_batch* b, int64_t row_off) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (row_off < 0) return set_err(EBL_EINVAL, "row offset must be >= 0");
   b->row_off = row_off;
@@ -1132,6 +1137,7 @@ int ebl_batch_set_row_offset(ebl_batch* b, int64_t row_off) {
 }
 
 int ebl_batch_copy_rows(ebl_batch* dst, int dst_row, const ebl_batch* src, int src_row, int n_rows) {
+  EBL_DEVICE_GUARD(dst);
   if (int e = check_sync(dst)) return e;
   if (int e = check_sync(const_cast<ebl_batch*>(src))) return e;
   if (dst->w != src->w || dst->n_envs != src->n_envs) return set_err(EBL_EINVAL, "copy_rows: widths/env counts differ");
@@ -1164,6 +1170,7 @@ int ebl_batch_copy_rows(ebl_batch* dst, int dst_row, const ebl_batch* src, int s
 }
 
 int ebl_batch_set_band(ebl_batch* b, int row_lo, int row_hi) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (row_lo < 0 || row_hi > b->h || row_lo >= row_hi) return set_err(EBL_EINVAL, "band outside the layer");
   b->band_lo = row_lo;
@@ -1177,6 +1184,7 @@ int ebl_batch_set_band(ebl_batch* b, int row_lo, int row_hi) {
 // (stream events, no host sync) for its neighbours' previous launches before the next one.
 int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
   if (!shards || n_shards < 1) return set_err(EBL_EINVAL, "no shards");
+  EBL_DEVICE_GUARD(shards[0]);
   if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
   if (halo < 1) return set_err(EBL_EINVAL, "halo must be >= 1");
   for (int s = 0; s < n_shards; ++s) {
@@ -1184,8 +1192,14 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
     if (int e = check_sync(b)) return e;
     if (b->n_envs != 1 || b->w != shards[0]->w) return set_err(EBL_EINVAL, "shards: one env each, equal widths");
     if (b->band_lo < 0) return set_err(EBL_ESTATE, "shards: ebl_batch_set_band first");
-    if (b->kernel == EBL_KERNEL_TILED || b->kernel == EBL_KERNEL_FRONTIER)
-      return set_err(EBL_EINVAL, "shards: blocked kernel only");
+    if (b->kernel == EBL_KERNEL_TILED) return set_err(EBL_EINVAL, "shards: blocked kernel only");
+    // every side with a neighbour must hold the light cone of one chunk (k <= halo steps), or
+    // reach the landscape's edge there
+    const int k0 = n_shards > 1 ? std::min(halo, std::max(n_steps, 1)) : 0;
+    const int64_t global_h = shards[n_shards - 1]->row_off + shards[n_shards - 1]->h;
+    if ((s > 0 && b->band_lo < k0 && b->row_off > 0) ||
+        (s + 1 < n_shards && b->h - b->band_hi < k0 && b->row_off + b->h < global_h))
+      return set_err(EBL_EINVAL, "shards: a shard holds fewer halo rows than `halo` on a side with a neighbour");
     if (s > 0 && b->row_off + b->band_lo != shards[s - 1]->row_off + shards[s - 1]->band_hi)
       return set_err(EBL_EINVAL, "shards: bands must tile the landscape in order");
     if (int e = prepare(b)) return e;
@@ -1276,6 +1290,7 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
 }
 
 int ebl_batch_rows_device(ebl_batch* b, int row0, int n_rows, void* dptr, int to_batch) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   if (n_rows < 0 || row0 < 0 || row0 + n_rows > b->h) return set_err(EBL_EINVAL, "rows: range outside the layer");
   EBL_CUDA(cudaSetDevice(b->device));
@@ -1292,6 +1307,7 @@ int ebl_batch_rows_device(ebl_batch* b, int row0, int n_rows, void* dptr, int to
 }
 
 int ebl_batch_set_tiling(ebl_batch* b, int tile_h, int tile_w, int halo) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (tile_h == 0) {
     b->tile_h = 0;
@@ -1310,6 +1326,7 @@ int ebl_batch_set_tiling(ebl_batch* b, int tile_h, int tile_w, int halo) {
 }
 
 int ebl_batch_counts(ebl_batch* b, int32_t* out) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   EBL_CUDA(cudaSetDevice(b->device));
   if (!b->counts_valid) {
@@ -1327,6 +1344,7 @@ int ebl_batch_intensity(ebl_batch* b, float* lambda, float* p) {
 }
 
 int ebl_batch_intensity_form(ebl_batch* b, int record_form, float* lambda, float* p) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   if (int e = prepare(b)) return e;
   const size_t total = b->ncell * b->n_envs;
@@ -1343,6 +1361,7 @@ int ebl_batch_intensity_form(ebl_batch* b, int record_form, float* lambda, float
 }
 
 int ebl_batch_set_profiling(ebl_batch* b, int on) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   EBL_CUDA(cudaSetDevice(b->device));
   if (on && !ebl::phase_prof_built())
@@ -1356,6 +1375,7 @@ int ebl_batch_set_profiling(ebl_batch* b, int on) {
 }
 
 int ebl_batch_profile(ebl_batch* b, int64_t* out) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (!b->profiling) return set_err(EBL_ESTATE, "profiling is off (ebl_batch_set_profiling)");
   EBL_CUDA(cudaMemcpyAsync(out, b->prof.p, static_cast<size_t>(b->n_envs) * 10 * sizeof(long long),
@@ -1364,19 +1384,9 @@ int ebl_batch_profile(ebl_batch* b, int64_t* out) {
   return EBL_OK;
 }
 
-int ebl_batch_frontier_handovers(ebl_batch* b, int* count) {
-  if (int e = check_batch(b)) return e;
-  if (!count) return set_err(EBL_EINVAL, "null count");
-  *count = 0;
-  if (b->frontier_steps == 0) return EBL_OK;
-  std::vector<int> r(b->n_envs);
-  EBL_CUDA(cudaMemcpyAsync(r.data(), b->resume.p, r.size() * sizeof(int), cudaMemcpyDeviceToHost, b->stream));
-  EBL_CUDA(cudaStreamSynchronize(b->stream));
-  for (int v : r) *count += v < b->frontier_steps;
-  return EBL_OK;
-}
 
 int ebl_batch_diag(ebl_batch* b, uint64_t* out4, int reset) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   unsigned long long d[2];
   EBL_CUDA(cudaMemcpyAsync(d, b->diag.p, sizeof d, cudaMemcpyDeviceToHost, b->stream));
@@ -1393,9 +1403,23 @@ int ebl_batch_diag(ebl_batch* b, uint64_t* out4, int reset) {
   return EBL_OK;
 }
 
+int ebl_batch_tile_stats(ebl_batch* b, uint64_t* out2, int reset) {
+  EBL_DEVICE_GUARD(b);
+  if (int e = check_batch(b)) return e;
+  if (!out2) return set_err(EBL_EINVAL, "null out");
+  unsigned long long d[2];
+  EBL_CUDA(cudaMemcpyAsync(d, b->diag.p + 2, sizeof d, cudaMemcpyDeviceToHost, b->stream));
+  EBL_CUDA(cudaStreamSynchronize(b->stream));
+  out2[0] = d[0];
+  out2[1] = d[1];
+  if (reset) EBL_CUDA(cudaMemsetAsync(b->diag.p + 2, 0, sizeof d, b->stream));
+  return EBL_OK;
+}
+
 // ---- snapshots (snapshot.hpp / snapshot.cpp) --------------------------------------------------
 int ebl_batch_snapshot_text(ebl_batch* b, const void* layers_dev, int n_layers, const uint64_t* steps,
                             const int32_t* agents, char* out, size_t cap, size_t* len) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   if (!len) return set_err(EBL_EINVAL, "ebl_batch_snapshot_text: len is NULL");
   const int n = layers_dev ? n_layers : b->n_envs;
@@ -1584,7 +1608,7 @@ int ebl_device_rng_words(int n, const uint64_t* keys5, uint64_t* out) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return set_err(EBL_ECUDA, "no CUDA device available (the engine has no CPU path)");
-  EBL_CUDA(cudaSetDevice(0));
+  DeviceGuard guard(0);
   DevBuf<uint64_t> dk, dout;
   EBL_CUDA(dk.alloc(5 * static_cast<size_t>(n)));
   EBL_CUDA(dout.alloc(n));
@@ -1595,6 +1619,7 @@ int ebl_device_rng_words(int n, const uint64_t* keys5, uint64_t* out) {
 }
 
 int ebl_batch_sync(ebl_batch* b) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   EBL_CUDA(cudaStreamSynchronize(b->stream));
   return EBL_OK;
@@ -1697,6 +1722,7 @@ ebl::RlArgs rl_args(ebl_batch* b) {
 
 int ebl_rl_configure(ebl_batch* b, int variant, const ebl_env_config* c, int tanker_ignitions,
                      int tanker_max_steps, uint32_t env_id0) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   if (variant != EBL_RL_REFERENCE && variant != EBL_RL_TANKER) return set_err(EBL_EINVAL, "unknown RL variant");
   if (b->ncell > static_cast<size_t>(ebl::kRlMaxCells))
@@ -1740,6 +1766,7 @@ int ebl_rl_configure(ebl_batch* b, int variant, const ebl_env_config* c, int tan
 }
 
 int ebl_rl_reset(ebl_batch* b, uint64_t seed, const uint64_t* streams, const uint8_t* mask) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
   if (int e = prepare(b)) return e;
@@ -1798,6 +1825,7 @@ int ebl_rl_reset(ebl_batch* b, uint64_t seed, const uint64_t* streams, const uin
 }
 
 int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* done, int device_io) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
   if (int e = prepare(b)) return e;
@@ -1845,6 +1873,7 @@ int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* d
 }
 
 int ebl_rl_rollout(ebl_batch* b, int n_steps, double* reward_sum, int32_t* episodes) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (b->rl_variant != EBL_RL_TANKER) return set_err(EBL_ESTATE, "rollout needs the tanker variant");
   if (n_steps < 1) return set_err(EBL_EINVAL, "n_steps must be >= 1");
@@ -1867,6 +1896,7 @@ int ebl_rl_rollout(ebl_batch* b, int n_steps, double* reward_sum, int32_t* episo
 }
 
 int ebl_rl_observe(ebl_batch* b, double* obs) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   if (b->rl_variant != EBL_RL_REFERENCE) return set_err(EBL_ESTATE, "observe needs the reference variant");
   const int osz = ebl_env_observation_size(&b->env_cfg);
@@ -1880,6 +1910,7 @@ int ebl_rl_observe(ebl_batch* b, double* obs) {
 }
 
 int ebl_rl_get_env_states(ebl_batch* b, ebl_env_state* out) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
   std::vector<ebl::RlEnv> ev(b->n_envs);
@@ -1894,6 +1925,7 @@ int ebl_rl_get_env_states(ebl_batch* b, ebl_env_state* out) {
 }
 
 int ebl_rl_set_env_states(ebl_batch* b, const ebl_env_state* in) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
   std::vector<ebl::RlEnv> ev(b->n_envs);
@@ -1908,6 +1940,7 @@ int ebl_rl_set_env_states(ebl_batch* b, const ebl_env_state* in) {
 }
 
 int ebl_rl_get_wet(ebl_batch* b, uint8_t* wet) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   if (b->rl_variant < 0) return set_err(EBL_ESTATE, "ebl_rl_configure first");
   EBL_CUDA(cudaMemcpyAsync(wet, b->wet.p, b->ncell * b->n_envs, cudaMemcpyDeviceToHost, b->stream));
@@ -2014,6 +2047,7 @@ int det_tables(ebl_batch* b) {
 }  // namespace
 
 int ebl_det_set_state(ebl_batch* b, const double* un, const double* burn, const double* bd) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (!un || !burn || !bd) return set_err(EBL_EINVAL, "null plane");
   EBL_CUDA(cudaSetDevice(b->device));
@@ -2030,6 +2064,7 @@ int ebl_det_set_state(ebl_batch* b, const double* un, const double* burn, const 
 }
 
 int ebl_det_set_state_from_fire(ebl_batch* b) {  // state_from_fire (engine.cpp:42-52)
+  EBL_DEVICE_GUARD(b);
   if (int e = check_sync(b)) return e;
   EBL_CUDA(cudaSetDevice(b->device));
   if (int e = det_alloc(b)) return e;
@@ -2042,6 +2077,7 @@ int ebl_det_set_state_from_fire(ebl_batch* b) {  // state_from_fire (engine.cpp:
 }
 
 int ebl_det_get_state(ebl_batch* b, double* un, double* burn, double* bd) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (!b->det_ready) return set_err(EBL_ESTATE, "ebl_det_set_state first");
   const size_t bytes = b->ncell * b->n_envs * sizeof(double);
@@ -2054,6 +2090,7 @@ int ebl_det_get_state(ebl_batch* b, double* un, double* burn, double* bd) {
 }
 
 int ebl_det_forward(ebl_batch* b, int n_steps, int record) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (!b->det_ready) return set_err(EBL_ESTATE, "ebl_det_set_state first");
   if (b->mode == ebl::kStaticNone) return set_err(EBL_ESTATE, "no grid or terrain set on the batch");
@@ -2094,6 +2131,7 @@ int ebl_det_forward(ebl_batch* b, int n_steps, int record) {
 }
 
 int ebl_det_set_mask(ebl_batch* b, const double* mask) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (!mask) return set_err(EBL_EINVAL, "mask is NULL");
   EBL_CUDA(cudaSetDevice(b->device));
@@ -2107,6 +2145,7 @@ int ebl_det_set_mask(ebl_batch* b, const double* mask) {
 
 int ebl_det_loss_grad(ebl_batch* b, const double* mask, double bce_w, double mse_w, int pool,
                       double* loss, double* grad6) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (b->traj_steps < 0 || !b->det_ready)
     return set_err(EBL_ESTATE, "ebl_det_loss_grad needs a recorded ebl_det_forward");
@@ -2170,6 +2209,7 @@ int ebl_calibrate(ebl_batch* b, const double* p_un, const double* p_burn, const 
                   const double* mask, int horizon, double bce_w, double mse_w, int pool,
                   const ebl_calib_options* opt, double* loss_hist, double* theta_hist,
                   double* best_theta, double* best_loss) {
+  EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
   if (!opt || !p_un || !p_burn || !p_bd || !mask || !loss_hist || !theta_hist || !best_theta || !best_loss)
     return set_err(EBL_EINVAL, "null argument");

@@ -17,28 +17,16 @@ constexpr int kBlockTileH = 64;     // tiled blocked kernel (large grids): 64 x 
 constexpr int kBlockTileW = 256;    // 8-row / 32-column light-cone halo, 8 steps per launch
 constexpr int kBlockHalo = 8;
 
-// AUTO never pairs: measured on C1 (1024 x 128^2 x 200, scripts/ab_pair.sh) pairs ran 1.14 ms vs
-// 1.07 ms unpaired -- the heavy envs' step latency is not P2-throughput bound.  EBL_KERNEL_PAIRED
-// keeps the pooled form selectable.
-constexpr int kPairMinEnvs = 1 << 30;
 bool phase_prof_built();
 size_t blocked_smem_bytes(int region_h, int region_w, int list_cap, int envs_per_cta);
 bool resident_fits(int h, int w);
 BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_off, int n_envs,
                       int envs_per_cta);
 cudaError_t launch_step_blocked(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s);
-// frontier kernel (ember_frontier.cu): resident envs with H*W <= 16384; hands envs whose active
-// list outgrows its capacity over to the blocked kernel (a.resume: n_envs device ints)
-int frontier_cap(int h, int w);
-size_t frontier_smem_bytes(int h, int w);
-bool frontier_fits(int h, int w);
-cudaError_t launch_step_frontier(const StepArgs& a, int mode, int n_steps, cudaStream_t s);
 // warp-local resident kernel (ember_warp.cu): whole env per CTA, one barrier per step
 size_t warp_smem_bytes(int h, int w);
 bool warp_fits(int h, int w);
 cudaError_t launch_step_warp(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s);
-size_t warp2_smem_bytes(int h, int w);
-cudaError_t launch_step_warp2(const StepArgs& a, int mode, int n_steps, cudaStream_t s);
 
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s);
 cudaError_t launch_det_loss(const DetArgs& d, cudaStream_t s);

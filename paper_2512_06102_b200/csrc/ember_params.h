@@ -59,7 +59,6 @@ struct StepArgs {
   double dist64[2];
   int force64;
   long long* prof;                // [n_envs][10] phase profile (EBL_PHASE_PROF builds), or null
-  int* resume;                    // [n_envs] first step of this launch per env (frontier hand-over), or null
   uint8_t* out2;                  // [n_envs][h*w] second copy of the output (e.g. mapped pinned host memory), or null
   // row shards (ebl_shards_step): the layer rows this launch writes back, and up to two peer
   // layers (a neighbour shard's output buffer, possibly on another GPU over NVLink) that receive
@@ -79,7 +78,7 @@ struct BlockGeom {
   int n_steps;
   int row_off;
   int list_cap;      // active-list entries per CTA (all its envs)
-  int envs_per_cta;  // 1, or 2 (whole-env residency, pooled P2 list)
+  int envs_per_cta;  // 1 (the blocked kernel's env pooling was measured slower and removed)
 };
 
 // Deterministic mode + adjoint (ember_det.cu).  fp64 planes [env][cell] (the

@@ -137,8 +137,15 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
       }
     }
     __syncthreads();
-    if (s_skip) return;
+    if (s_skip) {
+      if (threadIdx.x == 0 && a.diag) atomicAdd(a.diag + 3, 1ull);
+      return;
+    }
     streak0 = (tf_in[tile_id].x >> 1) & 3;
+  }
+  if (threadIdx.x == 0 && a.diag) {  // tile statistics: processed / launched CTAs
+    atomicAdd(a.diag + 2, 1ull);
+    atomicAdd(a.diag + 3, 1ull);
   }
   // ---- load ----------------------------------------------------------------------------------
   for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
@@ -531,324 +538,6 @@ cudaError_t launch_step_warp(const StepArgs& a, int mode, const BlockGeom& g, cu
   if (whole_width && wpr == 4) return launch_wp<kStaticTerrain, 4>(a, g, sm, s);
   if (whole_width && wpr == 2) return launch_wp<kStaticTerrain, 2>(a, g, sm, s);
   return launch_wp<kStaticTerrain, 0>(a, g, sm, s);
-}
-
-}  // namespace ebl
-
-// ---- two envs per CTA --------------------------------------------------------------------------
-// k_step_warp with two whole envs per 256-thread CTA: the 2H rows of both envs are dealt to the 8
-// warps interleaved (row g = 8l + w of the stacked pair), so a heavy env's active cells spread
-// over twice the warps (fewer passes per step on its critical path) while light envs share a
-// CTA-wide barrier they would otherwise idle at anyway.  Planes of the pair are stacked (each env
-// with its own zero padding rows); plane row R starts at word R*S + (R >> 3) (lanes 8 rows apart:
-// stride 8S+1, odd).
-namespace ebl {
-namespace {
-
-constexpr int kWp2Threads = 256;
-
-template <int MODE, int DIMC>
-__global__ void __launch_bounds__(kWp2Threads, 4) k_step_warp2(StepArgs a, int n_steps) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ int32_t s_cnt[2][4];
-  __shared__ uint64_t s_prefix[2][128];
-  constexpr bool kTer = MODE == kStaticTerrain;
-  __shared__ float s_pal[kTer ? 512 : 1];
-  __shared__ float s_kw[2][8];
-  __shared__ float s_srckw[2][kTer ? 32 * 8 : 1];
-
-  const int e0 = 2 * blockIdx.x;
-  const int nsub = min(2, a.n_envs - e0);
-  const int H = DIMC ? DIMC : a.h, W = DIMC ? DIMC : a.w;
-  const int wpr = (W + 31) >> 5;
-  const int S = plane_stride(wpr);
-  auto ro = [S](int R) { return R * S + (R >> 3); };
-  const int PB = ro(2 * (H + 2)) + 1, PX = ro(2 * H) + 1;
-  uint32_t* const Bp0 = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* const Bp1 = Bp0 + PB;
-  uint32_t* const X = Bp1 + PB;
-  uint32_t* const ACT = X + PX;
-  auto RB = [H](int sub, int r) { return sub * (H + 2) + r + 1; };  // B plane row of (sub, r), r in [-1, H]
-  auto RX = [H](int sub, int r) { return sub * H + r; };
-  const size_t ncell = static_cast<size_t>(H) * W;
-  const bool vec = (W & 15) == 0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t last_mask = low_mask(W - 32 * (wpr - 1));
-
-  for (int i = threadIdx.x; i < 2 * wpr; i += blockDim.x) {  // padding rows of both envs, both buffers
-    const int sub = i / wpr, j = i - sub * wpr;
-    Bp0[ro(RB(sub, -1)) + j] = Bp1[ro(RB(sub, -1)) + j] = 0u;
-    Bp0[ro(RB(sub, H)) + j] = Bp1[ro(RB(sub, H)) + j] = 0u;
-  }
-  for (WordIter it(wpr, 2 * H * wpr); it.ok(); it.next()) {
-    const int sub = it.r >= H, r = it.r - sub * H;
-    uint32_t b = 0u, x = 0u;
-    if (sub < nsub) {
-      const uint8_t* src = a.in + (e0 + sub) * ncell + static_cast<size_t>(r) * W + 32 * it.j;
-      const int nc = min(32, W - 32 * it.j);
-      if (nc == 32 && vec) {
-        bytes_to_bits(src, b, x);
-      } else {
-        for (int k = 0; k < nc; ++k) {
-          const uint8_t v = src[k];
-          b |= static_cast<uint32_t>(v == 1) << k;
-          x |= static_cast<uint32_t>(v == 2) << k;
-        }
-      }
-    }
-    Bp0[ro(RB(sub, r)) + it.j] = b;
-    X[ro(RX(sub, r)) + it.j] = x;
-  }
-  const bool use_rec = kTer && a.nfuel && a.n_pal <= 32;
-  auto load_wind = [&](int srow) {
-    if constexpr (kTer) {
-      if (threadIdx.x < 16) {
-        const int sub = threadIdx.x >> 3, k = threadIdx.x & 7;
-        s_kw[sub][k] = __ldg(a.kw32 + static_cast<size_t>(srow) * a.kw_sched_stride +
-                             static_cast<size_t>(min(e0 + sub, a.n_envs - 1)) * a.kw_stride + k);
-      }
-      if (use_rec)
-        for (int i = threadIdx.x; i < 2 * a.n_pal * 8; i += blockDim.x) {
-          const int sub = i / (a.n_pal * 8), ck = i - sub * a.n_pal * 8;
-          s_srckw[sub][ck] = __ldg(a.pal32 + (ck >> 3)) *
-                             __ldg(a.kw32 + static_cast<size_t>(srow) * a.kw_sched_stride +
-                                   static_cast<size_t>(min(e0 + sub, a.n_envs - 1)) * a.kw_stride + (ck & 7));
-        }
-    }
-  };
-  if constexpr (kTer)
-    for (int i = threadIdx.x; i < 2 * a.n_pal; i += blockDim.x)
-      s_pal[i < a.n_pal ? i : 256 + i - a.n_pal] = __ldg(a.pal32 + (i < a.n_pal ? i : 256 + i - a.n_pal));
-  load_wind(sched_row(a, a.step));
-  if (threadIdx.x < 8) s_cnt[threadIdx.x >> 2][threadIdx.x & 3] = 0;
-  uint64_t stream[2];
-  stream[0] = a.streams[e0];
-  stream[1] = a.streams[min(e0 + 1, a.n_envs - 1)];
-  for (int i = threadIdx.x; i < 128; i += blockDim.x) {
-    const int sub = i >> 6, k = i & 63;
-    s_prefix[sub][k] = key_prefix(a.seed, stream[sub], a.step + k);
-  }
-  __syncthreads();
-
-  const DiagCounters dg{a.diag};
-  const uint64_t gbase = static_cast<uint64_t>(a.row_off) * W;
-  auto win3 = [&](const uint32_t* row, int j, int b) -> uint32_t {
-    const uint32_t wj = row[j];
-    uint32_t v = b > 0 ? wj >> (b - 1) : ((j > 0 ? row[j - 1] >> 31 : 0u) | (wj << 1));
-    if (b == 31) v = (v & 3u) | ((j + 1 < wpr ? row[j + 1] & 1u : 0u) << 2);
-    return v & 7u;
-  };
-  auto store = [&](const uint32_t* Bs, int sub, uint8_t* __restrict__ base, int* cnt3) {
-    for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
-      const uint32_t bb = Bs[ro(RB(sub, it.r)) + it.j], xx = X[ro(RX(sub, it.r)) + it.j];
-      const int nc = min(32, W - 32 * it.j);
-      if (cnt3) {
-        cnt3[0] += nc - __popc(bb) - __popc(xx);
-        cnt3[1] += __popc(bb);
-        cnt3[2] += __popc(xx);
-      }
-      uint8_t* dst = base + static_cast<size_t>(it.r) * W + 32 * it.j;
-      if (nc == 32 && vec) bits_to_bytes(bb, xx, dst);
-      else
-        for (int k = 0; k < nc; ++k) dst[k] = static_cast<uint8_t>(((bb >> k) & 1u) | (((xx >> k) & 1u) << 1));
-    }
-  };
-
-  int cur = 0;
-  int newly[2] = {0, 0};
-  for (int t = 0; t < n_steps; ++t) {
-    const uint32_t* B = cur ? Bp1 : Bp0;
-    uint32_t* Bn = cur ? Bp0 : Bp1;
-    const int srow = sched_row(a, a.step + static_cast<uint64_t>(t));
-    if (t > 0 && a.sched_len > 1) {
-      load_wind(srow);
-      __syncthreads();
-    }
-    const bool last = t == n_steps - 1;
-    for (int rb = 0; rb < 2 * H; rb += kWp2Threads) {
-      const int g = rb + 8 * lane + warp;
-      const int sub = g >= H, r = g - sub * H;
-      int cnt = 0;
-      uint32_t cum = 0xffffffffu;
-      if (g < 2 * H && sub < nsub) {
-        const uint32_t* up = B + ro(RB(sub, r + 1));
-        const uint32_t* mid = B + ro(RB(sub, r));
-        const uint32_t* dn = B + ro(RB(sub, r - 1));
-        uint32_t* bn = Bn + ro(RB(sub, r));
-        const uint32_t* xr = X + ro(RX(sub, r));
-        uint32_t* ar = ACT + ro(RX(sub, r));
-        uint32_t vl = 0u;
-        uint32_t uc = up[0], mc = mid[0], dc = dn[0];
-        uint32_t vc = uc | mc | dc;
-#pragma unroll 4
-        for (int j = 0; j < wpr; ++j) {
-          uint32_t un = 0u, mn = 0u, dnn = 0u;
-          if (j + 1 < wpr) {
-            un = up[j + 1];
-            mn = mid[j + 1];
-            dnn = dn[j + 1];
-          }
-          const uint32_t vn = un | mn | dnn;
-          const uint32_t any = ((vc << 1) | (vl >> 31)) | ((vc >> 1) | (vn << 31)) | uc | dc;
-          bn[j] = mc;
-          const uint32_t valid = j + 1 < wpr ? 0xffffffffu : last_mask;
-          const uint32_t act = ((~(mc | xr[j]) & valid) & any) | mc;
-          ar[j] = act;
-          if (j + 1 < 4) cum = (cum & ~(0xffu << (8 * (j + 1)))) | (static_cast<uint32_t>(cnt + __popc(act)) << (8 * (j + 1)));
-          cnt += __popc(act);
-          vl = vc;
-          vc = vn;
-          uc = un;
-          mc = mn;
-          dc = dnn;
-        }
-      }
-      if (!__ballot_sync(0xffffffffu, cnt > 0)) continue;
-      __syncwarp();
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int excl = incl - cnt;
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      for (int p = 0; p < total; p += 32) {
-        const int idx = p + lane;
-        int L = 0;
-#pragma unroll
-        for (int st = 16; st > 0; st >>= 1) {
-          const int cand = L + st;
-          const int v = __shfl_sync(0xffffffffu, excl, cand & 31);
-          if (cand < 32 && v <= idx) L = cand;
-        }
-        int q = idx - __shfl_sync(0xffffffffu, excl, L);
-        const uint32_t cumL = __shfl_sync(0xffffffffu, cum, L);
-        if (idx >= total) continue;
-        const int gL = rb + 8 * L + warp;
-        const int sb = gL >= H, rr = gL - sb * H;
-        const int env = e0 + sb;
-        const uint32_t* ar = ACT + ro(RX(sb, rr));
-        int jj = 0;
-        uint32_t wv;
-        if (wpr <= 4) {
-          const uint32_t qq = static_cast<uint32_t>(q);
-          jj = (qq >= ((cumL >> 8) & 0xffu)) + (qq >= ((cumL >> 16) & 0xffu)) + (qq >= (cumL >> 24));
-          q -= jj ? static_cast<int>((cumL >> (8 * jj)) & 0xffu) : 0;
-          wv = ar[jj];
-        } else {
-          wv = ar[0];
-          for (;;) {
-            const int pc = __popc(wv);
-            if (q < pc) break;
-            q -= pc;
-            wv = ar[++jj];
-          }
-        }
-        const int cc = 32 * jj + nth_set_bit(wv, q);
-        CellRec rec{};
-        if (use_rec)
-          rec = load_rec(a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
-                         a.nfuel + static_cast<size_t>(env) * a.ter_stride, a.fuel + static_cast<size_t>(env) * a.ter_stride,
-                         rr * W + cc);
-        const int j = cc >> 5, b = cc & 31;
-        const uint32_t bit = 1u << b;
-        const int wi = ro(RB(sb, rr)) + j;
-        const uint64_t m = cell_bits53(s_prefix[sb][t & 127], gbase + static_cast<uint64_t>(rr) * W + cc, 0);
-        const uint32_t midw = win3(B + ro(RB(sb, rr)), j, b);
-        if (midw & 2u) {
-          if (m >= a.pc_thr) {
-            atomicAnd(Bn + wi, ~bit);
-            atomicOr(X + ro(RX(sb, rr)) + j, bit);
-          }
-        } else {
-          const uint32_t dnw = win3(B + ro(RB(sb, rr - 1)), j, b), upw = win3(B + ro(RB(sb, rr + 1)), j, b);
-          const uint32_t nb = (midw & 1u) | (dnw << 1) | ((midw >> 2) << 4) | ((upw >> 2) << 5) |
-                              ((upw & 2u) << 5) | ((upw & 1u) << 7);
-          bool ig;
-          if (use_rec)
-            ig = ignite_terrain_rec_pre(terrain_view(a, env, srow), rec, s_srckw[sb], s_pal + 256, a.alpha_s_l2, W,
-                                        rr, cc, nb, m, dg);
-          else if constexpr (kTer)
-            ig = ignite_terrain_tab(terrain_view(a, env, srow), a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
-                                    s_pal, s_kw[sb], W, H, rr, cc, nb, m, dg);
-          else
-            ig = ignite<MODE>(a, env, rr, cc, nb, m, dg, srow);
-          if (ig) {
-            atomicOr(Bn + wi, bit);
-            newly[sb] += last;
-          }
-        }
-      }
-    }
-    if (((t & 63) == 63) && t + 1 < n_steps) {
-      for (int i = threadIdx.x; i < 128; i += blockDim.x) {
-        const int sub = i >> 6, k = i & 63;
-        s_prefix[sub][(t + 1 + k) & 127] = key_prefix(a.seed, stream[sub], a.step + static_cast<uint64_t>(t + 1 + k));
-      }
-    }
-    __syncthreads();
-    cur ^= 1;
-    if (a.traj) {
-      const uint32_t* Bs = cur ? Bp1 : Bp0;
-      for (int sub = 0; sub < nsub; ++sub)
-        store(Bs, sub, a.traj + ((a.traj_t0 + t) * a.n_envs + e0 + sub) * ncell, nullptr);
-    }
-  }
-
-  const uint32_t* Bs = cur ? Bp1 : Bp0;
-  int c3[2][3] = {{0, 0, 0}, {0, 0, 0}};
-  for (int sub = 0; sub < nsub; ++sub) {
-    store(Bs, sub, a.out + (e0 + sub) * ncell, c3[sub]);
-    if (a.out2) store(Bs, sub, a.out2 + (e0 + sub) * ncell, nullptr);
-  }
-  if (!a.counts) return;
-#pragma unroll
-  for (int sub = 0; sub < 2; ++sub) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      c3[sub][0] += __shfl_xor_sync(0xffffffffu, c3[sub][0], o);
-      c3[sub][1] += __shfl_xor_sync(0xffffffffu, c3[sub][1], o);
-      c3[sub][2] += __shfl_xor_sync(0xffffffffu, c3[sub][2], o);
-      newly[sub] += __shfl_xor_sync(0xffffffffu, newly[sub], o);
-    }
-    if (lane == 0) {
-      atomicAdd(&s_cnt[sub][0], c3[sub][0]);
-      atomicAdd(&s_cnt[sub][1], c3[sub][1]);
-      atomicAdd(&s_cnt[sub][2], c3[sub][2]);
-      atomicAdd(&s_cnt[sub][3], newly[sub]);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < 4 * nsub) {
-    const int sub = threadIdx.x >> 2, k = threadIdx.x & 3;
-    atomicAdd(a.counts + (e0 + sub) * 4 + k, s_cnt[sub][k]);
-  }
-}
-
-template <int MODE, int DIMC>
-cudaError_t launch_wp2(const StepArgs& a, int n_steps, size_t sm, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(k_step_warp2<MODE, DIMC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sm));
-  if (e != cudaSuccess) return e;
-  k_step_warp2<MODE, DIMC><<<(a.n_envs + 1) / 2, kWp2Threads, sm, s>>>(a, n_steps);
-  return cudaGetLastError();
-}
-
-}  // namespace
-
-size_t warp2_smem_bytes(int h, int w) {
-  const size_t S = plane_stride((w + 31) / 32);
-  auto ro = [S](size_t R) { return R * S + (R >> 3); };
-  return (2 * (ro(2 * (static_cast<size_t>(h) + 2)) + 1) + 2 * (ro(2 * static_cast<size_t>(h)) + 1)) * sizeof(uint32_t);
-}
-
-// Two whole envs per CTA (resident envs whose pair fits shared memory).
-cudaError_t launch_step_warp2(const StepArgs& a, int mode, int n_steps, cudaStream_t s) {
-  const size_t sm = warp2_smem_bytes(a.h, a.w);
-  if (mode == kStaticTables) return launch_wp2<kStaticTables, 0>(a, n_steps, sm, s);
-  if (a.h == 128 && a.w == 128) return launch_wp2<kStaticTerrain, 128>(a, n_steps, sm, s);
-  return launch_wp2<kStaticTerrain, 0>(a, n_steps, sm, s);
 }
 
 }  // namespace ebl

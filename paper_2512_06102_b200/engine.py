@@ -16,8 +16,7 @@ from . import _lib
 from ._lib import EnvConfig, EnvState, SimConfig, check, lib
 
 UNBURNED, BURNING, BURNED = 0, 1, 2
-KERNEL_AUTO, KERNEL_TILED, KERNEL_RESIDENT, KERNEL_BLOCKED, KERNEL_PAIRED, KERNEL_FRONTIER, KERNEL_WARP = 0, 1, 2, 3, 4, 5, 6
-KERNEL_WARP2 = 7
+KERNEL_AUTO, KERNEL_TILED, KERNEL_RESIDENT, KERNEL_BLOCKED, KERNEL_WARP = 0, 1, 2, 3, 6
 
 
 def _ptr(a: np.ndarray | None):
@@ -228,16 +227,14 @@ class Batch:
         env chunks (ebl_batch_run); pass pinned arrays for overlapped copies."""
         st = np.ascontiguousarray(np.broadcast_to(np.asarray(initial, dtype=np.uint8),
                                                   (self.n_envs, self.height, self.width)))
+        shape = (self.n_envs, self.height, self.width)
         if out is None:
-            out = np.empty((self.n_envs, self.height, self.width), dtype=np.uint8)
+            out = np.empty(shape, dtype=np.uint8)
+        elif (not isinstance(out, np.ndarray) or out.dtype != np.uint8 or out.shape != shape
+              or not out.flags.c_contiguous or not out.flags.writeable):
+            raise ValueError(f"out must be a writeable C-contiguous uint8 array of shape {shape}")
         check(lib().ebl_batch_run(self._h, _ptr(st), n_steps, _ptr(out)))
         return out
-
-    def frontier_handovers(self) -> int:
-        """Envs of the last FRONTIER run continued by the blocked kernel (list over capacity)."""
-        n = C.c_int()
-        check(lib().ebl_batch_frontier_handovers(self._h, C.byref(n)))
-        return n.value
 
     def set_pipeline(self, chunks: int) -> None:
         check(lib().ebl_batch_set_pipeline(self._h, chunks))
@@ -361,9 +358,11 @@ class Batch:
 
     def diag(self, reset: bool = False) -> dict:
         out = np.zeros(4, dtype=np.uint64)
+        t = np.zeros(2, dtype=np.uint64)
+        check(lib().ebl_batch_tile_stats(self._h, _ptr(t), int(reset)))
         check(lib().ebl_batch_diag(self._h, _ptr(out), int(reset)))
         return {"fp64_fallbacks": int(out[0]), "ambiguous": int(out[1]), "steps": int(out[2]),
-                "launches": int(out[3])}
+                "launches": int(out[3]), "tiles_processed": int(t[0]), "tiles_launched": int(t[1])}
 
 
 # ---- one-shot reference signatures ----------------------------------------------------------
@@ -470,7 +469,7 @@ class VecFireEnv:
 
     def __init__(self, n_envs: int, cfg: EnvConfig | None = None, variant: int = _lib.RL_REFERENCE,
                  terrain: Terrain | None = None, sim_cfg=None, ignitions: int = 5,
-                 max_steps: int = 256, env_id0: int = 0, device: int = 0):
+                 max_steps: int = 256, env_id0: int = 0, device: int = 0, stream=None):
         self.variant = variant
         if variant == _lib.RL_REFERENCE:
             self.cfg = cfg if cfg is not None else default_preset()
@@ -479,7 +478,7 @@ class VecFireEnv:
             assert terrain is not None
             _, h, w = terrain.fuel_class.shape
             self.cfg = cfg
-        self.batch = Batch(n_envs, h, w, device=device)
+        self.batch = Batch(n_envs, h, w, device=device, stream=stream)
         if variant == _lib.RL_TANKER:
             self.batch.set_terrain(terrain.fuel_class, terrain.elevation, terrain.class_veg,
                                    terrain.class_den, terrain.cellsize)

@@ -5,7 +5,7 @@ set -e
 name=$1; shift
 cd "$(dirname "$0")/../paper_2512_06102_b200/csrc"
 mkdir -p /tmp/ab_build_$name ../../ab
-for f in ember_kernels ember_blocked ember_frontier ember_warp ember_det ember_rl_bits ember_synth ember_capi; do
+for f in ember_kernels ember_blocked ember_warp ember_det ember_rl_bits ember_synth ember_capi; do
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC \
        -Xcompiler -ffp-contract=off --expt-relaxed-constexpr "$@" -c $f.cu -o /tmp/ab_build_$name/$f.o &
 done

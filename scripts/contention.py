@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_06102_b200 as eb  # noqa: E402
 
 N, H, W, STEPS = 1024, 128, 128, 200
-KERNEL = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # ebl kernel id (0 auto, 5 frontier, 6 warp)
+KERNEL = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # ebl kernel id (0 auto, 2 resident, 6 warp)
 t = eb.synth_terrain(0, N, H, W)
 init = eb.synth_ignitions(0, t, 5)
 

@@ -273,3 +273,20 @@ def test_ref_landcover_mapping(ref):
     assert np.array_equal(v, rv) and np.array_equal(d, rd)
     with pytest.raises(RuntimeError, match="must lie in"):
         O.grid_from_rasters(ref, el, lc, {10: (1.5, 0.0)}, fallback=(0, 0))
+
+
+@pytest.mark.parametrize("n,h,w,env0", [(8, 128, 128, 0), (3, 64, 64, 1024), (2, 130, 520, 5),
+                                        (2, 2, 2, 0), (2, 7, 300, 3), (2, 256, 256, 7000)])
+def test_synth_inputs_port_equals_product_generator(n, h, w, env0):
+    """The port's restatement of the benchmark input generator (used by bench.py's CPU arms so
+    they never load the product library) is bit-identical to ebl_synth_terrain/_ignitions."""
+    import paper_2512_06102_b200 as eb
+    a = O.SynthTerrain(0, n, h, w, env_id0=env0)
+    b = eb.synth_terrain(0, n, h, w, env_id0=env0)
+    assert np.array_equal(a.fuel_class, b.fuel_class)
+    assert np.array_equal(a.elevation.view(np.uint32), b.elevation.view(np.uint32))
+    assert np.array_equal(a.wind_speed, b.wind_speed)
+    assert np.array_equal(a.wind_direction, b.wind_direction)
+    assert np.array_equal(a.class_veg, b.class_veg) and np.array_equal(a.class_den, b.class_den)
+    for k in (1, 5, 64):
+        assert np.array_equal(a.ignitions(k), eb.synth_ignitions(0, b, k, env_id0=env0))

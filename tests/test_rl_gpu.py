@@ -206,7 +206,8 @@ def test_c2_full_size_rollout(port):
     """BASELINE C2 at full size (16384 envs of 64 x 64, device random (x, y) policy, 256-step cap,
     auto-reset): the warp-local and the pooled-list tanker kernels agree bit for bit over a 300-step
     fused rollout (layers, wet layers, episode counters, reward sums), and envs sampled across the
-    batch match the C restatement step for step."""
+    batch (every 16th: 1024 envs) match the C restatement's layers, wet layers, reward sums and
+    episode counts."""
     n, h, w, seed, steps = 16384, 64, 64, 11, 300
     t = eb.synth_terrain(seed, n, h, w)
     cfg = [0.12, 0.2, 0.4, 1.0, 1.0, 0.6]
@@ -223,10 +224,8 @@ def test_c2_full_size_rollout(port):
         assert np.array_equal(x, y)
     assert a[4] == b[4]
     assert a[3].sum() > n // 2, "most envs should finish an episode within 300 steps"
-    ids = [0, 5000, 16383]
-    sub = eb.Terrain(t.fuel_class[ids], t.elevation[ids], t.wind_speed[ids], t.wind_direction[ids],
-                     t.class_veg, t.class_den, t.cellsize)
-    want = _port_tanker(port, sub, cfg, seed, ids, steps, O.TankerCfg(5, 256, 1))
-    for i, e in enumerate(ids):
-        assert np.array_equal(a[0][e], want[i]["fire"]) and np.array_equal(a[1][e], want[i]["wet"])
-        assert a[2][e] == sum(want[i]["rewards"]) and a[3][e] == sum(want[i]["dones"])
+    # every 16th env of the batch (1024 envs, all across it) vs the C restatement, OpenMP over envs
+    ids = np.arange(0, n, 16)
+    want = O.tanker_run_envs(t, ids, cfg, seed, steps)
+    assert np.array_equal(a[0][ids], want["fire"]) and np.array_equal(a[1][ids], want["wet"])
+    assert np.array_equal(a[2][ids], want["reward"]) and np.array_equal(a[3][ids], want["episodes"])

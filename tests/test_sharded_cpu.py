@@ -73,34 +73,36 @@ def test_gloo_halo_exchange(world):
     assert res == {r: True for r in range(world)}
 
 
-def _env_worker(rank, world, port, q):
+def _env_worker(rank, world, port, scaling, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import bench
-    ids = torch.tensor(bench.env_ids(rank), dtype=torch.int64)
-    out = [torch.empty_like(ids) for _ in range(world)]
-    dist.all_gather(out, ids)
+    e0, n = bench.rank_envs("C1", rank, world, scaling)
+    out = [None] * world
+    dist.all_gather_object(out, list(range(e0, e0 + n)))
     t = torch.tensor([float(rank + 1)], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)   # bench.py's max-over-ranks timing
-    q.put((rank, torch.cat(out).tolist(), float(t.item())))
+    q.put((rank, [i for part in out for i in part], float(t.item())))
     dist.destroy_process_group()
 
 
-def test_gloo_env_sharding_weak_scaling():
-    """bench.py at N>1: rank r owns global env ids [r*1024, (r+1)*1024) (streams = ids), the
-    union over ranks is disjoint and dense, and the time is the max over ranks."""
-    world = 2
+@pytest.mark.parametrize("scaling,world", [("weak", 2), ("strong", 2), ("strong", 3)])
+def test_gloo_env_sharding(scaling, world):
+    """bench.py at N>1: weak scaling -- rank r owns global env ids [r*1024, (r+1)*1024); strong --
+    the 1024 ids split in contiguous ranges (streams = ids); the union over ranks is disjoint and
+    dense, and the time is the max over ranks."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_env_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_env_worker, args=(r, world, port, scaling, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
+    total = world * 1024 if scaling == "weak" else 1024
     for rank, ids, tmax in res:
-        assert ids == list(range(world * 1024)) and tmax == float(world)
+        assert ids == list(range(total)) and tmax == float(world)
 
 
 def _grad_worker(rank, world, port, n_envs, q):

@@ -15,7 +15,7 @@ from test_oracle_pin import landcover_restated
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [eb.KERNEL_TILED, eb.KERNEL_RESIDENT, eb.KERNEL_BLOCKED, eb.KERNEL_PAIRED]
+KERNELS = [eb.KERNEL_TILED, eb.KERNEL_RESIDENT, eb.KERNEL_BLOCKED, eb.KERNEL_WARP, eb.KERNEL_AUTO]
 WORLDCOVER = {10: (0.4, 0.3), 20: (0.25, 0.1), 30: (0.15, -0.1), 40: (0.0, -0.2), 50: (-0.8, -0.8),
               60: (-0.7, -0.6), 70: (-1.0, -1.0), 80: (-1.0, -1.0), 90: (-0.4, -0.3),
               95: (-0.2, -0.1), 100: (-0.3, -0.4)}
@@ -156,12 +156,18 @@ def test_landcover_errors():
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
-def test_dem_nodata_all_kernels_vs_port(port, kernel):
-    n, h, w, seed = 3, 96, 80, 12
+@pytest.mark.parametrize("h,w", [(96, 80), (128, 128), (64, 64), (300, 260)])
+def test_dem_nodata_all_kernels_vs_port(port, kernel, h, w):
+    """DEM nodata (NaN elevation: slope 0 toward/from the cell, geodata.cpp:214,220) on every
+    kernel, including the production AUTO/WARP path with its pot32t rows at the compile-time
+    128x128 / 64x64 shapes and the halo-tiled geometry (300x260 > 65536 cells)."""
+    if kernel == eb.KERNEL_RESIDENT and h * w > 65536:
+        pytest.skip("resident kernel needs a whole env in shared memory")
+    n, seed = 3, 12
     t = eb.synth_terrain(seed, n, h, w)
     rs = np.random.default_rng(1)
     t.elevation[rs.random(t.elevation.shape) < 0.05] = np.nan
-    t.elevation[:, 40:44, :] = np.nan  # a nodata band across the fire path
+    t.elevation[:, h // 2 - 2:h // 2 + 2, :] = np.nan  # a nodata band across the fire path
     init = eb.synth_ignitions(seed, t, 6)
     b = eb.Batch(n, h, w)
     b.set_terrain(t.fuel_class, t.elevation, t.class_veg, t.class_den, 30.0)
