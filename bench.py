@@ -173,7 +173,7 @@ class ClockSampler:
 # has no such path).  Inputs come from the oracle's restatement of the input generator, pinned
 # bit-for-bit to the product's (tests/test_oracle_pin.py): the product library is never loaded.
 # ================================================================================================
-def _cpu_c1(n_envs, h=128, w=128, steps=200, threads=0):
+def _cpu_c1(n_envs, h=128, w=128, steps=200, threads=0, return_states=False):
     from oracle import oracle as O
     R = O.ref()
     kind = "reference" if R is not None else "port"
@@ -191,7 +191,8 @@ def _cpu_c1(n_envs, h=128, w=128, steps=200, threads=0):
     cores = (R.ref_max_threads() if R is not None else os.cpu_count()) if threads <= 0 else threads
     return dict(seconds=secs, units=n_envs * h * w * steps, kind=kind, cores=cores,
                 sample=f"{n_envs} of the C1 envs x {steps} steps: run_stochastic(Exec::serial) per env "
-                       f"(tables built inside, as the reference does), OpenMP over envs")
+                       f"(tables built inside, as the reference does), OpenMP over envs",
+                states=states if return_states else None)
 
 
 def _cpu_c0(reps):
@@ -605,8 +606,12 @@ def bench_c2(cx: Ctx, clk):
     ddone = torch.empty(n, dtype=torch.uint8, device=cx.dev)
 
     def dev_step(kev):
+        if kev:
+            kev[0].record(cx.stream)
         for k in range(steps):
             eb._lib.check(L.ebl_rl_step(hnd, dact[k].data_ptr(), drew.data_ptr(), ddone.data_ptr(), 1))
+        if kev:
+            kev[1].record(cx.stream)
     dms, _ = cx.timed(dev_step, max(2, a.steps // 2), 1)
     clk.__exit__(None, None, None)
     te = cx.max_over_ranks(sum(e2e_ms) / 1e3)

@@ -363,6 +363,11 @@ int ebl_rl_observe(ebl_batch* b, double* obs);
 int ebl_rl_get_env_states(ebl_batch* b, ebl_env_state* out);
 int ebl_rl_set_env_states(ebl_batch* b, const ebl_env_state* in);
 int ebl_rl_get_wet(ebl_batch* b, uint8_t* wet);
+/* TANKER observation for a learner on the device: [n_envs][H][W] bytes into out_dev (device
+ * memory), FireState in bits 0-1, wet flag in bit 2; asynchronous on the batch stream, reads the
+ * bit-resident state without invalidating it.  With ebl_rl_step(device_io = 1) the whole
+ * act -> step -> observe loop stays on the device (no host round trip). */
+int ebl_rl_observe_device(ebl_batch* b, void* out_dev);
 
 /* ---- input preparation (BASELINE configs; not part of the reference API) ---- */
 /* Synthetic per-env terrain for C1-C4: landcover class from

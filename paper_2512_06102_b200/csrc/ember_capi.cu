@@ -104,6 +104,11 @@ struct ebl_batch {
   DevBuf<uint2> nfuel;              // [grid][cell] fuel classes of the 8 sources (built with slope32)
   DevBuf<float> pot32t;             // [env or 1][cell][8] fp32 lambda terms (built by prepare)
   DevBuf<int32_t> tflags[2];           // per-tile activity records of halo-tiled runs (ping-pong)
+  // records of the last launch kept across ebl_step_batch calls: tiles count (-1: none), which
+  // buffer holds them, and the tile geometry they describe.  Any entry point other than stepping,
+  // reads, and halo-row writes outside the band drops them (check_batch / check_sync).
+  mutable int tf_carry_tiles = -1;
+  int tf_carry_par = 0, tf_carry_th = 0, tf_carry_tw = 0;
   DevBuf<char> snap_text, snap_meta;  // snapshot rendering staging (grow-only)
   DevBuf<unsigned long long> snap_off;
   bool pot32t_valid = false;
@@ -194,8 +199,9 @@ struct DeviceGuard {
 };
 #define EBL_DEVICE_GUARD(b) DeviceGuard ebl_device_guard_((b) ? (b)->device : -1)
 
-int check_batch(const ebl_batch* b) {
+int check_batch(const ebl_batch* b, bool keep_records = false) {
   if (!b) return set_err(EBL_EINVAL, "null batch");
+  if (!keep_records) b->tf_carry_tiles = -1;
   return EBL_OK;
 }
 
@@ -214,9 +220,8 @@ int rl_sync_bytes(ebl_batch* b) {
 }
 
 // check_batch + rl_sync_bytes: the entry of every public call that touches the layers
-int check_sync(ebl_batch* b) {
-  EBL_DEVICE_GUARD(b);
-  if (int e = check_batch(b)) return e;
+int check_sync(ebl_batch* b, bool keep_records = false) {
+  if (int e = check_batch(b, keep_records)) return e;
   return rl_sync_bytes(b);
 }
 
@@ -342,6 +347,8 @@ ebl::StepArgs step_args(const ebl_batch* b) {
   a.prof = b->profiling ? b->prof.p : nullptr;
   a.store_lo = 0;
   a.store_hi = b->h;
+  a.keep_lo = b->band_lo >= 0 ? b->band_lo : 0;
+  a.keep_hi = b->band_lo >= 0 ? b->band_hi : b->h;
   a.n_peers = 0;
   return a;
 }
@@ -874,7 +881,7 @@ int ebl_batch_set_state(ebl_batch* b, const uint8_t* states) {
 
 int ebl_batch_get_state(ebl_batch* b, uint8_t* states) {
   EBL_DEVICE_GUARD(b);
-  if (int e = check_sync(b)) return e;
+  if (int e = check_sync(b, true)) return e;
   EBL_CUDA(cudaSetDevice(b->device));
   EBL_CUDA(cudaMemcpyAsync(states, b->state[b->cur].p, b->ncell * b->n_envs, cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
@@ -937,7 +944,7 @@ int ebl_batch_set_kernel(ebl_batch* b, int which) {
 
 int ebl_step_batch(ebl_batch* b, int n_steps) {
   EBL_DEVICE_GUARD(b);
-  if (int e = check_sync(b)) return e;
+  if (int e = check_sync(b, true)) return e;
   if (n_steps < 0) return set_err(EBL_EINVAL, "n_steps must be >= 0");
   if (n_steps == 0) return EBL_OK;
   if (int e = prepare(b)) return e;
@@ -960,7 +967,10 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
     }
   } else {  // bit-sliced blocked kernel: whole env per CTA when it fits, else halo tiles
     const bool force_tiles = b->kernel == EBL_KERNEL_BLOCKED;
-    int tf_par = 0, tf_tiles = -1;  // tile activity records: valid from the 2nd launch of this call
+    // tile activity records: valid from the 2nd launch of this call, or carried over from the
+    // previous call when nothing but stepping / reads / halo-row writes happened in between
+    int tf_par = b->tf_carry_par, tf_tiles = b->tf_carry_tiles;
+    b->tf_carry_tiles = -1;
     for (int done = 0; done < n_steps;) {
       ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps - done, force_tiles, 0, b->n_envs, 1);
       if (b->tile_h > 0) {  // test hook: explicit tiling
@@ -983,16 +993,23 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
       a.traj_t0 = static_cast<size_t>(done);
       {  // quiet-tile skipping (warp-local kernel, halo inside the 8 neighbour tiles, no recording)
         const int tx = (b->w + g.tile_w - 1) / g.tile_w, ty = (b->h + g.tile_h - 1) / g.tile_h;
+        const bool exposed = a.keep_lo > 0 || a.keep_hi < b->h;  // halo rows of a row shard
         const bool tiled = tx * ty > 1 && g.halo_rows <= g.tile_h && g.halo_cols <= g.tile_w && !a.traj &&
-                           use_warp(b);
+                           use_warp(b) && (!exposed || g.tile_h >= 3 * g.halo_rows);
         if (tiled) {
           const size_t n = static_cast<size_t>(tx) * ty * b->n_envs * 4;
           for (auto& f : b->tflags)
-            if (f.n < n) EBL_CUDA(f.alloc(n));
-          a.tflag_in = tf_tiles == tx * ty ? b->tflags[tf_par].p : nullptr;
+            if (f.n < n) {
+              EBL_CUDA(f.alloc(n));
+              tf_tiles = -1;
+            }
+          const bool same = tf_tiles == tx * ty && b->tf_carry_th == g.tile_h && b->tf_carry_tw == g.tile_w;
+          a.tflag_in = same ? b->tflags[tf_par].p : nullptr;
           a.tflag_out = b->tflags[tf_par ^ 1].p;
           tf_par ^= 1;
           tf_tiles = tx * ty;
+          b->tf_carry_th = g.tile_h;
+          b->tf_carry_tw = g.tile_w;
         } else {
           tf_tiles = -1;
         }
@@ -1003,6 +1020,8 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
       b->launches += 1;
       done += g.n_steps;
     }
+    b->tf_carry_tiles = tf_tiles;
+    b->tf_carry_par = tf_par;
   }
   b->steps_done += n_steps;
   b->counts_valid = true;
@@ -1138,8 +1157,10 @@ int ebl_batch_set_row_offset(ebl_batch* b, int64_t row_off) {
 
 int ebl_batch_copy_rows(ebl_batch* dst, int dst_row, const ebl_batch* src, int src_row, int n_rows) {
   EBL_DEVICE_GUARD(dst);
-  if (int e = check_sync(dst)) return e;
-  if (int e = check_sync(const_cast<ebl_batch*>(src))) return e;
+  // the source is only read; halo-row writes outside the destination's band keep its records
+  const bool halo_only = dst && dst->band_lo >= 0 && (dst_row + n_rows <= dst->band_lo || dst_row >= dst->band_hi);
+  if (int e = check_sync(dst, halo_only)) return e;
+  if (int e = check_sync(const_cast<ebl_batch*>(src), true)) return e;
   if (dst->w != src->w || dst->n_envs != src->n_envs) return set_err(EBL_EINVAL, "copy_rows: widths/env counts differ");
   if (n_rows < 0 || dst_row < 0 || src_row < 0 || dst_row + n_rows > dst->h || src_row + n_rows > src->h)
     return set_err(EBL_EINVAL, "copy_rows: row range outside a layer");
@@ -1218,6 +1239,9 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
   }
   std::vector<uint8_t*> outs(n_shards);
   std::vector<ebl::BlockGeom> geo(n_shards);
+  // quiet-tile records per shard across the chunks of this call (tiles holding halo rows the
+  // neighbours store into are never skipped: ember_warp.cu)
+  std::vector<int> tf_par(n_shards, 0), tf_tiles(n_shards, -1);
   int chunk = 0;
   for (int done = 0; done < n_steps; ++chunk) {
     int k = n_shards > 1 ? std::min(halo, n_steps - done) : n_steps - done;
@@ -1254,6 +1278,26 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
       a.counts = b->counts.p;
       a.store_lo = b->band_lo;
       a.store_hi = b->band_hi;
+      {
+        const int tx = (b->w + g.tile_w - 1) / g.tile_w, ty = (b->h + g.tile_h - 1) / g.tile_h;
+        const bool exposed = a.keep_lo > 0 || a.keep_hi < b->h;
+        const bool tiled = tx * ty > 1 && g.halo_rows <= g.tile_h && g.halo_cols <= g.tile_w && use_warp(b) &&
+                           k <= std::max(1, g.halo_rows) && (!exposed || g.tile_h >= 3 * g.halo_rows);
+        if (tiled) {
+          const size_t n = static_cast<size_t>(tx) * ty * b->n_envs * 4;
+          for (auto& f : b->tflags)
+            if (f.n < n) {
+              EBL_CUDA(f.alloc(n));
+              tf_tiles[s] = -1;
+            }
+          a.tflag_in = tf_tiles[s] == tx * ty ? b->tflags[tf_par[s]].p : nullptr;
+          a.tflag_out = b->tflags[tf_par[s] ^ 1].p;
+          tf_par[s] ^= 1;
+          tf_tiles[s] = tx * ty;
+        } else {
+          tf_tiles[s] = -1;
+        }
+      }
       const int64_t g0 = b->row_off + b->band_lo, g1 = b->row_off + b->band_hi;
       for (int q = s - 1; q <= s + 1; q += 2) {
         if (q < 0 || q >= n_shards) continue;
@@ -1291,7 +1335,9 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
 
 int ebl_batch_rows_device(ebl_batch* b, int row0, int n_rows, void* dptr, int to_batch) {
   EBL_DEVICE_GUARD(b);
-  if (int e = check_sync(b)) return e;
+  // reads, and writes of halo rows outside the shard's band, keep the tile activity records
+  const bool halo_only = b && b->band_lo >= 0 && (row0 + n_rows <= b->band_lo || row0 >= b->band_hi);
+  if (int e = check_sync(b, !to_batch || halo_only)) return e;
   if (n_rows < 0 || row0 < 0 || row0 + n_rows > b->h) return set_err(EBL_EINVAL, "rows: range outside the layer");
   EBL_CUDA(cudaSetDevice(b->device));
   const size_t bytes = static_cast<size_t>(n_rows) * b->w;
@@ -1327,7 +1373,7 @@ int ebl_batch_set_tiling(ebl_batch* b, int tile_h, int tile_w, int halo) {
 
 int ebl_batch_counts(ebl_batch* b, int32_t* out) {
   EBL_DEVICE_GUARD(b);
-  if (int e = check_sync(b)) return e;
+  if (int e = check_sync(b, true)) return e;
   EBL_CUDA(cudaSetDevice(b->device));
   if (!b->counts_valid) {
     EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
@@ -1387,7 +1433,7 @@ int ebl_batch_profile(ebl_batch* b, int64_t* out) {
 
 int ebl_batch_diag(ebl_batch* b, uint64_t* out4, int reset) {
   EBL_DEVICE_GUARD(b);
-  if (int e = check_batch(b)) return e;
+  if (int e = check_batch(b, true)) return e;
   unsigned long long d[2];
   EBL_CUDA(cudaMemcpyAsync(d, b->diag.p, sizeof d, cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
@@ -1405,7 +1451,7 @@ int ebl_batch_diag(ebl_batch* b, uint64_t* out4, int reset) {
 
 int ebl_batch_tile_stats(ebl_batch* b, uint64_t* out2, int reset) {
   EBL_DEVICE_GUARD(b);
-  if (int e = check_batch(b)) return e;
+  if (int e = check_batch(b, true)) return e;
   if (!out2) return set_err(EBL_EINVAL, "null out");
   unsigned long long d[2];
   EBL_CUDA(cudaMemcpyAsync(d, b->diag.p + 2, sizeof d, cudaMemcpyDeviceToHost, b->stream));
@@ -1620,7 +1666,7 @@ int ebl_device_rng_words(int n, const uint64_t* keys5, uint64_t* out) {
 
 int ebl_batch_sync(ebl_batch* b) {
   EBL_DEVICE_GUARD(b);
-  if (int e = check_batch(b)) return e;
+  if (int e = check_batch(b, true)) return e;
   EBL_CUDA(cudaStreamSynchronize(b->stream));
   return EBL_OK;
 }
@@ -1936,6 +1982,17 @@ int ebl_rl_set_env_states(ebl_batch* b, const ebl_env_state* in) {
   }
   EBL_CUDA(cudaMemcpyAsync(b->rl_env.p, ev.data(), ev.size() * sizeof(ebl::RlEnv), cudaMemcpyHostToDevice, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_rl_observe_device(ebl_batch* b, void* out_dev) {
+  EBL_DEVICE_GUARD(b);
+  if (int e = check_batch(b, true)) return e;  // read-only: the bit-resident state stays valid
+  if (b->rl_variant != EBL_RL_TANKER) return set_err(EBL_ESTATE, "observe_device needs the tanker variant");
+  if (!out_dev) return set_err(EBL_EINVAL, "null out");
+  EBL_CUDA(ebl::launch_rl_observe_planes(b->rl_bits_truth ? b->rl_bits.p : nullptr, b->state[b->cur].p, b->wet.p,
+                                         static_cast<uint8_t*>(out_dev), b->n_envs, b->h, b->w, b->stream));
+  b->launches += 1;
   return EBL_OK;
 }
 

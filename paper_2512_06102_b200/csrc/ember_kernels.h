@@ -49,6 +49,8 @@ bool rl_bits_fits(int h, int w);
 cudaError_t launch_rl_tanker_bits(const RlArgs& g, int mode, cudaStream_t s);
 size_t rl_warp_smem_bytes(int h, int w);
 cudaError_t launch_rl_tanker_warp(const RlArgs& g, int mode, cudaStream_t s);
+cudaError_t launch_rl_observe_planes(const uint32_t* bits, const uint8_t* state, const uint8_t* wet, uint8_t* out,
+                                     int n_envs, int h, int w, cudaStream_t s);
 cudaError_t launch_rl_bits_to_bytes(const uint32_t* bits, uint8_t* state, uint8_t* wet, int n_envs, int h, int w,
                                     cudaStream_t s);
 cudaError_t launch_rl_tanker_reset(const RlArgs& g, int mode, const uint8_t* mask, cudaStream_t s);

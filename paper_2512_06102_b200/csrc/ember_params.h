@@ -21,12 +21,13 @@ struct StepArgs {
   const uint8_t* in;              // [n_envs][h*w]
   uint8_t* out;
   int32_t* counts;                // [n_envs][4] U,B,X,newly (nullable)
-  // halo-tiled launches of one ebl_step_batch call: per-tile activity records [env][tile]
-  // {bit0 burning in the output tile, bits 1-2 quiet streak (saturating at 2), U, B, X}; read
-  // from the previous launch (null: first launch), written for the next
+  // halo-tiled launches: per-tile activity records [env][tile] {bit0 burning in the output tile,
+  // bits 1-2 quiet streak (saturating at 2), U, B, X}; read from the previous launch (null: no
+  // valid records), written for the next.  Tiles whose output rows reach outside
+  // [keep_lo, keep_hi) (row shards: halo rows a neighbour writes) are never skipped outright.
   const int32_t* tflag_in;        // int4 records
   int32_t* tflag_out;
-  unsigned long long* diag;       // [2]
+  unsigned long long* diag;       // [4] fp64 fallbacks, ambiguous draws, tiles processed, launched
   // general form (SpreadTables)
   const double* pot;              // [grid][h*w*8]
   const double* gamma;            // [grid][h*w]
@@ -65,6 +66,7 @@ struct StepArgs {
   // rows [peer_lo, peer_hi) of this layer at their row peer_dst -- the halo exchange fused into
   // the producing kernel's store
   int store_lo, store_hi;
+  int keep_lo, keep_hi;           // rows outside: halo rows written by neighbour shards (exposed tiles)
   int n_peers;
   uint8_t* peer_out[2];
   int peer_lo[2], peer_hi[2], peer_dst[2];

@@ -675,6 +675,39 @@ __global__ void k_rl_bits_to_bytes(const uint32_t* __restrict__ bits, uint8_t* s
   }
 }
 
+// Tanker observation on the device: one byte per cell, FireState in bits 0-1 and the wet flag in
+// bit 2, [n_envs][H][W] into a caller buffer (e.g. a learner's torch tensor).  Reads the bit-resident
+// planes (bits != null) without invalidating them, else the byte layers.
+__global__ void k_rl_observe_planes(const uint32_t* __restrict__ bits, const uint8_t* __restrict__ state,
+                                    const uint8_t* __restrict__ wet, uint8_t* out, int n_envs, int H, int W) {
+  const int wpr = (W + 31) >> 5;
+  const size_t plane = static_cast<size_t>(H) * wpr;
+  const size_t total = plane * n_envs;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t env = i / plane, k = i - env * plane;
+    const int r = static_cast<int>(k / wpr), j = static_cast<int>(k - static_cast<size_t>(r) * wpr);
+    const size_t off = env * H * W + static_cast<size_t>(r) * W + 32 * j;
+    const int nc = min(32, W - 32 * j);
+    if (bits) {
+      const uint32_t* eb = bits + env * 3 * plane;
+      const uint32_t b = eb[k], x = eb[plane + k], wb = eb[2 * plane + k];
+      for (int c = 0; c < nc; ++c)
+        out[off + c] = static_cast<uint8_t>(((b >> c) & 1u) | (((x >> c) & 1u) << 1) | (((wb >> c) & 1u) << 2));
+    } else {
+      for (int c = 0; c < nc; ++c) out[off + c] = static_cast<uint8_t>(state[off + c] | (wet[off + c] << 2));
+    }
+  }
+}
+
+cudaError_t launch_rl_observe_planes(const uint32_t* bits, const uint8_t* state, const uint8_t* wet, uint8_t* out,
+                                     int n_envs, int h, int w, cudaStream_t s) {
+  const size_t total = static_cast<size_t>(n_envs) * h * ((w + 31) / 32);
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 16));
+  k_rl_observe_planes<<<blocks, 256, 0, s>>>(bits, state, wet, out, n_envs, h, w);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rl_bits_to_bytes(const uint32_t* bits, uint8_t* state, uint8_t* wet, int n_envs, int h, int w,
                                     cudaStream_t s) {
   const size_t total = static_cast<size_t>(n_envs) * h * ((w + 31) / 32);

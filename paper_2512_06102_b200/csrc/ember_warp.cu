@@ -37,6 +37,12 @@
 #ifndef EBL_WARP_UNROLL2  // step loop unrolled by two (B / Bn roles alternate)
 #define EBL_WARP_UNROLL2 1  // C1 kernel 0.524 -> 0.509 ms (a few spilled bytes)
 #endif
+#ifndef EBL_WARP_MICRO  // newly-ignited counts from the planes at the store (not per ignition),
+#define EBL_WARP_MICRO 0  // schedule / record branches hoisted out of the step loop
+#endif
+#ifndef EBL_WARP_PFIGN  // at an ignition, prefetch the pot32t rows of the 8 neighbours (the next
+#define EBL_WARP_PFIGN 0  // step's new candidates): 1 into L1, 2 into L2
+#endif
 #ifndef EBL_WARP_POT  // lambda terms from the pot32t table (0: slope + source-class records)
 #define EBL_WARP_POT 1
 #endif
@@ -127,7 +133,11 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
           if (ty >= 0 && ty < static_cast<int>(gridDim.y) && tx >= 0 && tx < static_cast<int>(gridDim.x))
             quiet &= !(tf_in[(static_cast<size_t>(env) * gridDim.y + ty) * gridDim.x + tx].x & 1);
         }
-      s_skip = quiet && ((me.x >> 1) & 3) >= 2;
+      // tiles holding halo rows a neighbour shard writes are never skipped outright (their
+      // records do not see those writes); DESIGN.md §6 gives the distance argument that keeps
+      // the other tiles' skip decisions exact
+      const bool exposed = r0 < a.keep_lo || r0 + g.tile_h > a.keep_hi;
+      s_skip = quiet && ((me.x >> 1) & 3) >= 2 && !exposed;
       if (s_skip) {
         tf_out[tile_id] = me;
         if (a.counts) {
@@ -210,7 +220,7 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
   // output tile -> uint8 layer at `layer` (+ U/B/X counts when cnt3); layer rows outside
   // [row_lo, row_hi) skipped, rows shifted by dst_shift (peer layers)
   auto store_tile = [&](const uint32_t* Bs, uint8_t* __restrict__ layer, int* cnt3, int row_lo, int row_hi,
-                        int dst_shift) {
+                        int dst_shift, const uint32_t* Bprev = nullptr, int* newly_out = nullptr) {
     for (WordIter it(twords, (tr1 - tr0) * twords); it.ok(); it.next()) {
       const int rr = tr0 + it.r, j = tj0 + it.j;
       const int lrow = R0 + rr;
@@ -221,6 +231,8 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
         cnt3[0] += nc - __popc(bb) - __popc(xx);
         cnt3[1] += __popc(bb);
         cnt3[2] += __popc(xx);
+        // ignited in the last step: burning now, not burning before it (Burning never re-ignites)
+        if (Bprev) *newly_out += __popc(bb & ~Bprev[ro(rr + 1) + j]);
       }
       uint8_t* dst = layer + static_cast<size_t>(lrow + dst_shift) * W + C0 + 32 * j;
       if (nc == 32 && vec) bits_to_bytes(bb, xx, dst);
@@ -231,11 +243,12 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
 
   int cur = 0;
   int newly = 0;
+  const bool has_sched = a.sched_len > 1, rec_traj = a.traj != nullptr;
 #if EBL_PHASE_PROF
   // per warp (lane 0): dense-pass cycles, decide-pass cycles, passes, cells; CTA: step cycles
   long long pw_dense = 0, pw_dec = 0, pw_pass = 0, pw_cells = 0, pw_t0 = 0, p_step = 0, p_wait = 0;
-  long long pw_loc = 0, pw_body = 0, pw_ts = 0;
-  __shared__ long long s_wd[4][6];
+  long long pw_loc = 0, pw_body = 0, pw_ts = 0, pw_lat = 0;
+  __shared__ long long s_wd[4][7];
 #endif
 #if EBL_WARP_UNROLL2
 #pragma unroll 2
@@ -247,13 +260,24 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
 #endif
     const uint32_t* B = cur ? Bp1 : Bp0;
     uint32_t* Bn = cur ? Bp0 : Bp1;
+#if EBL_WARP_MICRO
+    int srow = 0;
+    if (has_sched) {  // CTA-uniform: time-varying wind
+      srow = sched_row(a, a.step + static_cast<uint64_t>(t));
+      if (t > 0) {
+        load_wind(srow);
+        __syncthreads();
+      }
+    }
+#else
     const int srow = a.sched_len > 1 ? sched_row(a, a.step + static_cast<uint64_t>(t)) : 0;
     if (t > 0 && a.sched_len > 1) {  // CTA-uniform: time-varying wind
       load_wind(srow);
       __syncthreads();
     }
+#endif
     const uint64_t prefix = s_prefix[t & 127];
-    const bool last = t == n_steps - 1;
+    [[maybe_unused]] const bool last = t == n_steps - 1;
     for (int rb = 0; rb < H; rb += kWpThreads) {
       // ---- dense pass over the lane's row ------------------------------------------------------
       const int r = rb + 4 * lane + warp;
@@ -370,6 +394,13 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
                              2 * (gr * W + gc);
           rec.s0 = __ldg(tp);
           rec.s1 = __ldg(tp + 1);
+#if EBL_PHASE_PROF
+          if (lane == 0) {  // issue -> data ready of lane 0's record (the asm waits on the registers)
+            long long c1;
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(c1) : "f"(rec.s0.x), "f"(rec.s1.w));
+            pw_lat += c1 - pw_ts;
+          }
+#endif
         } else if (use_rec) {
           rec = load_rec(a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8,
                          a.nfuel + static_cast<size_t>(env) * a.ter_stride, a.fuel + static_cast<size_t>(env) * a.ter_stride,
@@ -406,7 +437,29 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
 #endif
           if (ig) {
             atomicOr(Bn + wi, bit);
+#if !EBL_WARP_MICRO
             newly += last && rr >= tr0 && rr < tr1 && cc >= tc0 && cc < tc1;  // counted in the tile only
+#endif
+#if EBL_WARP_PFIGN
+            if (use_tab) {  // the next step's new candidates: rows gr-1..gr+1, columns gc-1..gc+1
+              const float* base = a.pot32t + static_cast<size_t>(env) * a.pot32t_stride;
+              const int c_lo = gc > 0 ? gc - 1 : 0, c_hi = gc + 1 < W ? gc + 1 : W - 1;
+#pragma unroll
+              for (int dr = -1; dr <= 1; ++dr) {
+                const int row = gr + dr;
+                if (row < 0 || row >= BH) continue;
+                const float* p0 = base + (static_cast<size_t>(row) * W + c_lo) * 8;
+                const float* p1 = base + (static_cast<size_t>(row) * W + c_hi) * 8 + 7;
+                if (EBL_WARP_PFIGN == 1) {
+                  asm volatile("prefetch.global.L1 [%0];" ::"l"(p0));
+                  asm volatile("prefetch.global.L1 [%0];" ::"l"(p1));
+                } else {
+                  asm volatile("prefetch.global.L2 [%0];" ::"l"(p0));
+                  asm volatile("prefetch.global.L2 [%0];" ::"l"(p1));
+                }
+              }
+            }
+#endif
           }
         }
       }
@@ -429,7 +482,7 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
     if (threadIdx.x == 0) p_step += clock64() - st0;
 #endif
     cur ^= 1;
-    if (a.traj) {  // record (run_stochastic(record=true), engine.cpp:116): the tile after this step
+    if (rec_traj) {  // record (run_stochastic(record=true), engine.cpp:116): the tile after this step
       const uint32_t* Bs = cur ? Bp1 : Bp0;
       store_tile(Bs, a.traj + ((a.traj_t0 + t) * a.n_envs + env) * ncell, nullptr, 0, BH, 0);
     }
@@ -444,19 +497,20 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
       s_wd[warp][3] = pw_wait_dummy(p_wait);
       s_wd[warp][4] = pw_loc;
       s_wd[warp][5] = pw_body;
+      s_wd[warp][6] = pw_lat;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      long long mx[6] = {0, 0, 0, 0, 0, 0}, passes = 0;
+      long long mx[7] = {0, 0, 0, 0, 0, 0, 0}, passes = 0;
       for (int q = 0; q < 4; ++q) {
-        for (int k = 0; k < 6; ++k) mx[k] = max(mx[k], s_wd[q][k]);
+        for (int k = 0; k < 7; ++k) mx[k] = max(mx[k], s_wd[q][k]);
         passes += s_wd[q][2];
       }
       long long* o = a.prof + static_cast<size_t>(env) * 10;
       o[0] = mx[0];      // slowest warp: dense-pass cycles (sum over steps)
       o[1] = mx[1];      // slowest warp: decide cycles
       o[2] = pw_cells;   // warp 0's cells (for reference)
-      o[3] = n_steps;
+      o[3] = mx[6];      // max warp: lane 0's record load latency (issue -> data ready)
       o[4] = mx[2];      // max passes of a warp (sum over steps)
       o[5] = passes;     // passes of all warps
       o[6] = p_step;     // CTA step cycles (thread 0)
@@ -469,7 +523,12 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
   // ---- store + counts ----------------------------------------------------------------------------
   const uint32_t* Bs = cur ? Bp1 : Bp0;
   int c3[3] = {0, 0, 0};
+#if EBL_WARP_MICRO
+  store_tile(Bs, a.out + env * ncell, c3, a.store_lo, a.store_hi, 0, n_run > 0 ? (cur ? Bp0 : Bp1) : nullptr,
+             &newly);
+#else
   store_tile(Bs, a.out + env * ncell, c3, a.store_lo, a.store_hi, 0);
+#endif
   if (a.out2) store_tile(Bs, a.out2 + env * ncell, nullptr, a.store_lo, a.store_hi, 0);
   for (int p = 0; p < a.n_peers; ++p)  // fused halo exchange: owned rows straight into the neighbour
     store_tile(Bs, a.peer_out[p], nullptr, a.peer_lo[p], a.peer_hi[p], a.peer_dst[p] - a.peer_lo[p]);

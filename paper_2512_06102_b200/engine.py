@@ -508,6 +508,24 @@ class VecFireEnv:
         check(lib().ebl_rl_rollout(self.batch.handle, n_steps, _ptr(rs), _ptr(ep)))
         return rs, ep
 
+    def step_device(self, actions, reward, done) -> None:
+        """One step with DEVICE tensors (a learner in the loop, no host round trip): actions int32
+        [n] (row*W+col for the tanker; None: the device random policy), reward float64 [n] and
+        done uint8 [n] written on the batch stream (ebl_rl_step device_io=1)."""
+        for t, dt in ((actions, "int32"), (reward, "float64"), (done, "uint8")):
+            if t is not None and (not t.is_cuda or str(t.dtype) != "torch." + dt or t.numel() != self.n_envs
+                                  or not t.is_contiguous()):
+                raise ValueError(f"expected a contiguous cuda {dt} tensor of {self.n_envs} elements")
+        check(lib().ebl_rl_step(self.batch.handle, None if actions is None else C.c_void_p(actions.data_ptr()),
+                                C.c_void_p(reward.data_ptr()), C.c_void_p(done.data_ptr()), 1))
+
+    def observe_device(self, out) -> None:
+        """Tanker observation into a device uint8 tensor [n, H, W]: FireState | wet << 2."""
+        if not out.is_cuda or str(out.dtype) != "torch.uint8" or out.numel() != self.n_envs * self.height * self.width \
+                or not out.is_contiguous():
+            raise ValueError("expected a contiguous cuda uint8 tensor of n*H*W elements")
+        check(lib().ebl_rl_observe_device(self.batch.handle, C.c_void_p(out.data_ptr())))
+
     def observe(self) -> np.ndarray:
         osz = observation_size(self.cfg)
         out = np.empty((self.n_envs, osz), dtype=np.float64)

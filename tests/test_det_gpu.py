@@ -108,6 +108,40 @@ def test_c4_full_batch_runs_and_is_deterministic():
     assert np.isfinite(outs[0][1]).all() and (np.abs(outs[0][1]).sum(1) > 0).all()
 
 
+def test_c4_all_256_envs_vs_reference_dual():
+    """BASELINE C4 at full size: every one of the 256 envs (128^2, 100 steps, MSE vs the
+    hidden-parameter target) -- the device's reverse-mode gradient against the reference's own
+    run_deterministic<Dual<6>> + loss (oracle/_ref, OpenMP over envs; the pattern of
+    tests/test_calibrate.cpp:276-298), within 1e-4 relative; losses within 1e-9."""
+    R = O.ref()
+    if R is None:
+        pytest.skip("reference not built (oracle/_ref)")
+    n, h, w, steps, seed = 256, 128, 128, 100, 4
+    t = eb.synth_terrain(seed, n, h, w)
+    init = eb.synth_ignitions(seed, t, 5)
+    _, mask = _hidden_target(t, init, seed, steps)
+    b = _batch(t, None)
+    b.set_state(init)
+    b.det_set_state_from_fire()
+    b.det_forward(steps, record=True)
+    loss, grad = b.det_loss_grad(mask, 0.0, 1.0, 1)
+    grids = [O.grid_terrain(R, "ref", t.veg()[e], t.den()[e], t.elevation[e], 30.0, t.wind_speed[e],
+                            t.wind_direction[e]) for e in range(n)]
+    hs = (O._P * n)(*[g.h for g in grids])
+    want_l = np.empty(n)
+    want_g = np.empty((n, 6))
+    secs = R.ref_loss_grad_envs(hs, n, O.ptr(O.cfg_array(O.DEFAULT_CFG)), steps, O.ptr(np.ascontiguousarray(init)),
+                                O.ptr(np.ascontiguousarray(mask)), 0.0, 1.0, 1, O.ptr(want_l), O.ptr(want_g), 0)
+    assert secs >= 0, R.ref_last_error()
+    np.testing.assert_allclose(loss, want_l, rtol=1e-9, atol=0)
+    for e in range(n):
+        scale = np.abs(want_g[e]).max()
+        np.testing.assert_allclose(grad[e], want_g[e], rtol=GRAD_RTOL, atol=GRAD_RTOL * 1e-2 * scale,
+                                   err_msg=f"env {e}")
+    # the batch gradient the calibration step consumes (fixed-order sum over envs)
+    np.testing.assert_allclose(grad.sum(0), want_g.sum(0), rtol=GRAD_RTOL)
+
+
 def _calib_case(seed=3, h=20, w=17):
     rs = np.random.default_rng(seed)
     L = dict(speed=np.full((h, w), 1.5), dir=np.full((h, w), 0.9), veg=rs.random((h, w)) * 0.6 + 0.1,

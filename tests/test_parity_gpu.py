@@ -560,14 +560,23 @@ def test_bench_c1_workload_every_env_vs_reference():
     env's final layer from the device equals the reference engine's own run_stochastic
     (oracle/_ref, OpenMP over envs; the C restatement where the reference is not built)."""
     import bench
-    t = eb.synth_terrain(bench.SEED, bench.N_ENVS, bench.H, bench.W)
-    init = eb.synth_ignitions(bench.SEED, t, bench.IGNITIONS)
+    s = bench.SPEC["C1"]
+    t = eb.synth_terrain(bench.SEED, s["n_envs"], s["h"], s["w"])
+    init = eb.synth_ignitions(bench.SEED, t, s["ignitions"])
     b = _terrain_batch(t, None)
     b.set_state(init)
     b.set_key(bench.SEED, 0)
-    b.step(bench.CA_STEPS)
+    b.step(s["steps"])
     got = b.get_state()
     assert b.diag()["ambiguous"] == 0
+    # the e2e path of the bench (pipelined host-buffer run into mapped huge-page memory)
+    h_in = eb.host_buffer(init.shape)
+    h_in[:] = init
+    h_out = eb.host_buffer(init.shape)
+    b.set_key(bench.SEED, 0)
+    b.run(h_in, s["steps"], out=h_out)
     b.close()
-    _, _, kind, _, want = bench.cpu_reference_sample(bench.N_ENVS)
-    assert np.array_equal(got, want.reshape(got.shape)), kind
+    r = bench._cpu_c1(s["n_envs"], return_states=True)
+    want = r["states"].reshape(got.shape)
+    assert np.array_equal(got, want), r["kind"]
+    assert np.array_equal(h_out, want)

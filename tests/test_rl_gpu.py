@@ -229,3 +229,45 @@ def test_c2_full_size_rollout(port):
     want = O.tanker_run_envs(t, ids, cfg, seed, steps)
     assert np.array_equal(a[0][ids], want["fire"]) and np.array_equal(a[1][ids], want["wet"])
     assert np.array_equal(a[2][ids], want["reward"]) and np.array_equal(a[3][ids], want["episodes"])
+
+
+def test_tanker_learner_in_the_loop_device_io(port):
+    """A learner in the loop on the device (north_star (4): no host round trip): each step the
+    policy reads the device observation (ebl_rl_observe_device: FireState | wet << 2), picks the
+    first burning cell of every env with torch ops on the GPU, and ebl_rl_step(device_io=1) takes
+    those device actions and writes reward/done to device tensors.  Rewards, dones, the final
+    layers and the observation equal the C restatement driven by the same actions."""
+    import torch
+    n, h, w, seed, steps = 12, 64, 64, 9, 80
+    t = eb.synth_terrain(seed, n, h, w)
+    env = eb.VecFireEnv(n, variant=eb.RL_TANKER, terrain=t, sim_cfg=None, ignitions=5, max_steps=256)
+    env.reset(seed)
+    dev = "cuda:0"
+    obs = torch.empty((n, h, w), dtype=torch.uint8, device=dev)
+    rew = torch.empty(n, dtype=torch.float64, device=dev)
+    done = torch.empty(n, dtype=torch.uint8, device=dev)
+    acts, rews, dones = [], [], []
+    cur = torch.cuda.current_stream()
+    for k in range(steps):
+        env.observe_device(obs)
+        env.batch.sync()  # the batch stream -> torch's stream (the policy reads obs)
+        burning = (obs & 3).view(n, -1) == 1
+        a = torch.where(burning.any(1), burning.to(torch.int8).argmax(1), torch.full((n,), 17, device=dev))
+        a = a.to(torch.int32).contiguous()
+        cur.synchronize()
+        env.step_device(a, rew, done)
+        env.batch.sync()
+        acts.append(a.cpu().numpy())
+        rews.append(rew.cpu().numpy().copy())
+        dones.append(done.cpu().numpy().copy())
+    want = _port_tanker(port, t, O.DEFAULT_CFG, seed, list(range(n)), steps, O.TankerCfg(5, 256, 1),
+                        actions=np.stack(acts))
+    for e in range(n):
+        assert [r[e] for r in rews] == want[e]["rewards"], e
+        assert [int(d[e]) for d in dones] == want[e]["dones"], e
+    env.observe_device(obs)
+    env.batch.sync()
+    fire = np.stack([x["fire"] for x in want])
+    wet = np.stack([x["wet"] for x in want])
+    assert np.array_equal(obs.cpu().numpy(), fire | (wet << 2))
+    assert np.array_equal(env.fire(), fire) and np.array_equal(env.wet(), wet)

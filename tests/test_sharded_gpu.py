@@ -92,3 +92,67 @@ def test_c3_full_size_shards_equal_unsharded():
     assert np.array_equal(got, want)
     total = sum(b.counts()[0] for b in sh.batches)
     assert total[:3].tolist() == cnt[:3].tolist()
+
+
+def _c3_landscape(size, seed=0):
+    t = eb.synth_terrain(seed, 1, size, size)
+    t.wind_speed[:] = 6.0
+    t.wind_direction[:] = 0.0  # "from the west"
+    return t, eb.synth_ignitions(seed, t, 64)
+
+
+def test_c3_4096_500_steps_quiet_tiles_vs_reference():
+    """The C3 geometry at 4096^2 x 500 steps (C3 generator, wind 6 from the west, 64 ignitions):
+    the production path (63 halo-tiled launches of 8 steps, quiet tiles skipped outright) equals
+    the reference's own run_stochastic (oracle/_ref, OpenMP) bit for bit, counts included; then
+    fused row shards G = 2 / 4 / 8 (quiet tiles kept across the chunks, boundary tiles exposed)
+    and the per-rank form (step + halo-row copies, records carried across calls) equal it too.
+    Every run really skips tiles (tile statistics)."""
+    R = O.ref()
+    if R is None:
+        pytest.skip("reference not built (oracle/_ref)")
+    size, steps, seed = 4096, 500, 0
+    t, init = _c3_landscape(size, seed)
+    full = eb.Batch(1, size, size)
+    full.set_terrain(t.fuel_class, t.elevation, t.class_veg, t.class_den, 30.0)
+    full.set_wind(t.wind_speed, t.wind_direction)
+    full.set_state(init)
+    full.set_key(seed, 0, first_stream=0)
+    full.diag(reset=True)
+    full.step(steps)
+    got = full.get_state()[0]
+    cnt = full.counts()[0]
+    d = full.diag()
+    full.close()
+    assert d["launches"] == 63 and d["ambiguous"] == 0
+    assert 0 < d["tiles_processed"] < 0.8 * d["tiles_launched"], d
+    g = O.grid_terrain(R, "ref", t.veg()[0], t.den()[0], t.elevation[0], 30.0, 6.0, 0.0)
+    out = np.empty_like(init[0])
+    rc = R.ref_run_stochastic(g.h, O.ptr(O.cfg_array(O.DEFAULT_CFG)), seed, 0, 0, steps, 1,
+                              O.ptr(np.ascontiguousarray(init[0])), O.ptr(out))
+    assert rc == 0
+    assert np.array_equal(got, out), np.argwhere(got != out)[:5]
+    assert cnt[:3].tolist() == [int((out == k).sum()) for k in range(3)]
+    for G in (2, 4, 8):
+        sh = ShardedLandscape(t, G, halo=8, fused=True)
+        sh.set_state(init[0])
+        sh.set_key(seed, 0, 0)
+        for b in sh.batches:
+            b.diag(reset=True)
+        sh.step(steps)
+        assert np.array_equal(sh.get_state(), out), G
+        tot = sum(b.counts()[0] for b in sh.batches)
+        assert tot[:3].tolist() == cnt[:3].tolist()
+        run = sum(b.diag()["tiles_processed"] for b in sh.batches)
+        launched = sum(b.diag()["tiles_launched"] for b in sh.batches)
+        assert run < 0.8 * launched, (G, run, launched)
+    sh = ShardedLandscape(t, 4, halo=8, fused=False)   # per-rank form: step(8) + halo copies
+    sh.set_state(init[0])
+    sh.set_key(seed, 0, 0)
+    for b in sh.batches:
+        b.diag(reset=True)
+    sh.step(steps)
+    assert np.array_equal(sh.get_state(), out)
+    run = sum(b.diag()["tiles_processed"] for b in sh.batches)
+    launched = sum(b.diag()["tiles_launched"] for b in sh.batches)
+    assert run < 0.8 * launched, (run, launched)
