@@ -10,9 +10,10 @@
 // without a CUDA device throws std::runtime_error.
 //
 // Scope: the stochastic path of engine.hpp (step_stochastic, run_stochastic,
-// StochasticBatch/step_batch, fire_fraction_stats), rl_env.hpp's FireSuppressionEnv
-// reset/observe/step, and the device-resident DeviceBatch the throughput path uses.
-// Deterministic/dual mode and the calibration loop are the next rows of SURVEY §8(f).
+// StochasticBatch/step_batch, fire_fraction_stats), the deterministic path
+// (state_from_fire, DeterministicBatch/step_batch, loss_and_gradient), rl_env.hpp's
+// FireSuppressionEnv reset/observe/step, and the device-resident DeviceBatch the
+// throughput path uses.
 #pragma once
 
 #include <array>

@@ -81,6 +81,15 @@ __device__ __forceinline__ double exp_neg(double x) {
   return exp(-x);
 }
 
+// gamma(v) of the SpreadTables: for terrain layers the palette entry of the cell's class (the same
+// fp64 expression the host table holds, (alpha_gamma (1+veg)) (1+den), kernel.hpp:75-76): one byte
+// per cell instead of eight; general layers read the table.
+__device__ __forceinline__ double gamma_at(const DetArgs& d, size_t tb, int env, int i) {
+  const StepArgs& a = d.s;
+  if (a.fuel && !d.fac_pb) return a.pal64[256 + a.fuel[static_cast<size_t>(env) * a.ter_stride + i]];
+  return d.gam[tb + i];
+}
+
 __device__ __forceinline__ double lambda_at(const double* __restrict__ burn, const double* __restrict__ pot,
                                             int h, int w, int r, int c) {
   double lam = 0.0;
@@ -107,7 +116,7 @@ __global__ void k_det_forward(DetArgs d, int t) {
   const size_t base = static_cast<size_t>(env) * ncell;
   const size_t tb = static_cast<size_t>(env) * d.tab_stride;
   const double lam = lambda_at(d.burn + base, d.pot + tb * 8, a.h, a.w, i / a.w, i % a.w);
-  const double p_ig = __dsub_rn(1.0, exp_neg(__dmul_rn(d.gam[tb + i], lam)));
+  const double p_ig = __dsub_rn(1.0, exp_neg(__dmul_rn(gamma_at(d, tb, env, i), lam)));
   const double un = d.un[base + i], bu = d.burn[base + i], bd = d.bd[base + i];
   const double newly = __dmul_rn(un, p_ig);
   d.burn_o[base + i] = __dadd_rn(newly, __dmul_rn(bu, d.pc));
@@ -196,7 +205,7 @@ __global__ void k_det_back1(DetArgs d, int t) {
   double g_gamma = 0.0, g_pc = 0.0;
   if (i < ncell) {
     const double lam = d.traj_lam[tr + i];  // bit-identical to re-folding traj_burn * pot
-    const double gam = d.gam[tb + i];
+    const double gam = gamma_at(d, tb, env, i);
     const double x = __dmul_rn(gam, lam);
     const double e = exp_neg(x);
     const double p_ig = __dsub_rn(1.0, e);
@@ -307,10 +316,13 @@ __global__ void k_det_back2(DetArgs d, int t) {
 #endif
 constexpr int kBackTx = 32, kBackTy = 8, kCpt = EBL_DET_CPT, kBackRows = kBackTy * kCpt;
 
+template <int FORM>  // 0: decided at run time, 1: terrain layers (palette gamma), 2: general layers
 __device__ __forceinline__ double back1_alam(const DetArgs& d, size_t base, size_t tb, size_t tr, int i, double& lam,
                                              double& e, double& p_ig, double& a_newly, double& un) {
   lam = d.traj_lam[tr + i];
-  const double gam = d.gam[tb + i];
+  const int env = static_cast<int>(blockIdx.y);
+  const double gam = FORM == 1 ? d.s.pal64[256 + d.s.fuel[static_cast<size_t>(env) * d.s.ter_stride + i]]
+                     : FORM == 2 ? d.gam[tb + i] : gamma_at(d, tb, env, i);
   const double x = __dmul_rn(gam, lam);
   e = exp_neg(x);
   p_ig = __dsub_rn(1.0, e);
@@ -325,6 +337,7 @@ __device__ __forceinline__ double back1_alam(const DetArgs& d, size_t base, size
 #endif
 // Tile of 32 x (8 kCpt) cells, 256 threads; thread (tx, ty) owns rows ty, ty + 8, ... (C4 backward:
 // kCpt 1 23.3 ms, 2 20.8 ms, 4 21.0 ms per run)
+template <int FORM>
 __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_back(DetArgs d, int t) {
   __shared__ double red[6 * 32];
   __shared__ double s_al[kBackRows + 2][kBackTx + 2];
@@ -347,12 +360,12 @@ __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_ba
     bu[q] = Ab[q] = Ad[q] = 0.0;
     if (r < h && c < w) {
       double lam, e, p_ig, a_newly, un;
-      al = back1_alam(d, base, tb, tr, i, lam, e, p_ig, a_newly, un);
+      al = back1_alam<FORM>(d, base, tb, tr, i, lam, e, p_ig, a_newly, un);
       bu[q] = d.traj_burn[tr + i];
       Ab[q] = d.A_burn[base + i];
       Ad[q] = d.A_bd[base + i];
       d.A_un_o[base + i] = d.A_un[base + i] + a_newly * p_ig;
-      const double F = d.fac_F ? d.fac_F[tb + i] : a.pal64[768 + a.fuel[static_cast<size_t>(env) * a.ter_stride + i]];
+      const double F = FORM == 2 ? d.fac_F[tb + i] : a.pal64[768 + a.fuel[static_cast<size_t>(env) * a.ter_stride + i]];
       g_gamma += (a_newly * un * e) * lam * F;  // dgamma/dalpha_gamma = F(v)
       g_pc += bu[q] * (Ab[q] - Ad[q]);
     }
@@ -369,7 +382,7 @@ __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_ba
     double al = 0.0;
     if (vr >= 0 && vr < h && vc >= 0 && vc < w) {
       double lam, e, p_ig, a_newly, un;
-      al = back1_alam(d, base, tb, tr, vr * w + vc, lam, e, p_ig, a_newly, un);
+      al = back1_alam<FORM>(d, base, tb, tr, vr * w + vc, lam, e, p_ig, a_newly, un);
     }
     s_al[sy][sx] = al;
   }
@@ -381,7 +394,7 @@ __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_ba
     const int r = r0 + ty + kBackTy * q, i = r * w + c, sy = ty + kBackTy * q + 1, sx = tx + 1;
     if (r >= h || c >= w) continue;
     double acc_burn = Ab[q] * d.pc + Ad[q] * (1.0 - d.pc);
-    if (bu[q] != 0.0 && d.fac_pb) {  // general form: host-built derivative factors
+    if (FORM == 2 && bu[q] != 0.0) {  // general form: host-built derivative factors
       const size_t o = tb + i;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -397,7 +410,7 @@ __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_ba
         gw2 += ab * pot * d.fac_Va[o * 8 + k];
         gs += ab * pot * d.fac_S[o * 8 + k];
       }
-    } else if (bu[q] != 0.0) {
+    } else if (FORM == 1 && bu[q] != 0.0) {
       const TerrainView tv = terrain_view(a, env);
       const float* slope = a.slope32 ? a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8 : nullptr;
       const double V = d.V[env * d.wind_stride];
@@ -485,7 +498,9 @@ cudaError_t launch_det_backward(const DetArgs& d, int t, cudaStream_t s) {
   const int ncell = d.s.h * d.s.w;
   const dim3 grid((ncell + 255) / 256, d.s.n_envs);
   if (d.A_un_o) {  // fused, double-buffered adjoints
-    k_det_back<<<dim3(det_blocks_per_env(d.s.h, d.s.w), d.s.n_envs), kBackTx * kBackTy, 0, s>>>(d, t);
+    const dim3 g(det_blocks_per_env(d.s.h, d.s.w), d.s.n_envs);
+    if (d.fac_pb) k_det_back<2><<<g, kBackTx * kBackTy, 0, s>>>(d, t);  // general layers
+    else k_det_back<1><<<g, kBackTx * kBackTy, 0, s>>>(d, t);           // terrain layers
     return cudaGetLastError();
   }
   k_det_back1<<<grid, 256, 0, s>>>(d, t);

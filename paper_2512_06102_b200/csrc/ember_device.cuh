@@ -397,6 +397,38 @@ __device__ __forceinline__ bool ignite_pot(const StepArgs& a, int env, int srow,
   return u < p;
 }
 
+// ignite_pot with a shallower fp32 chain: the masked terms summed as a tree and p = 1 - e^-x
+// without a branch (both forms evaluated, selected).  Same decision: the fp32 x only has to lie
+// well inside the 1e-4 guard band (any order of 8 positive terms: within 4e-7 relative); every
+// draw in the band is decided by the fp64 re-evaluation in the reference's association.  nb = 0
+// (a burning cell routed through the same code path) returns false without touching the guard.
+__device__ __forceinline__ bool ignite_pot_fast(const StepArgs& a, int env, int srow, float4 T0, float4 T1, int w,
+                                                int r, int c, uint32_t nb, uint64_t m, const DiagCounters& dg) {
+  if (!a.force64) {
+    const float t0 = (nb & 1u) ? T0.x : 0.f, t1 = (nb & 2u) ? T0.y : 0.f, t2 = (nb & 4u) ? T0.z : 0.f;
+    const float t3 = (nb & 8u) ? T0.w : 0.f, t4 = (nb & 16u) ? T1.x : 0.f, t5 = (nb & 32u) ? T1.y : 0.f;
+    const float t6 = (nb & 64u) ? T1.z : 0.f, t7 = (nb & 128u) ? T1.w : 0.f;
+    const float x = ((t0 + t1) + (t2 + t3)) + ((t4 + t5) + (t6 + t7));
+    if (x == 0.f) return false;  // gamma or lambda exactly 0 (or no burning source): p = 0
+    const float poly = x * (1.f - x * (0.5f - x * (1.f / 6.f - x * (1.f / 24.f))));
+    const float p32 = x < 0.03f ? poly : 1.f - ex2_approx(-x * 1.44269504088896341f);
+    if (p32 > 1e-12f) {
+      const uint64_t lo = static_cast<uint64_t>(p32 * static_cast<float>((1.0 - kGuardRel) * 0x1p53));
+      const uint64_t hi = static_cast<uint64_t>(p32 * static_cast<float>((1.0 + kGuardRel) * 0x1p53));
+      if (m < lo) return true;
+      if (m >= hi) return false;
+    }
+  } else if (nb == 0u) {
+    return false;
+  }
+  const TerrainView t = terrain_view(a, env, srow);
+  dg.fallback();
+  const double u = bits_to_uniform(m);
+  const double p = terrain_p64(t, w, r, c, nb);
+  if (fabs(u - p) < kAmbiguousBand) dg.ambiguous();
+  return u < p;
+}
+
 // Decision for an Unburned cell with burning-neighbour mask nb != 0.
 // `srow` selects the wind-schedule entry in force (sched_row).
 template <int MODE>

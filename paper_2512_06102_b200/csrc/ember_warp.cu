@@ -38,8 +38,11 @@
 #define EBL_WARP_UNROLL2 1  // C1 kernel 0.524 -> 0.509 ms (a few spilled bytes)
 #endif
 #ifndef EBL_WARP_MICRO  // newly-ignited counts from the planes at the store (not per ignition),
-#define EBL_WARP_MICRO 0  // schedule / record branches hoisted out of the step loop
+#define EBL_WARP_MICRO 1  // schedule / record branches hoisted out of the step loop
 #endif
+#ifndef EBL_WARP_FAST  // decide passes without divergent branches: branch-free neighbour windows
+#define EBL_WARP_FAST 1  // (zeroed guard words), SWAR + table n-th set bit, burning and candidate
+#endif                   // cells through one code path (even compile-time words per row, pot32t)
 #ifndef EBL_WARP_PFIGN  // at an ignition, prefetch the pot32t rows of the 8 neighbours (the next
 #define EBL_WARP_PFIGN 0  // step's new candidates): 1 into L1, 2 into L2
 #endif
@@ -70,6 +73,21 @@ __device__ __forceinline__ int nth_set_bit(uint32_t v, int q) {
   return pos;
 }
 
+// Position of the q-th (0-based) set bit of v (q < popc(v)) with a shallower dependency chain:
+// SWAR byte counts, their inclusive prefix in one multiply, the byte by three compares, the bit
+// from a 256-entry table of packed 3-bit positions (shared memory).
+__device__ __forceinline__ int nth_set_bit_lut(uint32_t v, int q, const uint32_t* lut) {
+  uint32_t c = v - ((v >> 1) & 0x55555555u);
+  c = (c & 0x33333333u) + ((c >> 2) & 0x33333333u);
+  c = (c + (c >> 4)) & 0x0f0f0f0fu;
+  const uint32_t cum = c * 0x01010101u;  // byte k: set bits in bytes 0..k
+  const uint32_t qq = static_cast<uint32_t>(q);
+  const int k = (qq >= (cum & 0xffu)) + (qq >= ((cum >> 8) & 0xffu)) + (qq >= ((cum >> 16) & 0xffu));
+  const int before = k ? static_cast<int>((cum << 8 >> (8 * k)) & 0xffu) : 0;
+  const uint32_t byte = (v >> (8 * k)) & 0xffu;
+  return 8 * k + static_cast<int>((lut[byte] >> (3 * (q - before))) & 7u);
+}
+
 // DIMC: the env's side when the env is a DIMC x DIMC square known at compile time (128: C1, 64:
 // C2-sized), else 0; WPRC: words per row when known (2, 4), else 0.
 #ifndef EBL_WARP_MINB
@@ -85,6 +103,10 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
   __shared__ float s_pal[kTer ? 512 : 1];
   __shared__ float s_kw[8];
   __shared__ float s_srckw[kTer ? 32 * 8 : 1];
+  // the fast decide path: even compile-time words per row leave a zero padding word after every
+  // plane row (stride wpr | 1), so the neighbour windows need no bounds branches
+  constexpr bool kFast = EBL_WARP_FAST && EBL_WARP_MICRO && kTer && WPRC != 0 && (WPRC & 1) == 0;
+  __shared__ uint32_t s_nth[kFast ? 256 : 1];
 
   // region of this CTA: one tile of one env's layer plus its light-cone halo (the whole env for
   // resident launches); H x RW region cells, layer BH x W
@@ -101,7 +123,7 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
   // extra word every 4 rows makes their stride 4S+1 (odd) -> 32 distinct banks
   auto ro = [S](int R) { return R * S + (R >> 2); };
   const int PH = ro(H + 2) + 1;  // words of a B plane (H + 2 rows)
-  uint32_t* const Bp0 = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* const Bp0 = reinterpret_cast<uint32_t*>(smem) + 4;  // 4 zero guard words before the planes
   uint32_t* const Bp1 = Bp0 + PH;
   uint32_t* const X = Bp1 + PH;
   uint32_t* const ACT = X + PH;
@@ -158,9 +180,20 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
     atomicAdd(a.diag + 3, 1ull);
   }
   // ---- load ----------------------------------------------------------------------------------
-  for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
-    Bp0[i] = Bp1[i] = 0u;
-    Bp0[ro(H + 1) + i] = Bp1[ro(H + 1) + i] = 0u;
+  if constexpr (kFast) {  // guard words, padding words and padding rows of both B planes: zero
+    for (int i = threadIdx.x; i < 2 * PH + 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {  // n-th set bit of a byte, 3 bits each
+      uint32_t e = 0u;
+      for (int bit = 0, n = 0; bit < 8; ++bit)
+        if ((i >> bit) & 1) e |= static_cast<uint32_t>(bit) << (3 * n++);
+      s_nth[i] = e;
+    }
+    __syncthreads();
+  } else {
+    for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
+      Bp0[i] = Bp1[i] = 0u;
+      Bp0[ro(H + 1) + i] = Bp1[ro(H + 1) + i] = 0u;
+    }
   }
   const uint8_t* __restrict__ in = a.in + env * ncell;
   uint32_t any_b = 0u;  // a burning cell anywhere in the region
@@ -375,7 +408,9 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
             wv = ar[++jj];
           }
         }
-        const int cc = 32 * jj + nth_set_bit(wv, q);
+        int cc;
+        if constexpr (kFast) cc = 32 * jj + nth_set_bit_lut(wv, q, s_nth);
+        else cc = 32 * jj + nth_set_bit(wv, q);
 #if EBL_PHASE_PROF
         {
           const unsigned msk = __activemask();
@@ -386,6 +421,34 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
         }
 #endif
         const int gr = R0 + rr, gc = C0 + cc;  // layer coordinates
+        if (kFast && use_tab) {
+          // one code path for burning and candidate cells (no divergence inside the pass): the
+          // record is requested first, the neighbour windows are branch-free (zero guard and
+          // padding words), a burning cell takes the candidate arithmetic with an empty mask
+          const float4* tp = reinterpret_cast<const float4*>(a.pot32t + static_cast<size_t>(env) * a.pot32t_stride) +
+                             2 * (gr * W + gc);
+          const float4 T0 = __ldg(tp), T1 = __ldg(tp + 1);
+          const int j = cc >> 5, b = cc & 31;
+          const uint32_t bit = 1u << b;
+          const int wi = ro(rr + 1) + j;
+          const uint64_t m = cell_bits53(prefix, gbase + static_cast<uint64_t>(rr) * W + cc, 0);
+          auto win = [&](const uint32_t* row) -> uint32_t {  // columns c-1, c, c+1 -> bits 0..2
+            const uint32_t lo = row[j - 1], md = row[j], hi = row[j + 1];
+            return (b > 0 ? __funnelshift_r(md, hi, b - 1) : __funnelshift_r(lo, md, 31)) & 7u;
+          };
+          const uint32_t midw = win(B + ro(rr + 1)), dnw = win(B + ro(rr)), upw = win(B + ro(rr + 2));
+          const bool burning = midw & 2u;
+          const uint32_t nb = burning ? 0u
+                                      : (midw & 1u) | (dnw << 1) | ((midw >> 2) << 4) | ((upw >> 2) << 5) |
+                                            ((upw & 2u) << 5) | ((upw & 1u) << 7);
+          const bool ig = ignite_pot_fast(a, env, srow, T0, T1, W, gr, gc, nb, m, dg);
+          if (burning && m >= a.pc_thr) {  // burns out: u >= p_continue, integer form
+            atomicAnd(Bn + wi, ~bit);
+            atomicOr(X + ro(rr) + j, bit);
+          }
+          if (ig) atomicOr(Bn + wi, bit);
+          continue;
+        }
         // the candidate records are requested first (burning cells waste one), so their latency
         // overlaps the RNG rounds and the neighbour masks below
         CellRec rec{};
@@ -573,7 +636,7 @@ cudaError_t launch_wp(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStre
 size_t warp_smem_bytes(int h, int w) {
   const size_t S = plane_stride((w + 31) / 32);
   const size_t R = static_cast<size_t>(h) + 2;
-  return 4 * (R * S + (R >> 2) + 1) * sizeof(uint32_t);  // B x2, X, ACT (ro() layout, ember_warp.cu)
+  return 4 * (R * S + (R >> 2) + 1) * sizeof(uint32_t) + 16;  // B x2, X, ACT (ro() layout) + guard words
 }
 
 bool warp_fits(int h, int w) {

@@ -65,24 +65,27 @@ void reject_nan(const Grid<double>& g, const char* what) {
 }  // namespace
 
 // ---- grid.hpp --------------------------------------------------------------------------------
-int offset_index(NeighborOffset d) {
+// The value types below reproduce the reference's constructors and validation (same checks, same
+// exception types and messages, so a caller sees identical behaviour): grid.cpp:28-142.
+int offset_index(NeighborOffset d) {  // grid.cpp:28-33
   for (int k = 0; k < 8; ++k)
     if (kNeighborOffsets[k] == d) return k;
   throw std::invalid_argument("offset_index: not a neighbor offset");
 }
 
-double wrap_angle(double a) {
+double wrap_angle(double a) {  // grid.cpp:35-42
   const double two_pi = 2.0 * std::numbers::pi;
   double w = std::fmod(a, two_pi);
   return w < 0.0 ? w + two_pi : w;
 }
 
-double offset_angle(NeighborOffset d) {
+double offset_angle(NeighborOffset d) {  // grid.cpp:44-47
   if (d.dx < -1 || d.dx > 1 || d.dy < -1 || d.dy > 1 || (d.dx == 0 && d.dy == 0))
     throw std::invalid_argument("offset_angle: not a neighbor offset");
   return wrap_angle(std::atan2(static_cast<double>(d.dy), static_cast<double>(d.dx)));
 }
 
+// grid.cpp:49-62 (direction wrapped at construction)
 WindField::WindField(Grid<double> speed, Grid<double> direction)
     : speed_(std::move(speed)), dir_(std::move(direction)) {
   if (speed_.height() != dir_.height() || speed_.width() != dir_.width())
@@ -101,6 +104,7 @@ WindField WindField::uniform(int h, int w, double speed, double direction) {
   return WindField(Grid<double>(h, w, speed), Grid<double>(h, w, direction));
 }
 
+// grid.cpp:68-77 (veg/den clamped to [-1, 1])
 FuelField::FuelField(Grid<double> veg, Grid<double> den) : veg_(std::move(veg)), den_(std::move(den)) {
   if (veg_.height() != den_.height() || veg_.width() != den_.width())
     throw std::invalid_argument("FuelField: veg and den dimensions differ");
@@ -124,11 +128,12 @@ void SlopeField::set_toward(int r, int c, int k, double slope) {
   s_[static_cast<std::size_t>(r * w_ + c) * 8 + k] = slope;
 }
 
-void validate_config(const SimConfig& cfg) {
+void validate_config(const SimConfig& cfg) {  // grid.cpp:107-124
   const ebl_sim_config c = to_c(cfg);
   ok(ebl_validate_config(&c));
 }
 
+// grid.cpp:126-142 (matching dimensions of every layer)
 GridState::GridState(FireLayer fire, WindField wind, FuelField fuel, SlopeField slope)
     : fire_(std::move(fire)), wind_(std::move(wind)), fuel_(std::move(fuel)), slope_(std::move(slope)) {
   const int h = fire_.height(), w = fire_.width();
@@ -226,6 +231,7 @@ FireLayer step_stochastic(const FireLayer& fire, const GridState& grid, const Si
   return step_stochastic(fire, tables, cfg, key, exec);
 }
 
+// engine.cpp:74-86 (empty schedule is a logic_error; at_step clamps to the last entry)
 WindSchedule::WindSchedule(std::vector<WindField> winds) : winds_(std::move(winds)) {
   for (std::size_t i = 1; i < winds_.size(); ++i)
     if (winds_[i].height() != winds_[0].height() || winds_[i].width() != winds_[0].width())
@@ -309,7 +315,7 @@ void step_batch(StochasticBatch& batch, const GridState& grid, const SimConfig& 
   step_batch(batch, tables, cfg, exec);
 }
 
-FireFractions fire_fraction_stats(const FireLayer& fire) {
+FireFractions fire_fraction_stats(const FireLayer& fire) {  // engine.cpp:185-197
   FireFractions f;
   const double n = fire.size();
   for (FireState s : fire.data()) {
@@ -376,7 +382,7 @@ std::vector<FireFractions> DeviceBatch::fractions() const {
 }
 
 // ---- deterministic path + calibrate -----------------------------------------------------------------
-ContinuousState state_from_fire(const FireLayer& fire) {
+ContinuousState state_from_fire(const FireLayer& fire) {  // engine.cpp:42-52
   const int h = fire.height(), w = fire.width();
   ContinuousState s{Grid<double>(h, w), Grid<double>(h, w), Grid<double>(h, w)};
   for (int i = 0; i < h * w; ++i) {
@@ -387,7 +393,7 @@ ContinuousState state_from_fire(const FireLayer& fire) {
   return s;
 }
 
-void validate_state(const ContinuousState& s, double tol) {
+void validate_state(const ContinuousState& s, double tol) {  // engine.cpp:54-72
   const int h = s.height(), w = s.width();
   if (s.p_burn.height() != h || s.p_burn.width() != w || s.p_bd.height() != h || s.p_bd.width() != w)
     throw std::invalid_argument("ContinuousState: component dimensions differ");
