@@ -280,6 +280,11 @@ int ebl_det_get_state(ebl_batch* b, double* p_un, double* p_burn, double* p_bd);
 /* run_deterministic (engine.hpp:225-245) for n_steps on the terrain statics, in the
  * reference's fp64 arithmetic on the device (DESIGN.md §4 explains why not fp32); record = 1
  * keeps (p_un, p_burn) of every step in HBM for ebl_det_loss_grad. */
+/* Where the terrain-form SpreadTables<double> of the deterministic path are built: on the device
+ * (default: the config-free fp64 slopes cached once per terrain, pot = (source kappa_wind)
+ * exp(alpha_s S) with a restatement of the reference libm's exp, bit-identical to the host build,
+ * so calibration iterations need no host table build) or on the host (on_device = 0). */
+int ebl_batch_set_det_tables(ebl_batch* b, int on_device);
 int ebl_det_forward(ebl_batch* b, int n_steps, int record);
 /* loss = bce_w * BCE(clamp(pred)) + mse_w * MSE(avgpool(pred, pool), avgpool(mask, pool)),
  * pred = p_burn + p_bd (calibrate.hpp:86-146), per env, and its gradient with respect to

@@ -132,6 +132,7 @@ SIGNATURES = {
     "ebl_batch_diag": (_I, [_P, _P, _I]),
     "ebl_batch_tile_stats": (_I, [_P, _P, _I]),
     "ebl_rl_observe_device": (_I, [_P, _P]),
+    "ebl_batch_set_det_tables": (_I, [_P, _I]),
     "ebl_batch_sync": (_I, [_P]),
     "ebl_device_rng_words": (_I, [_I, _P, _P]),
     "ebl_step_stochastic": (_I, [_I, _I, _P, _P, _P, _P, _P, _P, C.POINTER(SimConfig), _U64,

@@ -142,6 +142,9 @@ struct ebl_batch {
   int det_cur = 0;
   bool det_ready = false;
   DevBuf<double> det_pot, det_gam, det_fac, det_V, det_align, traj, adj, det_mask, acc, det_loss, det_grad, det_init;
+  DevBuf<double> det_S;             // [grid][cell][8] cached fp64 slopes (host atan, once per terrain)
+  bool det_S_valid = false;
+  bool det_dev_tables = true;       // terrain-form SpreadTables built on the device (ebl_batch_set_det_tables)
   int det_tables = 0;
   bool det_tables_valid = false;
   ebl_sim_config det_cfg{};
@@ -568,6 +571,7 @@ int ebl_batch_set_terrain(ebl_batch* b, int n_grids, const uint8_t* fuel_class, 
   b->derived_dirty = true;
   b->slope_dirty = true;
   b->det_tables_valid = false;
+  b->det_S_valid = false;
   b->pot.reset();
   b->gamma.reset();
   if (b->n_winds == 0) {  // calm air until set
@@ -593,6 +597,7 @@ void adopt_device_terrain(ebl_batch* b, int n_grids, std::vector<double> veg, st
   b->derived_dirty = true;
   b->slope_dirty = true;
   b->det_tables_valid = false;
+  b->det_S_valid = false;
   b->pot.reset();
   b->gamma.reset();
   if (b->n_winds == 0) {
@@ -2051,7 +2056,8 @@ int det_tables(ebl_batch* b) {
   const bool general = b->mode == ebl::kStaticTables;
   const int T = general ? b->n_grids : ((b->n_grids > 1 || b->n_winds > 1) ? b->n_envs : 1);
   const size_t n = b->ncell;
-  std::vector<double> pot(n * 8 * T), gam(n * T);
+  const bool dev_built = !general && b->det_dev_tables && std::abs(cfg6(b->cfg).alpha_s) < 325.0;
+  std::vector<double> pot(dev_built ? 0 : n * 8 * T), gam(dev_built ? 0 : n * T);
   if (general) {  // per-cell layers: the SpreadTables plus the adjoint's derivative factors
     const size_t nt = n * T;
     ebl::build_tables(nt, b->g_speed.data(), b->g_dir.data(), b->g_veg.data(), b->g_den.data(),
@@ -2076,10 +2082,28 @@ int det_tables(ebl_batch* b) {
       EBL_CUDA(cudaStreamSynchronize(b->stream));
       b->h_terrain_stale = false;
     }
-    ebl::build_terrain_tables(T, b->h, b->w, b->h_fuel.data(), b->h_elev.data(), b->n_grids > 1 ? n : 0,
-                              b->pal_veg.data(), b->pal_den.data(), b->cellsize, b->wind_speed.data(),
-                              b->wind_dir.data(), b->n_winds > 1 ? 1 : 0, c, pot.data(), gam.data());
     b->det_fac.reset();
+    // on the device: pot = (source kappa_wind) exp(alpha_s S) with the cached fp64 slopes and the
+    // restated libm exp, bit-identical to the host build (ember_det.cu); exact for |alpha_s S| < 512,
+    // i.e. |alpha_s| < 325 (|S| < pi/2), else the host build.  gamma comes from the palette.
+    if (dev_built) {
+      if (!b->det_S_valid) {
+        std::vector<double> S(n * 8 * b->n_grids);
+        ebl::build_terrain_slopes64(b->n_grids, b->h, b->w, b->h_elev.data(), n, b->cellsize, S.data());
+        EBL_CUDA(b->det_S.alloc(S.size()));
+        EBL_CUDA(cudaMemcpyAsync(b->det_S.p, S.data(), S.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+        EBL_CUDA(cudaStreamSynchronize(b->stream));
+        b->det_S_valid = true;
+      }
+      EBL_CUDA(b->det_pot.alloc(n * 8 * T));
+      EBL_CUDA(ebl::launch_det_tables_terrain(b->det_S.p, b->fuel.p, b->pal64.p, b->kw64.p, c.alpha_s, T, n,
+                                              b->n_grids > 1 ? n : 0, b->n_winds > 1 ? 1 : 0, b->det_pot.p,
+                                              b->stream));
+    } else {
+      ebl::build_terrain_tables(T, b->h, b->w, b->h_fuel.data(), b->h_elev.data(), b->n_grids > 1 ? n : 0,
+                                b->pal_veg.data(), b->pal_den.data(), b->cellsize, b->wind_speed.data(),
+                                b->wind_dir.data(), b->n_winds > 1 ? 1 : 0, c, pot.data(), gam.data());
+    }
   }
   std::vector<double> V(b->n_winds), al(static_cast<size_t>(b->n_winds) * 8);
   for (int w = 0; w < b->n_winds; ++w) {  // kernel.hpp:24: cos(phi_k - theta) - 1
@@ -2087,12 +2111,14 @@ int det_tables(ebl_batch* b) {
     const double dir = ebl::wrap_angle(b->wind_dir[w]);
     for (int k = 0; k < 8; ++k) al[w * 8 + k] = std::cos(ebl::offset_angle(k) - dir) - 1.0;
   }
-  EBL_CUDA(b->det_pot.alloc(pot.size()));
-  EBL_CUDA(b->det_gam.alloc(gam.size()));
+  if (!dev_built) {
+    EBL_CUDA(b->det_pot.alloc(pot.size()));
+    EBL_CUDA(b->det_gam.alloc(gam.size()));
+    EBL_CUDA(cudaMemcpyAsync(b->det_pot.p, pot.data(), pot.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+    EBL_CUDA(cudaMemcpyAsync(b->det_gam.p, gam.data(), gam.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  }
   EBL_CUDA(b->det_V.alloc(V.size()));
   EBL_CUDA(b->det_align.alloc(al.size()));
-  EBL_CUDA(cudaMemcpyAsync(b->det_pot.p, pot.data(), pot.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
-  EBL_CUDA(cudaMemcpyAsync(b->det_gam.p, gam.data(), gam.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
   EBL_CUDA(cudaMemcpyAsync(b->det_V.p, V.data(), V.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
   EBL_CUDA(cudaMemcpyAsync(b->det_align.p, al.data(), al.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
@@ -2143,6 +2169,14 @@ int ebl_det_get_state(ebl_batch* b, double* un, double* burn, double* bd) {
   if (burn) EBL_CUDA(cudaMemcpyAsync(burn, b->det[c + 1].p, bytes, cudaMemcpyDeviceToHost, b->stream));
   if (bd) EBL_CUDA(cudaMemcpyAsync(bd, b->det[c + 2].p, bytes, cudaMemcpyDeviceToHost, b->stream));
   EBL_CUDA(cudaStreamSynchronize(b->stream));
+  return EBL_OK;
+}
+
+int ebl_batch_set_det_tables(ebl_batch* b, int on_device) {
+  EBL_DEVICE_GUARD(b);
+  if (int e = check_batch(b)) return e;
+  b->det_dev_tables = on_device != 0;
+  b->det_tables_valid = false;
   return EBL_OK;
 }
 

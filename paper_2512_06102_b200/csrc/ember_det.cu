@@ -26,6 +26,7 @@
 #include <cstdint>
 
 #include "ember_device.cuh"
+#include "ember_exp.cuh"
 #include "ember_kernels.h"
 #include "ember_params.h"
 
@@ -464,6 +465,245 @@ __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_ba
   }
 }
 
+#ifndef EBL_DET_STREAM
+#define EBL_DET_STREAM 1  // row-streaming backward with bulk asynchronous copies (terrain layers)
+#endif
+
+// ---- row-streaming backward (terrain layers, W <= 128, W % 16 == 0) ----------------------------
+// One CTA per (env, band of kSB rows), one thread per column.  The dense per-cell inputs of every
+// row (lambda, p_un, p_burn of step t, the three adjoints, the fuel class) are streamed into a ring
+// of shared-memory stages by bulk asynchronous copies (cp.async.bulk, completion on an mbarrier)
+// kSD rows ahead, so the SM keeps ~tens of KB in flight without per-thread loads; each source's pot
+// and slope records (needed only where p_burn != 0) are requested one step of the loop early.  Row
+// q: back1 (a_lambda into a 3-row ring, A_un' of band rows), then back2 of row q-1 (A_burn', the
+// pot-parameter gradients).  Same arithmetic per cell as k_det_back; the band's halo rows get
+// their a_lambda recomputed (bit-identical inputs).  Gradient partials per (env, band), reduced in
+// a fixed order by k_det_reduce.
+constexpr int kSB = 16;       // rows per band
+#ifndef EBL_DET_SD
+#define EBL_DET_SD 2  // C4 run: 2 rows 16.8 ms, 3 rows 17.6 ms, 4 rows 19.2 ms (occupancy vs rows in flight)
+#endif
+constexpr int kSD = EBL_DET_SD;  // rows requested ahead
+constexpr int kSlots = kSD + 3;  // + the rows back1 and back2 read, + the one refilled this iteration
+constexpr int kAl = 4;        // a_lambda ring: back2 of row q-1 reads rows q-2..q while back1 writes q+1
+constexpr int kSW = 128;      // max columns
+struct StreamRow {
+  double lam[kSW], un[kSW], burn[kSW], au[kSW], ab[kSW], ad[kSW];
+  uint8_t fuel[kSW];
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_addr(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kSW, EBL_DET_SD <= 2 ? 6 : 5) k_det_back_stream(DetArgs d, int t) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  StreamRow* const st = reinterpret_cast<StreamRow*>(dsm);
+  double (*const alam)[kSW + 2] = reinterpret_cast<double (*)[kSW + 2]>(dsm + kSlots * sizeof(StreamRow));
+  auto al_row = [&](int q) { return alam[(q + kAl) % kAl]; };
+  __shared__ __align__(8) uint64_t bar[kSlots];
+  __shared__ double red[6 * 32];
+  const StepArgs& a = d.s;
+  const int h = a.h, w = a.w, ncell = h * w;
+  const int env = blockIdx.y;
+  const int r0 = blockIdx.x * kSB, r1 = min(h, r0 + kSB);
+  const int qa = max(0, r0 - 1), qb = min(h - 1, r1);  // rows whose a_lambda the band needs
+  const int c = threadIdx.x;
+  const bool col = c < w;
+  const size_t base = static_cast<size_t>(env) * ncell;
+  const size_t tr = static_cast<size_t>(t) * a.n_envs * ncell + base;
+  const uint8_t* fuel = a.fuel + static_cast<size_t>(env) * a.ter_stride;
+  const unsigned rowb = static_cast<unsigned>(w) * 8u;
+  auto issue = [&](int q) {  // one thread: the stage of row q (6 dense rows + the fuel row)
+    const int slot = (q - qa) % kSlots;
+    StreamRow& S = st[slot];
+    const size_t o = static_cast<size_t>(q) * w;
+    mbar_expect_tx(&bar[slot], 6 * rowb + static_cast<unsigned>(w));
+    bulk_g2s(S.lam, d.traj_lam + tr + o, rowb, &bar[slot]);
+    bulk_g2s(S.un, d.traj_un + tr + o, rowb, &bar[slot]);
+    bulk_g2s(S.burn, d.traj_burn + tr + o, rowb, &bar[slot]);
+    bulk_g2s(S.au, d.A_un + base + o, rowb, &bar[slot]);
+    bulk_g2s(S.ab, d.A_burn + base + o, rowb, &bar[slot]);
+    bulk_g2s(S.ad, d.A_bd + base + o, rowb, &bar[slot]);
+    bulk_g2s(S.fuel, fuel + o, static_cast<unsigned>(w), &bar[slot]);
+  };
+  if (c < kSlots) mbar_init(&bar[c], 1);
+  for (int i = c; i < kAl * (kSW + 2); i += blockDim.x) (&alam[0][0])[i] = 0.0;  // OOB rows / columns
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  if (c == 0)
+    for (int q = qa; q <= qb && q < qa + kSlots; ++q) issue(q);
+
+  const double pc = d.pc, qc = 1.0 - d.pc;
+  const double V = d.V[env * d.wind_stride];
+  const double* align = d.align + env * d.wind_stride * 8;
+  const float* slope = a.slope32 + static_cast<size_t>(env) * a.ter_stride * 8;
+  const double* pot = d.pot + static_cast<size_t>(env) * d.tab_stride * 8;
+  double g_gamma = 0.0, g_pc = 0.0, gp = 0.0, gw1 = 0.0, gw2 = 0.0, gs = 0.0;
+  double potk[8];
+  float sown[8];
+  for (int q = qa; q <= r1; ++q) {
+    // ---- the source records of row q-1 (back2 below), requested before this row's wait ----
+    const int rs = q - 1;
+    const bool b2 = rs >= r0 && rs < r1;
+    double bu = 0.0;
+    if (b2 && col) {
+      bu = st[(rs - qa) % kSlots].burn[c];
+      if (bu != 0.0) {  // into L1 now (two lines of pot, one of slope), read after back1
+        const size_t i = static_cast<size_t>(rs) * w + c;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(pot + i * 8));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(pot + i * 8 + 4));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(slope + i * 8));
+      }
+    }
+    // ---- back1 of row q (a real row), or an all-zero a_lambda row below the landscape ----
+    double* al_q = al_row(q);
+    if (q <= qb) {
+      const int slot = (q - qa) % kSlots;
+      mbar_wait(&bar[slot], static_cast<unsigned>(((q - qa) / kSlots) & 1));
+      const StreamRow& S = st[slot];
+      double al = 0.0;
+      if (col) {
+        const int f = S.fuel[c];
+        const double lam = S.lam[c], gam = a.pal64[256 + f];
+        const double x = __dmul_rn(gam, lam);
+        const double e = exp_neg(x);
+        const double p_ig = __dsub_rn(1.0, e);
+        const double un = S.un[c];
+        const double a_newly = S.ab[c] - S.au[c];
+        const double a_x = a_newly * un * e;  // dp_ig/dx = e^{-x} (Dual's exp)
+        al = a_x * gam;
+        if (q >= r0 && q < r1) {
+          d.A_un_o[base + static_cast<size_t>(q) * w + c] = S.au[c] + a_newly * p_ig;
+          g_gamma += a_x * lam * a.pal64[768 + f];  // dgamma/dalpha_gamma = F(v)
+          g_pc += S.burn[c] * (S.ab[c] - S.ad[c]);
+        }
+      }
+      al_q[c + 1] = al;
+    } else {
+      al_q[c + 1] = 0.0;
+    }
+    __syncthreads();  // a_lambda of rows q-2 .. q complete; every thread is past back2 of row q-2
+    if (c == 0 && q - 2 >= qa) {  // the stage of row q-2 is free: refill it kSlots rows later
+      const int nq = q - 2 + kSlots;
+      if (nq <= qb) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(nq);
+      }
+    }
+    // ---- back2 of row q-1 (source u = (rs, c), targets u + d_k) ----
+    if (b2 && col) {
+      const StreamRow& S = st[(rs - qa) % kSlots];
+      double acc_burn = S.ab[c] * pc + S.ad[c] * qc;
+      if (bu != 0.0) {
+        const size_t i = static_cast<size_t>(rs) * w + c;
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+          const double2 pp = __ldg(reinterpret_cast<const double2*>(pot + i * 8 + k));
+          potk[k] = pp.x;
+          potk[k + 1] = pp.y;
+        }
+        const float4 s0 = __ldg(reinterpret_cast<const float4*>(slope + i * 8));
+        const float4 s1 = __ldg(reinterpret_cast<const float4*>(slope + i * 8 + 4));
+        sown[0] = s0.x, sown[1] = s0.y, sown[2] = s0.z, sown[3] = s0.w;
+        sown[4] = s1.x, sown[5] = s1.y, sown[6] = s1.z, sown[7] = s1.w;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int vr = rs + kDy[k], vc = c + kDx[k];
+          if (vr < 0 || vr >= h || vc < 0 || vc >= w) continue;
+          const double al = al_row(vr)[vc + 1];
+          if (al == 0.0) continue;
+          const double pt = potk[k];
+          acc_burn += al * pt;
+          // dpot/dp_base = pot / p_base, dpot/dalpha_w1 = pot V, dpot/dalpha_w2 = pot V (cos - 1),
+          // dpot/dalpha_s = pot S; S of direction k = the source's own record of k + 4, negated
+          const double S_k = -static_cast<double>(sown[(k + 4) & 7]);
+          const double ab = al * bu;
+          gp += ab * (pt * d.inv_p_base);
+          gw1 += ab * pt * V;
+          gw2 += ab * pt * V * align[k];
+          gs += ab * pt * S_k;
+        }
+      }
+      d.A_burn_o[base + static_cast<size_t>(rs) * w + c] = acc_burn;  // A_bd is unchanged
+    }
+  }
+  double g6[6] = {gp, gw1, gw2, gs, g_gamma, g_pc};
+  block_sum_n<6>(g6, red);
+  if (threadIdx.x == 0) {
+    double* acc = d.acc + (static_cast<size_t>(env) * gridDim.x + blockIdx.x) * 8;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) acc[k] += g6[k];
+  }
+}
+
+
+bool det_stream_ok(const DetArgs& d) {  // terrain layers, whole rows of <= 128 cells, 16-byte rows
+  return !d.fac_pb && d.s.fuel && d.s.slope32 && d.s.w <= kSW && (d.s.w % 16) == 0;
+}
+
+size_t det_stream_smem() { return kSlots * sizeof(StreamRow) + kAl * (kSW + 2) * sizeof(double); }
+
+int det_blocks_per_env_stream(int h) { return (h + kSB - 1) / kSB; }
+
+// SpreadTables<double>::pot of terrain layers built on the device (engine.hpp:88-107 /
+// build_terrain_tables): pot[t][cell][k] = (source(class) kappa_wind_t(k)) exp(alpha_s S[g][cell][k])
+// with S the cached config-free slopes (host atan, once per terrain), source the palette's fp64
+// value and exp the restatement of the reference's libm exp (ember_exp.cuh): bit-identical to the
+// host-built table, so a config change (every calibration iteration) needs no host rebuild.
+__device__ const uint64_t kExpTabDev[256] = EBL_EXP_TAB_INIT;
+
+__global__ void k_det_tables_terrain(const double* __restrict__ S, const uint8_t* __restrict__ fuel,
+                                     const double* __restrict__ pal64, const double* __restrict__ kw64, double alpha_s,
+                                     int n_tables, size_t ncell, size_t grid_stride, int wind_stride, double* pot) {
+  __shared__ uint64_t tab[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = kExpTabDev[i];
+  __syncthreads();
+  const size_t total = static_cast<size_t>(n_tables) * ncell * 8;
+  for (size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < total;
+       j += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t tcell = j >> 3;
+    const int k = static_cast<int>(j & 7);
+    const int t = static_cast<int>(tcell / ncell);
+    const size_t cell = tcell - static_cast<size_t>(t) * ncell;
+    const size_t g = grid_stride ? static_cast<size_t>(t) : 0;  // grid of table t
+    const double src = pal64[fuel[g * ncell + cell]];
+    const double kw = kw64[static_cast<size_t>(t) * wind_stride * 8 + k];
+    bool exact = true;
+    const double ks = exp_glibc(__dmul_rn(alpha_s, S[(g * ncell + cell) * 8 + k]), tab, &exact);
+    pot[j] = __dmul_rn(__dmul_rn(src, kw), ks);
+  }
+}
+
+cudaError_t launch_det_tables_terrain(const double* S, const uint8_t* fuel, const double* pal64, const double* kw64,
+                                      double alpha_s, int n_tables, size_t ncell, size_t grid_stride, int wind_stride,
+                                      double* pot, cudaStream_t s) {
+  const size_t total = static_cast<size_t>(n_tables) * ncell * 8;
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 8));
+  k_det_tables_terrain<<<blocks, 256, 0, s>>>(S, fuel, pal64, kw64, alpha_s, n_tables, ncell, grid_stride, wind_stride,
+                                              pot);
+  return cudaGetLastError();
+}
+
 int det_blocks_per_env(int h, int w) {
   return ((w + kBackTx - 1) / kBackTx) * ((h + kBackRows - 1) / kBackRows);
 }
@@ -497,6 +737,13 @@ cudaError_t launch_det_loss(const DetArgs& d, cudaStream_t s) {
 cudaError_t launch_det_backward(const DetArgs& d, int t, cudaStream_t s) {
   const int ncell = d.s.h * d.s.w;
   const dim3 grid((ncell + 255) / 256, d.s.n_envs);
+  if (EBL_DET_STREAM && det_stream_ok(d) && d.A_un_o) {
+    const size_t sm = det_stream_smem();
+    cudaError_t e = cudaFuncSetAttribute(k_det_back_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    if (e != cudaSuccess) return e;
+    k_det_back_stream<<<dim3(det_blocks_per_env_stream(d.s.h), d.s.n_envs), kSW, sm, s>>>(d, t);
+    return cudaGetLastError();
+  }
   if (d.A_un_o) {  // fused, double-buffered adjoints
     const dim3 g(det_blocks_per_env(d.s.h, d.s.w), d.s.n_envs);
     if (d.fac_pb) k_det_back<2><<<g, kBackTx * kBackTy, 0, s>>>(d, t);  // general layers
@@ -510,7 +757,9 @@ cudaError_t launch_det_backward(const DetArgs& d, int t, cudaStream_t s) {
 
 cudaError_t launch_det_reduce(const DetArgs& d, cudaStream_t s) {
   const int ncell = d.s.h * d.s.w;
-  k_det_reduce<<<d.s.n_envs, 32, 0, s>>>(d, d.A_un_o ? det_blocks_per_env(d.s.h, d.s.w) : (ncell + 255) / 256);
+  const int bpe = EBL_DET_STREAM && det_stream_ok(d) && d.A_un_o ? det_blocks_per_env_stream(d.s.h)
+                  : d.A_un_o ? det_blocks_per_env(d.s.h, d.s.w) : (ncell + 255) / 256;
+  k_det_reduce<<<d.s.n_envs, 32, 0, s>>>(d, bpe);
   return cudaGetLastError();
 }
 

@@ -132,6 +132,30 @@ void build_terrain_tables(int n_tables, int h, int w, const uint8_t* fuel, const
   }
 }
 
+void build_terrain_slopes64(int n_grids, int h, int w, const float* elev, size_t grid_stride, double cellsize,
+                            double* S) {
+  const size_t n = static_cast<size_t>(h) * w;
+  const double dist[2] = {cellsize * 1.0, cellsize * 1.41421356237309504880};  // geodata.cpp:222-223
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int g = 0; g < n_grids; ++g) {
+    const float* z = elev + g * grid_stride;
+    double* out = S + g * n * 8;
+    for (int r = 0; r < h; ++r)
+      for (int col = 0; col < w; ++col) {
+        const size_t i = static_cast<size_t>(r) * w + col;
+        for (int k = 0; k < 8; ++k) {
+          const int nr = r + kDy[k], nc = col + kDx[k];
+          double s = 0.0;  // exactly the expression of build_terrain_tables
+          if (nr >= 0 && nr < h && nc >= 0 && nc < w) {
+            const double dz = static_cast<double>(z[static_cast<size_t>(nr) * w + nc]) - static_cast<double>(z[i]);
+            if (dz == dz) s = std::atan(dz / dist[k & 1]);
+          }
+          out[i * 8 + k] = s;
+        }
+      }
+  }
+}
+
 uint64_t continue_threshold(double pc) {
   if (!(pc > 0.0)) return 0;  // also NaN: u < NaN is false
   if (pc >= 1.0) return 1ull << 53;

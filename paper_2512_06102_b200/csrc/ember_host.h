@@ -32,6 +32,10 @@ void build_terrain_tables(int n_tables, int h, int w, const uint8_t* fuel, const
                           size_t grid_stride, const double* class_veg, const double* class_den,
                           double cellsize, const double* wind_speed, const double* wind_dir,
                           int wind_stride, const Cfg6& c, double* pot, double* gamma);
+// The config-free part of build_terrain_tables: S[g][cell][k] = atan(dz / dist) of every grid (0
+// toward out-of-bounds or nodata neighbours), the value whose exp(alpha_s S) the table holds.
+void build_terrain_slopes64(int n_grids, int h, int w, const float* elev, size_t grid_stride, double cellsize,
+                            double* S);
 // ceil(p_continue * 2^53): a Burning cell survives iff (word >> 11) < this.
 uint64_t continue_threshold(double p_continue);
 

@@ -29,6 +29,9 @@ bool warp_fits(int h, int w);
 cudaError_t launch_step_warp(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s);
 
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s);
+cudaError_t launch_det_tables_terrain(const double* S, const uint8_t* fuel, const double* pal64, const double* kw64,
+                                      double alpha_s, int n_tables, size_t ncell, size_t grid_stride, int wind_stride,
+                                      double* pot, cudaStream_t s);
 cudaError_t launch_det_loss(const DetArgs& d, cudaStream_t s);
 cudaError_t launch_det_from_fire(const uint8_t* st, double* un, double* bu, double* bd, size_t n,
                                  cudaStream_t s);
