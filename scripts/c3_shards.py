@@ -1,0 +1,58 @@
+"""C3 (16384^2 x 500 steps) as G fused row shards on ONE device vs the unsharded batch: wall time of
+step(500) + sync (launches of all shards issued from one host thread), the share of tile launches
+actually stepped (quiet tiles skipped), and bitwise equality of the final layers.  All shards share
+one GPU, so this measures the sharding overhead (halo exchange, exposed boundary tiles), not
+multi-GPU scaling.   python scripts/c3_shards.py [size] [steps]"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2512_06102_b200 as eb  # noqa: E402
+from paper_2512_06102_b200.sharded import ShardedLandscape  # noqa: E402
+
+size = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 500
+b = eb.Batch(1, size, size)
+b.synth_terrain(0)
+b.set_wind([6.0], [0.0])
+b.synth_ignitions(0, 64)
+init = b.get_state()[0]
+fc, el = b.get_terrain()
+ms = []
+for rep in range(4):
+    b.set_state(init)
+    b.set_key(0, 0)
+    b.diag(reset=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    b.step(steps)
+    b.sync()
+    ms.append(1e3 * (time.perf_counter() - t0))
+d = b.diag()
+ref = b.get_state()[0]
+print(f"unsharded: {np.median(ms[1:]):.2f} ms  tiles stepped {d['tiles_processed'] / d['tiles_launched']:.3f}", flush=True)
+b.close()
+_, veg, den = eb.worldcover_palette()
+t = eb.Terrain(fc, el, np.array([6.0]), np.array([0.0]), veg, den)
+for g in (1, 2, 4, 8):
+    sh = ShardedLandscape(t, g, fused=True)
+    ms = []
+    for rep in range(4):
+        sh.set_state(init)
+        sh.set_key(0, 0, 0)
+        for bb in sh.batches:
+            bb.diag(reset=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sh.step(steps)
+        sh.sync()
+        ms.append(1e3 * (time.perf_counter() - t0))
+    run = sum(bb.diag()["tiles_processed"] for bb in sh.batches)
+    tot = sum(bb.diag()["tiles_launched"] for bb in sh.batches)
+    ok = np.array_equal(sh.get_state(), ref)
+    print(f"G={g} fused: {np.median(ms[1:]):.2f} ms  tiles stepped {run / max(tot, 1):.3f}  equal={ok}", flush=True)
+    del sh

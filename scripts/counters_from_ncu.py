@@ -1,0 +1,54 @@
+"""Writes profiles/ncu_counters.json (the per-launch counters bench.py's roofline reads) from ncu
+--set full captures of this build:
+    python scripts/counters_from_ncu.py --c1 gpurun_out/prof_r02_c1.ncu-rep [--c2 prof_c2.ncu-rep]"""
+import argparse
+import csv
+import io
+import json
+import os
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    d = {}
+    for i, name in enumerate(rows[0]):
+        d[name] = (rows[2][i], rows[1][i])
+    return d
+
+
+def num(v, unit):
+    x = float(v)
+    return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--c1")
+    ap.add_argument("--c2")
+    a = ap.parse_args()
+    path = os.path.join(ROOT, "profiles", "ncu_counters.json")
+    out = json.load(open(path)) if os.path.exists(path) else {}
+    if a.c1:
+        r = raw(a.c1)
+        out["k_step_warp:1024x128x128x200"] = {
+            "inst_executed_per_launch": num(*r["smsp__inst_executed.sum"]),
+            "dram_bytes_per_launch": num(*r["dram__bytes_read.sum"]) + num(*r["dram__bytes_write.sum"]),
+            "duration_us_cold": num(*r["gpu__time_duration.sum"]),
+            "source": os.path.basename(a.c1)}
+    if a.c2:
+        r = raw(a.c2)
+        out["k_rl_tanker_warp:16384x64x64x256"] = {
+            "dram_bytes_per_launch": num(*r["dram__bytes_read.sum"]) + num(*r["dram__bytes_write.sum"]),
+            "inst_executed_per_launch": num(*r["smsp__inst_executed.sum"]),
+            "source": os.path.basename(a.c2)}
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,9 +1,12 @@
-# Evidence run (under gpurun from the repo root): the bench lines of every config (ours + the
-# reference arm), the C1 launch list + full capture of the dominant kernel, C2/C3/C4 captures.
-# Every profiled command first runs plain (&& ncu) so a failing program is never profiled.
+# Evidence run (under gpurun from the repo root): the GPU suite + smoke, the bench lines of every
+# config (ours + the reference arm), the C1 launch list + full capture of the dominant kernel,
+# C2 / C4 captures, the C3 shard measurement.  Every profiled command first runs plain (&& ncu).
 cd "${GRAFT_REPO_ROOT:-.}"
 TAG=${TAG:-r02}
 mkdir -p gpurun_out
+python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu_${TAG}.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG}.log 2>&1
+python bench.py > gpurun_out/bench_${TAG}_default.log 2>&1
 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_${TAG}_c1.log 2>&1
 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_${TAG}_c1_ref.log 2>&1
 for c in C0 C2 C3 C4; do
@@ -17,6 +20,7 @@ C2="python bench.py --config C2 --steps 1 --warmup 3 --no-cpu-baseline"
 $C2 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_rl_tanker_warp -s 3 -c 1 -o gpurun_out/prof_${TAG}_c2 $C2 > gpurun_out/ncu_c2.log 2>&1
 C4="python bench.py --config C4 --steps 1 --warmup 3 --no-cpu-baseline"
 $C4 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_c4.csv $C4 > gpurun_out/ncu_launches_c4.log 2>&1
-$C4 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_det_back -s 450 -c 1 -o gpurun_out/prof_${TAG}_c4back $C4 > gpurun_out/ncu_c4back.log 2>&1
+$C4 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_det_back_stream -s 450 -c 1 -o gpurun_out/prof_${TAG}_c4back $C4 > gpurun_out/ncu_c4back.log 2>&1
 $C4 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_det_forward -s 450 -c 1 -o gpurun_out/prof_${TAG}_c4fwd $C4 > gpurun_out/ncu_c4fwd.log 2>&1
+python scripts/c3_shards.py > gpurun_out/c3_shards_${TAG}.log 2>&1
 echo done
