@@ -109,6 +109,10 @@ struct ebl_batch {
   // reads, and halo-row writes outside the band drops them (check_batch / check_sync).
   mutable int tf_carry_tiles = -1;
   int tf_carry_par = 0, tf_carry_th = 0, tf_carry_tw = 0;
+  // work-list runs (C3-like single landscapes): in-place tile records, dedup stamps, two lists and
+  // their counters [count0, count1, cursor]
+  DevBuf<int32_t> trec, tqueued, tlist[2], tcount;
+  int32_t list_stamp = 0;
   DevBuf<char> snap_text, snap_meta;  // snapshot rendering staging (grow-only)
   DevBuf<unsigned long long> snap_off;
   bool pot32t_valid = false;
@@ -976,6 +980,8 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
     // previous call when nothing but stepping / reads / halo-row writes happened in between
     int tf_par = b->tf_carry_par, tf_tiles = b->tf_carry_tiles;
     b->tf_carry_tiles = -1;
+    int list_launch = -1;  // work-list run of this call: index of the launch, -1 = grid launches
+    size_t list_tiles = 0;
     for (int done = 0; done < n_steps;) {
       ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps - done, force_tiles, 0, b->n_envs, 1);
       if (b->tile_h > 0) {  // test hook: explicit tiling
@@ -1001,7 +1007,43 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
         const bool exposed = a.keep_lo > 0 || a.keep_hi < b->h;  // halo rows of a row shard
         const bool tiled = tx * ty > 1 && g.halo_rows <= g.tile_h && g.halo_cols <= g.tile_w && !a.traj &&
                            use_warp(b) && (!exposed || g.tile_h >= 3 * g.halo_rows);
-        if (tiled) {
+        // work-list run: the whole call on one unsharded batch with no records carried in; after the
+        // first (grid) launch only the tiles the skip rule would not skip are launched, on persistent
+        // CTAs (EBL_WORK_LIST=0 keeps grid launches with per-CTA skipping)
+        static const bool work_list = [] {
+          const char* e = std::getenv("EBL_WORK_LIST");
+          return !e || std::atoi(e) != 0;
+        }();
+        if (tiled && work_list && !exposed && (list_launch >= 0 || (tf_tiles < 0 && n_steps > g.n_steps))) {
+          const size_t nt = static_cast<size_t>(tx) * ty * b->n_envs;
+          if (b->trec.n < nt * 4 || b->tqueued.n < nt) {
+            EBL_CUDA(b->trec.alloc(nt * 4));
+            EBL_CUDA(b->tqueued.alloc(nt));
+            EBL_CUDA(cudaMemsetAsync(b->tqueued.p, 0, nt * sizeof(int32_t), b->stream));
+            b->list_stamp = 0;
+          }
+          for (auto& l : b->tlist)
+            if (l.n < nt) EBL_CUDA(l.alloc(nt));
+          if (b->tcount.n < 3) EBL_CUDA(b->tcount.alloc(3));
+          list_launch += 1;
+          list_tiles = nt;
+          const int cur_l = list_launch & 1, nxt = cur_l ^ 1;
+          a.list_mode = list_launch == 0 ? 1 : 2;
+          a.trec = b->trec.p;
+          a.queued = b->tqueued.p;
+          a.list_stamp = ++b->list_stamp;
+          a.next_list = b->tlist[nxt].p;
+          a.next_count = b->tcount.p + nxt;
+          a.tile_list = b->tlist[cur_l].p;
+          a.tile_count = b->tcount.p + cur_l;
+          a.list_cursor = b->tcount.p + 2;
+          a.tiles_x = tx;
+          a.tiles_y = ty;
+          a.tiles_total = static_cast<int>(nt);
+          EBL_CUDA(cudaMemsetAsync(b->tcount.p + nxt, 0, sizeof(int32_t), b->stream));
+          EBL_CUDA(cudaMemsetAsync(b->tcount.p + 2, 0, sizeof(int32_t), b->stream));
+          tf_tiles = -1;
+        } else if (tiled) {
           const size_t n = static_cast<size_t>(tx) * ty * b->n_envs * 4;
           for (auto& f : b->tflags)
             if (f.n < n) {
@@ -1024,6 +1066,11 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
       b->step += g.n_steps;
       b->launches += 1;
       done += g.n_steps;
+      if (list_launch >= 0 && done == n_steps) {  // U/B/X of every tile from the in-place records
+        EBL_CUDA(ebl::launch_tile_counts(b->trec.p, b->n_envs, static_cast<int>(list_tiles / b->n_envs),
+                                         b->counts.p, b->stream));
+        b->launches += 1;
+      }
     }
     b->tf_carry_tiles = tf_tiles;
     b->tf_carry_par = tf_par;

@@ -67,6 +67,20 @@ struct StepArgs {
   // the producing kernel's store
   int store_lo, store_hi;
   int keep_lo, keep_hi;           // rows outside: halo rows written by neighbour shards (exposed tiles)
+  // work-list runs of halo tiles (one batch, ebl_step_batch): list_mode 1 = grid launch, 2 = the
+  // launch runs the tiles of tile_list[0 .. *tile_count) on persistent CTAs (list_cursor: the
+  // claim counter); both keep the tile records in place (trec, int4 per tile) and append the next
+  // launch's tiles to next_list / next_count, deduplicated by stamping queued[tile] = list_stamp
+  int list_mode;
+  int32_t* trec;
+  int32_t* queued;
+  int32_t list_stamp;
+  int32_t* next_list;
+  int32_t* next_count;
+  const int32_t* tile_list;
+  const int32_t* tile_count;
+  int32_t* list_cursor;
+  int tiles_x, tiles_y, tiles_total;
   int n_peers;
   uint8_t* peer_out[2];
   int peer_lo[2], peer_hi[2], peer_dst[2];

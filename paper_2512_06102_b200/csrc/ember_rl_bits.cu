@@ -300,7 +300,23 @@ cudaError_t launch_rl_tanker_bits(const RlArgs& g, int mode, cudaStream_t s) {
 // step needs two block barriers (after the drop, at the end) instead of five: every thread draws
 // the action itself, and the Burning count is kept incrementally (burning(t+1) = burning(t) -
 // extinguished - burnt out + ignited) instead of a popc pass.
+#ifndef EBL_RL_FAST
+#define EBL_RL_FAST 1  // the branch-free decide pass in the tanker kernel
+#endif
 namespace {
+
+// the shallower n-th set bit of the warp kernel (ember_warp.cu)
+__device__ __forceinline__ int nth_set_bit_lut32(uint32_t v, int q, const uint32_t* lut) {
+  uint32_t c = v - ((v >> 1) & 0x55555555u);
+  c = (c & 0x33333333u) + ((c >> 2) & 0x33333333u);
+  c = (c + (c >> 4)) & 0x0f0f0f0fu;
+  const uint32_t cum = c * 0x01010101u;
+  const uint32_t qq = static_cast<uint32_t>(q);
+  const int k = (qq >= (cum & 0xffu)) + (qq >= ((cum >> 8) & 0xffu)) + (qq >= ((cum >> 16) & 0xffu));
+  const int before = k ? static_cast<int>((cum << 8 >> (8 * k)) & 0xffu) : 0;
+  const uint32_t byte = (v >> (8 * k)) & 0xffu;
+  return 8 * k + static_cast<int>((lut[byte] >> (3 * (q - before))) & 7u);
+}
 
 __device__ __forceinline__ int nth_set_bit32(uint32_t v, int q) {
   int pos = 0;
@@ -328,6 +344,9 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
   __shared__ float s_pal[kTer ? 512 : 1];
   __shared__ float s_kw[8];
   __shared__ float s_srckw[kTer ? 32 * 8 : 1];
+  // the branch-free decide pass of k_step_warp (even compile-time words per row, pot32t rows)
+  constexpr bool kFast = EBL_RL_FAST && kTer && DIMC != 0 && ((DIMC + 31) / 32) % 2 == 0;
+  __shared__ uint32_t s_nth[kFast ? 256 : 1];
 
   const StepArgs& a = g.s;
   const int env = blockIdx.x;
@@ -336,7 +355,7 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
   const int S = plane_stride(wpr);
   auto ro = [S](int R) { return R * S + (R >> 2); };  // conflict-free rows 4 apart (ember_warp.cu)
   const int PH = ro(H + 2) + 1;
-  uint32_t* const Bp0 = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* const Bp0 = reinterpret_cast<uint32_t*>(smem) + 4;  // 4 zero guard words before the planes
   uint32_t* const Bp1 = Bp0 + PH;
   uint32_t* const X = Bp1 + PH;
   uint32_t* const WET = X + PH;
@@ -347,9 +366,20 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
 
   uint8_t* st = g.state + static_cast<size_t>(env) * n;
   uint8_t* wt = g.wet + static_cast<size_t>(env) * n;
-  for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
-    Bp0[i] = Bp1[i] = 0u;
-    Bp0[ro(H + 1) + i] = Bp1[ro(H + 1) + i] = 0u;
+  if constexpr (kFast) {  // guard, padding words and padding rows of both B planes stay zero
+    for (int i = threadIdx.x; i < 2 * PH + 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+      uint32_t e = 0u;
+      for (int bit = 0, cnt = 0; bit < 8; ++bit)
+        if ((i >> bit) & 1) e |= static_cast<uint32_t>(bit) << (3 * cnt++);
+      s_nth[i] = e;
+    }
+    __syncthreads();
+  } else {
+    for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
+      Bp0[i] = Bp1[i] = 0u;
+      Bp0[ro(H + 1) + i] = Bp1[ro(H + 1) + i] = 0u;
+    }
   }
   if (threadIdx.x < 2) s_newly[threadIdx.x] = s_gone[threadIdx.x] = 0;
   if (threadIdx.x == 0) s_burning[0] = 0;
@@ -515,7 +545,38 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
             wv = ar[++jj];
           }
         }
-        const int cc = 32 * jj + nth_set_bit32(wv, q);
+        int cc;
+        if constexpr (kFast) cc = 32 * jj + nth_set_bit_lut32(wv, q, s_nth);
+        else cc = 32 * jj + nth_set_bit32(wv, q);
+        if (kFast && use_tab) {  // one branch-free path for burning and candidate cells (ember_warp.cu)
+          const float4* tp = reinterpret_cast<const float4*>(a.pot32t + static_cast<size_t>(env) * a.pot32t_stride) +
+                             2 * (rr * W + cc);
+          const float4 T0 = __ldg(tp), T1 = __ldg(tp + 1);
+          const int j = cc >> 5, b = cc & 31;
+          const uint32_t bit = 1u << b;
+          const int wi = ro(rr + 1) + j;
+          const uint64_t m = cell_bits53(prefix, static_cast<uint64_t>(rr * W + cc), 0);
+          auto win = [&](const uint32_t* row) -> uint32_t {
+            const uint32_t lo = row[j - 1], md = row[j], hi = row[j + 1];
+            return (b > 0 ? __funnelshift_r(md, hi, b - 1) : __funnelshift_r(lo, md, 31)) & 7u;
+          };
+          const uint32_t midw = win(B + ro(rr + 1)), dnw = win(B + ro(rr)), upw = win(B + ro(rr + 2));
+          const bool burning = midw & 2u;
+          const uint32_t nb = burning ? 0u
+                                      : (midw & 1u) | (dnw << 1) | ((midw >> 2) << 4) | ((upw >> 2) << 5) |
+                                            ((upw & 2u) << 5) | ((upw & 1u) << 7);
+          const bool ig = ignite_pot_fast(a, env, 0, T0, T1, W, rr, cc, nb, m, dg);
+          if (burning && m >= a.pc_thr) {
+            atomicAnd(Bn + wi, ~bit);
+            atomicOr(X + ro(rr) + j, bit);
+            ++burnt;
+          }
+          if (ig) {
+            atomicOr(Bn + wi, bit);
+            ++newly;
+          }
+          continue;
+        }
         CellRec rec{};
         if (use_tab) {  // the candidate's 8 terms of gamma * lambda (pot32t)
           const float4* tp = reinterpret_cast<const float4*>(a.pot32t + static_cast<size_t>(env) * a.pot32t_stride) +
@@ -719,7 +780,7 @@ cudaError_t launch_rl_bits_to_bytes(const uint32_t* bits, uint8_t* state, uint8_
 size_t rl_warp_smem_bytes(int h, int w) {
   const size_t S = plane_stride((w + 31) / 32);
   const size_t R = static_cast<size_t>(h) + 2;
-  return 5 * (R * S + (R >> 2) + 1) * sizeof(uint32_t);  // B x2, X, WET, ACT (ro() layout)
+  return 5 * (R * S + (R >> 2) + 1) * sizeof(uint32_t) + 16;  // B x2, X, WET, ACT (ro() layout) + guard words
 }
 
 template <int MODE, int DIMC>

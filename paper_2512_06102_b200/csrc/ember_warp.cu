@@ -17,6 +17,7 @@
 // per cell; the RNG is counter-based).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "ember_bits.cuh"
@@ -108,12 +109,13 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
   constexpr bool kFast = EBL_WARP_FAST && EBL_WARP_MICRO && kTer && WPRC != 0 && (WPRC & 1) == 0;
   __shared__ uint32_t s_nth[kFast ? 256 : 1];
 
-  // region of this CTA: one tile of one env's layer plus its light-cone halo (the whole env for
-  // resident launches); H x RW region cells, layer BH x W
-  const int env = blockIdx.z;
+  // one region: one tile of one env's layer plus its light-cone halo (the whole env for resident
+  // launches); H x RW region cells, layer BH x W.  Grid launches run the CTA's own region, work-list
+  // launches (a.list_mode == 2) loop over the listed tiles (below).
+  auto region = [&](const int env, const int bxi, const int byi, const int ntx, const int nty) {
   const int n_steps = g.n_steps;
   const int BH = DIMC ? DIMC : a.h, W = DIMC ? DIMC : a.w;
-  const int r0 = DIMC ? 0 : blockIdx.y * g.tile_h, c0 = DIMC ? 0 : blockIdx.x * g.tile_w;  // c0 % 32 == 0
+  const int r0 = DIMC ? 0 : byi * g.tile_h, c0 = DIMC ? 0 : bxi * g.tile_w;  // c0 % 32 == 0
   const int R0 = DIMC ? 0 : max(0, r0 - g.halo_rows), R1 = DIMC ? BH : min(BH, r0 + g.tile_h + g.halo_rows);
   const int C0 = DIMC ? 0 : max(0, c0 - g.halo_cols), C1 = DIMC ? W : min(W, c0 + g.tile_w + g.halo_cols);
   const int H = R1 - R0, RW = C1 - C0;
@@ -140,8 +142,11 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
   // A tile whose own and 8 neighbours' output tiles had no burning cell after the previous launch
   // has a quiet region (the halo lies in the neighbours); after two quiet launches both layer
   // buffers hold its (canonical) bytes, so there is nothing to load, step or store.
-  const size_t tile_id = (static_cast<size_t>(env) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  const size_t tile_id = (static_cast<size_t>(env) * nty + byi) * ntx + bxi;
   int streak0 = 0;
+  // work-list launches (C3, one batch): the in-place record of this tile gives its quiet streak;
+  // listed tiles always run (the list holds exactly the tiles the skip rule would not skip)
+  if (a.list_mode == 2) streak0 = (reinterpret_cast<const int4*>(a.trec)[tile_id].x >> 1) & 3;
   const int4* const tf_in = reinterpret_cast<const int4*>(a.tflag_in);
   int4* const tf_out = reinterpret_cast<int4*>(a.tflag_out);
   if (tf_in) {
@@ -151,9 +156,9 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
       bool quiet = true;
       for (int dy = -1; dy <= 1; ++dy)
         for (int dx = -1; dx <= 1; ++dx) {
-          const int ty = static_cast<int>(blockIdx.y) + dy, tx = static_cast<int>(blockIdx.x) + dx;
-          if (ty >= 0 && ty < static_cast<int>(gridDim.y) && tx >= 0 && tx < static_cast<int>(gridDim.x))
-            quiet &= !(tf_in[(static_cast<size_t>(env) * gridDim.y + ty) * gridDim.x + tx].x & 1);
+          const int ty = byi + dy, tx = bxi + dx;
+          if (ty >= 0 && ty < nty && tx >= 0 && tx < ntx)
+            quiet &= !(tf_in[(static_cast<size_t>(env) * nty + ty) * ntx + tx].x & 1);
         }
       // tiles holding halo rows a neighbour shard writes are never skipped outright (their
       // records do not see those writes); DESIGN.md §6 gives the distance argument that keeps
@@ -175,9 +180,9 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
     }
     streak0 = (tf_in[tile_id].x >> 1) & 3;
   }
-  if (threadIdx.x == 0 && a.diag) {  // tile statistics: processed / launched CTAs
+  if (threadIdx.x == 0 && a.diag) {  // tile statistics: processed / launched regions
     atomicAdd(a.diag + 2, 1ull);
-    atomicAdd(a.diag + 3, 1ull);
+    if (a.list_mode != 2) atomicAdd(a.diag + 3, 1ull);
   }
   // ---- load ----------------------------------------------------------------------------------
   if constexpr (kFast) {  // guard words, padding words and padding rows of both B planes: zero
@@ -596,7 +601,7 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
   for (int p = 0; p < a.n_peers; ++p)  // fused halo exchange: owned rows straight into the neighbour
     store_tile(Bs, a.peer_out[p], nullptr, a.peer_lo[p], a.peer_hi[p], a.peer_dst[p] - a.peer_lo[p]);
   int cu = c3[0], cb = c3[1], cx = c3[2];
-  if (!a.counts && !a.tflag_out) return;
+  if (!a.counts && !a.tflag_out && !a.list_mode) return;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     cu += __shfl_xor_sync(0xffffffffu, cu, o);
@@ -611,13 +616,52 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
     atomicAdd(&s_newly, newly);
   }
   __syncthreads();
-  if (a.counts) {
-    if (threadIdx.x < 3) atomicAdd(a.counts + env * 4 + threadIdx.x, s_cnt[threadIdx.x]);
+  if (a.counts) {  // (work-list runs: U/B/X summed from the records after the call, k_tile_counts)
+    if (threadIdx.x < 3 && !a.list_mode) atomicAdd(a.counts + env * 4 + threadIdx.x, s_cnt[threadIdx.x]);
     if (threadIdx.x == 3) atomicAdd(a.counts + env * 4 + 3, s_newly);
   }
   if (tf_out && threadIdx.x == 0) {
     const int streak = n_run == 0 ? min(streak0 + 1, 2) : 0;  // output == input this launch
     tf_out[tile_id] = make_int4((s_cnt[1] > 0 ? 1 : 0) | (streak << 1), s_cnt[0], s_cnt[1], s_cnt[2]);
+  }
+  if (a.list_mode && threadIdx.x == 0) {
+    // record in place, then the next launch's work list: a tile with a burning cell makes its 3x3
+    // neighbourhood run (the light cone of one launch stays within the neighbours), a tile whose
+    // buffers are not both canonical yet (streak < 2) makes itself run -- exactly the tiles the
+    // grid form's skip rule would not skip (tiles outside the list keep a quiet record)
+    const int streak = n_run == 0 ? min(streak0 + 1, 2) : 0;
+    const bool burning = s_cnt[1] > 0;
+    reinterpret_cast<int4*>(a.trec)[tile_id] = make_int4((burning ? 1 : 0) | (streak << 1), s_cnt[0], s_cnt[1], s_cnt[2]);
+    auto enqueue = [&](int tx, int ty) {
+      const size_t id = (static_cast<size_t>(env) * nty + ty) * ntx + tx;
+      if (atomicExch(a.queued + id, a.list_stamp) != a.list_stamp) a.next_list[atomicAdd(a.next_count, 1)] = static_cast<int>(id);
+    };
+    if (burning) {
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx)
+          if (byi + dy >= 0 && byi + dy < nty && bxi + dx >= 0 && bxi + dx < ntx) enqueue(bxi + dx, byi + dy);
+    } else if (streak < 2) {
+      enqueue(bxi, byi);
+    }
+  }
+  };  // region
+
+  if (a.list_mode == 2) {  // work list of this launch: persistent CTAs take tiles until it runs out
+    __shared__ int s_item;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && a.diag) atomicAdd(a.diag + 3, static_cast<unsigned long long>(a.tiles_total));
+    for (;;) {
+      __syncthreads();  // the previous region's shared state is consumed
+      if (threadIdx.x == 0) s_item = atomicAdd(a.list_cursor, 1);
+      __syncthreads();
+      const int item = s_item;
+      if (item >= *a.tile_count) break;
+      const int tile = a.tile_list[item];
+      const int bx = tile % a.tiles_x, rest = tile / a.tiles_x;
+      region(rest / a.tiles_y, bx, rest % a.tiles_y, a.tiles_x, a.tiles_y);
+    }
+  } else {
+    region(static_cast<int>(blockIdx.z), static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.y),
+           static_cast<int>(gridDim.x), static_cast<int>(gridDim.y));
   }
 }
 
@@ -626,12 +670,48 @@ cudaError_t launch_wp(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStre
   cudaError_t e = cudaFuncSetAttribute(k_step_warp<MODE, WPRC, DIMC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(sm));
   if (e != cudaSuccess) return e;
+  if (a.list_mode == 2) {  // persistent: one wave of CTAs over the work list
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_warp<MODE, WPRC, DIMC>, kWpThreads, sm);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int ctas = std::max(1, std::min(a.tiles_total, std::max(1, per_sm) * sms));
+    k_step_warp<MODE, WPRC, DIMC><<<ctas, kWpThreads, sm, s>>>(a, g);
+    return cudaGetLastError();
+  }
   const dim3 grid((a.w + g.tile_w - 1) / g.tile_w, (a.h + g.tile_h - 1) / g.tile_h, a.n_envs);
   k_step_warp<MODE, WPRC, DIMC><<<grid, kWpThreads, sm, s>>>(a, g);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+// counts[env][0..2] = the U/B/X of every tile's record (work-list runs: tiles not in the last
+// list kept their recorded counts); counts[env][3] (ignited in the last step) is left as is
+__global__ void k_tile_counts(const int4* __restrict__ trec, int tiles_per_env, int32_t* counts) {
+  __shared__ int s[3];
+  if (threadIdx.x < 3) s[threadIdx.x] = 0;
+  __syncthreads();
+  int u = 0, bb = 0, x = 0;
+  for (int i = threadIdx.x; i < tiles_per_env; i += blockDim.x) {
+    const int4 r = trec[static_cast<size_t>(blockIdx.x) * tiles_per_env + i];
+    u += r.y;
+    bb += r.z;
+    x += r.w;
+  }
+  atomicAdd(&s[0], u);
+  atomicAdd(&s[1], bb);
+  atomicAdd(&s[2], x);
+  __syncthreads();
+  if (threadIdx.x < 3) counts[blockIdx.x * 4 + threadIdx.x] = s[threadIdx.x];
+}
+
+cudaError_t launch_tile_counts(const int32_t* trec, int n_envs, int tiles_per_env, int32_t* counts, cudaStream_t s) {
+  k_tile_counts<<<n_envs, 256, 0, s>>>(reinterpret_cast<const int4*>(trec), tiles_per_env, counts);
+  return cudaGetLastError();
+}
 
 size_t warp_smem_bytes(int h, int w) {
   const size_t S = plane_stride((w + 31) / 32);
