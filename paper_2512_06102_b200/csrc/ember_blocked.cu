@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <algorithm>
 
 #include "ember_bits.cuh"
 #include "ember_device.cuh"
@@ -553,10 +555,19 @@ BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_o
     g.halo_cols = 0;
     g.n_steps = n_steps;
   } else {
+    // tile geometry of halo-tiled runs (EBL_TILE_H / EBL_TILE_W override, multiples of 32 columns)
+    static const int tile_h_env = [] {
+      const char* e = std::getenv("EBL_TILE_H");
+      return e ? std::max(1, std::atoi(e)) : kBlockTileH;
+    }();
+    static const int tile_w_env = [] {
+      const char* e = std::getenv("EBL_TILE_W");
+      return e ? std::max(32, std::atoi(e) / 32 * 32) : kBlockTileW;
+    }();
     g.halo_rows = kBlockHalo;
-    g.tile_w = w <= kBlockTileW + 64 ? ((w + 31) / 32) * 32 : kBlockTileW;
+    g.tile_w = w <= tile_w_env + 64 ? ((w + 31) / 32) * 32 : tile_w_env;
     g.halo_cols = g.tile_w >= w ? 0 : 32;
-    g.tile_h = kBlockTileH;
+    g.tile_h = tile_h_env;
     if (g.tile_h >= buf_h) {
       g.tile_h = buf_h;
       g.halo_rows = 0;

@@ -156,6 +156,10 @@ __global__ void k_det_loss(DetArgs d) {
   const double eps = 1e-6;  // LossConfig::bce_epsilon
   double bce = 0.0, mse = 0.0;
   for (int i = threadIdx.x; i < ncell; i += blockDim.x) {
+    if (d.bce_w == 0.0) {  // the BCE term is bce_w * (finite) = +0 exactly: skip its two fp64 logs
+      d.A_burn[base + i] = 0.0;
+      continue;
+    }
     const double pred = d.burn[base + i] + d.bd[base + i];
     const double m = d.mask[base + i];
     const double p = fmin(fmax(pred, eps), 1.0 - eps);

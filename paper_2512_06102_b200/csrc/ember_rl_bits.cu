@@ -315,7 +315,7 @@ __device__ __forceinline__ int nth_set_bit_lut32(uint32_t v, int q, const uint32
   const int k = (qq >= (cum & 0xffu)) + (qq >= ((cum >> 8) & 0xffu)) + (qq >= ((cum >> 16) & 0xffu));
   const int before = k ? static_cast<int>((cum << 8 >> (8 * k)) & 0xffu) : 0;
   const uint32_t byte = (v >> (8 * k)) & 0xffu;
-  return 8 * k + static_cast<int>((lut[byte] >> (3 * (q - before))) & 7u);
+  return 8 * k + static_cast<int>((__ldg(lut + byte) >> (3 * (q - before))) & 7u);
 }
 
 __device__ __forceinline__ int nth_set_bit32(uint32_t v, int q) {
@@ -346,7 +346,6 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
   __shared__ float s_srckw[kTer ? 32 * 8 : 1];
   // the branch-free decide pass of k_step_warp (even compile-time words per row, pot32t rows)
   constexpr bool kFast = EBL_RL_FAST && kTer && DIMC != 0 && ((DIMC + 31) / 32) % 2 == 0;
-  __shared__ uint32_t s_nth[kFast ? 256 : 1];
 
   const StepArgs& a = g.s;
   const int env = blockIdx.x;
@@ -368,12 +367,6 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
   uint8_t* wt = g.wet + static_cast<size_t>(env) * n;
   if constexpr (kFast) {  // guard, padding words and padding rows of both B planes stay zero
     for (int i = threadIdx.x; i < 2 * PH + 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-      uint32_t e = 0u;
-      for (int bit = 0, cnt = 0; bit < 8; ++bit)
-        if ((i >> bit) & 1) e |= static_cast<uint32_t>(bit) << (3 * cnt++);
-      s_nth[i] = e;
-    }
     __syncthreads();
   } else {
     for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
@@ -546,7 +539,7 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
           }
         }
         int cc;
-        if constexpr (kFast) cc = 32 * jj + nth_set_bit_lut32(wv, q, s_nth);
+        if constexpr (kFast) cc = 32 * jj + nth_set_bit_lut32(wv, q, kNthBitLut);
         else cc = 32 * jj + nth_set_bit32(wv, q);
         if (kFast && use_tab) {  // one branch-free path for burning and candidate cells (ember_warp.cu)
           const float4* tp = reinterpret_cast<const float4*>(a.pot32t + static_cast<size_t>(env) * a.pot32t_stride) +

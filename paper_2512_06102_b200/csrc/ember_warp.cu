@@ -76,7 +76,7 @@ __device__ __forceinline__ int nth_set_bit(uint32_t v, int q) {
 
 // Position of the q-th (0-based) set bit of v (q < popc(v)) with a shallower dependency chain:
 // SWAR byte counts, their inclusive prefix in one multiply, the byte by three compares, the bit
-// from a 256-entry table of packed 3-bit positions (shared memory).
+// from a 256-entry table of packed 3-bit positions (kNthBitLut, read-only cache).
 __device__ __forceinline__ int nth_set_bit_lut(uint32_t v, int q, const uint32_t* lut) {
   uint32_t c = v - ((v >> 1) & 0x55555555u);
   c = (c & 0x33333333u) + ((c >> 2) & 0x33333333u);
@@ -86,7 +86,7 @@ __device__ __forceinline__ int nth_set_bit_lut(uint32_t v, int q, const uint32_t
   const int k = (qq >= (cum & 0xffu)) + (qq >= ((cum >> 8) & 0xffu)) + (qq >= ((cum >> 16) & 0xffu));
   const int before = k ? static_cast<int>((cum << 8 >> (8 * k)) & 0xffu) : 0;
   const uint32_t byte = (v >> (8 * k)) & 0xffu;
-  return 8 * k + static_cast<int>((lut[byte] >> (3 * (q - before))) & 7u);
+  return 8 * k + static_cast<int>((__ldg(lut + byte) >> (3 * (q - before))) & 7u);
 }
 
 // DIMC: the env's side when the env is a DIMC x DIMC square known at compile time (128: C1, 64:
@@ -107,7 +107,6 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
   // the fast decide path: even compile-time words per row leave a zero padding word after every
   // plane row (stride wpr | 1), so the neighbour windows need no bounds branches
   constexpr bool kFast = EBL_WARP_FAST && EBL_WARP_MICRO && kTer && WPRC != 0 && (WPRC & 1) == 0;
-  __shared__ uint32_t s_nth[kFast ? 256 : 1];
 
   // one region: one tile of one env's layer plus its light-cone halo (the whole env for resident
   // launches); H x RW region cells, layer BH x W.  Grid launches run the CTA's own region, work-list
@@ -187,12 +186,6 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
   // ---- load ----------------------------------------------------------------------------------
   if constexpr (kFast) {  // guard words, padding words and padding rows of both B planes: zero
     for (int i = threadIdx.x; i < 2 * PH + 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {  // n-th set bit of a byte, 3 bits each
-      uint32_t e = 0u;
-      for (int bit = 0, n = 0; bit < 8; ++bit)
-        if ((i >> bit) & 1) e |= static_cast<uint32_t>(bit) << (3 * n++);
-      s_nth[i] = e;
-    }
     __syncthreads();
   } else {
     for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
@@ -414,7 +407,7 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
           }
         }
         int cc;
-        if constexpr (kFast) cc = 32 * jj + nth_set_bit_lut(wv, q, s_nth);
+        if constexpr (kFast) cc = 32 * jj + nth_set_bit_lut(wv, q, kNthBitLut);
         else cc = 32 * jj + nth_set_bit(wv, q);
 #if EBL_PHASE_PROF
         {
