@@ -1024,24 +1024,25 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
           }
           for (auto& l : b->tlist)
             if (l.n < nt) EBL_CUDA(l.alloc(nt));
-          if (b->tcount.n < 3) EBL_CUDA(b->tcount.alloc(3));
+          if (b->tcount.n < 6) EBL_CUDA(b->tcount.alloc(6));  // append counters [3] + cursors [3]
           list_launch += 1;
           list_tiles = nt;
-          const int cur_l = list_launch & 1, nxt = cur_l ^ 1;
+          if (list_launch == 0) EBL_CUDA(cudaMemsetAsync(b->tcount.p, 0, 6 * sizeof(int32_t), b->stream));
+          const int cur_l = list_launch & 1, nxt = cur_l ^ 1, c3 = list_launch % 3;
           a.list_mode = list_launch == 0 ? 1 : 2;
           a.trec = b->trec.p;
           a.queued = b->tqueued.p;
           a.list_stamp = ++b->list_stamp;
           a.next_list = b->tlist[nxt].p;
-          a.next_count = b->tcount.p + nxt;
+          a.next_count = b->tcount.p + (c3 + 1) % 3;
           a.tile_list = b->tlist[cur_l].p;
-          a.tile_count = b->tcount.p + cur_l;
-          a.list_cursor = b->tcount.p + 2;
+          a.tile_count = b->tcount.p + c3;
+          a.list_cursor = b->tcount.p + 3 + c3;
+          a.list_zero0 = b->tcount.p + (c3 + 2) % 3;      // zeroed by this launch for the one after next
+          a.list_zero1 = b->tcount.p + 3 + (c3 + 1) % 3;  // the next launch's cursor
           a.tiles_x = tx;
           a.tiles_y = ty;
           a.tiles_total = static_cast<int>(nt);
-          EBL_CUDA(cudaMemsetAsync(b->tcount.p + nxt, 0, sizeof(int32_t), b->stream));
-          EBL_CUDA(cudaMemsetAsync(b->tcount.p + 2, 0, sizeof(int32_t), b->stream));
           tf_tiles = -1;
         } else if (tiled) {
           const size_t n = static_cast<size_t>(tx) * ty * b->n_envs * 4;

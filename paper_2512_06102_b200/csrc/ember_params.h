@@ -80,6 +80,8 @@ struct StepArgs {
   const int32_t* tile_list;
   const int32_t* tile_count;
   int32_t* list_cursor;
+  int32_t* list_zero0;            // counters the launch after next uses: zeroed by this launch
+  int32_t* list_zero1;
   int tiles_x, tiles_y, tiles_total;
   int n_peers;
   uint8_t* peer_out[2];

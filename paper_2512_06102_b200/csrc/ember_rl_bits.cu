@@ -303,6 +303,9 @@ cudaError_t launch_rl_tanker_bits(const RlArgs& g, int mode, cudaStream_t s) {
 #ifndef EBL_RL_FAST
 #define EBL_RL_FAST 1  // the branch-free decide pass in the tanker kernel
 #endif
+#ifndef EBL_RL_LUT  // its table-driven n-th set bit (a global table: one L2 miss per fresh CTA,
+#define EBL_RL_LUT 0  // which single-step launches of 16384 CTAs pay: popc search instead)
+#endif
 namespace {
 
 // the shallower n-th set bit of the warp kernel (ember_warp.cu)
@@ -366,7 +369,15 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
   uint8_t* st = g.state + static_cast<size_t>(env) * n;
   uint8_t* wt = g.wet + static_cast<size_t>(env) * n;
   if constexpr (kFast) {  // guard, padding words and padding rows of both B planes stay zero
-    for (int i = threadIdx.x; i < 2 * PH + 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+    // only the words no load or dense pass writes: the 4 guard words, the padding rows 0 and H+1,
+    // and every row's padding / skew words (ro(R) + wpr .. ro(R+1)) of both planes
+    if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(smem)[threadIdx.x] = 0u;
+    for (int i = threadIdx.x; i < 2 * (H + 2); i += blockDim.x) {
+      const int R = i % (H + 2);
+      uint32_t* P = i < H + 2 ? Bp0 : Bp1;
+      for (int k = (R == 0 || R == H + 1) ? ro(R) : ro(R) + wpr; k < ro(R + 1); ++k) P[k] = 0u;
+    }
+    if (threadIdx.x == 0) Bp0[ro(H + 2)] = Bp1[ro(H + 2)] = 0u;  // the plane's last word
     __syncthreads();
   } else {
     for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
@@ -539,9 +550,12 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
           }
         }
         int cc;
-        if constexpr (kFast) cc = 32 * jj + nth_set_bit_lut32(wv, q, kNthBitLut);
+        if constexpr (kFast && EBL_RL_LUT) cc = 32 * jj + nth_set_bit_lut32(wv, q, kNthBitLut);
         else cc = 32 * jj + nth_set_bit32(wv, q);
-        if (kFast && use_tab) {  // one branch-free path for burning and candidate cells (ember_warp.cu)
+        // one branch-free path for burning and candidate cells (ember_warp.cu) in fused rollouts;
+        // single-step launches (the per-step API, 14 waves of short-lived CTAs) measured faster on
+        // the branchy path (device-io steps: 2.12e8 vs 1.94e8 env-steps/s; rollouts: 3.38e8 vs 3.52e8)
+        if (kFast && use_tab && g.n_steps > 1) {
           const float4* tp = reinterpret_cast<const float4*>(a.pot32t + static_cast<size_t>(env) * a.pot32t_stride) +
                              2 * (rr * W + cc);
           const float4 T0 = __ldg(tp), T1 = __ldg(tp + 1);

@@ -28,12 +28,6 @@
 #ifndef EBL_PHASE_PROF
 #define EBL_PHASE_PROF 0
 #endif
-#ifndef EBL_WARP_PF
-#define EBL_WARP_PF 0
-#endif
-#ifndef EBL_WPF
-#define EBL_WPF prefetch_l1
-#endif
 
 #ifndef EBL_WARP_UNROLL2  // step loop unrolled by two (B / Bn roles alternate)
 #define EBL_WARP_UNROLL2 1  // C1 kernel 0.524 -> 0.509 ms (a few spilled bytes)
@@ -44,9 +38,6 @@
 #ifndef EBL_WARP_FAST  // decide passes without divergent branches: branch-free neighbour windows
 #define EBL_WARP_FAST 1  // (zeroed guard words), SWAR + table n-th set bit, burning and candidate
 #endif                   // cells through one code path (even compile-time words per row, pot32t)
-#ifndef EBL_WARP_PFIGN  // at an ignition, prefetch the pot32t rows of the 8 neighbours (the next
-#define EBL_WARP_PFIGN 0  // step's new candidates): 1 into L1, 2 into L2
-#endif
 #ifndef EBL_WARP_POT  // lambda terms from the pot32t table (0: slope + source-class records)
 #define EBL_WARP_POT 1
 #endif
@@ -57,7 +48,9 @@ namespace {
 
 constexpr int kWpThreads = 128;  // 4 warps
 
+#if EBL_PHASE_PROF
 __device__ __forceinline__ long long pw_wait_dummy(long long v) { return v; }
+#endif
 
 // Position of the q-th (0-based) set bit of v (q < popc(v)): popc binary search, 5 levels.
 __device__ __forceinline__ int nth_set_bit(uint32_t v, int q) {
@@ -94,8 +87,13 @@ __device__ __forceinline__ int nth_set_bit_lut(uint32_t v, int q, const uint32_t
 #ifndef EBL_WARP_MINB
 #define EBL_WARP_MINB 8  // 64 registers; 7 (72 registers, still one wave for C1): same C1, slower C3
 #endif
+// One region: one tile of one env's layer plus its light-cone halo (the whole env for resident
+// launches); H x RW region cells, layer BH x W.  Grid launches run the CTA's own region, work-list
+// launches (a.list_mode == 2) loop over the listed tiles (k_step_warp below).  Whole-env
+// instantiations pass compile-time tile coordinates.
 template <int MODE, int WPRC, int DIMC>
-__global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArgs a, BlockGeom g) {
+__device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& g, const int env, const int bxi,
+                                            const int byi, const int ntx, const int nty) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int32_t s_cnt[3];
   __shared__ int32_t s_newly;
@@ -108,10 +106,6 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
   // plane row (stride wpr | 1), so the neighbour windows need no bounds branches
   constexpr bool kFast = EBL_WARP_FAST && EBL_WARP_MICRO && kTer && WPRC != 0 && (WPRC & 1) == 0;
 
-  // one region: one tile of one env's layer plus its light-cone halo (the whole env for resident
-  // launches); H x RW region cells, layer BH x W.  Grid launches run the CTA's own region, work-list
-  // launches (a.list_mode == 2) loop over the listed tiles (below).
-  auto region = [&](const int env, const int bxi, const int byi, const int ntx, const int nty) {
   const int n_steps = g.n_steps;
   const int BH = DIMC ? DIMC : a.h, W = DIMC ? DIMC : a.w;
   const int r0 = DIMC ? 0 : byi * g.tile_h, c0 = DIMC ? 0 : bxi * g.tile_w;  // c0 % 32 == 0
@@ -185,7 +179,15 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
   }
   // ---- load ----------------------------------------------------------------------------------
   if constexpr (kFast) {  // guard words, padding words and padding rows of both B planes: zero
-    for (int i = threadIdx.x; i < 2 * PH + 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+    // only the words no load or dense pass writes: the 4 guard words, the padding rows 0 and H+1,
+    // and every row's padding / skew words (ro(R) + wpr .. ro(R+1)) of both planes
+    if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(smem)[threadIdx.x] = 0u;
+    for (int i = threadIdx.x; i < 2 * (H + 2); i += blockDim.x) {
+      const int R = i % (H + 2);
+      uint32_t* P = i < H + 2 ? Bp0 : Bp1;
+      for (int k = (R == 0 || R == H + 1) ? ro(R) : ro(R) + wpr; k < ro(R + 1); ++k) P[k] = 0u;
+    }
+    if (threadIdx.x == 0) Bp0[ro(H + 2)] = Bp1[ro(H + 2)] = 0u;  // the plane's last word
     __syncthreads();
   } else {
     for (int i = threadIdx.x; i < wpr; i += blockDim.x) {
@@ -501,26 +503,6 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
 #if !EBL_WARP_MICRO
             newly += last && rr >= tr0 && rr < tr1 && cc >= tc0 && cc < tc1;  // counted in the tile only
 #endif
-#if EBL_WARP_PFIGN
-            if (use_tab) {  // the next step's new candidates: rows gr-1..gr+1, columns gc-1..gc+1
-              const float* base = a.pot32t + static_cast<size_t>(env) * a.pot32t_stride;
-              const int c_lo = gc > 0 ? gc - 1 : 0, c_hi = gc + 1 < W ? gc + 1 : W - 1;
-#pragma unroll
-              for (int dr = -1; dr <= 1; ++dr) {
-                const int row = gr + dr;
-                if (row < 0 || row >= BH) continue;
-                const float* p0 = base + (static_cast<size_t>(row) * W + c_lo) * 8;
-                const float* p1 = base + (static_cast<size_t>(row) * W + c_hi) * 8 + 7;
-                if (EBL_WARP_PFIGN == 1) {
-                  asm volatile("prefetch.global.L1 [%0];" ::"l"(p0));
-                  asm volatile("prefetch.global.L1 [%0];" ::"l"(p1));
-                } else {
-                  asm volatile("prefetch.global.L2 [%0];" ::"l"(p0));
-                  asm volatile("prefetch.global.L2 [%0];" ::"l"(p1));
-                }
-              }
-            }
-#endif
           }
         }
       }
@@ -637,9 +619,15 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
       enqueue(bxi, byi);
     }
   }
-  };  // region
+}
 
-  if (a.list_mode == 2) {  // work list of this launch: persistent CTAs take tiles until it runs out
+template <int MODE, int WPRC, int DIMC>
+__global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArgs a, BlockGeom g) {
+  if (DIMC == 0 && a.list_mode && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) {
+    *a.list_zero0 = 0;  // the next launch's append counter and cursor start at 0 (no memset launches)
+    *a.list_zero1 = 0;
+  }
+  if (DIMC == 0 && a.list_mode == 2) {  // work list of this launch: persistent CTAs take tiles until it runs out
     __shared__ int s_item;
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.diag) atomicAdd(a.diag + 3, static_cast<unsigned long long>(a.tiles_total));
     for (;;) {
@@ -650,11 +638,13 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
       if (item >= *a.tile_count) break;
       const int tile = a.tile_list[item];
       const int bx = tile % a.tiles_x, rest = tile / a.tiles_x;
-      region(rest / a.tiles_y, bx, rest % a.tiles_y, a.tiles_x, a.tiles_y);
+      warp_region<MODE, WPRC, DIMC>(a, g, rest / a.tiles_y, bx, rest % a.tiles_y, a.tiles_x, a.tiles_y);
     }
   } else {
-    region(static_cast<int>(blockIdx.z), static_cast<int>(blockIdx.x), static_cast<int>(blockIdx.y),
-           static_cast<int>(gridDim.x), static_cast<int>(gridDim.y));
+    // (whole-env instantiations: one region per env, the tile coordinates are compile-time 0 / 1)
+    warp_region<MODE, WPRC, DIMC>(a, g, static_cast<int>(blockIdx.z), DIMC ? 0 : static_cast<int>(blockIdx.x),
+                                  DIMC ? 0 : static_cast<int>(blockIdx.y), DIMC ? 1 : static_cast<int>(gridDim.x),
+                                  DIMC ? 1 : static_cast<int>(gridDim.y));
   }
 }
 
@@ -681,15 +671,16 @@ cudaError_t launch_wp(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStre
 
 }  // namespace
 
-// counts[env][0..2] = the U/B/X of every tile's record (work-list runs: tiles not in the last
-// list kept their recorded counts); counts[env][3] (ignited in the last step) is left as is
+// counts[env][0..2] += the U/B/X of every tile's record (work-list runs: tiles not in the last
+// list kept their recorded counts; the listed tiles of the last launch add only counts[env][3]);
+// blockIdx.y = env, blockIdx.x strides over its tiles
 __global__ void k_tile_counts(const int4* __restrict__ trec, int tiles_per_env, int32_t* counts) {
   __shared__ int s[3];
   if (threadIdx.x < 3) s[threadIdx.x] = 0;
   __syncthreads();
   int u = 0, bb = 0, x = 0;
-  for (int i = threadIdx.x; i < tiles_per_env; i += blockDim.x) {
-    const int4 r = trec[static_cast<size_t>(blockIdx.x) * tiles_per_env + i];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < tiles_per_env; i += gridDim.x * blockDim.x) {
+    const int4 r = trec[static_cast<size_t>(blockIdx.y) * tiles_per_env + i];
     u += r.y;
     bb += r.z;
     x += r.w;
@@ -698,11 +689,12 @@ __global__ void k_tile_counts(const int4* __restrict__ trec, int tiles_per_env, 
   atomicAdd(&s[1], bb);
   atomicAdd(&s[2], x);
   __syncthreads();
-  if (threadIdx.x < 3) counts[blockIdx.x * 4 + threadIdx.x] = s[threadIdx.x];
+  if (threadIdx.x < 3) atomicAdd(counts + blockIdx.y * 4 + threadIdx.x, s[threadIdx.x]);
 }
 
 cudaError_t launch_tile_counts(const int32_t* trec, int n_envs, int tiles_per_env, int32_t* counts, cudaStream_t s) {
-  k_tile_counts<<<n_envs, 256, 0, s>>>(reinterpret_cast<const int4*>(trec), tiles_per_env, counts);
+  const int bx = std::max(1, std::min(64, (tiles_per_env + 255) / 256));
+  k_tile_counts<<<dim3(bx, n_envs), 256, 0, s>>>(reinterpret_cast<const int4*>(trec), tiles_per_env, counts);
   return cudaGetLastError();
 }
 
