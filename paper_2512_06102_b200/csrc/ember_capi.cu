@@ -1112,44 +1112,6 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
     return ebl_batch_get_state(b, final_states);
   }
   EBL_CUDA(cudaSetDevice(b->device));
-  // Both host buffers mapped pinned memory (ebl_host_alloc / cudaHostAlloc(Mapped)): ONE launch whose
-  // CTAs read their env's initial layer over PCIe themselves and write the final layer straight back,
-  // so every env starts as soon as its own 16 KB has arrived instead of waiting for its chunk's copy
-  // (the run ends at max over envs of arrival + compute, not at full input + a chunk's slowest env).
-  // EBL_PIPE_ZCIN=0 keeps the chunked copy pipeline below.
-  static const bool zc_in = [] {
-    const char* e = std::getenv("EBL_PIPE_ZCIN");
-    return !e || std::atoi(e) != 0;
-  }();
-  if (zc_in) {
-    auto mapped = [](const void* p) -> uint8_t* {
-      cudaPointerAttributes pa{};
-      uint8_t* d = nullptr;
-      if (cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer &&
-          (reinterpret_cast<uintptr_t>(pa.devicePointer) & 15) == 0)
-        d = static_cast<uint8_t*>(pa.devicePointer);
-      cudaGetLastError();
-      return d;
-    };
-    uint8_t* const in_dev = mapped(initial);
-    uint8_t* const out_dev = in_dev ? mapped(final_states) : nullptr;
-    if (in_dev && out_dev) {
-      const ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps, false, 0, b->n_envs, 1);
-      ebl::StepArgs a = step_args(b);
-      EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
-      a.counts = b->counts.p;
-      a.in = in_dev;
-      a.out2 = out_dev;
-      EBL_CUDA(launch_ca(b, a, g, b->stream));
-      EBL_CUDA(cudaStreamSynchronize(b->stream));
-      b->cur ^= 1;
-      b->step += n_steps;
-      b->launches += 1;
-      b->steps_done += n_steps;
-      b->counts_valid = true;
-      return EBL_OK;
-    }
-  }
   if (int e = ensure_pipeline(b, chunks)) return e;
   const ebl::BlockGeom g = ebl::plan_blocks(b->h, b->w, n_steps, false, 0, b->n_envs, 1);
   ebl::StepArgs a = step_args(b);
