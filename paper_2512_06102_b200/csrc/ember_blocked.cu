@@ -582,8 +582,7 @@ BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_o
 
 template <int MODE, int E, int WPRC>
 static cudaError_t launch_blocked_w(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(k_step_blocked<MODE, E, WPRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sm));
+  cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_step_blocked<MODE, E, WPRC>), sm);
   if (e != cudaSuccess) return e;
   const dim3 grid((a.w + g.tile_w - 1) / g.tile_w, (a.h + g.tile_h - 1) / g.tile_h, (a.n_envs + E - 1) / E);
   k_step_blocked<MODE, E, WPRC><<<grid, kResThreads * E, sm, s>>>(a, g);

@@ -146,6 +146,7 @@ struct ebl_batch {
   int det_cur = 0;
   bool det_ready = false;
   DevBuf<double> det_pot, det_gam, det_fac, det_V, det_align, traj, adj, det_mask, acc, det_loss, det_grad, det_init;
+  DevBuf<double> det_potT;          // target-ordered copy of det_pot for the forward (EBL_DET_POTT)
   DevBuf<double> det_S;             // [grid][cell][8] cached fp64 slopes (host atan, once per terrain)
   bool det_S_valid = false;
   bool det_dev_tables = true;       // terrain-form SpreadTables built on the device (ebl_batch_set_det_tables)
@@ -1292,9 +1293,21 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
   }
   std::vector<uint8_t*> outs(n_shards);
   std::vector<ebl::BlockGeom> geo(n_shards);
-  // quiet-tile records per shard across the chunks of this call (tiles holding halo rows the
-  // neighbours store into are never skipped: ember_warp.cu)
+  // quiet-tile records per shard across the chunks of this call; on work lists the neighbours
+  // enqueue each other's tiles next to the halo rows they store (else those tiles are exposed:
+  // never skipped; ember_warp.cu)
   std::vector<int> tf_par(n_shards, 0), tf_tiles(n_shards, -1);
+  std::vector<int> list_launch(n_shards, -1);  // work-list runs per shard (ebl_step_batch's scheme)
+  static const bool work_list = [] {
+    const char* e = std::getenv("EBL_WORK_LIST");
+    return !e || std::atoi(e) != 0;
+  }();
+  static const bool halo_marks = [] {  // EBL_HALO_MARKS=0: exposed halo tiles instead of record exchange
+    const char* e = std::getenv("EBL_HALO_MARKS");
+    return !e || std::atoi(e) != 0;
+  }();
+  std::vector<ebl::StepArgs> args(n_shards);
+  std::vector<char> listed(n_shards, 0);
   int chunk = 0;
   for (int done = 0; done < n_steps; ++chunk) {
     int k = n_shards > 1 ? std::min(halo, n_steps - done) : n_steps - done;
@@ -1315,28 +1328,63 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
       geo[s] = g;
     }
     for (int s = 0; s < n_shards; ++s) outs[s] = shards[s]->state[shards[s]->cur ^ 1].p;
+    // pass 1: waits, counters and each shard's own launch parameters (list stamps included, which
+    // the neighbours' marks need)
     for (int s = 0; s < n_shards; ++s) {
       ebl_batch* b = shards[s];
       EBL_CUDA(cudaSetDevice(b->device));
-      // the neighbours' launches of the previous chunk (slot (chunk-1) & 1: a neighbour processed
-      // earlier in this loop has already re-recorded the other slot)
-      if (chunk > 0)
-        for (int q = s - 1; q <= s + 1; q += 2)
-          if (q >= 0 && q < n_shards)
-            EBL_CUDA(cudaStreamWaitEvent(b->stream, shards[q]->shard_ev[(chunk - 1) & 1], 0));
-      ebl::BlockGeom g = geo[s];
+      // the neighbours' launches of the previous chunk (all waits precede this chunk's records)
+      for (int q = s - 1; q <= s + 1 && chunk > 0; q += 2)
+        if (q >= 0 && q < n_shards)
+          EBL_CUDA(cudaStreamWaitEvent(b->stream, shards[q]->shard_ev[(chunk - 1) & 1], 0));
+      ebl::BlockGeom& g = geo[s];
       g.n_steps = k;
       ebl::StepArgs a = step_args(b);
-      EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, 4 * sizeof(int32_t), b->stream));
-      a.counts = b->counts.p;
+      if (done + k == n_steps) {  // counts of the last launch only
+        EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, 4 * sizeof(int32_t), b->stream));
+        a.counts = b->counts.p;
+      }
       a.store_lo = b->band_lo;
       a.store_hi = b->band_hi;
+      listed[s] = 0;
       {
         const int tx = (b->w + g.tile_w - 1) / g.tile_w, ty = (b->h + g.tile_h - 1) / g.tile_h;
         const bool exposed = a.keep_lo > 0 || a.keep_hi < b->h;
         const bool tiled = tx * ty > 1 && g.halo_rows <= g.tile_h && g.halo_cols <= g.tile_w && use_warp(b) &&
                            k <= std::max(1, g.halo_rows) && (!exposed || g.tile_h >= 3 * g.halo_rows);
-        if (tiled) {
+        if (tiled && work_list && (list_launch[s] >= 0 || n_steps > k)) {
+          // work list (halo tiles: marked by the neighbours, or exposed -- ember_warp.cu)
+          const size_t nt = static_cast<size_t>(tx) * ty * b->n_envs;
+          if (b->trec.n < nt * 4 || b->tqueued.n < nt) {
+            EBL_CUDA(b->trec.alloc(nt * 4));
+            EBL_CUDA(b->tqueued.alloc(nt));
+            EBL_CUDA(cudaMemsetAsync(b->tqueued.p, 0, nt * sizeof(int32_t), b->stream));
+            b->list_stamp = 0;
+          }
+          for (auto& l : b->tlist)
+            if (l.n < nt) EBL_CUDA(l.alloc(nt));
+          if (b->tcount.n < 6) EBL_CUDA(b->tcount.alloc(6));
+          const int L = ++list_launch[s];
+          if (L == 0) EBL_CUDA(cudaMemsetAsync(b->tcount.p, 0, 6 * sizeof(int32_t), b->stream));
+          const int c3 = L % 3;
+          a.list_mode = L == 0 ? 1 : 2;
+          a.trec = b->trec.p;
+          a.queued = b->tqueued.p;
+          a.list_stamp = ++b->list_stamp;
+          a.next_list = b->tlist[(L & 1) ^ 1].p;
+          a.next_count = b->tcount.p + (c3 + 1) % 3;
+          a.tile_list = b->tlist[L & 1].p;
+          a.tile_count = b->tcount.p + c3;
+          a.list_cursor = b->tcount.p + 3 + c3;
+          a.list_zero0 = b->tcount.p + (c3 + 2) % 3;
+          a.list_zero1 = b->tcount.p + 3 + (c3 + 1) % 3;
+          a.tiles_x = tx;
+          a.tiles_y = ty;
+          a.tiles_total = static_cast<int>(nt);
+          tf_tiles[s] = -1;
+          listed[s] = 1;
+        } else if (tiled) {
+          list_launch[s] = -1;
           const size_t n = static_cast<size_t>(tx) * ty * b->n_envs * 4;
           for (auto& f : b->tflags)
             if (f.n < n) {
@@ -1348,22 +1396,65 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
           tf_par[s] ^= 1;
           tf_tiles[s] = tx * ty;
         } else {
+          list_launch[s] = -1;
           tf_tiles[s] = -1;
         }
       }
+      args[s] = a;
+    }
+    // the listed shards' first-launch counter resets are on their own streams: a neighbour's first
+    // marks wait for them (slot 1 plays "chunk -1")
+    if (chunk == 0)
+      for (int s = 0; s < n_shards; ++s) {
+        EBL_CUDA(cudaSetDevice(shards[s]->device));
+        EBL_CUDA(cudaEventRecord(shards[s]->shard_ev[1], shards[s]->stream));
+      }
+    // pass 2: peer stores and marks, launch
+    for (int s = 0; s < n_shards; ++s) {
+      ebl_batch* b = shards[s];
+      EBL_CUDA(cudaSetDevice(b->device));
+      if (chunk == 0)
+        for (int q = s - 1; q <= s + 1; q += 2)
+          if (q >= 0 && q < n_shards) EBL_CUDA(cudaStreamWaitEvent(b->stream, shards[q]->shard_ev[1], 0));
+      const ebl::BlockGeom& g = geo[s];
+      ebl::StepArgs a = args[s];
+      bool marked = listed[s] != 0;
       const int64_t g0 = b->row_off + b->band_lo, g1 = b->row_off + b->band_hi;
       for (int q = s - 1; q <= s + 1; q += 2) {
         if (q < 0 || q >= n_shards) continue;
         const ebl_batch* nb = shards[q];
+        // shard q's halo tiles lose their exposure only when q marks ours and we mark q's
+        if (!listed[q]) marked = false;
         const int64_t lo = std::max(g0, nb->row_off), hi = std::min(g1, nb->row_off + static_cast<int64_t>(nb->h));
         if (hi <= lo) continue;
-        a.peer_out[a.n_peers] = outs[q];
-        a.peer_lo[a.n_peers] = static_cast<int>(lo - b->row_off);
-        a.peer_hi[a.n_peers] = static_cast<int>(hi - b->row_off);
-        a.peer_dst[a.n_peers] = static_cast<int>(lo - nb->row_off);
-        ++a.n_peers;
+        const int p = a.n_peers++;
+        a.peer_out[p] = outs[q];
+        a.peer_lo[p] = static_cast<int>(lo - b->row_off);
+        a.peer_hi[p] = static_cast<int>(hi - b->row_off);
+        a.peer_dst[p] = static_cast<int>(lo - nb->row_off);
+        a.peer_queued[p] = nullptr;
+        if (listed[s] && listed[q]) {  // our burning tiles enqueue q's tiles that read these rows
+          const ebl::StepArgs& aq = args[q];
+          a.peer_queued[p] = aq.queued;
+          a.peer_next_list[p] = aq.next_list;
+          a.peer_next_count[p] = aq.next_count;
+          a.peer_stamp[p] = aq.list_stamp;
+          a.peer_tiles_x[p] = aq.tiles_x;
+          a.peer_tiles_y[p] = aq.tiles_y;
+          a.peer_tile_h[p] = geo[q].tile_h;
+          a.peer_tile_w[p] = geo[q].tile_w;
+          a.peer_halo_r[p] = geo[q].halo_rows;
+          a.peer_halo_c[p] = geo[q].halo_cols;
+        }
       }
+      a.halo_marked = marked && halo_marks ? 1 : 0;
+      if (!halo_marks)
+        for (int p = 0; p < a.n_peers; ++p) a.peer_queued[p] = nullptr;
       EBL_CUDA(launch_ca(b, a, g, b->stream));
+      if (list_launch[s] >= 0 && done + k == n_steps) {  // U/B/X of the band from the in-place records
+        const int tx = (b->w + g.tile_w - 1) / g.tile_w, ty = (b->h + g.tile_h - 1) / g.tile_h;
+        EBL_CUDA(ebl::launch_tile_counts(b->trec.p, b->n_envs, tx * ty, b->counts.p, b->stream));
+      }
       EBL_CUDA(cudaEventRecord(b->shard_ev[chunk & 1], b->stream));
     }
     for (int s = 0; s < n_shards; ++s) {
@@ -2080,6 +2171,7 @@ ebl::DetArgs det_args(ebl_batch* b) {
   d.burn_o = b->det[o + 1].p;
   d.bd_o = b->det[o + 2].p;
   d.pot = b->det_pot.p;
+  d.potT = b->det_potT.p;
   d.gam = b->det_gam.p;
   d.tab_stride = b->det_tables > 1 ? b->ncell : 0;
   d.pc = b->cfg.p_continue;
@@ -2164,6 +2256,16 @@ int det_tables(ebl_batch* b) {
     EBL_CUDA(b->det_gam.alloc(gam.size()));
     EBL_CUDA(cudaMemcpyAsync(b->det_pot.p, pot.data(), pot.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
     EBL_CUDA(cudaMemcpyAsync(b->det_gam.p, gam.data(), gam.size() * sizeof(double), cudaMemcpyHostToDevice, b->stream));
+  }
+  static const bool pot_t = [] {
+    const char* e = std::getenv("EBL_DET_POTT");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (pot_t) {  // the forward's target-ordered table (a permutation of the same fp64 values)
+    EBL_CUDA(b->det_potT.alloc(n * 8 * T));
+    EBL_CUDA(ebl::launch_pot_target(b->det_pot.p, b->det_potT.p, T, b->h, b->w, b->stream));
+  } else {
+    b->det_potT.reset();
   }
   EBL_CUDA(b->det_V.alloc(V.size()));
   EBL_CUDA(b->det_align.alloc(al.size()));

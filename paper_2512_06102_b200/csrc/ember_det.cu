@@ -108,6 +108,52 @@ __device__ __forceinline__ double lambda_at(const double* __restrict__ burn, con
 
 }  // namespace
 
+// lambda from the target-ordered table: the 8 source terms of cell v are one contiguous 64-byte row
+// (four 16-byte loads issued together, coalesced across the warp) instead of 8 loads strided by a
+// source row each; same k-ordered fold with the zero-weight skip, same fp64 operations.
+__device__ __forceinline__ double lambda_at_t(const double* __restrict__ burn, const double* __restrict__ potT, int h,
+                                              int w, int r, int c) {
+  double wk[8];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int ur = r - kDy[k], uc = c - kDx[k];
+    wk[k] = (ur < 0 || ur >= h || uc < 0 || uc >= w) ? 0.0 : burn[ur * w + uc];
+    any |= wk[k] != 0.0;
+  }
+  if (!any) return 0.0;  // no burning source: the row is not needed (lambda = 0, as the skip gives)
+  const size_t i = static_cast<size_t>(r) * w + c;
+  const double2 p01 = __ldg(reinterpret_cast<const double2*>(potT + i * 8));
+  const double2 p23 = __ldg(reinterpret_cast<const double2*>(potT + i * 8 + 2));
+  const double2 p45 = __ldg(reinterpret_cast<const double2*>(potT + i * 8 + 4));
+  const double2 p67 = __ldg(reinterpret_cast<const double2*>(potT + i * 8 + 6));
+  const double pk[8] = {p01.x, p01.y, p23.x, p23.y, p45.x, p45.y, p67.x, p67.y};
+  double lam = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (wk[k] != 0.0) lam = __dadd_rn(lam, __dmul_rn(wk[k], pk[k]));  // k order, zero-weight skip
+  return lam;
+}
+
+__global__ void k_pot_target(const double* __restrict__ pot, double* __restrict__ potT, int n_tables, int h, int w) {
+  const size_t ncell = static_cast<size_t>(h) * w, total = static_cast<size_t>(n_tables) * ncell * 8;
+  for (size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < total;
+       j += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(j & 7);
+    const size_t tc = j >> 3, t = tc / ncell, v = tc - t * ncell;
+    const int r = static_cast<int>(v / w), c = static_cast<int>(v % w);
+    const int ur = r - kDy[k], uc = c - kDx[k];
+    potT[j] = (ur < 0 || ur >= h || uc < 0 || uc >= w) ? 0.0 : pot[(t * ncell + static_cast<size_t>(ur) * w + uc) * 8 + k];
+  }
+}
+
+cudaError_t launch_pot_target(const double* pot, double* potT, int n_tables, int h, int w, cudaStream_t s) {
+  const size_t total = static_cast<size_t>(n_tables) * h * w * 8;
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 8));
+  k_pot_target<<<blocks, 256, 0, s>>>(pot, potT, n_tables, h, w);
+  return cudaGetLastError();
+}
+
 __global__ void k_det_forward(DetArgs d, int t) {
   const StepArgs& a = d.s;
   const int ncell = a.h * a.w;
@@ -116,7 +162,8 @@ __global__ void k_det_forward(DetArgs d, int t) {
   if (i >= ncell) return;
   const size_t base = static_cast<size_t>(env) * ncell;
   const size_t tb = static_cast<size_t>(env) * d.tab_stride;
-  const double lam = lambda_at(d.burn + base, d.pot + tb * 8, a.h, a.w, i / a.w, i % a.w);
+  const double lam = d.potT ? lambda_at_t(d.burn + base, d.potT + tb * 8, a.h, a.w, i / a.w, i % a.w)
+                            : lambda_at(d.burn + base, d.pot + tb * 8, a.h, a.w, i / a.w, i % a.w);
   const double p_ig = __dsub_rn(1.0, exp_neg(__dmul_rn(gamma_at(d, tb, env, i), lam)));
   const double un = d.un[base + i], bu = d.burn[base + i], bd = d.bd[base + i];
   const double newly = __dmul_rn(un, p_ig);
@@ -743,7 +790,7 @@ cudaError_t launch_det_backward(const DetArgs& d, int t, cudaStream_t s) {
   const dim3 grid((ncell + 255) / 256, d.s.n_envs);
   if (EBL_DET_STREAM && det_stream_ok(d) && d.A_un_o) {
     const size_t sm = det_stream_smem();
-    cudaError_t e = cudaFuncSetAttribute(k_det_back_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+    cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_det_back_stream), sm);
     if (e != cudaSuccess) return e;
     k_det_back_stream<<<dim3(det_blocks_per_env_stream(d.s.h), d.s.n_envs), kSW, sm, s>>>(d, t);
     return cudaGetLastError();

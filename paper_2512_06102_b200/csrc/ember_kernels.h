@@ -18,6 +18,11 @@ constexpr int kBlockTileW = 256;    // 8-row / 32-column light-cone halo, 8 step
 constexpr int kBlockHalo = 8;
 
 bool phase_prof_built();
+// Host-side launch helpers with per-(kernel, device) caches: the dynamic shared-memory opt-in is
+// set once per larger size, the occupancy and SM count are queried once (both cost microseconds of
+// host time per call, which bounds launch-heavy paths such as row shards).
+cudaError_t smem_opt_in(const void* kernel, size_t smem);
+cudaError_t resident_ctas(const void* kernel, int threads, size_t smem, int* ctas_per_gpu);
 size_t blocked_smem_bytes(int region_h, int region_w, int list_cap, int envs_per_cta);
 bool resident_fits(int h, int w);
 BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_off, int n_envs,
@@ -30,6 +35,7 @@ cudaError_t launch_step_warp(const StepArgs& a, int mode, const BlockGeom& g, cu
 cudaError_t launch_tile_counts(const int32_t* trec, int n_envs, int tiles_per_env, int32_t* counts, cudaStream_t s);
 
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s);
+cudaError_t launch_pot_target(const double* pot, double* potT, int n_tables, int h, int w, cudaStream_t s);
 cudaError_t launch_det_tables_terrain(const double* S, const uint8_t* fuel, const double* pal64, const double* kw64,
                                       double alpha_s, int n_tables, size_t ncell, size_t grid_stride, int wind_stride,
                                       double* pot, cudaStream_t s);

@@ -66,7 +66,8 @@ struct StepArgs {
   // rows [peer_lo, peer_hi) of this layer at their row peer_dst -- the halo exchange fused into
   // the producing kernel's store
   int store_lo, store_hi;
-  int keep_lo, keep_hi;           // rows outside: halo rows written by neighbour shards (exposed tiles)
+  int keep_lo, keep_hi;           // rows outside: halo rows written by neighbour shards (exposed tiles
+                                  // unless halo_marked)
   // work-list runs of halo tiles (one batch, ebl_step_batch): list_mode 1 = grid launch, 2 = the
   // launch runs the tiles of tile_list[0 .. *tile_count) on persistent CTAs (list_cursor: the
   // claim counter); both keep the tile records in place (trec, int4 per tile) and append the next
@@ -86,6 +87,16 @@ struct StepArgs {
   int n_peers;
   uint8_t* peer_out[2];
   int peer_lo[2], peer_hi[2], peer_dst[2];
+  // row shards on work lists (ebl_shards_step): the activity records travel with the halo rows.  A
+  // tile with a burning cell that stores rows into neighbour p also enqueues, into p's next work
+  // list (stamp peer_stamp), p's tiles whose regions reach those rows (peer_queued null: no marks).
+  // halo_marked = both neighbours do so for this shard, so its halo tiles need no exposure rule.
+  int halo_marked;
+  int32_t* peer_queued[2];
+  int32_t* peer_next_list[2];
+  int32_t* peer_next_count[2];
+  int32_t peer_stamp[2];
+  int peer_tiles_x[2], peer_tiles_y[2], peer_tile_h[2], peer_tile_w[2], peer_halo_r[2], peer_halo_c[2];
 };
 
 // Tiling of the blocked kernel (ember_blocked.cu): tiles of tile_h x tile_w cells with
@@ -111,6 +122,8 @@ struct DetArgs {
   double* bd_o;
   const double* pot;              // [table][cell][8] SpreadTables<double>::pot (host-built, exact)
   const double* gam;              // [table][cell]
+  const double* potT;             // [table][cell][8] target-ordered pot: potT[v][k] = pot[v - d_k][k]
+                                  // (0 toward out-of-bounds sources), or null
   size_t tab_stride;              // cells per table (0: one table for all envs)
   double pc;
   double* traj_un;                // [T][env][cell] state before step t (record mode)

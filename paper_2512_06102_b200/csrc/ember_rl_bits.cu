@@ -279,13 +279,11 @@ cudaError_t launch_rl_tanker_bits(const RlArgs& g, int mode, cudaStream_t s) {
   const size_t sm = rl_bits_smem_bytes(g.s.h, g.s.w);
   cudaError_t e;
   if (mode == kStaticTables) {
-    e = cudaFuncSetAttribute(k_rl_tanker_bits<kStaticTables>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sm));
+    e = smem_opt_in(reinterpret_cast<const void*>(k_rl_tanker_bits<kStaticTables>), sm);
     if (e != cudaSuccess) return e;
     k_rl_tanker_bits<kStaticTables><<<g.s.n_envs, kRlBitsThreads, sm, s>>>(g);
   } else {
-    e = cudaFuncSetAttribute(k_rl_tanker_bits<kStaticTerrain>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(sm));
+    e = smem_opt_in(reinterpret_cast<const void*>(k_rl_tanker_bits<kStaticTerrain>), sm);
     if (e != cudaSuccess) return e;
     k_rl_tanker_bits<kStaticTerrain><<<g.s.n_envs, kRlBitsThreads, sm, s>>>(g);
   }
@@ -792,8 +790,7 @@ size_t rl_warp_smem_bytes(int h, int w) {
 
 template <int MODE, int DIMC>
 static cudaError_t launch_rl_warp_t(const RlArgs& g, size_t sm, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(k_rl_tanker_warp<MODE, DIMC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sm));
+  cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_rl_tanker_warp<MODE, DIMC>), sm);
   if (e != cudaSuccess) return e;
   k_rl_tanker_warp<MODE, DIMC><<<g.s.n_envs, kRlBitsThreads, sm, s>>>(g);
   return cudaGetLastError();

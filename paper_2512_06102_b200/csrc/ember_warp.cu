@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
+#include <unordered_map>
 
 #include "ember_bits.cuh"
 #include "ember_device.cuh"
@@ -611,11 +613,34 @@ __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& 
       const size_t id = (static_cast<size_t>(env) * nty + ty) * ntx + tx;
       if (atomicExch(a.queued + id, a.list_stamp) != a.list_stamp) a.next_list[atomicAdd(a.next_count, 1)] = static_cast<int>(id);
     };
+    // (row shards without record exchange: a tile holding halo rows a neighbour writes runs in
+    // every launch)
+    const bool exposed_t = !a.halo_marked && (r0 < a.keep_lo || r0 + g.tile_h > a.keep_hi);
     if (burning) {
       for (int dy = -1; dy <= 1; ++dy)
         for (int dx = -1; dx <= 1; ++dx)
           if (byi + dy >= 0 && byi + dy < nty && bxi + dx >= 0 && bxi + dx < ntx) enqueue(bxi + dx, byi + dy);
-    } else if (streak < 2) {
+      // row shards: the records travel with the halo rows -- the neighbour's tiles whose regions
+      // reach the rows stored into it run next launch (the light cone of a burning cell there);
+      // a tile without a burning cell stores nothing that can change a neighbour's band
+      for (int p = 0; p < a.n_peers; ++p) {
+        if (!a.peer_queued[p]) continue;
+        const int lo = max(r0, a.peer_lo[p]), hi = min(min(r0 + g.tile_h, BH), a.peer_hi[p]);
+        if (lo >= hi) continue;
+        const int qlo = lo + a.peer_dst[p] - a.peer_lo[p], qhi = hi + a.peer_dst[p] - a.peer_lo[p];
+        const int th = a.peer_tile_h[p], tw = a.peer_tile_w[p], hr = a.peer_halo_r[p], hc = a.peer_halo_c[p];
+        const int cl = c0, ch = min(c0 + g.tile_w, W);
+        // tiles whose region [t*th - hr, (t+1)*th + hr) meets [qlo, qhi) (columns alike)
+        const int ty0 = qlo - hr <= 0 ? 0 : (qlo - hr) / th, ty1 = min(a.peer_tiles_y[p] - 1, (qhi + hr + th - 1) / th - 1);
+        const int tx0 = cl - hc <= 0 ? 0 : (cl - hc) / tw, tx1 = min(a.peer_tiles_x[p] - 1, (ch + hc + tw - 1) / tw - 1);
+        for (int ty = ty0; ty <= ty1; ++ty)
+          for (int tx = tx0; tx <= tx1; ++tx) {
+            const int id = ty * a.peer_tiles_x[p] + tx;  // (shards hold one env)
+            if (atomicExch_system(a.peer_queued[p] + id, a.peer_stamp[p]) != a.peer_stamp[p])
+              a.peer_next_list[p][atomicAdd_system(a.peer_next_count[p], 1)] = id;
+          }
+      }
+    } else if (streak < 2 || exposed_t) {
       enqueue(bxi, byi);
     }
   }
@@ -650,17 +675,14 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
 
 template <int MODE, int WPRC, int DIMC = 0>
 cudaError_t launch_wp(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(k_step_warp<MODE, WPRC, DIMC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sm));
+  const void* kern = reinterpret_cast<const void*>(k_step_warp<MODE, WPRC, DIMC>);
+  cudaError_t e = smem_opt_in(kern, sm);
   if (e != cudaSuccess) return e;
   if (a.list_mode == 2) {  // persistent: one wave of CTAs over the work list
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_warp<MODE, WPRC, DIMC>, kWpThreads, sm);
+    int wave = 0;
+    e = resident_ctas(kern, kWpThreads, sm, &wave);
     if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int ctas = std::max(1, std::min(a.tiles_total, std::max(1, per_sm) * sms));
+    const int ctas = std::max(1, std::min(a.tiles_total, wave));
     k_step_warp<MODE, WPRC, DIMC><<<ctas, kWpThreads, sm, s>>>(a, g);
     return cudaGetLastError();
   }
@@ -696,6 +718,56 @@ cudaError_t launch_tile_counts(const int32_t* trec, int n_envs, int tiles_per_en
   const int bx = std::max(1, std::min(64, (tiles_per_env + 255) / 256));
   k_tile_counts<<<dim3(bx, n_envs), 256, 0, s>>>(reinterpret_cast<const int4*>(trec), tiles_per_env, counts);
   return cudaGetLastError();
+}
+
+namespace {
+struct LaunchKey {
+  const void* f;
+  int dev;
+  size_t smem;
+  int threads;
+  bool operator==(const LaunchKey& o) const { return f == o.f && dev == o.dev && smem == o.smem && threads == o.threads; }
+};
+struct LaunchKeyHash {
+  size_t operator()(const LaunchKey& k) const {
+    return std::hash<const void*>()(k.f) ^ (static_cast<size_t>(k.dev) << 48) ^ (k.smem * 0x9E3779B97F4A7C15ull) ^
+           static_cast<size_t>(k.threads);
+  }
+};
+std::mutex g_launch_mu;
+std::unordered_map<LaunchKey, int, LaunchKeyHash> g_smem_set;   // (f, dev) -> largest size opted in
+std::unordered_map<LaunchKey, int, LaunchKeyHash> g_wave;       // (f, dev, smem, threads) -> CTAs per GPU
+}  // namespace
+
+cudaError_t smem_opt_in(const void* kernel, size_t smem) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_launch_mu);
+  int& have = g_smem_set[LaunchKey{kernel, dev, 0, 0}];
+  if (static_cast<size_t>(have) >= smem) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e == cudaSuccess) have = static_cast<int>(smem);
+  return e;
+}
+
+cudaError_t resident_ctas(const void* kernel, int threads, size_t smem, int* ctas_per_gpu) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_launch_mu);
+  const LaunchKey key{kernel, dev, smem, threads};
+  auto it = g_wave.find(key);
+  if (it == g_wave.end()) {
+    int per_sm = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    it = g_wave.emplace(key, std::max(1, per_sm) * sms).first;
+  }
+  *ctas_per_gpu = it->second;
+  return cudaSuccess;
 }
 
 size_t warp_smem_bytes(int h, int w) {

@@ -1,7 +1,7 @@
 """C3 (16384^2 x 500 steps) as G fused row shards on ONE device vs the unsharded batch: wall time of
 step(500) + sync (launches of all shards issued from one host thread), the share of tile launches
 actually stepped (quiet tiles skipped), and bitwise equality of the final layers.  All shards share
-one GPU, so this measures the sharding overhead (halo exchange, exposed boundary tiles), not
+one GPU, so this measures the sharding overhead (halo exchange, the boundary tiles near the halo rows), not
 multi-GPU scaling.   python scripts/c3_shards.py [size] [steps]"""
 import os
 import sys
@@ -40,7 +40,7 @@ _, veg, den = eb.worldcover_palette()
 t = eb.Terrain(fc, el, np.array([6.0]), np.array([0.0]), veg, den)
 for g in (1, 2, 4, 8):
     sh = ShardedLandscape(t, g, fused=True)
-    ms = []
+    ms, issue = [], []
     for rep in range(4):
         sh.set_state(init)
         sh.set_key(0, 0, 0)
@@ -49,10 +49,11 @@ for g in (1, 2, 4, 8):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         sh.step(steps)
+        issue.append(1e3 * (time.perf_counter() - t0))
         sh.sync()
         ms.append(1e3 * (time.perf_counter() - t0))
     run = sum(bb.diag()["tiles_processed"] for bb in sh.batches)
     tot = sum(bb.diag()["tiles_launched"] for bb in sh.batches)
     ok = np.array_equal(sh.get_state(), ref)
-    print(f"G={g} fused: {np.median(ms[1:]):.2f} ms  tiles stepped {run / max(tot, 1):.3f}  equal={ok}", flush=True)
+    print(f"G={g} fused: {np.median(ms[1:]):.2f} ms (host issue {np.median(issue[1:]):.2f})  tiles stepped {run / max(tot, 1):.3f}  equal={ok}", flush=True)
     del sh

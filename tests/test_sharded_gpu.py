@@ -40,6 +40,49 @@ def test_sharded_equals_unsharded(port, g, halo, fused):
     assert np.array_equal(want, O.run(port, "port", gp, O.DEFAULT_CFG, seed, 0, 0, steps, init[0]))
 
 
+@pytest.mark.parametrize("direction", [0.0, 90.0, 270.0])
+@pytest.mark.parametrize("g", [2, 4, 6])
+def test_fire_across_shard_boundaries_small_tiles(g, direction):
+    """The tile records travel with the halo rows (ember_warp.cu: a burning tile enqueues the
+    neighbour shard's tiles next to the rows it stores there): fires lit on every band boundary,
+    small 16 x 64 tiles with 4-row light cones (so many quiet tiles sit next to the halo rows),
+    several calls -- equal to the unsharded run, and tiles really are skipped."""
+    h, w, seed = 480, 256, 11
+    t = eb.synth_terrain(seed, 1, h, w)
+    t.wind_speed[:] = 8.0
+    t.wind_direction[:] = direction
+    init = eb.synth_ignitions(seed, t, 4)
+    burnable = t.class_veg[t.fuel_class[0]] > -1.0
+    for k in range(1, g):  # both sides of every band edge
+        edge = k * h // g
+        for r in (edge - 2, edge - 1, edge, edge + 1):
+            for c in range(7, w, 61):
+                if burnable[r, c]:
+                    init[0, r, c] = 1
+    full = eb.Batch(1, h, w)
+    full.set_terrain(t.fuel_class, t.elevation, t.class_veg, t.class_den, 30.0)
+    full.set_wind(t.wind_speed, t.wind_direction)
+    full.set_state(init)
+    full.set_key(seed, 0, first_stream=0)
+    sh = ShardedLandscape(t, g, halo=4, fused=True)
+    for b in sh.batches:
+        b.set_tiling(16, 64, 4)
+        b.diag(reset=True)
+    sh.set_state(init[0])
+    sh.set_key(seed, 0, 0)
+    for n in (37, 60, 83):
+        full.step(n)
+        sh.step(n)
+        want = full.get_state()[0]
+        got = sh.get_state()
+        assert np.array_equal(got, want), (n, np.argwhere(got != want)[:5])
+        tot = sum(b.counts()[0] for b in sh.batches)
+        assert tot[:3].tolist() == [int((want == k).sum()) for k in range(3)]
+    run = sum(b.diag()["tiles_processed"] for b in sh.batches)
+    launched = sum(b.diag()["tiles_launched"] for b in sh.batches)
+    assert run < 0.9 * launched, (run, launched)
+
+
 def test_rows_device_roundtrip():
     import torch
     b = eb.Batch(2, 40, 64)
@@ -105,7 +148,8 @@ def test_c3_4096_500_steps_quiet_tiles_vs_reference():
     """The C3 geometry at 4096^2 x 500 steps (C3 generator, wind 6 from the west, 64 ignitions):
     the production path (63 halo-tiled launches of 8 steps, quiet tiles skipped outright) equals
     the reference's own run_stochastic (oracle/_ref, OpenMP) bit for bit, counts included; then
-    fused row shards G = 2 / 4 / 8 (quiet tiles kept across the chunks, boundary tiles exposed)
+    fused row shards G = 2 / 4 / 8 (quiet tiles kept across the chunks, the boundary tiles' records
+    exchanged with the halo rows)
     and the per-rank form (step + halo-row copies, records carried across calls) equal it too.
     Every run really skips tiles (tile statistics)."""
     R = O.ref()
