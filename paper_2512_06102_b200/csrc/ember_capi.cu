@@ -1308,6 +1308,24 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
   }();
   std::vector<ebl::StepArgs> args(n_shards);
   std::vector<char> listed(n_shards, 0);
+  // shards sharing one device run on shard 0's stream (stream order replaces the per-chunk
+  // events), and a chunk whose shards are all on work lists is ONE launch (k_step_warp_shards)
+  bool single = n_shards <= ebl::kMaxShardLaunch;
+  for (int s = 1; s < n_shards; ++s) single = single && shards[s]->device == shards[0]->device;
+  cudaStream_t S0 = shards[0]->stream;
+  auto strm = [&](int s) { return single ? S0 : shards[s]->stream; };
+  if (single)
+    for (int s = 1; s < n_shards; ++s) {  // the shards' pending work precedes the call
+      EBL_CUDA(cudaEventRecord(shards[s]->shard_ev[0], shards[s]->stream));
+      EBL_CUDA(cudaStreamWaitEvent(S0, shards[s]->shard_ev[0], 0));
+    }
+  EBL_CUDA(cudaSetDevice(shards[0]->device));
+  int cur_dev = shards[0]->device;
+  auto set_dev = [&](int d) -> cudaError_t {
+    if (d == cur_dev) return cudaSuccess;
+    cur_dev = d;
+    return cudaSetDevice(d);
+  };
   int chunk = 0;
   for (int done = 0; done < n_steps; ++chunk) {
     int k = n_shards > 1 ? std::min(halo, n_steps - done) : n_steps - done;
@@ -1332,16 +1350,16 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
     // the neighbours' marks need)
     for (int s = 0; s < n_shards; ++s) {
       ebl_batch* b = shards[s];
-      EBL_CUDA(cudaSetDevice(b->device));
+      EBL_CUDA(set_dev(b->device));
       // the neighbours' launches of the previous chunk (all waits precede this chunk's records)
-      for (int q = s - 1; q <= s + 1 && chunk > 0; q += 2)
+      for (int q = s - 1; q <= s + 1 && chunk > 0 && !single; q += 2)
         if (q >= 0 && q < n_shards)
           EBL_CUDA(cudaStreamWaitEvent(b->stream, shards[q]->shard_ev[(chunk - 1) & 1], 0));
       ebl::BlockGeom& g = geo[s];
       g.n_steps = k;
       ebl::StepArgs a = step_args(b);
       if (done + k == n_steps) {  // counts of the last launch only
-        EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, 4 * sizeof(int32_t), b->stream));
+        EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, 4 * sizeof(int32_t), strm(s)));
         a.counts = b->counts.p;
       }
       a.store_lo = b->band_lo;
@@ -1358,14 +1376,14 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
           if (b->trec.n < nt * 4 || b->tqueued.n < nt) {
             EBL_CUDA(b->trec.alloc(nt * 4));
             EBL_CUDA(b->tqueued.alloc(nt));
-            EBL_CUDA(cudaMemsetAsync(b->tqueued.p, 0, nt * sizeof(int32_t), b->stream));
+            EBL_CUDA(cudaMemsetAsync(b->tqueued.p, 0, nt * sizeof(int32_t), strm(s)));
             b->list_stamp = 0;
           }
           for (auto& l : b->tlist)
             if (l.n < nt) EBL_CUDA(l.alloc(nt));
           if (b->tcount.n < 6) EBL_CUDA(b->tcount.alloc(6));
           const int L = ++list_launch[s];
-          if (L == 0) EBL_CUDA(cudaMemsetAsync(b->tcount.p, 0, 6 * sizeof(int32_t), b->stream));
+          if (L == 0) EBL_CUDA(cudaMemsetAsync(b->tcount.p, 0, 6 * sizeof(int32_t), strm(s)));
           const int c3 = L % 3;
           a.list_mode = L == 0 ? 1 : 2;
           a.trec = b->trec.p;
@@ -1404,16 +1422,23 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
     }
     // the listed shards' first-launch counter resets are on their own streams: a neighbour's first
     // marks wait for them (slot 1 plays "chunk -1")
-    if (chunk == 0)
+    if (chunk == 0 && !single)
       for (int s = 0; s < n_shards; ++s) {
-        EBL_CUDA(cudaSetDevice(shards[s]->device));
+        EBL_CUDA(set_dev(shards[s]->device));
         EBL_CUDA(cudaEventRecord(shards[s]->shard_ev[1], shards[s]->stream));
       }
+    // one launch for the chunk: every shard on the same device and on its work list
+    bool fused_launch = single && n_shards > 1 && use_warp(shards[0]);
+    for (int s = 0; s < n_shards && fused_launch; ++s)
+      fused_launch = listed[s] && args[s].list_mode == args[0].list_mode && use_warp(shards[s]) &&
+                     shards[s]->mode == shards[0]->mode;
+    ebl::ShardsLaunch multi{};
+    multi.all_tiles = args[0].list_mode == 1;
     // pass 2: peer stores and marks, launch
     for (int s = 0; s < n_shards; ++s) {
       ebl_batch* b = shards[s];
-      EBL_CUDA(cudaSetDevice(b->device));
-      if (chunk == 0)
+      EBL_CUDA(set_dev(b->device));
+      if (chunk == 0 && !single)
         for (int q = s - 1; q <= s + 1; q += 2)
           if (q >= 0 && q < n_shards) EBL_CUDA(cudaStreamWaitEvent(b->stream, shards[q]->shard_ev[1], 0));
       const ebl::BlockGeom& g = geo[s];
@@ -1450,12 +1475,27 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
       a.halo_marked = marked && halo_marks ? 1 : 0;
       if (!halo_marks)
         for (int p = 0; p < a.n_peers; ++p) a.peer_queued[p] = nullptr;
-      EBL_CUDA(launch_ca(b, a, g, b->stream));
+      if (fused_launch) {
+        multi.sa[s] = a;
+        multi.g[s] = g;
+        multi.n = s + 1;
+        continue;
+      }
+      EBL_CUDA(launch_ca(b, a, g, strm(s)));
       if (list_launch[s] >= 0 && done + k == n_steps) {  // U/B/X of the band from the in-place records
         const int tx = (b->w + g.tile_w - 1) / g.tile_w, ty = (b->h + g.tile_h - 1) / g.tile_h;
-        EBL_CUDA(ebl::launch_tile_counts(b->trec.p, b->n_envs, tx * ty, b->counts.p, b->stream));
+        EBL_CUDA(ebl::launch_tile_counts(b->trec.p, b->n_envs, tx * ty, b->counts.p, strm(s)));
       }
-      EBL_CUDA(cudaEventRecord(b->shard_ev[chunk & 1], b->stream));
+      if (!single) EBL_CUDA(cudaEventRecord(b->shard_ev[chunk & 1], b->stream));
+    }
+    if (fused_launch) {
+      EBL_CUDA(ebl::launch_step_warp_shards(multi, shards[0]->mode, S0));
+      for (int s = 0; s < n_shards && done + k == n_steps; ++s) {
+        const ebl_batch* b = shards[s];
+        const ebl::BlockGeom& g = geo[s];
+        const int tx = (b->w + g.tile_w - 1) / g.tile_w, ty = (b->h + g.tile_h - 1) / g.tile_h;
+        EBL_CUDA(ebl::launch_tile_counts(b->trec.p, b->n_envs, tx * ty, b->counts.p, S0));
+      }
     }
     for (int s = 0; s < n_shards; ++s) {
       ebl_batch* b = shards[s];
@@ -1468,6 +1508,11 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
     done += k;
   }
   // the last launches' peer rows land before anything else on each shard's stream
+  if (single) {
+    EBL_CUDA(cudaEventRecord(shards[0]->shard_ev[0], S0));
+    for (int s = 1; s < n_shards; ++s) EBL_CUDA(cudaStreamWaitEvent(shards[s]->stream, shards[0]->shard_ev[0], 0));
+    return EBL_OK;
+  }
   for (int s = 0; s < n_shards && chunk > 0; ++s) {
     EBL_CUDA(cudaSetDevice(shards[s]->device));
     for (int q = s - 1; q <= s + 1; q += 2)

@@ -32,6 +32,7 @@ cudaError_t launch_step_blocked(const StepArgs& a, int mode, const BlockGeom& g,
 size_t warp_smem_bytes(int h, int w);
 bool warp_fits(int h, int w);
 cudaError_t launch_step_warp(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s);
+cudaError_t launch_step_warp_shards(const ShardsLaunch& p, int mode, cudaStream_t s);
 cudaError_t launch_tile_counts(const int32_t* trec, int n_envs, int tiles_per_env, int32_t* counts, cudaStream_t s);
 
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s);

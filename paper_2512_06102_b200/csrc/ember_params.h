@@ -110,6 +110,17 @@ struct BlockGeom {
   int envs_per_cta;  // 1 (the blocked kernel's env pooling was measured slower and removed)
 };
 
+// Row shards sharing one device (ebl_shards_step): one work-list launch for all of them -- the
+// persistent CTAs take tiles from the shards' lists in order (k_step_warp_shards), so a chunk costs
+// one launch instead of one per shard.  Passed as a __grid_constant__ kernel parameter.
+constexpr int kMaxShardLaunch = 8;
+struct ShardsLaunch {
+  StepArgs sa[kMaxShardLaunch];
+  BlockGeom g[kMaxShardLaunch];
+  int n;
+  int all_tiles;  // first launch of a call (list_mode 1): every tile of every shard, no lists read
+};
+
 // Deterministic mode + adjoint (ember_det.cu).  fp64 planes [env][cell] (the
 // reference's trajectory is ulp-sensitive, so parity needs its exact fp64 arithmetic).
 struct DetArgs {

@@ -673,6 +673,56 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
   }
 }
 
+// Work-list launch of several row shards on one device: the persistent CTAs claim items of the
+// concatenated lists (shard 0's cursor), item -> (shard, tile) by the list counts' prefix.  Each
+// region runs with its shard's StepArgs, read in place from the kernel parameter block.
+template <int MODE, int WPRC>
+__global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp_shards(const __grid_constant__ ShardsLaunch P) {
+  __shared__ int s_pref[kMaxShardLaunch + 1];
+  __shared__ int s_item;
+  if (blockIdx.x == 0 && threadIdx.x < P.n) {
+    *P.sa[threadIdx.x].list_zero0 = 0;
+    *P.sa[threadIdx.x].list_zero1 = 0;
+    if (P.sa[threadIdx.x].diag && !P.all_tiles)  // (list_mode 1 regions count themselves)
+      atomicAdd(P.sa[threadIdx.x].diag + 3, static_cast<unsigned long long>(P.sa[threadIdx.x].tiles_total));
+  }
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int s = 0; s < P.n; ++s) {
+      s_pref[s] = acc;
+      acc += P.all_tiles ? P.sa[s].tiles_total : *P.sa[s].tile_count;
+    }
+    s_pref[P.n] = acc;
+  }
+  for (;;) {
+    __syncthreads();  // the previous region's shared state is consumed (and s_pref written)
+    if (threadIdx.x == 0) s_item = atomicAdd(P.sa[0].list_cursor, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= s_pref[P.n]) break;
+    int sh = 0;
+    while (item >= s_pref[sh + 1]) ++sh;
+    const StepArgs& a = P.sa[sh];
+    const int tile = P.all_tiles ? item - s_pref[sh] : a.tile_list[item - s_pref[sh]];
+    const int bx = tile % a.tiles_x, rest = tile / a.tiles_x;
+    warp_region<MODE, WPRC, 0>(a, P.g[sh], rest / a.tiles_y, bx, rest % a.tiles_y, a.tiles_x, a.tiles_y);
+  }
+}
+
+template <int MODE, int WPRC>
+cudaError_t launch_wp_shards(const ShardsLaunch& P, size_t sm, cudaStream_t s) {
+  const void* kern = reinterpret_cast<const void*>(k_step_warp_shards<MODE, WPRC>);
+  cudaError_t e = smem_opt_in(kern, sm);
+  if (e != cudaSuccess) return e;
+  int wave = 0;
+  e = resident_ctas(kern, kWpThreads, sm, &wave);
+  if (e != cudaSuccess) return e;
+  int tiles = 0;
+  for (int i = 0; i < P.n; ++i) tiles += P.sa[i].tiles_total;
+  k_step_warp_shards<MODE, WPRC><<<std::max(1, std::min(tiles, wave)), kWpThreads, sm, s>>>(P);
+  return cudaGetLastError();
+}
+
 template <int MODE, int WPRC, int DIMC = 0>
 cudaError_t launch_wp(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStream_t s) {
   const void* kern = reinterpret_cast<const void*>(k_step_warp<MODE, WPRC, DIMC>);
@@ -781,6 +831,28 @@ bool warp_fits(int h, int w) {
 }
 
 // Any geometry plan_blocks produces with one env per CTA (whole env, or halo tiles).
+cudaError_t launch_step_warp_shards(const ShardsLaunch& P, int mode, cudaStream_t s) {
+  size_t sm = 0;
+  bool whole_width = true;
+  for (int i = 0; i < P.n; ++i) {
+    const StepArgs& a = P.sa[i];
+    const BlockGeom& g = P.g[i];
+    const int rh = a.h < g.tile_h + 2 * g.halo_rows ? a.h : g.tile_h + 2 * g.halo_rows;
+    const int rw = a.w < g.tile_w + 2 * g.halo_cols ? a.w : g.tile_w + 2 * g.halo_cols;
+    sm = std::max(sm, warp_smem_bytes(rh, rw));
+    whole_width = whole_width && g.tile_w >= a.w;
+  }
+  const int wpr = (P.sa[0].w + 31) / 32;
+  if (mode == kStaticTables) {
+    if (whole_width && wpr == 4) return launch_wp_shards<kStaticTables, 4>(P, sm, s);
+    if (whole_width && wpr == 2) return launch_wp_shards<kStaticTables, 2>(P, sm, s);
+    return launch_wp_shards<kStaticTables, 0>(P, sm, s);
+  }
+  if (whole_width && wpr == 4) return launch_wp_shards<kStaticTerrain, 4>(P, sm, s);
+  if (whole_width && wpr == 2) return launch_wp_shards<kStaticTerrain, 2>(P, sm, s);
+  return launch_wp_shards<kStaticTerrain, 0>(P, sm, s);
+}
+
 cudaError_t launch_step_warp(const StepArgs& a, int mode, const BlockGeom& g, cudaStream_t s) {
   const int rh = a.h < g.tile_h + 2 * g.halo_rows ? a.h : g.tile_h + 2 * g.halo_rows;
   const int rw = a.w < g.tile_w + 2 * g.halo_cols ? a.w : g.tile_w + 2 * g.halo_cols;

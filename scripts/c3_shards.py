@@ -16,6 +16,8 @@ from paper_2512_06102_b200.sharded import ShardedLandscape  # noqa: E402
 
 size = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 500
+shard_counts = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 2, 4, 8]
+reps = int(os.environ.get("C3_REPS", "4"))
 b = eb.Batch(1, size, size)
 b.synth_terrain(0)
 b.set_wind([6.0], [0.0])
@@ -23,7 +25,7 @@ b.synth_ignitions(0, 64)
 init = b.get_state()[0]
 fc, el = b.get_terrain()
 ms = []
-for rep in range(4):
+for rep in range(reps):
     b.set_state(init)
     b.set_key(0, 0)
     b.diag(reset=True)
@@ -34,14 +36,14 @@ for rep in range(4):
     ms.append(1e3 * (time.perf_counter() - t0))
 d = b.diag()
 ref = b.get_state()[0]
-print(f"unsharded: {np.median(ms[1:]):.2f} ms  tiles stepped {d['tiles_processed'] / d['tiles_launched']:.3f}", flush=True)
+print(f"unsharded: {np.median(ms[1:] or ms):.2f} ms  tiles stepped {d['tiles_processed'] / d['tiles_launched']:.3f}", flush=True)
 b.close()
 _, veg, den = eb.worldcover_palette()
 t = eb.Terrain(fc, el, np.array([6.0]), np.array([0.0]), veg, den)
-for g in (1, 2, 4, 8):
+for g in shard_counts:
     sh = ShardedLandscape(t, g, fused=True)
     ms, issue = [], []
-    for rep in range(4):
+    for rep in range(reps):
         sh.set_state(init)
         sh.set_key(0, 0, 0)
         for bb in sh.batches:
@@ -55,5 +57,5 @@ for g in (1, 2, 4, 8):
     run = sum(bb.diag()["tiles_processed"] for bb in sh.batches)
     tot = sum(bb.diag()["tiles_launched"] for bb in sh.batches)
     ok = np.array_equal(sh.get_state(), ref)
-    print(f"G={g} fused: {np.median(ms[1:]):.2f} ms (host issue {np.median(issue[1:]):.2f})  tiles stepped {run / max(tot, 1):.3f}  equal={ok}", flush=True)
+    print(f"G={g} fused: {np.median(ms[1:] or ms):.2f} ms (host issue {np.median(issue[1:] or issue):.2f})  tiles stepped {run / max(tot, 1):.3f}  equal={ok}", flush=True)
     del sh
