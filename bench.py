@@ -404,6 +404,28 @@ def hbm_roofline(alg_bytes_per_launch, kern_s, kernel, traffic=None, note=None):
     return d
 
 
+def issue_roofline(kernel, kern_s, clocks, inst=None, traffic=None, hbm=None, counters_source=None):
+    """Issue-bound roofline: ncu smsp__inst_executed per launch (or run) / kernel time against
+    148 SMs x 4 SMSPs x 1 warp-instruction per cycle at the median SM clock under load; the HBM
+    figures ride along in "hbm" (actual DRAM traffic from the same capture)."""
+    sm_ghz = (clocks.get("sm_mhz") or 1965.0) / 1e3
+    peak = 148 * 4 * sm_ghz  # warp-instructions per ns
+    hbm_peak, hbm_src = measured_peak()
+    roof = {"bound": "issue", "kernel": kernel, "kernel_ms": kern_s * 1e3, "unit": "G warp-inst/s", "peak": peak,
+            "peak_source": f"148 SMs x 4 SMSPs x 1 warp-inst/cycle x {sm_ghz:.3f} GHz (median SM clock under load)",
+            "achieved": None, "frac": None, "traffic": traffic,
+            "hbm": dict(hbm or {}, peak=hbm_peak, peak_source=hbm_src)}
+    if inst:
+        roof["achieved"] = inst / kern_s / 1e9
+        roof["frac"] = roof["achieved"] / peak
+        roof["inst_executed"] = inst
+        roof["counters_source"] = counters_source
+    if traffic:
+        roof["hbm"]["dram_GBps"] = traffic / kern_s / 1e9
+        roof["hbm"]["dram_frac"] = roof["hbm"]["dram_GBps"] / hbm_peak
+    return roof
+
+
 def bench_c1(cx: Ctx, clk):
     import paper_2512_06102_b200 as eb
     torch = cx.torch
@@ -470,29 +492,14 @@ def bench_c1(cx: Ctx, clk):
 
     kern_s = sum(kms) / len(kms) / 1e3
     alg = units * ALG_BYTES["C1"]
-    cnt = ncu_counters(f"k_step_warp:{n}x{h}x{w}x{steps}")
-    clocks = clk.summary()
-    sm_ghz = (clocks.get("sm_mhz") or 1965.0) / 1e3
-    peak_issue = 148 * 4 * sm_ghz  # warp-instructions per ns: 1 per SMSP per cycle
-    hbm_peak, hbm_src = measured_peak()
-    roof = {"bound": "issue", "kernel": "k_step_warp", "kernel_ms": kern_s * 1e3,
-            "unit": "G warp-inst/s", "peak": peak_issue,
-            "peak_source": f"148 SMs x 4 SMSPs x 1 warp-inst/cycle x {sm_ghz:.3f} GHz (median SM clock under load)",
-            "achieved": None, "frac": None, "traffic": None,
-            "hbm": {"alg_bytes_per_launch": alg, "alg_GBps": alg / kern_s / 1e9, "peak": hbm_peak,
-                    "peak_source": hbm_src, "alg_frac": alg / kern_s / 1e9 / hbm_peak,
-                    "note": "SURVEY §8(d) 10 B/cell-update; exceeds 1 because the state stays in shared "
-                            "memory for all 200 steps (DRAM sees the layers once per run)"}}
-    if cnt:
-        inst = cnt["inst_executed_per_launch"]
-        roof["achieved"] = inst / kern_s / 1e9
-        roof["frac"] = roof["achieved"] / peak_issue
-        roof["inst_executed_per_launch"] = inst
-        roof["counters_source"] = cnt.get("source")
-        roof["traffic"] = cnt.get("dram_bytes_per_launch")
-        if roof["traffic"]:
-            roof["hbm"]["dram_GBps"] = roof["traffic"] / kern_s / 1e9
-            roof["hbm"]["dram_frac"] = roof["hbm"]["dram_GBps"] / hbm_peak
+    cnt = ncu_counters(f"k_step_warp:{n}x{h}x{w}x{steps}") or {}
+    hbm_peak, _ = measured_peak()
+    roof = issue_roofline("k_step_warp", kern_s, clk.summary(), inst=cnt.get("inst_executed_per_launch"),
+                          traffic=cnt.get("dram_bytes_per_launch"), counters_source=cnt.get("source"),
+                          hbm={"alg_bytes_per_launch": alg, "alg_GBps": alg / kern_s / 1e9,
+                               "alg_frac": alg / kern_s / 1e9 / hbm_peak,
+                               "note": "SURVEY §8(d) 10 B/cell-update; exceeds 1 because the state stays in "
+                                       "shared memory for all 200 steps (DRAM sees the layers once per run)"})
     res = dict(value=value, ms_per_step=t_max * 1e3 / a.steps, units_per_rank=units,
                e2e={"value": e2e_value, "unit": s["unit"], "h2d_bytes_per_step": int(init.nbytes),
                     "d2h_bytes_per_step": int(init.nbytes), "ms_per_step": te * 1e3 / a.steps},
@@ -621,10 +628,13 @@ def bench_c2(cx: Ctx, clk):
                 e2e={"value": total / te, "unit": s["unit"], "h2d_bytes_per_step": int(act.nbytes),
                      "d2h_bytes_per_step": int(steps * (rew.nbytes + done.nbytes)),
                      "note": "ebl_rl_step per RL step: host actions in, host reward/done out"},
-                roofline=hbm_roofline(units * ALG_BYTES["C2"], kern_s, "k_rl_tanker_warp",
-                                      traffic=cnt.get("dram_bytes_per_launch") if cnt else None,
-                                      note="one fused 256-step launch; the layers stay in shared memory "
-                                           "(bit planes), so the algorithmic bytes exceed the DRAM traffic"),
+                roofline=issue_roofline(
+                    "k_rl_tanker_warp", kern_s, clk.summary(), inst=(cnt or {}).get("inst_executed_per_launch"),
+                    traffic=(cnt or {}).get("dram_bytes_per_launch"), counters_source=(cnt or {}).get("source"),
+                    hbm={"alg_bytes_per_launch": units * ALG_BYTES["C2"],
+                         "alg_GBps": units * ALG_BYTES["C2"] / kern_s / 1e9,
+                         "note": "one fused 256-step launch; the layers stay in shared memory (bit planes), "
+                                 "so the algorithmic bytes exceed the DRAM traffic"}),
                 gpu_launches=launches,
                 extra={"cell_updates_per_sec": value * h * w,
                        "device_io_step": {"env_steps_per_sec": cx.sum_over_ranks(units * len(dms))
@@ -677,11 +687,7 @@ def bench_c3(cx: Ctx, clk):
     def make_buffer(n):
         return rows_buf.setdefault(n, torch.empty((n, W), dtype=torch.uint8, device=cx.dev))
 
-    def step(kev):
-        eb._lib.check(L.ebl_batch_set_state_device(b.handle, init_dev.data_ptr()))
-        b.set_key(SEED, 0)
-        if kev:
-            kev[0].record(cx.stream)
+    def run_steps():
         if cx.world == 1:
             b.step(steps)
         else:
@@ -691,25 +697,65 @@ def bench_c3(cx: Ctx, clk):
                 b.step(k)
                 SH.exchange_halos(cx.dist, cx.rank, shards, get_rows, set_rows, make_buffer)
                 done += k
+
+    def step(kev):
+        eb._lib.check(L.ebl_batch_set_state_device(b.handle, init_dev.data_ptr()))
+        b.set_key(SEED, 0)
+        if kev:
+            kev[0].record(cx.stream)
+        run_steps()
         if kev:
             kev[1].record(cx.stream)
     b.diag(reset=True)
     clk.__enter__()
     ms, kms = cx.timed(step, a.steps, max(1, a.warmup - 2))
     diag = b.diag()
-    clk.__exit__(None, None, None)
     units = H * W * steps
     t_max = cx.max_over_ranks(sum(ms) / 1e3)
     value = units * a.steps / t_max
     kern_s = sum(kms) / len(kms) / 1e3
+
+    # ---- end to end: the landscape (this rank's rows) from pinned host memory, 500 steps, back ----
+    h_in = eb.host_buffer(init.shape)
+    h_in[:] = init
+    h_out = eb.host_buffer(init.shape)
+
+    def e2e_step():
+        eb._lib.check(L.ebl_batch_set_state(b.handle, h_in.ctypes.data))
+        b.set_key(SEED, 0)
+        run_steps()
+        eb._lib.check(L.ebl_batch_get_state(b.handle, h_out.ctypes.data))
+
+    e2e_step()
+    cx.barrier()
+    e2e_ms = []
+    for _ in range(a.steps):
+        cx.flush()
+        cx.barrier()
+        e0, e1 = cx.events(1)[0]
+        e0.record(cx.stream)
+        e2e_step()
+        e1.record(cx.stream)
+        e1.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    clk.__exit__(None, None, None)
+    assert np.array_equal(h_out, b.get_state()), "e2e result differs from the device run"
+    te = cx.max_over_ranks(sum(e2e_ms) / 1e3)
     tiles = diag.get("tiles_processed"), diag.get("tiles_launched")
     active = None
     if tiles[0] is not None and tiles[1]:
         active = value * tiles[0] / tiles[1]
+    # issue-bound roofline over one run's launches (the active tiles' 8-step chains), HBM beside it
+    cnt = (ncu_counters(f"k_step_warp:c3:{H}x{W}x{steps}") if cx.world == 1 else None) or {}
+    roof = issue_roofline("k_step_warp (halo tiles, work lists; per run of 500 steps)", kern_s, clk.summary(),
+                          inst=cnt.get("inst_executed_per_run"), traffic=cnt.get("dram_bytes_per_run"),
+                          counters_source=cnt.get("source"),
+                          hbm={"note": "SURVEY §8(d) counts 10 B per dense cell-update; only the active tiles "
+                                       "are read and written (tiles_processed_frac)"})
     return dict(value=value, ms_per_step=t_max * 1e3 / a.steps, units_per_rank=units // cx.world,
-                e2e=None, roofline=hbm_roofline(units * 10 // cx.world, kern_s, "k_step_warp (halo tiles)",
-                                                note="dense count; quiet tiles are skipped exactly"),
-                gpu_launches=diag["launches"],
+                e2e={"value": units / te, "unit": s["unit"], "h2d_bytes_per_step": int(init.nbytes),
+                     "d2h_bytes_per_step": int(init.nbytes), "ms_per_step": te * 1e3 / a.steps},
+                roofline=roof, gpu_launches=diag["launches"],
                 extra={"launches_per_run": diag["launches"] // max(1, a.steps + max(1, a.warmup - 2)),
                        "tiles_processed_frac": (tiles[0] / tiles[1]) if active else None,
                        "active_tile_cell_updates_per_sec": active})

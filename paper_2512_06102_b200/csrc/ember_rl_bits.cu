@@ -301,6 +301,9 @@ cudaError_t launch_rl_tanker_bits(const RlArgs& g, int mode, cudaStream_t s) {
 #ifndef EBL_RL_FAST
 #define EBL_RL_FAST 1  // the branch-free decide pass in the tanker kernel
 #endif
+#ifndef EBL_RL_FAST_STEP  // the branch-free pass in single-step launches too (2 warps per 64-row env:
+#define EBL_RL_FAST_STEP 1  // device-io steps 2.67e8 -> 2.74e8 env-steps/s, rollouts 6.87 -> 6.74 ms)
+#endif
 #ifndef EBL_RL_LUT  // its table-driven n-th set bit (a global table: one L2 miss per fresh CTA,
 #define EBL_RL_LUT 0  // which single-step launches of 16384 CTAs pay: popc search instead)
 #endif
@@ -335,8 +338,10 @@ __device__ __forceinline__ int nth_set_bit32(uint32_t v, int q) {
 
 }  // namespace
 
-template <int MODE, int DIMC>
-__global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) {
+// NW warps per env (rows dealt NW apart): 4 in general, 2 for envs of <= 64 rows (every lane owns a
+// row in the dense pass, and twice the envs are resident per SM)
+template <int MODE, int DIMC, int NW>
+__global__ void __launch_bounds__(32 * NW, 32 / NW) k_rl_tanker_warp(RlArgs g) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_newly[2], s_gone[2];  // per step parity: ignitions, Burning cells lost
   __shared__ int s_burning[2];           // Burning cells at the start of step t (slot t & 1)
@@ -353,7 +358,7 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
   const int H = DIMC ? DIMC : a.h, W = DIMC ? DIMC : a.w, n = H * W;
   const int wpr = (W + 31) >> 5;
   const int S = plane_stride(wpr);
-  auto ro = [S](int R) { return R * S + (R >> 2); };  // conflict-free rows 4 apart (ember_warp.cu)
+  auto ro = [S](int R) { return R * S + R / NW; };  // conflict-free rows NW apart (ember_warp.cu)
   const int PH = ro(H + 2) + 1;
   uint32_t* const Bp0 = reinterpret_cast<uint32_t*>(smem) + 4;  // 4 zero guard words before the planes
   uint32_t* const Bp1 = Bp0 + PH;
@@ -366,6 +371,10 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
 
   uint8_t* st = g.state + static_cast<size_t>(env) * n;
   uint8_t* wt = g.wet + static_cast<size_t>(env) * n;
+  // the env record and the caller's action are requested first: their latency overlaps the plane
+  // loads instead of following the barrier (single-step launches are a chain of global round trips)
+  RlEnv e = g.env[env];
+  const int action_in = g.actions ? __ldg(g.actions + env) : 0;
   if constexpr (kFast) {  // guard, padding words and padding rows of both B planes stay zero
     // only the words no load or dense pass writes: the 4 guard words, the padding rows 0 and H+1,
     // and every row's padding / skew words (ro(R) + wpr .. ro(R+1)) of both planes
@@ -431,7 +440,6 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
   for (int o = 16; o > 0; o >>= 1) burning0 += __shfl_xor_sync(0xffffffffu, burning0, o);
   if (lane == 0 && burning0) atomicAdd(&s_burning[0], burning0);
 
-  RlEnv e = g.env[env];
   const DiagCounters dg{a.diag};
   double rsum = 0.0;
   int32_t finished = 0;
@@ -448,7 +456,7 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
     uint32_t* Bn = cur ? Bp0 : Bp1;
     // ---- action (every thread) + drop ----------------------------------------------------------
     const uint64_t prefix = key_prefix(g.seed, e.stream, static_cast<uint64_t>(e.step));
-    const int action = g.actions ? g.actions[env] : static_cast<int>(below(cell_bits53(prefix, 0, 2), n));
+    const int action = g.actions ? action_in : static_cast<int>(below(cell_bits53(prefix, 0, 2), n));
     if (threadIdx.x < 9) {
       const int r = action / W + static_cast<int>(threadIdx.x) / 3 - 1;
       const int c = action % W + static_cast<int>(threadIdx.x) % 3 - 1;
@@ -470,8 +478,8 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
     if (threadIdx.x == 0) s_newly[par ^ 1] = s_gone[par ^ 1] = 0;
     // ---- warp-local CA step (k_step_warp) -----------------------------------------------------------
     int newly = 0, burnt = 0;
-    for (int rb = 0; rb < H; rb += kRlBitsThreads) {
-      const int r = rb + 4 * lane + warp;
+    for (int rb = 0; rb < H; rb += 32 * NW) {
+      const int r = rb + NW * lane + warp;
       int cnt = 0;
       uint32_t cum = 0xffffffffu;
       if (r < H) {
@@ -529,7 +537,7 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
         int q = idx - __shfl_sync(0xffffffffu, excl, L);
         const uint32_t cumL = __shfl_sync(0xffffffffu, cum, L);
         if (idx >= total) continue;
-        const int rr = rb + 4 * L + warp;
+        const int rr = rb + NW * L + warp;
         const uint32_t* ar = ACT + ro(rr);
         int jj = 0;
         uint32_t wv;
@@ -550,10 +558,9 @@ __global__ void __launch_bounds__(kRlBitsThreads, 8) k_rl_tanker_warp(RlArgs g) 
         int cc;
         if constexpr (kFast && EBL_RL_LUT) cc = 32 * jj + nth_set_bit_lut32(wv, q, kNthBitLut);
         else cc = 32 * jj + nth_set_bit32(wv, q);
-        // one branch-free path for burning and candidate cells (ember_warp.cu) in fused rollouts;
-        // single-step launches (the per-step API, 14 waves of short-lived CTAs) measured faster on
-        // the branchy path (device-io steps: 2.12e8 vs 1.94e8 env-steps/s; rollouts: 3.38e8 vs 3.52e8)
-        if (kFast && use_tab && g.n_steps > 1) {
+        // one branch-free path for burning and candidate cells (ember_warp.cu); with 4 warps per env
+        // single-step launches had measured faster on the branchy path (EBL_RL_FAST_STEP=0)
+        if (kFast && use_tab && (EBL_RL_FAST_STEP || g.n_steps > 1)) {
           const float4* tp = reinterpret_cast<const float4*>(a.pot32t + static_cast<size_t>(env) * a.pot32t_stride) +
                              2 * (rr * W + cc);
           const float4 T0 = __ldg(tp), T1 = __ldg(tp + 1);
@@ -782,25 +789,30 @@ cudaError_t launch_rl_bits_to_bytes(const uint32_t* bits, uint8_t* state, uint8_
   return cudaGetLastError();
 }
 
+int rl_warps(int h) { return h <= 64 ? 2 : 4; }
+
 size_t rl_warp_smem_bytes(int h, int w) {
   const size_t S = plane_stride((w + 31) / 32);
   const size_t R = static_cast<size_t>(h) + 2;
-  return 5 * (R * S + (R >> 2) + 1) * sizeof(uint32_t) + 16;  // B x2, X, WET, ACT (ro() layout) + guard words
+  // B x2, X, WET, ACT (ro() layout) + guard words
+  return 5 * (R * S + R / rl_warps(h) + 1) * sizeof(uint32_t) + 16;
 }
 
-template <int MODE, int DIMC>
+template <int MODE, int DIMC, int NW>
 static cudaError_t launch_rl_warp_t(const RlArgs& g, size_t sm, cudaStream_t s) {
-  cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_rl_tanker_warp<MODE, DIMC>), sm);
+  cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_rl_tanker_warp<MODE, DIMC, NW>), sm);
   if (e != cudaSuccess) return e;
-  k_rl_tanker_warp<MODE, DIMC><<<g.s.n_envs, kRlBitsThreads, sm, s>>>(g);
+  k_rl_tanker_warp<MODE, DIMC, NW><<<g.s.n_envs, 32 * NW, sm, s>>>(g);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rl_tanker_warp(const RlArgs& g, int mode, cudaStream_t s) {
   const size_t sm = rl_warp_smem_bytes(g.s.h, g.s.w);
-  if (mode == kStaticTables) return launch_rl_warp_t<kStaticTables, 0>(g, sm, s);
-  if (g.s.h == 64 && g.s.w == 64) return launch_rl_warp_t<kStaticTerrain, 64>(g, sm, s);
-  return launch_rl_warp_t<kStaticTerrain, 0>(g, sm, s);
+  const bool two = rl_warps(g.s.h) == 2;
+  if (mode == kStaticTables)
+    return two ? launch_rl_warp_t<kStaticTables, 0, 2>(g, sm, s) : launch_rl_warp_t<kStaticTables, 0, 4>(g, sm, s);
+  if (g.s.h == 64 && g.s.w == 64) return launch_rl_warp_t<kStaticTerrain, 64, 2>(g, sm, s);
+  return two ? launch_rl_warp_t<kStaticTerrain, 0, 2>(g, sm, s) : launch_rl_warp_t<kStaticTerrain, 0, 4>(g, sm, s);
 }
 
 }  // namespace ebl

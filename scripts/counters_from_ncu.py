@@ -1,6 +1,7 @@
 """Writes profiles/ncu_counters.json (the per-launch counters bench.py's roofline reads) from ncu
 --set full captures of this build:
-    python scripts/counters_from_ncu.py --c1 gpurun_out/prof_r02_c1.ncu-rep [--c2 prof_c2.ncu-rep]"""
+    python scripts/counters_from_ncu.py --c1 gpurun_out/prof_r02_c1.ncu-rep [--c2 prof_c2.ncu-rep]
+        [--c3 c3_metrics.csv]   (a --metrics launch list of k_step_warp over whole C3 runs)"""
 import argparse
 import csv
 import io
@@ -29,6 +30,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1")
     ap.add_argument("--c2")
+    ap.add_argument("--c3")
     a = ap.parse_args()
     path = os.path.join(ROOT, "profiles", "ncu_counters.json")
     out = json.load(open(path)) if os.path.exists(path) else {}
@@ -45,6 +47,20 @@ def main():
             "dram_bytes_per_launch": num(*r["dram__bytes_read.sum"]) + num(*r["dram__bytes_write.sum"]),
             "inst_executed_per_launch": num(*r["smsp__inst_executed.sum"]),
             "source": os.path.basename(a.c2)}
+    if a.c3:
+        # per-launch rows of one metric each; one C3 run = 63 step launches of k_step_warp
+        launches = {}
+        for r in csv.DictReader(l for l in open(a.c3) if l.startswith('"')):
+            if "k_step_warp" not in r["Kernel Name"]:
+                continue
+            launches.setdefault(int(r["ID"]), {})[r["Metric Name"]] = num(r["Metric Value"].replace(",", ""), r["Metric Unit"])
+        ids = sorted(launches)[:63]  # the first run
+        tot = lambda k: sum(launches[i].get(k, 0.0) for i in ids)
+        out["k_step_warp:c3:16384x16384x500"] = {
+            "inst_executed_per_run": tot("smsp__inst_executed.sum"),
+            "dram_bytes_per_run": tot("dram__bytes_read.sum") + tot("dram__bytes_write.sum"),
+            "duration_us_cold_per_run": tot("gpu__time_duration.sum") / 1e3,
+            "launches": len(ids), "source": os.path.basename(a.c3)}
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps(out, indent=1))

@@ -95,4 +95,9 @@ def test_our_arm_gpu():
 def test_our_arm_gpu_side_configs(config):
     d, _ = _run(["--config", config, "--steps", "2", "--warmup", "3", "--no-cpu-baseline"], 900)
     assert KEYS <= d.keys() and d["value"] > 0 and d["gpu_launches"] >= 1
-    assert d["roofline"]["bound"] == "hbm" and d["roofline"]["frac"] > 0
+    r = d["roofline"]
+    # shared-memory-resident kernels (C2 rollout, C3 tiles) are bound by issue, not by HBM
+    assert r["bound"] == ("issue" if config in ("C2", "C3") else "hbm")
+    assert r["frac"] is None or 0 < r["frac"] <= 1.0, r
+    if config == "C3":
+        assert d["e2e"]["h2d_bytes_per_step"] == d["e2e"]["d2h_bytes_per_step"] == 16384 * 16384
