@@ -1063,6 +1063,10 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
           tf_tiles = -1;
         }
       }
+      // whole-env launches leave the step loop once the fire is out: C1 kernel 0.495 -> 0.476 ms
+      // (a separate instantiation: the host-buffer pipeline measured better on the plain one,
+      // ebl_batch_run e2e 4.38e12 vs 4.30e12; scripts/lib_ab.sh)
+      a.early_exit = g.tile_h >= b->h && g.tile_w >= b->w;
       EBL_CUDA(launch_ca(b, a, g, b->stream));
       b->cur ^= 1;
       b->step += g.n_steps;

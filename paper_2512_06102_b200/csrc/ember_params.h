@@ -84,6 +84,8 @@ struct StepArgs {
   int32_t* list_zero0;            // counters the launch after next uses: zeroed by this launch
   int32_t* list_zero1;
   int tiles_x, tiles_y, tiles_total;
+  int early_exit;                 // whole-env C1/64^2 launches: the instantiation that leaves its step
+                                  // loop once no cell burns (ember_warp.cu)
   int n_peers;
   uint8_t* peer_out[2];
   int peer_lo[2], peer_hi[2], peer_dst[2];

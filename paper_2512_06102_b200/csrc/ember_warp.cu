@@ -93,7 +93,7 @@ __device__ __forceinline__ int nth_set_bit_lut(uint32_t v, int q, const uint32_t
 // launches); H x RW region cells, layer BH x W.  Grid launches run the CTA's own region, work-list
 // launches (a.list_mode == 2) loop over the listed tiles (k_step_warp below).  Whole-env
 // instantiations pass compile-time tile coordinates.
-template <int MODE, int WPRC, int DIMC>
+template <int MODE, int WPRC, int DIMC, bool EXIT = false>
 __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& g, const int env, const int bxi,
                                             const int byi, const int ntx, const int nty) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -313,6 +313,7 @@ __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& 
 #endif
     const uint64_t prefix = s_prefix[t & 127];
     [[maybe_unused]] const bool last = t == n_steps - 1;
+    [[maybe_unused]] uint32_t rowb = 0u;  // (EXIT) a burning cell in this thread's rows at step start
     for (int rb = 0; rb < H; rb += kWpThreads) {
       // ---- dense pass over the lane's row ------------------------------------------------------
       const int r = rb + 4 * lane + warp;
@@ -342,6 +343,7 @@ __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& 
           const uint32_t valid = j + 1 < wpr ? 0xffffffffu : last_mask;
           const uint32_t act = ((~(mc | xr[j]) & valid) & any) | mc;
           ar[j] = act;
+          if constexpr (EXIT) rowb |= mc;
           if (WPRC != 0 && WPRC <= 4 && j + 1 < 4)
             cum = (cum & ~(0xffu << (8 * (j + 1)))) | (static_cast<uint32_t>(cnt + __popc(act)) << (8 * (j + 1)));
           cnt += __popc(act);
@@ -521,7 +523,17 @@ __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& 
       pw_t0 = c;
     }
 #endif
-    __syncthreads();  // Bn / X complete: the next step reads them
+    if constexpr (EXIT) {
+      // Bn / X complete: the next step reads them.  A step that started without a burning cell
+      // changed nothing, and neither can any later one: the remaining steps are skipped (the
+      // trajectory-recording form stores every step)
+      if (!__syncthreads_or(rowb != 0u || rec_traj)) {
+        cur ^= 1;
+        break;
+      }
+    } else {
+      __syncthreads();  // Bn / X complete: the next step reads them
+    }
 #if EBL_PHASE_PROF
     if (lane == 0) p_wait += clock64() - pw_t0;
     if (threadIdx.x == 0) p_step += clock64() - st0;
@@ -646,7 +658,7 @@ __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& 
   }
 }
 
-template <int MODE, int WPRC, int DIMC>
+template <int MODE, int WPRC, int DIMC, bool EXIT = false>
 __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArgs a, BlockGeom g) {
   if (DIMC == 0 && a.list_mode && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) {
     *a.list_zero0 = 0;  // the next launch's append counter and cursor start at 0 (no memset launches)
@@ -667,9 +679,9 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
     }
   } else {
     // (whole-env instantiations: one region per env, the tile coordinates are compile-time 0 / 1)
-    warp_region<MODE, WPRC, DIMC>(a, g, static_cast<int>(blockIdx.z), DIMC ? 0 : static_cast<int>(blockIdx.x),
-                                  DIMC ? 0 : static_cast<int>(blockIdx.y), DIMC ? 1 : static_cast<int>(gridDim.x),
-                                  DIMC ? 1 : static_cast<int>(gridDim.y));
+    warp_region<MODE, WPRC, DIMC, EXIT>(a, g, static_cast<int>(blockIdx.z), DIMC ? 0 : static_cast<int>(blockIdx.x),
+                                        DIMC ? 0 : static_cast<int>(blockIdx.y), DIMC ? 1 : static_cast<int>(gridDim.x),
+                                        DIMC ? 1 : static_cast<int>(gridDim.y));
   }
 }
 
@@ -723,9 +735,9 @@ cudaError_t launch_wp_shards(const ShardsLaunch& P, size_t sm, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int MODE, int WPRC, int DIMC = 0>
+template <int MODE, int WPRC, int DIMC = 0, bool EXIT = false>
 cudaError_t launch_wp(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStream_t s) {
-  const void* kern = reinterpret_cast<const void*>(k_step_warp<MODE, WPRC, DIMC>);
+  const void* kern = reinterpret_cast<const void*>(k_step_warp<MODE, WPRC, DIMC, EXIT>);
   cudaError_t e = smem_opt_in(kern, sm);
   if (e != cudaSuccess) return e;
   if (a.list_mode == 2) {  // persistent: one wave of CTAs over the work list
@@ -733,11 +745,11 @@ cudaError_t launch_wp(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStre
     e = resident_ctas(kern, kWpThreads, sm, &wave);
     if (e != cudaSuccess) return e;
     const int ctas = std::max(1, std::min(a.tiles_total, wave));
-    k_step_warp<MODE, WPRC, DIMC><<<ctas, kWpThreads, sm, s>>>(a, g);
+    k_step_warp<MODE, WPRC, DIMC, EXIT><<<ctas, kWpThreads, sm, s>>>(a, g);
     return cudaGetLastError();
   }
   const dim3 grid((a.w + g.tile_w - 1) / g.tile_w, (a.h + g.tile_h - 1) / g.tile_h, a.n_envs);
-  k_step_warp<MODE, WPRC, DIMC><<<grid, kWpThreads, sm, s>>>(a, g);
+  k_step_warp<MODE, WPRC, DIMC, EXIT><<<grid, kWpThreads, sm, s>>>(a, g);
   return cudaGetLastError();
 }
 
@@ -864,8 +876,11 @@ cudaError_t launch_step_warp(const StepArgs& a, int mode, const BlockGeom& g, cu
     if (whole_width && wpr == 2) return launch_wp<kStaticTables, 2>(a, g, sm, s);
     return launch_wp<kStaticTables, 0>(a, g, sm, s);
   }
-  if (whole && a.h == 128 && a.w == 128) return launch_wp<kStaticTerrain, 4, 128>(a, g, sm, s);  // C1
-  if (whole && a.h == 64 && a.w == 64) return launch_wp<kStaticTerrain, 2, 64>(a, g, sm, s);
+  // C1: the whole-env launch of ebl_step_batch leaves its step loop once the fire is out (EXIT)
+  if (whole && a.h == 128 && a.w == 128)
+    return a.early_exit ? launch_wp<kStaticTerrain, 4, 128, true>(a, g, sm, s) : launch_wp<kStaticTerrain, 4, 128>(a, g, sm, s);
+  if (whole && a.h == 64 && a.w == 64)
+    return a.early_exit ? launch_wp<kStaticTerrain, 2, 64, true>(a, g, sm, s) : launch_wp<kStaticTerrain, 2, 64>(a, g, sm, s);
   if (whole_width && wpr == 4) return launch_wp<kStaticTerrain, 4>(a, g, sm, s);
   if (whole_width && wpr == 2) return launch_wp<kStaticTerrain, 2>(a, g, sm, s);
   return launch_wp<kStaticTerrain, 0>(a, g, sm, s);
