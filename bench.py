@@ -753,7 +753,7 @@ def bench_c3(cx: Ctx, clk):
                           hbm={"note": "SURVEY §8(d) counts 10 B per dense cell-update; only the active tiles "
                                        "are read and written (tiles_processed_frac)"})
     return dict(value=value, ms_per_step=t_max * 1e3 / a.steps, units_per_rank=units // cx.world,
-                e2e={"value": units / te, "unit": s["unit"], "h2d_bytes_per_step": int(init.nbytes),
+                e2e={"value": units * a.steps / te, "unit": s["unit"], "h2d_bytes_per_step": int(init.nbytes),
                      "d2h_bytes_per_step": int(init.nbytes), "ms_per_step": te * 1e3 / a.steps},
                 roofline=roof, gpu_launches=diag["launches"],
                 extra={"launches_per_run": diag["launches"] // max(1, a.steps + max(1, a.warmup - 2)),

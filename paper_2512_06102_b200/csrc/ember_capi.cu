@@ -394,6 +394,25 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
 // EBL_KERNEL_BLOCKED keep selectable).
 bool use_warp(const ebl_batch* b) { return b->kernel == EBL_KERNEL_WARP || b->kernel == EBL_KERNEL_AUTO; }
 
+// EBL_HALO_MARKS=0: row shards' halo tiles are exposed (never skipped) instead of marked
+bool halo_marks_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("EBL_HALO_MARKS");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// Halo rows [row0, row0 + n) of a row shard were just written from outside (a neighbour's band):
+// their burning cells mark the carried tile records, so the skip rule sees them (ember_warp.cu).
+cudaError_t mark_halo_rows(ebl_batch* b, int row0, int n) {
+  if (b->tf_carry_tiles <= 0 || b->tf_carry_th <= 0 || b->tf_carry_tw <= 0) return cudaSuccess;
+  const int ntx = (b->w + b->tf_carry_tw - 1) / b->tf_carry_tw, nty = (b->h + b->tf_carry_th - 1) / b->tf_carry_th;
+  if (ntx * nty != b->tf_carry_tiles) return cudaSuccess;
+  return ebl::launch_mark_halo(b->state[b->cur].p, b->n_envs, b->ncell, b->w, row0, n, b->tflags[b->tf_carry_par].p,
+                               b->tf_carry_th, b->tf_carry_tw, ntx, nty, b->stream);
+}
+
 cudaError_t launch_ca(const ebl_batch* b, const ebl::StepArgs& a, const ebl::BlockGeom& g, cudaStream_t s) {
   if (use_warp(b)) return ebl::launch_step_warp(a, b->mode, g, s);
   return ebl::launch_step_blocked(a, b->mode, g, s);
@@ -1055,6 +1074,9 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
           const bool same = tf_tiles == tx * ty && b->tf_carry_th == g.tile_h && b->tf_carry_tw == g.tile_w;
           a.tflag_in = same ? b->tflags[tf_par].p : nullptr;
           a.tflag_out = b->tflags[tf_par ^ 1].p;
+          // halo rows written between calls mark the records they reach (mark_halo_rows), so a
+          // row shard's halo tiles follow the skip rule too (EBL_HALO_MARKS=0: exposed instead)
+          a.halo_marked = halo_marks_on() ? 1 : 0;
           tf_par ^= 1;
           tf_tiles = tx * ty;
           b->tf_carry_th = g.tile_h;
@@ -1244,6 +1266,7 @@ int ebl_batch_copy_rows(ebl_batch* dst, int dst_row, const ebl_batch* src, int s
       EBL_CUDA(cudaMemcpyPeerAsync(d, dst->device, s, src->device, bytes, dst->stream));
     }
   }
+  if (halo_only) EBL_CUDA(mark_halo_rows(dst, dst_row, n_rows));
   dst->counts_valid = false;
   return EBL_OK;
 }
@@ -1306,10 +1329,7 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
     const char* e = std::getenv("EBL_WORK_LIST");
     return !e || std::atoi(e) != 0;
   }();
-  static const bool halo_marks = [] {  // EBL_HALO_MARKS=0: exposed halo tiles instead of record exchange
-    const char* e = std::getenv("EBL_HALO_MARKS");
-    return !e || std::atoi(e) != 0;
-  }();
+  const bool halo_marks = halo_marks_on();
   std::vector<ebl::StepArgs> args(n_shards);
   std::vector<char> listed(n_shards, 0);
   // shards sharing one device run on shard 0's stream (stream order replaces the per-chunk
@@ -1540,6 +1560,7 @@ int ebl_batch_rows_device(ebl_batch* b, int row0, int n_rows, void* dptr, int to
     if (to_batch) EBL_CUDA(cudaMemcpyAsync(layer, ext, bytes, cudaMemcpyDeviceToDevice, b->stream));
     else EBL_CUDA(cudaMemcpyAsync(ext, layer, bytes, cudaMemcpyDeviceToDevice, b->stream));
   }
+  if (to_batch && halo_only) EBL_CUDA(mark_halo_rows(b, row0, n_rows));
   if (to_batch) b->counts_valid = false;
   EBL_CUDA(cudaStreamSynchronize(b->stream));
   return EBL_OK;

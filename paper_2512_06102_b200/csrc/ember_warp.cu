@@ -155,10 +155,10 @@ __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& 
           if (ty >= 0 && ty < nty && tx >= 0 && tx < ntx)
             quiet &= !(tf_in[(static_cast<size_t>(env) * nty + ty) * ntx + tx].x & 1);
         }
-      // tiles holding halo rows a neighbour shard writes are never skipped outright (their
-      // records do not see those writes); DESIGN.md §6 gives the distance argument that keeps
+      // tiles holding halo rows a neighbour shard writes are never skipped outright unless those
+      // writes mark the records (halo_marked); DESIGN.md §6 gives the distance argument that keeps
       // the other tiles' skip decisions exact
-      const bool exposed = r0 < a.keep_lo || r0 + g.tile_h > a.keep_hi;
+      const bool exposed = !a.halo_marked && (r0 < a.keep_lo || r0 + g.tile_h > a.keep_hi);
       s_skip = quiet && ((me.x >> 1) & 3) >= 2 && !exposed;
       if (s_skip) {
         tf_out[tile_id] = me;
@@ -774,6 +774,37 @@ __global__ void k_tile_counts(const int4* __restrict__ trec, int tiles_per_env, 
   atomicAdd(&s[2], x);
   __syncthreads();
   if (threadIdx.x < 3) atomicAdd(counts + blockIdx.y * 4 + threadIdx.x, s[threadIdx.x]);
+}
+
+// Halo rows written into a row shard's layer between calls (ebl_batch_rows_device /
+// ebl_batch_copy_rows): a burning cell sets the burning bit of its tile's carried record, so that
+// tile and its 8 neighbours -- every tile whose region reaches the cell -- run next launch.
+__global__ void k_mark_halo(const uint8_t* __restrict__ layer, int n_envs, size_t ncell, int w, int row0, int n_rows,
+                            int4* tflags, int tile_h, int tile_w, int ntx, int nty) {
+  const int chunks = (w + 15) / 16;
+  const size_t total = static_cast<size_t>(n_envs) * n_rows * chunks;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int env = static_cast<int>(i / (static_cast<size_t>(n_rows) * chunks));
+    const int rem = static_cast<int>(i - static_cast<size_t>(env) * n_rows * chunks);
+    const int r = row0 + rem / chunks, c0 = 16 * (rem % chunks);
+    const uint8_t* row = layer + env * ncell + static_cast<size_t>(r) * w;
+    for (int c = c0; c < min(c0 + 16, w); ++c)
+      if (row[c] == 1) {
+        atomicOr(&tflags[(static_cast<size_t>(env) * nty + r / tile_h) * ntx + c / tile_w].x, 1);
+        break;  // (a 16-byte chunk never straddles a tile column: tile_w is a multiple of 32)
+      }
+  }
+}
+
+cudaError_t launch_mark_halo(const uint8_t* layer, int n_envs, size_t ncell, int w, int row0, int n_rows,
+                             int32_t* tflags, int tile_h, int tile_w, int ntx, int nty, cudaStream_t s) {
+  if (n_rows <= 0) return cudaSuccess;
+  const size_t total = static_cast<size_t>(n_envs) * n_rows * ((w + 15) / 16);
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, 148 * 8));
+  k_mark_halo<<<blocks, 256, 0, s>>>(layer, n_envs, ncell, w, row0, n_rows, reinterpret_cast<int4*>(tflags), tile_h,
+                                     tile_w, ntx, nty);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_tile_counts(const int32_t* trec, int n_envs, int tiles_per_env, int32_t* counts, cudaStream_t s) {

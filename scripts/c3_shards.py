@@ -59,3 +59,18 @@ for g in shard_counts:
     ok = np.array_equal(sh.get_state(), ref)
     print(f"G={g} fused: {np.median(ms[1:] or ms):.2f} ms (host issue {np.median(issue[1:] or issue):.2f})  tiles stepped {run / max(tot, 1):.3f}  equal={ok}", flush=True)
     del sh
+# the per-rank form (one process per GPU: step(8) + halo-row copies between calls), emulated here
+# on one device: bitwise equality and the share of tiles stepped (its wall time is host-bound by
+# the per-copy synchronisation of this emulation, not a multi-GPU number)
+if os.environ.get("C3_PER_RANK", "1") != "0":
+    sh = ShardedLandscape(t, 8, fused=False)
+    sh.set_state(init)
+    sh.set_key(0, 0, 0)
+    for bb in sh.batches:
+        bb.diag(reset=True)
+    sh.step(steps)
+    sh.sync()
+    run = sum(bb.diag()["tiles_processed"] for bb in sh.batches)
+    tot = sum(bb.diag()["tiles_launched"] for bb in sh.batches)
+    print(f"G=8 per-rank form: tiles stepped {run / max(tot, 1):.3f}  equal={np.array_equal(sh.get_state(), ref)}",
+          flush=True)
