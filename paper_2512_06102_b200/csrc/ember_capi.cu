@@ -2084,6 +2084,18 @@ int ebl_rl_reset(ebl_batch* b, uint64_t seed, const uint64_t* streams, const uin
   return EBL_OK;
 }
 
+// The device address of a mapped pinned host buffer (ebl_host_alloc, cudaHostAlloc(Mapped)), or
+// null for any other pointer.
+void* mapped_device_ptr(const void* p, size_t align) {
+  cudaPointerAttributes pa{};
+  void* d = nullptr;
+  if (p && cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer &&
+      (reinterpret_cast<uintptr_t>(pa.devicePointer) % align) == 0)
+    d = pa.devicePointer;
+  cudaGetLastError();
+  return d;
+}
+
 int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* done, int device_io) {
   EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
@@ -2091,9 +2103,21 @@ int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* d
   if (int e = prepare(b)) return e;
   EBL_CUDA(cudaSetDevice(b->device));
   ebl::RlArgs g = rl_args(b);
+  // tanker steps with host buffers in mapped pinned memory: the kernel reads the actions and writes
+  // reward / done through the mapping (no copy launches around the step; EBL_RL_ZC=0 copies)
+  static const int rl_zc = [] {  // 0: copies, 1: outputs and actions mapped, 2: outputs only
+    const char* e = std::getenv("EBL_RL_ZC");
+    return e ? std::atoi(e) : 2;
+  }();
+  const bool zc = rl_zc && !device_io && b->rl_variant != EBL_RL_REFERENCE;
+  double* const zc_reward = zc && reward ? static_cast<double*>(mapped_device_ptr(reward, 8)) : nullptr;
+  uint8_t* const zc_done = zc && done ? static_cast<uint8_t*>(mapped_device_ptr(done, 1)) : nullptr;
   if (actions) {
+    const int32_t* zc_act = zc && rl_zc == 1 ? static_cast<const int32_t*>(mapped_device_ptr(actions, 4)) : nullptr;
     if (device_io) {
       g.actions = actions;
+    } else if (zc_act) {
+      g.actions = zc_act;
     } else {
       if (b->rl_variant == EBL_RL_REFERENCE)
         for (int e = 0; e < b->n_envs; ++e)
@@ -2103,8 +2127,8 @@ int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* d
       g.actions = b->actions.p;
     }
   }
-  g.reward = device_io && reward ? reward : b->reward.p;
-  g.done = device_io && done ? done : b->done.p;
+  g.reward = device_io && reward ? reward : zc_reward ? zc_reward : b->reward.p;
+  g.done = device_io && done ? done : zc_done ? zc_done : b->done.p;
   if (b->rl_variant == EBL_RL_REFERENCE) {
     if (int e = rl_sync_bytes(b)) return e;
     EBL_CUDA(ebl::launch_rl_ref_step(g, b->mode, b->stream));
@@ -2115,8 +2139,9 @@ int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* d
   b->steps_done += 1;
   b->counts_valid = false;
   if (!device_io) {
-    if (reward) EBL_CUDA(cudaMemcpyAsync(reward, b->reward.p, b->n_envs * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
-    if (done) EBL_CUDA(cudaMemcpyAsync(done, b->done.p, b->n_envs, cudaMemcpyDeviceToHost, b->stream));
+    if (reward && !zc_reward)
+      EBL_CUDA(cudaMemcpyAsync(reward, b->reward.p, b->n_envs * sizeof(double), cudaMemcpyDeviceToHost, b->stream));
+    if (done && !zc_done) EBL_CUDA(cudaMemcpyAsync(done, b->done.p, b->n_envs, cudaMemcpyDeviceToHost, b->stream));
   }
   if (b->rl_variant == EBL_RL_REFERENCE) {
     int32_t err = 0;
@@ -2126,7 +2151,8 @@ int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* d
       EBL_CUDA(cudaMemsetAsync(b->error.p, 0, sizeof(int32_t), b->stream));
       return set_err(EBL_ELOGIC, "FireSuppressionEnv::step: episode already finished");
     }
-  } else if (!device_io && (reward || done)) {
+  } else if (!device_io && (reward || done || (actions && g.actions != b->actions.p))) {
+    // (host results, or host actions the kernel reads through the mapping: done before returning)
     EBL_CUDA(cudaStreamSynchronize(b->stream));
   }
   return EBL_OK;

@@ -271,3 +271,36 @@ def test_tanker_learner_in_the_loop_device_io(port):
     wet = np.stack([x["wet"] for x in want])
     assert np.array_equal(obs.cpu().numpy(), fire | (wet << 2))
     assert np.array_equal(env.fire(), fire) and np.array_equal(env.wet(), wet)
+
+
+def test_tanker_host_step_mapped_buffers(port):
+    """ebl_rl_step with host buffers in mapped pinned memory (eb.host_buffer): the kernel writes
+    reward / done straight through the mapping (no copy after the step) and the call returns them
+    complete -- rewards, dones and the final layers equal the C restatement driven by the same
+    actions, and equal the same steps with pageable buffers (DMA copies)."""
+    n, h, w, seed, steps = 16, 64, 64, 4, 70
+    t = eb.synth_terrain(seed, n, h, w)
+    rs = np.random.default_rng(3)
+    acts = rs.integers(0, h * w, (steps, n)).astype(np.int32)
+    L = eb.lib()
+    got = {}
+    for mapped in (True, False):
+        env = eb.VecFireEnv(n, variant=eb.RL_TANKER, terrain=t, sim_cfg=None, ignitions=5, max_steps=256)
+        env.reset(seed)
+        mk = eb.host_buffer if mapped else (lambda shape, dtype=np.uint8: np.empty(shape, dtype))
+        a, r, d = mk((n,), np.int32), mk((n,), np.float64), mk((n,), np.uint8)
+        log = []
+        for k in range(steps):
+            a[:] = acts[k]
+            eb._lib.check(L.ebl_rl_step(env.batch.handle, a.ctypes.data, r.ctypes.data, d.ctypes.data, 0))
+            log.append((r.copy(), d.copy()))
+        got[mapped] = (log, env.fire(), env.wet())
+    want = _port_tanker(port, t, O.DEFAULT_CFG, seed, list(range(n)), steps, O.TankerCfg(5, 256, 1), actions=acts)
+    log, fire, wet = got[True]
+    for e in range(n):
+        assert [x[0][e] for x in log] == want[e]["rewards"], e
+        assert [int(x[1][e]) for x in log] == want[e]["dones"], e
+    assert np.array_equal(fire, np.stack([x["fire"] for x in want]))
+    assert np.array_equal(wet, np.stack([x["wet"] for x in want]))
+    for (r1, d1), (r0, d0) in zip(got[True][0], got[False][0]):
+        assert np.array_equal(r1, r0) and np.array_equal(d1, d0)
