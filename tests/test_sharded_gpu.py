@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("fused", [True, False])
-@pytest.mark.parametrize("g,halo", [(1, 8), (2, 8), (3, 4), (4, 8), (5, 2)])
+@pytest.mark.parametrize("g,halo", [(1, 8), (2, 8), (3, 4), (4, 8), (5, 2), (10, 4)])
 def test_sharded_equals_unsharded(port, g, halo, fused):
     h, w, steps, seed = 300, 200, 45, 3
     t = eb.synth_terrain(seed, 1, h, w)
@@ -42,7 +42,7 @@ def test_sharded_equals_unsharded(port, g, halo, fused):
 
 @pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("direction", [0.0, 90.0, 270.0])
-@pytest.mark.parametrize("g", [2, 4, 6])
+@pytest.mark.parametrize("g", [2, 4, 6, 9])  # 9 > kMaxShardLaunch: per-shard launches and events
 def test_fire_across_shard_boundaries_small_tiles(g, direction, fused):
     """The tile records travel with the halo rows -- fused: a burning tile enqueues the neighbour
     shard's tiles next to the rows it stores there; per-rank form: the halo-row copies mark the
