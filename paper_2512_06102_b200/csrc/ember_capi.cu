@@ -1184,6 +1184,11 @@ int ebl_batch_run(ebl_batch* b, const uint8_t* initial, int n_steps, uint8_t* fi
   }();
   const int zc_keep = zc_env >= 0 ? zc_env : (chunks + 1) / 2;
   const int zc_from = host_dev ? std::max(0, chunks - zc_keep) : chunks;
+  static const int pipe_exit = [] {  // the early-exit instantiation for the pipeline's launches too
+    const char* e = std::getenv("EBL_PIPE_EXIT");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.early_exit = pipe_exit;
   for (int c = 0; c < chunks; ++c) {
     const int off = bound[c], n = bound[c + 1] - off;
     if (n <= 0) continue;
