@@ -358,7 +358,9 @@ int ebl_rl_reset(ebl_batch* b, uint64_t seed, const uint64_t* streams, const uin
  * (random_policy, rl_env.cpp:237-239 / uniform (x,y) for TANKER).  reward/done
  * may be NULL; host pointers unless `device_io` is 1.  Returns EBL_ELOGIC if a
  * REFERENCE env is already done (rl_env.cpp:173).  TANKER: the layers stay bit-resident
- * between consecutive calls; any other call that reads or writes them rebuilds the bytes. */
+ * between consecutive calls; any other call that reads or writes them rebuilds the bytes;
+ * host reward/done buffers in mapped pinned memory (ebl_host_alloc) are written by the kernel
+ * through the mapping (no copy after the step); either way they are complete on return. */
 int ebl_rl_step(ebl_batch* b, const int32_t* actions, double* reward, uint8_t* done, int device_io);
 /* Tanker fused rollout: n_steps random-policy steps on device, rewards summed
  * into reward_sum[e] (host), episodes finished counted into episodes[e]. */
