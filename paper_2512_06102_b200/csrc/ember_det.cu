@@ -180,6 +180,50 @@ __global__ void k_det_forward(DetArgs d, int t) {
   if (d.traj_lam) d.traj_lam[tr] = lam;
 }
 
+// The forward with two horizontally adjacent cells per thread (target-ordered pot, even widths):
+// the state and trajectory planes move as 16-byte vectors and every thread keeps twice the loads in
+// flight; each cell's arithmetic is k_det_forward's.
+#ifndef EBL_DET_FWD2
+#define EBL_DET_FWD2 1
+#endif
+__global__ void k_det_forward2(DetArgs d, int t) {
+  const StepArgs& a = d.s;
+  const int ncell = a.h * a.w;
+  const int env = blockIdx.y;
+  const int i0 = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (i0 >= ncell) return;
+  const size_t base = static_cast<size_t>(env) * ncell;
+  const size_t tb = static_cast<size_t>(env) * d.tab_stride;
+  const int r = i0 / a.w, c = i0 % a.w;
+  const double2 un2 = *reinterpret_cast<const double2*>(d.un + base + i0);
+  const double2 bu2 = *reinterpret_cast<const double2*>(d.burn + base + i0);
+  const double2 bd2 = *reinterpret_cast<const double2*>(d.bd + base + i0);
+  double lam[2], pig[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    lam[k] = lambda_at_t(d.burn + base, d.potT + tb * 8, a.h, a.w, r, c + k);
+    pig[k] = __dsub_rn(1.0, exp_neg(__dmul_rn(gamma_at(d, tb, env, i0 + k), lam[k])));
+  }
+  const double un[2] = {un2.x, un2.y}, bu[2] = {bu2.x, bu2.y}, bd[2] = {bd2.x, bd2.y};
+  double o_b[2], o_u[2], o_d[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double newly = __dmul_rn(un[k], pig[k]);
+    o_b[k] = __dadd_rn(newly, __dmul_rn(bu[k], d.pc));
+    o_u[k] = __dsub_rn(un[k], newly);
+    o_d[k] = __dadd_rn(bd[k], __dmul_rn(bu[k], __dsub_rn(1.0, d.pc)));
+  }
+  *reinterpret_cast<double2*>(d.burn_o + base + i0) = make_double2(o_b[0], o_b[1]);
+  *reinterpret_cast<double2*>(d.un_o + base + i0) = make_double2(o_u[0], o_u[1]);
+  *reinterpret_cast<double2*>(d.bd_o + base + i0) = make_double2(o_d[0], o_d[1]);
+  const size_t tr = static_cast<size_t>(t) * a.n_envs * ncell + base + i0;
+  if (d.traj_un) {
+    *reinterpret_cast<double2*>(d.traj_un + tr) = un2;
+    *reinterpret_cast<double2*>(d.traj_burn + tr) = bu2;
+  }
+  if (d.traj_lam) *reinterpret_cast<double2*>(d.traj_lam + tr) = make_double2(lam[0], lam[1]);
+}
+
 // state_from_fire (engine.cpp:42-52): one-hot planes from the member layers, on the device.
 __global__ void k_det_from_fire(const uint8_t* __restrict__ st, double* un, double* bu, double* bd, size_t n) {
   const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -770,6 +814,10 @@ __global__ void k_det_reduce(DetArgs d, int blocks_per_env) {
 
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s) {
   const int ncell = d.s.h * d.s.w;
+  if (EBL_DET_FWD2 && d.potT && (d.s.w % 2) == 0) {
+    k_det_forward2<<<dim3((ncell / 2 + 255) / 256, d.s.n_envs), 256, 0, s>>>(d, t);
+    return cudaGetLastError();
+  }
   k_det_forward<<<dim3((ncell + 255) / 256, d.s.n_envs), 256, 0, s>>>(d, t);
   return cudaGetLastError();
 }
