@@ -28,9 +28,11 @@
 #include "ember_device.cuh"
 #include "ember_exp.cuh"
 #include "ember_kernels.h"
+#include "ember_pdl.cuh"
 #include "ember_params.h"
 
 namespace ebl {
+
 
 namespace {
 
@@ -187,6 +189,7 @@ __global__ void k_det_forward(DetArgs d, int t) {
 #define EBL_DET_FWD2 1
 #endif
 __global__ void k_det_forward2(DetArgs d, int t) {
+  pdl_enter();
   const StepArgs& a = d.s;
   const int ncell = a.h * a.w;
   const int env = blockIdx.y;
@@ -611,6 +614,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
 }
 
 __global__ void __launch_bounds__(kSW, EBL_DET_SD <= 2 ? 6 : 5) k_det_back_stream(DetArgs d, int t) {
+  pdl_enter();
   extern __shared__ __align__(128) uint8_t dsm[];
   StreamRow* const st = reinterpret_cast<StreamRow*>(dsm);
   double (*const alam)[kSW + 2] = reinterpret_cast<double (*)[kSW + 2]>(dsm + kSlots * sizeof(StreamRow));
@@ -815,8 +819,7 @@ __global__ void k_det_reduce(DetArgs d, int blocks_per_env) {
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s) {
   const int ncell = d.s.h * d.s.w;
   if (EBL_DET_FWD2 && d.potT && (d.s.w % 2) == 0) {
-    k_det_forward2<<<dim3((ncell / 2 + 255) / 256, d.s.n_envs), 256, 0, s>>>(d, t);
-    return cudaGetLastError();
+    return launch_pdl(k_det_forward2, dim3((ncell / 2 + 255) / 256, d.s.n_envs), dim3(256), 0, s, d, t);
   }
   k_det_forward<<<dim3((ncell + 255) / 256, d.s.n_envs), 256, 0, s>>>(d, t);
   return cudaGetLastError();
@@ -840,8 +843,7 @@ cudaError_t launch_det_backward(const DetArgs& d, int t, cudaStream_t s) {
     const size_t sm = det_stream_smem();
     cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_det_back_stream), sm);
     if (e != cudaSuccess) return e;
-    k_det_back_stream<<<dim3(det_blocks_per_env_stream(d.s.h), d.s.n_envs), kSW, sm, s>>>(d, t);
-    return cudaGetLastError();
+    return launch_pdl(k_det_back_stream, dim3(det_blocks_per_env_stream(d.s.h), d.s.n_envs), dim3(kSW), sm, s, d, t);
   }
   if (d.A_un_o) {  // fused, double-buffered adjoints
     const dim3 g(det_blocks_per_env(d.s.h, d.s.w), d.s.n_envs);

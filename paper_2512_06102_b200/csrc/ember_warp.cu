@@ -25,6 +25,7 @@
 #include "ember_bits.cuh"
 #include "ember_device.cuh"
 #include "ember_kernels.h"
+#include "ember_pdl.cuh"
 #include "ember_params.h"
 
 #ifndef EBL_PHASE_PROF
@@ -660,6 +661,7 @@ __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& 
 
 template <int MODE, int WPRC, int DIMC, bool EXIT = false>
 __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArgs a, BlockGeom g) {
+  if (DIMC == 0 && a.list_mode == 2) pdl_enter();  // work-list launches follow one another (PDL)
   if (DIMC == 0 && a.list_mode && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) {
     *a.list_zero0 = 0;  // the next launch's append counter and cursor start at 0 (no memset launches)
     *a.list_zero1 = 0;
@@ -690,6 +692,7 @@ __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp(StepArg
 // region runs with its shard's StepArgs, read in place from the kernel parameter block.
 template <int MODE, int WPRC>
 __global__ void __launch_bounds__(kWpThreads, EBL_WARP_MINB) k_step_warp_shards(const __grid_constant__ ShardsLaunch P) {
+  pdl_enter();
   __shared__ int s_pref[kMaxShardLaunch + 1];
   __shared__ int s_item;
   if (blockIdx.x == 0 && threadIdx.x < P.n) {
@@ -731,8 +734,7 @@ cudaError_t launch_wp_shards(const ShardsLaunch& P, size_t sm, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   int tiles = 0;
   for (int i = 0; i < P.n; ++i) tiles += P.sa[i].tiles_total;
-  k_step_warp_shards<MODE, WPRC><<<std::max(1, std::min(tiles, wave)), kWpThreads, sm, s>>>(P);
-  return cudaGetLastError();
+  return launch_pdl(k_step_warp_shards<MODE, WPRC>, dim3(std::max(1, std::min(tiles, wave))), dim3(kWpThreads), sm, s, P);
 }
 
 template <int MODE, int WPRC, int DIMC = 0, bool EXIT = false>
@@ -745,8 +747,7 @@ cudaError_t launch_wp(const StepArgs& a, const BlockGeom& g, size_t sm, cudaStre
     e = resident_ctas(kern, kWpThreads, sm, &wave);
     if (e != cudaSuccess) return e;
     const int ctas = std::max(1, std::min(a.tiles_total, wave));
-    k_step_warp<MODE, WPRC, DIMC, EXIT><<<ctas, kWpThreads, sm, s>>>(a, g);
-    return cudaGetLastError();
+    return launch_pdl(k_step_warp<MODE, WPRC, DIMC, EXIT>, dim3(ctas), dim3(kWpThreads), sm, s, a, g);
   }
   const dim3 grid((a.w + g.tile_w - 1) / g.tile_w, (a.h + g.tile_h - 1) / g.tile_h, a.n_envs);
   k_step_warp<MODE, WPRC, DIMC, EXIT><<<grid, kWpThreads, sm, s>>>(a, g);
