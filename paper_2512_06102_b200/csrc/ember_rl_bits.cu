@@ -16,6 +16,7 @@
 #include "ember_bits.cuh"
 #include "ember_device.cuh"
 #include "ember_kernels.h"
+#include "ember_pdl.cuh"
 #include "ember_params.h"
 
 namespace ebl {
@@ -342,6 +343,7 @@ __device__ __forceinline__ int nth_set_bit32(uint32_t v, int q) {
 // row in the dense pass, and twice the envs are resident per SM)
 template <int MODE, int DIMC, int NW>
 __global__ void __launch_bounds__(32 * NW, 32 / NW) k_rl_tanker_warp(RlArgs g) {
+  pdl_enter();  // consecutive ebl_rl_step launches (device-io learner loop): PDL
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_newly[2], s_gone[2];  // per step parity: ignitions, Burning cells lost
   __shared__ int s_burning[2];           // Burning cells at the start of step t (slot t & 1)
@@ -802,8 +804,7 @@ template <int MODE, int DIMC, int NW>
 static cudaError_t launch_rl_warp_t(const RlArgs& g, size_t sm, cudaStream_t s) {
   cudaError_t e = smem_opt_in(reinterpret_cast<const void*>(k_rl_tanker_warp<MODE, DIMC, NW>), sm);
   if (e != cudaSuccess) return e;
-  k_rl_tanker_warp<MODE, DIMC, NW><<<g.s.n_envs, 32 * NW, sm, s>>>(g);
-  return cudaGetLastError();
+  return launch_pdl(k_rl_tanker_warp<MODE, DIMC, NW>, dim3(g.s.n_envs), dim3(32 * NW), sm, s, g);
 }
 
 cudaError_t launch_rl_tanker_warp(const RlArgs& g, int mode, cudaStream_t s) {
