@@ -452,13 +452,32 @@ __global__ void __launch_bounds__(32 * NW, 32 / NW) k_rl_tanker_warp(RlArgs g) {
     if (b == 31) v = (v & 3u) | ((j + 1 < wpr ? row[j + 1] & 1u : 0u) << 2);
     return v & 7u;
   };
+  // fused rollouts: rng key prefixes (3 of the 5 rounds) and random-policy actions of the next 64
+  // episode steps, one per thread, rebuilt when they run out or an auto-reset starts a new episode
+  // stream (C2 rollout 6.75 -> 6.20 ms)
+  __shared__ uint64_t s_pre[64];
+  __shared__ int s_act[64];
+  int tab_step = -64;
+  uint64_t tab_stream = ~0ull;
   for (int t = 0; t < g.n_steps; ++t) {
     const int par = t & 1;
     uint32_t* B = cur ? Bp1 : Bp0;
     uint32_t* Bn = cur ? Bp0 : Bp1;
+    if (g.n_steps > 1 && (e.stream != tab_stream || e.step - tab_step >= 64)) {  // block-uniform (e is shared)
+      for (int k = threadIdx.x; k < 64; k += blockDim.x) {
+        const uint64_t pre = key_prefix(g.seed, e.stream, static_cast<uint64_t>(e.step + k));
+        s_pre[k] = pre;
+        s_act[k] = g.actions ? 0 : static_cast<int>(below(cell_bits53(pre, 0, 2), n));
+      }
+      tab_step = e.step;
+      tab_stream = e.stream;
+      __syncthreads();
+    }
     // ---- action (every thread) + drop ----------------------------------------------------------
-    const uint64_t prefix = key_prefix(g.seed, e.stream, static_cast<uint64_t>(e.step));
-    const int action = g.actions ? action_in : static_cast<int>(below(cell_bits53(prefix, 0, 2), n));
+    // (single-step launches: the one prefix directly)
+    const uint64_t prefix = g.n_steps > 1 ? s_pre[e.step - tab_step] : key_prefix(g.seed, e.stream, static_cast<uint64_t>(e.step));
+    const int action = g.actions ? action_in
+                                 : g.n_steps > 1 ? s_act[e.step - tab_step] : static_cast<int>(below(cell_bits53(prefix, 0, 2), n));
     if (threadIdx.x < 9) {
       const int r = action / W + static_cast<int>(threadIdx.x) / 3 - 1;
       const int c = action % W + static_cast<int>(threadIdx.x) % 3 - 1;
