@@ -83,6 +83,27 @@ __device__ __forceinline__ void bytes_to_bits(const uint8_t* src, uint32_t& b, u
   }
 }
 
+// The same, also ORing into `nc` a nonzero value when a byte is not a FireState (>= 3).
+__device__ __forceinline__ void bytes_to_bits_nc(const uint8_t* src, uint32_t& b, uint32_t& x, uint32_t& nc) {
+  const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(src));
+  const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+  const uint32_t wds[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+  b = 0u;
+  x = 0u;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t v = wds[q];
+    const uint32_t z = v & 0xFCFCFCFCu;
+    const uint32_t small = ~((((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) >> 7) & 0x01010101u;
+    const uint32_t b0 = v & 0x01010101u, b1 = (v >> 1) & 0x01010101u;
+    const uint32_t lo = b0 & ~b1 & small;
+    const uint32_t hi = b1 & ~b0 & small;
+    nc |= (~small & 0x01010101u) | (b0 & b1);  // byte >= 4, or byte == 3
+    b |= ((lo * 0x01020408u) >> 24 & 0xfu) << (4 * q);
+    x |= ((hi * 0x01020408u) >> 24 & 0xfu) << (4 * q);
+  }
+}
+
 // Burning / Burned bits -> 32 uint8 cells (two 16-byte stores).
 __device__ __forceinline__ void bits_to_bytes(uint32_t b, uint32_t x, uint8_t* dst) {
   uint32_t wds[8];

@@ -200,17 +200,20 @@ __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& 
   }
   const uint8_t* __restrict__ in = a.in + env * ncell;
   uint32_t any_b = 0u;  // a burning cell anywhere in the region
+  uint32_t noncanon = 0u;  // (records) a byte that is not a FireState in the region
   for (WordIter it(wpr, H * wpr); it.ok(); it.next()) {
     const int nc = min(32, RW - 32 * it.j);
     uint32_t b = 0u, x = 0u;
     const uint8_t* src = in + static_cast<size_t>(R0 + it.r) * W + C0 + 32 * it.j;
     if (nc == 32 && vec) {
-      bytes_to_bits(src, b, x);
+      if (DIMC) bytes_to_bits(src, b, x);
+      else bytes_to_bits_nc(src, b, x, noncanon);
     } else {
       for (int k = 0; k < nc; ++k) {
         const uint8_t v = src[k];
         b |= static_cast<uint32_t>(v == 1) << k;
         x |= static_cast<uint32_t>(v == 2) << k;
+        noncanon |= v > 2;
       }
     }
     Bp0[ro(it.r + 1) + it.j] = b;
@@ -243,6 +246,10 @@ __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& 
   // Unburned cell without a burning neighbour; the light cone of outside fire stays in the halo):
   // straight to the store (which maps other byte values to Unburned as a step does)
   const int n_run = __syncthreads_or(any_b != 0u) || a.traj ? n_steps : 0;
+  // a quiet region whose bytes are all FireStates stores exactly what it loaded: both layer buffers
+  // then hold the tile's canonical bytes at once (records: quiet streak 2 after one launch, so the
+  // launch after a call's first one does not rerun every quiet tile)
+  const bool canon_quiet = !DIMC && n_run == 0 && (a.list_mode || a.tflag_out) && !__syncthreads_or(noncanon != 0u);
 
   const DiagCounters dg{a.diag};
   const uint64_t gbase = static_cast<uint64_t>(a.row_off + R0) * W + C0;  // RNG index of region (0, 0)
@@ -611,7 +618,7 @@ __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& 
     if (threadIdx.x == 3) atomicAdd(a.counts + env * 4 + 3, s_newly);
   }
   if (tf_out && threadIdx.x == 0) {
-    const int streak = n_run == 0 ? min(streak0 + 1, 2) : 0;  // output == input this launch
+    const int streak = n_run == 0 ? (canon_quiet ? 2 : min(streak0 + 1, 2)) : 0;  // output == input this launch
     tf_out[tile_id] = make_int4((s_cnt[1] > 0 ? 1 : 0) | (streak << 1), s_cnt[0], s_cnt[1], s_cnt[2]);
   }
   if (a.list_mode && threadIdx.x == 0) {
@@ -619,7 +626,7 @@ __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& 
     // neighbourhood run (the light cone of one launch stays within the neighbours), a tile whose
     // buffers are not both canonical yet (streak < 2) makes itself run -- exactly the tiles the
     // grid form's skip rule would not skip (tiles outside the list keep a quiet record)
-    const int streak = n_run == 0 ? min(streak0 + 1, 2) : 0;
+    const int streak = n_run == 0 ? (canon_quiet ? 2 : min(streak0 + 1, 2)) : 0;
     const bool burning = s_cnt[1] > 0;
     reinterpret_cast<int4*>(a.trec)[tile_id] = make_int4((burning ? 1 : 0) | (streak << 1), s_cnt[0], s_cnt[1], s_cnt[2]);
     auto enqueue = [&](int tx, int ty) {
