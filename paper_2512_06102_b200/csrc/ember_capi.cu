@@ -394,6 +394,21 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
 // EBL_KERNEL_BLOCKED keep selectable).
 bool use_warp(const ebl_batch* b) { return b->kernel == EBL_KERNEL_WARP || b->kernel == EBL_KERNEL_AUTO; }
 
+// Halo-tiled warp-kernel runs of the default 64 x 256 tiles on terrain layers of >= 80 x 320: every
+// tile's region is the full 80 x 320 (clamped inside the layer: edge tiles take their halo inward),
+// so all tiles take the compile-time 10-word rows and the branch-free decide pass.
+// EBL_FIXED_REGION=0: edge regions cut at the layer edge (the generic path).
+void apply_fixed_regions(const ebl_batch* b, ebl::BlockGeom& g) {
+  static const bool on = [] {
+    const char* e = std::getenv("EBL_FIXED_REGION");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on || !use_warp(b) || b->mode != ebl::kStaticTerrain) return;
+  if (g.tile_h != 64 || g.tile_w != 256 || g.halo_rows != 8 || g.halo_cols != 32) return;
+  if (b->h < g.tile_h + 2 * g.halo_rows || b->w < g.tile_w + 2 * g.halo_cols || (b->w % 32) != 0) return;
+  g.fixed_region = 1;
+}
+
 // EBL_HALO_MARKS=0: row shards' halo tiles are exposed (never skipped) instead of marked
 bool halo_marks_on() {
   static const bool on = [] {
@@ -1015,6 +1030,7 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
         const int rw = std::min(b->w, g.tile_w + 2 * g.halo_cols);
         g.list_cap = std::max(1, rh * rw / 4);
       }
+      apply_fixed_regions(b, g);
       ebl::StepArgs a = step_args(b);
       if (done + g.n_steps == n_steps) {
         EBL_CUDA(cudaMemsetAsync(b->counts.p, 0, b->n_envs * 4 * sizeof(int32_t), b->stream));
@@ -1371,6 +1387,7 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
         const int rw = std::min(b->w, g.tile_w + 2 * g.halo_cols);
         g.list_cap = std::max(1, rh * rw / 4);
       }
+      apply_fixed_regions(b, g);
       if (g.halo_rows > 0 || g.halo_cols > 0) k = std::min(k, std::max(1, g.halo_rows));
       geo[s] = g;
     }

@@ -109,6 +109,8 @@ struct BlockGeom {
   int n_steps;
   int row_off;
   int list_cap;      // active-list entries per CTA (all its envs)
+  int fixed_region;  // every tile's region is (tile + 2 halo) in both dims, clamped inside the layer
+                     // (edge tiles take more halo inward): compile-time words per row for tiles
   int envs_per_cta;  // 1 (the blocked kernel's env pooling was measured slower and removed)
 };
 

@@ -112,8 +112,13 @@ __device__ __forceinline__ void warp_region(const StepArgs& a, const BlockGeom& 
   const int n_steps = g.n_steps;
   const int BH = DIMC ? DIMC : a.h, W = DIMC ? DIMC : a.w;
   const int r0 = DIMC ? 0 : byi * g.tile_h, c0 = DIMC ? 0 : bxi * g.tile_w;  // c0 % 32 == 0
-  const int R0 = DIMC ? 0 : max(0, r0 - g.halo_rows), R1 = DIMC ? BH : min(BH, r0 + g.tile_h + g.halo_rows);
-  const int C0 = DIMC ? 0 : max(0, c0 - g.halo_cols), C1 = DIMC ? W : min(W, c0 + g.tile_w + g.halo_cols);
+  // fixed regions: (tile + 2 halo) rows / columns for every tile, clamped inside the layer
+  const bool fixed = !DIMC && g.fixed_region;
+  const int frh = g.tile_h + 2 * g.halo_rows, frw = g.tile_w + 2 * g.halo_cols;
+  const int R0 = DIMC ? 0 : fixed ? min(max(0, r0 - g.halo_rows), BH - frh) : max(0, r0 - g.halo_rows);
+  const int R1 = DIMC ? BH : fixed ? R0 + frh : min(BH, r0 + g.tile_h + g.halo_rows);
+  const int C0 = DIMC ? 0 : fixed ? min(max(0, c0 - g.halo_cols), W - frw) : max(0, c0 - g.halo_cols);
+  const int C1 = DIMC ? W : fixed ? C0 + frw : min(W, c0 + g.tile_w + g.halo_cols);
   const int H = R1 - R0, RW = C1 - C0;
   const int wpr = WPRC ? WPRC : (RW + 31) >> 5;
   const int S = plane_stride(wpr);
@@ -894,6 +899,9 @@ cudaError_t launch_step_warp_shards(const ShardsLaunch& P, int mode, cudaStream_
     whole_width = whole_width && g.tile_w >= a.w;
   }
   const int wpr = (P.sa[0].w + 31) / 32;
+  bool fixed320 = mode == kStaticTerrain;
+  for (int i = 0; i < P.n; ++i) fixed320 = fixed320 && P.g[i].fixed_region && P.g[i].tile_w + 2 * P.g[i].halo_cols == 320;
+  if (fixed320) return launch_wp_shards<kStaticTerrain, 10>(P, sm, s);
   if (mode == kStaticTables) {
     if (whole_width && wpr == 4) return launch_wp_shards<kStaticTables, 4>(P, sm, s);
     if (whole_width && wpr == 2) return launch_wp_shards<kStaticTables, 2>(P, sm, s);
@@ -918,6 +926,9 @@ cudaError_t launch_step_warp(const StepArgs& a, int mode, const BlockGeom& g, cu
   // C1: the whole-env launch of ebl_step_batch leaves its step loop once the fire is out (EXIT)
   if (whole && a.h == 128 && a.w == 128)
     return a.early_exit ? launch_wp<kStaticTerrain, 4, 128, true>(a, g, sm, s) : launch_wp<kStaticTerrain, 4, 128>(a, g, sm, s);
+  // fixed 320-column regions (64 x 256 tiles with their halo): compile-time words per row and the
+  // branch-free decide pass for every halo tile
+  if (g.fixed_region && rw == 320) return launch_wp<kStaticTerrain, 10>(a, g, sm, s);
   if (whole && a.h == 64 && a.w == 64)
     return a.early_exit ? launch_wp<kStaticTerrain, 2, 64, true>(a, g, sm, s) : launch_wp<kStaticTerrain, 2, 64>(a, g, sm, s);
   if (whole_width && wpr == 4) return launch_wp<kStaticTerrain, 4>(a, g, sm, s);
