@@ -394,9 +394,10 @@ ebl::StepArgs chunk_args(const ebl_batch* b, ebl::StepArgs a, int off, int n) {
 // EBL_KERNEL_BLOCKED keep selectable).
 bool use_warp(const ebl_batch* b) { return b->kernel == EBL_KERNEL_WARP || b->kernel == EBL_KERNEL_AUTO; }
 
-// Halo-tiled warp-kernel runs of the default 64 x 256 tiles on terrain layers of >= 80 x 320: every
-// tile's region is the full 80 x 320 (clamped inside the layer: edge tiles take their halo inward),
-// so all tiles take the compile-time 10-word rows and the branch-free decide pass.
+// Halo-tiled warp-kernel runs (default 32 x 128 tiles) on terrain layers at least one region large:
+// every tile's region is the full (tile + halo) -- 48 x 192 by default, clamped inside the layer:
+// edge tiles take their halo inward -- so all tiles take compile-time words per row and the
+// branch-free decide pass.
 // EBL_FIXED_REGION=0: edge regions cut at the layer edge (the generic path).
 void apply_fixed_regions(const ebl_batch* b, ebl::BlockGeom& g) {
   static const bool on = [] {
@@ -404,7 +405,8 @@ void apply_fixed_regions(const ebl_batch* b, ebl::BlockGeom& g) {
     return !e || std::atoi(e) != 0;
   }();
   if (!on || !use_warp(b) || b->mode != ebl::kStaticTerrain) return;
-  if (g.tile_h != 64 || g.tile_w != 256 || g.halo_rows != 8 || g.halo_cols != 32) return;
+  const int rw = g.tile_w + 2 * g.halo_cols;  // the compile-time region widths (ember_warp.cu)
+  if (g.halo_rows != 8 || g.halo_cols != 32 || !(rw == 128 || rw == 192 || rw == 320)) return;
   if (b->h < g.tile_h + 2 * g.halo_rows || b->w < g.tile_w + 2 * g.halo_cols || (b->w % 32) != 0) return;
   g.fixed_region = 1;
 }

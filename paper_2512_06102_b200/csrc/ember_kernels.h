@@ -13,8 +13,8 @@ constexpr int kRlThreads = 256;   // RL kernels: one CTA per env
 constexpr int kRlMaxCells = 16384;  // env layer(s) resident in shared memory
 constexpr int kResThreads = 128;    // blocked kernel: one CTA per tile (whole env if it fits)
 constexpr size_t kResMaxSmem = 200 * 1024;
-constexpr int kBlockTileH = 64;     // tiled blocked kernel (large grids): 64 x 256 tiles,
-constexpr int kBlockTileW = 256;    // 8-row / 32-column light-cone halo, 8 steps per launch
+constexpr int kBlockTileH = 32;     // tiled runs (large grids): 32 x 128 tiles (C3 sweep,
+constexpr int kBlockTileW = 128;    // scripts/c3_tiles.sh), 8-row / 32-column light-cone halo, 8 steps per launch
 constexpr int kBlockHalo = 8;
 
 bool phase_prof_built();

@@ -899,9 +899,12 @@ cudaError_t launch_step_warp_shards(const ShardsLaunch& P, int mode, cudaStream_
     whole_width = whole_width && g.tile_w >= a.w;
   }
   const int wpr = (P.sa[0].w + 31) / 32;
-  bool fixed320 = mode == kStaticTerrain;
-  for (int i = 0; i < P.n; ++i) fixed320 = fixed320 && P.g[i].fixed_region && P.g[i].tile_w + 2 * P.g[i].halo_cols == 320;
-  if (fixed320) return launch_wp_shards<kStaticTerrain, 10>(P, sm, s);
+  const int frw = P.g[0].tile_w + 2 * P.g[0].halo_cols;
+  bool fixed = mode == kStaticTerrain;
+  for (int i = 0; i < P.n; ++i) fixed = fixed && P.g[i].fixed_region && P.g[i].tile_w + 2 * P.g[i].halo_cols == frw;
+  if (fixed && frw == 320) return launch_wp_shards<kStaticTerrain, 10>(P, sm, s);
+  if (fixed && frw == 192) return launch_wp_shards<kStaticTerrain, 6>(P, sm, s);
+  if (fixed && frw == 128) return launch_wp_shards<kStaticTerrain, 4>(P, sm, s);
   if (mode == kStaticTables) {
     if (whole_width && wpr == 4) return launch_wp_shards<kStaticTables, 4>(P, sm, s);
     if (whole_width && wpr == 2) return launch_wp_shards<kStaticTables, 2>(P, sm, s);
@@ -926,9 +929,11 @@ cudaError_t launch_step_warp(const StepArgs& a, int mode, const BlockGeom& g, cu
   // C1: the whole-env launch of ebl_step_batch leaves its step loop once the fire is out (EXIT)
   if (whole && a.h == 128 && a.w == 128)
     return a.early_exit ? launch_wp<kStaticTerrain, 4, 128, true>(a, g, sm, s) : launch_wp<kStaticTerrain, 4, 128>(a, g, sm, s);
-  // fixed 320-column regions (64 x 256 tiles with their halo): compile-time words per row and the
-  // branch-free decide pass for every halo tile
+  // fixed 128 / 192 / 320-column regions (64 / 128 / 256-column tiles with their halo): compile-time
+  // words per row and the branch-free decide pass for every halo tile
   if (g.fixed_region && rw == 320) return launch_wp<kStaticTerrain, 10>(a, g, sm, s);
+  if (g.fixed_region && rw == 192) return launch_wp<kStaticTerrain, 6>(a, g, sm, s);
+  if (g.fixed_region && rw == 128) return launch_wp<kStaticTerrain, 4>(a, g, sm, s);
   if (whole && a.h == 64 && a.w == 64)
     return a.early_exit ? launch_wp<kStaticTerrain, 2, 64, true>(a, g, sm, s) : launch_wp<kStaticTerrain, 2, 64>(a, g, sm, s);
   if (whole_width && wpr == 4) return launch_wp<kStaticTerrain, 4>(a, g, sm, s);

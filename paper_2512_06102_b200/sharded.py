@@ -88,7 +88,7 @@ class ShardedLandscape:
             b.set_config(cfg)
             check(lib().ebl_batch_set_row_offset(b.handle, g0))
             if g1 - g0 < self.height:  # halo tiles: never more steps per launch than halo rows
-                b.set_tiling(min(64, g1 - g0), min(256, -(-self.width // 32) * 32), halo)
+                b.set_tiling(min(32, g1 - g0), min(128, -(-self.width // 32) * 32), halo)
             check(lib().ebl_batch_set_band(b.handle, sh.band[0] - g0, sh.band[1] - g0))
             self.batches.append(b)
         self._handles = (C.c_void_p * len(self.batches))(*[b.handle.value for b in self.batches])
