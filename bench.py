@@ -12,7 +12,7 @@ one pass of the hot path over one batch of synthetic inputs:
   C2  16384 envs of 64x64 air-tanker RL (device random (x,y) policy, 3x3 drop, auto-reset):
       256 RL steps of every env (4.19e6 env-steps)
   C3  one 16384x16384 landscape, wind 6 from the west, 64 ignitions: a 500-step run
-      (1.34e11 cell-updates); N>1: row bands per rank, 8-row halos exchanged every 8 steps
+      (1.34e11 cell-updates); N>1: row bands per rank, 16-row halos exchanged every 16 steps
   C4  256 envs of 128x128, 100 deterministic fp64 steps + MSE loss + reverse-mode gradient of
       the 6 SimConfig parameters (4.19e8 cell-steps, forward + backward)
 
@@ -648,7 +648,7 @@ def bench_c3(cx: Ctx, clk):
     from paper_2512_06102_b200 import sharded as SH
     torch = cx.torch
     a, s = cx.args, SPEC["C3"]
-    H, W, steps, K = s["h"], s["w"], s["steps"], 8
+    H, W, steps, K = s["h"], s["w"], s["steps"], 16  # the tiles' light-cone halo (kBlockHalo)
     shards = SH.plan_shards(H, cx.world, K)
     me = shards[cx.rank]
     g0, g1 = me.rows

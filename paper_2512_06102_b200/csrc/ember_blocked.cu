@@ -564,7 +564,11 @@ BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_o
       const char* e = std::getenv("EBL_TILE_W");
       return e ? std::max(32, std::atoi(e) / 32 * 32) : kBlockTileW;
     }();
-    g.halo_rows = kBlockHalo;
+    static const int halo_env = [] {  // EBL_TILE_HALO: rows of light-cone halo = steps per launch
+      const char* e = std::getenv("EBL_TILE_HALO");
+      return e ? std::max(1, std::min(32, std::atoi(e))) : kBlockHalo;
+    }();
+    g.halo_rows = halo_env;
     g.tile_w = w <= tile_w_env + 64 ? ((w + 31) / 32) * 32 : tile_w_env;
     g.halo_cols = g.tile_w >= w ? 0 : 32;
     g.tile_h = tile_h_env;
@@ -573,7 +577,8 @@ BlockGeom plan_blocks(int buf_h, int w, int n_steps, bool force_tiles, int row_o
       g.halo_rows = 0;
     }
     const bool fuzzy = g.halo_rows > 0 || g.halo_cols > 0;
-    g.n_steps = !fuzzy ? n_steps : (n_steps < kBlockHalo ? n_steps : kBlockHalo);
+    const int lim = g.halo_rows > 0 ? g.halo_rows : kBlockHalo;  // steps per launch <= the light-cone halo
+    g.n_steps = !fuzzy ? n_steps : (n_steps < lim ? n_steps : lim);
   }
   const int rh = g.tile_h + 2 * g.halo_rows, rw = g.tile_w + 2 * g.halo_cols;
   g.list_cap = g.envs_per_cta * list_cap_for((rh < buf_h ? rh : buf_h) * (rw < w ? rw : w));

@@ -406,7 +406,7 @@ void apply_fixed_regions(const ebl_batch* b, ebl::BlockGeom& g) {
   }();
   if (!on || !use_warp(b) || b->mode != ebl::kStaticTerrain) return;
   const int rw = g.tile_w + 2 * g.halo_cols;  // the compile-time region widths (ember_warp.cu)
-  if (g.halo_rows != 8 || g.halo_cols != 32 || !(rw == 128 || rw == 192 || rw == 320)) return;
+  if (g.halo_rows < 1 || g.halo_rows > 32 || g.halo_cols != 32 || !(rw == 128 || rw == 192 || rw == 320)) return;
   if (b->h < g.tile_h + 2 * g.halo_rows || b->w < g.tile_w + 2 * g.halo_cols || (b->w % 32) != 0) return;
   g.fixed_region = 1;
 }
@@ -1043,8 +1043,9 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
       {  // quiet-tile skipping (warp-local kernel, halo inside the 8 neighbour tiles, no recording)
         const int tx = (b->w + g.tile_w - 1) / g.tile_w, ty = (b->h + g.tile_h - 1) / g.tile_h;
         const bool exposed = a.keep_lo > 0 || a.keep_hi < b->h;  // halo rows of a row shard
+        // (exposed halo tiles need tile_h >= 3 halo for the distance argument; marked ones do not)
         const bool tiled = tx * ty > 1 && g.halo_rows <= g.tile_h && g.halo_cols <= g.tile_w && !a.traj &&
-                           use_warp(b) && (!exposed || g.tile_h >= 3 * g.halo_rows);
+                           use_warp(b) && (!exposed || halo_marks_on() || g.tile_h >= 3 * g.halo_rows);
         // work-list run: the whole call on one unsharded batch with no records carried in; after the
         // first (grid) launch only the tiles the skip rule would not skip are launched, on persistent
         // CTAs (EBL_WORK_LIST=0 keeps grid launches with per-CTA skipping)
@@ -1416,8 +1417,10 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
       {
         const int tx = (b->w + g.tile_w - 1) / g.tile_w, ty = (b->h + g.tile_h - 1) / g.tile_h;
         const bool exposed = a.keep_lo > 0 || a.keep_hi < b->h;
+        // (exposed halo tiles need tile_h >= 3 halo; on work lists the neighbours mark them instead)
         const bool tiled = tx * ty > 1 && g.halo_rows <= g.tile_h && g.halo_cols <= g.tile_w && use_warp(b) &&
-                           k <= std::max(1, g.halo_rows) && (!exposed || g.tile_h >= 3 * g.halo_rows);
+                           k <= std::max(1, g.halo_rows) &&
+                           (!exposed || (work_list && halo_marks) || g.tile_h >= 3 * g.halo_rows);
         if (tiled && work_list && (list_launch[s] >= 0 || n_steps > k)) {
           // work list (halo tiles: marked by the neighbours, or exposed -- ember_warp.cu)
           const size_t nt = static_cast<size_t>(tx) * ty * b->n_envs;

@@ -13,9 +13,9 @@ constexpr int kRlThreads = 256;   // RL kernels: one CTA per env
 constexpr int kRlMaxCells = 16384;  // env layer(s) resident in shared memory
 constexpr int kResThreads = 128;    // blocked kernel: one CTA per tile (whole env if it fits)
 constexpr size_t kResMaxSmem = 200 * 1024;
-constexpr int kBlockTileH = 32;     // tiled runs (large grids): 32 x 128 tiles (C3 sweep,
-constexpr int kBlockTileW = 128;    // scripts/c3_tiles.sh), 8-row / 32-column light-cone halo, 8 steps per launch
-constexpr int kBlockHalo = 8;
+constexpr int kBlockTileH = 32;     // tiled runs (large grids): 32 x 128 tiles with a 16-row / 32-column
+constexpr int kBlockTileW = 128;    // light-cone halo, 16 steps per launch (C3 sweeps: scripts/c3_tiles.sh,
+constexpr int kBlockHalo = 16;      // scripts/c3_halo_sweep.sh)
 
 bool phase_prof_built();
 // Host-side launch helpers with per-(kernel, device) caches: the dynamic shared-memory opt-in is

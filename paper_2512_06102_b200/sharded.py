@@ -69,7 +69,7 @@ def halo_copies(shards: list[Shard]) -> list[tuple]:
 class ShardedLandscape:
     """C3 driver: G shards on `devices` (default: all on device 0) of one terrain."""
 
-    def __init__(self, terrain: Terrain, n_shards: int, devices=None, halo: int = 8, cfg=None,
+    def __init__(self, terrain: Terrain, n_shards: int, devices=None, halo: int = 16, cfg=None,
                  fused: bool = True):
         assert terrain.fuel_class.shape[0] == 1, "one landscape"
         _, self.height, self.width = terrain.fuel_class.shape
