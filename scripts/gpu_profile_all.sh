@@ -23,6 +23,6 @@ $C4 > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control non
 $C4 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_det_back_stream -s 450 -c 1 -o gpurun_out/prof_${TAG}_c4back $C4 > gpurun_out/ncu_c4back.log 2>&1
 $C4 > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_det_forward -s 450 -c 1 -o gpurun_out/prof_${TAG}_c4fwd $C4 > gpurun_out/ncu_c4fwd.log 2>&1
 C3="python bench.py --config C3 --steps 1 --warmup 3 --no-cpu-baseline"
-$C3 > /dev/null 2>&1 && ncu --metrics smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:k_step_warp -c 63 --csv --log-file gpurun_out/c3_metrics_${TAG}.csv $C3 > gpurun_out/ncu_c3.log 2>&1
+$C3 > /dev/null 2>&1 && ncu --metrics smsp__inst_executed.sum,dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:k_step_warp -c 40 --csv --log-file gpurun_out/c3_metrics_${TAG}.csv $C3 > gpurun_out/ncu_c3.log 2>&1
 python scripts/c3_shards.py > gpurun_out/c3_shards_${TAG}.log 2>&1
 echo done
