@@ -1067,6 +1067,20 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
           list_launch += 1;
           list_tiles = nt;
           if (list_launch == 0) EBL_CUDA(cudaMemsetAsync(b->tcount.p, 0, 6 * sizeof(int32_t), b->stream));
+          // the run's first launch over every tile is replaced by k_tile_init (copy + records + the
+          // first list): the first step launch already runs a work list (EBL_TILE_INIT=0: grid launch)
+          static const bool tile_init = [] {
+            const char* e = std::getenv("EBL_TILE_INIT");
+            return !e || std::atoi(e) != 0;
+          }();
+          if (list_launch == 0 && tile_init) {
+            const int32_t stamp0 = ++b->list_stamp;
+            EBL_CUDA(ebl::launch_tile_init(b->state[b->cur].p, b->state[b->cur ^ 1].p, b->h, b->w, b->n_envs, g.tile_h,
+                                           g.tile_w, b->trec.p, b->tqueued.p, stamp0, b->tlist[1].p, b->tcount.p + 1,
+                                           b->stream));
+            b->launches += 1;
+            list_launch = 1;
+          }
           const int cur_l = list_launch & 1, nxt = cur_l ^ 1, c3 = list_launch % 3;
           a.list_mode = list_launch == 0 ? 1 : 2;
           a.trec = b->trec.p;

@@ -789,6 +789,87 @@ __global__ void k_tile_counts(const int4* __restrict__ trec, int tiles_per_env, 
   if (threadIdx.x < 3) atomicAdd(counts + blockIdx.y * 4 + threadIdx.x, s[threadIdx.x]);
 }
 
+// First step of a work-list run without a grid launch: one CTA per tile copies the tile's bytes into
+// the other layer buffer, counts U/B/X, and writes its record {burning, quiet streak, U, B, X} --
+// streak 2 when every byte is a FireState (both buffers then hold the tile's canonical bytes),
+// else 0 (the tile must run once: its store maps the other bytes to Unburned) -- and enqueues the
+// first launch's tiles: a burning tile's 3x3 neighbourhood, a non-canonical tile itself.  A tile
+// no launch lists keeps these bytes, which is what stepping a region without fire produces.
+__global__ void k_tile_init(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int h, int w, size_t ncell,
+                            int tile_h, int tile_w, int ntx, int nty, int4* trec, int32_t* queued, int32_t stamp,
+                            int32_t* next_list, int32_t* next_count) {
+  __shared__ int s_c[4];  // U, B, X, non-canonical
+  const int tx = blockIdx.x, ty = blockIdx.y, env = blockIdx.z;
+  const int r0 = ty * tile_h, c0 = tx * tile_w;
+  const int rows = min(tile_h, h - r0), cols = min(tile_w, w - c0);
+  if (threadIdx.x < 4) s_c[threadIdx.x] = 0;
+  __syncthreads();
+  int u = 0, bb = 0, x = 0, nc = 0;
+  const uint8_t* src = in + env * ncell;
+  uint8_t* dst = out + env * ncell;
+  const bool vec = (w % 16) == 0 && (cols % 16) == 0;
+  const int per_row = vec ? cols / 16 : cols;
+  for (int i = threadIdx.x; i < rows * per_row; i += blockDim.x) {
+    const int r = r0 + i / per_row, k = i % per_row;
+    if (vec) {
+      const size_t o = static_cast<size_t>(r) * w + c0 + 16 * k;
+      const uint4 q = *reinterpret_cast<const uint4*>(src + o);
+      *reinterpret_cast<uint4*>(dst + o) = q;
+      const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t v = wd[j];
+        const uint32_t z = v & 0xFCFCFCFCu;
+        const uint32_t small = ~((((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) >> 7) & 0x01010101u;
+        const uint32_t b0 = v & 0x01010101u, b1 = (v >> 1) & 0x01010101u;
+        const int n1 = __popc(b0 & ~b1 & small), n2 = __popc(b1 & ~b0 & small);
+        bb += n1;
+        x += n2;
+        u += 4 - n1 - n2;  // (non-FireState bytes count as Unburned, as a step maps them)
+        nc |= static_cast<int>((~small & 0x01010101u) | (b0 & b1));
+      }
+    } else {
+      const size_t o = static_cast<size_t>(r) * w + c0 + k;
+      const uint8_t v = src[o];
+      dst[o] = v;
+      bb += v == 1;
+      x += v == 2;
+      u += v != 1 && v != 2;
+      nc |= v > 2;
+    }
+  }
+  atomicAdd(&s_c[0], u);
+  atomicAdd(&s_c[1], bb);
+  atomicAdd(&s_c[2], x);
+  if (nc) atomicOr(&s_c[3], 1);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const bool burning = s_c[1] > 0, canon = s_c[3] == 0;
+  const size_t id = (static_cast<size_t>(env) * nty + ty) * ntx + tx;
+  trec[id] = make_int4((burning ? 1 : 0) | ((canon ? 2 : 0) << 1), s_c[0], s_c[1], s_c[2]);
+  auto enqueue = [&](int qx, int qy) {
+    const size_t q = (static_cast<size_t>(env) * nty + qy) * ntx + qx;
+    if (atomicExch(queued + q, stamp) != stamp) next_list[atomicAdd(next_count, 1)] = static_cast<int>(q);
+  };
+  if (burning) {
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx)
+        if (ty + dy >= 0 && ty + dy < nty && tx + dx >= 0 && tx + dx < ntx) enqueue(tx + dx, ty + dy);
+  } else if (!canon) {
+    enqueue(tx, ty);
+  }
+}
+
+cudaError_t launch_tile_init(const uint8_t* in, uint8_t* out, int h, int w, int n_envs, int tile_h, int tile_w,
+                             int32_t* trec, int32_t* queued, int32_t stamp, int32_t* next_list, int32_t* next_count,
+                             cudaStream_t s) {
+  const int ntx = (w + tile_w - 1) / tile_w, nty = (h + tile_h - 1) / tile_h;
+  k_tile_init<<<dim3(ntx, nty, n_envs), 128, 0, s>>>(in, out, h, w, static_cast<size_t>(h) * w, tile_h, tile_w, ntx,
+                                                     nty, reinterpret_cast<int4*>(trec), queued, stamp, next_list,
+                                                     next_count);
+  return cudaGetLastError();
+}
+
 // Halo rows written into a row shard's layer between calls (ebl_batch_rows_device /
 // ebl_batch_copy_rows): a burning cell sets the burning bit of its tile's carried record, so that
 // tile and its 8 neighbours -- every tile whose region reaches the cell -- run next launch.
