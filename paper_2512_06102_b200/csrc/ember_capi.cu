@@ -411,6 +411,15 @@ void apply_fixed_regions(const ebl_batch* b, ebl::BlockGeom& g) {
   g.fixed_region = 1;
 }
 
+// EBL_TILE_INIT=0: work-list runs start with a grid launch over every tile instead of k_tile_init
+bool tile_init_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("EBL_TILE_INIT");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 // EBL_HALO_MARKS=0: row shards' halo tiles are exposed (never skipped) instead of marked
 bool halo_marks_on() {
   static const bool on = [] {
@@ -1069,15 +1078,11 @@ int ebl_step_batch(ebl_batch* b, int n_steps) {
           if (list_launch == 0) EBL_CUDA(cudaMemsetAsync(b->tcount.p, 0, 6 * sizeof(int32_t), b->stream));
           // the run's first launch over every tile is replaced by k_tile_init (copy + records + the
           // first list): the first step launch already runs a work list (EBL_TILE_INIT=0: grid launch)
-          static const bool tile_init = [] {
-            const char* e = std::getenv("EBL_TILE_INIT");
-            return !e || std::atoi(e) != 0;
-          }();
-          if (list_launch == 0 && tile_init) {
+          if (list_launch == 0 && tile_init_on()) {
             const int32_t stamp0 = ++b->list_stamp;
             EBL_CUDA(ebl::launch_tile_init(b->state[b->cur].p, b->state[b->cur ^ 1].p, b->h, b->w, b->n_envs, g.tile_h,
                                            g.tile_w, b->trec.p, b->tqueued.p, stamp0, b->tlist[1].p, b->tcount.p + 1,
-                                           b->stream));
+                                           a.store_lo, a.store_hi, b->stream));
             b->launches += 1;
             list_launch = 1;
           }
@@ -1368,6 +1373,7 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
     return !e || std::atoi(e) != 0;
   }();
   const bool halo_marks = halo_marks_on();
+  const bool tile_init = tile_init_on();
   std::vector<ebl::StepArgs> args(n_shards);
   std::vector<char> listed(n_shards, 0);
   // shards sharing one device run on shard 0's stream (stream order replaces the per-chunk
@@ -1447,8 +1453,16 @@ int ebl_shards_step(ebl_batch** shards, int n_shards, int n_steps, int halo) {
           for (auto& l : b->tlist)
             if (l.n < nt) EBL_CUDA(l.alloc(nt));
           if (b->tcount.n < 6) EBL_CUDA(b->tcount.alloc(6));
-          const int L = ++list_launch[s];
+          int L = ++list_launch[s];
           if (L == 0) EBL_CUDA(cudaMemsetAsync(b->tcount.p, 0, 6 * sizeof(int32_t), strm(s)));
+          if (L == 0 && tile_init) {  // records + first list instead of a grid launch (ebl_step_batch);
+            // the shard's layer holds its halo rows' initial fire, so its own init lists those tiles
+            const int32_t stamp0 = ++b->list_stamp;
+            EBL_CUDA(ebl::launch_tile_init(b->state[b->cur].p, b->state[b->cur ^ 1].p, b->h, b->w, b->n_envs,
+                                           g.tile_h, g.tile_w, b->trec.p, b->tqueued.p, stamp0, b->tlist[1].p,
+                                           b->tcount.p + 1, a.store_lo, a.store_hi, strm(s)));
+            L = list_launch[s] = 1;
+          }
           const int c3 = L % 3;
           a.list_mode = L == 0 ? 1 : 2;
           a.trec = b->trec.p;

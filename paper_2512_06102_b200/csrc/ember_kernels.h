@@ -35,7 +35,7 @@ cudaError_t launch_step_warp(const StepArgs& a, int mode, const BlockGeom& g, cu
 cudaError_t launch_step_warp_shards(const ShardsLaunch& p, int mode, cudaStream_t s);
 cudaError_t launch_tile_init(const uint8_t* in, uint8_t* out, int h, int w, int n_envs, int tile_h, int tile_w,
                              int32_t* trec, int32_t* queued, int32_t stamp, int32_t* next_list, int32_t* next_count,
-                             cudaStream_t s);
+                             int count_lo, int count_hi, cudaStream_t s);
 cudaError_t launch_mark_halo(const uint8_t* layer, int n_envs, size_t ncell, int w, int row0, int n_rows,
                              int32_t* tflags, int tile_h, int tile_w, int ntx, int nty, cudaStream_t s);
 cudaError_t launch_tile_counts(const int32_t* trec, int n_envs, int tiles_per_env, int32_t* counts, cudaStream_t s);

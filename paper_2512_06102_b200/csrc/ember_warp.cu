@@ -797,20 +797,21 @@ __global__ void k_tile_counts(const int4* __restrict__ trec, int tiles_per_env, 
 // no launch lists keeps these bytes, which is what stepping a region without fire produces.
 __global__ void k_tile_init(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int h, int w, size_t ncell,
                             int tile_h, int tile_w, int ntx, int nty, int4* trec, int32_t* queued, int32_t stamp,
-                            int32_t* next_list, int32_t* next_count) {
+                            int32_t* next_list, int32_t* next_count, int count_lo, int count_hi) {
   __shared__ int s_c[4];  // U, B, X, non-canonical
   const int tx = blockIdx.x, ty = blockIdx.y, env = blockIdx.z;
   const int r0 = ty * tile_h, c0 = tx * tile_w;
   const int rows = min(tile_h, h - r0), cols = min(tile_w, w - c0);
   if (threadIdx.x < 4) s_c[threadIdx.x] = 0;
   __syncthreads();
-  int u = 0, bb = 0, x = 0, nc = 0;
+  int u = 0, bb = 0, x = 0, nc = 0, burn_any = 0;
   const uint8_t* src = in + env * ncell;
   uint8_t* dst = out + env * ncell;
   const bool vec = (w % 16) == 0 && (cols % 16) == 0;
   const int per_row = vec ? cols / 16 : cols;
   for (int i = threadIdx.x; i < rows * per_row; i += blockDim.x) {
     const int r = r0 + i / per_row, k = i % per_row;
+    const bool counted = r >= count_lo && r < count_hi;  // (row shards: the band rows only)
     if (vec) {
       const size_t o = static_cast<size_t>(r) * w + c0 + 16 * k;
       const uint4 q = *reinterpret_cast<const uint4*>(src + o);
@@ -823,28 +824,38 @@ __global__ void k_tile_init(const uint8_t* __restrict__ in, uint8_t* __restrict_
         const uint32_t small = ~((((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) >> 7) & 0x01010101u;
         const uint32_t b0 = v & 0x01010101u, b1 = (v >> 1) & 0x01010101u;
         const int n1 = __popc(b0 & ~b1 & small), n2 = __popc(b1 & ~b0 & small);
-        bb += n1;
-        x += n2;
-        u += 4 - n1 - n2;  // (non-FireState bytes count as Unburned, as a step maps them)
+        if (counted) {
+          bb += n1;
+          x += n2;
+          u += 4 - n1 - n2;  // (non-FireState bytes count as Unburned, as a step maps them)
+        }
+        burn_any |= n1;
         nc |= static_cast<int>((~small & 0x01010101u) | (b0 & b1));
       }
     } else {
       const size_t o = static_cast<size_t>(r) * w + c0 + k;
       const uint8_t v = src[o];
       dst[o] = v;
-      bb += v == 1;
-      x += v == 2;
-      u += v != 1 && v != 2;
+      if (counted) {
+        bb += v == 1;
+        x += v == 2;
+        u += v != 1 && v != 2;
+      }
+      burn_any |= v == 1;
       nc |= v > 2;
     }
   }
+  __shared__ int s_burn;
+  if (threadIdx.x == 0) s_burn = 0;
+  __syncthreads();
   atomicAdd(&s_c[0], u);
   atomicAdd(&s_c[1], bb);
   atomicAdd(&s_c[2], x);
   if (nc) atomicOr(&s_c[3], 1);
+  if (burn_any) atomicOr(&s_burn, 1);
   __syncthreads();
   if (threadIdx.x != 0) return;
-  const bool burning = s_c[1] > 0, canon = s_c[3] == 0;
+  const bool burning = s_burn != 0, canon = s_c[3] == 0;  // (a burning halo row counts for the lists)
   const size_t id = (static_cast<size_t>(env) * nty + ty) * ntx + tx;
   trec[id] = make_int4((burning ? 1 : 0) | ((canon ? 2 : 0) << 1), s_c[0], s_c[1], s_c[2]);
   auto enqueue = [&](int qx, int qy) {
@@ -862,11 +873,11 @@ __global__ void k_tile_init(const uint8_t* __restrict__ in, uint8_t* __restrict_
 
 cudaError_t launch_tile_init(const uint8_t* in, uint8_t* out, int h, int w, int n_envs, int tile_h, int tile_w,
                              int32_t* trec, int32_t* queued, int32_t stamp, int32_t* next_list, int32_t* next_count,
-                             cudaStream_t s) {
+                             int count_lo, int count_hi, cudaStream_t s) {
   const int ntx = (w + tile_w - 1) / tile_w, nty = (h + tile_h - 1) / tile_h;
   k_tile_init<<<dim3(ntx, nty, n_envs), 128, 0, s>>>(in, out, h, w, static_cast<size_t>(h) * w, tile_h, tile_w, ntx,
                                                      nty, reinterpret_cast<int4*>(trec), queued, stamp, next_list,
-                                                     next_count);
+                                                     next_count, count_lo, count_hi);
   return cudaGetLastError();
 }
 
