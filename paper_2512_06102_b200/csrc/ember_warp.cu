@@ -858,6 +858,7 @@ __global__ void k_tile_init(const uint8_t* __restrict__ in, uint8_t* __restrict_
   const bool burning = s_burn != 0, canon = s_c[3] == 0;  // (a burning halo row counts for the lists)
   const size_t id = (static_cast<size_t>(env) * nty + ty) * ntx + tx;
   trec[id] = make_int4((burning ? 1 : 0) | ((canon ? 2 : 0) << 1), s_c[0], s_c[1], s_c[2]);
+  if (!next_list) return;  // grid-form records (carried across calls): no work list
   auto enqueue = [&](int qx, int qy) {
     const size_t q = (static_cast<size_t>(env) * nty + qy) * ntx + qx;
     if (atomicExch(queued + q, stamp) != stamp) next_list[atomicAdd(next_count, 1)] = static_cast<int>(q);

@@ -420,6 +420,41 @@ def test_quiet_tiles_skipped_landscape_vs_oracle(port):
     assert np.array_equal(outs[0][0], O.run(port, "port", g, O.DEFAULT_CFG, 12, 0, 0, steps, init[0]))
 
 
+def test_quiet_tiles_records_carried_across_calls_vs_oracle(port):
+    """The same mostly quiet landscape stepped as 15 calls of 16 steps (one halo-tiled grid launch
+    per call, tile records carried from call to call; the first call's records written by
+    k_tile_init from the layer instead of a launch stepping every tile), then as uneven calls:
+    final layers and counts == the one-call run == oracle, and the first launch no longer steps
+    every tile."""
+    h, w, steps = 512, 2048, 240
+    t = eb.synth_terrain(12, 1, h, w)
+    t.wind_speed[:] = 8.0
+    t.wind_direction[:] = 0.0
+    init = np.zeros((1, h, w), np.uint8)
+    for r, c in ((40, 100), (300, 1000), (480, 1900)):
+        init[0, r, c] = 1
+    init[0, 200, 1500] = 7
+    init[0, 10, 10:20] = 2
+    g = O.grid_terrain(port, "port", t.veg()[0], t.den()[0], t.elevation[0], 30.0, 8.0, 0.0)
+    want = O.run(port, "port", g, O.DEFAULT_CFG, 12, 0, 0, steps, init[0])
+    for chunks in ([16] * 15, [5, 16, 16, 3, 100, 16, 84]):
+        assert sum(chunks) == steps
+        b = _terrain_batch(t, None)
+        b.set_state(init)
+        b.set_key(12, 0)
+        b.diag(reset=True)
+        b.step(chunks[0])
+        d = b.diag()
+        assert d["tiles_processed"] < d["tiles_launched"] // 4, d  # the first launch skips quiet tiles
+        for c in chunks[1:]:
+            b.step(c)
+        got = b.get_state()[0]
+        assert np.array_equal(got, want), chunks
+        cnt = b.counts()
+        assert [int(cnt[0][k]) for k in range(3)] == [int((got == v).sum()) for v in (0, 1, 2)]
+        b.close()
+
+
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_record_trajectory_vs_oracle(port, kernel):
     """run_stochastic(record=true) (engine.cpp:108,116) on the device: every step's layers."""
