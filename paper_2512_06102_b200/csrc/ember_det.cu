@@ -188,7 +188,10 @@ __global__ void k_det_forward(DetArgs d, int t) {
 #ifndef EBL_DET_FWD2
 #define EBL_DET_FWD2 1
 #endif
-__global__ void k_det_forward2(DetArgs d, int t) {
+#ifndef EBL_DET_FWD_MINB
+#define EBL_DET_FWD_MINB 1
+#endif
+__global__ void __launch_bounds__(256, EBL_DET_FWD_MINB) k_det_forward2(DetArgs d, int t) {
   pdl_enter();
   const StepArgs& a = d.s;
   const int ncell = a.h * a.w;
@@ -577,7 +580,10 @@ __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_ba
 // pot-parameter gradients).  Same arithmetic per cell as k_det_back; the band's halo rows get
 // their a_lambda recomputed (bit-identical inputs).  Gradient partials per (env, band), reduced in
 // a fixed order by k_det_reduce.
-constexpr int kSB = 16;       // rows per band
+#ifndef EBL_DET_SB
+#define EBL_DET_SB 13  // C4: 16 rows 16.15 ms, 8: 16.08, 10: 15.93, 12: 15.83, 13: 15.79, 14: 16.08, 24: 16.84
+#endif
+constexpr int kSB = EBL_DET_SB;  // rows per band
 #ifndef EBL_DET_SD
 #define EBL_DET_SD 2  // C4 run: 2 rows 16.8 ms, 3 rows 17.6 ms, 4 rows 19.2 ms (occupancy vs rows in flight)
 #endif
