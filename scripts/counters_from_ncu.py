@@ -1,7 +1,8 @@
 """Writes profiles/ncu_counters.json (the per-launch counters bench.py's roofline reads) from ncu
 --set full captures of this build:
     python scripts/counters_from_ncu.py --c1 gpurun_out/prof_r02_c1.ncu-rep [--c2 prof_c2.ncu-rep]
-        [--c3 c3_metrics.csv]   (a --metrics launch list of k_step_warp over whole C3 runs)"""
+        [--c3 c3_metrics.csv]   (a --metrics launch list of k_step_warp over whole C3 runs)
+        [--c4 c4_metrics.csv]   (a --metrics launch list of the k_det_* kernels of C4 runs)"""
 import argparse
 import csv
 import io
@@ -31,6 +32,7 @@ def main():
     ap.add_argument("--c1")
     ap.add_argument("--c2")
     ap.add_argument("--c3")
+    ap.add_argument("--c4")
     a = ap.parse_args()
     path = os.path.join(ROOT, "profiles", "ncu_counters.json")
     out = json.load(open(path)) if os.path.exists(path) else {}
@@ -61,6 +63,32 @@ def main():
             "dram_bytes_per_run": tot("dram__bytes_read.sum") + tot("dram__bytes_write.sum"),
             "duration_us_cold_per_run": tot("gpu__time_duration.sum") / 1e3,
             "launches": len(ids), "source": os.path.basename(a.c3)}
+    if a.c4:
+        # one C4 run (256 x 128^2 x 100): the forward launches, the loss, the backward launches and
+        # the gradient reduction, up to the 100th backward launch and the reduction after it
+        launches = {}
+        for r in csv.DictReader(l for l in open(a.c4) if l.startswith('"')):
+            if "k_det_" not in r["Kernel Name"]:
+                continue
+            d = launches.setdefault(int(r["ID"]), {"name": r["Kernel Name"]})
+            d[r["Metric Name"]] = num(r["Metric Value"].replace(",", ""), r["Metric Unit"])
+        ids, n_back = [], 0
+        for i in sorted(launches):
+            nm = launches[i]["name"]
+            if n_back == 100 and "reduce" not in nm:
+                break
+            ids.append(i)
+            n_back += "k_det_back" in nm
+            if n_back == 100 and "reduce" in nm:
+                break
+        tot = lambda k, f="": sum(launches[i].get(k, 0.0) for i in ids if f in launches[i]["name"])
+        dram = lambda f="": tot("dram__bytes_read.sum", f) + tot("dram__bytes_write.sum", f)
+        out["c4:256x128x128x100"] = {
+            "dram_bytes_per_run": dram(),
+            "dram_bytes_forward_per_run": dram("k_det_forward"),
+            "dram_bytes_backward_per_run": dram("k_det_back"),
+            "duration_us_cold_per_run": tot("gpu__time_duration.sum") / 1e3,
+            "launches": len(ids), "backward_launches": n_back, "source": os.path.basename(a.c4)}
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps(out, indent=1))
