@@ -581,11 +581,11 @@ __global__ void __launch_bounds__(kBackTx * kBackTy, EBL_DET_BACK_MINB) k_det_ba
 // their a_lambda recomputed (bit-identical inputs).  Gradient partials per (env, band), reduced in
 // a fixed order by k_det_reduce.
 #ifndef EBL_DET_SB
-#define EBL_DET_SB 13  // C4: 16 rows 16.15 ms, 8: 16.08, 10: 15.93, 12: 15.83, 13: 15.79, 14: 16.08, 24: 16.84
+#define EBL_DET_SB 16  // C4 at 1 row ahead: 16 rows 15.07 ms, 10: 15.29, 13: 15.49, 21: 16.19, 26: 16.68, 32: 15.11
 #endif
 constexpr int kSB = EBL_DET_SB;  // rows per band
 #ifndef EBL_DET_SD
-#define EBL_DET_SD 2  // C4 run: 2 rows 16.8 ms, 3 rows 17.6 ms, 4 rows 19.2 ms (occupancy vs rows in flight)
+#define EBL_DET_SD 1  // C4 run: 1 row (7 CTAs/SM) 15.07 ms, 2 rows (6 CTAs/SM) 15.80-16.15, 3 rows 17.6, 4 rows 19.2
 #endif
 constexpr int kSD = EBL_DET_SD;  // rows requested ahead
 constexpr int kSlots = kSD + 3;  // + the rows back1 and back2 read, + the one refilled this iteration
@@ -619,7 +619,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
       : "memory");
 }
 
-__global__ void __launch_bounds__(kSW, EBL_DET_SD <= 2 ? 6 : 5) k_det_back_stream(DetArgs d, int t) {
+__global__ void __launch_bounds__(kSW, EBL_DET_SD <= 1 ? 7 : (EBL_DET_SD <= 2 ? 6 : 5)) k_det_back_stream(DetArgs d, int t) {
   pdl_enter();
   extern __shared__ __align__(128) uint8_t dsm[];
   StreamRow* const st = reinterpret_cast<StreamRow*>(dsm);
