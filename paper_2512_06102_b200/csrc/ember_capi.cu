@@ -2491,6 +2491,15 @@ int ebl_batch_set_det_tables(ebl_batch* b, int on_device) {
   return EBL_OK;
 }
 
+// EBL_DET_BD_DEFERRED=0: the recorded forward steps p_bd every step as the unrecorded one does
+static bool det_bd_deferred() {
+  static const bool on = [] {
+    const char* e = std::getenv("EBL_DET_BD_DEFERRED");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 int ebl_det_forward(ebl_batch* b, int n_steps, int record) {
   EBL_DEVICE_GUARD(b);
   if (int e = check_batch(b)) return e;
@@ -2504,8 +2513,14 @@ int ebl_det_forward(ebl_batch* b, int n_steps, int record) {
   if (record) EBL_CUDA(b->traj.alloc(3 * n * std::max(1, n_steps)));
   double* const tu = b->traj.p;
   double* const tbn = b->traj.p + n * std::max(1, n_steps);
+  // record mode: p_bd is left out of the steps and accumulated after them (k_det_bd_run)
+  const int cur0 = b->det_cur;
   for (int t = 0; t < n_steps; ++t) {
     ebl::DetArgs d = det_args(b);
+    if (record && det_bd_deferred()) {
+      d.bd = nullptr;
+      d.bd_o = nullptr;
+    }
     if (record) {
       // the trajectory slots are the states: step t reads slot t (step 0: the state buffers, which
       // it copies into slot 0) and writes slot t+1 (the last step: the state buffers); bd and the
@@ -2525,6 +2540,11 @@ int ebl_det_forward(ebl_batch* b, int n_steps, int record) {
     }
     EBL_CUDA(ebl::launch_det_forward(d, t, b->stream));
     b->det_cur ^= 1;
+    b->launches += 1;
+  }
+  if (record && det_bd_deferred() && n_steps > 0) {
+    EBL_CUDA(ebl::launch_det_bd_run(b->det[cur0 * 3 + 2].p, b->det[b->det_cur * 3 + 2].p, tbn, n, n_steps,
+                                    b->cfg.p_continue, b->stream));
     b->launches += 1;
   }
   b->traj_steps = record ? n_steps : -1;

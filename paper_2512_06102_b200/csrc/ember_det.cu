@@ -167,11 +167,12 @@ __global__ void k_det_forward(DetArgs d, int t) {
   const double lam = d.potT ? lambda_at_t(d.burn + base, d.potT + tb * 8, a.h, a.w, i / a.w, i % a.w)
                             : lambda_at(d.burn + base, d.pot + tb * 8, a.h, a.w, i / a.w, i % a.w);
   const double p_ig = __dsub_rn(1.0, exp_neg(__dmul_rn(gamma_at(d, tb, env, i), lam)));
-  const double un = d.un[base + i], bu = d.burn[base + i], bd = d.bd[base + i];
+  const double un = d.un[base + i], bu = d.burn[base + i];
   const double newly = __dmul_rn(un, p_ig);
   d.burn_o[base + i] = __dadd_rn(newly, __dmul_rn(bu, d.pc));
   d.un_o[base + i] = __dsub_rn(un, newly);
-  d.bd_o[base + i] = __dadd_rn(bd, __dmul_rn(bu, __dsub_rn(1.0, d.pc)));
+  if (d.bd)  // (record mode: p_bd is accumulated after the run from the recorded p_burn, k_det_bd_run)
+    d.bd_o[base + i] = __dadd_rn(d.bd[base + i], __dmul_rn(bu, __dsub_rn(1.0, d.pc)));
   // record mode: the states of steps >= 1 are written straight into their trajectory slots (the
   // host points un_o / burn_o there), so only step 0 copies its input; lambda every step
   const size_t tr = static_cast<size_t>(t) * a.n_envs * ncell + base + i;
@@ -203,25 +204,28 @@ __global__ void __launch_bounds__(256, EBL_DET_FWD_MINB) k_det_forward2(DetArgs 
   const int r = i0 / a.w, c = i0 % a.w;
   const double2 un2 = *reinterpret_cast<const double2*>(d.un + base + i0);
   const double2 bu2 = *reinterpret_cast<const double2*>(d.burn + base + i0);
-  const double2 bd2 = *reinterpret_cast<const double2*>(d.bd + base + i0);
   double lam[2], pig[2];
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     lam[k] = lambda_at_t(d.burn + base, d.potT + tb * 8, a.h, a.w, r, c + k);
     pig[k] = __dsub_rn(1.0, exp_neg(__dmul_rn(gamma_at(d, tb, env, i0 + k), lam[k])));
   }
-  const double un[2] = {un2.x, un2.y}, bu[2] = {bu2.x, bu2.y}, bd[2] = {bd2.x, bd2.y};
-  double o_b[2], o_u[2], o_d[2];
+  const double un[2] = {un2.x, un2.y}, bu[2] = {bu2.x, bu2.y};
+  double o_b[2], o_u[2];
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const double newly = __dmul_rn(un[k], pig[k]);
     o_b[k] = __dadd_rn(newly, __dmul_rn(bu[k], d.pc));
     o_u[k] = __dsub_rn(un[k], newly);
-    o_d[k] = __dadd_rn(bd[k], __dmul_rn(bu[k], __dsub_rn(1.0, d.pc)));
   }
   *reinterpret_cast<double2*>(d.burn_o + base + i0) = make_double2(o_b[0], o_b[1]);
   *reinterpret_cast<double2*>(d.un_o + base + i0) = make_double2(o_u[0], o_u[1]);
-  *reinterpret_cast<double2*>(d.bd_o + base + i0) = make_double2(o_d[0], o_d[1]);
+  if (d.bd) {  // (record mode: p_bd is accumulated after the run from the recorded p_burn, k_det_bd_run)
+    const double2 bd2 = *reinterpret_cast<const double2*>(d.bd + base + i0);
+    const double q = __dsub_rn(1.0, d.pc);
+    *reinterpret_cast<double2*>(d.bd_o + base + i0) =
+        make_double2(__dadd_rn(bd2.x, __dmul_rn(bu[0], q)), __dadd_rn(bd2.y, __dmul_rn(bu[1], q)));
+  }
   const size_t tr = static_cast<size_t>(t) * a.n_envs * ncell + base + i0;
   if (d.traj_un) {
     *reinterpret_cast<double2*>(d.traj_un + tr) = un2;
@@ -820,6 +824,28 @@ __global__ void k_det_reduce(DetArgs d, int blocks_per_env) {
   double s = 0.0;
   for (int b = 0; b < blocks_per_env; ++b) s += d.acc[(static_cast<size_t>(env) * blocks_per_env + b) * 8 + k];
   d.grad[env * 6 + k] = s;
+}
+
+// p_bd of a recorded run (record mode): p_bd never feeds back into the dynamics, so
+// the forward steps skip it (16 B per cell-step) and this pass replays the reference's per-step
+// update p_bd += p_burn(t) (1 - p_continue) (engine.hpp:164-167) over the recorded p_burn planes, in
+// step order -- the same fp64 operations in the same order, so the same bits.
+__global__ void k_det_bd_run(const double* __restrict__ bd0, double* bd_out, const double* __restrict__ traj_burn,
+                             size_t n, int n_steps, double pc) {
+  pdl_enter();
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double q = __dsub_rn(1.0, pc);
+  double bd = bd0[i];
+#pragma unroll 8
+  for (int t = 0; t < n_steps; ++t) bd = __dadd_rn(bd, __dmul_rn(__ldg(traj_burn + static_cast<size_t>(t) * n + i), q));
+  bd_out[i] = bd;
+}
+
+cudaError_t launch_det_bd_run(const double* bd0, double* bd_out, const double* traj_burn, size_t n, int n_steps,
+                              double pc, cudaStream_t s) {
+  return launch_pdl(k_det_bd_run, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, bd0, bd_out,
+                    traj_burn, n, n_steps, pc);
 }
 
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s) {

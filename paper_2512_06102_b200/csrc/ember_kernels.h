@@ -41,6 +41,8 @@ cudaError_t launch_mark_halo(const uint8_t* layer, int n_envs, size_t ncell, int
 cudaError_t launch_tile_counts(const int32_t* trec, int n_envs, int tiles_per_env, int32_t* counts, cudaStream_t s);
 
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s);
+cudaError_t launch_det_bd_run(const double* bd0, double* bd_out, const double* traj_burn, size_t n, int n_steps,
+                              double pc, cudaStream_t s);
 cudaError_t launch_pot_target(const double* pot, double* potT, int n_tables, int h, int w, cudaStream_t s);
 cudaError_t launch_det_tables_terrain(const double* S, const uint8_t* fuel, const double* pal64, const double* kw64,
                                       double alpha_s, int n_tables, size_t ncell, size_t grid_stride, int wind_stride,
