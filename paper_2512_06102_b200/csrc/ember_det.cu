@@ -190,7 +190,7 @@ __global__ void k_det_forward(DetArgs d, int t) {
 #define EBL_DET_FWD2 1
 #endif
 #ifndef EBL_DET_FWD_MINB
-#define EBL_DET_FWD_MINB 1
+#define EBL_DET_FWD_MINB 6  // 40 registers, 6 CTAs/SM: C4 14.95 -> 14.65 ms (5: 14.73, 7: 16.30, 8: 17.75)
 #endif
 __global__ void __launch_bounds__(256, EBL_DET_FWD_MINB) k_det_forward2(DetArgs d, int t) {
   pdl_enter();
