@@ -246,7 +246,10 @@ __global__ void k_det_from_fire(const uint8_t* __restrict__ st, double* un, doub
 
 // Loss (calibrate.hpp:120-146) per env and dL/dpred -> the adjoints of the final state.
 // One CTA per env.
-__global__ void k_det_loss(DetArgs d) {
+#ifndef EBL_DET_LOSS_THREADS
+#define EBL_DET_LOSS_THREADS 1024  // one CTA per env: 256 threads took 192 us of a C4 run (1.7 CTAs per SM)
+#endif
+__global__ void __launch_bounds__(EBL_DET_LOSS_THREADS) k_det_loss(DetArgs d) {
   __shared__ double red[32];
   const StepArgs& a = d.s;
   const int ncell = a.h * a.w;
@@ -864,7 +867,7 @@ cudaError_t launch_det_from_fire(const uint8_t* st, double* un, double* bu, doub
 }
 
 cudaError_t launch_det_loss(const DetArgs& d, cudaStream_t s) {
-  k_det_loss<<<d.s.n_envs, 256, 0, s>>>(d);
+  k_det_loss<<<d.s.n_envs, EBL_DET_LOSS_THREADS, 0, s>>>(d);
   return cudaGetLastError();
 }
 
