@@ -259,3 +259,24 @@ def test_device_built_tables_bit_identical_to_host(shared_grid):
     for x, y in zip(res[0], res[1]):
         for p, q in zip(x, y):
             assert np.array_equal(np.asarray(p).view(np.uint64), np.asarray(q).view(np.uint64))
+
+
+@pytest.mark.parametrize("steps", [1, 2, 37])
+def test_recorded_forward_p_bd_after_the_run_bit_identical(steps):
+    """The recorded forward leaves p_bd out of its steps and replays p_bd += p_burn(t)(1 - p_continue)
+    (engine.hpp:164-167) over the recorded p_burn planes after the run (k_det_bd_run): its final
+    state, p_bd included, is bit-identical to the unrecorded forward's (odd and even step counts:
+    the state buffers end on either side of the ping-pong)."""
+    n, h, w = 3, 64, 48
+    t = eb.synth_terrain(5, n, h, w)
+    init = eb.synth_ignitions(5, t, 4)
+    out = []
+    for record in (False, True):
+        b = _batch(t, [0.2, 0.15, 0.3, 1.2, 0.9, 0.7])
+        b.set_state(init)
+        b.det_set_state_from_fire()
+        b.det_forward(steps, record=record)
+        out.append(b.det_get_state())
+        b.close()
+    for p, q in zip(*out):
+        assert np.array_equal(np.asarray(p).view(np.uint64), np.asarray(q).view(np.uint64))
