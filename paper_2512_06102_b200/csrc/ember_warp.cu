@@ -789,7 +789,7 @@ __global__ void k_tile_counts(const int4* __restrict__ trec, int tiles_per_env, 
   if (threadIdx.x < 3) atomicAdd(counts + blockIdx.y * 4 + threadIdx.x, s[threadIdx.x]);
 }
 
-// First step of a work-list run without a grid launch: one CTA per tile copies the tile's bytes into
+// First step of a work-list run without a grid launch: one warp per tile copies the tile's bytes into
 // the other layer buffer, counts U/B/X, and writes its record {burning, quiet streak, U, B, X} --
 // streak 2 when every byte is a FireState (both buffers then hold the tile's canonical bytes),
 // else 0 (the tile must run once: its store maps the other bytes to Unburned) -- and enqueues the
@@ -798,18 +798,20 @@ __global__ void k_tile_counts(const int4* __restrict__ trec, int tiles_per_env, 
 __global__ void k_tile_init(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int h, int w, size_t ncell,
                             int tile_h, int tile_w, int ntx, int nty, int4* trec, int32_t* queued, int32_t stamp,
                             int32_t* next_list, int32_t* next_count, int count_lo, int count_hi) {
-  __shared__ int s_c[4];  // U, B, X, non-canonical
-  const int tx = blockIdx.x, ty = blockIdx.y, env = blockIdx.z;
+  // one warp per tile (kInitTiles tiles per CTA along x, no block barriers): the lanes stream the
+  // tile's rows as 16-byte words, counts and flags by warp reductions
+  const int lane = threadIdx.x & 31;
+  const int tx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), ty = blockIdx.y, env = blockIdx.z;
+  if (tx >= ntx) return;
   const int r0 = ty * tile_h, c0 = tx * tile_w;
   const int rows = min(tile_h, h - r0), cols = min(tile_w, w - c0);
-  if (threadIdx.x < 4) s_c[threadIdx.x] = 0;
-  __syncthreads();
   int u = 0, bb = 0, x = 0, nc = 0, burn_any = 0;
   const uint8_t* src = in + env * ncell;
   uint8_t* dst = out + env * ncell;
   const bool vec = (w % 16) == 0 && (cols % 16) == 0;
   const int per_row = vec ? cols / 16 : cols;
-  for (int i = threadIdx.x; i < rows * per_row; i += blockDim.x) {
+#pragma unroll 4
+  for (int i = lane; i < rows * per_row; i += 32) {
     const int r = r0 + i / per_row, k = i % per_row;
     const bool counted = r >= count_lo && r < count_hi;  // (row shards: the band rows only)
     if (vec) {
@@ -845,19 +847,17 @@ __global__ void k_tile_init(const uint8_t* __restrict__ in, uint8_t* __restrict_
       nc |= v > 2;
     }
   }
-  __shared__ int s_burn;
-  if (threadIdx.x == 0) s_burn = 0;
-  __syncthreads();
-  atomicAdd(&s_c[0], u);
-  atomicAdd(&s_c[1], bb);
-  atomicAdd(&s_c[2], x);
-  if (nc) atomicOr(&s_c[3], 1);
-  if (burn_any) atomicOr(&s_burn, 1);
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  const bool burning = s_burn != 0, canon = s_c[3] == 0;  // (a burning halo row counts for the lists)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    u += __shfl_xor_sync(0xffffffffu, u, o);
+    bb += __shfl_xor_sync(0xffffffffu, bb, o);
+    x += __shfl_xor_sync(0xffffffffu, x, o);
+  }
+  const bool burning = __any_sync(0xffffffffu, burn_any != 0);  // (a burning halo row counts for the lists)
+  const bool canon = !__any_sync(0xffffffffu, nc != 0);
+  if (lane != 0) return;
   const size_t id = (static_cast<size_t>(env) * nty + ty) * ntx + tx;
-  trec[id] = make_int4((burning ? 1 : 0) | ((canon ? 2 : 0) << 1), s_c[0], s_c[1], s_c[2]);
+  trec[id] = make_int4((burning ? 1 : 0) | ((canon ? 2 : 0) << 1), u, bb, x);
   if (!next_list) return;  // grid-form records (carried across calls): no work list
   auto enqueue = [&](int qx, int qy) {
     const size_t q = (static_cast<size_t>(env) * nty + qy) * ntx + qx;
@@ -872,13 +872,16 @@ __global__ void k_tile_init(const uint8_t* __restrict__ in, uint8_t* __restrict_
   }
 }
 
+#ifndef EBL_INIT_TILES
+#define EBL_INIT_TILES 4  // tiles (warps) per k_tile_init CTA
+#endif
 cudaError_t launch_tile_init(const uint8_t* in, uint8_t* out, int h, int w, int n_envs, int tile_h, int tile_w,
                              int32_t* trec, int32_t* queued, int32_t stamp, int32_t* next_list, int32_t* next_count,
                              int count_lo, int count_hi, cudaStream_t s) {
   const int ntx = (w + tile_w - 1) / tile_w, nty = (h + tile_h - 1) / tile_h;
-  k_tile_init<<<dim3(ntx, nty, n_envs), 128, 0, s>>>(in, out, h, w, static_cast<size_t>(h) * w, tile_h, tile_w, ntx,
-                                                     nty, reinterpret_cast<int4*>(trec), queued, stamp, next_list,
-                                                     next_count, count_lo, count_hi);
+  k_tile_init<<<dim3((ntx + EBL_INIT_TILES - 1) / EBL_INIT_TILES, nty, n_envs), 32 * EBL_INIT_TILES, 0, s>>>(
+      in, out, h, w, static_cast<size_t>(h) * w, tile_h, tile_w, ntx, nty, reinterpret_cast<int4*>(trec), queued, stamp,
+      next_list, next_count, count_lo, count_hi);
   return cudaGetLastError();
 }
 
