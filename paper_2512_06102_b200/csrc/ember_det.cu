@@ -190,9 +190,12 @@ __global__ void k_det_forward(DetArgs d, int t) {
 #define EBL_DET_FWD2 1
 #endif
 #ifndef EBL_DET_FWD_MINB
-#define EBL_DET_FWD_MINB 6  // 40 registers, 6 CTAs/SM: C4 14.95 -> 14.65 ms (5: 14.73, 7: 16.30, 8: 17.75)
+#define EBL_DET_FWD_MINB 12  // 40 registers at 128 threads (256: 6 CTAs/SM, C4 14.95 -> 14.58 ms; 5: 14.73, 7: 16.30)
 #endif
-__global__ void __launch_bounds__(256, EBL_DET_FWD_MINB) k_det_forward2(DetArgs d, int t) {
+#ifndef EBL_DET_FWD_THREADS
+#define EBL_DET_FWD_THREADS 128  // C4: 128 x 12 CTAs/SM 14.37 ms, 256 x 6 14.58, 64 x 24 14.38, 512 x 3 14.93
+#endif
+__global__ void __launch_bounds__(EBL_DET_FWD_THREADS, EBL_DET_FWD_MINB) k_det_forward2(DetArgs d, int t) {
   pdl_enter();
   const StepArgs& a = d.s;
   const int ncell = a.h * a.w;
@@ -854,7 +857,8 @@ cudaError_t launch_det_bd_run(const double* bd0, double* bd_out, const double* t
 cudaError_t launch_det_forward(const DetArgs& d, int t, cudaStream_t s) {
   const int ncell = d.s.h * d.s.w;
   if (EBL_DET_FWD2 && d.potT && (d.s.w % 2) == 0) {
-    return launch_pdl(k_det_forward2, dim3((ncell / 2 + 255) / 256, d.s.n_envs), dim3(256), 0, s, d, t);
+    return launch_pdl(k_det_forward2, dim3((ncell / 2 + EBL_DET_FWD_THREADS - 1) / EBL_DET_FWD_THREADS, d.s.n_envs),
+                      dim3(EBL_DET_FWD_THREADS), 0, s, d, t);
   }
   k_det_forward<<<dim3((ncell + 255) / 256, d.s.n_envs), 256, 0, s>>>(d, t);
   return cudaGetLastError();
